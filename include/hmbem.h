@@ -1,0 +1,119 @@
+/*
+ * hmbem.h -- flat C API of the host layer (libhmbem.so): meshes, cluster
+ * tree / block partition, the GPU-backed H-operator and the adaptive
+ * matvec.  It is the binding surface of the Python package
+ * paper_2205_04752_b200 (ctypes) and mirrors the reference's operator API:
+ *
+ *   hmb_mesh_*          SurfaceMesh / load_mesh / meshgen  (mesh.hpp:15-78,
+ *                       proj/tools/meshgen.cpp:27-83)
+ *   hmb_op_kelvin       evaluate_interior's 3x3 grid of CollocSingleOracle
+ *                       H-matrices at triangle centroids (baca.cpp:645-687)
+ *   hmb_op_newton/dense test fixtures (test_hmatrix.cpp:12-53, aca.hpp:34-44)
+ *   hmb_tree_*, hmb_partition_*   ClusterTree / BlockPartition /
+ *                       sparsity_constant / partition_to_json (cluster.hpp)
+ *   hmb_assemble        assemble()                 (hmatrix.hpp:88-90)
+ *   hmb_matvec          matvec(BlockGrid, x, Mode)  (expr.cpp:197-215)
+ *   hmb_promote/extend  HMatrix::promote / extend_lookahead
+ *   hmb_gamma/hmb_mark  gamma_contributions / mark_blocks (amvm.hpp:36-48)
+ *   hmb_amvm            amvm_multiply               (amvm.hpp:67-71)
+ *
+ * Status convention: 0 = ok, otherwise an hmbem error class
+ * (1 Error, 2 MeshError, 3 ConfigError, 4 DimensionError, 5 DeviceError);
+ * hmb_last_error() returns the message (thread-local).
+ */
+#ifndef HMBEM_H
+#define HMBEM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hmb_mesh hmb_mesh;
+typedef struct hmb_op hmb_op;
+
+enum {
+  HMB_OK = 0,
+  HMB_ERROR = 1,
+  HMB_MESH_ERROR = 2,
+  HMB_CONFIG_ERROR = 3,
+  HMB_DIMENSION_ERROR = 4,
+  HMB_DEVICE_ERROR = 5
+};
+
+const char* hmb_last_error(void);
+int hmb_device_status(void); /* last DeviceError's hmgpu status */
+
+/* ---- meshes ---- */
+int hmb_mesh_icosphere(int level, hmb_mesh** out);
+int hmb_mesh_ellipsoid(int level, double ax, double ay, double az, hmb_mesh** out);
+int hmb_mesh_voxel_cube(int n, double lo, double hi, hmb_mesh** out);
+int hmb_mesh_from_arrays(int nv, const double* verts, int nt, const int* tris,
+                         hmb_mesh** out);
+int hmb_mesh_load_off(const char* path, hmb_mesh** out);
+int hmb_mesh_save_off(const hmb_mesh* m, const char* path);
+int hmb_mesh_validate(const hmb_mesh* m);
+int hmb_mesh_label(hmb_mesh* m, const char* dirichlet_predicate);
+int hmb_mesh_sizes(const hmb_mesh* m, int* nv, int* nt);
+/* any output may be NULL; dirichlet as 0/1 per triangle (0s if unlabeled) */
+int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
+                 double* areas, double* normals, double* diam, int* dirichlet);
+void hmb_mesh_free(hmb_mesh* m);
+
+/* ---- operators (device < 0: host-only, tree and partition) ---- */
+int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
+                  int device, int shard_rank, int shard_count, hmb_op** out);
+int hmb_op_newton(int n, const double* pts, const double* boxes6, double diag,
+                  int b_min, double eta, int device, hmb_op** out);
+int hmb_op_dense(int m, int n, const double* a_colmajor, const double* row_pts,
+                 const double* col_pts, int b_min, double eta, int device,
+                 hmb_op** out);
+void hmb_op_free(hmb_op* op);
+/* rows/cols in DOFs, ncomp (6 Kelvin, 1 scalar), owned row range */
+int hmb_op_info(const hmb_op* op, long long* rows, long long* cols, int* ncomp,
+                int* row_begin, int* row_end);
+/* underlying hmgpu_ctx* (NULL for host-only operators) */
+void* hmb_op_gpu(const hmb_op* op);
+
+/* which = 0 row tree, 1 column tree */
+int hmb_tree_info(const hmb_op* op, int which, int* n_nodes, int* depth, int* size);
+/* nodes as [begin, end, child0, child1, level], boxes [lo, hi], perm */
+int hmb_tree_nodes(const hmb_op* op, int which, int* nodes5, double* boxes6, int* perm);
+int hmb_partition_info(const hmb_op* op, int* n_blocks, int* n_admissible, int* c_sp);
+int hmb_partition_blocks(const hmb_op* op, int* blocks4);
+int hmb_partition_json(const hmb_op* op, char* buf, long long* len);
+
+/* stats7: aca_entries, dense_entries, aca_steps, pivots, ms_total,
+ * ms_nearfield, relaunches (NULL allowed) */
+int hmb_assemble(hmb_op* op, double eps, double beta, int initial_rank,
+                 int lookahead, long long max_rank, double* stats7);
+int hmb_matvec(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
+               int device_ptrs);
+int hmb_ranks(const hmb_op* op, int* k_cur, int* k_look, int* consumed, int* last_stop);
+int hmb_promote(hmb_op* op, int n, const int* comp_block);
+int hmb_extend(hmb_op* op, int n, const int* comp_block, int steps);
+/* mb_current, mb_tail, mb_dense, mb_arena, matvec_bytes, matvec_flops, pivots */
+int hmb_storage(const hmb_op* op, double* out7);
+int hmb_factor(const hmb_op* op, int comp, int block, int* m, int* n, int* K,
+               int* k_cur, double* U, double* V, int* piv, double* frob_sq);
+int hmb_dense_block(const hmb_op* op, int comp, int block, double* out);
+
+/* ---- adaptive matvec ---- */
+/* computes the estimator and keeps it in the operator for hmb_gamma_* */
+int hmb_gamma(hmb_op* op, const double* x, double* gamma, double* difference,
+              int* n_terms);
+/* per term: comp, block, nnz, norm_sq */
+int hmb_gamma_terms(const hmb_op* op, int* comp, int* block, int* nnz, double* norm_sq);
+int hmb_gamma_term_data(const hmb_op* op, int t, long long* idx, double* val);
+int hmb_mark(const hmb_op* op, double theta, int c_sp, long long m_rows,
+             long long n_cols, int* marked, int* n_marked, double* gamma_pk);
+/* iterations as rows of 8 doubles [k, gamma, gamma_pk, marked,
+ * cumulative_pivots, storage_mb, e_hat, ms]; iters8 holds max_iterations+1 rows */
+int hmb_amvm(hmb_op* op, const double* x, double theta, double eps_amvm,
+             int lookahead_steps, int max_iterations, double* b, double* iters8,
+             int* n_iters, int* converged);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMBEM_H */

@@ -1,0 +1,194 @@
+/*
+ * hmgpu.h -- C ABI of the B200 hot path of the adaptive H-matrix BEM
+ * (ACA assembly of Kelvin collocation blocks, near-field fill, H-matvec,
+ * look-ahead tail terms for the adaptive matvec).
+ *
+ * This is the drop-in boundary under the reference's L4 "low-rank core"
+ * (SURVEY.md section 8b).  Each entry point replaces one reference interface:
+ *
+ *   hmgpu_set_kelvin_geometry  CollocSingleOracle / GalerkinKernels::
+ *                              colloc_single + point_order + kelvin_tensor
+ *                              (proj/include/hmbem/kernels.hpp:107-126,
+ *                               proj/src/kernels.cpp:21-28,87-93,176-187),
+ *                              fused into the kernels instead of a callback
+ *   hmgpu_set_rule             gauss_rule(order) tables (proj/src/quadrature.cpp:55-95)
+ *   hmgpu_set_points           test fixtures CentroidKernelOracle / PointKernelOracle
+ *                              (proj/tests/test_hmatrix.cpp:12-28, test_amvm.cpp:9-22)
+ *   hmgpu_set_dense_matrix     DenseOracle (proj/include/hmbem/aca.hpp:34-44)
+ *   hmgpu_set_partition        BlockPartition / ClusterTree handed to assemble()
+ *                              (proj/include/hmbem/cluster.hpp:35-89, hmatrix.hpp:88-90)
+ *   hmgpu_assemble             assemble() -> aca_run / aca_extend / dense fill
+ *                              (proj/src/hmatrix.cpp:147-186, proj/src/aca.cpp:41-143)
+ *   hmgpu_ranks                HBlock::current_rank / factor.rank() (hmatrix.hpp:31-39)
+ *   hmgpu_matvec               HMatrix::matvec (hmatrix.cpp:22-45) composed by the
+ *                              BlockGrid matvec (proj/src/expr.cpp:197-215)
+ *   hmgpu_promote              HMatrix::promote (hmatrix.cpp:95-97)
+ *   hmgpu_extend               HMatrix::extend_lookahead (hmatrix.cpp:104-111)
+ *   hmgpu_tail_terms           the apply_range(k_cur, k_look) products of
+ *                              gamma_contributions (proj/src/amvm.cpp:72-122)
+ *   hmgpu_download_factor      LowRankFactor state (aca.hpp:76-94), parity dumps
+ *   hmgpu_storage              storage_mb_current / storage_mb_tail (hmatrix.cpp:113-138)
+ *
+ * Conventions: plain pointers and sizes only; no exceptions cross the ABI.
+ * Every call returns an int status (HMGPU_OK = 0); hmgpu_last_error(ctx)
+ * returns a message for the last failure.  Reference errors map as:
+ * DimensionError -> HMGPU_ERR_DIMENSION, Error (eps/beta range, state)
+ * -> HMGPU_ERR_INVALID / HMGPU_ERR_STATE.
+ * Threading: one ctx per device, not re-entrant; all work is issued on the
+ * ctx's own CUDA stream (hmgpu_get_stream).  Host arrays are borrowed for
+ * the duration of a call.  Index spaces: "external" ids are the reference's
+ * DOF ids; "internal" positions are cluster-tree permuted positions
+ * (perm[internal] = external, cluster.hpp:51-52).
+ */
+#ifndef HMGPU_H
+#define HMGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hmgpu_ctx hmgpu_ctx;
+
+enum {
+  HMGPU_OK = 0,
+  HMGPU_ERR_INVALID = 1,   /* bad argument (reference: hmbem::Error) */
+  HMGPU_ERR_OOM = 2,       /* device allocation failed */
+  HMGPU_ERR_CUDA = 3,      /* CUDA runtime / launch error */
+  HMGPU_ERR_NODEVICE = 4,  /* no CUDA device visible */
+  HMGPU_ERR_STATE = 5,     /* call out of order (e.g. matvec before assemble) */
+  HMGPU_ERR_DIMENSION = 6  /* size mismatch (reference: DimensionError) */
+};
+
+enum {
+  HMGPU_KERNEL_KELVIN = 0, /* 6-component Kelvin collocation (3x3 grid) */
+  HMGPU_KERNEL_NEWTON = 1, /* scalar 1/|x-y| over points, bounded diagonal */
+  HMGPU_KERNEL_DENSE = 2   /* scalar entries of an explicit matrix */
+};
+
+enum { HMGPU_MODE_CURRENT = 0, HMGPU_MODE_LOOKAHEAD = 1 };
+enum { HMGPU_PTR_HOST = 0, HMGPU_PTR_DEVICE = 1 };
+
+/* ACA stop reasons, as AcaStop (proj/include/hmbem/aca.hpp:66-72) */
+enum {
+  HMGPU_STOP_NONE = 0,
+  HMGPU_STOP_INEQUALITY = 1,
+  HMGPU_STOP_EXHAUSTED = 2,
+  HMGPU_STOP_RANKCAP = 3,
+  HMGPU_STOP_STEPSDONE = 4
+};
+
+typedef struct hmgpu_assembly_stats {
+  long long aca_entries;      /* kernel entries evaluated by ACA (rows+cols) */
+  long long dense_entries;    /* near-field component entries */
+  long long aca_steps;        /* accepted + rejected cross attempts */
+  long long pivots;           /* sum of look-ahead ranks */
+  double ms_total;            /* device time of the whole assembly */
+  double ms_nearfield;        /* device time of the near-field fill */
+  double ms_aca;              /* device time of the ACA launches */
+  int aca_relaunches;         /* capacity regrow passes */
+} hmgpu_assembly_stats;
+
+typedef struct hmgpu_storage_info {
+  double mb_current;          /* U,V of the current factors + dense (MB, 2^20) */
+  double mb_tail;             /* look-ahead tails */
+  double mb_dense;            /* dense near-field part */
+  double mb_arena_allocated;  /* device bytes reserved for U,V */
+  long long matvec_bytes;     /* algorithmic bytes of one MODE_CURRENT matvec, nrhs=1 */
+  long long matvec_flops;     /* flops of one MODE_CURRENT matvec, nrhs=1 */
+} hmgpu_storage_info;
+
+int hmgpu_device_count(int* n);
+int hmgpu_create(int device, hmgpu_ctx** out);
+int hmgpu_destroy(hmgpu_ctx* ctx);
+const char* hmgpu_last_error(const hmgpu_ctx* ctx);
+int hmgpu_get_stream(hmgpu_ctx* ctx, void** cuda_stream);
+
+/* quadrature tier t (0: far, order-2 rule; 1: mid, order-4; 2: near, order-5)
+ * with reference coordinates (a,b) and weights summing to 1/2.  far_ratio /
+ * mid_ratio are QuadratureConfig::far_ratio / mid_ratio (kernels.hpp:44-52). */
+int hmgpu_set_rule(hmgpu_ctx* ctx, int tier, int npts, const double* a,
+                   const double* b, const double* w);
+int hmgpu_set_tier_ratios(hmgpu_ctx* ctx, double far_ratio, double mid_ratio);
+
+/* Kelvin collocation at triangle centroids, external triangle order.
+ * verts: n_vert x 3, tris: n_tri x 3, centroid/area/diam as load_mesh
+ * computes them (mesh.cpp:235-244, 105-109); material E, nu. */
+int hmgpu_set_kelvin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
+                              int n_tri, const int* tris,
+                              const double* centroid, const double* area,
+                              const double* diam, double E, double nu);
+/* scalar Newton kernel 1/|x_i - x_j| with entry `diag` where x_i == x_j */
+int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag);
+/* scalar explicit matrix, column-major m x n, external ids */
+int hmgpu_set_dense_matrix(hmgpu_ctx* ctx, int m, int n, const double* a);
+
+/* Cluster trees (nodes as rows [begin, end, child0, child1]) with their
+ * permutations, and the block partition (rows [row_node, col_node,
+ * admissible, level]).  The ctx owns the blocks whose row node lies inside
+ * the internal row range [row_begin, row_end) -- the block-row shard of
+ * this device (pass 0, n_rows for a single device). */
+int hmgpu_set_partition(hmgpu_ctx* ctx, int n_rows, const int* row_perm,
+                        int n_row_nodes, const int* row_nodes4, int n_cols,
+                        const int* col_perm, int n_col_nodes,
+                        const int* col_nodes4, int n_blocks,
+                        const int* blocks4, int row_begin, int row_end);
+
+/* assemble(): full mode (initial_rank < 0: ACA to the stopping rule at eps
+ * with beta_stop) or coarse mode (initial_rank pivots), then `lookahead`
+ * further pivots; dense fill of non-admissible blocks.  stats may be NULL. */
+int hmgpu_assemble(hmgpu_ctx* ctx, double eps, double beta_stop,
+                   int initial_rank, int lookahead, long long max_rank,
+                   hmgpu_assembly_stats* stats);
+
+/* per (component, block): current and look-ahead rank (-1 = dense or not
+ * owned), consumed rows, last stop rule; arrays of ncomp * n_blocks,
+ * component-major.  Any pointer may be NULL. */
+int hmgpu_ranks(hmgpu_ctx* ctx, int* k_cur, int* k_look, int* consumed,
+                int* last_stop);
+
+/* y = A x over the owned block rows (other rows of y are written 0).
+ * x, y: dofs x nrhs column-major in external component-major order
+ * (dofs = 3 * n for Kelvin, n otherwise).  ptr_kind: host or device
+ * pointers; host calls stage through pinned buffers. */
+int hmgpu_matvec(hmgpu_ctx* ctx, const double* x, double* y, int nrhs,
+                 int mode, int ptr_kind);
+
+/* promote / extend work items given as (component, block) pairs */
+int hmgpu_promote(hmgpu_ctx* ctx, int n, const int* comp_block);
+int hmgpu_extend(hmgpu_ctx* ctx, int n, const int* comp_block, int steps);
+
+/* Look-ahead tail products for every owned (component, block) with
+ * k_look > k_cur: for occurrence o of the block in the operator (1 for
+ * scalar kernels and diagonal Kelvin components, 2 for off-diagonal ones:
+ * o = 0 is cell (r,c) applied to x_c, o = 1 is cell (c,r) applied to x_r),
+ * vals[off + o*m + i] = (U[:,kc:kl] V[:,kc:kl]^T x_seg)[i], i over the block
+ * rows in internal order.  Two-call protocol: with meta == NULL returns the
+ * number of terms and total values; then fills meta rows
+ * [comp, block, n_occ, off] and vals.  x is a host pointer. */
+int hmgpu_tail_terms(hmgpu_ctx* ctx, const double* x, int* n_terms,
+                     long long* n_vals, long long* meta4, double* vals);
+
+/* factor of (comp, block): U (m x K) and V (n x K) column-major, pivots
+ * (K x 2, local), frob_sq; with U == NULL only the sizes are returned */
+int hmgpu_download_factor(hmgpu_ctx* ctx, int comp, int block, int* m, int* n,
+                          int* K, int* k_cur, double* U, double* V, int* piv,
+                          double* frob_sq);
+/* dense payload of a non-admissible block for one component, m x n
+ * column-major (rows/cols in internal order) */
+int hmgpu_download_dense(hmgpu_ctx* ctx, int comp, int block, double* out);
+
+int hmgpu_storage(hmgpu_ctx* ctx, hmgpu_storage_info* info);
+
+/* CUDA-event timing of every kernel launch (off by default).  names are
+ * "gather", "nearfield", "aca", "hmv_blocks", "hmv_reduce", "tail", ...
+ * hmgpu_kernel_times returns accumulated milliseconds and launch counts for
+ * the kernel name and resets them when reset != 0. */
+int hmgpu_set_profiling(hmgpu_ctx* ctx, int on);
+int hmgpu_kernel_times(hmgpu_ctx* ctx, const char* name, double* ms,
+                       long long* launches, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMGPU_H */

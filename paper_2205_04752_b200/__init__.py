@@ -1,0 +1,18 @@
+"""B200-native hot path of the adaptive H-matrix BEM for the Lame equations
+(Bauer & Bebendorf, arXiv 2205.04752): batched ACA of Kelvin collocation
+blocks, near-field fill and the H-matvec on sm_100a, behind the C ABI of
+include/hmgpu.h, with a host layer mirroring the reference's operator API.
+"""
+from .api import (AcaStop, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
+                  AssemblyStats, BlockTerm, ClusterTree, ConfigError, DeviceError,
+                  DimensionError, Error, GammaContributions, HMatrix, Mesh, MeshError,
+                  Mode, amvm_multiply, assemble, device_count, gamma_contributions,
+                  host_tree_and_partition)
+
+__all__ = [
+    "AcaStop", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
+    "AssemblyStats", "BlockTerm", "ClusterTree", "ConfigError", "DeviceError",
+    "DimensionError", "Error", "GammaContributions", "HMatrix", "Mesh", "MeshError",
+    "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",
+    "host_tree_and_partition",
+]

@@ -1,0 +1,95 @@
+"""ctypes binding of the native libraries (lib/libhmbem.so -> lib/libhmgpu.so).
+
+The product path is native only: if the libraries are missing the import
+fails loudly -- there is no Python or CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_PKG, "lib")
+HMBEM_PATH = os.path.join(LIB_DIR, "libhmbem.so")
+HMGPU_PATH = os.path.join(LIB_DIR, "libhmgpu.so")
+
+if not os.path.exists(HMBEM_PATH) or not os.path.exists(HMGPU_PATH):
+    raise ImportError(
+        "paper_2205_04752_b200 native libraries are not built; run "
+        "`python -m paper_2205_04752_b200.build` (or __graft_entry__.build())")
+
+gpu = C.CDLL(HMGPU_PATH, mode=C.RTLD_GLOBAL)
+host = C.CDLL(HMBEM_PATH)
+
+P = C.c_void_p
+I = C.c_int
+LL = C.c_longlong
+D = C.c_double
+IP = C.POINTER(C.c_int)
+DP = C.POINTER(C.c_double)
+LLP = C.POINTER(C.c_longlong)
+
+
+def _sig(lib, name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+# ---- hmbem.h ----
+_sig(host, "hmb_last_error", C.c_char_p)
+_sig(host, "hmb_device_status", I)
+_sig(host, "hmb_mesh_icosphere", I, I, C.POINTER(P))
+_sig(host, "hmb_mesh_ellipsoid", I, I, D, D, D, C.POINTER(P))
+_sig(host, "hmb_mesh_voxel_cube", I, I, D, D, C.POINTER(P))
+_sig(host, "hmb_mesh_from_arrays", I, I, P, I, P, C.POINTER(P))
+_sig(host, "hmb_mesh_load_off", I, C.c_char_p, C.POINTER(P))
+_sig(host, "hmb_mesh_save_off", I, P, C.c_char_p)
+_sig(host, "hmb_mesh_validate", I, P)
+_sig(host, "hmb_mesh_label", I, P, C.c_char_p)
+_sig(host, "hmb_mesh_sizes", I, P, IP, IP)
+_sig(host, "hmb_mesh_get", I, P, P, P, P, P, P, P, P)
+_sig(host, "hmb_mesh_free", None, P)
+_sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
+_sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))
+_sig(host, "hmb_op_dense", I, I, I, P, P, P, I, D, I, C.POINTER(P))
+_sig(host, "hmb_op_free", None, P)
+_sig(host, "hmb_op_info", I, P, LLP, LLP, IP, IP, IP)
+_sig(host, "hmb_op_gpu", P, P)
+_sig(host, "hmb_tree_info", I, P, I, IP, IP, IP)
+_sig(host, "hmb_tree_nodes", I, P, I, P, P, P)
+_sig(host, "hmb_partition_info", I, P, IP, IP, IP)
+_sig(host, "hmb_partition_blocks", I, P, P)
+_sig(host, "hmb_partition_json", I, P, C.c_char_p, LLP)
+_sig(host, "hmb_assemble", I, P, D, D, I, I, LL, P)
+_sig(host, "hmb_matvec", I, P, P, P, I, I, I)
+_sig(host, "hmb_ranks", I, P, P, P, P, P)
+_sig(host, "hmb_promote", I, P, I, P)
+_sig(host, "hmb_extend", I, P, I, P, I)
+_sig(host, "hmb_storage", I, P, P)
+_sig(host, "hmb_factor", I, P, I, I, IP, IP, IP, IP, P, P, P, DP)
+_sig(host, "hmb_dense_block", I, P, I, I, P)
+_sig(host, "hmb_gamma", I, P, P, DP, P, IP)
+_sig(host, "hmb_gamma_terms", I, P, P, P, P, P)
+_sig(host, "hmb_gamma_term_data", I, P, I, P, P)
+_sig(host, "hmb_mark", I, P, D, I, LL, LL, P, IP, DP)
+_sig(host, "hmb_amvm", I, P, P, D, D, I, I, P, P, IP, IP)
+
+# ---- hmgpu.h (direct device-level calls: stream, profiling) ----
+_sig(gpu, "hmgpu_device_count", I, IP)
+_sig(gpu, "hmgpu_last_error", C.c_char_p, P)
+_sig(gpu, "hmgpu_get_stream", I, P, C.POINTER(P))
+_sig(gpu, "hmgpu_set_profiling", I, P, I)
+_sig(gpu, "hmgpu_kernel_times", I, P, C.c_char_p, DP, LLP, I)
+_sig(gpu, "hmgpu_storage", I, P, P)
+
+HMGPU_SYMBOLS = [
+    "hmgpu_device_count", "hmgpu_create", "hmgpu_destroy", "hmgpu_last_error",
+    "hmgpu_get_stream", "hmgpu_set_rule", "hmgpu_set_tier_ratios",
+    "hmgpu_set_kelvin_geometry", "hmgpu_set_points", "hmgpu_set_dense_matrix",
+    "hmgpu_set_partition", "hmgpu_assemble", "hmgpu_ranks", "hmgpu_matvec",
+    "hmgpu_promote", "hmgpu_extend", "hmgpu_tail_terms", "hmgpu_download_factor",
+    "hmgpu_download_dense", "hmgpu_storage", "hmgpu_set_profiling",
+    "hmgpu_kernel_times",
+]

@@ -1,0 +1,507 @@
+"""Python mirror of the reference's operator API for the hot path.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/hmbem): ``build_cluster_tree`` /
+``build_block_partition`` / ``sparsity_constant`` / ``partition_to_json``
+(cluster.hpp), ``AssemblyConfig`` + ``assemble`` + ``HMatrix.matvec(x, Mode)``
++ ``promote`` / ``extend_lookahead`` + storage accounting (hmatrix.hpp),
+``gamma_contributions`` / ``mark_blocks`` / ``amvm_multiply`` (amvm.hpp).
+Every call goes through the native C API (include/hmbem.h) and the CUDA
+C ABI (include/hmgpu.h); there is no Python compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import host as _h
+
+
+# ---- errors: the reference's exception hierarchy (types.hpp:20-38) -------
+class Error(RuntimeError):
+    pass
+
+
+class MeshError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class DimensionError(Error):
+    pass
+
+
+class DeviceError(Error):
+    def __init__(self, msg: str, status: int = 0):
+        super().__init__(msg)
+        self.status = status
+
+
+_ERRORS = {1: Error, 2: MeshError, 3: ConfigError, 4: DimensionError}
+
+
+def _check(st: int) -> None:
+    if st == 0:
+        return
+    msg = _h.hmb_last_error().decode(errors="replace")
+    if st == 5:
+        raise DeviceError(msg, _h.hmb_device_status())
+    raise _ERRORS.get(st, Error)(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _lib.gpu.hmgpu_device_count(C.byref(n))
+    return n.value
+
+
+class Mode(enum.IntEnum):  # hmatrix.hpp:18
+    Current = 0
+    Lookahead = 1
+
+
+class AcaStop(enum.IntEnum):  # aca.hpp:66-72
+    NONE = 0
+    Inequality = 1
+    Exhausted = 2
+    RankCap = 3
+    StepsDone = 4
+
+
+# ---------------------------------------------------------------------------
+class Mesh:
+    """Closed triangulated surface (SurfaceMesh, mesh.hpp:15-40)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _h.hmb_mesh_free(self._h)
+            self._h = None
+
+    @staticmethod
+    def _make(fn, *args) -> "Mesh":
+        out = C.c_void_p()
+        _check(fn(*args, C.byref(out)))
+        return Mesh(out)
+
+    @classmethod
+    def icosphere(cls, level: int) -> "Mesh":
+        return cls._make(_h.hmb_mesh_icosphere, level)
+
+    @classmethod
+    def ellipsoid(cls, level: int, ax: float, ay: float, az: float) -> "Mesh":
+        return cls._make(_h.hmb_mesh_ellipsoid, level, ax, ay, az)
+
+    @classmethod
+    def voxel_cube(cls, n: int, lo: float = 0.0, hi: float = 1.0) -> "Mesh":
+        return cls._make(_h.hmb_mesh_voxel_cube, n, lo, hi)
+
+    @classmethod
+    def from_arrays(cls, verts, tris) -> "Mesh":
+        v = _f64(verts).reshape(-1, 3)
+        t = np.ascontiguousarray(tris, dtype=np.int32).reshape(-1, 3)
+        return cls._make(_h.hmb_mesh_from_arrays, len(v), _ptr(v), len(t), _ptr(t))
+
+    @classmethod
+    def load_off(cls, path: str) -> "Mesh":
+        return cls._make(_h.hmb_mesh_load_off, path.encode())
+
+    def save_off(self, path: str) -> None:
+        _check(_h.hmb_mesh_save_off(self._h, path.encode()))
+
+    def validate(self) -> None:
+        _check(_h.hmb_mesh_validate(self._h))
+
+    def label_dirichlet(self, predicate: str) -> None:
+        _check(_h.hmb_mesh_label(self._h, predicate.encode()))
+
+    @property
+    def sizes(self):
+        nv, nt = C.c_int(), C.c_int()
+        _check(_h.hmb_mesh_sizes(self._h, C.byref(nv), C.byref(nt)))
+        return nv.value, nt.value
+
+    def arrays(self) -> dict:
+        nv, nt = self.sizes
+        out = dict(vertices=np.zeros((nv, 3)), triangles=np.zeros((nt, 3), np.int32),
+                   centroids=np.zeros((nt, 3)), areas=np.zeros(nt),
+                   normals=np.zeros((nt, 3)), diam=np.zeros(nt),
+                   dirichlet=np.zeros(nt, np.int32))
+        _check(_h.hmb_mesh_get(self._h, *[_ptr(out[k]) for k in (
+            "vertices", "triangles", "centroids", "areas", "normals", "diam",
+            "dirichlet")]))
+        return out
+
+    @property
+    def num_triangles(self) -> int:
+        return self.sizes[1]
+
+    @property
+    def num_vertices(self) -> int:
+        return self.sizes[0]
+
+
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class AssemblyConfig:  # hmatrix.hpp:20-27
+    eps: float = 1e-6
+    beta: float = 0.8
+    initial_rank: int = -1
+    lookahead: int = 2
+    max_rank: int = 1 << 30
+
+
+@dataclasses.dataclass
+class AssemblyStats:
+    aca_entries: int
+    dense_entries: int
+    aca_steps: int
+    pivots: int
+    ms_total: float
+    ms_nearfield: float
+    relaunches: int
+
+    @property
+    def entries(self) -> int:
+        return self.aca_entries + self.dense_entries
+
+
+@dataclasses.dataclass
+class ClusterTree:  # cluster.hpp:35-61 (a host-side snapshot)
+    nodes: np.ndarray  # rows [begin, end, child0, child1, level]
+    boxes: np.ndarray  # rows [lo(3), hi(3)]
+    perm: np.ndarray
+    depth: int
+
+    @property
+    def inv_perm(self) -> np.ndarray:
+        inv = np.empty_like(self.perm)
+        inv[self.perm] = np.arange(len(self.perm), dtype=self.perm.dtype)
+        return inv
+
+    def leaves(self) -> np.ndarray:
+        return np.nonzero(self.nodes[:, 2] < 0)[0]
+
+
+@dataclasses.dataclass
+class BlockTerm:  # amvm.hpp:19-25
+    comp: int
+    block: int
+    idx: np.ndarray
+    val: np.ndarray
+    norm_sq: float
+
+
+@dataclasses.dataclass
+class GammaContributions:  # amvm.hpp:27-31
+    gamma: float
+    difference: np.ndarray
+    terms: list
+
+
+@dataclasses.dataclass
+class AmvmConfig:  # amvm.hpp:10-15
+    theta: float = 0.7
+    eps_amvm: float = 1e-6
+    lookahead_steps: int = 2
+    max_iterations: int = 100
+
+
+@dataclasses.dataclass
+class AmvmIteration:
+    k: int
+    gamma: float
+    gamma_pk: float
+    marked: int
+    cumulative_pivots: int
+    storage_mb: float
+    e_hat: float
+    ms: float
+
+
+@dataclasses.dataclass
+class AmvmReport:
+    iterations: list
+    termination: str
+    converged: bool
+    c_sp: int
+
+
+class HMatrix:
+    """GPU-resident H-matrix (scalar) or 3x3 Kelvin block grid of six
+    component H-matrices sharing one partition (baca.cpp:669-687)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        rows, cols = C.c_longlong(), C.c_longlong()
+        nc, rb, re = C.c_int(), C.c_int(), C.c_int()
+        _check(_h.hmb_op_info(handle, C.byref(rows), C.byref(cols), C.byref(nc),
+                              C.byref(rb), C.byref(re)))
+        self.rows, self.cols, self.ncomp = rows.value, cols.value, nc.value
+        self.row_range = (rb.value, re.value)
+        self.config: Optional[AssemblyConfig] = None
+        self.last_stats: Optional[AssemblyStats] = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _h.hmb_op_free(self._h)
+            self._h = None
+
+    # ---- construction ----
+    @classmethod
+    def kelvin(cls, mesh: Mesh, E: float = 1.0, nu: float = 0.3, b_min: int = 32,
+               eta: float = 1.0, device: int = 0, shard: tuple = (0, 1)) -> "HMatrix":
+        out = C.c_void_p()
+        _check(_h.hmb_op_kelvin(mesh._h, E, nu, b_min, eta, device, shard[0], shard[1],
+                                C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def newton(cls, points, boxes=None, diag: float = 2.0, b_min: int = 10,
+               eta: float = 0.8, device: int = 0) -> "HMatrix":
+        p = _f64(points).reshape(-1, 3)
+        b = None if boxes is None else _f64(boxes).reshape(-1, 6)
+        out = C.c_void_p()
+        _check(_h.hmb_op_newton(len(p), _ptr(p), _ptr(b), diag, b_min, eta, device,
+                                C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def dense(cls, a, row_points, col_points, b_min: int = 10, eta: float = 0.8,
+              device: int = 0) -> "HMatrix":
+        a = np.asfortranarray(a, dtype=np.float64)
+        m, n = a.shape
+        rp = _f64(row_points).reshape(-1, 3)
+        cp = _f64(col_points).reshape(-1, 3)
+        out = C.c_void_p()
+        _check(_h.hmb_op_dense(m, n, a.ctypes.data_as(C.c_void_p), _ptr(rp), _ptr(cp),
+                               b_min, eta, device, C.byref(out)))
+        return cls(out)
+
+    @property
+    def gpu_ctx(self):
+        return _h.hmb_op_gpu(self._h)
+
+    # ---- tree / partition ----
+    def tree(self, which: int = 0) -> ClusterTree:
+        nn, dep, sz = C.c_int(), C.c_int(), C.c_int()
+        _check(_h.hmb_tree_info(self._h, which, C.byref(nn), C.byref(dep), C.byref(sz)))
+        nodes = np.zeros((nn.value, 5), np.int32)
+        boxes = np.zeros((nn.value, 6))
+        perm = np.zeros(sz.value, np.int32)
+        _check(_h.hmb_tree_nodes(self._h, which, _ptr(nodes), _ptr(boxes), _ptr(perm)))
+        return ClusterTree(nodes, boxes, perm, dep.value)
+
+    def partition_info(self):
+        nb, na, csp = C.c_int(), C.c_int(), C.c_int()
+        _check(_h.hmb_partition_info(self._h, C.byref(nb), C.byref(na), C.byref(csp)))
+        return nb.value, na.value, csp.value
+
+    @property
+    def num_blocks(self) -> int:
+        return self.partition_info()[0]
+
+    @property
+    def sparsity_constant(self) -> int:
+        return self.partition_info()[2]
+
+    def partition_blocks(self) -> np.ndarray:
+        out = np.zeros((self.num_blocks, 4), np.int32)
+        _check(_h.hmb_partition_blocks(self._h, _ptr(out)))
+        return out
+
+    def partition_json(self) -> str:
+        n = C.c_longlong()
+        _check(_h.hmb_partition_json(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(_h.hmb_partition_json(self._h, buf, C.byref(n)))
+        return buf.value.decode()
+
+    # ---- assembly / products ----
+    def assemble(self, cfg: Optional[AssemblyConfig] = None, **kw) -> AssemblyStats:
+        cfg = cfg or AssemblyConfig(**kw)
+        st = np.zeros(7)
+        _check(_h.hmb_assemble(self._h, cfg.eps, cfg.beta, cfg.initial_rank,
+                               cfg.lookahead, cfg.max_rank, _ptr(st)))
+        self.config = cfg
+        self.last_stats = AssemblyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]),
+                                        float(st[4]), float(st[5]), int(st[6]))
+        return self.last_stats
+
+    def matvec(self, x, mode: Mode = Mode.Current) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float64)
+        vec = x.ndim == 1
+        xm = x.reshape(x.shape[0], -1)
+        if xm.shape[0] != self.cols:
+            raise DimensionError("HMatrix::matvec: size")
+        nrhs = xm.shape[1]
+        xf = np.asfortranarray(xm)
+        y = np.zeros((self.rows, nrhs), order="F")
+        _check(_h.hmb_matvec(self._h, xf.ctypes.data_as(C.c_void_p),
+                             y.ctypes.data_as(C.c_void_p), nrhs, int(mode), 0))
+        return y[:, 0].copy() if vec else y
+
+    def matvec_ptr(self, x_ptr: int, y_ptr: int, nrhs: int = 1,
+                   mode: Mode = Mode.Current, device: bool = True) -> None:
+        """y = A x on raw pointers (device pointers by default, e.g. torch
+        tensors' data_ptr(); host pointers should be pinned)."""
+        _check(_h.hmb_matvec(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), nrhs,
+                             int(mode), 1 if device else 0))
+
+    def _pairs(self, pairs) -> np.ndarray:
+        return np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+
+    def promote(self, pairs) -> None:
+        p = self._pairs(pairs)
+        _check(_h.hmb_promote(self._h, len(p), _ptr(p)))
+
+    def extend_lookahead(self, pairs, steps: int) -> None:
+        p = self._pairs(pairs)
+        _check(_h.hmb_extend(self._h, len(p), _ptr(p), steps))
+
+    def ranks(self):
+        n = self.ncomp * self.num_blocks
+        kc, kl, co, ls = (np.zeros(n, np.int32) for _ in range(4))
+        _check(_h.hmb_ranks(self._h, _ptr(kc), _ptr(kl), _ptr(co), _ptr(ls)))
+        shape = (self.ncomp, self.num_blocks)
+        return kc.reshape(shape), kl.reshape(shape), co.reshape(shape), ls.reshape(shape)
+
+    def storage(self) -> dict:
+        out = np.zeros(7)
+        _check(_h.hmb_storage(self._h, _ptr(out)))
+        return dict(mb_current=out[0], mb_tail=out[1], mb_dense=out[2],
+                    mb_arena=out[3], matvec_bytes=int(out[4]), matvec_flops=int(out[5]),
+                    total_pivots=int(out[6]))
+
+    def storage_mb_current(self) -> float:
+        return self.storage()["mb_current"]
+
+    def storage_mb_tail(self) -> float:
+        return self.storage()["mb_tail"]
+
+    def total_pivots(self) -> int:
+        return self.storage()["total_pivots"]
+
+    def factor(self, comp: int, block: int):
+        m, n, K, kc = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        fs = C.c_double()
+        _check(_h.hmb_factor(self._h, comp, block, C.byref(m), C.byref(n), C.byref(K),
+                             C.byref(kc), None, None, None, C.byref(fs)))
+        U = np.zeros((m.value, K.value), order="F")
+        V = np.zeros((n.value, K.value), order="F")
+        piv = np.zeros((K.value, 2), np.int32)
+        _check(_h.hmb_factor(self._h, comp, block, C.byref(m), C.byref(n), C.byref(K),
+                             C.byref(kc), U.ctypes.data_as(C.c_void_p),
+                             V.ctypes.data_as(C.c_void_p), _ptr(piv), C.byref(fs)))
+        return dict(U=U, V=V, pivots=piv, frob_sq=fs.value, k_cur=kc.value)
+
+    def dense_block(self, comp: int, block: int) -> np.ndarray:
+        nodes_r = self.tree(0).nodes
+        nodes_c = self.tree(1).nodes
+        b = self.partition_blocks()[block]
+        m = nodes_r[b[0], 1] - nodes_r[b[0], 0]
+        n = nodes_c[b[1], 1] - nodes_c[b[1], 0]
+        out = np.zeros((m, n), order="F")
+        _check(_h.hmb_dense_block(self._h, comp, block, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    # ---- adaptive matvec ----
+    def gamma_contributions(self, x) -> GammaContributions:
+        x = _f64(x)
+        g = C.c_double()
+        diff = np.zeros(self.rows)
+        nt = C.c_int()
+        _check(_h.hmb_gamma(self._h, _ptr(x), C.byref(g), _ptr(diff), C.byref(nt)))
+        n = nt.value
+        self._last_nterms = n
+        comp, block, nnz = (np.zeros(n, np.int32) for _ in range(3))
+        nsq = np.zeros(n)
+        _check(_h.hmb_gamma_terms(self._h, _ptr(comp), _ptr(block), _ptr(nnz), _ptr(nsq)))
+        terms = []
+        for t in range(n):
+            idx = np.zeros(nnz[t], np.int64)
+            val = np.zeros(nnz[t])
+            _check(_h.hmb_gamma_term_data(self._h, t, _ptr(idx), _ptr(val)))
+            terms.append(BlockTerm(int(comp[t]), int(block[t]), idx, val, float(nsq[t])))
+        return GammaContributions(g.value, diff, terms)
+
+    def mark_blocks(self, theta: float, c_sp: int, m_rows: int, n_cols: int):
+        """Marks on the estimator of the last gamma_contributions call."""
+        cap = max(1, getattr(self, "_last_nterms", 0))
+        marked = np.zeros(cap, np.int32)
+        nm = C.c_int()
+        gpk = C.c_double()
+        _check(_h.hmb_mark(self._h, theta, c_sp, m_rows, n_cols, _ptr(marked),
+                           C.byref(nm), C.byref(gpk)))
+        return marked[: nm.value].copy(), gpk.value
+
+    def amvm_multiply(self, x, cfg: Optional[AmvmConfig] = None, **kw):
+        cfg = cfg or AmvmConfig(**kw)
+        x = _f64(x)
+        b = np.zeros(self.rows)
+        iters = np.zeros((cfg.max_iterations + 1, 8))
+        ni, conv = C.c_int(), C.c_int()
+        _check(_h.hmb_amvm(self._h, _ptr(x), cfg.theta, cfg.eps_amvm, cfg.lookahead_steps,
+                           cfg.max_iterations, _ptr(b), _ptr(iters), C.byref(ni),
+                           C.byref(conv)))
+        its = [AmvmIteration(int(r[0]), r[1], r[2], int(r[3]), int(r[4]), r[5], r[6], r[7])
+               for r in iters[: ni.value]]
+        term = "tolerance" if conv.value else "max_iterations"
+        return b, AmvmReport(its, term, bool(conv.value), self.sparsity_constant)
+
+    # ---- device-level helpers ----
+    def stream(self) -> int:
+        s = C.c_void_p()
+        st = _lib.gpu.hmgpu_get_stream(self.gpu_ctx, C.byref(s))
+        if st:
+            raise DeviceError(_lib.gpu.hmgpu_last_error(self.gpu_ctx).decode(), st)
+        return s.value or 0
+
+    def set_profiling(self, on: bool) -> None:
+        _lib.gpu.hmgpu_set_profiling(self.gpu_ctx, 1 if on else 0)
+
+    def kernel_times(self, name: str, reset: bool = False):
+        ms = C.c_double()
+        n = C.c_longlong()
+        st = _lib.gpu.hmgpu_kernel_times(self.gpu_ctx, name.encode(), C.byref(ms),
+                                         C.byref(n), 1 if reset else 0)
+        if st:
+            raise DeviceError(_lib.gpu.hmgpu_last_error(self.gpu_ctx).decode(), st)
+        return ms.value, n.value
+
+
+# ---- reference-style free functions ----------------------------------------
+def assemble(h: HMatrix, cfg: AssemblyConfig) -> HMatrix:
+    h.assemble(cfg)
+    return h
+
+
+def gamma_contributions(h: HMatrix, x) -> GammaContributions:
+    return h.gamma_contributions(x)
+
+
+def amvm_multiply(h: HMatrix, x, cfg: AmvmConfig):
+    return h.amvm_multiply(x, cfg)
+
+
+def host_tree_and_partition(mesh: Mesh, b_min: int, eta: float):
+    """Cluster tree + partition without touching a GPU (device = -1)."""
+    return HMatrix.kelvin(mesh, b_min=b_min, eta=eta, device=-1)

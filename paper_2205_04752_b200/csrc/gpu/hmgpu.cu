@@ -1,0 +1,1197 @@
+// hmgpu.cu -- host side of the C ABI declared in include/hmgpu.h.
+//
+// One hmgpu_ctx owns every device buffer of one H-matrix problem on one
+// device: geometry in cluster-tree (internal) order, the ACA work items
+// (one per admissible block and component) with their resumable state,
+// the packed U/V arena, the near-field arena and the matvec work lists.
+// All work runs on the ctx's own stream.  No exceptions cross the ABI.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hmgpu.h"
+#include "hmgpu_device.cuh"
+
+using namespace hmgpu;
+
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                              \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) {                                               \
+      const int code_ = e_ == cudaErrorMemoryAllocation ? HMGPU_ERR_OOM    \
+                                                        : HMGPU_ERR_CUDA;  \
+      throw Fail{code_, std::string(#x) + ": " + cudaGetErrorString(e_)};  \
+    }                                                                      \
+  } while (0)
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;  // elements
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    free();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n || !p) alloc(count);
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) {
+    ensure(h.size());
+    if (!h.empty())
+      CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct KTime {
+  double ms = 0.0;
+  long long launches = 0;
+};
+
+struct PendingEv {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+long long align2(long long v) { return (v + 1) & ~1LL; }
+inline int c_comp_host_r(int q) {
+  static const int r[6] = {0, 0, 0, 1, 1, 2};
+  return r[q];
+}
+inline int c_comp_host_c(int q) {
+  static const int c[6] = {0, 1, 2, 1, 2, 2};
+  return c[q];
+}
+long long align16(long long v) { return (v + 15) & ~15LL; }
+
+}  // namespace
+
+struct hmgpu_ctx {
+  int device = -1;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // ---- problem definition (host copies) ----
+  int kind = -1;
+  int NC = 1;  // components: 6 for the Kelvin grid, 1 otherwise
+  std::vector<double> verts, centroid, area, diam, pts, amat;
+  std::vector<int> tris;
+  int n_vert = 0, n_tri = 0, n_pts = 0, am = 0, an = 0;
+  double E = 1.0, nu = 0.3, diag = 2.0;
+  RuleTable rules{};
+  bool rules_set[3] = {false, false, false};
+
+  // ---- partition ----
+  bool have_partition = false;
+  int n_rows = 0, n_cols = 0;
+  std::vector<int> rperm, cperm;
+  std::vector<int> rnodes, cnodes;  // 4 ints per node
+  std::vector<int> blocks;          // 4 ints per block
+  int n_blocks = 0;
+  int row_begin = 0, row_end = 0;
+  bool same_tree = false;
+
+  // ---- device geometry ----
+  DBuf<double4> d_rowpt, d_colpt;
+  DBuf<double> d_tri, d_A;
+  DBuf<int> d_rperm, d_cperm;
+  Geom geom{};
+
+  // ---- assembly state ----
+  bool assembled = false;
+  double eps = 0, beta = 0;
+  int initial_rank = -1, lookahead = 2;
+  long long max_rank = 1LL << 30;
+  std::vector<Item> items;        // host mirror (sizes, offsets, ranks)
+  std::vector<int> item_of_block; // first item of block b (-1: dense/not owned)
+  std::vector<int> dense_of_block;
+  std::vector<DenseBlock> dblocks;
+  DBuf<Item> d_items;
+  DBuf<double> d_arena;
+  long long arena_used = 0;
+  DBuf<int2> d_piv;
+  long long piv_used = 0;
+  DBuf<uint8_t> d_cons;
+  DBuf<double> d_dense;
+  long long dense_used = 0;
+  DBuf<DenseBlock> d_dblocks;
+  DBuf<int> d_counter, d_overflow, d_list;
+
+  // ---- matvec structures ----
+  std::vector<MvBlock> mvb;
+  DBuf<MvBlock> d_mvb;
+  DBuf<int> d_mvorder;
+  int n_mv = 0;
+  long long part_rows = 0;
+  std::vector<int> leaf_begin, leaf_end, leaf_ptr;
+  std::vector<long long> leaf_prow;
+  DBuf<int> d_leaf_begin, d_leaf_end, d_leaf_ptr;
+  DBuf<long long> d_leaf_prow;
+  int kmax = 0;
+  DBuf<double> d_x, d_y, d_xi, d_ypart;
+
+  // ---- profiling ----
+  bool prof = false;
+  std::map<std::string, KTime> times;
+  std::vector<PendingEv> pending;
+  std::vector<cudaEvent_t> ev_pool;
+
+  ~hmgpu_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& p : pending) {
+      ev_pool.push_back(p.a);
+      ev_pool.push_back(p.b);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    d_rowpt.free(); d_colpt.free(); d_tri.free(); d_A.free();
+    d_rperm.free(); d_cperm.free(); d_items.free(); d_arena.free();
+    d_piv.free(); d_cons.free(); d_dense.free(); d_dblocks.free();
+    d_counter.free(); d_overflow.free(); d_list.free(); d_mvb.free();
+    d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
+    d_leaf_ptr.free(); d_leaf_prow.free(); d_x.free(); d_y.free();
+    d_xi.free(); d_ypart.free();
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int ndof_rows() const { return n_rows * (NC == 6 ? 3 : 1); }
+  int ndof_cols() const { return n_cols * (NC == 6 ? 3 : 1); }
+
+  cudaEvent_t ev() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  // brackets a launch with events when profiling is on
+  template <class F>
+  void timed(const char* name, F&& launch) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (prof) {
+      a = ev();
+      b = ev();
+      CK(cudaEventRecord(a, stream));
+    }
+    launch();
+    CK(cudaGetLastError());
+    if (prof) {
+      CK(cudaEventRecord(b, stream));
+      pending.push_back({name, a, b});
+    }
+  }
+  void resolve_times() {
+    for (auto& p : pending) {
+      CK(cudaEventSynchronize(p.b));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, p.a, p.b));
+      KTime& t = times[p.name];
+      t.ms += ms;
+      t.launches += 1;
+      ev_pool.push_back(p.a);
+      ev_pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+};
+
+namespace {
+
+template <class F>
+int guard(hmgpu_ctx* c, F&& f) {
+  if (!c) return HMGPU_ERR_INVALID;
+  try {
+    if (c->device >= 0) CK(cudaSetDevice(c->device));
+    f();
+    return HMGPU_OK;
+  } catch (const Fail& e) {
+    c->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return HMGPU_ERR_OOM;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return HMGPU_ERR_INVALID;
+  }
+}
+
+int grid_for(hmgpu_ctx* c, long long work, int per_sm = 8) {
+  const long long g = std::min<long long>(work, (long long)c->sm_count * per_sm);
+  return (int)std::max<long long>(1, g);
+}
+
+// ---- device geometry in internal order ------------------------------------
+void build_geometry(hmgpu_ctx* c) {
+  Geom g{};
+  g.kind = c->kind;
+  g.same_tree = c->same_tree ? 1 : 0;
+  c->d_rperm.upload(c->rperm, c->stream);
+  c->d_cperm.upload(c->cperm, c->stream);
+  g.rperm = c->d_rperm.p;
+  g.cperm = c->d_cperm.p;
+  if (c->kind == KIND_KELVIN) {
+    if (c->n_tri != c->n_rows || c->n_tri != c->n_cols)
+      fail(HMGPU_ERR_DIMENSION, "kelvin geometry does not match the partition");
+    std::vector<double4> rp(c->n_rows);
+    for (int i = 0; i < c->n_rows; ++i) {
+      const int t = c->rperm[i];
+      rp[i] = make_double4(c->centroid[3 * t], c->centroid[3 * t + 1],
+                           c->centroid[3 * t + 2], 0.0);
+    }
+    std::vector<double> tr(16LL * c->n_cols, 0.0);
+    for (int j = 0; j < c->n_cols; ++j) {
+      const int t = c->cperm[j];
+      const double* v0 = &c->verts[3LL * c->tris[3 * t]];
+      const double* v1 = &c->verts[3LL * c->tris[3 * t + 1]];
+      const double* v2 = &c->verts[3LL * c->tris[3 * t + 2]];
+      double* T = &tr[16LL * j];
+      for (int d = 0; d < 3; ++d) {
+        T[d] = v0[d];
+        T[3 + d] = v1[d] - v0[d];
+        T[6 + d] = v2[d] - v0[d];
+        T[9 + d] = c->centroid[3 * t + d];
+      }
+      T[12] = c->area[t];
+      T[13] = c->diam[t];
+    }
+    c->d_rowpt.upload(rp, c->stream);
+    c->d_tri.upload(tr, c->stream);
+    g.rowpt = c->d_rowpt.p;
+    g.tri = c->d_tri.p;
+    // c = (1+nu) / (8 pi E (1-nu)) in the reference's evaluation order
+    g.cst = (1.0 + c->nu) / (8.0 * M_PI * c->E * (1.0 - c->nu));
+    g.c34 = 3.0 - 4.0 * c->nu;
+  } else if (c->kind == KIND_NEWTON) {
+    if (c->n_pts != c->n_rows || c->n_pts != c->n_cols)
+      fail(HMGPU_ERR_DIMENSION, "points do not match the partition");
+    std::vector<double4> rp(c->n_rows), cp(c->n_cols);
+    for (int i = 0; i < c->n_rows; ++i) {
+      const int t = c->rperm[i];
+      rp[i] = make_double4(c->pts[3 * t], c->pts[3 * t + 1], c->pts[3 * t + 2], 0);
+    }
+    for (int j = 0; j < c->n_cols; ++j) {
+      const int t = c->cperm[j];
+      cp[j] = make_double4(c->pts[3 * t], c->pts[3 * t + 1], c->pts[3 * t + 2], 0);
+    }
+    c->d_rowpt.upload(rp, c->stream);
+    c->d_colpt.upload(cp, c->stream);
+    g.rowpt = c->d_rowpt.p;
+    g.colpt = c->d_colpt.p;
+    g.diag = c->diag;
+  } else if (c->kind == KIND_DENSE) {
+    if (c->am != c->n_rows || c->an != c->n_cols)
+      fail(HMGPU_ERR_DIMENSION, "matrix does not match the partition");
+    c->d_A.upload(c->amat, c->stream);
+    g.A = c->d_A.p;
+    g.lda = c->am;
+  } else {
+    fail(HMGPU_ERR_STATE, "no entry provider set");
+  }
+  c->geom = g;
+}
+
+void upload_rules(hmgpu_ctx* c) {
+  for (int t = 0; t < 3; ++t)
+    if (!c->rules_set[t]) fail(HMGPU_ERR_STATE, "quadrature rule tier missing");
+  CK(cudaMemcpyToSymbolAsync(c_rules, &c->rules, sizeof(RuleTable), 0,
+                             cudaMemcpyHostToDevice, c->stream));
+}
+
+// ---- ACA launch with capacity regrow ---------------------------------------
+// Grows the U/V arena so that `extra` more doubles fit at its end.
+void arena_reserve(hmgpu_ctx* c, long long extra_doubles, long long extra_piv) {
+  const long long need = c->arena_used + extra_doubles;
+  if (need > (long long)c->d_arena.n) {
+    DBuf<double> nb;
+    nb.alloc((size_t)std::max<long long>(need, (long long)(c->d_arena.n * 3 / 2)));
+    if (c->arena_used)
+      CK(cudaMemcpyAsync(nb.p, c->d_arena.p, c->arena_used * sizeof(double),
+                         cudaMemcpyDeviceToDevice, c->stream));
+    c->sync();
+    c->d_arena.free();
+    c->d_arena = nb;
+  }
+  const long long needp = c->piv_used + extra_piv;
+  if (needp > (long long)c->d_piv.n) {
+    DBuf<int2> nb;
+    nb.alloc((size_t)std::max<long long>(needp, (long long)(c->d_piv.n * 3 / 2)));
+    if (c->piv_used)
+      CK(cudaMemcpyAsync(nb.p, c->d_piv.p, c->piv_used * sizeof(int2),
+                         cudaMemcpyDeviceToDevice, c->stream));
+    c->sync();
+    c->d_piv.free();
+    c->d_piv = nb;
+  }
+}
+
+void download_items(hmgpu_ctx* c) {
+  if (c->items.empty()) return;
+  CK(cudaMemcpyAsync(c->items.data(), c->d_items.p, c->items.size() * sizeof(Item),
+                     cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+}
+
+// moves `ids` to fresh storage at the arena end with `caps` columns
+void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>& caps) {
+  if (ids.empty()) return;
+  long long extra = 0, extrap = 0;
+  std::vector<long long> nu(ids.size()), nv(ids.size()), np(ids.size());
+  for (size_t t = 0; t < ids.size(); ++t) {
+    const Item& it = c->items[ids[t]];
+    nu[t] = c->arena_used + extra;
+    extra += align2((long long)it.m * caps[t]);
+    nv[t] = c->arena_used + extra;
+    extra += align2((long long)it.n * caps[t]);
+    np[t] = c->piv_used + extrap;
+    extrap += caps[t];
+  }
+  arena_reserve(c, extra, extrap);
+  DBuf<int> d_ids, d_caps;
+  DBuf<long long> d_nu, d_nv, d_np;
+  d_ids.upload(ids, c->stream);
+  d_caps.upload(caps, c->stream);
+  d_nu.upload(nu, c->stream);
+  d_nv.upload(nv, c->stream);
+  d_np.upload(np, c->stream);
+  c->timed("relocate", [&] {
+    relocate_kernel<<<grid_for(c, (long long)ids.size() / 8 + 1), 256, 0, c->stream>>>(
+        c->d_items.p, d_ids.p, d_nu.p, d_nv.p, d_np.p, d_caps.p, (int)ids.size(),
+        c->d_arena.p, c->d_arena.p, c->d_piv.p, c->d_piv.p);
+  });
+  c->arena_used += extra;
+  c->piv_used += extrap;
+  c->sync();
+  d_ids.free(); d_caps.free(); d_nu.free(); d_nv.free(); d_np.free();
+}
+
+// runs the ACA state machines of `list` to completion, regrowing the column
+// capacity of items that run out of it (resume is exact: same state)
+void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches) {
+  const double sf = c->eps * (1.0 - c->beta) / (1.0 + c->eps);  // aca.cpp:114
+  int passes = 0;
+  while (!list.empty()) {
+    c->d_list.upload(list, c->stream);
+    CK(cudaMemsetAsync(c->d_counter.p, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_overflow.p, 0, sizeof(int), c->stream));
+    const int nwarps = (int)list.size();
+    const int grid = grid_for(c, (nwarps + 7) / 8, 8);
+    c->timed("aca", [&] {
+      aca_kernel<<<grid, 256, 0, c->stream>>>(
+          c->geom, c->d_items.p, c->d_list.p, (int)list.size(), c->d_counter.p,
+          c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
+          c->d_overflow.p);
+    });
+    int over = 0;
+    CK(cudaMemcpyAsync(&over, c->d_overflow.p, sizeof(int), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    if (over == 0) break;
+    ++passes;
+    download_items(c);
+    std::vector<int> ids, caps;
+    for (int idx : list) {
+      const Item& it = c->items[idx];
+      if (it.status != ST_OVERFLOW) continue;
+      const long long capr = std::min<long long>(c->max_rank, std::min(it.m, it.n));
+      ids.push_back(idx);
+      caps.push_back((int)std::min<long long>(capr, std::max(2 * it.cap, it.cap + 8)));
+    }
+    relocate(c, ids, caps);
+    list = ids;
+  }
+  if (relaunches) *relaunches += passes;
+}
+
+// packs the arena: every item gets exactly K (+ slack) columns
+void compact(hmgpu_ctx* c, int slack) {
+  download_items(c);
+  const size_t ni = c->items.size();
+  if (ni == 0) return;
+  std::vector<long long> nu(ni), nv(ni), np(ni);
+  std::vector<int> ids(ni), caps(ni);
+  long long used = 0, usedp = 0;
+  for (size_t t = 0; t < ni; ++t) {
+    const Item& it = c->items[t];
+    const long long capr = std::min<long long>(c->max_rank, std::min(it.m, it.n));
+    const int cap = (int)std::min<long long>(capr, it.k + slack);
+    ids[t] = (int)t;
+    caps[t] = std::max(cap, it.k);
+    nu[t] = used;
+    used += align2((long long)it.m * caps[t]);
+    nv[t] = used;
+    used += align2((long long)it.n * caps[t]);
+    np[t] = usedp;
+    usedp += std::max(caps[t], 1);
+  }
+  DBuf<double> na;
+  na.alloc((size_t)used + 2);
+  DBuf<int2> npv;
+  npv.alloc((size_t)usedp + 1);
+  DBuf<int> d_ids, d_caps;
+  DBuf<long long> d_nu, d_nv, d_np;
+  d_ids.upload(ids, c->stream);
+  d_caps.upload(caps, c->stream);
+  d_nu.upload(nu, c->stream);
+  d_nv.upload(nv, c->stream);
+  d_np.upload(np, c->stream);
+  c->timed("compact", [&] {
+    relocate_kernel<<<grid_for(c, (long long)ni / 8 + 1), 256, 0, c->stream>>>(
+        c->d_items.p, d_ids.p, d_nu.p, d_nv.p, d_np.p, d_caps.p, (int)ni,
+        c->d_arena.p, na.p, c->d_piv.p, npv.p);
+  });
+  c->sync();
+  c->d_arena.free();
+  c->d_arena = na;
+  c->arena_used = used;
+  c->d_piv.free();
+  c->d_piv = npv;
+  c->piv_used = usedp;
+  d_ids.free(); d_caps.free(); d_nu.free(); d_nv.free(); d_np.free();
+  download_items(c);
+}
+
+// block-row matvec work lists and the leaf reduction CSR
+void build_matvec(hmgpu_ctx* c) {
+  c->mvb.clear();
+  c->kmax = 1;
+  long long prow = 0;
+  std::vector<long long> bytes;
+  for (int b = 0; b < c->n_blocks; ++b) {
+    const int* B = &c->blocks[4 * b];
+    const int* rn = &c->rnodes[4 * B[0]];
+    const int* cn = &c->cnodes[4 * B[1]];
+    if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
+    MvBlock mb{};
+    mb.m = rn[1] - rn[0];
+    mb.n = cn[1] - cn[0];
+    mb.row0 = rn[0];
+    mb.col0 = cn[0];
+    mb.dense = B[2] ? 0 : 1;
+    mb.item0 = c->item_of_block[b];
+    mb.dense_off = mb.dense ? c->dblocks[c->dense_of_block[b]].off : 0;
+    mb.prow = prow;
+    prow += mb.m;
+    long long by = 0;
+    if (mb.dense) {
+      by = (long long)c->NC * mb.m * mb.n;
+    } else {
+      for (int q = 0; q < c->NC; ++q) {
+        const Item& it = c->items[mb.item0 + q];
+        by += (long long)it.k * (mb.m + mb.n);
+        c->kmax = std::max(c->kmax, it.k);
+      }
+    }
+    bytes.push_back(by);
+    c->mvb.push_back(mb);
+  }
+  c->part_rows = prow;
+  c->n_mv = (int)c->mvb.size();
+  std::vector<int> order(c->n_mv);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return bytes[a] > bytes[b]; });
+  c->d_mvb.upload(c->mvb, c->stream);
+  c->d_mvorder.upload(order, c->stream);
+
+  // leaves of the row tree inside the shard, in index order
+  c->leaf_begin.clear();
+  c->leaf_end.clear();
+  const int nrn = (int)c->rnodes.size() / 4;
+  for (int t = 0; t < nrn; ++t) {
+    const int* nd = &c->rnodes[4 * t];
+    if (nd[2] >= 0) continue;
+    if (nd[0] < c->row_begin || nd[1] > c->row_end) continue;
+    c->leaf_begin.push_back(nd[0]);
+    c->leaf_end.push_back(nd[1]);
+  }
+  std::vector<int> lorder(c->leaf_begin.size());
+  std::iota(lorder.begin(), lorder.end(), 0);
+  std::sort(lorder.begin(), lorder.end(),
+            [&](int a, int b) { return c->leaf_begin[a] < c->leaf_begin[b]; });
+  std::vector<int> lb(lorder.size()), le(lorder.size());
+  for (size_t i = 0; i < lorder.size(); ++i) {
+    lb[i] = c->leaf_begin[lorder[i]];
+    le[i] = c->leaf_end[lorder[i]];
+  }
+  c->leaf_begin = lb;
+  c->leaf_end = le;
+  const int nl = (int)lb.size();
+  std::vector<std::vector<long long>> lists(nl);
+  for (const MvBlock& mb : c->mvb) {
+    // leaves covered by rows [row0, row0+m)
+    int l0 = (int)(std::lower_bound(lb.begin(), lb.end(), mb.row0) - lb.begin());
+    for (int l = l0; l < nl && lb[l] < mb.row0 + mb.m; ++l) {
+      if (le[l] > mb.row0 + mb.m)
+        fail(HMGPU_ERR_INVALID, "block rows do not align with row-tree leaves");
+      lists[l].push_back(mb.prow + (lb[l] - mb.row0));
+    }
+  }
+  c->leaf_ptr.assign(nl + 1, 0);
+  c->leaf_prow.clear();
+  for (int l = 0; l < nl; ++l) {
+    c->leaf_ptr[l + 1] = c->leaf_ptr[l] + (int)lists[l].size();
+    c->leaf_prow.insert(c->leaf_prow.end(), lists[l].begin(), lists[l].end());
+  }
+  c->d_leaf_begin.upload(c->leaf_begin, c->stream);
+  c->d_leaf_end.upload(c->leaf_end, c->stream);
+  c->d_leaf_ptr.upload(c->leaf_ptr, c->stream);
+  c->d_leaf_prow.upload(c->leaf_prow, c->stream);
+  c->sync();
+}
+
+// refresh kmax after rank changes (promote / extend)
+void refresh_matvec_ranks(hmgpu_ctx* c) {
+  c->kmax = 1;
+  for (const Item& it : c->items) c->kmax = std::max(c->kmax, it.k);
+}
+
+void check_ptr_kind(int ptr_kind) {
+  if (ptr_kind != HMGPU_PTR_HOST && ptr_kind != HMGPU_PTR_DEVICE)
+    fail(HMGPU_ERR_INVALID, "ptr_kind must be HMGPU_PTR_HOST or HMGPU_PTR_DEVICE");
+}
+
+void gather_x(hmgpu_ctx* c, const double* dx, int nrhs) {
+  const long long total = (long long)c->ndof_cols() * nrhs;
+  c->d_xi.ensure((size_t)total);
+  c->timed("gather", [&] {
+    const int grid = grid_for(c, (total + 255) / 256, 16);
+    if (c->NC == 6)
+      gather_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
+                                                   c->n_cols, nrhs);
+    else
+      gather_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
+                                                   c->n_cols, nrhs);
+  });
+}
+
+std::vector<int> items_from_pairs(hmgpu_ctx* c, int n, const int* cb) {
+  std::vector<int> out;
+  for (int t = 0; t < n; ++t) {
+    const int comp = cb[2 * t], b = cb[2 * t + 1];
+    if (comp < 0 || comp >= c->NC || b < 0 || b >= c->n_blocks)
+      fail(HMGPU_ERR_INVALID, "bad (component, block) pair");
+    const int i0 = c->item_of_block[b];
+    if (i0 < 0) continue;  // dense or not owned: no-op like the reference
+    out.push_back(i0 + comp);
+  }
+  return out;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int hmgpu_device_count(int* n) {
+  if (!n) return HMGPU_ERR_INVALID;
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  *n = c;
+  return HMGPU_OK;
+}
+
+int hmgpu_create(int device, hmgpu_ctx** out) {
+  if (!out) return HMGPU_ERR_INVALID;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return HMGPU_ERR_NODEVICE;
+  if (device < 0 || device >= count) return HMGPU_ERR_INVALID;
+  hmgpu_ctx* c = new (std::nothrow) hmgpu_ctx();
+  if (!c) return HMGPU_ERR_OOM;
+  c->device = device;
+  const int st = guard(c, [&] {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    c->d_counter.alloc(1);
+    c->d_overflow.alloc(1);
+    c->rules.far_ratio = 4.0;
+    c->rules.mid_ratio = 1.5;
+  });
+  if (st != HMGPU_OK) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return HMGPU_OK;
+}
+
+int hmgpu_destroy(hmgpu_ctx* ctx) {
+  if (!ctx) return HMGPU_ERR_INVALID;
+  delete ctx;
+  return HMGPU_OK;
+}
+
+const char* hmgpu_last_error(const hmgpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+int hmgpu_get_stream(hmgpu_ctx* ctx, void** s) {
+  return guard(ctx, [&] {
+    if (!s) fail(HMGPU_ERR_INVALID, "null output");
+    *s = (void*)ctx->stream;
+  });
+}
+
+int hmgpu_set_rule(hmgpu_ctx* ctx, int tier, int npts, const double* a,
+                   const double* b, const double* w) {
+  return guard(ctx, [&] {
+    if (tier < 0 || tier > 2) fail(HMGPU_ERR_INVALID, "tier must be 0, 1 or 2");
+    if (npts < 1 || npts > 12 || !a || !b || !w)
+      fail(HMGPU_ERR_INVALID, "rule must have 1..12 points");
+    ctx->rules.n[tier] = npts;
+    for (int q = 0; q < npts; ++q) {
+      ctx->rules.a[tier][q] = a[q];
+      ctx->rules.b[tier][q] = b[q];
+      ctx->rules.w[tier][q] = w[q];
+    }
+    ctx->rules_set[tier] = true;
+  });
+}
+
+int hmgpu_set_tier_ratios(hmgpu_ctx* ctx, double far_ratio, double mid_ratio) {
+  return guard(ctx, [&] {
+    if (!(far_ratio > 0) || !(mid_ratio > 0))
+      fail(HMGPU_ERR_INVALID, "ratios must be positive");
+    ctx->rules.far_ratio = far_ratio;
+    ctx->rules.mid_ratio = mid_ratio;
+  });
+}
+
+int hmgpu_set_kelvin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
+                              int n_tri, const int* tris, const double* centroid,
+                              const double* area, const double* diam, double E,
+                              double nu) {
+  return guard(ctx, [&] {
+    if (n_vert < 3 || n_tri < 1 || !verts || !tris || !centroid || !area || !diam)
+      fail(HMGPU_ERR_INVALID, "bad kelvin geometry");
+    if (E <= 0.0) fail(HMGPU_ERR_INVALID, "lame_constants: E must be positive");
+    if (nu <= 0.0 || nu >= 0.5)
+      fail(HMGPU_ERR_INVALID, "lame_constants: nu must lie in (0, 1/2)");
+    for (long long t = 0; t < 3LL * n_tri; ++t)
+      if (tris[t] < 0 || tris[t] >= n_vert)
+        fail(HMGPU_ERR_INVALID, "vertex index out of range");
+    ctx->kind = KIND_KELVIN;
+    ctx->NC = 6;
+    ctx->n_vert = n_vert;
+    ctx->n_tri = n_tri;
+    ctx->verts.assign(verts, verts + 3LL * n_vert);
+    ctx->tris.assign(tris, tris + 3LL * n_tri);
+    ctx->centroid.assign(centroid, centroid + 3LL * n_tri);
+    ctx->area.assign(area, area + n_tri);
+    ctx->diam.assign(diam, diam + n_tri);
+    ctx->E = E;
+    ctx->nu = nu;
+    ctx->assembled = false;
+  });
+}
+
+int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag) {
+  return guard(ctx, [&] {
+    if (n < 1 || !pts) fail(HMGPU_ERR_INVALID, "bad points");
+    ctx->kind = KIND_NEWTON;
+    ctx->NC = 1;
+    ctx->n_pts = n;
+    ctx->pts.assign(pts, pts + 3LL * n);
+    ctx->diag = diag;
+    ctx->assembled = false;
+  });
+}
+
+int hmgpu_set_dense_matrix(hmgpu_ctx* ctx, int m, int n, const double* a) {
+  return guard(ctx, [&] {
+    if (m < 1 || n < 1 || !a) fail(HMGPU_ERR_INVALID, "bad matrix");
+    ctx->kind = KIND_DENSE;
+    ctx->NC = 1;
+    ctx->am = m;
+    ctx->an = n;
+    ctx->amat.assign(a, a + (long long)m * n);
+    ctx->assembled = false;
+  });
+}
+
+int hmgpu_set_partition(hmgpu_ctx* ctx, int n_rows, const int* row_perm,
+                        int n_row_nodes, const int* row_nodes4, int n_cols,
+                        const int* col_perm, int n_col_nodes, const int* col_nodes4,
+                        int n_blocks, const int* blocks4, int row_begin,
+                        int row_end) {
+  return guard(ctx, [&] {
+    if (n_rows < 1 || n_cols < 1 || !row_perm || !col_perm || !row_nodes4 ||
+        !col_nodes4 || !blocks4 || n_blocks < 1 || n_row_nodes < 1 ||
+        n_col_nodes < 1)
+      fail(HMGPU_ERR_INVALID, "bad partition arguments");
+    if (row_begin < 0 || row_end > n_rows || row_begin >= row_end)
+      fail(HMGPU_ERR_INVALID, "bad row shard range");
+    ctx->n_rows = n_rows;
+    ctx->n_cols = n_cols;
+    ctx->rperm.assign(row_perm, row_perm + n_rows);
+    ctx->cperm.assign(col_perm, col_perm + n_cols);
+    ctx->rnodes.assign(row_nodes4, row_nodes4 + 4LL * n_row_nodes);
+    ctx->cnodes.assign(col_nodes4, col_nodes4 + 4LL * n_col_nodes);
+    ctx->blocks.assign(blocks4, blocks4 + 4LL * n_blocks);
+    ctx->n_blocks = n_blocks;
+    ctx->row_begin = row_begin;
+    ctx->row_end = row_end;
+    for (int b = 0; b < n_blocks; ++b)
+      if (blocks4[4 * b] < 0 || blocks4[4 * b] >= n_row_nodes ||
+          blocks4[4 * b + 1] < 0 || blocks4[4 * b + 1] >= n_col_nodes)
+        fail(HMGPU_ERR_INVALID, "block references a missing node");
+    ctx->same_tree = n_rows == n_cols && ctx->rperm == ctx->cperm &&
+                     ctx->rnodes == ctx->cnodes;
+    ctx->have_partition = true;
+    ctx->assembled = false;
+  });
+}
+
+int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
+                   int lookahead, long long max_rank, hmgpu_assembly_stats* stats) {
+  return guard(c, [&] {
+    if (!c->have_partition) fail(HMGPU_ERR_STATE, "set_partition first");
+    if (c->kind < 0) fail(HMGPU_ERR_STATE, "set an entry provider first");
+    if (initial_rank < 0) {  // aca_run argument checks (aca.cpp:108-110)
+      if (eps <= 0.0) fail(HMGPU_ERR_INVALID, "aca_run: eps must be positive");
+      if (beta_stop <= 0.0 || beta_stop >= 1.0)
+        fail(HMGPU_ERR_INVALID, "aca_run: beta must be in (0,1)");
+    }
+    if (lookahead < 0 || max_rank < 1) fail(HMGPU_ERR_INVALID, "bad lookahead/max_rank");
+    if (c->kind == KIND_KELVIN) upload_rules(c);
+    build_geometry(c);
+    c->eps = eps;
+    c->beta = beta_stop;
+    c->initial_rank = initial_rank;
+    c->lookahead = lookahead;
+    c->max_rank = max_rank;
+    for (auto& p : c->pending) {
+      c->ev_pool.push_back(p.a);
+      c->ev_pool.push_back(p.b);
+    }
+    c->pending.clear();
+
+    cudaEvent_t t0, t1, tn0, tn1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventCreate(&tn0));
+    CK(cudaEventCreate(&tn1));
+    CK(cudaEventRecord(t0, c->stream));
+
+    // work items and dense blocks of the owned block rows
+    c->items.clear();
+    c->dblocks.clear();
+    c->item_of_block.assign(c->n_blocks, -1);
+    c->dense_of_block.assign(c->n_blocks, -1);
+    c->arena_used = 0;
+    c->piv_used = 0;
+    c->dense_used = 0;
+    long long cons_used = 0;
+    const int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
+    for (int b = 0; b < c->n_blocks; ++b) {
+      const int* B = &c->blocks[4 * b];
+      const int* rn = &c->rnodes[4 * B[0]];
+      const int* cn = &c->cnodes[4 * B[1]];
+      if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
+      const int m = rn[1] - rn[0], n = cn[1] - cn[0];
+      if (B[2]) {
+        c->item_of_block[b] = (int)c->items.size();
+        const long long capr = std::min<long long>(max_rank, std::min(m, n));
+        const int cap = (int)std::min<long long>(capr, cap_init);
+        for (int q = 0; q < c->NC; ++q) {
+          Item it{};
+          it.m = m;
+          it.n = n;
+          it.row0 = rn[0];
+          it.col0 = cn[0];
+          it.comp = q;
+          it.cap = cap;
+          it.block = b;
+          it.phase = initial_rank >= 0 ? PH_INIT : PH_RUN;
+          it.steps_left = initial_rank >= 0 ? initial_rank : 0;
+          it.last_stop = STOP_NONE;
+          it.u_off = c->arena_used;
+          c->arena_used += align2((long long)m * cap);
+          it.v_off = c->arena_used;
+          c->arena_used += align2((long long)n * cap);
+          it.p_off = c->piv_used;
+          c->piv_used += std::max(cap, 1);
+          it.z_off = cons_used;
+          cons_used += align16(m);
+          c->items.push_back(it);
+        }
+      } else {
+        c->dense_of_block[b] = (int)c->dblocks.size();
+        DenseBlock db{m, n, rn[0], cn[0], c->dense_used};
+        c->dense_used += align2((long long)c->NC * m * n);
+        c->dblocks.push_back(db);
+      }
+    }
+    c->d_items.upload(c->items, c->stream);
+    c->d_arena.alloc((size_t)c->arena_used + 2);
+    c->d_piv.alloc((size_t)c->piv_used + 1);
+    c->d_cons.alloc((size_t)cons_used + 16);
+    CK(cudaMemsetAsync(c->d_cons.p, 0, cons_used + 16, c->stream));
+    c->d_dense.alloc((size_t)c->dense_used + 2);
+    c->d_dblocks.upload(c->dblocks, c->stream);
+
+    // near-field fill
+    CK(cudaEventRecord(tn0, c->stream));
+    if (!c->dblocks.empty()) {
+      c->timed("nearfield", [&] {
+        const int grid = grid_for(c, (long long)c->dblocks.size(), 8);
+        if (c->NC == 6)
+          nearfield_kernel<6><<<grid, 256, 0, c->stream>>>(
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p);
+        else
+          nearfield_kernel<1><<<grid, 256, 0, c->stream>>>(
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p);
+      });
+    }
+    CK(cudaEventRecord(tn1, c->stream));
+
+    // ACA, largest blocks first
+    std::vector<int> list(c->items.size());
+    std::iota(list.begin(), list.end(), 0);
+    std::stable_sort(list.begin(), list.end(), [&](int a, int b) {
+      return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
+    });
+    int relaunch = 0;
+    run_aca(c, list, &relaunch);
+    compact(c, 0);
+    CK(cudaEventRecord(t1, c->stream));
+    c->sync();
+    float ms_total = 0, ms_near = 0;
+    CK(cudaEventElapsedTime(&ms_total, t0, t1));
+    CK(cudaEventElapsedTime(&ms_near, tn0, tn1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaEventDestroy(tn0);
+    cudaEventDestroy(tn1);
+    build_matvec(c);
+    c->assembled = true;
+    if (stats) {
+      hmgpu_assembly_stats s{};
+      for (const Item& it : c->items) {
+        s.aca_entries += it.entries;
+        s.aca_steps += it.steps;
+        s.pivots += it.k;
+      }
+      for (const DenseBlock& d : c->dblocks)
+        s.dense_entries += (long long)c->NC * d.m * d.n;
+      s.ms_total = ms_total;
+      s.ms_nearfield = ms_near;
+      s.ms_aca = ms_total - ms_near;
+      s.aca_relaunches = relaunch;
+      *stats = s;
+    }
+  });
+}
+
+int hmgpu_ranks(hmgpu_ctx* c, int* k_cur, int* k_look, int* consumed, int* last_stop) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    for (int q = 0; q < c->NC; ++q)
+      for (int b = 0; b < c->n_blocks; ++b) {
+        const long long o = (long long)q * c->n_blocks + b;
+        const int i0 = c->item_of_block[b];
+        const Item* it = i0 >= 0 ? &c->items[i0 + q] : nullptr;
+        if (k_cur) k_cur[o] = it ? it->kcur : -1;
+        if (k_look) k_look[o] = it ? it->k : -1;
+        if (consumed) consumed[o] = it ? it->nconsumed : -1;
+        if (last_stop) last_stop[o] = it ? it->last_stop : -1;
+      }
+  });
+}
+
+int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
+                 int ptr_kind) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (!x || !y || nrhs < 1) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
+    if (mode != HMGPU_MODE_CURRENT && mode != HMGPU_MODE_LOOKAHEAD)
+      fail(HMGPU_ERR_INVALID, "bad mode");
+    check_ptr_kind(ptr_kind);
+    const int NOUT = c->NC == 6 ? 3 : 1;
+    const long long nx = (long long)c->ndof_cols() * nrhs;
+    const long long ny = (long long)c->ndof_rows() * nrhs;
+    const double* dx = x;
+    double* dy = y;
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      c->d_x.ensure((size_t)nx);
+      c->d_y.ensure((size_t)ny);
+      CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+      dx = c->d_x.p;
+      dy = c->d_y.p;
+    }
+    if (c->row_begin != 0 || c->row_end != c->n_rows)
+      CK(cudaMemsetAsync(dy, 0, ny * sizeof(double), c->stream));
+    gather_x(c, dx, nrhs);
+    c->d_ypart.ensure((size_t)std::max<long long>(1, c->part_rows * NOUT * nrhs));
+    const size_t smem = sizeof(double) * 2 * (size_t)c->kmax * nrhs;
+    if (smem > 200 * 1024) fail(HMGPU_ERR_INVALID, "rank x nrhs too large for matvec");
+    c->timed("hmv_blocks", [&] {
+      const int grid = grid_for(c, c->n_mv, 8);
+      if (c->NC == 6) {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
+            c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+            c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+      } else {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
+            c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+            c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+      }
+    });
+    c->timed("hmv_reduce", [&] {
+      const int nl = (int)c->leaf_begin.size();
+      const int grid = grid_for(c, nl, 16);
+      if (c->NC == 6)
+        hmv_reduce_kernel<3><<<grid, 128, 0, c->stream>>>(
+            c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+            nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+      else
+        hmv_reduce_kernel<1><<<grid, 128, 0, c->stream>>>(
+            c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+            nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+    });
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    }
+  });
+}
+
+int hmgpu_promote(hmgpu_ctx* c, int n, const int* comp_block) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (n < 0 || (n > 0 && !comp_block)) fail(HMGPU_ERR_INVALID, "bad pairs");
+    std::vector<int> ids = items_from_pairs(c, n, comp_block);
+    if (ids.empty()) return;
+    c->d_list.upload(ids, c->stream);
+    c->timed("promote", [&] {
+      promote_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
+          c->d_items.p, c->d_list.p, (int)ids.size());
+    });
+    for (int i : ids) c->items[i].kcur = c->items[i].k;
+    c->sync();
+  });
+}
+
+int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (n < 0 || (n > 0 && !comp_block) || steps < 0)
+      fail(HMGPU_ERR_INVALID, "bad extend arguments");
+    std::vector<int> ids = items_from_pairs(c, n, comp_block);
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    if (ids.empty() || steps == 0) return;
+    if (c->kind == KIND_KELVIN) upload_rules(c);
+    c->d_list.upload(ids, c->stream);
+    c->timed("prep_extend", [&] {
+      prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
+          c->d_items.p, c->d_list.p, (int)ids.size(), steps);
+    });
+    c->sync();
+    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+      return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
+    });
+    run_aca(c, ids, nullptr);
+    download_items(c);
+    refresh_matvec_ranks(c);
+  });
+}
+
+int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_vals,
+                     long long* meta4, double* vals) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (!n_terms || !n_vals) fail(HMGPU_ERR_INVALID, "null outputs");
+    std::vector<TailTerm> terms;
+    long long off = 0;
+    for (int b = 0; b < c->n_blocks; ++b) {
+      const int i0 = c->item_of_block[b];
+      if (i0 < 0) continue;
+      for (int q = 0; q < c->NC; ++q) {
+        const Item& it = c->items[i0 + q];
+        if (it.k <= it.kcur) continue;
+        const int nocc = (c->NC == 6 && c_comp_host_r(q) != c_comp_host_c(q)) ? 2 : 1;
+        terms.push_back({i0 + q, nocc, off});
+        off += (long long)nocc * it.m;
+      }
+    }
+    // terms in component-major order (the by-H-matrix grouping of
+    // gamma_contributions, amvm.cpp:135-150)
+    std::stable_sort(terms.begin(), terms.end(), [&](const TailTerm& a, const TailTerm& b) {
+      return c->items[a.item].comp < c->items[b.item].comp;
+    });
+    off = 0;
+    for (TailTerm& t : terms) {
+      t.off = off;
+      off += (long long)t.nocc * c->items[t.item].m;
+    }
+    *n_terms = (int)terms.size();
+    *n_vals = off;
+    if (!meta4) return;
+    if (!x || !vals) fail(HMGPU_ERR_INVALID, "null x/vals");
+    for (size_t t = 0; t < terms.size(); ++t) {
+      const Item& it = c->items[terms[t].item];
+      meta4[4 * t] = it.comp;
+      meta4[4 * t + 1] = it.block;
+      meta4[4 * t + 2] = terms[t].nocc;
+      meta4[4 * t + 3] = terms[t].off;
+    }
+    if (terms.empty()) return;
+    const long long nx = c->ndof_cols();
+    c->d_x.ensure((size_t)nx);
+    CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    gather_x(c, c->d_x.p, 1);
+    DBuf<TailTerm> d_terms;
+    d_terms.upload(terms, c->stream);
+    DBuf<double> d_out;
+    d_out.alloc((size_t)off);
+    c->timed("tail", [&] {
+      const int grid = grid_for(c, ((long long)terms.size() + 7) / 8, 8);
+      if (c->NC == 6)
+        tail_kernel<3><<<grid, 256, 0, c->stream>>>(d_terms.p, (int)terms.size(),
+                                                   c->d_items.p, c->d_arena.p,
+                                                   c->d_xi.p, d_out.p, 1);
+      else
+        tail_kernel<1><<<grid, 256, 0, c->stream>>>(d_terms.p, (int)terms.size(),
+                                                   c->d_items.p, c->d_arena.p,
+                                                   c->d_xi.p, d_out.p, 0);
+    });
+    CK(cudaMemcpyAsync(vals, d_out.p, off * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    d_terms.free();
+    d_out.free();
+  });
+}
+
+int hmgpu_download_factor(hmgpu_ctx* c, int comp, int block, int* m, int* n, int* K,
+                          int* k_cur, double* U, double* V, int* piv, double* frob_sq) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (comp < 0 || comp >= c->NC || block < 0 || block >= c->n_blocks)
+      fail(HMGPU_ERR_INVALID, "bad (comp, block)");
+    const int i0 = c->item_of_block[block];
+    if (i0 < 0) fail(HMGPU_ERR_INVALID, "block is dense or not owned");
+    Item it;
+    CK(cudaMemcpyAsync(&it, c->d_items.p + i0 + comp, sizeof(Item),
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (m) *m = it.m;
+    if (n) *n = it.n;
+    if (K) *K = it.k;
+    if (k_cur) *k_cur = it.kcur;
+    if (frob_sq) *frob_sq = it.frob_sq;
+    if (!U) return;
+    if (!V || !piv) fail(HMGPU_ERR_INVALID, "null V/piv");
+    CK(cudaMemcpyAsync(U, c->d_arena.p + it.u_off, sizeof(double) * it.m * it.k,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(V, c->d_arena.p + it.v_off, sizeof(double) * it.n * it.k,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(piv, c->d_piv.p + it.p_off, sizeof(int2) * it.k,
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  });
+}
+
+int hmgpu_download_dense(hmgpu_ctx* c, int comp, int block, double* out) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (comp < 0 || comp >= c->NC || block < 0 || block >= c->n_blocks || !out)
+      fail(HMGPU_ERR_INVALID, "bad (comp, block)");
+    const int d = c->dense_of_block[block];
+    if (d < 0) fail(HMGPU_ERR_INVALID, "block is low-rank or not owned");
+    const DenseBlock& db = c->dblocks[d];
+    const long long mn = (long long)db.m * db.n;
+    CK(cudaMemcpyAsync(out, c->d_dense.p + db.off + comp * mn, sizeof(double) * mn,
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  });
+}
+
+int hmgpu_storage(hmgpu_ctx* c, hmgpu_storage_info* info) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (!info) fail(HMGPU_ERR_INVALID, "null info");
+    double cur = 0, tail = 0, dense = 0;
+    long long flops = 0;
+    for (const Item& it : c->items) {
+      cur += (double)it.kcur * (it.m + it.n);
+      tail += (double)(it.k - it.kcur) * (it.m + it.n);
+      const int w = (c->NC == 6 && c_comp_host_r(it.comp) != c_comp_host_c(it.comp)) ? 2 : 1;
+      flops += 2LL * w * it.kcur * (it.m + it.n);
+    }
+    for (const DenseBlock& d : c->dblocks) {
+      for (int q = 0; q < c->NC; ++q) {
+        const int w = (c->NC == 6 && c_comp_host_r(q) != c_comp_host_c(q)) ? 2 : 1;
+        flops += 2LL * w * d.m * d.n;
+      }
+      dense += (double)c->NC * d.m * d.n;
+    }
+    info->mb_current = (cur + dense) * 8.0 / (1 << 20);
+    info->mb_tail = tail * 8.0 / (1 << 20);
+    info->mb_dense = dense * 8.0 / (1 << 20);
+    info->mb_arena_allocated = (double)c->d_arena.n * 8.0 / (1 << 20);
+    // compulsory traffic: every stored entry once + x read + y written
+    info->matvec_bytes = (long long)(8.0 * (cur + dense)) +
+                         8LL * (c->ndof_cols() + c->ndof_rows());
+    info->matvec_flops = flops;
+  });
+}
+
+int hmgpu_set_profiling(hmgpu_ctx* c, int on) {
+  return guard(c, [&] { c->prof = on != 0; });
+}
+
+int hmgpu_kernel_times(hmgpu_ctx* c, const char* name, double* ms, long long* launches,
+                       int reset) {
+  return guard(c, [&] {
+    if (!name) fail(HMGPU_ERR_INVALID, "null name");
+    c->resolve_times();
+    auto it = c->times.find(name);
+    if (ms) *ms = it == c->times.end() ? 0.0 : it->second.ms;
+    if (launches) *launches = it == c->times.end() ? 0 : it->second.launches;
+    if (reset && it != c->times.end()) it->second = KTime{};
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,742 @@
+// Device side of the B200 H-matrix hot path: fused Kelvin / Newton / dense
+// entry providers, batched warp-per-block ACA, near-field fill, H-matvec
+// sweep and look-ahead tail products.  fp64 throughout (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hmgpu {
+
+// ---------------------------------------------------------------------------
+// quadrature tiers in constant memory: tier 0 far (order 2, 3 points),
+// 1 mid (order 4, 6 points), 2 near (order 5, 7 points)
+// (point_order, proj/src/kernels.cpp:87-93; gauss_rule, quadrature.cpp:55-95)
+struct RuleTable {
+  int n[3];
+  int pad;
+  double a[3][12], b[3][12], w[3][12];
+  double far_ratio, mid_ratio;
+};
+__constant__ RuleTable c_rules;
+
+// component (r,c) of the symmetric 3x3 grid, row-major upper triangle
+__constant__ int c_comp_r[6] = {0, 0, 0, 1, 1, 2};
+__constant__ int c_comp_c[6] = {0, 1, 2, 1, 2, 2};
+
+enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2 };
+
+// Per-problem geometry, passed by value to every kernel.
+struct Geom {
+  int kind;
+  int same_tree;            // row internal index == col internal index <=> same DOF
+  const double4* rowpt;     // evaluation points, internal row order (x,y,z,-)
+  const double* tri;        // kelvin: 16 doubles per column triangle, internal order
+                            //   v0[3] e1[3] e2[3] cen[3] area diam pad pad
+  const double4* colpt;     // newton: column points, internal column order
+  const double* A;          // dense: column-major matrix, external ids
+  long long lda;
+  const int* rperm;         // internal -> external (rows)
+  const int* cperm;         // internal -> external (cols)
+  double cst;               // (1+nu) / (8 pi E (1-nu))      (kernels.cpp:24)
+  double c34;               // 3 - 4 nu
+  double diag;              // newton diagonal value
+};
+
+// ---------------------------------------------------------------------------
+// Kelvin collocation: quadrature tier decided with IEEE round-to-nearest
+// operations in the reference's order so that it is bit-identical to the
+// host/oracle decision: gap = |p - c_j| - 0.5 d_j (kernels.cpp:88-92).
+__device__ __forceinline__ int kelvin_tier(double px, double py, double pz,
+                                           const double* T) {
+  const double dx = __dsub_rn(px, T[9]);
+  const double dy = __dsub_rn(py, T[10]);
+  const double dz = __dsub_rn(pz, T[11]);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                              __dmul_rn(dz, dz));
+  const double dj = T[13];
+  const double gap = __dsub_rn(__dsqrt_rn(d2), __dmul_rn(0.5, dj));
+  if (gap >= __dmul_rn(c_rules.far_ratio, dj)) return 0;
+  if (gap >= __dmul_rn(c_rules.mid_ratio, dj)) return 1;
+  return 2;
+}
+
+__device__ __forceinline__ double sel3(int r, double x, double y, double z) {
+  return r == 0 ? x : (r == 1 ? y : z);
+}
+
+// Exact integral of the Kelvin tensor over the flat triangle for a point p
+// in its plane (builder-defined self term, closed form; see
+// oracle/hmbem_oracle.cpp Kelvin::self_term for the derivation).
+__device__ void kelvin_self6(const Geom& g, double px, double py, double pz,
+                             const double* T, double* out6) {
+  const double v[3][3] = {{T[0], T[1], T[2]},
+                          {T[0] + T[3], T[1] + T[4], T[2] + T[5]},
+                          {T[0] + T[6], T[1] + T[7], T[2] + T[8]}};
+  double nx = T[4] * T[8] - T[5] * T[7];
+  double ny = T[5] * T[6] - T[3] * T[8];
+  double nz = T[3] * T[7] - T[4] * T[6];
+  const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  nx /= nn;
+  ny /= nn;
+  nz /= nn;
+  double i1 = 0.0;
+  double irc[6] = {0, 0, 0, 0, 0, 0};
+  for (int e = 0; e < 3; ++e) {
+    const double* a = v[e];
+    const double* b = v[(e + 1) % 3];
+    double tx = b[0] - a[0], ty = b[1] - a[1], tz = b[2] - a[2];
+    const double len = sqrt(tx * tx + ty * ty + tz * tz);
+    tx /= len;
+    ty /= len;
+    tz /= len;
+    const double mx = ty * nz - tz * ny, my = tz * nx - tx * nz,
+                 mz = tx * ny - ty * nx;
+    const double pax = a[0] - px, pay = a[1] - py, paz = a[2] - pz;
+    const double pbx = b[0] - px, pby = b[1] - py, pbz = b[2] - pz;
+    const double h = pax * mx + pay * my + paz * mz;
+    const double s1 = pax * tx + pay * ty + paz * tz;
+    const double s2 = pbx * tx + pby * ty + pbz * tz;
+    const double r1 = sqrt(pax * pax + pay * pay + paz * paz);
+    const double r2 = sqrt(pbx * pbx + pby * pby + pbz * pbz);
+    const double lg = log((r2 + s2) / (r1 + s1));
+    const double dsin = s2 / r2 - s1 / r1;
+    const double dcos = h / r1 - h / r2;
+    i1 += h * lg;
+    const double m[3] = {mx, my, mz}, t[3] = {tx, ty, tz};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int r = c_comp_r[k], c = c_comp_c[k];
+      irc[k] += h * (m[r] * m[c] * dsin + (m[r] * t[c] + t[r] * m[c]) * dcos +
+                     t[r] * t[c] * (lg - dsin));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+    out6[k] = g.cst * ((c_comp_r[k] == c_comp_c[k] ? g.c34 * i1 : 0.0) + irc[k]);
+}
+
+// A_rc[i, j] = 2 area_j sum_q w_q S(p_i - y_q)_rc for one component
+// (colloc_single, kernels.cpp:176-187), S from kelvin_tensor (:21-28).
+__device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
+                                                int comp) {
+  const double4 p = g.rowpt[i];
+  const double* T = g.tri + 16LL * j;
+  const int r = c_comp_r[comp], c = c_comp_c[comp];
+  if (g.same_tree && i == j) {
+    double s6[6];
+    kelvin_self6(g, p.x, p.y, p.z, T, s6);
+    return s6[comp];
+  }
+  const int tier = kelvin_tier(p.x, p.y, p.z, T);
+  const double v0x = T[0], v0y = T[1], v0z = T[2];
+  const double e1x = T[3], e1y = T[4], e1z = T[5];
+  const double e2x = T[6], e2y = T[7], e2z = T[8];
+  double acc_d = 0.0, acc_x = 0.0;
+  const int nq = c_rules.n[tier];
+  for (int q = 0; q < nq; ++q) {
+    const double a = c_rules.a[tier][q], b = c_rules.b[tier][q],
+                 w = c_rules.w[tier][q];
+    const double dx = p.x - fma(b, e2x, fma(a, e1x, v0x));
+    const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
+    const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    const double ri = rsqrt(r2);
+    const double wr = w * ri;
+    acc_d += wr;
+    acc_x = fma(wr * ri * ri, sel3(r, dx, dy, dz) * sel3(c, dx, dy, dz), acc_x);
+  }
+  const double s = (r == c) ? fma(g.c34, acc_d, acc_x) : acc_x;
+  return 2.0 * T[12] * g.cst * s;
+}
+
+// all six components of one (point, triangle) pair (near-field fill)
+__device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
+                                              double* out6) {
+  const double4 p = g.rowpt[i];
+  const double* T = g.tri + 16LL * j;
+  if (g.same_tree && i == j) {
+    kelvin_self6(g, p.x, p.y, p.z, T, out6);
+    return;
+  }
+  const int tier = kelvin_tier(p.x, p.y, p.z, T);
+  const double v0x = T[0], v0y = T[1], v0z = T[2];
+  const double e1x = T[3], e1y = T[4], e1z = T[5];
+  const double e2x = T[6], e2y = T[7], e2z = T[8];
+  double ad = 0.0, a00 = 0.0, a01 = 0.0, a02 = 0.0, a11 = 0.0, a12 = 0.0,
+         a22 = 0.0;
+  const int nq = c_rules.n[tier];
+  for (int q = 0; q < nq; ++q) {
+    const double a = c_rules.a[tier][q], b = c_rules.b[tier][q],
+                 w = c_rules.w[tier][q];
+    const double dx = p.x - fma(b, e2x, fma(a, e1x, v0x));
+    const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
+    const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    const double ri = rsqrt(r2);
+    const double wr = w * ri;
+    const double wr3 = wr * ri * ri;
+    ad += wr;
+    const double tx = wr3 * dx, ty = wr3 * dy, tz = wr3 * dz;
+    a00 = fma(tx, dx, a00);
+    a01 = fma(tx, dy, a01);
+    a02 = fma(tx, dz, a02);
+    a11 = fma(ty, dy, a11);
+    a12 = fma(ty, dz, a12);
+    a22 = fma(tz, dz, a22);
+  }
+  const double f = 2.0 * T[12] * g.cst;
+  const double dd = g.c34 * ad;
+  out6[0] = f * (dd + a00);
+  out6[1] = f * a01;
+  out6[2] = f * a02;
+  out6[3] = f * (dd + a11);
+  out6[4] = f * a12;
+  out6[5] = f * (dd + a22);
+}
+
+// Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact
+__device__ __forceinline__ double newton_entry(const Geom& g, int i, int j) {
+  const double4 a = g.rowpt[i];
+  const double4 b = g.colpt[j];
+  const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y),
+               dz = __dsub_rn(a.z, b.z);
+  const double r = __dsqrt_rn(__dadd_rn(
+      __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  return r == 0.0 ? g.diag : __ddiv_rn(1.0, r);
+}
+
+__device__ __forceinline__ double dense_entry(const Geom& g, int i, int j) {
+  return g.A[(long long)g.rperm[i] + g.lda * (long long)g.cperm[j]];
+}
+
+// single entry of component `comp` at internal (row i, col j)
+__device__ __forceinline__ double entry1(const Geom& g, int i, int j,
+                                         int comp) {
+  if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp);
+  if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
+  return dense_entry(g, i, j);
+}
+
+// ---------------------------------------------------------------------------
+// ACA work item: one (admissible block, component).  State persists in
+// device memory so that assembly, capacity regrow and AMVM extension all
+// resume the same partial-pivoting sequence (aca.hpp:76-94, aca.cpp:106-143).
+enum { PH_RUN = 0, PH_INIT = 1, PH_EXT = 2, PH_DONE = 3 };
+enum { ST_OK = 0, ST_OVERFLOW = 1 };
+enum { STOP_NONE = 0, STOP_INEQ = 1, STOP_EXH = 2, STOP_RANKCAP = 3,
+       STOP_STEPS = 4 };
+
+struct __align__(16) Item {
+  int m, n, row0, col0;
+  int comp, cap, k, kcur;
+  int phase, steps_left, nconsumed, last_stop;
+  int status, block, pad0, pad1;
+  long long u_off, v_off;   // doubles; U is m x cap, V is n x cap, column-major
+  long long z_off, p_off;   // consumed-mask bytes; pivot (int2) slots
+  double frob_sq;
+  long long entries;        // kernel entries evaluated
+  long long steps;          // cross attempts (incl. vanishing rows)
+  long long pad2;
+};
+static_assert(sizeof(Item) == 128, "Item layout");
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// first-max arg-max: larger value wins, ties go to the smaller index
+__device__ __forceinline__ void warp_argmax(double& val, int& idx, double& aux) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, val, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    const double a2 = __shfl_xor_sync(0xffffffffu, aux, o);
+    if (v2 > val || (v2 == val && i2 >= 0 && (idx < 0 || i2 < idx))) {
+      val = v2;
+      idx = i2;
+      aux = a2;
+    }
+  }
+}
+__device__ __forceinline__ int warp_min_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One ACA step of aca_step (aca.cpp:41-102) executed by one warp.
+// sf < 0 disables the accuracy test (extension mode).  The candidate row
+// residual is built in V(:,k) and the column residual in U(:,k); both are
+// only committed (k += 1) when the step is accepted.
+__device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
+                             double* __restrict__ V, int2* __restrict__ piv,
+                             uint8_t* __restrict__ Z, double sf, int lane) {
+  const int m = s.m, n = s.n, k = s.k;
+  const int comp = s.comp;
+  for (;;) {
+    if (s.nconsumed == m) return STOP_EXH;
+    s.steps++;
+    // --- row pivot: first unconsumed row (k = 0) or first max |U(r,k-1)|
+    int i;
+    if (k == 0) {
+      int first = 0x7fffffff;
+      for (int r = lane; r < m; r += 32)
+        if (!Z[r]) {
+          first = r;
+          break;
+        }
+      i = warp_min_int(first);
+    } else {
+      const double* ul = U + (long long)(k - 1) * m;
+      double best = -1.0, aux = 0.0;
+      int bi = -1;
+      for (int r = lane; r < m; r += 32) {
+        if (Z[r]) continue;
+        const double mag = fabs(ul[r]);
+        if (mag > best) {
+          best = mag;
+          bi = r;
+        }
+      }
+      warp_argmax(best, bi, aux);
+      i = bi;
+    }
+    // --- row of the residual: v = A(i,:) - sum_l U(i,l) V(:,l)
+    double* vk = V + (long long)k * n;
+    double rs = 0.0, pm = -1.0, pv = 0.0;
+    int pj = -1;
+    for (int c = lane; c < n; c += 32) {
+      double val = entry1(g, s.row0 + i, s.col0 + c, comp);
+      rs = fmax(rs, fabs(val));
+      for (int l = 0; l < k; ++l)
+        val = fma(-U[(long long)l * m + i], V[(long long)l * n + c], val);
+      vk[c] = val;
+      if (fabs(val) > pm) {
+        pm = fabs(val);
+        pj = c;
+        pv = val;
+      }
+    }
+    s.entries += n;
+    const double row_scale = warp_max(rs);
+    warp_argmax(pm, pj, pv);
+    if (lane == 0) Z[i] = 1;
+    s.nconsumed++;
+    __syncwarp();
+    if (pm <= 1e-14 * row_scale || row_scale == 0.0) continue;  // vanishing
+    const int j = pj;
+    double vv = 0.0;
+    for (int c = lane; c < n; c += 32) {
+      const double t = vk[c] / pv;
+      vk[c] = t;
+      vv = fma(t, t, vv);
+    }
+    // --- column of the residual: u = A(:,j) - sum_l V(j,l) U(:,l)
+    double* uk = U + (long long)k * m;
+    double uu = 0.0;
+    for (int r = lane; r < m; r += 32) {
+      double val = entry1(g, s.row0 + r, s.col0 + j, comp);
+      for (int l = 0; l < k; ++l)
+        val = fma(-V[(long long)l * n + j], U[(long long)l * m + r], val);
+      uk[r] = val;
+      uu = fma(val, val, uu);
+    }
+    s.entries += m;
+    uu = warp_sum(uu);
+    vv = warp_sum(vv);
+    if (sf >= 0.0 && sqrt(uu) * sqrt(vv) <= sf * sqrt(fmax(s.frob_sq, 0.0))) {
+      __syncwarp();
+      return STOP_INEQ;
+    }
+    // ||S_k||^2 = ||S_{k-1}||^2 + 2 sum_l (u.u_l)(v.v_l) + ||u||^2 ||v||^2
+    double cross = 0.0;
+    for (int l = 0; l < k; ++l) {
+      double du = 0.0, dv = 0.0;
+      const double* ul = U + (long long)l * m;
+      const double* vl = V + (long long)l * n;
+      for (int r = lane; r < m; r += 32) du = fma(uk[r], ul[r], du);
+      for (int c = lane; c < n; c += 32) dv = fma(vk[c], vl[c], dv);
+      du = warp_sum(du);
+      dv = warp_sum(dv);
+      cross = fma(du, dv, cross);
+    }
+    s.frob_sq += 2.0 * cross + uu * vv;
+    if (lane == 0) piv[k] = make_int2(i, j);
+    s.k = k + 1;
+    __syncwarp();
+    return STOP_NONE;
+  }
+}
+
+// Runs one item's state machine until done or out of column capacity:
+//   PH_RUN  aca_run to the stopping rule (aca.cpp:106-124)
+//   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
+//   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
+__device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
+                              double* __restrict__ arena, int2* __restrict__ pivots,
+                              uint8_t* __restrict__ cons, double sf_run,
+                              long long max_rank, int lookahead,
+                              int* __restrict__ overflow, int lane) {
+  Item s = items[idx];
+  double* U = arena + s.u_off;
+  double* V = arena + s.v_off;
+  int2* piv = pivots + s.p_off;
+  uint8_t* Z = cons + s.z_off;
+  const long long capr_ll = min(max_rank, (long long)min(s.m, s.n));
+  const int capr = (int)capr_ll;
+  s.status = ST_OK;
+  while (s.phase != PH_DONE) {
+    if (s.phase == PH_RUN) {
+      bool stopped = false;
+      while (s.k < capr) {
+        if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
+        const int st = aca_step_warp(g, s, U, V, piv, Z, sf_run, lane);
+        if (st != STOP_NONE) {
+          s.last_stop = st;
+          stopped = true;
+          break;
+        }
+      }
+      if (!stopped) s.last_stop = (s.nconsumed == s.m) ? STOP_EXH : STOP_RANKCAP;
+      s.kcur = s.k;
+      s.phase = PH_EXT;
+      s.steps_left = lookahead;
+    } else {  // PH_INIT or PH_EXT
+      bool stopped = false;
+      while (s.steps_left > 0 && s.k < capr) {
+        if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
+        const int st = aca_step_warp(g, s, U, V, piv, Z, -1.0, lane);
+        if (st != STOP_NONE) {
+          s.last_stop = st;
+          stopped = true;
+          break;
+        }
+        s.steps_left--;
+      }
+      if (!stopped)
+        s.last_stop = (s.nconsumed == s.m)               ? STOP_EXH
+                      : (s.k >= capr && s.steps_left > 0) ? STOP_RANKCAP
+                                                          : STOP_STEPS;
+      if (s.phase == PH_INIT) {
+        s.kcur = s.k;
+        s.phase = PH_EXT;
+        s.steps_left = lookahead;
+      } else {
+        s.phase = PH_DONE;
+        s.steps_left = 0;
+      }
+    }
+  }
+save:
+  __syncwarp();
+  if (lane == 0) {
+    items[idx] = s;
+    if (s.status == ST_OVERFLOW) atomicAdd(overflow, 1);
+  }
+}
+
+// warps pull items from `list` (largest first) through a global counter
+__global__ void __launch_bounds__(256)
+aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
+           int nlist, int* __restrict__ counter, double* __restrict__ arena,
+           int2* __restrict__ pivots, uint8_t* __restrict__ cons, double sf_run,
+           long long max_rank, int lookahead, int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(counter, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= nlist) return;
+    aca_item_warp(g, items, list[t], arena, pivots, cons, sf_run, max_rank,
+                  lookahead, overflow, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// near-field fill: one CTA per non-admissible block, all NC components of a
+// pair computed together (they share r and 1/r); layout per block
+// [comp][n][m] (column-major per component, like HBlock::dense)
+struct DenseBlock {
+  int m, n, row0, col0;
+  long long off;  // doubles into the dense arena
+};
+
+template <int NC>
+__global__ void __launch_bounds__(256)
+nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
+                 double* __restrict__ dense) {
+  for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
+    const DenseBlock b = blocks[bi];
+    const int mn = b.m * b.n;
+    double* D = dense + b.off;
+    for (int p = threadIdx.x; p < mn; p += blockDim.x) {
+      const int i = p % b.m, j = p / b.m;
+      if (NC == 6) {
+        double e[6];
+        if (g.kind == KIND_KELVIN) {
+          kelvin_entry6(g, b.row0 + i, b.col0 + j, e);
+        } else {
+          const double v = entry1(g, b.row0 + i, b.col0 + j, 0);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) e[c] = v;
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) D[(long long)c * mn + p] = e[c];
+      } else {
+        D[p] = entry1(g, b.row0 + i, b.col0 + j, 0);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// H-matvec.  x is gathered into internal order xi[(p*NOUT + r)*nrhs + q];
+// every owned block writes a partial ypart[(prow + i)*NOUT*nrhs + r*nrhs + q]
+// for its rows; a per-leaf pass sums the partials of all blocks covering
+// the leaf in a fixed order (deterministic) and scatters to external order.
+struct MvBlock {
+  int m, n, row0, col0;
+  int dense, item0, pad0, pad1;
+  long long dense_off;
+  long long prow;  // partial row offset
+};
+
+template <int NOUT>
+__global__ void gather_kernel(const double* __restrict__ x, double* __restrict__ xi,
+                              const int* __restrict__ cperm, int ncols, int nrhs) {
+  const long long total = (long long)ncols * NOUT * nrhs;
+  const long long ndof = (long long)ncols * NOUT;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(t % nrhs);
+    const long long pr = t / nrhs;
+    const int r = (int)(pr % NOUT);
+    const int p = (int)(pr / NOUT);
+    xi[t] = x[q * ndof + (long long)r * ncols + cperm[p]];
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256)
+hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ order,
+                  int nblocks, const Item* __restrict__ items,
+                  const double* __restrict__ arena,
+                  const double* __restrict__ dense, const double* __restrict__ xi,
+                  double* __restrict__ ypart, int nrhs, int mode) {
+  constexpr int NOUT = NC == 6 ? 3 : 1;
+  extern __shared__ double zsm[];  // [2][kmax][nrhs]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int oi = blockIdx.x; oi < nblocks; oi += gridDim.x) {
+    const MvBlock b = blocks[order[oi]];
+    double* yp = ypart + b.prow * NOUT * nrhs;
+    if (b.dense) {
+      const long long mn = (long long)b.m * b.n;
+      for (int i = threadIdx.x; i < b.m; i += blockDim.x) {
+        for (int q = 0; q < nrhs; ++q) {
+          double acc[NOUT];
+#pragma unroll
+          for (int r = 0; r < NOUT; ++r) acc[r] = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const int rr = NC == 6 ? c_comp_r[c] : 0;
+            const int cc = NC == 6 ? c_comp_c[c] : 0;
+            const double* D = dense + b.dense_off + c * mn;
+            double s1 = 0.0, s2 = 0.0;
+            for (int j = 0; j < b.n; ++j) {
+              const double d = D[(long long)j * b.m + i];
+              const double* xj = xi + ((long long)(b.col0 + j) * NOUT) * nrhs + q;
+              s1 = fma(d, xj[cc * nrhs], s1);
+              if (rr != cc) s2 = fma(d, xj[rr * nrhs], s2);
+            }
+            acc[rr] += s1;
+            if (rr != cc) acc[cc] += s2;
+          }
+#pragma unroll
+          for (int r = 0; r < NOUT; ++r) yp[((long long)i * NOUT + r) * nrhs + q] = acc[r];
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    // low rank: per component z = V^T x_c (and w = V^T x_r), then U z
+    for (int c = 0; c < NC; ++c) {
+      const Item it = items[b.item0 + c];
+      const int k = mode ? it.k : it.kcur;
+      const int rr = NC == 6 ? c_comp_r[c] : 0;
+      const int cc = NC == 6 ? c_comp_c[c] : 0;
+      const bool two = rr != cc;
+      const double* V = arena + it.v_off;
+      const double* U = arena + it.u_off;
+      for (int l = warp; l < k; l += nwarps) {
+        const double* vl = V + (long long)l * b.n;
+        for (int q = 0; q < nrhs; ++q) {
+          double s1 = 0.0, s2 = 0.0;
+          for (int j = lane; j < b.n; j += 32) {
+            const double v = vl[j];
+            const double* xj = xi + ((long long)(b.col0 + j) * NOUT) * nrhs + q;
+            s1 = fma(v, xj[cc * nrhs], s1);
+            if (two) s2 = fma(v, xj[rr * nrhs], s2);
+          }
+          s1 = warp_sum(s1);
+          if (two) s2 = warp_sum(s2);
+          if (lane == 0) {
+            zsm[l * nrhs + q] = s1;
+            zsm[(k + l) * nrhs + q] = s2;
+          }
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < b.m; i += blockDim.x) {
+        for (int q = 0; q < nrhs; ++q) {
+          double s1 = 0.0, s2 = 0.0;
+          for (int l = 0; l < k; ++l) {
+            const double u = U[(long long)l * b.m + i];
+            s1 = fma(u, zsm[l * nrhs + q], s1);
+            if (two) s2 = fma(u, zsm[(k + l) * nrhs + q], s2);
+          }
+          double* y = yp + (long long)i * NOUT * nrhs + q;
+          if (c == 0) {
+#pragma unroll
+            for (int r = 0; r < NOUT; ++r) y[r * nrhs] = 0.0;
+          }
+          y[rr * nrhs] += s1;
+          if (two) y[cc * nrhs] += s2;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// per leaf: y(p) = sum over covering blocks (fixed order) of the partials
+template <int NOUT>
+__global__ void hmv_reduce_kernel(const int* __restrict__ leaf_begin,
+                                  const int* __restrict__ leaf_end,
+                                  const int* __restrict__ leaf_ptr,
+                                  const long long* __restrict__ leaf_prow,
+                                  int nleaves, const double* __restrict__ ypart,
+                                  const int* __restrict__ rperm, int nrows,
+                                  double* __restrict__ y, int nrhs) {
+  const long long ndof = (long long)nrows * NOUT;
+  for (int L = blockIdx.x; L < nleaves; L += gridDim.x) {
+    const int b0 = leaf_begin[L], b1 = leaf_end[L];
+    const int e0 = leaf_ptr[L], e1 = leaf_ptr[L + 1];
+    const int cnt = (b1 - b0) * NOUT * nrhs;
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int q = t % nrhs;
+      const int r = (t / nrhs) % NOUT;
+      const int i = t / (nrhs * NOUT);
+      double s = 0.0;
+      for (int e = e0; e < e1; ++e)
+        s += ypart[((leaf_prow[e] + i) * NOUT + r) * nrhs + q];
+      y[q * ndof + (long long)r * nrows + rperm[b0 + i]] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// look-ahead tail products for AMVM (apply_range(k_cur, k_look), aca.cpp:7-11
+// as used by gamma_contributions, amvm.cpp:72-122): one warp per item
+struct TailTerm {
+  int item, nocc;
+  long long off;
+};
+
+template <int NOUT>
+__global__ void tail_kernel(const TailTerm* __restrict__ terms, int nterms,
+                            const Item* __restrict__ items,
+                            const double* __restrict__ arena,
+                            const double* __restrict__ xi, double* __restrict__ out,
+                            int is_grid) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < nterms; t += nw) {
+    const TailTerm tt = terms[t];
+    const Item it = items[tt.item];
+    const int rr = is_grid ? c_comp_r[it.comp] : 0;
+    const int cc = is_grid ? c_comp_c[it.comp] : 0;
+    const double* U = arena + it.u_off;
+    const double* V = arena + it.v_off;
+    double* o = out + tt.off;
+    for (int i = lane; i < tt.nocc * it.m; i += 32) o[i] = 0.0;
+    __syncwarp();
+    for (int l = it.kcur; l < it.k; ++l) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int j = lane; j < it.n; j += 32) {
+        const double v = V[(long long)l * it.n + j];
+        const double* xj = xi + (long long)(it.col0 + j) * NOUT;
+        s1 = fma(v, xj[cc], s1);
+        if (tt.nocc == 2) s2 = fma(v, xj[rr], s2);
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      for (int i = lane; i < it.m; i += 32) {
+        const double u = U[(long long)l * it.m + i];
+        o[i] = fma(u, s1, o[i]);
+        if (tt.nocc == 2) o[it.m + i] = fma(u, s2, o[it.m + i]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small state kernels
+__global__ void promote_kernel(Item* items, const int* idx, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) items[idx[t]].kcur = items[idx[t]].k;
+}
+
+__global__ void prep_extend_kernel(Item* items, const int* idx, int n, int steps) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    Item& it = items[idx[t]];
+    it.phase = PH_EXT;
+    it.steps_left = steps;
+  }
+}
+
+// relocate item factors into new storage: copies U (m x K), V (n x K) prefix
+// columns and K pivots to the offsets in `dst` (same item order)
+__global__ void relocate_kernel(Item* __restrict__ items, const int* __restrict__ idx,
+                                const long long* __restrict__ new_u,
+                                const long long* __restrict__ new_v,
+                                const long long* __restrict__ new_p,
+                                const int* __restrict__ new_cap, int n,
+                                const double* __restrict__ src_arena,
+                                double* __restrict__ dst_arena,
+                                const int2* __restrict__ src_piv,
+                                int2* __restrict__ dst_piv) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < n; t += nw) {
+    Item it = items[idx[t]];
+    const long long nu = (long long)it.m * it.k, nv = (long long)it.n * it.k;
+    const double* su = src_arena + it.u_off;
+    const double* sv = src_arena + it.v_off;
+    double* du = dst_arena + new_u[t];
+    double* dv = dst_arena + new_v[t];
+    for (long long e = lane; e < nu; e += 32) du[e] = su[e];
+    for (long long e = lane; e < nv; e += 32) dv[e] = sv[e];
+    for (int e = lane; e < it.k; e += 32) dst_piv[new_p[t] + e] = src_piv[it.p_off + e];
+    __syncwarp();
+    if (lane == 0) {
+      it.u_off = new_u[t];
+      it.v_off = new_v[t];
+      it.p_off = new_p[t];
+      it.cap = new_cap[t];
+      items[idx[t]] = it;
+    }
+  }
+}
+
+}  // namespace hmgpu

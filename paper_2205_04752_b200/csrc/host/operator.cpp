@@ -1,0 +1,490 @@
+#include "operator.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+
+#include "errors.hpp"
+#include "hmgpu.h"
+
+namespace hmb {
+
+namespace {
+
+const int kCompR[6] = {0, 0, 0, 1, 1, 2};
+const int kCompC[6] = {0, 1, 2, 1, 2, 2};
+
+int check_status(hmgpu_ctx* ctx, int st, const char* what) {
+  if (st == HMGPU_OK) return st;
+  const std::string msg =
+      std::string(what) + ": " + (ctx ? hmgpu_last_error(ctx) : "no context");
+  if (st == HMGPU_ERR_DIMENSION) throw DimensionError(msg);
+  if (st == HMGPU_ERR_INVALID) throw Error(msg);
+  throw DeviceError(st, msg);
+}
+
+std::vector<int> nodes4(const ClusterTree& t) {
+  std::vector<int> out(4 * t.nodes.size());
+  for (std::size_t i = 0; i < t.nodes.size(); ++i) {
+    out[4 * i] = t.nodes[i].begin;
+    out[4 * i + 1] = t.nodes[i].end;
+    out[4 * i + 2] = t.nodes[i].child[0];
+    out[4 * i + 3] = t.nodes[i].child[1];
+  }
+  return out;
+}
+
+}  // namespace
+
+void HOperator::check(int status, const char* what) const {
+  check_status(ctx_, status, what);
+}
+
+HOperator::~HOperator() {
+  if (ctx_) hmgpu_destroy(ctx_);
+}
+
+long long HOperator::rows() const {
+  return static_cast<long long>(n_rows_) * (ncomp_ == 6 ? 3 : 1);
+}
+long long HOperator::cols() const {
+  return static_cast<long long>(n_cols_) * (ncomp_ == 6 ? 3 : 1);
+}
+
+// Block-row shard: the first tree level with >= count nodes (plus shallower
+// leaves) is split into `count` contiguous runs; every block's row cluster
+// must fall inside one run (true for the eta = 1 partitions, whose blocks
+// start below the top levels).
+void HOperator::init_partition(Real eta, Shard shard) {
+  part_ = build_block_partition(*rows_, col_tree(), eta);
+  if (shard.count < 1 || shard.rank < 0 || shard.rank >= shard.count)
+    throw ConfigError("bad shard (rank, count)");
+  row_begin_ = 0;
+  row_end_ = n_rows_;
+  if (shard.count == 1) return;
+  const ClusterTree& t = *rows_;
+  int level = 0;
+  std::vector<int> frontier;
+  for (;; ++level) {
+    frontier.clear();
+    for (std::size_t i = 0; i < t.nodes.size(); ++i) {
+      const ClusterNode& nd = t.nodes[i];
+      if (nd.level == level || (nd.is_leaf() && nd.level < level))
+        frontier.push_back(static_cast<int>(i));
+    }
+    if (static_cast<int>(frontier.size()) >= shard.count || level > t.depth) break;
+  }
+  if (static_cast<int>(frontier.size()) < shard.count)
+    throw ConfigError("more shards than row clusters");
+  std::sort(frontier.begin(), frontier.end(), [&](int a, int b) {
+    return t.nodes[a].begin < t.nodes[b].begin;
+  });
+  const int nf = static_cast<int>(frontier.size());
+  std::vector<int> owner(n_rows_, 0);
+  for (int f = 0; f < nf; ++f) {
+    const int r = static_cast<int>(static_cast<long long>(f) * shard.count / nf);
+    const ClusterNode& nd = t.nodes[frontier[f]];
+    for (int p = nd.begin; p < nd.end; ++p) owner[p] = r;
+    if (r == shard.rank) {
+      if (row_end_ == n_rows_ && row_begin_ == 0) row_begin_ = nd.begin;
+      row_end_ = nd.end;
+    }
+  }
+  // first frontier node of this rank gives the begin (reset above)
+  for (int f = 0; f < nf; ++f)
+    if (static_cast<int>(static_cast<long long>(f) * shard.count / nf) == shard.rank) {
+      row_begin_ = t.nodes[frontier[f]].begin;
+      break;
+    }
+  for (const BlockInfo& b : part_.blocks) {
+    const ClusterNode& rn = t.nodes[b.row_node];
+    if (owner[rn.begin] != owner[rn.end - 1])
+      throw ConfigError("a partition block spans two shards; use fewer GPUs");
+  }
+}
+
+std::unique_ptr<HOperator> HOperator::kelvin(const Mesh& mesh, Real E, Real nu,
+                                             int b_min, Real eta, int device,
+                                             Shard shard, QuadratureConfig qc) {
+  if (mesh.centroids.size() != mesh.triangles.size())
+    throw MeshError("mesh geometry caches missing (call finish())");
+  if (E <= 0.0) throw Error("lame_constants: E must be positive");
+  if (nu <= 0.0 || nu >= 0.5) throw Error("lame_constants: nu must lie in (0, 1/2)");
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = Kelvin;
+  op->ncomp_ = 6;
+  op->n_rows_ = op->n_cols_ = mesh.nt();
+  op->rows_ = std::make_unique<ClusterTree>(
+      build_cluster_tree(triangle_supports(mesh), b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;  // host-only: tree and partition
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  std::vector<double> verts(3 * mesh.nv()), cen(3 * mesh.nt());
+  std::vector<int> tris(3 * mesh.nt());
+  for (int v = 0; v < mesh.nv(); ++v)
+    for (int d = 0; d < 3; ++d) verts[3 * v + d] = mesh.vertices[v][d];
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int d = 0; d < 3; ++d) {
+      tris[3 * t + d] = mesh.triangles[t][d];
+      cen[3 * t + d] = mesh.centroids[t][d];
+    }
+  op->check(hmgpu_set_kelvin_geometry(op->ctx_, mesh.nv(), verts.data(), mesh.nt(),
+                                      tris.data(), cen.data(), mesh.areas.data(),
+                                      mesh.diam.data(), E, nu),
+            "hmgpu_set_kelvin_geometry");
+  for (int tier = 0; tier < 3; ++tier) {
+    const TriangleRule r = gauss_rule(qc.tier_order(tier));
+    op->check(hmgpu_set_rule(op->ctx_, tier, static_cast<int>(r.w.size()), r.a.data(),
+                             r.b.data(), r.w.data()),
+              "hmgpu_set_rule");
+  }
+  op->check(hmgpu_set_tier_ratios(op->ctx_, qc.far_ratio, qc.mid_ratio),
+            "hmgpu_set_tier_ratios");
+  return op;
+}
+
+std::unique_ptr<HOperator> HOperator::newton(const std::vector<V3>& pts,
+                                             const std::vector<Box>* boxes,
+                                             Real diag, int b_min, Real eta,
+                                             int device, Shard shard) {
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = Newton;
+  op->ncomp_ = 1;
+  op->n_rows_ = op->n_cols_ = static_cast<int>(pts.size());
+  std::vector<Box> b;
+  if (boxes) {
+    b = *boxes;
+  } else {
+    b.resize(pts.size());
+    for (std::size_t i = 0; i < pts.size(); ++i) b[i].absorb(pts[i]);
+  }
+  op->rows_ = std::make_unique<ClusterTree>(build_cluster_tree(b, b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  std::vector<double> flat(3 * pts.size());
+  for (std::size_t i = 0; i < pts.size(); ++i)
+    for (int d = 0; d < 3; ++d) flat[3 * i + d] = pts[i][d];
+  op->check(hmgpu_set_points(op->ctx_, static_cast<int>(pts.size()), flat.data(), diag),
+            "hmgpu_set_points");
+  return op;
+}
+
+std::unique_ptr<HOperator> HOperator::dense(int m, int n, const double* a,
+                                            const std::vector<V3>& row_pts,
+                                            const std::vector<V3>& col_pts,
+                                            int b_min, Real eta, int device,
+                                            Shard shard) {
+  if (static_cast<int>(row_pts.size()) != m || static_cast<int>(col_pts.size()) != n)
+    throw DimensionError("dense operator: point counts do not match the matrix");
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = Dense;
+  op->ncomp_ = 1;
+  op->n_rows_ = m;
+  op->n_cols_ = n;
+  std::vector<Box> rb(m), cb(n);
+  for (int i = 0; i < m; ++i) rb[i].absorb(row_pts[i]);
+  for (int j = 0; j < n; ++j) cb[j].absorb(col_pts[j]);
+  op->rows_ = std::make_unique<ClusterTree>(build_cluster_tree(rb, b_min));
+  op->cols_ = std::make_unique<ClusterTree>(build_cluster_tree(cb, b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  op->check(hmgpu_set_dense_matrix(op->ctx_, m, n, a), "hmgpu_set_dense_matrix");
+  return op;
+}
+
+AssemblyStats HOperator::assemble(const AssemblyConfig& cfg) {
+  if (!ctx_) throw DeviceError(HMGPU_ERR_NODEVICE, "assemble: operator has no device");
+  const ClusterTree& ct = col_tree();
+  const std::vector<int> rn = nodes4(*rows_), cn = nodes4(ct);
+  std::vector<int> bl(4 * part_.blocks.size());
+  for (std::size_t b = 0; b < part_.blocks.size(); ++b) {
+    bl[4 * b] = part_.blocks[b].row_node;
+    bl[4 * b + 1] = part_.blocks[b].col_node;
+    bl[4 * b + 2] = part_.blocks[b].admissible ? 1 : 0;
+    bl[4 * b + 3] = part_.blocks[b].level;
+  }
+  check(hmgpu_set_partition(ctx_, n_rows_, rows_->perm.data(),
+                            static_cast<int>(rows_->nodes.size()), rn.data(), n_cols_,
+                            ct.perm.data(), static_cast<int>(ct.nodes.size()), cn.data(),
+                            static_cast<int>(part_.blocks.size()), bl.data(),
+                            row_begin_, row_end_),
+        "hmgpu_set_partition");
+  hmgpu_assembly_stats s{};
+  check(hmgpu_assemble(ctx_, cfg.eps, cfg.beta, cfg.initial_rank, cfg.lookahead,
+                       cfg.max_rank, &s),
+        "hmgpu_assemble");
+  cfg_ = cfg;
+  assembled_ = true;
+  AssemblyStats out;
+  out.aca_entries = s.aca_entries;
+  out.dense_entries = s.dense_entries;
+  out.aca_steps = s.aca_steps;
+  out.pivots = s.pivots;
+  out.ms_total = s.ms_total;
+  out.ms_nearfield = s.ms_nearfield;
+  out.ms_aca = s.ms_aca;
+  out.relaunches = s.aca_relaunches;
+  return out;
+}
+
+void HOperator::matvec(const double* x, double* y, int nrhs, Mode mode,
+                       bool device_ptrs) const {
+  if (!assembled_) throw Error("matvec: operator not assembled");
+  check(hmgpu_matvec(ctx_, x, y, nrhs, static_cast<int>(mode),
+                     device_ptrs ? HMGPU_PTR_DEVICE : HMGPU_PTR_HOST),
+        "hmgpu_matvec");
+}
+
+std::vector<double> HOperator::matvec(const std::vector<double>& x, Mode mode) const {
+  if (static_cast<long long>(x.size()) != cols())
+    throw DimensionError("HMatrix::matvec: size");
+  std::vector<double> y(rows());
+  matvec(x.data(), y.data(), 1, mode);
+  return y;
+}
+
+void HOperator::promote(const std::vector<std::pair<int, int>>& cb) {
+  std::vector<int> flat;
+  for (auto& p : cb) {
+    flat.push_back(p.first);
+    flat.push_back(p.second);
+  }
+  check(hmgpu_promote(ctx_, static_cast<int>(cb.size()), flat.data()), "hmgpu_promote");
+}
+
+void HOperator::extend_lookahead(const std::vector<std::pair<int, int>>& cb, int steps) {
+  std::vector<int> flat;
+  for (auto& p : cb) {
+    flat.push_back(p.first);
+    flat.push_back(p.second);
+  }
+  check(hmgpu_extend(ctx_, static_cast<int>(cb.size()), flat.data(), steps),
+        "hmgpu_extend");
+}
+
+void HOperator::ranks(std::vector<int>& k_cur, std::vector<int>& k_look,
+                      std::vector<int>* consumed, std::vector<int>* last_stop) const {
+  const std::size_t n = static_cast<std::size_t>(ncomp_) * part_.blocks.size();
+  k_cur.resize(n);
+  k_look.resize(n);
+  if (consumed) consumed->resize(n);
+  if (last_stop) last_stop->resize(n);
+  check(hmgpu_ranks(ctx_, k_cur.data(), k_look.data(),
+                    consumed ? consumed->data() : nullptr,
+                    last_stop ? last_stop->data() : nullptr),
+        "hmgpu_ranks");
+}
+
+long long HOperator::total_pivots() const {
+  std::vector<int> kc, kl;
+  ranks(kc, kl);
+  long long p = 0;
+  for (int k : kl) p += k > 0 ? k : 0;
+  return p;
+}
+
+double HOperator::storage_mb_current() const {
+  hmgpu_storage_info s{};
+  check(hmgpu_storage(ctx_, &s), "hmgpu_storage");
+  return s.mb_current;
+}
+double HOperator::storage_mb_tail() const {
+  hmgpu_storage_info s{};
+  check(hmgpu_storage(ctx_, &s), "hmgpu_storage");
+  return s.mb_tail;
+}
+long long HOperator::matvec_bytes() const {
+  hmgpu_storage_info s{};
+  check(hmgpu_storage(ctx_, &s), "hmgpu_storage");
+  return s.matvec_bytes;
+}
+
+// ---------------------------------------------------------------------------
+// gamma_contributions (amvm.cpp:46-125): the device returns the tail
+// products of every (comp, block) with a look-ahead tail, grouped by
+// component (= by H-matrix in first-appearance order); the host turns them
+// into sparse terms over the operator's output rows exactly as the
+// occurrence scatter does (grid cells carry an embedding prefix, so zero
+// values are skipped there, amvm.cpp:112-116).
+GammaContributions gamma_contributions(const HOperator& op, const double* x) {
+  if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
+    throw ConfigError("gamma_contributions: sharded operators are not supported");
+  GammaContributions g;
+  const long long M = op.rows();
+  const int N = op.row_tree().size();
+  g.difference.assign(M, 0.0);
+  int n_terms = 0;
+  long long n_vals = 0;
+  check_status(op.gpu(), hmgpu_tail_terms(op.gpu(), x, &n_terms, &n_vals, nullptr, nullptr),
+               "hmgpu_tail_terms");
+  std::vector<long long> meta(4LL * n_terms);
+  std::vector<double> vals(n_vals);
+  if (n_terms > 0)
+    check_status(op.gpu(),
+                 hmgpu_tail_terms(op.gpu(), x, &n_terms, &n_vals, meta.data(), vals.data()),
+                 "hmgpu_tail_terms");
+  const bool grid = op.ncomp() == 6;
+  const auto& rperm = op.row_tree().perm;
+  std::vector<std::pair<long long, double>> buf;
+  for (int t = 0; t < n_terms; ++t) {
+    const int comp = static_cast<int>(meta[4 * t]);
+    const int b = static_cast<int>(meta[4 * t + 1]);
+    const int nocc = static_cast<int>(meta[4 * t + 2]);
+    const long long off = meta[4 * t + 3];
+    const ClusterNode& rn = op.row_tree().nodes[op.partition().blocks[b].row_node];
+    const int m = rn.size();
+    buf.clear();
+    for (int o = 0; o < nocc; ++o) {
+      const int rb = grid ? (o == 0 ? kCompR[comp] : kCompC[comp]) : 0;
+      for (int i = 0; i < m; ++i) {
+        const double v = vals[off + static_cast<long long>(o) * m + i];
+        if (grid && v == 0.0) continue;
+        buf.emplace_back(static_cast<long long>(rb) * N + rperm[rn.begin + i], v);
+      }
+    }
+    if (buf.empty()) continue;
+    std::sort(buf.begin(), buf.end(),
+              [](const auto& a, const auto& b) { return a.first < b.first; });
+    BlockTerm term;
+    term.comp = comp;
+    term.block = b;
+    term.idx.reserve(buf.size());
+    term.val.reserve(buf.size());
+    for (const auto& e : buf) {
+      term.idx.push_back(e.first);
+      term.val.push_back(e.second);
+      g.difference[e.first] += e.second;
+      term.norm_sq += e.second * e.second;
+    }
+    g.terms.push_back(std::move(term));
+  }
+  double s = 0.0;
+  for (double v : g.difference) s += v * v;
+  g.gamma = std::sqrt(s);
+  return g;
+}
+
+// row-sorted greedy marking (amvm.cpp:131-184)
+std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
+                             long long m_rows, long long n_cols, Real* gamma_pk_out) {
+  std::vector<int> marked;
+  if (g.gamma <= 0.0) {
+    if (gamma_pk_out) *gamma_pk_out = 0.0;
+    return marked;
+  }
+  const Real threshold = (1.0 - theta) * g.gamma /
+                         std::sqrt(static_cast<Real>(c_sp) * static_cast<Real>(m_rows) *
+                                   static_cast<Real>(n_cols));
+  const Real target = (1.0 - theta) * g.gamma;
+  // CSR of (row -> terms reaching the threshold there), terms in order
+  std::vector<int> cnt(m_rows + 1, 0);
+  for (const BlockTerm& t : g.terms)
+    for (std::size_t i = 0; i < t.idx.size(); ++i)
+      if (std::abs(t.val[i]) >= threshold) ++cnt[t.idx[i] + 1];
+  for (long long r = 0; r < m_rows; ++r) cnt[r + 1] += cnt[r];
+  std::vector<int> fill(cnt.begin(), cnt.end() - 1), lists(cnt[m_rows]);
+  for (std::size_t t = 0; t < g.terms.size(); ++t)
+    for (std::size_t i = 0; i < g.terms[t].idx.size(); ++i)
+      if (std::abs(g.terms[t].val[i]) >= threshold)
+        lists[fill[g.terms[t].idx[i]]++] = static_cast<int>(t);
+  std::vector<long long> order(m_rows);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](long long a, long long b) {
+    return std::abs(g.difference[a]) > std::abs(g.difference[b]);
+  });
+  std::vector<Real> residual = g.difference;
+  Real res_sq = 0.0;
+  for (Real v : residual) res_sq += v * v;
+  std::vector<char> in_set(g.terms.size(), 0);
+  const Real target_sq = target * target;
+  for (long long row : order) {
+    if (res_sq <= target_sq) break;
+    bool done = false;
+    for (int e = cnt[row]; e < cnt[row + 1]; ++e) {
+      const int t = lists[e];
+      if (in_set[t]) continue;
+      in_set[t] = 1;
+      marked.push_back(t);
+      const BlockTerm& term = g.terms[t];
+      Real dot = 0.0;
+      for (std::size_t i = 0; i < term.idx.size(); ++i)
+        dot += residual[term.idx[i]] * term.val[i];
+      res_sq += term.norm_sq - 2.0 * dot;
+      for (std::size_t i = 0; i < term.idx.size(); ++i)
+        residual[term.idx[i]] -= term.val[i];
+      if (res_sq <= target_sq) {
+        done = true;
+        break;
+      }
+    }
+    if (done) break;
+  }
+  Real s = 0.0;
+  for (Real v : residual) s += v * v;
+  if (gamma_pk_out) *gamma_pk_out = std::sqrt(s);
+  return marked;
+}
+
+// Algorithm 2 (amvm.cpp:199-268)
+std::vector<double> amvm_multiply(HOperator& op, const double* x,
+                                  const AmvmConfig& cfg, AmvmReport& report) {
+  if (cfg.theta <= 0.0 || cfg.theta >= 1.0)
+    throw Error("amvm_multiply: theta must lie in (0,1)");
+  if (cfg.eps_amvm <= 0.0) throw Error("amvm_multiply: eps_amvm must be positive");
+  using clk = std::chrono::steady_clock;
+  report = AmvmReport{};
+  report.c_sp = std::max(1, sparsity_constant(op.partition()));
+  const long long M = op.rows();
+  std::vector<double> b(M), b_hat_prev;
+  op.matvec(x, b.data(), 1, Mode::Current);
+  for (int k = 0;; ++k) {
+    const auto t0 = clk::now();
+    GammaContributions g = gamma_contributions(op, x);
+    if (!b_hat_prev.empty()) {
+      double s = 0.0;
+      for (long long i = 0; i < M; ++i) {
+        const double d = b[i] + g.difference[i] - b_hat_prev[i];
+        s += d * d;
+      }
+      report.iterations.back().e_hat = std::sqrt(s);
+    }
+    AmvmIteration it;
+    it.k = k;
+    it.gamma = g.gamma;
+    it.cumulative_pivots = op.total_pivots();
+    it.storage_mb = op.storage_mb_current();
+    if (g.gamma <= cfg.eps_amvm) {
+      it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+      report.iterations.push_back(it);
+      report.termination = "tolerance";
+      report.converged = true;
+      return b;
+    }
+    if (k >= cfg.max_iterations) {
+      it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+      report.iterations.push_back(it);
+      report.termination = "max_iterations";
+      report.converged = false;
+      return b;
+    }
+    Real gpk = 0.0;
+    const auto marked = mark_blocks(g, cfg.theta, report.c_sp, M, op.cols(), &gpk);
+    it.gamma_pk = gpk;
+    it.marked = static_cast<int>(marked.size());
+    b_hat_prev.resize(M);
+    for (long long i = 0; i < M; ++i) b_hat_prev[i] = b[i] + g.difference[i];
+    std::vector<std::pair<int, int>> cb;
+    cb.reserve(marked.size());
+    for (int t : marked) cb.emplace_back(g.terms[t].comp, g.terms[t].block);
+    op.promote(cb);
+    op.extend_lookahead(cb, cfg.lookahead_steps);
+    op.matvec(x, b.data(), 1, Mode::Current);
+    it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    report.iterations.push_back(it);
+  }
+}
+
+}  // namespace hmb
