@@ -59,6 +59,13 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
                  double* areas, double* normals, double* diam, int* dirichlet);
 void hmb_mesh_free(hmb_mesh* m);
 
+/* gauss_rule(order) tables as uploaded to the device (quadrature.cpp:55-95);
+ * a/b/w may be NULL to query npts */
+int hmb_gauss_rule(int order, int* npts, double* a, double* b, double* w);
+
+/* admissibility of boxes [lo(3), hi(3)]: min diam < eta * dist (cluster.cpp:21-24) */
+int hmb_admissible(const double* box_a6, const double* box_b6, double eta, int* out);
+
 /* ---- operators (device < 0: host-only, tree and partition) ---- */
 int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
                   int device, int shard_rank, int shard_count, hmb_op** out);

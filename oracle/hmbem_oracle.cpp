@@ -357,7 +357,39 @@ struct Kelvin {
   }
 
   // colloc_single: 2 area_j sum_q w_q S(p - y_q)_rc (kernels.cpp:176-187)
+  // with S(x)_rc = c [(3-4nu) delta_rc / |x| + x_r x_c / |x|^3]
+  // (kelvin_tensor, kernels.cpp:21-28).  Canonical evaluation order, shared
+  // bit for bit with the device kernels: the constant c is factored out of
+  // the quadrature sum, 1/|x| is one IEEE division of an IEEE square root,
+  // and every fused multiply-add is written explicitly (std::fma); Eigen's
+  // own association is not recoverable here, so this order
+  // is the parity contract.  Agrees with the literal kelvin_tensor form to
+  // rounding (tests/test_oracle_kats.py::test_canonical_entry_matches_literal).
   Real colloc_single(const Vec3& p, int r, int c, int tj) const {
+    const Rule& rule = rules[point_order(p, tj)];
+    const Vec3 y0 = mesh->corner(tj, 0), y1 = mesh->corner(tj, 1),
+               y2 = mesh->corner(tj, 2);
+    const Vec3 e1 = sub(y1, y0), e2 = sub(y2, y0);
+    Real acc_d = 0.0, acc_x = 0.0;
+    for (std::size_t q = 0; q < rule.w.size(); ++q) {
+      const Real a = rule.a[q], b = rule.b[q], w = rule.w[q];
+      const Real dx = p[0] - std::fma(b, e2[0], std::fma(a, e1[0], y0[0]));
+      const Real dy = p[1] - std::fma(b, e2[1], std::fma(a, e1[1], y0[1]));
+      const Real dz = p[2] - std::fma(b, e2[2], std::fma(a, e1[2], y0[2]));
+      const Real r2 = std::fma(dz, dz, std::fma(dy, dy, dx * dx));
+      const Real ri = 1.0 / std::sqrt(r2);
+      const Real wr = w * ri;
+      const Real d[3] = {dx, dy, dz};
+      acc_d = acc_d + wr;
+      acc_x = std::fma(wr * ri * ri, d[r] * d[c], acc_x);
+    }
+    const Real s = r == c ? std::fma(c34(), acc_d, acc_x) : acc_x;
+    return 2.0 * mesh->areas[tj] * cst() * s;
+  }
+
+  // the literal reference form (kelvin_tensor per point, one component
+  // kept) -- used only to check the canonical order above
+  Real colloc_single_literal(const Vec3& p, int r, int c, int tj) const {
     const Rule& rule = rules[point_order(p, tj)];
     const Vec3 y0 = mesh->corner(tj, 0), y1 = mesh->corner(tj, 1),
                y2 = mesh->corner(tj, 2);
@@ -373,6 +405,9 @@ struct Kelvin {
     }
     return 2.0 * mesh->areas[tj] * acc;
   }
+
+  Real cst() const { return (1.0 + mat.nu) / (8.0 * M_PI * mat.E * (1.0 - mat.nu)); }
+  Real c34() const { return 3.0 - 4.0 * mat.nu; }
 
   // BUILDER-DEFINED self term (reference undefined):
   // exact integral over triangle t of S(p - y) dA for p in the plane of t
@@ -712,6 +747,10 @@ struct Factor {
   const Real* Ucol(int l) const { return U.data() + static_cast<long>(l) * m; }
   const Real* Vcol(int l) const { return V.data() + static_cast<long>(l) * n; }
   // S x over pivot range [k_lo, k_hi): U_r (V_r^T x) (aca.cpp:7-11)
+  // tail products in the device order (z_l by warp_dot, y += U(:,l) z_l
+  // with fma), the parity contract of gamma_contributions
+  void apply_range_device_order(int k_lo, int k_hi, const Real* x, Real* y) const;
+
   void apply_range(int k_lo, int k_hi, const Real* x, Real* y_add,
                    Real coeff = 1.0) const {
     if (k_hi <= k_lo) return;
@@ -730,6 +769,19 @@ struct Factor {
   }
 };
 
+template <class A, class B>
+static Real warp_dot(long n, A a, B b);
+
+void Factor::apply_range_device_order(int k_lo, int k_hi, const Real* x,
+                                      Real* y) const {
+  for (int l = k_lo; l < k_hi; ++l) {
+    const Real* v = Vcol(l);
+    const Real* u = Ucol(l);
+    const Real z = warp_dot(n, [&](long j) { return v[j]; }, [&](long j) { return x[j]; });
+    for (long i = 0; i < m; ++i) y[i] = std::fma(u[i], z, y[i]);
+  }
+}
+
 static Factor empty_factor(long m, long n) {
   Factor f;
   f.m = m;
@@ -742,6 +794,22 @@ static Real vnorm(const std::vector<Real>& v) {
   Real s = 0.0;
   for (Real x : v) s += x * x;
   return std::sqrt(s);
+}
+
+// Sum of a_j * b_j in the device's warp order: 32 lane-strided partial sums
+// accumulated with fma, combined by an xor butterfly.  This is the parity
+// contract for every reduction inside the ACA (the reference's Eigen
+// reduction order is unpinned).
+template <class A, class B>
+static Real warp_dot(long n, A a, B b) {
+  Real p[32] = {0};
+  for (long j = 0; j < n; ++j) p[j & 31] = std::fma(a(j), b(j), p[j & 31]);
+  for (int o = 16; o > 0; o >>= 1) {
+    Real q[32];
+    for (int l = 0; l < 32; ++l) q[l] = p[l] + p[l ^ o];
+    std::copy(q, q + 32, p);
+  }
+  return p[0];
 }
 
 // one ACA step (aca.cpp:41-102); stop_factor < 0 disables the accuracy test
@@ -772,11 +840,9 @@ static int aca_step(Factor& f, const BlockView& blk, Real stop_factor) {
     blk.oracle->row(blk.row_ids[i], blk.col_ids, n, v.data());
     Real row_scale = 0.0;
     for (long c = 0; c < n; ++c) row_scale = std::max(row_scale, std::abs(v[c]));
-    for (int l = 0; l < f.rank(); ++l) {
-      const Real uil = f.Ucol(l)[i];
-      const Real* vl = f.Vcol(l);
-      for (long c = 0; c < n; ++c) v[c] -= uil * vl[c];
-    }
+    for (long c = 0; c < n; ++c)  // v -= U(i,l) V(:,l), l ascending
+      for (int l = 0; l < f.rank(); ++l)
+        v[c] = std::fma(-f.Ucol(l)[i], f.Vcol(l)[c], v[c]);
     f.consumed[i] = 1;
     ++f.num_consumed;
     int j = 0;
@@ -790,25 +856,23 @@ static int aca_step(Factor& f, const BlockView& blk, Real stop_factor) {
     const Real piv = v[j];
     for (long c = 0; c < n; ++c) v[c] /= piv;
     blk.oracle->col(blk.col_ids[j], blk.row_ids, m, u.data());
-    for (int l = 0; l < f.rank(); ++l) {
-      const Real vjl = f.Vcol(l)[j];
-      const Real* ul = f.Ucol(l);
-      for (long r = 0; r < m; ++r) u[r] -= vjl * ul[r];
-    }
-    if (stop_factor >= 0.0 && vnorm(u) * vnorm(v) <= stop_factor * f.frob())
+    for (long r = 0; r < m; ++r)  // u -= V(j,l) U(:,l), l ascending
+      for (int l = 0; l < f.rank(); ++l)
+        u[r] = std::fma(-f.Vcol(l)[j], f.Ucol(l)[r], u[r]);
+    const Real uu = warp_dot(m, [&](long r) { return u[r]; }, [&](long r) { return u[r]; });
+    const Real vv = warp_dot(n, [&](long c) { return v[c]; }, [&](long c) { return v[c]; });
+    if (stop_factor >= 0.0 &&
+        std::sqrt(uu) * std::sqrt(vv) <= stop_factor * f.frob())
       return STOP_INEQ;
+    // ||S_k||^2 = ||S_{k-1}||^2 + 2 sum_l (u.u_l)(v.v_l) + ||u||^2 ||v||^2
     Real cross = 0.0;
     for (int l = 0; l < f.rank(); ++l) {
-      Real du = 0.0, dv = 0.0;
       const Real* ul = f.Ucol(l);
       const Real* vl = f.Vcol(l);
-      for (long r = 0; r < m; ++r) du += u[r] * ul[r];
-      for (long c = 0; c < n; ++c) dv += v[c] * vl[c];
-      cross += du * dv;
+      const Real du = warp_dot(m, [&](long r) { return u[r]; }, [&](long r) { return ul[r]; });
+      const Real dv = warp_dot(n, [&](long c) { return v[c]; }, [&](long c) { return vl[c]; });
+      cross = std::fma(du, dv, cross);
     }
-    Real uu = 0.0, vv = 0.0;
-    for (long r = 0; r < m; ++r) uu += u[r] * u[r];
-    for (long c = 0; c < n; ++c) vv += v[c] * v[c];
     f.frob_sq += 2.0 * cross + uu * vv;
     f.U.insert(f.U.end(), u.begin(), u.end());
     f.V.insert(f.V.end(), v.begin(), v.end());
@@ -1118,7 +1182,7 @@ static Gamma gamma_contributions(const Grid& g, const Real* x) {
         const Real* xi = x + o.second * N;
         std::vector<Real> seg(cn.size()), y(rn.size(), 0.0);
         for (int c = 0; c < cn.size(); ++c) seg[c] = xi[cids[c]];
-        hb.factor.apply_range(k0, k1, seg.data(), y.data());
+        hb.factor.apply_range_device_order(k0, k1, seg.data(), y.data());
         for (int r = 0; r < rn.size(); ++r) {
           const Real v = 1.0 * y[r];
           if (g.ncomp == 1) {
@@ -1301,8 +1365,16 @@ using namespace oracle;
 namespace {
 thread_local std::string g_err;
 
+// built with -mfma (explicit std::fma in the canonical order): refuse to run
+// on a CPU without FMA instead of faulting
+const bool g_cpu_ok = __builtin_cpu_supports("fma");
+
 template <class F>
 int guard(F&& f) {
+  if (!g_cpu_ok) {
+    g_err = "oracle built with -mfma but this CPU has no FMA";
+    return 1;
+  }
   try {
     f();
     return 0;
@@ -1617,6 +1689,16 @@ int or_partition_json(void* h, char* buf, long* len) {
   });
 }
 
+// literal kelvin_tensor-based collocation entry (canonical-order check)
+int or_entry_literal(void* h, int comp, long i, long j, double* out) {
+  return guard([&] {
+    Problem* p = P(h);
+    if (p->kind != 0) throw Error("kelvin only");
+    *out = p->kelvin->colloc_single_literal(p->mesh.centroids[i], kCompR[comp],
+                                            kCompC[comp], static_cast<int>(j));
+  });
+}
+
 // single entry A_comp[i, j] in external ids
 int or_entry(void* h, int comp, long i, long j, double* out) {
   return guard([&] { *out = P(h)->oracles[comp]->entry(i, j); });
@@ -1831,6 +1913,43 @@ int or_amvm(void* h, const double* x, double theta, double eps_amvm,
       r[5] = it[i].storage_mb;
       r[6] = it[i].e_hat;
     }
+  });
+}
+
+// admissibility of two boxes [lo, hi] (cluster.cpp:21-24)
+int or_admissible(const double* a6, const double* b6, double eta, int* out) {
+  return guard([&] {
+    Box a, b;
+    a.absorb(Vec3{a6[0], a6[1], a6[2]});
+    a.absorb(Vec3{a6[3], a6[4], a6[5]});
+    b.absorb(Vec3{b6[0], b6[1], b6[2]});
+    b.absorb(Vec3{b6[3], b6[4], b6[5]});
+    *out = admissible(a, b, eta) ? 1 : 0;
+  });
+}
+
+// ACA of one admissible block of the problem's partition without
+// assembling the rest (sampled parity at full problem size):
+// full mode run + look-ahead extension as in assemble (hmatrix.cpp:160-168)
+int or_aca_block(void* h, int comp, int b, double eps, double beta,
+                 int initial_rank, int lookahead, int* k_cur, int* K,
+                 double* frob_sq, long* entries) {
+  return guard([&] {
+    Problem* p = P(h);
+    HMatrix tmp;
+    tmp.part = p->part.get();
+    tmp.oracle = p->oracles.at(comp).get();
+    const BlockView v = tmp.view(b);
+    if (!p->part->blocks.at(b).admissible) throw Error("block is not admissible");
+    const long before = tmp.oracle->evaluated.load();
+    Factor f = initial_rank >= 0
+                   ? aca_extend(empty_factor(v.m, v.n), initial_rank, v, 1L << 30)
+                   : aca_run(v, eps, beta, 1L << 30);
+    *k_cur = f.rank();
+    f = aca_extend(std::move(f), lookahead, v, 1L << 30);
+    *K = f.rank();
+    *frob_sq = f.frob_sq;
+    if (entries) *entries = tmp.oracle->evaluated.load() - before;
   });
 }
 

@@ -126,6 +126,14 @@ def self_term_i1(v9, p) -> float:
     return out.value
 
 
+def admissible(box_a, box_b, eta) -> bool:
+    a = np.ascontiguousarray(box_a, dtype=np.float64).reshape(6)
+    b = np.ascontiguousarray(box_b, dtype=np.float64).reshape(6)
+    out = C.c_int()
+    _ck(lib().or_admissible(_p(a), _p(b), D(eta), C.byref(out)))
+    return bool(out.value)
+
+
 class Problem:
     """An oracle problem: tree + partition + (after assemble) the component
     H-matrices of the reference semantics."""
@@ -159,7 +167,7 @@ class Problem:
         return cls(h, 1, len(p))
 
     @classmethod
-    def dense(cls, a, row_pts, col_pts, b_min=10, eta=0.8):
+    def dense_matrix(cls, a, row_pts, col_pts, b_min=10, eta=0.8):
         a = np.asfortranarray(a, dtype=np.float64)
         rp = np.ascontiguousarray(row_pts, dtype=np.float64)
         cp = np.ascontiguousarray(col_pts, dtype=np.float64)
@@ -200,12 +208,17 @@ class Problem:
 
     def entry(self, comp: int, i: int, j: int) -> float:
         out = D()
-        _ck(lib().or_entry(self._h, comp, C.c_long(i), C.c_long(j), C.byref(out)))
+        _ck(lib().or_entry(self._h, int(comp), C.c_long(i), C.c_long(j), C.byref(out)))
+        return out.value
+
+    def entry_literal(self, comp: int, i: int, j: int) -> float:
+        out = D()
+        _ck(lib().or_entry_literal(self._h, int(comp), C.c_long(i), C.c_long(j), C.byref(out)))
         return out.value
 
     def dense(self, comp: int = 0) -> np.ndarray:
         out = np.zeros((self.n, self.n))
-        _ck(lib().or_dense(self._h, comp, _p(out)))
+        _ck(lib().or_dense(self._h, int(comp), _p(out)))
         return out
 
     def dense_grid(self) -> np.ndarray:
@@ -241,19 +254,27 @@ class Problem:
     def factor(self, comp: int, b: int):
         m, n, K = C.c_int(), C.c_int(), C.c_int()
         fs = D()
-        _ck(lib().or_factor(self._h, comp, b, C.byref(m), C.byref(n), C.byref(K),
+        _ck(lib().or_factor(self._h, int(comp), int(b), C.byref(m), C.byref(n), C.byref(K),
                             None, None, None, C.byref(fs)))
         U = np.zeros((m.value, K.value), order="F")
         V = np.zeros((n.value, K.value), order="F")
         piv = np.zeros((K.value, 2), np.int32)
-        _ck(lib().or_factor(self._h, comp, b, C.byref(m), C.byref(n), C.byref(K),
+        _ck(lib().or_factor(self._h, int(comp), int(b), C.byref(m), C.byref(n), C.byref(K),
                             U.ctypes.data_as(C.c_void_p), V.ctypes.data_as(C.c_void_p),
                             _p(piv), C.byref(fs)))
         return dict(U=U, V=V, pivots=piv, frob_sq=fs.value)
 
+    def aca_block(self, comp, b, eps=1e-6, beta=0.8, initial_rank=-1, lookahead=2):
+        kc, K = C.c_int(), C.c_int()
+        fs = D()
+        ent = C.c_long()
+        _ck(lib().or_aca_block(self._h, int(comp), int(b), D(eps), D(beta), initial_rank, lookahead,
+                               C.byref(kc), C.byref(K), C.byref(fs), C.byref(ent)))
+        return kc.value, K.value, fs.value, ent.value
+
     def dense_block(self, comp: int, b: int, m: int, n: int) -> np.ndarray:
         out = np.zeros((m, n), order="F")
-        _ck(lib().or_dense_block(self._h, comp, b, out.ctypes.data_as(C.c_void_p)))
+        _ck(lib().or_dense_block(self._h, int(comp), int(b), out.ctypes.data_as(C.c_void_p)))
         return out
 
     def matvec(self, x, mode=0) -> np.ndarray:
@@ -281,10 +302,10 @@ class Problem:
         return dict(mb_current=a.value, mb_tail=b.value, total_pivots=p.value)
 
     def promote(self, comp, b):
-        _ck(lib().or_promote(self._h, comp, b))
+        _ck(lib().or_promote(self._h, int(comp), int(b)))
 
     def extend(self, comp, b, steps):
-        _ck(lib().or_extend(self._h, comp, b, steps))
+        _ck(lib().or_extend(self._h, int(comp), int(b), int(steps)))
 
     def gamma(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -16,7 +16,7 @@ HMGPU_PATH = os.path.join(LIB_DIR, "libhmgpu.so")
 if not os.path.exists(HMBEM_PATH) or not os.path.exists(HMGPU_PATH):
     raise ImportError(
         "paper_2205_04752_b200 native libraries are not built; run "
-        "`python -m paper_2205_04752_b200.build` (or __graft_entry__.build())")
+        "`python paper_2205_04752_b200/build.py` (or __graft_entry__.build())")
 
 gpu = C.CDLL(HMGPU_PATH, mode=C.RTLD_GLOBAL)
 host = C.CDLL(HMBEM_PATH)
@@ -51,6 +51,8 @@ _sig(host, "hmb_mesh_label", I, P, C.c_char_p)
 _sig(host, "hmb_mesh_sizes", I, P, IP, IP)
 _sig(host, "hmb_mesh_get", I, P, P, P, P, P, P, P, P)
 _sig(host, "hmb_mesh_free", None, P)
+_sig(host, "hmb_admissible", I, P, P, D, IP)
+_sig(host, "hmb_gauss_rule", I, I, IP, P, P, P)
 _sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_dense", I, I, I, P, P, P, I, D, I, C.POINTER(P))

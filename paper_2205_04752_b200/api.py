@@ -489,6 +489,24 @@ class HMatrix:
 
 
 # ---- reference-style free functions ----------------------------------------
+def gauss_rule(order: int):
+    """(a, b, w) of the symmetric triangle rule (quadrature.cpp:55-95)."""
+    n = C.c_int()
+    _check(_h.hmb_gauss_rule(order, C.byref(n), None, None, None))
+    a, b, w = np.zeros(n.value), np.zeros(n.value), np.zeros(n.value)
+    _check(_h.hmb_gauss_rule(order, C.byref(n), _ptr(a), _ptr(b), _ptr(w)))
+    return a, b, w
+
+
+def admissible(box_t, box_s, eta: float) -> bool:
+    """min(diam t, diam s) < eta * dist(t, s) on [lo, hi] boxes (cluster.cpp:21-24)."""
+    a = _f64(box_t).reshape(6)
+    b = _f64(box_s).reshape(6)
+    out = C.c_int()
+    _check(_h.hmb_admissible(_ptr(a), _ptr(b), eta, C.byref(out)))
+    return bool(out.value)
+
+
 def assemble(h: HMatrix, cfg: AssemblyConfig) -> HMatrix:
     h.assemble(cfg)
     return h

@@ -6,7 +6,7 @@
   lib/libhmbem.so  -- host C++ layer + C API of include/hmbem.h, linked
                       against libhmgpu.so (rpath $ORIGIN)
 
-Run ``python -m paper_2205_04752_b200.build`` or call ``build()``.
+Run ``python paper_2205_04752_b200/build.py`` or call ``build()``.
 """
 from __future__ import annotations
 
@@ -51,7 +51,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     gpu_so = os.path.join(LIB, "libhmgpu.so")
     gpu_deps = _glob(GPU_SRC, (".cu", ".cuh")) + [os.path.join(INC, "hmgpu.h")]
     if force or _newer(gpu_so, gpu_deps):
-        cmd = [NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+        # --fmad=false: every fused multiply-add in device code is an explicit
+        # fma(), so the ACA arithmetic is bit-reproducible by the CPU oracle
+        cmd = [NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "--fmad=false",
+               "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "-I", INC, "-shared", "-cudart",
                "static", "-o", gpu_so, os.path.join(GPU_SRC, "hmgpu.cu")]
         if verbose_ptxas:

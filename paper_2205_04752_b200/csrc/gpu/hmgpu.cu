@@ -9,8 +9,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -245,6 +247,11 @@ int guard(hmgpu_ctx* c, F&& f) {
   }
 }
 
+bool verbose() {
+  static const bool v = std::getenv("HMGPU_VERBOSE") != nullptr;
+  return v;
+}
+
 int grid_for(hmgpu_ctx* c, long long work, int per_sm = 8) {
   const long long g = std::min<long long>(work, (long long)c->sm_count * per_sm);
   return (int)std::max<long long>(1, g);
@@ -453,6 +460,9 @@ void compact(hmgpu_ctx* c, int slack) {
     np[t] = usedp;
     usedp += std::max(caps[t], 1);
   }
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  if (8.0 * (double)used + 4.0 * (double)usedp * 2 > 0.9 * (double)free_b) return;
   DBuf<double> na;
   na.alloc((size_t)used + 2);
   DBuf<int2> npv;
@@ -798,6 +808,15 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     }
     c->pending.clear();
 
+    auto wall0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+      if (!verbose()) return;
+      c->sync();
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[hmgpu] %-12s %9.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - wall0).count());
+      wall0 = now;
+    };
     cudaEvent_t t0, t1, tn0, tn1;
     CK(cudaEventCreate(&t0));
     CK(cudaEventCreate(&t1));
@@ -814,7 +833,35 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     c->piv_used = 0;
     c->dense_used = 0;
     long long cons_used = 0;
-    const int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
+    // release the previous assembly before sizing this one
+    c->d_arena.free();
+    c->d_dense.free();
+    c->d_piv.free();
+    c->d_cons.free();
+    c->d_ypart.free();
+    // Initial column capacity per item: the coarse mode knows its final
+    // rank; full mode starts at 24 + lookahead columns, lowered when the
+    // device memory would not hold it (items that outgrow their capacity
+    // are relocated and resumed, see run_aca).
+    long long sum_mn = 0, dense_total = 0;
+    for (int b = 0; b < c->n_blocks; ++b) {
+      const int* B = &c->blocks[4 * b];
+      const int* rn = &c->rnodes[4 * B[0]];
+      const int* cn = &c->cnodes[4 * B[1]];
+      if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
+      const long long m = rn[1] - rn[0], n = cn[1] - cn[0];
+      if (B[2]) sum_mn += (m + n) * c->NC;
+      else dense_total += align2((long long)c->NC * m * n);
+    }
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double avail =
+        (double)free_b - 8.0 * (double)dense_total - 4.0 * (1 << 30);
+    int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
+    if (initial_rank < 0 && sum_mn > 0) {
+      const long long fit = (long long)(0.55 * avail / (8.0 * (double)sum_mn));
+      cap_init = (int)std::max<long long>(lookahead + 6, std::min<long long>(cap_init, fit));
+    }
     for (int b = 0; b < c->n_blocks; ++b) {
       const int* B = &c->blocks[4 * b];
       const int* rn = &c->rnodes[4 * B[0]];
@@ -854,14 +901,20 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         c->dblocks.push_back(db);
       }
     }
+    // headroom at the arena end for relocated (regrown) items
+    const double want = 8.0 * (double)c->arena_used * 1.3;
+    const size_t arena_cap = want < 0.85 * avail ? (size_t)(c->arena_used * 1.3)
+                                                 : (size_t)c->arena_used;
+    phase("items");
     c->d_items.upload(c->items, c->stream);
-    c->d_arena.alloc((size_t)c->arena_used + 2);
-    c->d_piv.alloc((size_t)c->piv_used + 1);
+    c->d_arena.alloc(arena_cap + 2);
+    c->d_piv.alloc((size_t)(c->piv_used * 1.3) + 1);
     c->d_cons.alloc((size_t)cons_used + 16);
     CK(cudaMemsetAsync(c->d_cons.p, 0, cons_used + 16, c->stream));
     c->d_dense.alloc((size_t)c->dense_used + 2);
     c->d_dblocks.upload(c->dblocks, c->stream);
 
+    phase("alloc+upload");
     // near-field fill
     CK(cudaEventRecord(tn0, c->stream));
     if (!c->dblocks.empty()) {
@@ -877,6 +930,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     }
     CK(cudaEventRecord(tn1, c->stream));
 
+    phase("nearfield");
     // ACA, largest blocks first
     std::vector<int> list(c->items.size());
     std::iota(list.begin(), list.end(), 0);
@@ -885,7 +939,17 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     });
     int relaunch = 0;
     run_aca(c, list, &relaunch);
+    phase("aca");
     compact(c, 0);
+    phase("compact");
+    if (verbose()) {
+      size_t f2 = 0, t2 = 0;
+      cudaMemGetInfo(&f2, &t2);
+      std::fprintf(stderr, "[hmgpu] items=%zu cap_init=%d arena=%.2f GB dense=%.2f GB "
+                           "free_after=%.2f GB relaunches=%d\n",
+                   c->items.size(), cap_init, 8.0 * c->arena_used / 1e9,
+                   8.0 * c->dense_used / 1e9, f2 / 1e9, relaunch);
+    }
     CK(cudaEventRecord(t1, c->stream));
     c->sync();
     float ms_total = 0, ms_near = 0;
@@ -896,6 +960,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     cudaEventDestroy(tn0);
     cudaEventDestroy(tn1);
     build_matvec(c);
+    phase("build_matvec");
     c->assembled = true;
     if (stats) {
       hmgpu_assembly_stats s{};

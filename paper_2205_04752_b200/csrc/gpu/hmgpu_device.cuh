@@ -118,6 +118,11 @@ __device__ void kelvin_self6(const Geom& g, double px, double py, double pz,
 
 // A_rc[i, j] = 2 area_j sum_q w_q S(p_i - y_q)_rc for one component
 // (colloc_single, kernels.cpp:176-187), S from kelvin_tensor (:21-28).
+// Canonical evaluation order (the parity contract with the CPU oracle,
+// oracle/hmbem_oracle.cpp Kelvin::colloc_single): c factored out of the
+// sum, 1/|x| as one IEEE division of an IEEE square root, explicit fma
+// (the library is compiled with --fmad=false so nothing else contracts).
+// With it ACA pivots, ranks and factors are bit-identical to the oracle.
 __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
                                                 int comp) {
   const double4 p = g.rowpt[i];
@@ -141,16 +146,17 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
     const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
     const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    const double ri = rsqrt(r2);
+    const double ri = 1.0 / sqrt(r2);
     const double wr = w * ri;
-    acc_d += wr;
+    acc_d = acc_d + wr;
     acc_x = fma(wr * ri * ri, sel3(r, dx, dy, dz) * sel3(c, dx, dy, dz), acc_x);
   }
   const double s = (r == c) ? fma(g.c34, acc_d, acc_x) : acc_x;
   return 2.0 * T[12] * g.cst * s;
 }
 
-// all six components of one (point, triangle) pair (near-field fill)
+// all six components of one (point, triangle) pair (near-field fill), each
+// in the same canonical order as kelvin_entry1
 __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
                                               double* out6) {
   const double4 p = g.rowpt[i];
@@ -173,26 +179,24 @@ __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
     const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
     const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    const double ri = rsqrt(r2);
+    const double ri = 1.0 / sqrt(r2);
     const double wr = w * ri;
-    const double wr3 = wr * ri * ri;
-    ad += wr;
-    const double tx = wr3 * dx, ty = wr3 * dy, tz = wr3 * dz;
-    a00 = fma(tx, dx, a00);
-    a01 = fma(tx, dy, a01);
-    a02 = fma(tx, dz, a02);
-    a11 = fma(ty, dy, a11);
-    a12 = fma(ty, dz, a12);
-    a22 = fma(tz, dz, a22);
+    const double w3 = wr * ri * ri;
+    ad = ad + wr;
+    a00 = fma(w3, dx * dx, a00);
+    a01 = fma(w3, dx * dy, a01);
+    a02 = fma(w3, dx * dz, a02);
+    a11 = fma(w3, dy * dy, a11);
+    a12 = fma(w3, dy * dz, a12);
+    a22 = fma(w3, dz * dz, a22);
   }
   const double f = 2.0 * T[12] * g.cst;
-  const double dd = g.c34 * ad;
-  out6[0] = f * (dd + a00);
+  out6[0] = f * fma(g.c34, ad, a00);
   out6[1] = f * a01;
   out6[2] = f * a02;
-  out6[3] = f * (dd + a11);
+  out6[3] = f * fma(g.c34, ad, a11);
   out6[4] = f * a12;
-  out6[5] = f * (dd + a22);
+  out6[5] = f * fma(g.c34, ad, a22);
 }
 
 // Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact

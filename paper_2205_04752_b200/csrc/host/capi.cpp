@@ -11,6 +11,7 @@
 #include "hmbem.h"
 #include "hmgpu.h"
 #include "operator.hpp"
+#include "quadrature.hpp"
 
 struct hmb_mesh {
   hmb::Mesh mesh;
@@ -173,6 +174,31 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
 }
 
 void hmb_mesh_free(hmb_mesh* m) { delete m; }
+
+int hmb_gauss_rule(int order, int* npts, double* a, double* b, double* w) {
+  return guard([&] {
+    need(npts, "npts");
+    const hmb::TriangleRule r = hmb::gauss_rule(order);
+    *npts = static_cast<int>(r.w.size());
+    if (a) std::memcpy(a, r.a.data(), r.a.size() * sizeof(double));
+    if (b) std::memcpy(b, r.b.data(), r.b.size() * sizeof(double));
+    if (w) std::memcpy(w, r.w.data(), r.w.size() * sizeof(double));
+  });
+}
+
+int hmb_admissible(const double* a6, const double* b6, double eta, int* out) {
+  return guard([&] {
+    need(a6, "a");
+    need(b6, "b");
+    need(out, "out");
+    hmb::Box a, b;
+    a.absorb(hmb::V3{a6[0], a6[1], a6[2]});
+    a.absorb(hmb::V3{a6[3], a6[4], a6[5]});
+    b.absorb(hmb::V3{b6[0], b6[1], b6[2]});
+    b.absorb(hmb::V3{b6[3], b6[4], b6[5]});
+    *out = hmb::admissible(a, b, eta) ? 1 : 0;
+  });
+}
 
 int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
                   int device, int shard_rank, int shard_count, hmb_op** out) {
