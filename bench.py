@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py -- H-matvec dofs/s & ACA assembly entries/s (fp64) on B200.
+
+One "step" = one H-matrix-vector product y = A x of the 3x3 Kelvin
+collocation H-matrix (BASELINE.json configs[1] by default: unit-sphere
+icosphere, 20480 triangles, 61440 dofs, b_min 32, eta 1, ACA eps 1e-6,
+x uniform [-1,1] seed 1).  The H-matrix is assembled once on the GPU before
+the timed region; assembly is timed separately and reported under
+"assembly" (entries/s and fp64 roofline).
+
+  value : dofs/s of the device-resident matvec (x, y already in HBM), K steps
+          timed with CUDA events on the library's stream, max over ranks
+  e2e   : the same metric through the public API with pinned host buffers
+          (H2D of x and D2H of y inside every timed step)
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+        python bench.py --impl reference ...   (CPU oracle of the reference path)
+Multi-GPU (torchrun): block rows sharded over ranks, x broadcast and y
+summed (disjoint rows) with NCCL on the library's stream.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H-matvec dofs/s & ACA assembly entries/s (fp64), % of HBM/FP64 roofline"
+
+CONFIGS = {
+    # BASELINE.json configs[k]; meshes are synthetic (no dataset ships)
+    "c1": dict(desc="icosphere L3, 1280 triangles, 3840 dofs", mesh=("icosphere", 3),
+               b_min=32, eta=1.0, eps=1e-4, nrhs=1, seed=0, x="uniform"),
+    "c2": dict(desc="icosphere L5, 20480 triangles, 61440 dofs", mesh=("icosphere", 5),
+               b_min=32, eta=1.0, eps=1e-6, nrhs=1, seed=1, x="uniform"),
+    "c3": dict(desc="voxel cube [0,1]^3 128^2/face, 196608 triangles, 589824 dofs",
+               mesh=("cube", 128), b_min=64, eta=1.0, eps=1e-5, nrhs=1, seed=2,
+               x="normal_dirichlet0"),
+    "c4": dict(desc="ellipsoid (2,1,0.5) L6, 81920 triangles, 245760 dofs",
+               mesh=("ellipsoid", 6), b_min=32, eta=1.0, eps=1e-2, nrhs=1, seed=3,
+               x="bump"),
+    "c5": dict(desc="icosphere L8, 1310720 triangles, 3932160 dofs, 16 RHS",
+               mesh=("icosphere", 8), b_min=64, eta=1.0, eps=1e-5, nrhs=16, seed=4,
+               x="normal"),
+}
+
+BETA_STOP = 0.8  # ACA stopping beta (partition eta = 1 is outside (0,1))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_mesh(hm, cfg):
+    kind, p = cfg["mesh"]
+    if kind == "icosphere":
+        return hm.Mesh.icosphere(p)
+    if kind == "ellipsoid":
+        return hm.Mesh.ellipsoid(p, 2.0, 1.0, 0.5)
+    m = hm.Mesh.voxel_cube(p, 0.0, 1.0)
+    m.label_dirichlet("x3<=0")
+    return m
+
+
+def make_x(hm, cfg, mesh, n_dofs):
+    nrhs = cfg["nrhs"]
+    kind = cfg["x"]
+    if kind == "uniform":
+        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "uniform")
+    elif kind == "normal":
+        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "normal")
+    elif kind == "normal_dirichlet0":
+        x = hm.random_vector(n_dofs, cfg["seed"], "normal")
+        d = mesh.arrays()["dirichlet"].astype(bool)
+        x.reshape(3, -1)[:, d] = 0.0  # g_N extension convention (hmbem_cli.cpp:76-77)
+    else:  # Gaussian bump at (2,0,0), sigma 0.05, + 1e-3 uniform noise
+        c = mesh.arrays()["centroids"]
+        bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.05 ** 2))
+        x = np.tile(bump, 3) + 1e-3 * hm.random_vector(n_dofs, cfg["seed"], "uniform")
+    return np.asfortranarray(x.reshape(nrhs, n_dofs).T) if nrhs > 1 else x
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def profile_traffic(config_name):
+    """dram bytes per matvec of the streamed kernels from the committed ncu
+    summary (profiles/ncu_<config>_matvec.json), if present."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{config_name}_matvec.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_matvec")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(args, cfg, emit_line: bool):
+    """The reference path's CPU implementation (oracle port) on this config:
+    assembly with all host threads (parallel_for over blocks) and the serial
+    H-matvec (hmatrix.cpp:22-45), each step one matvec."""
+    import paper_2205_04752_b200 as hm
+    from oracle import oracle as orc
+    mesh = make_mesh(hm, cfg)
+    a = mesh.arrays()
+    cores = os.cpu_count() or 1
+    prob = orc.Problem.kelvin(a["vertices"], a["triangles"], 1.0, 0.3, cfg["b_min"], cfg["eta"])
+    t0 = time.perf_counter()
+    prob.assemble(eps=cfg["eps"], beta=BETA_STOP)
+    t_asm = time.perf_counter() - t0
+    _, entries = prob.assemble_time()
+    n = 3 * mesh.num_triangles
+    x = make_x(hm, cfg, mesh, n)
+    xs = x if x.ndim == 1 else x[:, 0]
+    times = []
+    steps = args.steps if emit_line else 3
+    warm = args.warmup if emit_line else 1
+    for it in range(warm + steps):
+        t0 = time.perf_counter()
+        prob.matvec(xs)
+        dt = time.perf_counter() - t0
+        if it >= warm:
+            times.append(dt)
+    t_mv = float(np.mean(times))
+    value = n / t_mv
+    sample = (f"{cfg['desc']}: oracle assembly ({cores} threads, {t_asm:.1f} s) + "
+              f"{steps} serial H-matvecs (1 RHS, {t_mv * 1e3:.1f} ms each)")
+    out = {
+        "cpu_baseline": {"value": value, "unit": "dofs/s", "cores": 1, "kind": "port",
+                         "sample": sample, "ms_per_matvec": t_mv * 1e3},
+        "assembly": {"value": entries / t_asm, "unit": "entries/s", "cores": cores,
+                     "seconds": t_asm, "entries": entries},
+    }
+    return out, t_mv
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    res, t_mv = cpu_reference(args, cfg, emit_line=True)
+    v = res["cpu_baseline"]["value"]
+    line = {
+        "metric": METRIC, "value": v, "unit": "dofs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_mv * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": args.config + ": " + cfg["desc"], "b_min": cfg["b_min"],
+                   "eta": cfg["eta"], "eps_aca": cfg["eps"], "beta_stop": BETA_STOP,
+                   "nrhs": 1},
+        "cpu_baseline": res["cpu_baseline"],
+        "assembly_cpu": res["assembly"],
+        "e2e": {"value": v, "unit": "dofs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import paper_2205_04752_b200 as hm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    torch.cuda.set_device(device)
+
+    mesh = make_mesh(hm, cfg)
+    nrhs = cfg["nrhs"]
+    h = hm.HMatrix.kelvin(mesh, E=1.0, nu=0.3, b_min=cfg["b_min"], eta=cfg["eta"],
+                          device=device, shard=(rank, world))
+    n = h.cols
+    # ---- assembly (timed on the device, best of 2 after one warm-up) ----
+    asm = []
+    for _ in range(3):
+        st = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        asm.append(st)
+    best = min(asm[1:], key=lambda s: s.ms_total)
+    storage = h.storage()
+    fp64_peak = hm.fp64_peak_tflops(device)
+
+    x = make_x(hm, cfg, mesh, n)
+    xt = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x), dtype=torch.float64,
+                      device=f"cuda:{device}")
+    # library layout: dofs x nrhs column-major == nrhs x dofs row-major
+    yt = torch.zeros((nrhs, h.rows) if nrhs > 1 else h.rows, dtype=torch.float64,
+                     device=f"cuda:{device}")
+    stream = torch.cuda.ExternalStream(h.stream(), device=f"cuda:{device}")
+
+    def step():
+        with torch.cuda.stream(stream):
+            if dist is not None:
+                dist.broadcast(xt, src=0)
+            h.matvec_ptr(xt.data_ptr(), yt.data_ptr(), nrhs)
+            if dist is not None:
+                dist.all_reduce(yt)  # rows are disjoint across ranks: sum = gather
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-kernel device times from a separate profiled pass (not the timed one)
+    h.set_profiling(True)
+    for k in ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_reduce", "hmv_blocks"):
+        h.kernel_times(k, reset=True)
+    for _ in range(max(3, min(args.steps, 10))):
+        step()
+    torch.cuda.synchronize()
+    kt = {k: h.kernel_times(k, reset=True) for k in
+          ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_reduce", "hmv_blocks")}
+    h.set_profiling(False)
+
+    # ---- timed region: K device-resident matvecs ----
+    clocks = ClockSampler(device)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)  # sampler warm-up
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = h.rows * nrhs / (ms_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers ----
+    xh = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x),
+                      dtype=torch.float64).pin_memory()
+    yh = torch.zeros(yt.shape, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if dist is not None:  # host-driven: x from host on every rank, y reduced
+            h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
+            yd = yh.to(f"cuda:{device}", non_blocking=True)
+            dist.all_reduce(yd)
+            yh.copy_(yd)
+        else:
+            h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # ---- roofline of the dominant kernel (the streamed sweep) ----
+    peak, peak_src = measured_peaks()
+    ms_stream = (kt["hmv_stream"][0] + kt["hmv_ypart"][0]) / max(kt["hmv_stream"][1], 1)
+    ms_blocks = kt["hmv_blocks"][0] / max(kt["hmv_blocks"][1], 1)
+    ms_dom = ms_stream if ms_stream > 0 else ms_blocks
+    dom_name = "hmv_stream_kernel (pass A + pass B)" if ms_stream > 0 else "hmv_blocks_kernel"
+    alg_bytes = storage["matvec_bytes"] + 8 * (nrhs - 1) * (h.rows + h.cols)
+    achieved = alg_bytes / (ms_dom * 1e-3) / 1e9 if ms_dom > 0 else None
+    traffic = profile_traffic(args.config)
+
+    res = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res, _ = cpu_reference(args, cfg, emit_line=False)
+    # counted fp64 flops per entry: 30 n_q + 1 with n_q = 7 for
+    # near-field pairs; ACA entries mostly far (n_q = 3); report entries/s
+    asm_s = best.ms_total * 1e-3
+    entries = best.aca_entries + best.dense_entries
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "dofs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded mesh + x; random_vector mt19937_64)",
+        "config": {"workload": args.config + ": " + cfg["desc"], "b_min": cfg["b_min"],
+                   "eta": cfg["eta"], "eps_aca": cfg["eps"], "beta_stop": BETA_STOP,
+                   "lookahead": 2, "nrhs": nrhs,
+                   "parallelism": f"block-row shards x{world}" if world > 1 else "1 GPU",
+                   "l2": f"inputs larger than L2: {alg_bytes / 1e9:.2f} GB streamed per step"},
+        "roofline": {"bound": "hbm", "kernel": dom_name,
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_step": alg_bytes,
+                     "ms_kernel": ms_dom,
+                     "ms_matvec_device": ms_step,
+                     "matvec_frac_incl_gather_reduce": alg_bytes / (ms_step * 1e-3) / 1e9 / peak},
+        "e2e": {"value": h.rows * nrhs / e2e_s, "unit": "dofs/s",
+                "h2d_bytes_per_step": int(8 * h.cols * nrhs),
+                "d2h_bytes_per_step": int(8 * h.rows * nrhs)},
+        "gpu_launches": int(args.steps * (3 + (kt["hmv_zreduce"][1] > 0) +
+                                          (kt["hmv_ypart"][1] > 0))),
+        "clocks": ck,
+        "assembly": {"value": entries / asm_s, "unit": "entries/s", "ms": best.ms_total,
+                     "ms_nearfield": best.ms_nearfield, "aca_entries": best.aca_entries,
+                     "dense_entries": best.dense_entries, "pivots": best.pivots,
+                     "fp64_peak_tflops_measured": fp64_peak,
+                     "storage_mb": storage["mb_current"]},
+        "kernel_ms": {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kt.items()},
+    }
+    if res is not None:
+        line["cpu_baseline"] = res["cpu_baseline"]
+        line["assembly"]["cpu_entries_per_s"] = res["assembly"]["value"]
+        line["assembly"]["cpu_cores"] = res["assembly"]["cores"]
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("note: warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

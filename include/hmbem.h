@@ -59,6 +59,10 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
                  double* areas, double* normals, double* diam, int* dirichlet);
 void hmb_mesh_free(hmb_mesh* m);
 
+/* seeded synthetic input: kind 0 = uniform [-1,1) (mt19937_64, the
+ * reference's random_vector, oracles.cpp:415-421), 1 = standard normal */
+int hmb_random_vector(long long n, unsigned long long seed, int kind, double* out);
+
 /* gauss_rule(order) tables as uploaded to the device (quadrature.cpp:55-95);
  * a/b/w may be NULL to query npts */
 int hmb_gauss_rule(int order, int* npts, double* a, double* b, double* w);

@@ -179,6 +179,10 @@ int hmgpu_download_dense(hmgpu_ctx* ctx, int comp, int block, double* out);
 
 int hmgpu_storage(hmgpu_ctx* ctx, hmgpu_storage_info* info);
 
+/* measured DFMA throughput of the device (TFLOP/s, 2 flops per FMA): the
+ * fp64 roofline denominator of the assembly kernels */
+int hmgpu_fp64_peak(int device, double* tflops);
+
 /* CUDA-event timing of every kernel launch (off by default).  names are
  * "gather", "nearfield", "aca", "hmv_blocks", "hmv_reduce", "tail", ...
  * hmgpu_kernel_times returns accumulated milliseconds and launch counts for

@@ -53,6 +53,7 @@ _sig(host, "hmb_mesh_get", I, P, P, P, P, P, P, P, P)
 _sig(host, "hmb_mesh_free", None, P)
 _sig(host, "hmb_admissible", I, P, P, D, IP)
 _sig(host, "hmb_gauss_rule", I, I, IP, P, P, P)
+_sig(host, "hmb_random_vector", I, LL, C.c_ulonglong, I, P)
 _sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_dense", I, I, I, P, P, P, I, D, I, C.POINTER(P))
@@ -85,6 +86,7 @@ _sig(gpu, "hmgpu_get_stream", I, P, C.POINTER(P))
 _sig(gpu, "hmgpu_set_profiling", I, P, I)
 _sig(gpu, "hmgpu_kernel_times", I, P, C.c_char_p, DP, LLP, I)
 _sig(gpu, "hmgpu_storage", I, P, P)
+_sig(gpu, "hmgpu_fp64_peak", I, I, DP)
 
 HMGPU_SYMBOLS = [
     "hmgpu_device_count", "hmgpu_create", "hmgpu_destroy", "hmgpu_last_error",
@@ -93,5 +95,5 @@ HMGPU_SYMBOLS = [
     "hmgpu_set_partition", "hmgpu_assemble", "hmgpu_ranks", "hmgpu_matvec",
     "hmgpu_promote", "hmgpu_extend", "hmgpu_tail_terms", "hmgpu_download_factor",
     "hmgpu_download_dense", "hmgpu_storage", "hmgpu_set_profiling",
-    "hmgpu_kernel_times",
+    "hmgpu_kernel_times", "hmgpu_fp64_peak",
 ]

@@ -489,6 +489,23 @@ class HMatrix:
 
 
 # ---- reference-style free functions ----------------------------------------
+def random_vector(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
+    """Seeded synthetic input: mt19937_64 + uniform [-1,1) (the reference's
+    random_vector) or standard normal."""
+    out = np.zeros(n)
+    _check(_h.hmb_random_vector(n, seed, 0 if kind == "uniform" else 1, _ptr(out)))
+    return out
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DFMA throughput of the device (fp64 roofline denominator)."""
+    v = C.c_double()
+    st = _lib.gpu.hmgpu_fp64_peak(device, C.byref(v))
+    if st:
+        raise DeviceError("hmgpu_fp64_peak failed", st)
+    return v.value
+
+
 def gauss_rule(order: int):
     """(a, b, w) of the symmetric triangle rule (quadrature.cpp:55-95)."""
     n = C.c_int()

@@ -23,6 +23,7 @@
 
 #include "hmgpu.h"
 #include "hmgpu_device.cuh"
+#include "hmgpu_stream.cuh"
 
 using namespace hmgpu;
 
@@ -158,6 +159,22 @@ struct hmgpu_ctx {
   int kmax = 0;
   DBuf<double> d_x, d_y, d_xi, d_ypart;
 
+  // ---- streamed matvec plan (packed current-rank arena, task list) ----
+  bool plan_valid = false;
+  int plan_mode = -1, plan_nrhs = -1;
+  int p_ntasks = 0, p_nz = 0;
+  long long p_slots = 0, p_zslots = 0, p_arena_len = 0;
+  int p_xs = 0, p_stage = 0, p_xbuf = 0, p_zbuf = 0, p_ybuf = 0;
+  size_t p_smem = 0;
+  int p_ctas_per_sm = 1;
+  DBuf<MvTask> d_ptasks;
+  DBuf<double> d_sarena, d_zpart;
+  DBuf<LeafEntry> d_pentries;
+  DBuf<int> d_pleaf_ptr;
+  DBuf<ZReduce> d_zred;
+  int p_nzred = 0;
+  std::vector<int> p_leaf_ptr;
+
   // ---- profiling ----
   bool prof = false;
   std::map<std::string, KTime> times;
@@ -178,6 +195,9 @@ struct hmgpu_ctx {
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
     d_leaf_ptr.free(); d_leaf_prow.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
+    d_ptasks.free(); d_sarena.free(); d_zpart.free(); d_pentries.free();
+    d_pleaf_ptr.free();
+    d_zred.free();
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -585,6 +605,307 @@ void refresh_matvec_ranks(hmgpu_ctx* c) {
   for (const Item& it : c->items) c->kmax = std::max(c->kmax, it.k);
 }
 
+
+// ---- streamed matvec plan ----------------------------------------------------
+// Task kinds (hmgpu_stream.cuh): FUSED blocks whose six components fit one
+// stage; otherwise VCOLS column ranges of V_c (row tiles of at most xrows,
+// partials summed by zreduce) and YPART row tiles of all components' U;
+// DENSE row tiles.  Every block row gets exactly one partial row per
+// covering block.
+constexpr int kStage = 3072;   // doubles per stage (24 KB)
+constexpr int kNStage = 3;     // TMA pipeline depth per CTA
+constexpr int kMaxKTask = 256; // z slots of a FUSED task (shared-memory z)
+
+void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
+  const int NC = c->NC;
+  const int NOUT = NC == 6 ? 3 : 1;
+  const int xs = (NOUT == 3 ? 4 : 2) * nrhs;
+  const int xbuf = std::max(512, 64 * xs);
+  const int xrows = xbuf / xs;
+  std::vector<MvTask> ta, tb;
+  std::vector<PackDesc> packs;
+  std::vector<ZReduce> zred;
+  long long alen = 0, slots = 0, zfinal = 0;
+  std::vector<std::pair<long long, long long>> vcols_parts;  // (task index in ta, partial base)
+  long long zpartial = 0;
+  const int nl = (int)c->leaf_begin.size();
+  std::vector<std::vector<LeafEntry>> lists(nl);
+  auto add_rows = [&](int r_lo, int nrows, long long slot) {
+    const int r_hi = r_lo + nrows;
+    int l = (int)(std::upper_bound(c->leaf_begin.begin(), c->leaf_begin.end(), r_lo) -
+                  c->leaf_begin.begin()) - 1;
+    for (l = std::max(l, 0); l < nl && c->leaf_begin[l] < r_hi; ++l) {
+      const int lb = c->leaf_begin[l], le = c->leaf_end[l];
+      const int lo = std::max(lb, r_lo), hi = std::min(le, r_hi);
+      if (lo >= hi) continue;
+      lists[l].push_back(LeafEntry{slot + (lo - r_lo), lo - lb, hi - lb});
+    }
+  };
+  auto pack = [&](long long src, int ld, int rows, int cols, long long dst) {
+    if (rows > 0 && cols > 0) packs.push_back(PackDesc{src, dst, ld, rows, cols, 0});
+  };
+  for (const MvBlock& mb : c->mvb) {
+    const int m = mb.m, n = mb.n;
+    if (mb.dense) {
+      const int rowlen = (int)align2((long long)n * NC);
+      if (n > xrows || rowlen > kStage)
+        fail(HMGPU_ERR_INVALID, "near-field block too wide for the streamed matvec");
+      const int tile = std::max(1, std::min(m, kStage / rowlen));
+      for (int r0 = 0; r0 < m; r0 += tile) {
+        const int rt = std::min(tile, m - r0);
+        MvTask t{};
+        t.kind = TK_DENSE;
+        t.c1 = NC;
+        t.rows = rt;
+        t.cols = n;
+        t.src = 1;
+        t.x_rows = n;
+        t.x_col0 = mb.col0;
+        t.data_off = mb.dense_off + (long long)r0 * rowlen;
+        t.data_len = rt * rowlen;
+        t.out_off = slots;
+        add_rows(mb.row0 + r0, rt, slots);
+        slots += rt;
+        ta.push_back(t);
+      }
+      continue;
+    }
+    int k[6] = {0, 0, 0, 0, 0, 0};
+    long long total = 0;
+    int ksum = 0;
+    for (int q = 0; q < NC; ++q) {
+      const Item& it = c->items[mb.item0 + q];
+      k[q] = mode ? it.k : it.kcur;
+      total += (long long)k[q] * (m + n);
+      ksum += k[q];
+    }
+    if (ksum == 0) continue;
+    if (n <= xrows && total <= kStage && ksum <= kMaxKTask) {
+      MvTask t{};
+      t.kind = TK_FUSED;
+      t.c1 = NC;
+      t.rows = m;
+      t.cols = n;
+      t.x_rows = n;
+      t.x_col0 = mb.col0;
+      t.data_off = alen;
+      long long cur = alen;
+      for (int q = 0; q < NC; ++q) {
+        t.k[q] = k[q];
+        pack(c->items[mb.item0 + q].v_off, n, n, k[q], cur);
+        cur += (long long)n * k[q];
+      }
+      for (int q = 0; q < NC; ++q) {
+        pack(c->items[mb.item0 + q].u_off, m, m, k[q], cur);
+        cur += (long long)m * k[q];
+      }
+      t.data_len = (int)align2(cur - alen);
+      alen += t.data_len;
+      t.out_off = slots;
+      add_rows(mb.row0, m, slots);
+      slots += m;
+      ta.push_back(t);
+      continue;
+    }
+    // split block: V column ranges -> z (global), then U row tiles
+    const long long zoff = zfinal;
+    zfinal += ksum;
+    long long coff = 0;
+    for (int q = 0; q < NC; ++q) {
+      const int kq = k[q];
+      if (kq == 0) continue;
+      const Item& it = c->items[mb.item0 + q];
+      const int nt = (n + xrows - 1) / xrows;
+      const int trows = (n + nt - 1) / nt;
+      const long long pbase = zpartial;
+      if (nt > 1) zpartial += (long long)nt * kq;
+      for (int tt = 0; tt < nt; ++tt) {
+        const int j0 = tt * trows, rt = std::min(trows, n - j0);
+        const int cl = std::max(1, kStage / std::max(rt, 1));
+        for (int l0 = 0; l0 < kq; l0 += cl) {
+          const int lc = std::min(cl, kq - l0);
+          MvTask t{};
+          t.kind = TK_VCOLS;
+          t.c0 = q;
+          t.c1 = q + 1;
+          t.k[q] = lc;
+          t.l0 = l0;
+          t.rows = rt;
+          t.cols = lc;
+          t.x_rows = rt;
+          t.x_col0 = mb.col0 + j0;
+          t.data_off = alen;
+          pack(it.v_off + j0 + (long long)l0 * n, n, rt, lc, alen);
+          t.data_len = (int)align2((long long)rt * lc);
+          alen += t.data_len;
+          // final slot, or a partial slot (rebased after zfinal is known)
+          t.out_off = nt == 1 ? zoff + coff + l0 : -(pbase + (long long)tt * kq + l0) - 1;
+          ta.push_back(t);
+        }
+      }
+      if (nt > 1) zred.push_back(ZReduce{zoff + coff, pbase, kq, nt, kq, 0});
+      coff += kq;
+    }
+    // U row tiles over component groups whose z slots fit the x area
+    long long zg = zoff;
+    for (int q0 = 0; q0 < NC;) {
+      int q1 = q0, kg = 0;
+      while (q1 < NC && (long long)(kg + k[q1]) * 2 * nrhs <= xbuf) kg += k[q1++];
+      if (q1 == q0) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
+      if (kg == 0) {
+        q0 = q1;
+        continue;
+      }
+      const int tu = std::max(1, std::min(512, kStage / kg));
+      for (int i0 = 0; i0 < m; i0 += tu) {
+        const int rt = std::min(tu, m - i0);
+        MvTask t{};
+        t.kind = TK_YPART;
+        t.c0 = q0;
+        t.c1 = q1;
+        t.rows = rt;
+        t.x_rows = kg;  // z slots delivered with the task
+        t.data_off = alen;
+        long long cur = alen;
+        for (int q = q0; q < q1; ++q) {
+          t.k[q] = k[q];
+          pack(c->items[mb.item0 + q].u_off + i0, m, rt, k[q], cur);
+          cur += (long long)rt * k[q];
+        }
+        t.data_len = (int)align2(cur - alen);
+        alen += t.data_len;
+        t.z_off = zg;
+        t.out_off = slots;
+        add_rows(mb.row0 + i0, rt, slots);
+        slots += rt;
+        tb.push_back(t);
+      }
+      zg += kg;
+      q0 = q1;
+    }
+  }
+  // partial z slots live after the final ones in one buffer
+  for (MvTask& t : ta)
+    if (t.kind == TK_VCOLS && t.out_off < 0) t.out_off = zfinal + (-t.out_off - 1);
+  for (ZReduce& r : zred) r.src += zfinal;
+  auto by_size = [](const MvTask& a, const MvTask& b) { return a.data_len > b.data_len; };
+  std::stable_sort(ta.begin(), ta.end(), by_size);
+  std::stable_sort(tb.begin(), tb.end(), by_size);
+  std::vector<MvTask> all(ta);
+  all.insert(all.end(), tb.begin(), tb.end());
+  std::vector<LeafEntry> entries;
+  c->p_leaf_ptr.assign(nl + 1, 0);
+  for (int l = 0; l < nl; ++l) {
+    entries.insert(entries.end(), lists[l].begin(), lists[l].end());
+    c->p_leaf_ptr[l + 1] = (int)entries.size();
+  }
+  c->d_sarena.free();
+  c->d_sarena.alloc((size_t)alen + 2);
+  if (!packs.empty()) {
+    DBuf<PackDesc> d_packs;
+    d_packs.upload(packs, c->stream);
+    c->timed("pack", [&] {
+      pack_kernel<<<grid_for(c, ((long long)packs.size() + 7) / 8, 16), 256, 0, c->stream>>>(
+          d_packs.p, (int)packs.size(), c->d_arena.p, c->d_sarena.p);
+    });
+    c->sync();
+    d_packs.free();
+  }
+  c->d_ptasks.upload(all, c->stream);
+  c->d_pentries.upload(entries, c->stream);
+  c->d_pleaf_ptr.upload(c->p_leaf_ptr, c->stream);
+  c->d_zred.upload(zred, c->stream);
+  c->p_nzred = (int)zred.size();
+  c->p_ntasks = (int)all.size();
+  c->p_nz = (int)ta.size();  // pass A = [0, p_nz), pass B = YPART
+  c->p_slots = slots;
+  c->p_zslots = zfinal + zpartial;
+  c->p_arena_len = alen;
+  c->p_xs = xs;
+  c->p_stage = kStage;
+  c->p_xbuf = xbuf;
+  c->p_zbuf = kMaxKTask * 2 * nrhs;
+  c->p_ybuf = 0;
+  c->p_smem = sizeof(double) * ((size_t)kNStage * (kStage + xbuf) + c->p_zbuf);
+  c->p_ctas_per_sm = c->p_smem * 2 + 8192 <= 227 * 1024 ? 2 : 1;
+  c->plan_mode = mode;
+  c->plan_nrhs = nrhs;
+  c->plan_valid = true;
+  c->sync();
+  if (verbose())
+    std::fprintf(stderr, "[hmgpu] plan: tasks=%d (pass A %d, YPART %zu) zreduce=%zu "
+                         "arena=%.3f GB slots=%lld zslots=%lld entries=%zu smem=%zu B "
+                         "ctas/sm=%d\n",
+                 c->p_ntasks, c->p_nz, tb.size(), zred.size(), 8.0 * alen / 1e9, slots,
+                 c->p_zslots, entries.size(), c->p_smem, c->p_ctas_per_sm);
+}
+
+void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
+  const int NOUT = c->NC == 6 ? 3 : 1;
+  c->d_xi.ensure((size_t)c->n_cols * c->p_xs + 2);
+  c->timed("gather", [&] {
+    const long long total = (long long)c->n_cols * c->p_xs;
+    const int grid = grid_for(c, (total + 255) / 256, 16);
+    if (NOUT == 3)
+      gather_stream_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
+                                                          c->n_cols, nrhs, c->p_xs);
+    else
+      gather_stream_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
+                                                          c->n_cols, nrhs, c->p_xs);
+  });
+  c->d_ypart.ensure((size_t)std::max<long long>(1, c->p_slots * NOUT * nrhs));
+  c->d_zpart.ensure((size_t)std::max<long long>(1, c->p_zslots * 2 * nrhs));
+  StreamParams P{};
+  P.arena = c->d_sarena.p;
+  P.dense = c->d_dense.p;
+  P.xi = c->d_xi.p;
+  P.ypart = c->d_ypart.p;
+  P.zpart = c->d_zpart.p;
+  P.zfinal = c->d_zpart.p;
+  P.nrhs = nrhs;
+  P.xs = c->p_xs;
+  P.stage_doubles = c->p_stage;
+  P.xbuf_doubles = c->p_xbuf;
+  P.zbuf_doubles = c->p_zbuf;
+  const int grid = c->sm_count * c->p_ctas_per_sm;
+  auto run = [&](int first, int count, const char* name) {
+    if (count <= 0) return;
+    P.tasks = c->d_ptasks.p + first;
+    P.ntasks = count;
+    const int g = std::min(grid, count);
+    auto go = [&](auto kernel) {
+      CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)c->p_smem));
+      kernel<<<g, 256, c->p_smem, c->stream>>>(P);
+    };
+    c->timed(name, [&] {
+      if (c->NC == 6)
+        nrhs == 1 ? go(hmv_stream_kernel<6, kNStage, 1>) : go(hmv_stream_kernel<6, kNStage, 0>);
+      else
+        nrhs == 1 ? go(hmv_stream_kernel<1, kNStage, 1>) : go(hmv_stream_kernel<1, kNStage, 0>);
+    });
+  };
+  run(0, c->p_nz, "hmv_stream");
+  if (c->p_nzred > 0)
+    c->timed("hmv_zreduce", [&] {
+      zreduce_kernel<<<grid_for(c, (c->p_nzred + 7) / 8, 16), 256, 0, c->stream>>>(
+          c->d_zred.p, c->p_nzred, c->d_zpart.p, c->d_zpart.p, 2 * nrhs);
+    });
+  run(c->p_nz, c->p_ntasks - c->p_nz, "hmv_ypart");
+  c->timed("hmv_reduce", [&] {
+    const int nl = (int)c->leaf_begin.size();
+    const int g = grid_for(c, nl, 16);
+    if (NOUT == 3)
+      hmv_leaf_reduce_kernel<3><<<g, 128, 0, c->stream>>>(
+          c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
+          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+    else
+      hmv_leaf_reduce_kernel<1><<<g, 128, 0, c->stream>>>(
+          c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
+          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+  });
+}
+
 void check_ptr_kind(int ptr_kind) {
   if (ptr_kind != HMGPU_PTR_HOST && ptr_kind != HMGPU_PTR_DEVICE)
     fail(HMGPU_ERR_INVALID, "ptr_kind must be HMGPU_PTR_HOST or HMGPU_PTR_DEVICE");
@@ -851,7 +1172,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
       const long long m = rn[1] - rn[0], n = cn[1] - cn[0];
       if (B[2]) sum_mn += (m + n) * c->NC;
-      else dense_total += align2((long long)c->NC * m * n);
+      else dense_total += m * align2((long long)c->NC * n);
     }
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -897,7 +1218,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       } else {
         c->dense_of_block[b] = (int)c->dblocks.size();
         DenseBlock db{m, n, rn[0], cn[0], c->dense_used};
-        c->dense_used += align2((long long)c->NC * m * n);
+        c->dense_used += (long long)m * align2((long long)c->NC * n);
         c->dblocks.push_back(db);
       }
     }
@@ -960,6 +1281,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     cudaEventDestroy(tn0);
     cudaEventDestroy(tn1);
     build_matvec(c);
+    c->plan_valid = false;
     phase("build_matvec");
     c->assembled = true;
     if (stats) {
@@ -1019,40 +1341,55 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
     }
     if (c->row_begin != 0 || c->row_end != c->n_rows)
       CK(cudaMemsetAsync(dy, 0, ny * sizeof(double), c->stream));
-    gather_x(c, dx, nrhs);
-    c->d_ypart.ensure((size_t)std::max<long long>(1, c->part_rows * NOUT * nrhs));
-    const size_t smem = sizeof(double) * 2 * (size_t)c->kmax * nrhs;
-    if (smem > 200 * 1024) fail(HMGPU_ERR_INVALID, "rank x nrhs too large for matvec");
-    c->timed("hmv_blocks", [&] {
-      const int grid = grid_for(c, c->n_mv, 8);
-      if (c->NC == 6) {
-        if (smem > 48 * 1024)
-          CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
-            c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
-            c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
-      } else {
-        if (smem > 48 * 1024)
-          CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
-            c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
-            c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+    static const bool force_v1 = std::getenv("HMGPU_MATVEC_V1") != nullptr;
+    bool streamed = !force_v1;
+    if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
+      try {
+        build_plan(c, mode, nrhs);
+      } catch (const Fail& f) {
+        if (f.code != HMGPU_ERR_INVALID) throw;
+        streamed = false;  // ranks / widths beyond the stream layout: block sweep
+        c->plan_valid = false;
       }
-    });
-    c->timed("hmv_reduce", [&] {
-      const int nl = (int)c->leaf_begin.size();
-      const int grid = grid_for(c, nl, 16);
-      if (c->NC == 6)
-        hmv_reduce_kernel<3><<<grid, 128, 0, c->stream>>>(
-            c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
-            nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
-      else
-        hmv_reduce_kernel<1><<<grid, 128, 0, c->stream>>>(
-            c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
-            nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
-    });
+    }
+    if (streamed) {
+      launch_stream(c, dx, dy, nrhs);
+    } else {
+      gather_x(c, dx, nrhs);
+      c->d_ypart.ensure((size_t)std::max<long long>(1, c->part_rows * NOUT * nrhs));
+      const size_t smem = sizeof(double) * 2 * (size_t)c->kmax * nrhs;
+      if (smem > 200 * 1024) fail(HMGPU_ERR_INVALID, "rank x nrhs too large for matvec");
+      c->timed("hmv_blocks", [&] {
+        const int grid = grid_for(c, c->n_mv, 8);
+        if (c->NC == 6) {
+          if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
+              c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+              c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+        } else {
+          if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
+              c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+              c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+        }
+      });
+      c->timed("hmv_reduce", [&] {
+        const int nl = (int)c->leaf_begin.size();
+        const int grid = grid_for(c, nl, 16);
+        if (c->NC == 6)
+          hmv_reduce_kernel<3><<<grid, 128, 0, c->stream>>>(
+              c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+              nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+        else
+          hmv_reduce_kernel<1><<<grid, 128, 0, c->stream>>>(
+              c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+              nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+      });
+    }
     if (ptr_kind == HMGPU_PTR_HOST) {
       CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       c->sync();
@@ -1072,6 +1409,7 @@ int hmgpu_promote(hmgpu_ctx* c, int n, const int* comp_block) {
           c->d_items.p, c->d_list.p, (int)ids.size());
     });
     for (int i : ids) c->items[i].kcur = c->items[i].k;
+    c->plan_valid = false;
     c->sync();
   });
 }
@@ -1098,6 +1436,7 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
     run_aca(c, ids, nullptr);
     download_items(c);
     refresh_matvec_ranks(c);
+    c->plan_valid = false;
   });
 }
 
@@ -1206,9 +1545,14 @@ int hmgpu_download_dense(hmgpu_ctx* c, int comp, int block, double* out) {
     const int d = c->dense_of_block[block];
     if (d < 0) fail(HMGPU_ERR_INVALID, "block is low-rank or not owned");
     const DenseBlock& db = c->dblocks[d];
-    const long long mn = (long long)db.m * db.n;
-    CK(cudaMemcpyAsync(out, c->d_dense.p + db.off + comp * mn, sizeof(double) * mn,
+    const long long pitch = align2((long long)db.n * c->NC);
+    std::vector<double> tmp(db.m * pitch);
+    CK(cudaMemcpyAsync(tmp.data(), c->d_dense.p + db.off, sizeof(double) * tmp.size(),
                        cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    for (int i = 0; i < db.m; ++i)  // [i][j][comp] rows -> column-major m x n
+      for (int j = 0; j < db.n; ++j)
+        out[(long long)j * db.m + i] = tmp[i * pitch + (long long)j * c->NC + comp];
     c->sync();
   });
 }
@@ -1241,6 +1585,41 @@ int hmgpu_storage(hmgpu_ctx* c, hmgpu_storage_info* info) {
                          8LL * (c->ndof_cols() + c->ndof_rows());
     info->matvec_flops = flops;
   });
+}
+
+int hmgpu_fp64_peak(int device, double* tflops) {
+  if (!tflops) return HMGPU_ERR_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return HMGPU_ERR_NODEVICE;
+  if (device < 0 || device >= count) return HMGPU_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return HMGPU_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return HMGPU_ERR_OOM;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = sms * 8, iters = 1 << 14;
+  dfma_peak_kernel<<<grid, 256>>>(out, 64, 1.0000001, 1e-9);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    dfma_peak_kernel<<<grid, 256>>>(out, iters, 1.0000001, 1e-9);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    best = std::min(best, ms);
+  }
+  const cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  if (e != cudaSuccess) return HMGPU_ERR_CUDA;
+  const double flops = 2.0 * 8.0 * iters * (double)grid * 256.0;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return HMGPU_OK;
 }
 
 int hmgpu_set_profiling(hmgpu_ctx* c, int on) {

@@ -466,7 +466,8 @@ aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
 // ---------------------------------------------------------------------------
 // near-field fill: one CTA per non-admissible block, all NC components of a
 // pair computed together (they share r and 1/r); layout per block
-// [comp][n][m] (column-major per component, like HBlock::dense)
+// [i][j][comp] (row-major, components interleaved: one block row is one
+// contiguous run of NC*n doubles, the unit the matvec streams)
 struct DenseBlock {
   int m, n, row0, col0;
   long long off;  // doubles into the dense arena
@@ -479,9 +480,10 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
   for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
     const DenseBlock b = blocks[bi];
     const int mn = b.m * b.n;
+    const int pitch = (b.n * NC + 1) & ~1;  // rows padded to 16 bytes
     double* D = dense + b.off;
     for (int p = threadIdx.x; p < mn; p += blockDim.x) {
-      const int i = p % b.m, j = p / b.m;
+      const int i = p / b.n, j = p % b.n;
       if (NC == 6) {
         double e[6];
         if (g.kind == KIND_KELVIN) {
@@ -492,9 +494,9 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
           for (int c = 0; c < 6; ++c) e[c] = v;
         }
 #pragma unroll
-        for (int c = 0; c < 6; ++c) D[(long long)c * mn + p] = e[c];
+        for (int c = 0; c < 6; ++c) D[(long long)i * pitch + 6 * j + c] = e[c];
       } else {
-        D[p] = entry1(g, b.row0 + i, b.col0 + j, 0);
+        D[(long long)i * pitch + j] = entry1(g, b.row0 + i, b.col0 + j, 0);
       }
     }
   }
@@ -542,7 +544,6 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
     const MvBlock b = blocks[order[oi]];
     double* yp = ypart + b.prow * NOUT * nrhs;
     if (b.dense) {
-      const long long mn = (long long)b.m * b.n;
       for (int i = threadIdx.x; i < b.m; i += blockDim.x) {
         for (int q = 0; q < nrhs; ++q) {
           double acc[NOUT];
@@ -552,10 +553,11 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
           for (int c = 0; c < NC; ++c) {
             const int rr = NC == 6 ? c_comp_r[c] : 0;
             const int cc = NC == 6 ? c_comp_c[c] : 0;
-            const double* D = dense + b.dense_off + c * mn;
+            const double* D =
+                dense + b.dense_off + (long long)i * ((b.n * NC + 1) & ~1) + c;
             double s1 = 0.0, s2 = 0.0;
             for (int j = 0; j < b.n; ++j) {
-              const double d = D[(long long)j * b.m + i];
+              const double d = D[(long long)j * NC];
               const double* xj = xi + ((long long)(b.col0 + j) * NOUT) * nrhs + q;
               s1 = fma(d, xj[cc * nrhs], s1);
               if (rr != cc) s2 = fma(d, xj[rr * nrhs], s2);
@@ -690,6 +692,24 @@ __global__ void tail_kernel(const TailTerm* __restrict__ terms, int nterms,
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// DFMA throughput probe (roofline denominator for the fp64 kernels): 8
+// independent FMA chains per thread, the result kept live.
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a,
+                                                        double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // practically never; keeps the chains live
 }
 
 // ---------------------------------------------------------------------------

@@ -2,6 +2,7 @@
 // to status codes here; nothing throws across the ABI.
 
 #include <cstring>
+#include <random>
 #include <memory>
 #include <string>
 
@@ -174,6 +175,22 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
 }
 
 void hmb_mesh_free(hmb_mesh* m) { delete m; }
+
+int hmb_random_vector(long long n, unsigned long long seed, int kind, double* out) {
+  return guard([&] {
+    need(out, "out");
+    std::mt19937_64 gen(seed);
+    if (kind == 0) {  // uniform [-1, 1) (proj/tests/oracles.cpp:415-421)
+      std::uniform_real_distribution<double> dist(-1.0, 1.0);
+      for (long long i = 0; i < n; ++i) out[i] = dist(gen);
+    } else if (kind == 1) {  // standard normal
+      std::normal_distribution<double> dist(0.0, 1.0);
+      for (long long i = 0; i < n; ++i) out[i] = dist(gen);
+    } else {
+      throw hmb::Error("random_vector: kind must be 0 (uniform) or 1 (normal)");
+    }
+  });
+}
 
 int hmb_gauss_rule(int order, int* npts, double* a, double* b, double* w) {
   return guard([&] {

@@ -1,0 +1,13 @@
+"""C2 matvec loop for ncu (development helper)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2205_04752_b200 as hm
+from oracle import oracle as orc
+level = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+mesh = hm.Mesh.icosphere(level)
+h = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+h.assemble(eps=1e-6, beta=0.8)
+x = orc.random_vector(h.cols, 1)
+for it in range(3):
+    y = h.matvec(x)
+print("ok")

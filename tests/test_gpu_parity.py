@@ -89,7 +89,8 @@ def test_c1_matvec_deterministic_and_multi_rhs(c1):
     for q in range(4):
         y = g.matvec(X[:, q])
         assert (y == g.matvec(X[:, q])).all()  # bitwise repeatable
-        assert np.allclose(Y[:, q], y, rtol=1e-14, atol=1e-16 * np.abs(y).max())
+        # same products, different reduction segmentation per nrhs
+        assert np.allclose(Y[:, q], y, rtol=1e-12, atol=1e-14 * np.abs(y).max())
     # linearity
     y01 = g.matvec(2.0 * X[:, 0] - 0.5 * X[:, 1])
     assert rel(y01, 2.0 * Y[:, 0] - 0.5 * Y[:, 1]) < 1e-13
