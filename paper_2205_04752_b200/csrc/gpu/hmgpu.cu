@@ -164,15 +164,12 @@ struct hmgpu_ctx {
   int plan_mode = -1, plan_nrhs = -1;
   int p_ntasks = 0, p_nz = 0;
   long long p_slots = 0, p_zslots = 0, p_arena_len = 0;
-  int p_xs = 0, p_stage = 0, p_xbuf = 0, p_zbuf = 0, p_ybuf = 0;
   size_t p_smem = 0;
-  int p_ctas_per_sm = 1;
-  DBuf<MvTask> d_ptasks;
+  DBuf<WJob> d_pjobs;
+  DBuf<WChunk> d_pchunks;
   DBuf<double> d_sarena, d_zpart;
   DBuf<LeafEntry> d_pentries;
   DBuf<int> d_pleaf_ptr;
-  DBuf<ZReduce> d_zred;
-  int p_nzred = 0;
   std::vector<int> p_leaf_ptr;
 
   // ---- profiling ----
@@ -195,9 +192,8 @@ struct hmgpu_ctx {
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
     d_leaf_ptr.free(); d_leaf_prow.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
-    d_ptasks.free(); d_sarena.free(); d_zpart.free(); d_pentries.free();
-    d_pleaf_ptr.free();
-    d_zred.free();
+    d_pjobs.free(); d_pchunks.free(); d_sarena.free(); d_zpart.free();
+    d_pentries.free(); d_pleaf_ptr.free();
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -606,28 +602,22 @@ void refresh_matvec_ranks(hmgpu_ctx* c) {
 }
 
 
-// ---- streamed matvec plan ----------------------------------------------------
-// Task kinds (hmgpu_stream.cuh): FUSED blocks whose six components fit one
-// stage; otherwise VCOLS column ranges of V_c (row tiles of at most xrows,
-// partials summed by zreduce) and YPART row tiles of all components' U;
-// DENSE row tiles.  Every block row gets exactly one partial row per
-// covering block.
-constexpr int kStage = 3072;   // doubles per stage (24 KB)
-constexpr int kNStage = 3;     // TMA pipeline depth per CTA
-constexpr int kMaxKTask = 256; // z slots of a FUSED task (shared-memory z)
+// ---- streamed matvec plan (warp-private jobs, hmgpu_stream.cuh) -------------
+constexpr int kWarps = 5;      // warps per CTA (one CTA per SM)
+constexpr int kNStage = 3;     // TMA ring depth per warp
+constexpr int kStage = 1536;   // doubles per stage (12 KB: header + data + aux)
+constexpr int kStageData = kStage - 16;  // data + aux capacity after the header
+constexpr int kScratch = 1024; // doubles of per-warp job scratch (x + W)
+constexpr int kMaxKFused = 192;  // scratch: x (256) + W (4 K)
+constexpr int kMaxKSplit = 256;
 
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
+  if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
   const int NC = c->NC;
-  const int NOUT = NC == 6 ? 3 : 1;
-  const int xs = (NOUT == 3 ? 4 : 2) * nrhs;
-  const int xbuf = std::max(512, 64 * xs);
-  const int xrows = xbuf / xs;
-  std::vector<MvTask> ta, tb;
+  std::vector<WJob> ja, jb;
+  std::vector<std::vector<WChunk>> ca, cb;  // chunks per job
   std::vector<PackDesc> packs;
-  std::vector<ZReduce> zred;
-  long long alen = 0, slots = 0, zfinal = 0;
-  std::vector<std::pair<long long, long long>> vcols_parts;  // (task index in ta, partial base)
-  long long zpartial = 0;
+  long long alen = 0, slots = 0, wslots = 0;
   const int nl = (int)c->leaf_begin.size();
   std::vector<std::vector<LeafEntry>> lists(nl);
   auto add_rows = [&](int r_lo, int nrows, long long slot) {
@@ -641,158 +631,192 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       lists[l].push_back(LeafEntry{slot + (lo - r_lo), lo - lb, hi - lb});
     }
   };
-  auto pack = [&](long long src, int ld, int rows, int cols, long long dst) {
-    if (rows > 0 && cols > 0) packs.push_back(PackDesc{src, dst, ld, rows, cols, 0});
+  // packs rows x cols of a column-major source into the arena; returns the offset
+  auto pack = [&](long long src, int ld, int rows, int cols, int trans) {
+    const long long off = alen;
+    if (rows > 0 && cols > 0)
+      packs.push_back(PackDesc{src, alen, ld, trans ? cols : rows, rows, cols, trans, 0});
+    alen += align2((long long)rows * cols);
+    return off;
+  };
+  auto chunk = [](long long src, int len, int src_kind, int aux_kind, long long aux,
+                  int aux_len, int g0, int g1, int part) {
+    WChunk ch{};
+    ch.src = src;
+    ch.len = (int)align2(len);
+    ch.src_kind = src_kind;
+    ch.aux_kind = aux_kind;
+    ch.aux = aux;
+    ch.aux_len = aux_len;
+    ch.g0 = g0;
+    ch.g1 = g1;
+    ch.part = part;
+    return ch;
   };
   for (const MvBlock& mb : c->mvb) {
     const int m = mb.m, n = mb.n;
     if (mb.dense) {
-      const int rowlen = (int)align2((long long)n * NC);
-      if (n > xrows || rowlen > kStage)
-        fail(HMGPU_ERR_INVALID, "near-field block too wide for the streamed matvec");
-      const int tile = std::max(1, std::min(m, kStage / rowlen));
-      for (int r0 = 0; r0 < m; r0 += tile) {
-        const int rt = std::min(tile, m - r0);
-        MvTask t{};
-        t.kind = TK_DENSE;
-        t.c1 = NC;
-        t.rows = rt;
-        t.cols = n;
-        t.src = 1;
-        t.x_rows = n;
-        t.x_col0 = mb.col0;
-        t.data_off = mb.dense_off + (long long)r0 * rowlen;
-        t.data_len = rt * rowlen;
-        t.out_off = slots;
-        add_rows(mb.row0 + r0, rt, slots);
-        slots += rt;
-        ta.push_back(t);
+      if (m > 64 || n > 64)
+        fail(HMGPU_ERR_INVALID, "near-field block larger than 64 for the streamed matvec");
+      const int cp = (int)align2((long long)NC * m);
+      const int cpc = std::max(1, (kStageData - 4 * n) / cp);
+      WJob j{};
+      j.kind = WJ_DENSE;
+      j.m = m;
+      j.n = n;
+      j.ncols = n;
+      j.out = slots;
+      std::vector<WChunk> chs;
+      for (int g0 = 0; g0 < n; g0 += cpc) {
+        const int g1 = std::min(n, g0 + cpc);
+        chs.push_back(chunk(mb.dense_off + (long long)g0 * cp, (g1 - g0) * cp, 1,
+                            g0 == 0 ? WA_X : WA_NONE, mb.col0, g0 == 0 ? n : 0, g0, g1, 0));
       }
+      add_rows(mb.row0, m, slots);
+      slots += m;
+      ja.push_back(j);
+      ca.push_back(chs);
       continue;
     }
     int k[6] = {0, 0, 0, 0, 0, 0};
-    long long total = 0;
-    int ksum = 0;
+    int K = 0;
     for (int q = 0; q < NC; ++q) {
       const Item& it = c->items[mb.item0 + q];
       k[q] = mode ? it.k : it.kcur;
-      total += (long long)k[q] * (m + n);
-      ksum += k[q];
+      K += k[q];
     }
-    if (ksum == 0) continue;
-    if (n <= xrows && total <= kStage && ksum <= kMaxKTask) {
-      MvTask t{};
-      t.kind = TK_FUSED;
-      t.c1 = NC;
-      t.rows = m;
-      t.cols = n;
-      t.x_rows = n;
-      t.x_col0 = mb.col0;
-      t.data_off = alen;
-      long long cur = alen;
-      for (int q = 0; q < NC; ++q) {
-        t.k[q] = k[q];
-        pack(c->items[mb.item0 + q].v_off, n, n, k[q], cur);
-        cur += (long long)n * k[q];
+    if (K == 0) continue;
+    int kp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < 6; ++q) kp[q + 1] = kp[q] + (q < NC ? k[q] : 0);
+    kp[7] = kp[6];
+    if (m <= 64 && n <= 64 && K <= kMaxKFused) {
+      WJob j{};
+      j.kind = WJ_FUSED;
+      j.m = m;
+      j.n = n;
+      j.ncols = K;
+      j.out = slots;
+      std::copy(kp, kp + 8, j.kp);
+      std::vector<WChunk> chs;
+      // V part: row-major [j][g] chunks over whole columns, x rides along
+      const int vcpc = std::max(1, (kStageData - 4 * n) / n);
+      for (int g0 = 0; g0 < K; g0 += vcpc) {
+        const int g1 = std::min(K, g0 + vcpc);
+        // the chunk's columns may span components: pack per component piece
+        const long long off = alen;
+        const int w = g1 - g0;  // row length of the row-major [j][g] tile
+        for (int q = 0; q < NC; ++q) {
+          const int a = std::max(g0, kp[q]), b = std::min(g1, kp[q + 1]);
+          if (a >= b) continue;
+          packs.push_back(PackDesc{c->items[mb.item0 + q].v_off + (long long)(a - kp[q]) * n,
+                                   off + (a - g0), n, w, n, b - a, 1, 0});
+        }
+        alen += align2((long long)n * w);
+        chs.push_back(chunk(off, n * w, 0, g0 == 0 ? WA_X : WA_NONE, mb.col0, g0 == 0 ? n : 0,
+                            g0, g1, 0));
       }
-      for (int q = 0; q < NC; ++q) {
-        pack(c->items[mb.item0 + q].u_off, m, m, k[q], cur);
-        cur += (long long)m * k[q];
+      // U part: column-major [g][i] chunks
+      const int ucpc = std::max(1, kStageData / m);
+      for (int g0 = 0; g0 < K; g0 += ucpc) {
+        const int g1 = std::min(K, g0 + ucpc);
+        const long long off = alen;
+        for (int q = 0; q < NC; ++q) {
+          const int a = std::max(g0, kp[q]), b = std::min(g1, kp[q + 1]);
+          if (a >= b) continue;
+          packs.push_back(PackDesc{c->items[mb.item0 + q].u_off + (long long)(a - kp[q]) * m,
+                                   off + (long long)(a - g0) * m, m, m, m, b - a, 0, 0});
+        }
+        alen += align2((long long)m * (g1 - g0));
+        chs.push_back(chunk(off, m * (g1 - g0), 0, WA_NONE, 0, 0, g0, g1, 1));
       }
-      t.data_len = (int)align2(cur - alen);
-      alen += t.data_len;
-      t.out_off = slots;
       add_rows(mb.row0, m, slots);
       slots += m;
-      ta.push_back(t);
+      ja.push_back(j);
+      ca.push_back(chs);
       continue;
     }
-    // split block: V column ranges -> z (global), then U row tiles
-    const long long zoff = zfinal;
-    zfinal += ksum;
-    long long coff = 0;
+    if (K > kMaxKSplit) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
+    // split block: VSPLIT column groups of each component -> W (global)
+    const long long wbase = wslots;
+    wslots += K;
     for (int q = 0; q < NC; ++q) {
-      const int kq = k[q];
-      if (kq == 0) continue;
       const Item& it = c->items[mb.item0 + q];
-      const int nt = (n + xrows - 1) / xrows;
-      const int trows = (n + nt - 1) / nt;
-      const long long pbase = zpartial;
-      if (nt > 1) zpartial += (long long)nt * kq;
-      for (int tt = 0; tt < nt; ++tt) {
-        const int j0 = tt * trows, rt = std::min(trows, n - j0);
-        const int cl = std::max(1, kStage / std::max(rt, 1));
-        for (int l0 = 0; l0 < kq; l0 += cl) {
-          const int lc = std::min(cl, kq - l0);
-          MvTask t{};
-          t.kind = TK_VCOLS;
-          t.c0 = q;
-          t.c1 = q + 1;
-          t.k[q] = lc;
-          t.l0 = l0;
-          t.rows = rt;
-          t.cols = lc;
-          t.x_rows = rt;
-          t.x_col0 = mb.col0 + j0;
-          t.data_off = alen;
-          pack(it.v_off + j0 + (long long)l0 * n, n, rt, lc, alen);
-          t.data_len = (int)align2((long long)rt * lc);
-          alen += t.data_len;
-          // final slot, or a partial slot (rebased after zfinal is known)
-          t.out_off = nt == 1 ? zoff + coff + l0 : -(pbase + (long long)tt * kq + l0) - 1;
-          ta.push_back(t);
+      for (int l0 = 0; l0 < k[q]; l0 += 32) {
+        const int nc = std::min(32, k[q] - l0);
+        const int rpc = std::max(1, kStageData / (nc + 4));
+        WJob j{};
+        j.kind = WJ_VSPLIT;
+        j.n = n;
+        j.ncols = nc;
+        j.comp = q;
+        j.out = wbase + kp[q] + l0;
+        std::vector<WChunk> chs;
+        for (int r0 = 0; r0 < n; r0 += rpc) {
+          const int r1 = std::min(n, r0 + rpc);
+          const long long off =
+              pack(it.v_off + r0 + (long long)l0 * n, n, r1 - r0, nc, 1);  // row-major
+          chs.push_back(chunk(off, (r1 - r0) * nc, 0, WA_X, mb.col0 + r0, r1 - r0, r0, r1, 0));
         }
+        ja.push_back(j);
+        ca.push_back(chs);
       }
-      if (nt > 1) zred.push_back(ZReduce{zoff + coff, pbase, kq, nt, kq, 0});
-      coff += kq;
     }
-    // U row tiles over component groups whose z slots fit the x area
-    long long zg = zoff;
-    for (int q0 = 0; q0 < NC;) {
-      int q1 = q0, kg = 0;
-      while (q1 < NC && (long long)(kg + k[q1]) * 2 * nrhs <= xbuf) kg += k[q1++];
-      if (q1 == q0) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
-      if (kg == 0) {
-        q0 = q1;
-        continue;
-      }
-      const int tu = std::max(1, std::min(512, kStage / kg));
-      for (int i0 = 0; i0 < m; i0 += tu) {
-        const int rt = std::min(tu, m - i0);
-        MvTask t{};
-        t.kind = TK_YPART;
-        t.c0 = q0;
-        t.c1 = q1;
-        t.rows = rt;
-        t.x_rows = kg;  // z slots delivered with the task
-        t.data_off = alen;
-        long long cur = alen;
-        for (int q = q0; q < q1; ++q) {
-          t.k[q] = k[q];
-          pack(c->items[mb.item0 + q].u_off + i0, m, rt, k[q], cur);
-          cur += (long long)rt * k[q];
+    // USPLIT row tiles of all components
+    for (int i0 = 0; i0 < m; i0 += 64) {
+      const int rt = std::min(64, m - i0);
+      WJob j{};
+      j.kind = WJ_USPLIT;
+      j.m = rt;
+      j.ncols = K;
+      j.out = slots;
+      std::copy(kp, kp + 8, j.kp);
+      std::vector<WChunk> chs;
+      const int first_cols = std::max(1, (kStageData - 4 * K) / rt);
+      const int cols = std::max(1, kStageData / rt);
+      for (int g0 = 0; g0 < K;) {
+        const int g1 = std::min(K, g0 + (g0 == 0 ? first_cols : cols));
+        const long long off = alen;
+        for (int q = 0; q < NC; ++q) {
+          const int a = std::max(g0, kp[q]), b = std::min(g1, kp[q + 1]);
+          if (a >= b) continue;
+          packs.push_back(PackDesc{c->items[mb.item0 + q].u_off + i0 +
+                                       (long long)(a - kp[q]) * m,
+                                   off + (long long)(a - g0) * rt, m, rt, rt, b - a, 0, 0});
         }
-        t.data_len = (int)align2(cur - alen);
-        alen += t.data_len;
-        t.z_off = zg;
-        t.out_off = slots;
-        add_rows(mb.row0 + i0, rt, slots);
-        slots += rt;
-        tb.push_back(t);
+        alen += align2((long long)rt * (g1 - g0));
+        chs.push_back(chunk(off, rt * (g1 - g0), 0, g0 == 0 ? WA_W : WA_NONE, wbase,
+                            g0 == 0 ? K : 0, g0, g1, 1));
+        g0 = g1;
       }
-      zg += kg;
-      q0 = q1;
+      add_rows(mb.row0 + i0, rt, slots);
+      slots += rt;
+      jb.push_back(j);
+      cb.push_back(chs);
     }
   }
-  // partial z slots live after the final ones in one buffer
-  for (MvTask& t : ta)
-    if (t.kind == TK_VCOLS && t.out_off < 0) t.out_off = zfinal + (-t.out_off - 1);
-  for (ZReduce& r : zred) r.src += zfinal;
-  auto by_size = [](const MvTask& a, const MvTask& b) { return a.data_len > b.data_len; };
-  std::stable_sort(ta.begin(), ta.end(), by_size);
-  std::stable_sort(tb.begin(), tb.end(), by_size);
-  std::vector<MvTask> all(ta);
-  all.insert(all.end(), tb.begin(), tb.end());
+  // order each pass by size (largest first) and lay out the chunk table
+  auto order = [](const std::vector<std::vector<WChunk>>& cs) {
+    std::vector<int> o(cs.size());
+    std::iota(o.begin(), o.end(), 0);
+    std::vector<long long> sz(cs.size(), 0);
+    for (size_t i = 0; i < cs.size(); ++i)
+      for (const WChunk& ch : cs[i]) sz[i] += ch.len + 4LL * ch.aux_len;
+    std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return sz[a] > sz[b]; });
+    return o;
+  };
+  std::vector<WJob> jobs;
+  std::vector<WChunk> chunks;
+  for (int pass = 0; pass < 2; ++pass) {
+    auto& J = pass == 0 ? ja : jb;
+    auto& C = pass == 0 ? ca : cb;
+    for (int idx : order(C)) {
+      WJob j = J[idx];
+      j.chunk0 = (int)chunks.size();
+      j.nchunks = (int)C[idx].size();
+      chunks.insert(chunks.end(), C[idx].begin(), C[idx].end());
+      jobs.push_back(j);
+    }
+  }
   std::vector<LeafEntry> entries;
   c->p_leaf_ptr.assign(nl + 1, 0);
   for (int l = 0; l < nl; ++l) {
@@ -811,86 +835,69 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     c->sync();
     d_packs.free();
   }
-  c->d_ptasks.upload(all, c->stream);
+  c->d_pjobs.upload(jobs, c->stream);
+  c->d_pchunks.upload(chunks, c->stream);
   c->d_pentries.upload(entries, c->stream);
   c->d_pleaf_ptr.upload(c->p_leaf_ptr, c->stream);
-  c->d_zred.upload(zred, c->stream);
-  c->p_nzred = (int)zred.size();
-  c->p_ntasks = (int)all.size();
-  c->p_nz = (int)ta.size();  // pass A = [0, p_nz), pass B = YPART
+  c->p_ntasks = (int)jobs.size();
+  c->p_nz = (int)ja.size();  // pass A = [0, p_nz), pass B = USPLIT
   c->p_slots = slots;
-  c->p_zslots = zfinal + zpartial;
+  c->p_zslots = wslots;
   c->p_arena_len = alen;
-  c->p_xs = xs;
-  c->p_stage = kStage;
-  c->p_xbuf = xbuf;
-  c->p_zbuf = kMaxKTask * 2 * nrhs;
-  c->p_ybuf = 0;
-  c->p_smem = sizeof(double) * ((size_t)kNStage * (kStage + xbuf) + c->p_zbuf);
-  c->p_ctas_per_sm = c->p_smem * 2 + 8192 <= 227 * 1024 ? 2 : 1;
+  c->p_smem = sizeof(double) * (size_t)kWarps * (kNStage * kStage + kScratch);
   c->plan_mode = mode;
   c->plan_nrhs = nrhs;
   c->plan_valid = true;
   c->sync();
   if (verbose())
-    std::fprintf(stderr, "[hmgpu] plan: tasks=%d (pass A %d, YPART %zu) zreduce=%zu "
-                         "arena=%.3f GB slots=%lld zslots=%lld entries=%zu smem=%zu B "
-                         "ctas/sm=%d\n",
-                 c->p_ntasks, c->p_nz, tb.size(), zred.size(), 8.0 * alen / 1e9, slots,
-                 c->p_zslots, entries.size(), c->p_smem, c->p_ctas_per_sm);
+    std::fprintf(stderr, "[hmgpu] plan: jobs=%d (pass A %zu, USPLIT %zu) chunks=%zu "
+                         "arena=%.3f GB slots=%lld wslots=%lld entries=%zu smem=%zu B\n",
+                 c->p_ntasks, ja.size(), jb.size(), chunks.size(), 8.0 * alen / 1e9, slots,
+                 wslots, entries.size(), c->p_smem);
 }
 
 void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
+  (void)nrhs;
   const int NOUT = c->NC == 6 ? 3 : 1;
-  c->d_xi.ensure((size_t)c->n_cols * c->p_xs + 2);
+  c->d_xi.ensure((size_t)c->n_cols * 4 + 2);
   c->timed("gather", [&] {
-    const long long total = (long long)c->n_cols * c->p_xs;
+    const long long total = 4LL * c->n_cols;
     const int grid = grid_for(c, (total + 255) / 256, 16);
     if (NOUT == 3)
-      gather_stream_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
-                                                          c->n_cols, nrhs, c->p_xs);
+      gather4_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols);
     else
-      gather_stream_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p,
-                                                          c->n_cols, nrhs, c->p_xs);
+      gather4_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols);
   });
-  c->d_ypart.ensure((size_t)std::max<long long>(1, c->p_slots * NOUT * nrhs));
-  c->d_zpart.ensure((size_t)std::max<long long>(1, c->p_zslots * 2 * nrhs));
-  StreamParams P{};
+  c->d_ypart.ensure((size_t)std::max<long long>(1, c->p_slots * NOUT));
+  c->d_zpart.ensure((size_t)std::max<long long>(1, c->p_zslots * 4));
+  WarpStreamParams P{};
+  P.chunks = c->d_pchunks.p;
   P.arena = c->d_sarena.p;
   P.dense = c->d_dense.p;
   P.xi = c->d_xi.p;
+  P.wout = c->d_zpart.p;
+  P.win = c->d_zpart.p;
   P.ypart = c->d_ypart.p;
-  P.zpart = c->d_zpart.p;
-  P.zfinal = c->d_zpart.p;
-  P.nrhs = nrhs;
-  P.xs = c->p_xs;
-  P.stage_doubles = c->p_stage;
-  P.xbuf_doubles = c->p_xbuf;
-  P.zbuf_doubles = c->p_zbuf;
-  const int grid = c->sm_count * c->p_ctas_per_sm;
+  P.stage = kStage;
+  P.scratch = kScratch;
   auto run = [&](int first, int count, const char* name) {
     if (count <= 0) return;
-    P.tasks = c->d_ptasks.p + first;
-    P.ntasks = count;
-    const int g = std::min(grid, count);
+    P.jobs = c->d_pjobs.p + first;
+    P.njobs = count;
+    const int g = std::min(c->sm_count, (count + kWarps - 1) / kWarps);
     auto go = [&](auto kernel) {
       CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->p_smem));
-      kernel<<<g, 256, c->p_smem, c->stream>>>(P);
+      kernel<<<g, kWarps * 32, c->p_smem, c->stream>>>(P);
     };
     c->timed(name, [&] {
       if (c->NC == 6)
-        nrhs == 1 ? go(hmv_stream_kernel<6, kNStage, 1>) : go(hmv_stream_kernel<6, kNStage, 0>);
+        go(hmv_warp_kernel<6, kNStage, kWarps>);
       else
-        nrhs == 1 ? go(hmv_stream_kernel<1, kNStage, 1>) : go(hmv_stream_kernel<1, kNStage, 0>);
+        go(hmv_warp_kernel<1, kNStage, kWarps>);
     });
   };
   run(0, c->p_nz, "hmv_stream");
-  if (c->p_nzred > 0)
-    c->timed("hmv_zreduce", [&] {
-      zreduce_kernel<<<grid_for(c, (c->p_nzred + 7) / 8, 16), 256, 0, c->stream>>>(
-          c->d_zred.p, c->p_nzred, c->d_zpart.p, c->d_zpart.p, 2 * nrhs);
-    });
   run(c->p_nz, c->p_ntasks - c->p_nz, "hmv_ypart");
   c->timed("hmv_reduce", [&] {
     const int nl = (int)c->leaf_begin.size();
@@ -898,11 +905,11 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     if (NOUT == 3)
       hmv_leaf_reduce_kernel<3><<<g, 128, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
-          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
     else
       hmv_leaf_reduce_kernel<1><<<g, 128, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
-          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
+          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
   });
 }
 
@@ -1172,7 +1179,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
       const long long m = rn[1] - rn[0], n = cn[1] - cn[0];
       if (B[2]) sum_mn += (m + n) * c->NC;
-      else dense_total += m * align2((long long)c->NC * n);
+      else dense_total += n * align2((long long)c->NC * m);
     }
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1218,7 +1225,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       } else {
         c->dense_of_block[b] = (int)c->dblocks.size();
         DenseBlock db{m, n, rn[0], cn[0], c->dense_used};
-        c->dense_used += (long long)m * align2((long long)c->NC * n);
+        c->dense_used += (long long)n * align2((long long)c->NC * m);
         c->dblocks.push_back(db);
       }
     }
@@ -1545,14 +1552,14 @@ int hmgpu_download_dense(hmgpu_ctx* c, int comp, int block, double* out) {
     const int d = c->dense_of_block[block];
     if (d < 0) fail(HMGPU_ERR_INVALID, "block is low-rank or not owned");
     const DenseBlock& db = c->dblocks[d];
-    const long long pitch = align2((long long)db.n * c->NC);
-    std::vector<double> tmp(db.m * pitch);
+    const long long cp = align2((long long)db.m * c->NC);
+    std::vector<double> tmp(db.n * cp);
     CK(cudaMemcpyAsync(tmp.data(), c->d_dense.p + db.off, sizeof(double) * tmp.size(),
                        cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-    for (int i = 0; i < db.m; ++i)  // [i][j][comp] rows -> column-major m x n
-      for (int j = 0; j < db.n; ++j)
-        out[(long long)j * db.m + i] = tmp[i * pitch + (long long)j * c->NC + comp];
+    for (int j = 0; j < db.n; ++j)  // [j][comp][i] -> column-major m x n
+      for (int i = 0; i < db.m; ++i)
+        out[(long long)j * db.m + i] = tmp[j * cp + (long long)comp * db.m + i];
     c->sync();
   });
 }

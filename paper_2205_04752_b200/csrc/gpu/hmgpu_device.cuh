@@ -466,8 +466,9 @@ aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
 // ---------------------------------------------------------------------------
 // near-field fill: one CTA per non-admissible block, all NC components of a
 // pair computed together (they share r and 1/r); layout per block
-// [i][j][comp] (row-major, components interleaved: one block row is one
-// contiguous run of NC*n doubles, the unit the matvec streams)
+// [j][comp][i] with column pitch align2(NC*m): a column range of the block
+// is one contiguous run (the unit the matvec streams) and rows are the
+// fastest index (lane = row, conflict-free in shared memory)
 struct DenseBlock {
   int m, n, row0, col0;
   long long off;  // doubles into the dense arena
@@ -480,10 +481,10 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
   for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
     const DenseBlock b = blocks[bi];
     const int mn = b.m * b.n;
-    const int pitch = (b.n * NC + 1) & ~1;  // rows padded to 16 bytes
+    const int cp = (b.m * NC + 1) & ~1;  // column pitch, 16-byte multiple
     double* D = dense + b.off;
     for (int p = threadIdx.x; p < mn; p += blockDim.x) {
-      const int i = p / b.n, j = p % b.n;
+      const int i = p % b.m, j = p / b.m;
       if (NC == 6) {
         double e[6];
         if (g.kind == KIND_KELVIN) {
@@ -494,9 +495,9 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
           for (int c = 0; c < 6; ++c) e[c] = v;
         }
 #pragma unroll
-        for (int c = 0; c < 6; ++c) D[(long long)i * pitch + 6 * j + c] = e[c];
+        for (int c = 0; c < 6; ++c) D[(long long)j * cp + c * b.m + i] = e[c];
       } else {
-        D[(long long)i * pitch + j] = entry1(g, b.row0 + i, b.col0 + j, 0);
+        D[(long long)j * cp + i] = entry1(g, b.row0 + i, b.col0 + j, 0);
       }
     }
   }
@@ -553,11 +554,11 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
           for (int c = 0; c < NC; ++c) {
             const int rr = NC == 6 ? c_comp_r[c] : 0;
             const int cc = NC == 6 ? c_comp_c[c] : 0;
-            const double* D =
-                dense + b.dense_off + (long long)i * ((b.n * NC + 1) & ~1) + c;
+            const long long cp = (b.m * NC + 1) & ~1;
+            const double* D = dense + b.dense_off + (long long)c * b.m + i;
             double s1 = 0.0, s2 = 0.0;
             for (int j = 0; j < b.n; ++j) {
-              const double d = D[(long long)j * NC];
+              const double d = D[j * cp];
               const double* xj = xi + ((long long)(b.col0 + j) * NOUT) * nrhs + q;
               s1 = fma(d, xj[cc * nrhs], s1);
               if (rr != cc) s2 = fma(d, xj[rr * nrhs], s2);

@@ -1,20 +1,30 @@
-// Streamed H-matvec (the bandwidth-bound sweep).
+// Streamed H-matvec (the bandwidth-bound sweep), warp-private pipelines.
 //
-// The host packs the current-rank factors into a "stream arena" laid out in
-// task order: every task's data (the V and/or U factors of a block and a
-// group of Kelvin components, or a row tile of a dense near-field block) is
-// ONE contiguous, 16-byte aligned run.  A persistent CTA double-buffers
-// tasks in shared memory: one elected thread issues a TMA bulk copy
-// (cp.async.bulk + mbarrier complete_tx) of task t+1 and of its x segment
-// while all warps compute task t from shared memory.  Every task writes a
-// partial result for its rows; a per-leaf pass sums the partials of all
-// tasks covering a leaf in a fixed order (deterministic, no atomics) and
-// scatters to external order.
+// The host packs the current-rank factors into a "stream arena" in job
+// order.  A job is processed by ONE warp; its data is a sequence of chunks,
+// each one contiguous, 16-byte aligned run that a lane-0 TMA bulk copy
+// (cp.async.bulk + mbarrier complete_tx) brings into the warp's private
+// NS-deep ring in shared memory while the warp computes the previous chunk.
+// No block-level barriers: warps only __syncwarp.
+//
+// Job kinds (one partial output row slot per block row):
+//   FUSED  low-rank block with m, n <= 64: V part packed row-major
+//          [j][g] (lane = column g: conflict-free), x with the first chunk;
+//          per column the three dot products f_s = V_g . x_s give the
+//          weights W[g][r] = (R==r) f_C + (C==r, R!=C) f_R; U part packed
+//          column-major [g][i] (lane = row i): y_r += U[i,g] W[g][r]
+//   VSPLIT up to 32 columns of one component of a large block, all rows
+//          streamed in row chunks (x rows with each chunk); W to global
+//   USPLIT a <= 64-row tile of all components' U of a large block; W of
+//          the block from global with the first chunk
+//   DENSE  a near-field block ([j][c][i] layout), m <= 64, x with chunk 0
+// A per-leaf pass sums the partial rows of all blocks covering a leaf in a
+// fixed order (deterministic, no atomics) and scatters to external order.
 //
 // Reference: HMatrix::matvec (proj/src/hmatrix.cpp:22-45) over the six
 // component H-matrices of the 3x3 Kelvin grid (BlockGrid matvec,
-// proj/src/expr.cpp:197-215); an off-diagonal component factor is read once
-// and applied to both x_c and x_r (cells (r,c) and (c,r)).
+// proj/src/expr.cpp:197-215); each off-diagonal component factor is read
+// once and applied to both x_c and x_r.
 #pragma once
 
 #include <cstdint>
@@ -22,47 +32,46 @@
 
 namespace hmgpu {
 
-enum { TK_FUSED = 0, TK_VCOLS = 1, TK_YPART = 2, TK_DENSE = 3 };
+enum { WJ_FUSED = 0, WJ_VSPLIT = 1, WJ_USPLIT = 2, WJ_DENSE = 3 };
 
-// One streamed task: its data is one contiguous run of the stream arena
-// (FUSED, VCOLS, YPART) or a row tile of a dense block (DENSE).
-//   FUSED  [V_c (n x k_c) | U_c (m x k_c)] for c in [c0,c1): z in shared
-//          memory, then the block rows of y (one partial row slot each)
-//   VCOLS  columns [l0, l1) of V_c restricted to a row tile: z slots
-//          (final, or per-tile partials summed by zreduce_kernel)
-//   YPART  a row tile of [U_c (rows x k_c)] for all c, z from global
-//   DENSE  a row tile of the [i][j][comp] near-field block
-struct __align__(16) MvTask {
+struct __align__(16) WJob {
   int kind;
-  int c0, c1;          // component range [c0, c1)
-  int rows;            // FUSED: m; VCOLS: V tile rows; YPART/DENSE: tile rows
-  int cols;            // FUSED/DENSE: n (block columns); VCOLS: l1 - l0
-  int src;             // 0: stream arena, 1: dense arena
-  int x_rows;          // rows of the x segment (0: none); YPART: z slots
-  int x_col0;          // first internal column of the x segment
-  long long data_off;  // doubles into the source arena
-  long long out_off;   // FUSED/YPART/DENSE: partial-row slot; VCOLS: z slot
-  long long z_off;     // YPART: first z slot of the block (comp-major)
-  int data_len;        // doubles (even)
-  int l0;              // VCOLS: first column
-  int k[6];            // rank per component (0 outside [c0, c1))
-  int pad[2];
+  int m;           // rows of the output tile (FUSED/USPLIT/DENSE); VSPLIT: 0
+  int n;           // FUSED/DENSE: block columns; VSPLIT: rows of V
+  int ncols;       // FUSED/USPLIT: K = sum k_c; VSPLIT: columns (<= 32); DENSE: n
+  int chunk0, nchunks;
+  int comp;        // VSPLIT: component of its columns
+  int pad0;
+  long long out;   // FUSED/USPLIT/DENSE: partial row slot; VSPLIT: W slot of column 0
+  int kp[8];       // FUSED/USPLIT: component prefix sums of the K columns
 };
-static_assert(sizeof(MvTask) % 16 == 0, "MvTask layout");
+static_assert(sizeof(WJob) == 80, "WJob layout");
 
-struct ZReduce {  // zfinal[dst + e] = sum_t zpart[src + t*stride + e], e < len
-  long long dst, src;
-  int len, tiles, stride, pad;
+enum { WA_NONE = 0, WA_X = 1, WA_W = 2 };
+
+struct __align__(16) WChunk {
+  long long src;   // doubles into the arena (src_kind 0) or the dense arena (1)
+  long long aux;   // WA_X: internal column of x; WA_W: W slot
+  int len;         // doubles of data (even)
+  int src_kind;
+  int aux_kind;
+  int aux_len;     // rows (WA_X) or columns (WA_W), 4 doubles each
+  int g0, g1;      // column range (FUSED V/U part, USPLIT, DENSE) or row range (VSPLIT)
+  int part;        // FUSED: 0 = V part, 1 = U part
+  int pad;
 };
+static_assert(sizeof(WChunk) == 48, "WChunk layout");
 
 struct LeafEntry {
-  long long slot;  // partial-row slot of the task row that maps to leaf row `lo`
+  long long slot;  // partial-row slot of the job row that maps to leaf row `lo`
   int lo, hi;      // covered leaf rows [lo, hi) (relative to the leaf begin)
 };
 
-struct PackDesc {  // dst[l*rows + i] = src[l*ld + i], i < rows, l < cols
+// dst = pack of src (column-major, leading dimension ld) rows x cols:
+// trans = 0: column-major dst[l*dld + i]; trans = 1: row-major dst[i*dld + l]
+struct PackDesc {
   long long src, dst;
-  int ld, rows, cols, pad;
+  int ld, dld, rows, cols, trans, pad;
 };
 
 // ---------------------------------------------------------------------------
@@ -93,7 +102,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// TMA bulk copy global -> shared, completion signalled on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -104,286 +112,363 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ---------------------------------------------------------------------------
-// Launch-wide constants of one streamed matvec.
-struct StreamParams {
-  const MvTask* tasks;
-  int ntasks;
-  int* counter;
-  const double* arena;    // stream arena (packed current-rank factors)
-  const double* dense;    // near-field arena ([i][j][comp] per block)
-  const double* xi;       // gathered x, XS doubles per internal column
-  double* ypart;          // partial rows: NOUT * nrhs doubles per slot
-  double* zpart;          // z slots written by VCOLS (2 * nrhs doubles each)
-  const double* zfinal;   // z slots read by YPART
-  int nrhs;
-  int xs;                 // doubles per x column (4*nrhs or 2*nrhs)
-  int stage_doubles;      // data capacity of one stage
-  int xbuf_doubles;       // x capacity of one stage
-  int zbuf_doubles;       // z buffer (FUSED / YPART)
-  int part_doubles;       // segment partial sums (<= blockDim)
+struct WarpStreamParams {
+  const WJob* jobs;
+  int njobs;
+  const WChunk* chunks;
+  const double* arena;   // packed factors
+  const double* dense;   // near-field blocks, [j][c][i] per block
+  const double* xi;      // gathered x, 4 doubles per internal column (x, y, z, 0)
+  double* wout;          // W slots written by VSPLIT (4 doubles each)
+  const double* win;     // W slots read by USPLIT
+  double* ypart;         // partial rows, 3 doubles each (1 for scalar kernels)
+  int stage;             // doubles per stage (data + aux)
+  int scratch;           // doubles of per-warp job scratch
 };
 
 template <int NC>
-__device__ __forceinline__ int comp_r(int c) {
-  return NC == 6 ? c_comp_r[c] : 0;
-}
-template <int NC>
-__device__ __forceinline__ int comp_c(int c) {
-  return NC == 6 ? c_comp_c[c] : 0;
+struct Comp {  // (R, C) of component c of the symmetric 3x3 grid
+  __device__ static __forceinline__ int r(int c) { return NC == 6 ? c_comp_r[c] : 0; }
+  __device__ static __forceinline__ int col(int c) { return NC == 6 ? c_comp_c[c] : 0; }
+};
+
+// component of column g from the prefix sums kp[0..6]
+__device__ __forceinline__ int comp_of_col(const int* kp, int g) {
+  return (g >= kp[1]) + (g >= kp[2]) + (g >= kp[3]) + (g >= kp[4]) + (g >= kp[5]);
 }
 
-// component index of the symmetric pair (r, s)
+// W[g][r] from the three dot products f_s of a column of component c
 template <int NC>
-__device__ __forceinline__ int comp_of(int r, int s) {
-  if (NC == 1) return 0;
-  const int lo = r < s ? r : s, hi = r < s ? s : r;
-  return lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+__device__ __forceinline__ void weights(int c, double f0, double f1, double f2, double* w) {
+  if (NC == 1) {
+    w[0] = f0;
+    w[1] = w[2] = w[3] = 0.0;
+    return;
+  }
+  const int R = Comp<NC>::r(c), C = Comp<NC>::col(c);
+  const double fC = C == 0 ? f0 : (C == 1 ? f1 : f2);
+  const double fR = R == 0 ? f0 : (R == 1 ? f1 : f2);
+  const bool off = R != C;
+  w[0] = (R == 0 ? fC : 0.0) + (off && C == 0 ? fR : 0.0);
+  w[1] = (R == 1 ? fC : 0.0) + (off && C == 1 ? fR : 0.0);
+  w[2] = (R == 2 ? fC : 0.0) + (off && C == 2 ? fR : 0.0);
+  w[3] = 0.0;
 }
 
-// lanes per unit: a power of two T = 2^lg <= 32 with units * T <= blockDim
-__device__ __forceinline__ int lanes_log2(int units, int max_len) {
-  const int a = (int)blockDim.x / max(units, 1);
-  const int m = min(min(a, max_len >> 2), 32);
-  return m >= 1 ? 31 - __clz(m) : 0;
-}
-// sum over T = 2^lg adjacent lanes; uniform control flow (all lanes shuffle)
-__device__ __forceinline__ double group_sum(double v, int T) {
+// f_s += sum_j V[j][col] x_s[j] over rows [0, nrows) of a row-major chunk
+// (row length rl); x rows at xs (4 doubles per row)
+template <int NC>
+__device__ __forceinline__ void vdots(const double* V, int rl, int nrows, const double* xs,
+                                      int col, double& f0, double& f1, double& f2) {
+  // four independent accumulator sets (rows j mod 4) for ILP
+  double a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
+  int j = 0;
+  for (; j + 3 < nrows; j += 4) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double other = __shfl_xor_sync(0xffffffffu, v, o);
-    if (o < T) v += other;
-  }
-  return v;
-}
-
-// z[p*2*NR + o*NR + q] = sum_j V_c[j,l] x_{o ? R : C}[j][q] for the (c, l)
-// pairs p of the task in component order.  T = 2^lg adjacent lanes share one
-// (p, o, q) unit over strided j and combine with shuffles.  NR = nrhs when
-// known at compile time (1), else 0 and `nrhs` is used.
-template <int NC, int NR>
-__device__ void stream_zdots(const MvTask& t, const double* V, int vrows, int ld,
-                             const double* xs, int XS, int nrhs_rt, double* zout) {
-  const int nrhs = NR > 0 ? NR : nrhs_rt;
-  // component prefix sums in registers (no local-memory array)
-  const int k0 = NC == 6 && t.c0 <= 0 && t.c1 > 0 ? t.k[0] : (NC == 1 ? t.k[0] : 0);
-  const int k1 = NC == 6 && t.c0 <= 1 && t.c1 > 1 ? t.k[1] : 0;
-  const int k2 = NC == 6 && t.c0 <= 2 && t.c1 > 2 ? t.k[2] : 0;
-  const int k3 = NC == 6 && t.c0 <= 3 && t.c1 > 3 ? t.k[3] : 0;
-  const int k4 = NC == 6 && t.c0 <= 4 && t.c1 > 4 ? t.k[4] : 0;
-  const int k5 = NC == 6 && t.c0 <= 5 && t.c1 > 5 ? t.k[5] : 0;
-  const int p1 = k0, p2 = p1 + k1, p3 = p2 + k2, p4 = p3 + k3, p5 = p4 + k4;
-  const int npairs = p5 + k5;
-  const int units = npairs * 2 * nrhs;
-  const int lg = lanes_log2(units, vrows);
-  const int T = 1 << lg;
-  const int Wr = ((units << lg) + 31) & ~31;  // whole warps (shuffles)
-  for (int w = threadIdx.x; w < Wr; w += blockDim.x) {
-    const int seg = w & (T - 1);
-    const int u = w >> lg;
-    double s = 0.0;
-    if (u < units) {
-      const int q = NR == 1 ? 0 : u % nrhs;
-      const int uq = NR == 1 ? u : u / nrhs;
-      const int o = uq & 1;
-      const int p = uq >> 1;
-      const int c = NC == 1 ? 0
-                            : (p >= p1) + (p >= p2) + (p >= p3) + (p >= p4) + (p >= p5);
-      const int base = c == 0 ? 0 : c == 1 ? p1 : c == 2 ? p2 : c == 3 ? p3 : c == 4 ? p4 : p5;
-      const int l = p - base;
-      const int rr = comp_r<NC>(c), cc = comp_c<NC>(c);
-      if (o == 0 || rr != cc) {
-        const double* vl = V + (long long)ld * base + (long long)l * ld;
-        const double* xb = xs + (o == 0 ? cc : rr) * nrhs + q;
-#pragma unroll 4
-        for (int j = seg; j < vrows; j += T) s = fma(vl[j], xb[j * XS], s);
+    for (int u = 0; u < 4; ++u) {
+      const double v = V[(j + u) * rl + col];
+      const double2 x01 = *reinterpret_cast<const double2*>(xs + 4 * (j + u));
+      a0[u] = fma(v, x01.x, a0[u]);
+      if (NC == 6) {
+        a1[u] = fma(v, x01.y, a1[u]);
+        a2[u] = fma(v, xs[4 * (j + u) + 2], a2[u]);
       }
     }
-    s = group_sum(s, T);
-    if (seg == 0 && u < units) zout[u] = s;
   }
+  for (; j < nrows; ++j) {
+    const double v = V[j * rl + col];
+    a0[0] = fma(v, xs[4 * j], a0[0]);
+    if (NC == 6) {
+      a1[0] = fma(v, xs[4 * j + 1], a1[0]);
+      a2[0] = fma(v, xs[4 * j + 2], a2[0]);
+    }
+  }
+  f0 += (a0[0] + a0[1]) + (a0[2] + a0[3]);
+  f1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
+  f2 += (a2[0] + a2[1]) + (a2[2] + a2[3]);
 }
 
-// y[i][r][q] = sum over components (r,s) of U_(r,s)[i,:] z_(r,s)[:, r > s]
-template <int NC, int NR>
-__device__ void stream_urows(const MvTask& t, const double* U, int urows, const double* z,
-                             int nrhs_rt, double* yout) {
-  constexpr int NOUT = NC == 6 ? 3 : 1;
-  const int nrhs = NR > 0 ? NR : nrhs_rt;
-  int kmax = 1;
-  for (int c = t.c0; c < t.c1; ++c) kmax = max(kmax, t.k[c]);
-  const int units = urows * NOUT * nrhs;
-  const int lg = lanes_log2(units, 3 * kmax);
-  const int T = 1 << lg;
-  const int Wr = ((units << lg) + 31) & ~31;
-  for (int w = threadIdx.x; w < Wr; w += blockDim.x) {
-    const int seg = w & (T - 1);
-    const int u = w >> lg;
-    double acc = 0.0;
-    if (u < units) {
-      const int q = NR == 1 ? 0 : u % nrhs;
-      const int ur = NR == 1 ? u : u / nrhs;
-      const int r = NOUT == 1 ? 0 : ur % NOUT;
-      const int i = NOUT == 1 ? ur : ur / NOUT;
-      long long uoff = 0;
-      int slot = 0, e = 0;
-      for (int c = t.c0; c < t.c1; ++c) {
-        const int k = t.k[c];
-        const int rr = comp_r<NC>(c), cc = comp_c<NC>(c);
-        const int o = rr == r ? 0 : (cc == r ? 1 : -1);
-        if (o >= 0) {
-          const double* uu = U + uoff + i;
-          const double* zz = z + slot * 2 * nrhs + o * nrhs + q;
-          // term e runs over the (c, l) pairs touching r; lane seg takes e = seg mod T
-          const int l0 = (seg - e) & (T - 1);
-#pragma unroll 4
-          for (int l = l0; l < k; l += T) acc = fma(uu[l * urows], zz[l * 2 * nrhs], acc);
-          e += k;
-        }
-        uoff += (long long)urows * k;
-        slot += k;
+// y rows (lane, lane + 32) += sum_g U[g][i] W[g][:] over columns [0, ncol)
+// of a column-major chunk with m rows
+template <int NC>
+__device__ __forceinline__ void urows1(const double* U, int m, int ncol, const double* W,
+                                       int lane, double* y) {
+  // m <= 32: one row per lane, four column accumulator sets
+  double a[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  const int i = lane < m ? lane : 0;
+  int g = 0;
+  for (; g + 3 < ncol; g += 4) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double2 w01 = *reinterpret_cast<const double2*>(W + 4 * (g + e));
+      const double u = U[(g + e) * m + i];
+      a[e][0] = fma(u, w01.x, a[e][0]);
+      if (NC == 6) {
+        a[e][1] = fma(u, w01.y, a[e][1]);
+        a[e][2] = fma(u, W[4 * (g + e) + 2], a[e][2]);
       }
     }
-    acc = group_sum(acc, T);
-    if (seg == 0 && u < units) yout[u] = acc;
+  }
+  for (; g < ncol; ++g) {
+    const double u = U[g * m + i];
+    a[0][0] = fma(u, W[4 * g], a[0][0]);
+    if (NC == 6) {
+      a[0][1] = fma(u, W[4 * g + 1], a[0][1]);
+      a[0][2] = fma(u, W[4 * g + 2], a[0][2]);
+    }
+  }
+  if (lane < m) {
+    y[0] += (a[0][0] + a[1][0]) + (a[2][0] + a[3][0]);
+    y[1] += (a[0][1] + a[1][1]) + (a[2][1] + a[3][1]);
+    y[2] += (a[0][2] + a[1][2]) + (a[2][2] + a[3][2]);
   }
 }
 
-// dense row tile: y[i][r][q] = sum_j sum_s A_(r,s)[i][j] x_s[j][q]
-template <int NC, int NR>
-__device__ void stream_dense(const MvTask& t, const double* D, const double* xs, int XS,
-                             int nrhs_rt, double* yout) {
-  constexpr int NOUT = NC == 6 ? 3 : 1;
-  const int nrhs = NR > 0 ? NR : nrhs_rt;
-  const int pitch = (t.cols * NC + 1) & ~1;  // rows padded to 16 bytes
-  const int units = t.rows * NOUT * nrhs;
-  const int lg = lanes_log2(units, t.cols);
-  const int T = 1 << lg;
-  const int Wr = ((units << lg) + 31) & ~31;
-  for (int w = threadIdx.x; w < Wr; w += blockDim.x) {
-    const int seg = w & (T - 1);
-    const int u = w >> lg;
-    double acc = 0.0;
-    if (u < units) {
-      const int q = NR == 1 ? 0 : u % nrhs;
-      const int ur = NR == 1 ? u : u / nrhs;
-      const int r = NOUT == 1 ? 0 : ur % NOUT;
-      const int i = NOUT == 1 ? ur : ur / NOUT;
-      const double* d = D + i * pitch;
-      const int c0 = comp_of<NC>(r, 0), c1 = comp_of<NC>(r, 1), c2 = comp_of<NC>(r, 2);
-#pragma unroll 2
-      for (int j = seg; j < t.cols; j += T) {
-        const double* xj = xs + j * XS + q;
-        const double* dj = d + j * NC;
-        acc = fma(dj[c0], xj[0], acc);
-        if (NOUT == 3) {
-          acc = fma(dj[c1], xj[nrhs], acc);
-          acc = fma(dj[c2], xj[2 * nrhs], acc);
-        }
+template <int NC>
+__device__ __forceinline__ void urows(const double* U, int m, int ncol, const double* W,
+                                      int lane, double* y) {
+  if (m <= 32) {
+    urows1<NC>(U, m, ncol, W, lane, y);
+    return;
+  }
+  const bool r0 = lane < m, r1 = lane + 32 < m;
+  const int i1 = r1 ? lane + 32 : lane;  // keeps the second load in bounds
+  double a[2][3] = {{0, 0, 0}, {0, 0, 0}}, c[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  int g = 0;
+  for (; g + 1 < ncol; g += 2) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double2 w01 = *reinterpret_cast<const double2*>(W + 4 * (g + e));
+      const double w2 = W[4 * (g + e) + 2];
+      const double u = U[(g + e) * m + lane];
+      const double v = U[(g + e) * m + i1];
+      a[e][0] = fma(u, w01.x, a[e][0]);
+      c[e][0] = fma(v, w01.x, c[e][0]);
+      if (NC == 6) {
+        a[e][1] = fma(u, w01.y, a[e][1]);
+        a[e][2] = fma(u, w2, a[e][2]);
+        c[e][1] = fma(v, w01.y, c[e][1]);
+        c[e][2] = fma(v, w2, c[e][2]);
       }
     }
-    acc = group_sum(acc, T);
-    if (seg == 0 && u < units) yout[u] = acc;
+  }
+  if (g < ncol) {
+    const double2 w01 = *reinterpret_cast<const double2*>(W + 4 * g);
+    const double w2 = W[4 * g + 2];
+    const double u = U[g * m + lane];
+    const double v = U[g * m + i1];
+    a[0][0] = fma(u, w01.x, a[0][0]);
+    c[0][0] = fma(v, w01.x, c[0][0]);
+    if (NC == 6) {
+      a[0][1] = fma(u, w01.y, a[0][1]);
+      a[0][2] = fma(u, w2, a[0][2]);
+      c[0][1] = fma(v, w01.y, c[0][1]);
+      c[0][2] = fma(v, w2, c[0][2]);
+    }
+  }
+  if (r0) {
+    y[0] += a[0][0] + a[1][0];
+    y[1] += a[0][1] + a[1][1];
+    y[2] += a[0][2] + a[1][2];
+  }
+  if (r1) {
+    y[3] += c[0][0] + c[1][0];
+    y[4] += c[0][1] + c[1][1];
+    y[5] += c[0][2] + c[1][2];
   }
 }
 
-// Persistent CTAs, static round-robin task assignment (tasks sorted by
-// size), NSTAGE-deep TMA pipeline: the task descriptor, its data and its x
-// segment arrive as one mbarrier transaction; after consuming task k the
-// elected thread refills the stage with task k + NSTAGE.
-template <int NC, int NSTAGE, int NR>
-__global__ void __launch_bounds__(256, 1)
-hmv_stream_kernel(StreamParams P) {
+// dense chunk columns [0, ncol): D[j][c][i] (column stride cp), x rows xs
+template <int NC>
+__device__ __forceinline__ void drows(const double* D, int m, int cp, int ncol,
+                                      const double* xs, int lane, double* y) {
+  const bool r0 = lane < m, r1 = lane + 32 < m;
+  double a0 = 0, a1 = 0, a2 = 0, c0 = 0, c1 = 0, c2 = 0;
+  for (int j = 0; j < ncol; ++j) {
+    const double* d = D + j * cp;
+    const double2 x01 = *reinterpret_cast<const double2*>(xs + 4 * j);
+    const double x2 = xs[4 * j + 2];
+    if (NC == 6) {
+      // y_r += sum_s A_(r,s) x_s with A_(r,s) = component (min(r,s), max(r,s))
+      const double p00 = r0 ? d[lane] : 0.0, p01 = r0 ? d[m + lane] : 0.0,
+                   p02 = r0 ? d[2 * m + lane] : 0.0, p11 = r0 ? d[3 * m + lane] : 0.0,
+                   p12 = r0 ? d[4 * m + lane] : 0.0, p22 = r0 ? d[5 * m + lane] : 0.0;
+      a0 = fma(p00, x01.x, fma(p01, x01.y, fma(p02, x2, a0)));
+      a1 = fma(p01, x01.x, fma(p11, x01.y, fma(p12, x2, a1)));
+      a2 = fma(p02, x01.x, fma(p12, x01.y, fma(p22, x2, a2)));
+      if (r1) {
+        const int i = lane + 32;
+        const double q00 = d[i], q01 = d[m + i], q02 = d[2 * m + i], q11 = d[3 * m + i],
+                     q12 = d[4 * m + i], q22 = d[5 * m + i];
+        c0 = fma(q00, x01.x, fma(q01, x01.y, fma(q02, x2, c0)));
+        c1 = fma(q01, x01.x, fma(q11, x01.y, fma(q12, x2, c1)));
+        c2 = fma(q02, x01.x, fma(q12, x01.y, fma(q22, x2, c2)));
+      }
+    } else {
+      a0 = fma(r0 ? d[lane] : 0.0, x01.x, a0);
+      c0 = fma(r1 ? d[lane + 32] : 0.0, x01.x, c0);
+    }
+  }
+  y[0] += a0;
+  y[1] += a1;
+  y[2] += a2;
+  y[3] += c0;
+  y[4] += c1;
+  y[5] += c2;
+}
+
+// Warp-private pipelines: WARPS warps per CTA, each with NS stages of
+// P.stage doubles and P.scratch doubles of job scratch.  Jobs are assigned
+// round-robin over all warps of the grid (the host sorts them by size).
+// Stage layout: [WChunk | WJob] header (128 B), data, aux -- descriptors
+// arrive in the same mbarrier transaction as the data.
+constexpr int kHdr = 16;  // doubles of stage header
+
+template <int NC, int NS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+hmv_warp_kernel(WarpStreamParams P) {
   constexpr int NOUT = NC == 6 ? 3 : 1;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bar[NSTAGE];
-  __shared__ __align__(16) MvTask tdesc[NSTAGE];
-  const int stage_total = P.stage_doubles + P.xbuf_doubles;
-  double* zbuf = sm + (long long)NSTAGE * stage_total;
-  const int G = gridDim.x;
+  __shared__ __align__(8) uint64_t bars[WARPS * NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NW = gridDim.x * WARPS;
+  const int gw = blockIdx.x * WARPS + warp;
+  double* ring = sm + (long long)warp * (NS * P.stage + P.scratch);
+  double* scratch = ring + NS * P.stage;
+  uint64_t* bar = bars + warp * NS;
 
-  auto issue = [&](int ti, int s) {
-    const MvTask& t = P.tasks[ti];
-    const uint32_t dbytes = (uint32_t)t.data_len * 8u;
-    // x segment, or (YPART) the task's z slots, into the stage's x area
-    const bool ztask = t.kind == TK_YPART;
-    const uint32_t xbytes = ztask ? (uint32_t)t.x_rows * 2u * (uint32_t)P.nrhs * 8u
-                                  : (uint32_t)t.x_rows * (uint32_t)P.xs * 8u;
-    mbar_expect_tx(&bar[s], dbytes + xbytes + (uint32_t)sizeof(MvTask));
-    bulk_g2s(&tdesc[s], &P.tasks[ti], (uint32_t)sizeof(MvTask), &bar[s]);
-    double* dst = sm + (long long)s * stage_total;
-    if (dbytes)
-      bulk_g2s(dst, (t.src == 0 ? P.arena : P.dense) + t.data_off, dbytes, &bar[s]);
-    if (xbytes)
-      bulk_g2s(dst + P.stage_doubles,
-               ztask ? P.zfinal + t.z_off * 2 * P.nrhs : P.xi + (long long)t.x_col0 * P.xs,
-               xbytes, &bar[s]);
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&bar[s], 1);
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
   }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int s = 0; s < NSTAGE; ++s) {
-      const int t = blockIdx.x + s * G;
-      if (t < P.ntasks) issue(t, s);
-    }
-  const int nrhs = P.nrhs;
-  for (int kk = 0;; ++kk) {
-    const int ti = blockIdx.x + kk * G;
-    if (ti >= P.ntasks) break;
-    const int s = kk % NSTAGE;
-    mbar_wait(&bar[s], (uint32_t)((kk / NSTAGE) & 1));
-    const MvTask& t = tdesc[s];
-    const double* data = sm + (long long)s * stage_total;
-    const double* xs = data + P.stage_doubles;
-    if (t.kind == TK_DENSE) {
-      stream_dense<NC, NR>(t, data, xs, P.xs, nrhs, P.ypart + t.out_off * NOUT * nrhs);
-    } else if (t.kind == TK_VCOLS) {
-      stream_zdots<NC, NR>(t, data, t.rows, t.rows, xs, P.xs, nrhs,
-                           P.zpart + t.out_off * 2 * nrhs);
-    } else if (t.kind == TK_FUSED) {
-      int ksum = 0;
-      for (int c = t.c0; c < t.c1; ++c) ksum += t.k[c];
-      stream_zdots<NC, NR>(t, data, t.cols, t.cols, xs, P.xs, nrhs, zbuf);
-      __syncthreads();
-      stream_urows<NC, NR>(t, data + (long long)t.cols * ksum, t.rows, zbuf, nrhs,
-                           P.ypart + t.out_off * NOUT * nrhs);
-    } else {  // TK_YPART: z slots arrived in the x area (x_rows = slot count)
-      stream_urows<NC, NR>(t, data, t.rows, xs, nrhs, P.ypart + t.out_off * NOUT * nrhs);
-    }
-    __syncthreads();  // stage s consumed
-    if (threadIdx.x == 0) {
-      const int tn = ti + NSTAGE * G;
-      if (tn < P.ntasks) {
-        fence_proxy_async();
-        issue(tn, s);
+  __syncwarp();
+
+  // issue cursor (lane 0): the descriptor of the next chunk to issue is
+  // loaded one issue ahead so its global latency is off the critical path
+  int ij = gw, ic = 0, ijc = 0, ijn = 0;
+  WChunk nx{};
+  auto advance = [&]() {
+    if (++ic == ijn) {
+      ic = 0;
+      ij += NW;
+      if (ij < P.njobs) {
+        ijc = P.jobs[ij].chunk0;
+        ijn = P.jobs[ij].nchunks;
       }
     }
+    if (ij < P.njobs) nx = P.chunks[ijc + ic];
+  };
+  if (lane == 0 && ij < P.njobs) {
+    ijc = P.jobs[ij].chunk0;
+    ijn = P.jobs[ij].nchunks;
+    nx = P.chunks[ijc];
   }
-}
-
-// zfinal = sum of per-row-tile z partials, fixed order
-__global__ void zreduce_kernel(const ZReduce* __restrict__ d, int n,
-                               const double* __restrict__ zpart,
-                               double* __restrict__ zfinal, int unit) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = gw; t < n; t += nw) {
-    const ZReduce r = d[t];
-    const long long len = (long long)r.len * unit;
-    for (long long e = lane; e < len; e += 32) {
-      double s = 0.0;
-      for (int k = 0; k < r.tiles; ++k) s += zpart[(r.src + (long long)k * r.stride) * unit + e];
-      zfinal[r.dst * unit + e] = s;
+  auto issue_next = [&](int s) {
+    if (ij >= P.njobs) return;
+    const WChunk ch = nx;
+    double* st = ring + s * P.stage;
+    const uint32_t bytes = (uint32_t)ch.len * 8u;
+    const uint32_t abytes = ch.aux_kind == WA_NONE ? 0u : (uint32_t)ch.aux_len * 32u;
+    mbar_expect_tx(&bar[s], 128u + bytes + abytes);
+    bulk_g2s(st, &P.chunks[ijc + ic], 48u, &bar[s]);
+    bulk_g2s(st + 6, &P.jobs[ij], 80u, &bar[s]);
+    if (bytes)
+      bulk_g2s(st + kHdr, (ch.src_kind == 0 ? P.arena : P.dense) + ch.src, bytes, &bar[s]);
+    if (abytes)
+      bulk_g2s(st + kHdr + ch.len, (ch.aux_kind == WA_X ? P.xi : P.win) + ch.aux * 4,
+               abytes, &bar[s]);
+    advance();
+  };
+  int issued = 0;  // lane 0's count, broadcast after every issue
+  if (lane == 0)
+    for (int s = 0; s < NS; ++s) {
+      const bool any = ij < P.njobs;
+      issue_next(s);
+      issued += any ? 1 : 0;
     }
+  issued = __shfl_sync(0xffffffffu, issued, 0);
+
+  int consumed = 0;
+  double y[6] = {0, 0, 0, 0, 0, 0};     // rows lane, lane+32 x 3 outputs
+  double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // VSPLIT dot products
+  while (consumed < issued) {
+    const int s = consumed % NS;
+    mbar_wait(&bar[s], (uint32_t)((consumed / NS) & 1));
+    const double* st = ring + s * P.stage;
+    const WChunk& ch = *reinterpret_cast<const WChunk*>(st);
+    const WJob& job = *reinterpret_cast<const WJob*>(st + 6);
+    const double* data = st + kHdr;
+    const double* aux = data + ch.len;
+    const int kind = job.kind;
+    const bool first = ch.part == 0 && ch.g0 == 0 && kind != WJ_VSPLIT
+                           ? true
+                           : (kind == WJ_USPLIT && ch.g0 == 0);
+    if (first) {  // keep the job's x / W for its later chunks
+      for (int e = lane; e < 4 * ch.aux_len; e += 32) scratch[e] = aux[e];
+      __syncwarp();
+    }
+    bool last;
+    if (kind == WJ_FUSED) {
+      double* W = scratch + 256;
+      if (ch.part == 0) {
+        const int ncol = ch.g1 - ch.g0;
+        for (int g = lane; g < ncol; g += 32) {
+          double a = 0.0, b = 0.0, c = 0.0;
+          vdots<NC>(data, ncol, job.n, scratch, g, a, b, c);
+          double w[4];
+          weights<NC>(comp_of_col(job.kp, ch.g0 + g), a, b, c, w);
+          *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g)) = make_double2(w[0], w[1]);
+          *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g) + 2) = make_double2(w[2], w[3]);
+        }
+        __syncwarp();
+      } else {
+        urows<NC>(data, job.m, ch.g1 - ch.g0, W + 4 * ch.g0, lane, y);
+      }
+      last = ch.part == 1 && ch.g1 == job.ncols;
+    } else if (kind == WJ_USPLIT) {
+      urows<NC>(data, job.m, ch.g1 - ch.g0, scratch + 4 * ch.g0, lane, y);
+      last = ch.g1 == job.ncols;
+    } else if (kind == WJ_DENSE) {
+      const int cp = (NC * job.m + 1) & ~1;
+      drows<NC>(data, job.m, cp, ch.g1 - ch.g0, scratch + 4 * ch.g0, lane, y);
+      last = ch.g1 == job.n;
+    } else {  // WJ_VSPLIT: rows [g0, g1) of V for this job's columns
+      if (lane < job.ncols) vdots<NC>(data, job.ncols, ch.g1 - ch.g0, aux, lane, f0, f1, f2);
+      last = ch.g1 == job.n;
+    }
+    // job epilogue (descriptor fields read before the stage is recycled)
+    if (last) {
+      if (kind == WJ_VSPLIT) {
+        if (lane < job.ncols) {
+          double w[4];
+          weights<NC>(job.comp, f0, f1, f2, w);
+          double* o = P.wout + (job.out + lane) * 4;
+          *reinterpret_cast<double2*>(o) = make_double2(w[0], w[1]);
+          *reinterpret_cast<double2*>(o + 2) = make_double2(w[2], w[3]);
+        }
+        f0 = f1 = f2 = 0.0;
+      } else {
+        double* yo = P.ypart + job.out * NOUT;
+        if (lane < job.m)
+          for (int r = 0; r < NOUT; ++r) yo[lane * NOUT + r] = y[r];
+        if (lane + 32 < job.m)
+          for (int r = 0; r < NOUT; ++r) yo[(lane + 32) * NOUT + r] = y[3 + r];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) y[r] = 0.0;
+      }
+    }
+    __syncwarp();  // all lanes done with stage s
+    if (lane == 0 && ij < P.njobs) {
+      fence_proxy_async();
+      issue_next(s);
+      ++issued;
+    }
+    ++consumed;
+    issued = __shfl_sync(0xffffffffu, issued, 0);
   }
 }
 
-
-// per leaf: y(p) = sum over covering task rows (fixed order)
+// per leaf: y(p) = sum over covering job rows (fixed order)
 template <int NOUT>
 __global__ void hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin,
                                        const int* __restrict__ leaf_end,
@@ -391,40 +476,32 @@ __global__ void hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin,
                                        const LeafEntry* __restrict__ entries, int nleaves,
                                        const double* __restrict__ ypart,
                                        const int* __restrict__ rperm, int nrows,
-                                       double* __restrict__ y, int nrhs) {
-  const long long ndof = (long long)nrows * NOUT;
+                                       double* __restrict__ y) {
   for (int L = blockIdx.x; L < nleaves; L += gridDim.x) {
     const int b0 = leaf_begin[L], b1 = leaf_end[L];
     const int e0 = leaf_ptr[L], e1 = leaf_ptr[L + 1];
-    const int cnt = (b1 - b0) * NOUT * nrhs;
+    const int cnt = (b1 - b0) * NOUT;
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const int q = t % nrhs;
-      const int r = (t / nrhs) % NOUT;
-      const int i = t / (nrhs * NOUT);
+      const int r = t % NOUT;
+      const int i = t / NOUT;
       double s = 0.0;
       for (int e = e0; e < e1; ++e) {
         const LeafEntry en = entries[e];
-        if (i >= en.lo && i < en.hi)
-          s += ypart[((en.slot + (i - en.lo)) * NOUT + r) * nrhs + q];
+        if (i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
       }
-      y[q * ndof + (long long)r * nrows + rperm[b0 + i]] = s;
+      y[(long long)r * nrows + rperm[b0 + i]] = s;
     }
   }
 }
 
-// gather x into the stream layout: XS doubles per internal column
+// gather x into the stream layout: 4 doubles per internal column
 template <int NOUT>
-__global__ void gather_stream_kernel(const double* __restrict__ x, double* __restrict__ xi,
-                                     const int* __restrict__ cperm, int ncols, int nrhs,
-                                     int xs) {
-  const long long total = (long long)ncols * xs;
-  const long long ndof = (long long)ncols * NOUT;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+__global__ void gather4_kernel(const double* __restrict__ x, double* __restrict__ xi,
+                               const int* __restrict__ cperm, int ncols) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 4LL * ncols;
        t += (long long)gridDim.x * blockDim.x) {
-    const int p = (int)(t / xs);
-    const int w = (int)(t % xs);
-    const int r = w / nrhs, q = w % nrhs;
-    xi[t] = r < NOUT ? x[q * ndof + (long long)r * ncols + cperm[p]] : 0.0;
+    const int p = (int)(t >> 2), r = (int)(t & 3);
+    xi[t] = r < NOUT ? x[(long long)r * ncols + cperm[p]] : 0.0;
   }
 }
 
@@ -438,8 +515,13 @@ __global__ void pack_kernel(const PackDesc* __restrict__ d, int n,
     const PackDesc p = d[t];
     const long long tot = (long long)p.rows * p.cols;
     for (long long e = lane; e < tot; e += 32) {
-      const long long l = e / p.rows, i = e % p.rows;
-      dst[p.dst + e] = src[p.src + l * p.ld + i];
+      if (p.trans) {  // row-major destination
+        const long long i = e / p.cols, l = e % p.cols;
+        dst[p.dst + i * p.dld + l] = src[p.src + l * p.ld + i];
+      } else {
+        const long long l = e / p.rows, i = e % p.rows;
+        dst[p.dst + l * p.dld + i] = src[p.src + l * p.ld + i];
+      }
     }
   }
 }

@@ -21,7 +21,7 @@ print("storage", h.storage())
 x = orc.random_vector(h.cols, 1)
 for it in range(5):
     y = h.matvec(x)
-for k in ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_blocks", "hmv_reduce", "pack"):
+for k in ("gather", "hmv_stream", "hmv_ypart", "hmv_blocks", "hmv_reduce", "pack"):
     ms, n = h.kernel_times(k, reset=True)
     print(k, ms / max(n, 1), "ms/launch", n)
 kc, kl, co, ls = h.ranks()

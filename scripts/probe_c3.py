@@ -15,6 +15,6 @@ print("storage", h.storage(), flush=True)
 x = orc.normal_vector(h.cols, 2)
 for it in range(3):
     y = h.matvec(x)
-for k in ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_blocks", "hmv_reduce", "pack"):
+for k in ("gather", "hmv_stream", "hmv_ypart", "hmv_blocks", "hmv_reduce", "pack"):
     ms, n = h.kernel_times(k, reset=True)
     print(k, ms / max(n, 1), "ms/launch", n)
