@@ -603,16 +603,34 @@ void refresh_matvec_ranks(hmgpu_ctx* c) {
 
 
 // ---- streamed matvec plan (warp-private jobs, hmgpu_stream.cuh) -------------
-constexpr int kWarps = 5;      // warps per CTA (one CTA per SM)
-constexpr int kNStage = 3;     // TMA ring depth per warp
-constexpr int kStage = 1536;   // doubles per stage (12 KB: header + data + aux)
-constexpr int kStageData = kStage - 16;  // data + aux capacity after the header
-constexpr int kScratch = 1024; // doubles of per-warp job scratch (x + W)
-constexpr int kMaxKFused = 192;  // scratch: x (256) + W (4 K)
-constexpr int kMaxKSplit = 256;
+// Default geometry of the warp pipelines (tuned on B200: 7 warps per SM,
+// two 12 KB stages each; larger stages beat deeper rings).  HMGPU_MV_CFG=
+// "warps,stages,stage_doubles,scratch_doubles" overrides it for tuning.
+struct MvCfg {
+  int warps = 7, ns = 2, stage = 1536, scratch = 1024;
+};
+MvCfg mv_cfg() {
+  static MvCfg cfg = [] {
+    MvCfg c;
+    if (const char* e = std::getenv("HMGPU_MV_CFG")) {
+      int w, n, s, k;
+      if (std::sscanf(e, "%d,%d,%d,%d", &w, &n, &s, &k) == 4) {
+        c.warps = w;
+        c.ns = n;
+        c.stage = s;
+        c.scratch = k;
+      }
+    }
+    return c;
+  }();
+  return cfg;
+}
 
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
+  const MvCfg cfg = mv_cfg();
+  const int kStageData = cfg.stage - 16;  // data + aux after the descriptor header
+  const int kMaxKFused = (cfg.scratch - 256) / 4;  // scratch: x (256) + W (4 K)
   const int NC = c->NC;
   std::vector<WJob> ja, jb;
   std::vector<std::vector<WChunk>> ca, cb;  // chunks per job
@@ -735,7 +753,6 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       ca.push_back(chs);
       continue;
     }
-    if (K > kMaxKSplit) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
     // split block: VSPLIT column groups of each component -> W (global)
     const long long wbase = wslots;
     wslots += K;
@@ -761,37 +778,51 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         ca.push_back(chs);
       }
     }
-    // USPLIT row tiles of all components
-    for (int i0 = 0; i0 < m; i0 += 64) {
-      const int rt = std::min(64, m - i0);
-      WJob j{};
-      j.kind = WJ_USPLIT;
-      j.m = rt;
-      j.ncols = K;
-      j.out = slots;
-      std::copy(kp, kp + 8, j.kp);
-      std::vector<WChunk> chs;
-      const int first_cols = std::max(1, (kStageData - 4 * K) / rt);
-      const int cols = std::max(1, kStageData / rt);
-      for (int g0 = 0; g0 < K;) {
-        const int g1 = std::min(K, g0 + (g0 == 0 ? first_cols : cols));
-        const long long off = alen;
-        for (int q = 0; q < NC; ++q) {
-          const int a = std::max(g0, kp[q]), b = std::min(g1, kp[q + 1]);
-          if (a >= b) continue;
-          packs.push_back(PackDesc{c->items[mb.item0 + q].u_off + i0 +
-                                       (long long)(a - kp[q]) * m,
-                                   off + (long long)(a - g0) * rt, m, rt, rt, b - a, 0, 0});
-        }
-        alen += align2((long long)rt * (g1 - g0));
-        chs.push_back(chunk(off, rt * (g1 - g0), 0, g0 == 0 ? WA_W : WA_NONE, wbase,
-                            g0 == 0 ? K : 0, g0, g1, 1));
-        g0 = g1;
+    // USPLIT row tiles over component groups whose W fits the warp scratch
+    for (int q0 = 0; q0 < NC;) {
+      int q1 = q0, kg = 0;
+      while (q1 < NC && 4 * (kg + k[q1]) <= cfg.scratch && 4 * (kg + k[q1]) <= kStageData / 2)
+        kg += k[q1++];
+      if (q1 == q0) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
+      if (kg == 0) {
+        q0 = q1;
+        continue;
       }
-      add_rows(mb.row0 + i0, rt, slots);
-      slots += rt;
-      jb.push_back(j);
-      cb.push_back(chs);
+      int gkp[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // prefix sums restricted to the group
+      for (int q = 0; q < 6; ++q) gkp[q + 1] = gkp[q] + (q >= q0 && q < q1 ? k[q] : 0);
+      gkp[7] = gkp[6];
+      for (int i0 = 0; i0 < m; i0 += 64) {
+        const int rt = std::min(64, m - i0);
+        WJob j{};
+        j.kind = WJ_USPLIT;
+        j.m = rt;
+        j.ncols = kg;
+        j.out = slots;
+        std::copy(gkp, gkp + 8, j.kp);
+        std::vector<WChunk> chs;
+        const int first_cols = std::max(1, (kStageData - 4 * kg) / rt);
+        const int cols = std::max(1, kStageData / rt);
+        for (int g0 = 0; g0 < kg;) {
+          const int g1 = std::min(kg, g0 + (g0 == 0 ? first_cols : cols));
+          const long long off = alen;
+          for (int q = q0; q < q1; ++q) {
+            const int a = std::max(g0, gkp[q]), b = std::min(g1, gkp[q + 1]);
+            if (a >= b) continue;
+            packs.push_back(PackDesc{c->items[mb.item0 + q].u_off + i0 +
+                                         (long long)(a - gkp[q]) * m,
+                                     off + (long long)(a - g0) * rt, m, rt, rt, b - a, 0, 0});
+          }
+          alen += align2((long long)rt * (g1 - g0));
+          chs.push_back(chunk(off, rt * (g1 - g0), 0, g0 == 0 ? WA_W : WA_NONE,
+                              wbase + kp[q0], g0 == 0 ? kg : 0, g0, g1, 1));
+          g0 = g1;
+        }
+        add_rows(mb.row0 + i0, rt, slots);
+        slots += rt;
+        jb.push_back(j);
+        cb.push_back(chs);
+      }
+      q0 = q1;
     }
   }
   // order each pass by size (largest first) and lay out the chunk table
@@ -844,7 +875,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   c->p_slots = slots;
   c->p_zslots = wslots;
   c->p_arena_len = alen;
-  c->p_smem = sizeof(double) * (size_t)kWarps * (kNStage * kStage + kScratch);
+  c->p_smem = sizeof(double) * (size_t)cfg.warps * (cfg.ns * cfg.stage + cfg.scratch);
   c->plan_mode = mode;
   c->plan_nrhs = nrhs;
   c->plan_valid = true;
@@ -878,24 +909,31 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
   P.wout = c->d_zpart.p;
   P.win = c->d_zpart.p;
   P.ypart = c->d_ypart.p;
-  P.stage = kStage;
-  P.scratch = kScratch;
+  const MvCfg cfg = mv_cfg();
+  P.stage = cfg.stage;
+  P.scratch = cfg.scratch;
   auto run = [&](int first, int count, const char* name) {
     if (count <= 0) return;
     P.jobs = c->d_pjobs.p + first;
     P.njobs = count;
-    const int g = std::min(c->sm_count, (count + kWarps - 1) / kWarps);
+    const int g = std::min(c->sm_count, (count + cfg.warps - 1) / cfg.warps);
     auto go = [&](auto kernel) {
       CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->p_smem));
-      kernel<<<g, kWarps * 32, c->p_smem, c->stream>>>(P);
+      kernel<<<g, cfg.warps * 32, c->p_smem, c->stream>>>(P);
     };
+#define HMV_CASE(W, S)                                        \
+  if (cfg.warps == W && cfg.ns == S) {                        \
+    if (c->NC == 6) go(hmv_warp_kernel<6, S, W>);             \
+    else go(hmv_warp_kernel<1, S, W>);                        \
+    return;                                                   \
+  }
     c->timed(name, [&] {
-      if (c->NC == 6)
-        go(hmv_warp_kernel<6, kNStage, kWarps>);
-      else
-        go(hmv_warp_kernel<1, kNStage, kWarps>);
+      HMV_CASE(7, 2) HMV_CASE(6, 2) HMV_CASE(8, 2) HMV_CASE(5, 3) HMV_CASE(4, 3)
+      HMV_CASE(6, 3) HMV_CASE(5, 2) HMV_CASE(4, 4)
+      fail(HMGPU_ERR_INVALID, "HMGPU_MV_CFG: unsupported (warps, stages)");
     });
+#undef HMV_CASE
   };
   run(0, c->p_nz, "hmv_stream");
   run(c->p_nz, c->p_ntasks - c->p_nz, "hmv_ypart");
