@@ -1,0 +1,135 @@
+"""Parity at the BASELINE.json sizes.
+
+config 2 (20,480 triangles): the whole oracle assembly fits in seconds, so
+ranks / pivots are compared for every (component, block) and the matvec
+against the oracle's.  config 3 (196,608 triangles): the oracle's full
+assembly would take minutes, so parity is by sampling (near-field entries,
+ACA of individual blocks re-run by the oracle, rows of A x from oracle
+entries) plus size-independent properties (linearity, determinism).
+config 4 (81,920 triangles): the adaptive matvec's record, sweep by sweep."""
+import numpy as np
+import pytest
+
+import paper_2205_04752_b200 as hm
+from oracle import oracle as orc
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_config2_full_parity():
+    mesh = hm.Mesh.icosphere(5)
+    a = mesh.arrays()
+    eps = 1e-6
+    g = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+    st = g.assemble(eps=eps, beta=0.8, lookahead=2)
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=32, eta=1.0)
+    o.assemble(eps=eps, beta=0.8, lookahead=2)
+    assert g.partition_json() == o.partition_json()
+    gk, gl, gc, _ = g.ranks()
+    ok, ol, oc, _ = o.ranks()
+    assert (gk == ok).all() and (gl == ol).all() and (gc == oc).all()
+    assert st.pivots == o.storage()["total_pivots"]
+    assert g.storage()["mb_current"] == pytest.approx(o.storage()["mb_current"], rel=1e-12)
+    x = hm.random_vector(g.cols, 1)
+    y = g.matvec(x)
+    assert rel(y, o.matvec(x)) < 1e-12
+    assert rel(g.matvec(x, hm.Mode.Lookahead), o.matvec(x, 1)) < 1e-12
+
+
+@pytest.fixture(scope="module")
+def c3():
+    mesh = hm.Mesh.voxel_cube(128, 0.0, 1.0)
+    a = mesh.arrays()
+    g = hm.HMatrix.kelvin(mesh, b_min=64, eta=1.0, device=0)
+    g.assemble(eps=1e-5, beta=0.8, lookahead=2)
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=64, eta=1.0)
+    return dict(g=g, o=o, mesh=mesh)
+
+
+def test_config3_partition_and_sampled_aca(c3):
+    g, o = c3["g"], c3["o"]
+    assert g.partition_json() == o.partition_json()
+    blocks = g.partition_blocks()
+    t = g.tree()
+    gk, gl, _, _ = g.ranks()
+    adm = np.nonzero(blocks[:, 2])[0]
+    sizes = t.nodes[blocks[adm, 0], 1] - t.nodes[blocks[adm, 0], 0]
+    rng = np.random.default_rng(0)
+    pick = list(adm[np.argsort(-sizes)[:6]]) + list(rng.choice(adm, 40, replace=False))
+    for b in pick:
+        comp = int(rng.integers(0, 6))
+        kc, K, fs, _ = o.aca_block(comp, int(b), eps=1e-5, beta=0.8, lookahead=2)
+        assert (gk[comp, b], gl[comp, b]) == (kc, K), (b, comp)
+        assert g.factor(comp, int(b))["frob_sq"] == fs
+
+
+def test_config3_sampled_nearfield(c3):
+    g, o = c3["g"], c3["o"]
+    blocks = g.partition_blocks()
+    t = g.tree()
+    dense = np.nonzero(blocks[:, 2] == 0)[0]
+    rng = np.random.default_rng(1)
+    for b in rng.choice(dense, 6, replace=False):
+        rn, cn = blocks[b, 0], blocks[b, 1]
+        rows = t.perm[t.nodes[rn, 0]:t.nodes[rn, 1]]
+        cols = t.perm[t.nodes[cn, 0]:t.nodes[cn, 1]]
+        comp = int(rng.integers(0, 6))
+        got = g.dense_block(comp, int(b))
+        for ii in rng.choice(len(rows), 6, replace=False):
+            for jj in rng.choice(len(cols), 6, replace=False):
+                want = o.entry(comp, int(rows[ii]), int(cols[jj]))
+                if rows[ii] == cols[jj]:
+                    assert got[ii, jj] == pytest.approx(want, rel=1e-13)
+                else:
+                    assert got[ii, jj] == want
+
+
+def test_config3_matvec_properties(c3):
+    g, o = c3["g"], c3["o"]
+    n = g.cols
+    x1 = hm.random_vector(n, 2, "normal")
+    x2 = hm.random_vector(n, 3, "normal")
+    y1 = g.matvec(x1)
+    assert (y1 == g.matvec(x1)).all()  # deterministic, no atomics
+    y12 = g.matvec(0.75 * x1 - 2.0 * x2)
+    assert rel(y12, 0.75 * y1 - 2.0 * g.matvec(x2)) < 1e-12
+    # rows of A x from oracle entries (H-approximation tolerance 10 eps)
+    N = n // 3
+    rng = np.random.default_rng(2)
+    for i in rng.choice(N, 2, replace=False):
+        r = int(rng.integers(0, 3))
+        exact = 0.0
+        mag = 0.0
+        for c in range(3):
+            comp = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 1): 3, (1, 2): 4, (2, 2): 5}[
+                (min(r, c), max(r, c))]
+            row = np.array([o.entry(comp, int(i), j) for j in range(N)])
+            exact += row @ x1[c * N:(c + 1) * N]
+            mag += np.abs(row) @ np.abs(x1[c * N:(c + 1) * N])
+        assert abs(y1[r * N + i] - exact) <= 1e-4 * mag
+
+
+def test_config4_amvm_matches_oracle():
+    mesh = hm.Mesh.ellipsoid(6, 2.0, 1.0, 0.5)
+    a = mesh.arrays()
+    g = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+    g.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=32, eta=1.0)
+    o.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    c = a["centroids"]
+    bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.05 ** 2))
+    x = np.tile(bump, 3) + 1e-3 * hm.random_vector(3 * len(c), 3)
+    bg, rep = g.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, max_iterations=5)
+    bo, it, conv = o.amvm(x, theta=0.7, eps_amvm=1e-6, max_iterations=5)
+    assert len(rep.iterations) == len(it)
+    for r, ref in zip(rep.iterations, it):
+        assert r.gamma == ref[1] and r.marked == int(ref[3])
+        assert r.cumulative_pivots == int(ref[4])
+    assert rel(bg, bo) < 1e-12
+    gk, gl, _, _ = g.ranks()
+    ok, ol, _, _ = o.ranks()
+    assert (gk == ok).all() and (gl == ol).all()
