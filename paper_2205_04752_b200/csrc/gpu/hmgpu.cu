@@ -167,6 +167,9 @@ struct hmgpu_ctx {
   size_t p_smem = 0;
   DBuf<WJob> d_pjobs;
   DBuf<WChunk> d_pchunks;
+  DBuf<int> d_pwoff;
+  int p_woff_base[2] = {0, 0}, p_chunk_base[2] = {0, 0};
+  int p_nwarps = 0, p_njb = 0;
   DBuf<double> d_sarena, d_zpart;
   DBuf<LeafEntry> d_pentries;
   DBuf<int> d_pleaf_ptr;
@@ -192,7 +195,7 @@ struct hmgpu_ctx {
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
     d_leaf_ptr.free(); d_leaf_prow.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
-    d_pjobs.free(); d_pchunks.free(); d_sarena.free(); d_zpart.free();
+    d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
     if (stream) cudaStreamDestroy(stream);
   }
@@ -835,19 +838,32 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return sz[a] > sz[b]; });
     return o;
   };
+  // job table (pass A then pass B, each largest first) and, per pass, a
+  // warp-major chunk table for the static round-robin job -> warp mapping
+  const int NWARPS = c->sm_count * cfg.warps;
   std::vector<WJob> jobs;
   std::vector<WChunk> chunks;
+  std::vector<int> woff;
   for (int pass = 0; pass < 2; ++pass) {
     auto& J = pass == 0 ? ja : jb;
     auto& C = pass == 0 ? ca : cb;
-    for (int idx : order(C)) {
-      WJob j = J[idx];
-      j.chunk0 = (int)chunks.size();
-      j.nchunks = (int)C[idx].size();
-      chunks.insert(chunks.end(), C[idx].begin(), C[idx].end());
-      jobs.push_back(j);
+    const std::vector<int> ord = order(C);
+    const int jbase = (int)jobs.size();
+    for (int idx : ord) jobs.push_back(J[idx]);
+    c->p_woff_base[pass] = (int)woff.size();
+    c->p_chunk_base[pass] = (int)chunks.size();
+    for (int w = 0; w < NWARPS; ++w) {
+      woff.push_back((int)chunks.size() - c->p_chunk_base[pass]);
+      for (int q = w; q < (int)ord.size(); q += NWARPS) {
+        for (WChunk ch : C[ord[q]]) {
+          ch.job = jbase + q;
+          chunks.push_back(ch);
+        }
+      }
     }
+    woff.push_back((int)chunks.size() - c->p_chunk_base[pass]);
   }
+  c->p_nwarps = NWARPS;
   std::vector<LeafEntry> entries;
   c->p_leaf_ptr.assign(nl + 1, 0);
   for (int l = 0; l < nl; ++l) {
@@ -868,10 +884,12 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   }
   c->d_pjobs.upload(jobs, c->stream);
   c->d_pchunks.upload(chunks, c->stream);
+  c->d_pwoff.upload(woff, c->stream);
   c->d_pentries.upload(entries, c->stream);
   c->d_pleaf_ptr.upload(c->p_leaf_ptr, c->stream);
   c->p_ntasks = (int)jobs.size();
   c->p_nz = (int)ja.size();  // pass A = [0, p_nz), pass B = USPLIT
+  c->p_njb = (int)jb.size();
   c->p_slots = slots;
   c->p_zslots = wslots;
   c->p_arena_len = alen;
@@ -912,11 +930,13 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
   const MvCfg cfg = mv_cfg();
   P.stage = cfg.stage;
   P.scratch = cfg.scratch;
-  auto run = [&](int first, int count, const char* name) {
+  P.jobs = c->d_pjobs.p;
+  P.nwarps = c->p_nwarps;
+  auto run = [&](int pass, int count, const char* name) {
     if (count <= 0) return;
-    P.jobs = c->d_pjobs.p + first;
-    P.njobs = count;
-    const int g = std::min(c->sm_count, (count + cfg.warps - 1) / cfg.warps);
+    P.chunks = c->d_pchunks.p + c->p_chunk_base[pass];
+    P.woff = c->d_pwoff.p + c->p_woff_base[pass];
+    const int g = c->p_nwarps / cfg.warps;  // the layout's grid: one CTA per SM
     auto go = [&](auto kernel) {
       CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->p_smem));
@@ -936,7 +956,7 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
 #undef HMV_CASE
   };
   run(0, c->p_nz, "hmv_stream");
-  run(c->p_nz, c->p_ntasks - c->p_nz, "hmv_ypart");
+  run(1, c->p_njb, "hmv_ypart");
   c->timed("hmv_reduce", [&] {
     const int nl = (int)c->leaf_begin.size();
     const int g = grid_for(c, nl, 16);

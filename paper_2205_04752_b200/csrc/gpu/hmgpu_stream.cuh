@@ -58,7 +58,7 @@ struct __align__(16) WChunk {
   int aux_len;     // rows (WA_X) or columns (WA_W), 4 doubles each
   int g0, g1;      // column range (FUSED V/U part, USPLIT, DENSE) or row range (VSPLIT)
   int part;        // FUSED: 0 = V part, 1 = U part
-  int pad;
+  int job;         // index of the chunk's job in the job table
 };
 static_assert(sizeof(WChunk) == 48, "WChunk layout");
 
@@ -114,8 +114,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // ---------------------------------------------------------------------------
 struct WarpStreamParams {
   const WJob* jobs;
-  int njobs;
-  const WChunk* chunks;
+  const WChunk* chunks;   // warp-major: warp w's chunks at [woff[w], woff[w+1])
+  const int* woff;
+  int nwarps;             // warps the chunk table was laid out for
   const double* arena;   // packed factors
   const double* dense;   // near-field blocks, [j][c][i] per block
   const double* xi;      // gathered x, 4 doubles per internal column (x, y, z, 0)
@@ -331,7 +332,6 @@ hmv_warp_kernel(WarpStreamParams P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bars[WARPS * NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NW = gridDim.x * WARPS;
   const int gw = blockIdx.x * WARPS + warp;
   double* ring = sm + (long long)warp * (NS * P.stage + P.scratch);
   double* scratch = ring + NS * P.stage;
@@ -343,55 +343,46 @@ hmv_warp_kernel(WarpStreamParams P) {
   }
   __syncwarp();
 
-  // issue cursor (lane 0): the descriptor of the next chunk to issue is
-  // loaded one issue ahead so its global latency is off the critical path
-  int ij = gw, ic = 0, ijc = 0, ijn = 0;
-  WChunk nx{};
-  auto advance = [&]() {
-    if (++ic == ijn) {
-      ic = 0;
-      ij += NW;
-      if (ij < P.njobs) {
-        ijc = P.jobs[ij].chunk0;
-        ijn = P.jobs[ij].nchunks;
-      }
-    }
-    if (ij < P.njobs) nx = P.chunks[ijc + ic];
+  // this warp's chunk sequence; descriptors are fetched 32 at a time (one
+  // coalesced load, lane l holds chunk base + l) and handed to lane 0 by
+  // shuffles when it issues, so no global latency sits on the issue path
+  const int c0 = gw < P.nwarps ? P.woff[gw] : 0;
+  const int nch = gw < P.nwarps ? P.woff[gw + 1] - c0 : 0;
+  WChunk win{};
+  int win_base = -64;
+  auto load_window = [&](int base) {
+    win_base = base;
+    if (base + lane < nch) win = P.chunks[c0 + base + lane];
   };
-  if (lane == 0 && ij < P.njobs) {
-    ijc = P.jobs[ij].chunk0;
-    ijn = P.jobs[ij].nchunks;
-    nx = P.chunks[ijc];
-  }
-  auto issue_next = [&](int s) {
-    if (ij >= P.njobs) return;
-    const WChunk ch = nx;
-    double* st = ring + s * P.stage;
-    const uint32_t bytes = (uint32_t)ch.len * 8u;
-    const uint32_t abytes = ch.aux_kind == WA_NONE ? 0u : (uint32_t)ch.aux_len * 32u;
-    mbar_expect_tx(&bar[s], 128u + bytes + abytes);
-    bulk_g2s(st, &P.chunks[ijc + ic], 48u, &bar[s]);
-    bulk_g2s(st + 6, &P.jobs[ij], 80u, &bar[s]);
-    if (bytes)
-      bulk_g2s(st + kHdr, (ch.src_kind == 0 ? P.arena : P.dense) + ch.src, bytes, &bar[s]);
-    if (abytes)
-      bulk_g2s(st + kHdr + ch.len, (ch.aux_kind == WA_X ? P.xi : P.win) + ch.aux * 4,
-               abytes, &bar[s]);
-    advance();
-  };
-  int issued = 0;  // lane 0's count, broadcast after every issue
-  if (lane == 0)
-    for (int s = 0; s < NS; ++s) {
-      const bool any = ij < P.njobs;
-      issue_next(s);
-      issued += any ? 1 : 0;
+  auto issue = [&](int idx, int s) {  // all lanes call (shuffles), lane 0 issues
+    if (idx >= nch) return;
+    if (idx >= win_base + 32) load_window(idx & ~31);
+    const int src_l = idx - win_base;
+    const long long src = __shfl_sync(0xffffffffu, win.src, src_l);
+    const long long aux = __shfl_sync(0xffffffffu, win.aux, src_l);
+    const int len = __shfl_sync(0xffffffffu, win.len, src_l);
+    const int kinds = __shfl_sync(0xffffffffu, win.src_kind | (win.aux_kind << 4), src_l);
+    const int aux_len = __shfl_sync(0xffffffffu, win.aux_len, src_l);
+    const int job = __shfl_sync(0xffffffffu, win.job, src_l);
+    if (lane == 0) {
+      double* st = ring + s * P.stage;
+      const int src_kind = kinds & 15, aux_kind = kinds >> 4;
+      const uint32_t bytes = (uint32_t)len * 8u;
+      const uint32_t abytes = aux_kind == WA_NONE ? 0u : (uint32_t)aux_len * 32u;
+      fence_proxy_async();
+      mbar_expect_tx(&bar[s], 128u + bytes + abytes);
+      bulk_g2s(st, &P.chunks[c0 + idx], 48u, &bar[s]);
+      bulk_g2s(st + 6, &P.jobs[job], 80u, &bar[s]);
+      if (bytes) bulk_g2s(st + kHdr, (src_kind == 0 ? P.arena : P.dense) + src, bytes, &bar[s]);
+      if (abytes)
+        bulk_g2s(st + kHdr + len, (aux_kind == WA_X ? P.xi : P.win) + aux * 4, abytes, &bar[s]);
     }
-  issued = __shfl_sync(0xffffffffu, issued, 0);
+  };
+  for (int s = 0; s < NS; ++s) issue(s, s);
 
-  int consumed = 0;
   double y[6] = {0, 0, 0, 0, 0, 0};     // rows lane, lane+32 x 3 outputs
   double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // VSPLIT dot products
-  while (consumed < issued) {
+  for (int consumed = 0; consumed < nch; ++consumed) {
     const int s = consumed % NS;
     mbar_wait(&bar[s], (uint32_t)((consumed / NS) & 1));
     const double* st = ring + s * P.stage;
@@ -458,13 +449,7 @@ hmv_warp_kernel(WarpStreamParams P) {
       }
     }
     __syncwarp();  // all lanes done with stage s
-    if (lane == 0 && ij < P.njobs) {
-      fence_proxy_async();
-      issue_next(s);
-      ++issued;
-    }
-    ++consumed;
-    issued = __shfl_sync(0xffffffffu, issued, 0);
+    issue(consumed + NS, s);
   }
 }
 
