@@ -246,10 +246,16 @@ def run_ours(args, cfg):
     n = h.cols
     # ---- assembly (timed on the device, best of 2 after one warm-up) ----
     asm = []
+    h.set_profiling(True)
     for _ in range(3):
+        for k in ("aca", "nearfield", "compact", "relocate"):
+            h.kernel_times(k, reset=True)
         st = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        asm.append(st)
-    best = min(asm[1:], key=lambda s: s.ms_total)
+        kt_asm = {k: h.kernel_times(k, reset=True)[0]
+                  for k in ("aca", "nearfield", "compact", "relocate")}
+        asm.append((st, kt_asm))
+    h.set_profiling(False)
+    best, best_kt = min(asm[1:], key=lambda p: p[0].ms_total)
     storage = h.storage()
     fp64_peak = hm.fp64_peak_tflops(device)
 
@@ -380,10 +386,17 @@ def run_ours(args, cfg):
                                           (kt["hmv_ypart"][1] > 0))),
         "clocks": ck,
         "assembly": {"value": entries / asm_s, "unit": "entries/s", "ms": best.ms_total,
-                     "ms_nearfield": best.ms_nearfield, "aca_entries": best.aca_entries,
+                     "kernel_ms": best_kt, "aca_entries": best.aca_entries,
                      "dense_entries": best.dense_entries, "pivots": best.pivots,
+                     "storage_mb": storage["mb_current"],
+                     # counted flops: 30 n_q + 1 per component entry
+                     "counted_tflops": best.counted_flops / asm_s / 1e12,
                      "fp64_peak_tflops_measured": fp64_peak,
-                     "storage_mb": storage["mb_current"]},
+                     "fp64_frac": best.counted_flops / asm_s / 1e12 / fp64_peak,
+                     "fp64_frac_kernels": best.counted_flops /
+                     ((best_kt["aca"] + best_kt["nearfield"]) * 1e-3) / 1e12 / fp64_peak,
+                     "nearfield_entries_per_s": best.dense_entries /
+                     (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None},
         "kernel_ms": {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kt.items()},
     }
     if res is not None:

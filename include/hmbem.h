@@ -93,10 +93,10 @@ int hmb_partition_info(const hmb_op* op, int* n_blocks, int* n_admissible, int* 
 int hmb_partition_blocks(const hmb_op* op, int* blocks4);
 int hmb_partition_json(const hmb_op* op, char* buf, long long* len);
 
-/* stats7: aca_entries, dense_entries, aca_steps, pivots, ms_total,
- * ms_nearfield, relaunches (NULL allowed) */
+/* stats8: aca_entries, dense_entries, aca_steps, pivots, ms_total,
+ * ms_nearfield, relaunches, counted_flops (NULL allowed) */
 int hmb_assemble(hmb_op* op, double eps, double beta, int initial_rank,
-                 int lookahead, long long max_rank, double* stats7);
+                 int lookahead, long long max_rank, double* stats8);
 int hmb_matvec(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
                int device_ptrs);
 int hmb_ranks(const hmb_op* op, int* k_cur, int* k_look, int* consumed, int* last_stop);

@@ -86,6 +86,8 @@ typedef struct hmgpu_assembly_stats {
   double ms_nearfield;        /* device time of the near-field fill */
   double ms_aca;              /* device time of the ACA launches */
   int aca_relaunches;         /* capacity regrow passes */
+  double counted_flops;       /* Kelvin only: sum of 30 n_q + 1 per component entry
+                                 (SURVEY.md 8d convention, n_q = rule points) */
 } hmgpu_assembly_stats;
 
 typedef struct hmgpu_storage_info {

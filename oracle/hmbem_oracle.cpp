@@ -311,6 +311,22 @@ static void voxel_surface(int n, Real lo, Real hi, Mesh& mesh) {
 }
 
 // ---------------------------------------------------------------------------
+// 1/sqrt(x), x > 0: bit-level seed 0x5fe6eb50c7b537a9 - (bits(x) >> 1) and
+// four Newton steps y <- y * fma(-(x/2 * y), y, 1.5).  Part of the canonical
+// evaluation order shared with the device (rsqrt_canon in
+// paper_2205_04752_b200/csrc/gpu/hmgpu_device.cuh): deterministic, ~1 ulp.
+static inline Real rsqrt_canon(Real x) {
+  long long i;
+  std::memcpy(&i, &x, sizeof(i));
+  i = 0x5fe6eb50c7b537a9LL - (i >> 1);
+  Real y;
+  std::memcpy(&y, &i, sizeof(y));
+  const Real h = 0.5 * x;
+  for (int it = 0; it < 4; ++it) y = y * std::fma(-(h * y), y, 1.5);
+  return y;
+}
+
+// ---------------------------------------------------------------------------
 // Kelvin tensor and collocation entries
 struct Material {
   Real E = 1.0, nu = 0.3;
@@ -360,7 +376,7 @@ struct Kelvin {
   // with S(x)_rc = c [(3-4nu) delta_rc / |x| + x_r x_c / |x|^3]
   // (kelvin_tensor, kernels.cpp:21-28).  Canonical evaluation order, shared
   // bit for bit with the device kernels: the constant c is factored out of
-  // the quadrature sum, 1/|x| is one IEEE division of an IEEE square root,
+  // the quadrature sum, 1/|x| is rsqrt_canon (bit-seeded Newton, ~1 ulp),
   // and every fused multiply-add is written explicitly (std::fma); Eigen's
   // own association is not recoverable here, so this order
   // is the parity contract.  Agrees with the literal kelvin_tensor form to
@@ -377,7 +393,7 @@ struct Kelvin {
       const Real dy = p[1] - std::fma(b, e2[1], std::fma(a, e1[1], y0[1]));
       const Real dz = p[2] - std::fma(b, e2[2], std::fma(a, e1[2], y0[2]));
       const Real r2 = std::fma(dz, dz, std::fma(dy, dy, dx * dx));
-      const Real ri = 1.0 / std::sqrt(r2);
+      const Real ri = rsqrt_canon(r2);
       const Real wr = w * ri;
       const Real d[3] = {dx, dy, dz};
       acc_d = acc_d + wr;

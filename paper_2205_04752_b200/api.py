@@ -178,6 +178,7 @@ class AssemblyStats:
     ms_total: float
     ms_nearfield: float
     relaunches: int
+    counted_flops: float = 0.0
 
     @property
     def entries(self) -> int:
@@ -338,12 +339,12 @@ class HMatrix:
     # ---- assembly / products ----
     def assemble(self, cfg: Optional[AssemblyConfig] = None, **kw) -> AssemblyStats:
         cfg = cfg or AssemblyConfig(**kw)
-        st = np.zeros(7)
+        st = np.zeros(8)
         _check(_h.hmb_assemble(self._h, cfg.eps, cfg.beta, cfg.initial_rank,
                                cfg.lookahead, cfg.max_rank, _ptr(st)))
         self.config = cfg
         self.last_stats = AssemblyStats(int(st[0]), int(st[1]), int(st[2]), int(st[3]),
-                                        float(st[4]), float(st[5]), int(st[6]))
+                                        float(st[4]), float(st[5]), int(st[6]), float(st[7]))
         return self.last_stats
 
     def matvec(self, x, mode: Mode = Mode.Current) -> np.ndarray:

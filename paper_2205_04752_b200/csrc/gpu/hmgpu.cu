@@ -145,6 +145,7 @@ struct hmgpu_ctx {
   long long dense_used = 0;
   DBuf<DenseBlock> d_dblocks;
   DBuf<int> d_counter, d_overflow, d_list;
+  DBuf<unsigned long long> d_nq;  // near-field quadrature points (counted flops)
 
   // ---- matvec structures ----
   std::vector<MvBlock> mvb;
@@ -430,12 +431,17 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches) {
     CK(cudaMemsetAsync(c->d_counter.p, 0, sizeof(int), c->stream));
     CK(cudaMemsetAsync(c->d_overflow.p, 0, sizeof(int), c->stream));
     const int nwarps = (int)list.size();
-    const int grid = grid_for(c, (nwarps + 7) / 8, 8);
+    const int grid = grid_for(c, (nwarps + 7) / 8, 16);
     c->timed("aca", [&] {
-      aca_kernel<<<grid, 256, 0, c->stream>>>(
-          c->geom, c->d_items.p, c->d_list.p, (int)list.size(), c->d_counter.p,
-          c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
-          c->d_overflow.p);
+      auto go = [&](auto kernel) {
+        kernel<<<grid, 256, 0, c->stream>>>(
+            c->geom, c->d_items.p, c->d_list.p, (int)list.size(), c->d_counter.p,
+            c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
+            c->d_overflow.p);
+      };
+      if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
+      else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
+      else go(aca_kernel<KIND_DENSE>);
     });
     int over = 0;
     CK(cudaMemcpyAsync(&over, c->d_overflow.p, sizeof(int), cudaMemcpyDeviceToHost,
@@ -1032,6 +1038,7 @@ int hmgpu_create(int device, hmgpu_ctx** out) {
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     c->d_counter.alloc(1);
     c->d_overflow.alloc(1);
+    c->d_nq.alloc(1);
     c->rules.far_ratio = 4.0;
     c->rules.mid_ratio = 1.5;
   });
@@ -1302,16 +1309,17 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
 
     phase("alloc+upload");
     // near-field fill
+    CK(cudaMemsetAsync(c->d_nq.p, 0, sizeof(unsigned long long), c->stream));
     CK(cudaEventRecord(tn0, c->stream));
     if (!c->dblocks.empty()) {
       c->timed("nearfield", [&] {
         const int grid = grid_for(c, (long long)c->dblocks.size(), 8);
         if (c->NC == 6)
           nearfield_kernel<6><<<grid, 256, 0, c->stream>>>(
-              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p);
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p, c->d_nq.p);
         else
           nearfield_kernel<1><<<grid, 256, 0, c->stream>>>(
-              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p);
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p, c->d_nq.p);
       });
     }
     CK(cudaEventRecord(tn1, c->stream));
@@ -1351,17 +1359,25 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     c->assembled = true;
     if (stats) {
       hmgpu_assembly_stats s{};
+      unsigned long long nq_dense = 0;
+      CK(cudaMemcpy(&nq_dense, c->d_nq.p, sizeof(nq_dense), cudaMemcpyDeviceToHost));
+      double flops = 0.0;
       for (const Item& it : c->items) {
         s.aca_entries += it.entries;
         s.aca_steps += it.steps;
         s.pivots += it.k;
+        flops += 30.0 * (double)it.nq_sum + (double)it.entries;
       }
+      // near-field: one rule per pair, six component entries of 30 n_q + 1
+      flops += 6.0 * 30.0 * (double)nq_dense;
       for (const DenseBlock& d : c->dblocks)
         s.dense_entries += (long long)c->NC * d.m * d.n;
       s.ms_total = ms_total;
       s.ms_nearfield = ms_near;
       s.ms_aca = ms_total - ms_near;
       s.aca_relaunches = relaunch;
+      for (const DenseBlock& d : c->dblocks) flops += (double)c->NC * d.m * d.n;
+      s.counted_flops = c->kind == KIND_KELVIN ? flops : 0.0;
       *stats = s;
     }
   });

@@ -61,6 +61,20 @@ __device__ __forceinline__ int kelvin_tier(double px, double py, double pz,
   return 2;
 }
 
+// 1/sqrt(x) for x > 0: bit-level seed and four Newton steps written with
+// explicit IEEE operations, y <- y (1.5 - (x/2) y y).  Deterministic, ~1 ulp,
+// and restated operation for operation by the oracle (oracle/hmbem_oracle.cpp
+// rsqrt_canon), so entries stay bit-identical; about 4x cheaper than the
+// IEEE division of an IEEE square root.
+__device__ __forceinline__ double rsqrt_canon(double x) {
+  const long long i = 0x5fe6eb50c7b537a9LL - (__double_as_longlong(x) >> 1);
+  double y = __longlong_as_double(i);
+  const double h = 0.5 * x;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) y = y * fma(-(h * y), y, 1.5);
+  return y;
+}
+
 __device__ __forceinline__ double sel3(int r, double x, double y, double z) {
   return r == 0 ? x : (r == 1 ? y : z);
 }
@@ -68,7 +82,7 @@ __device__ __forceinline__ double sel3(int r, double x, double y, double z) {
 // Exact integral of the Kelvin tensor over the flat triangle for a point p
 // in its plane (builder-defined self term, closed form; see
 // oracle/hmbem_oracle.cpp Kelvin::self_term for the derivation).
-__device__ void kelvin_self6(const Geom& g, double px, double py, double pz,
+__device__ __noinline__ void kelvin_self6(const Geom& g, double px, double py, double pz,
                              const double* T, double* out6) {
   const double v[3][3] = {{T[0], T[1], T[2]},
                           {T[0] + T[3], T[1] + T[4], T[2] + T[5]},
@@ -120,11 +134,11 @@ __device__ void kelvin_self6(const Geom& g, double px, double py, double pz,
 // (colloc_single, kernels.cpp:176-187), S from kelvin_tensor (:21-28).
 // Canonical evaluation order (the parity contract with the CPU oracle,
 // oracle/hmbem_oracle.cpp Kelvin::colloc_single): c factored out of the
-// sum, 1/|x| as one IEEE division of an IEEE square root, explicit fma
+// sum, 1/|x| by rsqrt_canon (deterministic Newton), explicit fma
 // (the library is compiled with --fmad=false so nothing else contracts).
 // With it ACA pivots, ranks and factors are bit-identical to the oracle.
 __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
-                                                int comp) {
+                                                int comp, int& nq_acc) {
   const double4 p = g.rowpt[i];
   const double* T = g.tri + 16LL * j;
   const int r = c_comp_r[comp], c = c_comp_c[comp];
@@ -139,6 +153,7 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
   const double e2x = T[6], e2y = T[7], e2z = T[8];
   double acc_d = 0.0, acc_x = 0.0;
   const int nq = c_rules.n[tier];
+  nq_acc += nq;
   for (int q = 0; q < nq; ++q) {
     const double a = c_rules.a[tier][q], b = c_rules.b[tier][q],
                  w = c_rules.w[tier][q];
@@ -146,7 +161,7 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
     const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
     const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    const double ri = 1.0 / sqrt(r2);
+    const double ri = rsqrt_canon(r2);
     const double wr = w * ri;
     acc_d = acc_d + wr;
     acc_x = fma(wr * ri * ri, sel3(r, dx, dy, dz) * sel3(c, dx, dy, dz), acc_x);
@@ -158,7 +173,7 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
 // all six components of one (point, triangle) pair (near-field fill), each
 // in the same canonical order as kelvin_entry1
 __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
-                                              double* out6) {
+                                              double* out6, int& nq_acc) {
   const double4 p = g.rowpt[i];
   const double* T = g.tri + 16LL * j;
   if (g.same_tree && i == j) {
@@ -172,6 +187,7 @@ __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
   double ad = 0.0, a00 = 0.0, a01 = 0.0, a02 = 0.0, a11 = 0.0, a12 = 0.0,
          a22 = 0.0;
   const int nq = c_rules.n[tier];
+  nq_acc += nq;
   for (int q = 0; q < nq; ++q) {
     const double a = c_rules.a[tier][q], b = c_rules.b[tier][q],
                  w = c_rules.w[tier][q];
@@ -179,7 +195,7 @@ __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
     const double dy = p.y - fma(b, e2y, fma(a, e1y, v0y));
     const double dz = p.z - fma(b, e2z, fma(a, e1z, v0z));
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    const double ri = 1.0 / sqrt(r2);
+    const double ri = rsqrt_canon(r2);
     const double wr = w * ri;
     const double w3 = wr * ri * ri;
     ad = ad + wr;
@@ -217,8 +233,18 @@ __device__ __forceinline__ double dense_entry(const Geom& g, int i, int j) {
 // single entry of component `comp` at internal (row i, col j)
 __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
                                          int comp) {
-  if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp);
+  int nq = 0;
+  if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq);
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
+  return dense_entry(g, i, j);
+}
+// the same with the provider fixed at compile time (ACA kernel instances);
+// nq_acc accumulates the quadrature points used (counted-flop bookkeeping)
+template <int KIND>
+__device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
+                                          int& nq_acc) {
+  if (KIND == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq_acc);
+  if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
 
@@ -241,7 +267,7 @@ struct __align__(16) Item {
   double frob_sq;
   long long entries;        // kernel entries evaluated
   long long steps;          // cross attempts (incl. vanishing rows)
-  long long pad2;
+  long long nq_sum;         // quadrature points over all evaluated entries
 };
 static_assert(sizeof(Item) == 128, "Item layout");
 
@@ -279,9 +305,10 @@ __device__ __forceinline__ int warp_min_int(int v) {
 // sf < 0 disables the accuracy test (extension mode).  The candidate row
 // residual is built in V(:,k) and the column residual in U(:,k); both are
 // only committed (k += 1) when the step is accepted.
+template <int KIND>
 __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
                              double* __restrict__ V, int2* __restrict__ piv,
-                             uint8_t* __restrict__ Z, double sf, int lane) {
+                             uint8_t* __restrict__ Z, double sf, int lane, int& nq_acc) {
   const int m = s.m, n = s.n, k = s.k;
   const int comp = s.comp;
   for (;;) {
@@ -317,7 +344,7 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
     double rs = 0.0, pm = -1.0, pv = 0.0;
     int pj = -1;
     for (int c = lane; c < n; c += 32) {
-      double val = entry1(g, s.row0 + i, s.col0 + c, comp);
+      double val = entry_k<KIND>(g, s.row0 + i, s.col0 + c, comp, nq_acc);
       rs = fmax(rs, fabs(val));
       for (int l = 0; l < k; ++l)
         val = fma(-U[(long long)l * m + i], V[(long long)l * n + c], val);
@@ -346,7 +373,7 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
     double* uk = U + (long long)k * m;
     double uu = 0.0;
     for (int r = lane; r < m; r += 32) {
-      double val = entry1(g, s.row0 + r, s.col0 + j, comp);
+      double val = entry_k<KIND>(g, s.row0 + r, s.col0 + j, comp, nq_acc);
       for (int l = 0; l < k; ++l)
         val = fma(-V[(long long)l * n + j], U[(long long)l * m + r], val);
       uk[r] = val;
@@ -383,6 +410,7 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
 //   PH_RUN  aca_run to the stopping rule (aca.cpp:106-124)
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
 //   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
+template <int KIND>
 __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
                               double* __restrict__ arena, int2* __restrict__ pivots,
                               uint8_t* __restrict__ cons, double sf_run,
@@ -396,12 +424,13 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
   const long long capr_ll = min(max_rank, (long long)min(s.m, s.n));
   const int capr = (int)capr_ll;
   s.status = ST_OK;
+  int nq_acc = 0;
   while (s.phase != PH_DONE) {
     if (s.phase == PH_RUN) {
       bool stopped = false;
       while (s.k < capr) {
         if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
-        const int st = aca_step_warp(g, s, U, V, piv, Z, sf_run, lane);
+        const int st = aca_step_warp<KIND>(g, s, U, V, piv, Z, sf_run, lane, nq_acc);
         if (st != STOP_NONE) {
           s.last_stop = st;
           stopped = true;
@@ -416,7 +445,7 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
       bool stopped = false;
       while (s.steps_left > 0 && s.k < capr) {
         if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
-        const int st = aca_step_warp(g, s, U, V, piv, Z, -1.0, lane);
+        const int st = aca_step_warp<KIND>(g, s, U, V, piv, Z, -1.0, lane, nq_acc);
         if (st != STOP_NONE) {
           s.last_stop = st;
           stopped = true;
@@ -440,6 +469,12 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
   }
 save:
   __syncwarp();
+  {
+    long long t = nq_acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    s.nq_sum += t;
+  }
   if (lane == 0) {
     items[idx] = s;
     if (s.status == ST_OVERFLOW) atomicAdd(overflow, 1);
@@ -447,7 +482,8 @@ save:
 }
 
 // warps pull items from `list` (largest first) through a global counter
-__global__ void __launch_bounds__(256)
+template <int KIND>
+__global__ void __launch_bounds__(256, 2)
 aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
            int nlist, int* __restrict__ counter, double* __restrict__ arena,
            int2* __restrict__ pivots, uint8_t* __restrict__ cons, double sf_run,
@@ -458,8 +494,8 @@ aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
     if (lane == 0) t = atomicAdd(counter, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nlist) return;
-    aca_item_warp(g, items, list[t], arena, pivots, cons, sf_run, max_rank,
-                  lookahead, overflow, lane);
+    aca_item_warp<KIND>(g, items, list[t], arena, pivots, cons, sf_run, max_rank,
+                        lookahead, overflow, lane);
   }
 }
 
@@ -477,7 +513,8 @@ struct DenseBlock {
 template <int NC>
 __global__ void __launch_bounds__(256)
 nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
-                 double* __restrict__ dense) {
+                 double* __restrict__ dense, unsigned long long* __restrict__ nq_total) {
+  int nq_acc = 0;
   for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
     const DenseBlock b = blocks[bi];
     const int mn = b.m * b.n;
@@ -488,7 +525,7 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
       if (NC == 6) {
         double e[6];
         if (g.kind == KIND_KELVIN) {
-          kelvin_entry6(g, b.row0 + i, b.col0 + j, e);
+          kelvin_entry6(g, b.row0 + i, b.col0 + j, e, nq_acc);
         } else {
           const double v = entry1(g, b.row0 + i, b.col0 + j, 0);
 #pragma unroll
@@ -501,6 +538,10 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
       }
     }
   }
+  unsigned long long t = (unsigned long long)nq_acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(nq_total, t);
 }
 
 // ---------------------------------------------------------------------------

@@ -354,7 +354,7 @@ int hmb_partition_json(const hmb_op* op, char* buf, long long* len) {
 }
 
 int hmb_assemble(hmb_op* op, double eps, double beta, int initial_rank, int lookahead,
-                 long long max_rank, double* stats7) {
+                 long long max_rank, double* stats8) {
   return guard([&] {
     need(op, "op");
     hmb::AssemblyConfig cfg;
@@ -364,14 +364,15 @@ int hmb_assemble(hmb_op* op, double eps, double beta, int initial_rank, int look
     cfg.lookahead = lookahead;
     cfg.max_rank = max_rank;
     const hmb::AssemblyStats s = op->op->assemble(cfg);
-    if (stats7) {
-      stats7[0] = static_cast<double>(s.aca_entries);
-      stats7[1] = static_cast<double>(s.dense_entries);
-      stats7[2] = static_cast<double>(s.aca_steps);
-      stats7[3] = static_cast<double>(s.pivots);
-      stats7[4] = s.ms_total;
-      stats7[5] = s.ms_nearfield;
-      stats7[6] = s.relaunches;
+    if (stats8) {
+      stats8[0] = static_cast<double>(s.aca_entries);
+      stats8[1] = static_cast<double>(s.dense_entries);
+      stats8[2] = static_cast<double>(s.aca_steps);
+      stats8[3] = static_cast<double>(s.pivots);
+      stats8[4] = s.ms_total;
+      stats8[5] = s.ms_nearfield;
+      stats8[6] = s.relaunches;
+      stats8[7] = s.counted_flops;
     }
   });
 }

@@ -227,6 +227,7 @@ AssemblyStats HOperator::assemble(const AssemblyConfig& cfg) {
   out.ms_nearfield = s.ms_nearfield;
   out.ms_aca = s.ms_aca;
   out.relaunches = s.aca_relaunches;
+  out.counted_flops = s.counted_flops;
   return out;
 }
 

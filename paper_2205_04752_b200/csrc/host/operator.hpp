@@ -38,6 +38,7 @@ struct AssemblyStats {
   long long aca_entries = 0, dense_entries = 0, aca_steps = 0, pivots = 0;
   double ms_total = 0, ms_nearfield = 0, ms_aca = 0;
   int relaunches = 0;
+  double counted_flops = 0;  // 30 n_q + 1 per Kelvin component entry
 };
 
 // Which rows of the operator this process owns (block-row sharding over
