@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "hmgpu.h"
 #include "hmgpu_device.cuh"
 #include "hmgpu_stream.cuh"
@@ -46,19 +48,62 @@ struct Fail {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
 
+// Device buffers are stream-ordered allocations from the context's own
+// memory pool (release threshold: never), so re-assembly reuses the HBM of
+// the previous one instead of paying cudaMalloc / cudaFree of gigabytes.
+// guard() points these at the calling context.
+thread_local cudaMemPool_t g_pool = nullptr;
+thread_local cudaStream_t g_stream = nullptr;
+
+void* pool_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (!g_pool) {
+    CK(cudaMalloc(&p, bytes));
+    return p;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, g_pool, g_stream);
+  if (e == cudaErrorMemoryAllocation) {  // give the pool's idle memory back, retry
+    (void)cudaGetLastError();
+    CK(cudaStreamSynchronize(g_stream));
+    CK(cudaMemPoolTrimTo(g_pool, 0));
+    e = cudaMallocFromPoolAsync(&p, bytes, g_pool, g_stream);
+  }
+  CK(e);
+  return p;
+}
+
+void pool_free(void* p) {
+  if (!p) return;
+  if (g_pool) cudaFreeAsync(p, g_stream);
+  else cudaFree(p);
+}
+
+// device memory still obtainable: free HBM plus the pool's idle reserve
+size_t avail_bytes() {
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  if (g_pool) {
+    unsigned long long reserved = 0, used = 0;
+    CK(cudaMemPoolGetAttribute(g_pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    CK(cudaMemPoolGetAttribute(g_pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    free_b += (size_t)(reserved - used);
+  }
+  return free_b;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;  // elements
   void free() {
-    if (p) cudaFree(p);
+    pool_free(p);
     p = nullptr;
     n = 0;
   }
   void alloc(size_t count) {
     free();
     if (count == 0) count = 1;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    p = (T*)pool_alloc(count * sizeof(T));
     n = count;
   }
   void ensure(size_t count) {
@@ -69,6 +114,49 @@ struct DBuf {
     if (!h.empty())
       CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
   }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// host vector in page-locked memory (fast D2H/H2D of the item mirror)
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() {
+    if (p) cudaFreeHost(p);
+  }
+  void reserve(size_t c) {
+    if (c <= cap) return;
+    T* q = nullptr;
+    CK(cudaMallocHost(&q, c * sizeof(T)));
+    if (p) {
+      std::memcpy(q, p, n * sizeof(T));
+      cudaFreeHost(p);
+    }
+    p = q;
+    cap = c;
+  }
+  void push_back(const T& v) {
+    if (n == cap) reserve(std::max<size_t>(1024, cap * 2));
+    p[n++] = v;
+  }
+  void clear() { n = 0; }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  T* data() { return p; }
+  const T* data() const { return p; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  T* begin() { return p; }
+  T* end() { return p + n; }
+  const T* begin() const { return p; }
+  const T* end() const { return p + n; }
 };
 
 struct KTime {
@@ -131,7 +219,7 @@ struct hmgpu_ctx {
   double eps = 0, beta = 0;
   int initial_rank = -1, lookahead = 2;
   long long max_rank = 1LL << 30;
-  std::vector<Item> items;        // host mirror (sizes, offsets, ranks)
+  PinnedVec<Item> items;          // host mirror (sizes, offsets, ranks), pinned
   std::vector<int> item_of_block; // first item of block b (-1: dense/not owned)
   std::vector<int> dense_of_block;
   std::vector<DenseBlock> dblocks;
@@ -182,8 +270,12 @@ struct hmgpu_ctx {
   std::vector<PendingEv> pending;
   std::vector<cudaEvent_t> ev_pool;
 
+  cudaMemPool_t pool = nullptr;
+
   ~hmgpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    g_pool = pool;
+    g_stream = stream;
     for (auto& p : pending) {
       ev_pool.push_back(p.a);
       ev_pool.push_back(p.b);
@@ -198,6 +290,10 @@ struct hmgpu_ctx {
     d_xi.free(); d_ypart.free();
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
+    if (stream) cudaStreamSynchronize(stream);
+    if (pool) cudaMemPoolDestroy(pool);
+    g_pool = nullptr;
+    g_stream = nullptr;
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -253,6 +349,8 @@ int guard(hmgpu_ctx* c, F&& f) {
   if (!c) return HMGPU_ERR_INVALID;
   try {
     if (c->device >= 0) CK(cudaSetDevice(c->device));
+    g_pool = c->pool;
+    g_stream = c->stream;
     f();
     return HMGPU_OK;
   } catch (const Fail& e) {
@@ -464,54 +562,70 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches) {
   if (relaunches) *relaunches += passes;
 }
 
-// packs the arena: every item gets exactly K (+ slack) columns
+// packs the arena: every item gets exactly K (+ slack) columns.  Sizes, a
+// CUB exclusive scan for the new offsets and the copies all run on the
+// device; the item mirror comes back once (pinned).
 void compact(hmgpu_ctx* c, int slack) {
-  download_items(c);
-  const size_t ni = c->items.size();
+  const int ni = (int)c->items.size();
   if (ni == 0) return;
-  std::vector<long long> nu(ni), nv(ni), np(ni);
-  std::vector<int> ids(ni), caps(ni);
-  long long used = 0, usedp = 0;
-  for (size_t t = 0; t < ni; ++t) {
-    const Item& it = c->items[t];
-    const long long capr = std::min<long long>(c->max_rank, std::min(it.m, it.n));
-    const int cap = (int)std::min<long long>(capr, it.k + slack);
-    ids[t] = (int)t;
-    caps[t] = std::max(cap, it.k);
-    nu[t] = used;
-    used += align2((long long)it.m * caps[t]);
-    nv[t] = used;
-    used += align2((long long)it.n * caps[t]);
-    np[t] = usedp;
-    usedp += std::max(caps[t], 1);
+  DBuf<long long> usz, psz, uoff, poff;
+  DBuf<int> caps;
+  usz.alloc(ni);
+  psz.alloc(ni);
+  uoff.alloc(ni + 1);
+  poff.alloc(ni + 1);
+  caps.alloc(ni);
+  const int grid = (ni + 255) / 256;
+  compact_sizes_kernel<<<grid, 256, 0, c->stream>>>(c->d_items.p, ni, c->max_rank, slack,
+                                                    usz.p, psz.p, caps.p);
+  CK(cudaGetLastError());
+  size_t tmp_bytes = 0, t2 = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, usz.p, uoff.p, ni + 0, c->stream));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, psz.p, poff.p, ni + 0, c->stream));
+  DBuf<uint8_t> tmp;
+  tmp.alloc(std::max(tmp_bytes, t2));
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, usz.p, uoff.p, ni, c->stream));
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, t2, psz.p, poff.p, ni, c->stream));
+  long long last[4];
+  CK(cudaMemcpyAsync(&last[0], uoff.p + ni - 1, sizeof(long long), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaMemcpyAsync(&last[1], usz.p + ni - 1, sizeof(long long), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaMemcpyAsync(&last[2], poff.p + ni - 1, sizeof(long long), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaMemcpyAsync(&last[3], psz.p + ni - 1, sizeof(long long), cudaMemcpyDeviceToHost,
+                     c->stream));
+  c->sync();
+  tmp.free();
+  usz.free();
+  psz.free();
+  const long long used = last[0] + last[1], usedp = last[2] + last[3];
+  const size_t free_b = avail_bytes();
+  if (8.0 * (double)used + 8.0 * (double)usedp > 0.9 * (double)free_b) {
+    uoff.free();
+    poff.free();
+    caps.free();
+    download_items(c);  // not enough room for the packed copy: keep the loose arena
+    return;
   }
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  if (8.0 * (double)used + 4.0 * (double)usedp * 2 > 0.9 * (double)free_b) return;
   DBuf<double> na;
   na.alloc((size_t)used + 2);
   DBuf<int2> npv;
   npv.alloc((size_t)usedp + 1);
-  DBuf<int> d_ids, d_caps;
-  DBuf<long long> d_nu, d_nv, d_np;
-  d_ids.upload(ids, c->stream);
-  d_caps.upload(caps, c->stream);
-  d_nu.upload(nu, c->stream);
-  d_nv.upload(nv, c->stream);
-  d_np.upload(np, c->stream);
   c->timed("compact", [&] {
-    relocate_kernel<<<grid_for(c, (long long)ni / 8 + 1), 256, 0, c->stream>>>(
-        c->d_items.p, d_ids.p, d_nu.p, d_nv.p, d_np.p, d_caps.p, (int)ni,
-        c->d_arena.p, na.p, c->d_piv.p, npv.p);
+    compact_kernel<<<grid_for(c, (long long)ni / 8 + 1), 256, 0, c->stream>>>(
+        c->d_items.p, ni, uoff.p, poff.p, caps.p, c->d_arena.p, na.p, c->d_piv.p, npv.p);
   });
   c->sync();
+  uoff.free();
+  poff.free();
+  caps.free();
   c->d_arena.free();
   c->d_arena = na;
   c->arena_used = used;
   c->d_piv.free();
   c->d_piv = npv;
   c->piv_used = usedp;
-  d_ids.free(); d_caps.free(); d_nu.free(); d_nv.free(); d_np.free();
   download_items(c);
 }
 
@@ -1035,6 +1149,16 @@ int hmgpu_create(int device, hmgpu_ctx** out) {
   const int st = guard(c, [&] {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    CK(cudaMemPoolCreate(&c->pool, &props));
+    unsigned long long keep = ~0ULL;
+    CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    g_pool = c->pool;
+    g_stream = c->stream;
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     c->d_counter.alloc(1);
     c->d_overflow.alloc(1);
@@ -1246,8 +1370,8 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       if (B[2]) sum_mn += (m + n) * c->NC;
       else dense_total += n * align2((long long)c->NC * m);
     }
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    c->sync();
+    const size_t free_b = avail_bytes();
     const double avail =
         (double)free_b - 8.0 * (double)dense_total - 4.0 * (1 << 30);
     int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
@@ -1299,7 +1423,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     const size_t arena_cap = want < 0.85 * avail ? (size_t)(c->arena_used * 1.3)
                                                  : (size_t)c->arena_used;
     phase("items");
-    c->d_items.upload(c->items, c->stream);
+    c->d_items.upload(c->items.data(), c->items.size(), c->stream);
     c->d_arena.alloc(arena_cap + 2);
     c->d_piv.alloc((size_t)(c->piv_used * 1.3) + 1);
     c->d_cons.alloc((size_t)cons_used + 16);
@@ -1325,20 +1449,24 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     CK(cudaEventRecord(tn1, c->stream));
 
     phase("nearfield");
-    // ACA, largest blocks first
+    // ACA, largest blocks first (stable counting sort on m + n)
     std::vector<int> list(c->items.size());
-    std::iota(list.begin(), list.end(), 0);
-    std::stable_sort(list.begin(), list.end(), [&](int a, int b) {
-      return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
-    });
+    {
+      int kmax_mn = 0;
+      for (const Item& it : c->items) kmax_mn = std::max(kmax_mn, it.m + it.n);
+      std::vector<int> cnt(kmax_mn + 2, 0);
+      for (const Item& it : c->items) ++cnt[kmax_mn - (it.m + it.n) + 1];
+      for (int k = 1; k <= kmax_mn + 1; ++k) cnt[k] += cnt[k - 1];
+      for (size_t t = 0; t < c->items.size(); ++t)
+        list[cnt[kmax_mn - (c->items[t].m + c->items[t].n)]++] = (int)t;
+    }
     int relaunch = 0;
     run_aca(c, list, &relaunch);
     phase("aca");
     compact(c, 0);
     phase("compact");
     if (verbose()) {
-      size_t f2 = 0, t2 = 0;
-      cudaMemGetInfo(&f2, &t2);
+      const size_t f2 = avail_bytes();
       std::fprintf(stderr, "[hmgpu] items=%zu cap_init=%d arena=%.2f GB dense=%.2f GB "
                            "free_after=%.2f GB relaunches=%d\n",
                    c->items.size(), cap_init, 8.0 * c->arena_used / 1e9,

@@ -770,6 +770,53 @@ __global__ void prep_extend_kernel(Item* items, const int* idx, int n, int steps
   }
 }
 
+// compaction: per item the packed size of U and V with cap = max(min(capr,
+// k + slack), k) columns, and its pivot slots
+__global__ void compact_sizes_kernel(const Item* __restrict__ items, int n,
+                                     long long max_rank, int slack,
+                                     long long* __restrict__ usz, long long* __restrict__ psz,
+                                     int* __restrict__ caps) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const Item it = items[t];
+  const long long capr = min(max_rank, (long long)min(it.m, it.n));
+  const int cap = max((int)min(capr, (long long)it.k + slack), it.k);
+  caps[t] = cap;
+  usz[t] = (((long long)it.m * cap + 1) & ~1LL) + (((long long)it.n * cap + 1) & ~1LL);
+  psz[t] = max(cap, 1);
+}
+
+// copies every item's U (m x K), V (n x K) and pivots to the scanned offsets
+__global__ void compact_kernel(Item* __restrict__ items, int n,
+                               const long long* __restrict__ uoff,
+                               const long long* __restrict__ poff,
+                               const int* __restrict__ caps,
+                               const double* __restrict__ src, double* __restrict__ dst,
+                               const int2* __restrict__ spiv, int2* __restrict__ dpiv) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < n; t += nw) {
+    Item it = items[t];
+    const long long nu = (long long)it.m * it.k, nv = (long long)it.n * it.k;
+    const long long u0 = uoff[t];
+    const long long v0 = u0 + (((long long)it.m * caps[t] + 1) & ~1LL);
+    const double* su = src + it.u_off;
+    const double* sv = src + it.v_off;
+    for (long long e = lane; e < nu; e += 32) dst[u0 + e] = su[e];
+    for (long long e = lane; e < nv; e += 32) dst[v0 + e] = sv[e];
+    for (int e = lane; e < it.k; e += 32) dpiv[poff[t] + e] = spiv[it.p_off + e];
+    __syncwarp();
+    if (lane == 0) {
+      it.u_off = u0;
+      it.v_off = v0;
+      it.p_off = poff[t];
+      it.cap = caps[t];
+      items[t] = it;
+    }
+  }
+}
+
 // relocate item factors into new storage: copies U (m x K), V (n x K) prefix
 // columns and K pivots to the offsets in `dst` (same item order)
 __global__ void relocate_kernel(Item* __restrict__ items, const int* __restrict__ idx,
