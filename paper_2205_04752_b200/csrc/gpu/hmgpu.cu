@@ -393,21 +393,23 @@ void build_geometry(hmgpu_ctx* c) {
       rp[i] = make_double4(c->centroid[3 * t], c->centroid[3 * t + 1],
                            c->centroid[3 * t + 2], 0.0);
     }
-    std::vector<double> tr(16LL * c->n_cols, 0.0);
+    // tiles of 32 triangles x 16 field slots (TriRef in hmgpu_device.cuh)
+    const long long ntile = (c->n_cols + 31) / 32;
+    std::vector<double> tr(ntile * 512, 0.0);
     for (int j = 0; j < c->n_cols; ++j) {
       const int t = c->cperm[j];
       const double* v0 = &c->verts[3LL * c->tris[3 * t]];
       const double* v1 = &c->verts[3LL * c->tris[3 * t + 1]];
       const double* v2 = &c->verts[3LL * c->tris[3 * t + 2]];
-      double* T = &tr[16LL * j];
+      double* T = &tr[(long long)(j >> 5) * 512 + (j & 31)];
       for (int d = 0; d < 3; ++d) {
-        T[d] = v0[d];
-        T[3 + d] = v1[d] - v0[d];
-        T[6 + d] = v2[d] - v0[d];
-        T[9 + d] = c->centroid[3 * t + d];
+        T[32 * d] = v0[d];
+        T[32 * (3 + d)] = v1[d] - v0[d];
+        T[32 * (6 + d)] = v2[d] - v0[d];
+        T[32 * (9 + d)] = c->centroid[3 * t + d];
       }
-      T[12] = c->area[t];
-      T[13] = c->diam[t];
+      T[32 * 12] = c->area[t];
+      T[32 * 13] = c->diam[t];
     }
     c->d_rowpt.upload(rp, c->stream);
     c->d_tri.upload(tr, c->stream);
@@ -537,7 +539,9 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches) {
             c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
             c->d_overflow.p);
       };
-      if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
+      static const bool occ3 = std::getenv("HMGPU_ACA_OCC3") != nullptr;
+      if (c->kind == KIND_KELVIN && occ3) go(aca_kernel<KIND_KELVIN, 3>);
+      else if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
       else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
       else go(aca_kernel<KIND_DENSE>);
     });

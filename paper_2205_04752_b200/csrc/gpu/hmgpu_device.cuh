@@ -31,8 +31,8 @@ struct Geom {
   int kind;
   int same_tree;            // row internal index == col internal index <=> same DOF
   const double4* rowpt;     // evaluation points, internal row order (x,y,z,-)
-  const double* tri;        // kelvin: 16 doubles per column triangle, internal order
-                            //   v0[3] e1[3] e2[3] cen[3] area diam pad pad
+  const double* tri;        // kelvin: 14 fields per column triangle, internal order,
+                            //   tiles of 32 (TriRef): v0[3] e1[3] e2[3] cen[3] area diam
   const double4* colpt;     // newton: column points, internal column order
   const double* A;          // dense: column-major matrix, external ids
   long long lda;
@@ -44,21 +44,47 @@ struct Geom {
 };
 
 // ---------------------------------------------------------------------------
+// one column triangle's fields (structure-of-arrays view)
+// tiles of 32 triangles x 16 field slots: field f of triangle j at
+// tri[(j / 32) * 512 + f * 32 + j % 32] -- consecutive j coalesce, and every
+// field is a constant offset from one base pointer
+struct TriRef {
+  const double* p;
+  __device__ __forceinline__ double operator[](int f) const { return p[f * 32]; }
+};
+__device__ __forceinline__ TriRef tri_ref(const Geom& g, int j) {
+  return TriRef{g.tri + ((long long)(j >> 5) << 9) + (j & 31)};
+}
+
 // Kelvin collocation: quadrature tier decided with IEEE round-to-nearest
 // operations in the reference's order so that it is bit-identical to the
 // host/oracle decision: gap = |p - c_j| - 0.5 d_j (kernels.cpp:88-92).
+__device__ __forceinline__ int kelvin_tier_exact(double d2, double dj) {
+  const double gap = __dsub_rn(__dsqrt_rn(d2), __dmul_rn(0.5, dj));
+  if (gap >= __dmul_rn(c_rules.far_ratio, dj)) return 0;
+  if (gap >= __dmul_rn(c_rules.mid_ratio, dj)) return 1;
+  return 2;
+}
+// The decision compares squared distances against the thresholds first and
+// takes the exact IEEE path only inside a 1e-12 relative band around them,
+// where the rounding of sqrt / subtract could matter; outside the band both
+// give the same tier.
 __device__ __forceinline__ int kelvin_tier(double px, double py, double pz,
-                                           const double* T) {
+                                           const TriRef& T) {
   const double dx = __dsub_rn(px, T[9]);
   const double dy = __dsub_rn(py, T[10]);
   const double dz = __dsub_rn(pz, T[11]);
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                               __dmul_rn(dz, dz));
   const double dj = T[13];
-  const double gap = __dsub_rn(__dsqrt_rn(d2), __dmul_rn(0.5, dj));
-  if (gap >= __dmul_rn(c_rules.far_ratio, dj)) return 0;
-  if (gap >= __dmul_rn(c_rules.mid_ratio, dj)) return 1;
-  return 2;
+  const double t0 = (c_rules.far_ratio + 0.5) * dj, t1 = (c_rules.mid_ratio + 0.5) * dj;
+  const double s0 = t0 * t0, s1 = t1 * t1;
+  if (d2 > s0 * (1.0 + 1e-12)) return 0;
+  if (d2 < s0 * (1.0 - 1e-12)) {
+    if (d2 > s1 * (1.0 + 1e-12)) return 1;
+    if (d2 < s1 * (1.0 - 1e-12)) return 2;
+  }
+  return kelvin_tier_exact(d2, dj);
 }
 
 // 1/sqrt(x) for x > 0: bit-level seed and four Newton steps written with
@@ -83,7 +109,7 @@ __device__ __forceinline__ double sel3(int r, double x, double y, double z) {
 // in its plane (builder-defined self term, closed form; see
 // oracle/hmbem_oracle.cpp Kelvin::self_term for the derivation).
 __device__ __noinline__ void kelvin_self6(const Geom& g, double px, double py, double pz,
-                             const double* T, double* out6) {
+                             const TriRef T, double* out6) {
   const double v[3][3] = {{T[0], T[1], T[2]},
                           {T[0] + T[3], T[1] + T[4], T[2] + T[5]},
                           {T[0] + T[6], T[1] + T[7], T[2] + T[8]}};
@@ -96,6 +122,7 @@ __device__ __noinline__ void kelvin_self6(const Geom& g, double px, double py, d
   nz /= nn;
   double i1 = 0.0;
   double irc[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 1
   for (int e = 0; e < 3; ++e) {
     const double* a = v[e];
     const double* b = v[(e + 1) % 3];
@@ -137,23 +164,18 @@ __device__ __noinline__ void kelvin_self6(const Geom& g, double px, double py, d
 // sum, 1/|x| by rsqrt_canon (deterministic Newton), explicit fma
 // (the library is compiled with --fmad=false so nothing else contracts).
 // With it ACA pivots, ranks and factors are bit-identical to the oracle.
-__device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
-                                                int comp, int& nq_acc) {
-  const double4 p = g.rowpt[i];
-  const double* T = g.tri + 16LL * j;
-  const int r = c_comp_r[comp], c = c_comp_c[comp];
-  if (g.same_tree && i == j) {
-    double s6[6];
-    kelvin_self6(g, p.x, p.y, p.z, T, s6);
-    return s6[comp];
-  }
-  const int tier = kelvin_tier(p.x, p.y, p.z, T);
+// SELF = false: the caller guarantees i != j (admissible blocks: the row and
+// column clusters are disjoint), so the self-term path is not compiled in.
+// quadrature sum of one component (R, C) fixed at compile time (no selects)
+template <int R, int C>
+__device__ __forceinline__ double kelvin_quad(const Geom& g, const double4& p,
+                                              const TriRef& T, int tier) {
   const double v0x = T[0], v0y = T[1], v0z = T[2];
   const double e1x = T[3], e1y = T[4], e1z = T[5];
   const double e2x = T[6], e2y = T[7], e2z = T[8];
   double acc_d = 0.0, acc_x = 0.0;
   const int nq = c_rules.n[tier];
-  nq_acc += nq;
+#pragma unroll 1
   for (int q = 0; q < nq; ++q) {
     const double a = c_rules.a[tier][q], b = c_rules.b[tier][q],
                  w = c_rules.w[tier][q];
@@ -163,11 +185,35 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     const double ri = rsqrt_canon(r2);
     const double wr = w * ri;
-    acc_d = acc_d + wr;
-    acc_x = fma(wr * ri * ri, sel3(r, dx, dy, dz) * sel3(c, dx, dy, dz), acc_x);
+    if (R == C) acc_d = acc_d + wr;
+    const double dr = R == 0 ? dx : (R == 1 ? dy : dz);
+    const double dc = C == 0 ? dx : (C == 1 ? dy : dz);
+    acc_x = fma(wr * ri * ri, dr * dc, acc_x);
   }
-  const double s = (r == c) ? fma(g.c34, acc_d, acc_x) : acc_x;
+  const double s = (R == C) ? fma(g.c34, acc_d, acc_x) : acc_x;
   return 2.0 * T[12] * g.cst * s;
+}
+
+template <bool SELF = true>
+__device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
+                                                int comp, int& nq_acc) {
+  const double4 p = g.rowpt[i];
+  const TriRef T = tri_ref(g, j);
+  if (SELF && g.same_tree && i == j) {
+    double s6[6];
+    kelvin_self6(g, p.x, p.y, p.z, T, s6);
+    return s6[comp];
+  }
+  const int tier = kelvin_tier(p.x, p.y, p.z, T);
+  nq_acc += c_rules.n[tier];
+  switch (comp) {  // warp-uniform
+    case 0: return kelvin_quad<0, 0>(g, p, T, tier);
+    case 1: return kelvin_quad<0, 1>(g, p, T, tier);
+    case 2: return kelvin_quad<0, 2>(g, p, T, tier);
+    case 3: return kelvin_quad<1, 1>(g, p, T, tier);
+    case 4: return kelvin_quad<1, 2>(g, p, T, tier);
+    default: return kelvin_quad<2, 2>(g, p, T, tier);
+  }
 }
 
 // all six components of one (point, triangle) pair (near-field fill), each
@@ -175,7 +221,7 @@ __device__ __forceinline__ double kelvin_entry1(const Geom& g, int i, int j,
 __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
                                               double* out6, int& nq_acc) {
   const double4 p = g.rowpt[i];
-  const double* T = g.tri + 16LL * j;
+  const TriRef T = tri_ref(g, j);
   if (g.same_tree && i == j) {
     kelvin_self6(g, p.x, p.y, p.z, T, out6);
     return;
@@ -238,12 +284,13 @@ __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
-// the same with the provider fixed at compile time (ACA kernel instances);
-// nq_acc accumulates the quadrature points used (counted-flop bookkeeping)
+// the same with the provider fixed at compile time, for admissible blocks
+// only (no diagonal entries; ACA kernel instances); nq_acc accumulates the
+// quadrature points used (counted-flop bookkeeping)
 template <int KIND>
 __device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
                                           int& nq_acc) {
-  if (KIND == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq_acc);
+  if (KIND == KIND_KELVIN) return kelvin_entry1<false>(g, i, j, comp, nq_acc);
   if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -301,6 +348,159 @@ __device__ __forceinline__ int warp_min_int(int v) {
   return v;
 }
 
+// Residual of one row (is_row) or one column of the block, one warp:
+//   row i:  out[c] = A(i, c) - sum_l U(i, l) V(c, l)      (W = U, X = V)
+//   col j:  out[r] = A(r, j) - sum_l V(j, l) U(r, l)      (W = V, X = U)
+// l ascending with fma, exactly as aca.cpp:61-64 / :79-82 restated by the
+// oracle.  Per lane: max |A| (row scale), first-max |out| and sum out^2.
+// The only call site of the entry provider inside the ACA (one copy of the
+// quadrature code: the ACA kernel is instruction-cache bound otherwise).
+struct LineStats {
+  double rs, pm, pv, sq;
+  int pj, nq;
+};
+
+template <int KIND>
+__device__ __forceinline__ LineStats residual_line(const Geom& g, int row0, int col0, int comp,
+                                                   bool is_row, int fix,
+                                                   const double* __restrict__ W, int ldw,
+                                                   const double* __restrict__ X, int ldx,
+                                                   int len, int k, double* __restrict__ out,
+                                                   double* __restrict__ ebuf, int lane) {
+  LineStats st{0.0, -1.0, 0.0, 0.0, -1, 0};
+  for (int base = 0; base < len; base += 128) {
+    const int nb = min(4, (len - base + 31) >> 5);  // warp-uniform
+    // phase A: the kernel entries of up to 4 columns per lane (arithmetic
+    // only; parked in this lane's shared-memory slots)
+#pragma unroll 1
+    for (int s = 0; s < nb; ++s) {
+      const int t = base + 32 * s + lane;
+      double a = 0.0;
+      if (t < len) {
+        const int i = is_row ? row0 + fix : row0 + t;
+        const int j = is_row ? col0 + t : col0 + fix;
+        a = entry_k<KIND>(g, i, j, comp, st.nq);
+      }
+      ebuf[32 * s + lane] = a;
+    }
+    // phase B: the low-rank correction, four independent columns per lane so
+    // that eight panel loads are in flight per lane
+    double v[4];
+    bool ok[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      ok[s] = s < nb && base + 32 * s + lane < len;
+      v[s] = ok[s] ? ebuf[32 * s + lane] : 0.0;
+      if (ok[s]) st.rs = fmax(st.rs, fabs(v[s]));
+    }
+    const double* xb = X + base + lane;
+#pragma unroll 2
+    for (int l = 0; l < k; ++l) {
+      const double w = -W[(long long)l * ldw + fix];
+      const double* xl = xb + (long long)l * ldx;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (ok[s]) v[s] = fma(w, xl[32 * s], v[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (!ok[s]) continue;
+      const int t = base + 32 * s + lane;
+      out[t] = v[s];
+      st.sq = fma(v[s], v[s], st.sq);
+      if (fabs(v[s]) > st.pm) {
+        st.pm = fabs(v[s]);
+        st.pj = t;
+        st.pv = v[s];
+      }
+    }
+  }
+  return st;
+}
+
+// sum_l du_l dv_l (fma, l ascending) with du_l = warp-order dot(u, U(:,l)),
+// dv_l = warp-order dot(v, V(:,l)).  Eight l at a time: lane-strided fma
+// partials, then a reduce-scatter butterfly (bits 4, 3, 2 exchange halves,
+// bits 1, 0 all-reduce).  Every node of that tree adds the same two operands
+// as warp_sum's xor butterfly, so each du_l is bit-identical to
+// warp_sum(partial) (the oracle's warp_dot), at 9 instead of 40 shuffles.
+__device__ __forceinline__ double rs8(double (&p)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double a[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const double send = b4 ? p[h] : p[h + 4];
+    const double keep = b4 ? p[h + 4] : p[h];
+    a[h] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  double b[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double send = b3 ? a[h] : a[h + 2];
+    const double keep = b3 ? a[h + 2] : a[h];
+    b[h] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const double send = b2 ? b[0] : b[1];
+  const double keep = b2 ? b[1] : b[0];
+  double v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;  // the full sum for index q = (lane >> 2) & 7
+}
+
+__device__ __forceinline__ double cross_terms(const double* __restrict__ uk,
+                                           const double* __restrict__ U, int m,
+                                           const double* __restrict__ vk,
+                                           const double* __restrict__ V, int n, int k,
+                                           int lane) {
+  double cross = 0.0;
+  for (int l0 = 0; l0 < k; l0 += 8) {
+    const int nl = min(8, k - l0);
+    double pu[8], pv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pu[q] = pv[q] = 0.0;
+    for (int r = lane; r < m; r += 64) {
+      const bool two = r + 32 < m;
+      const double a0 = uk[r], a1 = two ? uk[r + 32] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < nl) {
+          const double* ul = U + (long long)(l0 + q) * m + r;
+          const double x0 = ul[0];
+          const double x1 = two ? ul[32] : 0.0;
+          pu[q] = fma(a0, x0, pu[q]);
+          if (two) pu[q] = fma(a1, x1, pu[q]);
+        }
+      }
+    }
+    for (int c = lane; c < n; c += 64) {
+      const bool two = c + 32 < n;
+      const double a0 = vk[c], a1 = two ? vk[c + 32] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < nl) {
+          const double* vl = V + (long long)(l0 + q) * n + c;
+          const double x0 = vl[0];
+          const double x1 = two ? vl[32] : 0.0;
+          pv[q] = fma(a0, x0, pv[q]);
+          if (two) pv[q] = fma(a1, x1, pv[q]);
+        }
+      }
+    }
+    const double du = rs8(pu, lane);
+    const double dv = rs8(pv, lane);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < nl) {
+        const double a = __shfl_sync(0xffffffffu, du, 4 * q);
+        const double b = __shfl_sync(0xffffffffu, dv, 4 * q);
+        cross = fma(a, b, cross);
+      }
+    }
+  }
+  return cross;
+}
+
 // One ACA step of aca_step (aca.cpp:41-102) executed by one warp.
 // sf < 0 disables the accuracy test (extension mode).  The candidate row
 // residual is built in V(:,k) and the column residual in U(:,k); both are
@@ -308,9 +508,9 @@ __device__ __forceinline__ int warp_min_int(int v) {
 template <int KIND>
 __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
                              double* __restrict__ V, int2* __restrict__ piv,
-                             uint8_t* __restrict__ Z, double sf, int lane, int& nq_acc) {
+                             uint8_t* __restrict__ Z, double sf, int lane, int& nq_acc,
+                             double* __restrict__ ebuf) {
   const int m = s.m, n = s.n, k = s.k;
-  const int comp = s.comp;
   for (;;) {
     if (s.nconsumed == m) return STOP_EXH;
     s.steps++;
@@ -339,65 +539,53 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
       warp_argmax(best, bi, aux);
       i = bi;
     }
-    // --- row of the residual: v = A(i,:) - sum_l U(i,l) V(:,l)
+    // --- row of the residual: v = A(i,:) - sum_l U(i,l) V(:,l), then the
+    // column u = A(:,j) - sum_l V(j,l) U(:,l); one loop so that the entry
+    // provider is instantiated once (instruction cache)
     double* vk = V + (long long)k * n;
-    double rs = 0.0, pm = -1.0, pv = 0.0;
-    int pj = -1;
-    for (int c = lane; c < n; c += 32) {
-      double val = entry_k<KIND>(g, s.row0 + i, s.col0 + c, comp, nq_acc);
-      rs = fmax(rs, fabs(val));
-      for (int l = 0; l < k; ++l)
-        val = fma(-U[(long long)l * m + i], V[(long long)l * n + c], val);
-      vk[c] = val;
-      if (fabs(val) > pm) {
-        pm = fabs(val);
-        pj = c;
-        pv = val;
-      }
-    }
-    s.entries += n;
-    const double row_scale = warp_max(rs);
-    warp_argmax(pm, pj, pv);
-    if (lane == 0) Z[i] = 1;
-    s.nconsumed++;
-    __syncwarp();
-    if (pm <= 1e-14 * row_scale || row_scale == 0.0) continue;  // vanishing
-    const int j = pj;
-    double vv = 0.0;
-    for (int c = lane; c < n; c += 32) {
-      const double t = vk[c] / pv;
-      vk[c] = t;
-      vv = fma(t, t, vv);
-    }
-    // --- column of the residual: u = A(:,j) - sum_l V(j,l) U(:,l)
     double* uk = U + (long long)k * m;
-    double uu = 0.0;
-    for (int r = lane; r < m; r += 32) {
-      double val = entry_k<KIND>(g, s.row0 + r, s.col0 + j, comp, nq_acc);
-      for (int l = 0; l < k; ++l)
-        val = fma(-V[(long long)l * n + j], U[(long long)l * m + r], val);
-      uk[r] = val;
-      uu = fma(val, val, uu);
+    int fix = i, j = -1;
+    double vv = 0.0, uu = 0.0;
+    bool vanished = false;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool is_row = pass == 0;
+      const LineStats ls = residual_line<KIND>(
+          g, s.row0, s.col0, s.comp, is_row, fix, is_row ? U : V, is_row ? m : n,
+          is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, lane);
+      nq_acc += ls.nq;
+      s.entries += is_row ? n : m;
+      if (!is_row) {
+        uu = warp_sum(ls.sq);
+        break;
+      }
+      const double row_scale = warp_max(ls.rs);
+      double pm = ls.pm, pv = ls.pv;
+      int pj = ls.pj;
+      warp_argmax(pm, pj, pv);
+      if (lane == 0) Z[i] = 1;
+      s.nconsumed++;
+      __syncwarp();
+      if (pm <= 1e-14 * row_scale || row_scale == 0.0) {  // vanishing
+        vanished = true;
+        break;
+      }
+      j = pj;
+      for (int c = lane; c < n; c += 32) {
+        const double t = vk[c] / pv;
+        vk[c] = t;
+        vv = fma(t, t, vv);
+      }
+      fix = j;
     }
-    s.entries += m;
-    uu = warp_sum(uu);
+    if (vanished) continue;
     vv = warp_sum(vv);
     if (sf >= 0.0 && sqrt(uu) * sqrt(vv) <= sf * sqrt(fmax(s.frob_sq, 0.0))) {
       __syncwarp();
       return STOP_INEQ;
     }
     // ||S_k||^2 = ||S_{k-1}||^2 + 2 sum_l (u.u_l)(v.v_l) + ||u||^2 ||v||^2
-    double cross = 0.0;
-    for (int l = 0; l < k; ++l) {
-      double du = 0.0, dv = 0.0;
-      const double* ul = U + (long long)l * m;
-      const double* vl = V + (long long)l * n;
-      for (int r = lane; r < m; r += 32) du = fma(uk[r], ul[r], du);
-      for (int c = lane; c < n; c += 32) dv = fma(vk[c], vl[c], dv);
-      du = warp_sum(du);
-      dv = warp_sum(dv);
-      cross = fma(du, dv, cross);
-    }
+    const double cross = cross_terms(uk, U, m, vk, V, n, k, lane);
     s.frob_sq += 2.0 * cross + uu * vv;
     if (lane == 0) piv[k] = make_int2(i, j);
     s.k = k + 1;
@@ -410,12 +598,14 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
 //   PH_RUN  aca_run to the stopping rule (aca.cpp:106-124)
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
 //   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
+// One call site of the step for all phases (code size).
 template <int KIND>
 __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
                               double* __restrict__ arena, int2* __restrict__ pivots,
                               uint8_t* __restrict__ cons, double sf_run,
                               long long max_rank, int lookahead,
-                              int* __restrict__ overflow, int lane) {
+                              int* __restrict__ overflow, int lane,
+                              double* __restrict__ ebuf) {
   Item s = items[idx];
   double* U = arena + s.u_off;
   double* V = arena + s.v_off;
@@ -426,37 +616,30 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
   s.status = ST_OK;
   int nq_acc = 0;
   while (s.phase != PH_DONE) {
-    if (s.phase == PH_RUN) {
-      bool stopped = false;
-      while (s.k < capr) {
-        if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
-        const int st = aca_step_warp<KIND>(g, s, U, V, piv, Z, sf_run, lane, nq_acc);
-        if (st != STOP_NONE) {
-          s.last_stop = st;
-          stopped = true;
-          break;
-        }
+    const bool run = s.phase == PH_RUN;
+    const bool more = run ? s.k < capr : (s.steps_left > 0 && s.k < capr);
+    int st = STOP_NONE;
+    if (more) {
+      if (s.k >= s.cap) {
+        s.status = ST_OVERFLOW;
+        break;
       }
-      if (!stopped) s.last_stop = (s.nconsumed == s.m) ? STOP_EXH : STOP_RANKCAP;
+      st = aca_step_warp<KIND>(g, s, U, V, piv, Z, run ? sf_run : -1.0, lane, nq_acc, ebuf);
+      if (st == STOP_NONE) {
+        if (!run) s.steps_left--;
+        continue;
+      }
+    }
+    if (run) {
+      s.last_stop = st != STOP_NONE ? st : (s.nconsumed == s.m ? STOP_EXH : STOP_RANKCAP);
       s.kcur = s.k;
       s.phase = PH_EXT;
       s.steps_left = lookahead;
-    } else {  // PH_INIT or PH_EXT
-      bool stopped = false;
-      while (s.steps_left > 0 && s.k < capr) {
-        if (s.k >= s.cap) { s.status = ST_OVERFLOW; goto save; }
-        const int st = aca_step_warp<KIND>(g, s, U, V, piv, Z, -1.0, lane, nq_acc);
-        if (st != STOP_NONE) {
-          s.last_stop = st;
-          stopped = true;
-          break;
-        }
-        s.steps_left--;
-      }
-      if (!stopped)
-        s.last_stop = (s.nconsumed == s.m)               ? STOP_EXH
-                      : (s.k >= capr && s.steps_left > 0) ? STOP_RANKCAP
-                                                          : STOP_STEPS;
+    } else {
+      s.last_stop = st != STOP_NONE                      ? st
+                    : (s.nconsumed == s.m)               ? STOP_EXH
+                    : (s.k >= capr && s.steps_left > 0) ? STOP_RANKCAP
+                                                        : STOP_STEPS;
       if (s.phase == PH_INIT) {
         s.kcur = s.k;
         s.phase = PH_EXT;
@@ -467,7 +650,6 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
       }
     }
   }
-save:
   __syncwarp();
   {
     long long t = nq_acc;
@@ -482,20 +664,22 @@ save:
 }
 
 // warps pull items from `list` (largest first) through a global counter
-template <int KIND>
-__global__ void __launch_bounds__(256, 2)
+template <int KIND, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB)
 aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
            int nlist, int* __restrict__ counter, double* __restrict__ arena,
            int2* __restrict__ pivots, uint8_t* __restrict__ cons, double sf_run,
            long long max_rank, int lookahead, int* __restrict__ overflow) {
+  __shared__ double ebuf_all[8][128];  // per-warp entry slots (residual_line)
   const int lane = threadIdx.x & 31;
+  double* ebuf = ebuf_all[threadIdx.x >> 5];
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(counter, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nlist) return;
     aca_item_warp<KIND>(g, items, list[t], arena, pivots, cons, sf_run, max_rank,
-                        lookahead, overflow, lane);
+                        lookahead, overflow, lane, ebuf);
   }
 }
 
