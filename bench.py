@@ -418,11 +418,15 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--nrhs", type=int, default=0,
+                    help="override the config's number of right-hand sides")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rule)")
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.nrhs > 0:
+        cfg["nrhs"] = args.nrhs
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)
