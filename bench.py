@@ -78,9 +78,9 @@ def make_x(hm, cfg, mesh, n_dofs):
     elif kind == "normal":
         x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "normal")
     elif kind == "normal_dirichlet0":
-        x = hm.random_vector(n_dofs, cfg["seed"], "normal")
+        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "normal")
         d = mesh.arrays()["dirichlet"].astype(bool)
-        x.reshape(3, -1)[:, d] = 0.0  # g_N extension convention (hmbem_cli.cpp:76-77)
+        x.reshape(nrhs, 3, -1)[:, :, d] = 0.0  # g_N extension (hmbem_cli.cpp:76-77)
     else:  # Gaussian bump at (2,0,0), sigma 0.05, + 1e-3 uniform noise
         c = mesh.arrays()["centroids"]
         bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.05 ** 2))

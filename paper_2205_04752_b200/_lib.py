@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_DIR = os.path.join(_PKG, "lib")
+# HMGPU_LIB_DIR: an alternate build of the same sources (development A/B runs)
+LIB_DIR = os.environ.get("HMGPU_LIB_DIR") or os.path.join(_PKG, "lib")
 HMBEM_PATH = os.path.join(LIB_DIR, "libhmbem.so")
 HMGPU_PATH = os.path.join(LIB_DIR, "libhmgpu.so")
 

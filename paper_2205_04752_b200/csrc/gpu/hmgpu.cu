@@ -26,6 +26,7 @@
 #include "hmgpu.h"
 #include "hmgpu_device.cuh"
 #include "hmgpu_stream.cuh"
+#include "hmgpu_mrhs.cuh"
 
 using namespace hmgpu;
 
@@ -243,8 +244,10 @@ struct hmgpu_ctx {
   long long part_rows = 0;
   std::vector<int> leaf_begin, leaf_end, leaf_ptr;
   std::vector<long long> leaf_prow;
+  std::vector<int2> leaf_blk;     // per leaf entry: (matvec block, row offset in block)
   DBuf<int> d_leaf_begin, d_leaf_end, d_leaf_ptr;
   DBuf<long long> d_leaf_prow;
+  DBuf<int2> d_leaf_blk;
   int kmax = 0;
   DBuf<double> d_x, d_y, d_xi, d_ypart;
 
@@ -261,6 +264,18 @@ struct hmgpu_ctx {
   int p_nwarps = 0, p_njb = 0;
   DBuf<double> d_sarena, d_zpart;
   DBuf<LeafEntry> d_pentries;
+
+  // ---- multi-RHS (16 per pass, fp64 tensor cores) plan ----
+  bool p16_valid = false;
+  int p16_mode = -1;
+  int n_z16 = 0, n_zs16 = 0, n_tiles16 = 0;
+  long long p16_zsize = 0;
+  DBuf<Z16Task> d_z16;
+  DBuf<Z16Sum> d_zs16;
+  DBuf<long long> d_zb16;
+  DBuf<int> d_rk16;
+  DBuf<int2> d_tiles16;
+  DBuf<double> d_zpart16, d_xi16;
   DBuf<int> d_pleaf_ptr;
   std::vector<int> p_leaf_ptr;
 
@@ -286,10 +301,12 @@ struct hmgpu_ctx {
     d_piv.free(); d_cons.free(); d_dense.free(); d_dblocks.free();
     d_counter.free(); d_overflow.free(); d_list.free(); d_mvb.free();
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
-    d_leaf_ptr.free(); d_leaf_prow.free(); d_x.free(); d_y.free();
+    d_leaf_ptr.free(); d_leaf_prow.free(); d_leaf_blk.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
+    d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
+    d_rk16.free(); d_tiles16.free();
     if (stream) cudaStreamSynchronize(stream);
     if (pool) cudaMemPoolDestroy(pool);
     g_pool = nullptr;
@@ -700,24 +717,30 @@ void build_matvec(hmgpu_ctx* c) {
   c->leaf_end = le;
   const int nl = (int)lb.size();
   std::vector<std::vector<long long>> lists(nl);
-  for (const MvBlock& mb : c->mvb) {
+  std::vector<std::vector<int2>> blks(nl);
+  for (int bi = 0; bi < (int)c->mvb.size(); ++bi) {
+    const MvBlock& mb = c->mvb[bi];
     // leaves covered by rows [row0, row0+m)
     int l0 = (int)(std::lower_bound(lb.begin(), lb.end(), mb.row0) - lb.begin());
     for (int l = l0; l < nl && lb[l] < mb.row0 + mb.m; ++l) {
       if (le[l] > mb.row0 + mb.m)
         fail(HMGPU_ERR_INVALID, "block rows do not align with row-tree leaves");
       lists[l].push_back(mb.prow + (lb[l] - mb.row0));
+      blks[l].push_back(make_int2(bi, lb[l] - mb.row0));
     }
   }
   c->leaf_ptr.assign(nl + 1, 0);
   c->leaf_prow.clear();
+  c->leaf_blk.clear();
   for (int l = 0; l < nl; ++l) {
     c->leaf_ptr[l + 1] = c->leaf_ptr[l] + (int)lists[l].size();
     c->leaf_prow.insert(c->leaf_prow.end(), lists[l].begin(), lists[l].end());
+    c->leaf_blk.insert(c->leaf_blk.end(), blks[l].begin(), blks[l].end());
   }
   c->d_leaf_begin.upload(c->leaf_begin, c->stream);
   c->d_leaf_end.upload(c->leaf_end, c->stream);
   c->d_leaf_ptr.upload(c->leaf_ptr, c->stream);
+  c->d_leaf_blk.upload(c->leaf_blk, c->stream);
   c->d_leaf_prow.upload(c->leaf_prow, c->stream);
   c->sync();
 }
@@ -1027,6 +1050,83 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
                          "arena=%.3f GB slots=%lld wslots=%lld entries=%zu smem=%zu B\n",
                  c->p_ntasks, ja.size(), jb.size(), chunks.size(), 8.0 * alen / 1e9, slots,
                  wslots, entries.size(), c->p_smem);
+}
+
+// multi-RHS plan: phase-1 tasks per (admissible block, 128-column chunk),
+// the blocks' Z regions [nz][K][32]; phase 2 runs per leaf (leaf_blk)
+void build_plan16(hmgpu_ctx* c, int mode) {
+  std::vector<Z16Task> zt;
+  std::vector<Z16Sum> zsum;
+  std::vector<long long> zb(std::max(c->n_mv, 1), 0);
+  std::vector<int> rk(8 * (size_t)std::max(c->n_mv, 1), 0);
+  long long zsize = 0;
+  for (int bi = 0; bi < c->n_mv; ++bi) {
+    const MvBlock& mb = c->mvb[bi];
+    if (mb.dense) continue;
+    int K = 0;
+    for (int q = 0; q < 6; ++q) {
+      const Item& it = c->items[mb.item0 + q];
+      rk[8 * bi + q] = mode ? it.k : it.kcur;
+      K += rk[8 * bi + q];
+    }
+    rk[8 * bi + 6] = K;
+    if (K == 0) continue;
+    const int nz = (mb.n + JC - 1) / JC;
+    zb[bi] = zsize;
+    zsize += (long long)nz * K * 32;
+    for (int z = 0; z < nz; ++z)
+      zt.push_back({bi, z * JC, std::min(JC, mb.n - z * JC), z, zb[bi]});
+    if (nz > 1) zsum.push_back({zb[bi], K * 32, nz});
+  }
+  std::vector<int2> tiles;
+  for (size_t l = 0; l < c->leaf_begin.size(); ++l) {
+    const int rows = c->leaf_end[l] - c->leaf_begin[l];
+    for (int tt = 0; tt * 8 * TR < rows; ++tt) tiles.push_back(make_int2((int)l, tt));
+  }
+  c->d_z16.upload(zt, c->stream);
+  c->d_zs16.upload(zsum, c->stream);
+  c->d_zb16.upload(zb, c->stream);
+  c->d_rk16.upload(rk, c->stream);
+  c->d_tiles16.upload(tiles, c->stream);
+  c->d_zpart16.ensure((size_t)std::max<long long>(zsize, 1));
+  c->d_xi16.ensure((size_t)c->n_cols * 48);
+  c->n_z16 = (int)zt.size();
+  c->n_zs16 = (int)zsum.size();
+  c->n_tiles16 = (int)tiles.size();
+  c->p16_zsize = zsize;
+  c->p16_mode = mode;
+  c->p16_valid = true;
+  c->sync();
+}
+
+void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode) {
+  (void)mode;  // the plan carries the mode's ranks
+  for (int s0 = 0; s0 < nrhs; s0 += MR) {
+    const int nr = std::min(MR, nrhs - s0);
+    c->timed("gather", [&] {
+      const long long total = 48LL * c->n_cols;
+      gather16_kernel<<<grid_for(c, (total + 255) / 256, 16), 256, 0, c->stream>>>(
+          dx, c->d_xi16.p, c->d_cperm.p, c->n_cols, s0, nr);
+    });
+    if (c->n_z16 > 0)
+      c->timed("hmv16_z", [&] {
+        hmv16_z_kernel<<<grid_for(c, c->n_z16, 8), 192, 0, c->stream>>>(
+            c->d_z16.p, c->n_z16, c->d_mvb.p, c->d_items.p, c->d_rk16.p, c->d_arena.p,
+            c->d_xi16.p, c->d_zpart16.p);
+      });
+    if (c->n_zs16 > 0)
+      c->timed("hmv16_zsum", [&] {
+        hmv16_zsum_kernel<<<grid_for(c, c->n_zs16, 8), 256, 0, c->stream>>>(
+            c->d_zs16.p, c->n_zs16, c->d_zpart16.p);
+      });
+    c->timed("hmv16_leaf", [&] {
+      hmv16_leaf_kernel<<<grid_for(c, (c->n_tiles16 + 7) / 8, 8), 256, 0, c->stream>>>(
+          c->d_tiles16.p, c->n_tiles16, c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p,
+          c->d_leaf_blk.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p, c->d_zb16.p,
+          c->d_arena.p, c->d_dense.p, c->d_xi16.p, c->d_zpart16.p, c->d_rperm.p,
+          c->n_rows, dy, s0, nr);
+    });
+  }
 }
 
 void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
@@ -1487,6 +1587,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     cudaEventDestroy(tn1);
     build_matvec(c);
     c->plan_valid = false;
+    c->p16_valid = false;
     phase("build_matvec");
     c->assembled = true;
     if (stats) {
@@ -1555,6 +1656,26 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
     if (c->row_begin != 0 || c->row_end != c->n_rows)
       CK(cudaMemsetAsync(dy, 0, ny * sizeof(double), c->stream));
     static const bool force_v1 = std::getenv("HMGPU_MATVEC_V1") != nullptr;
+    if (nrhs > 1 && c->NC == 6 && !force_v1) {
+      bool ok = true;
+      if (!c->p16_valid || c->p16_mode != mode) {
+        try {
+          build_plan16(c, mode);
+        } catch (const Fail& f) {
+          if (f.code != HMGPU_ERR_INVALID) throw;
+          ok = false;  // ranks beyond the shared-memory Z: block sweep below
+          c->p16_valid = false;
+        }
+      }
+      if (ok) {
+        launch_mrhs(c, dx, dy, nrhs, mode);
+        if (ptr_kind == HMGPU_PTR_HOST) {
+          CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          c->sync();
+        }
+        return;
+      }
+    }
     bool streamed = !force_v1;
     if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
       try {
@@ -1623,6 +1744,7 @@ int hmgpu_promote(hmgpu_ctx* c, int n, const int* comp_block) {
     });
     for (int i : ids) c->items[i].kcur = c->items[i].k;
     c->plan_valid = false;
+    c->p16_valid = false;
     c->sync();
   });
 }
@@ -1650,6 +1772,7 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
     download_items(c);
     refresh_matvec_ranks(c);
     c->plan_valid = false;
+    c->p16_valid = false;
   });
 }
 

@@ -96,6 +96,22 @@ def test_c1_matvec_deterministic_and_multi_rhs(c1):
     assert rel(y01, 2.0 * Y[:, 0] - 0.5 * Y[:, 1]) < 1e-13
 
 
+@pytest.mark.parametrize("nrhs", [2, 16, 17, 35])
+def test_c1_multi_rhs_dmma_sweep(c1, nrhs):
+    """nrhs > 1 runs the fp64 tensor-core sweep (16 RHS per pass, zero-padded
+    remainder); every column must equal the single-RHS product."""
+    g, o = c1["g"], c1["o"]
+    X = np.asfortranarray(np.stack([RV(3 * 1280, 100 + s) for s in range(nrhs)], axis=1))
+    for mode, om in ((hm.Mode.Current, 0), (hm.Mode.Lookahead, 1)):
+        Y = g.matvec(X, mode)
+        assert Y.shape == X.shape
+        assert (Y == g.matvec(X, mode)).all()  # deterministic
+        for q in (0, nrhs // 2, nrhs - 1):
+            y = g.matvec(np.ascontiguousarray(X[:, q]), mode)
+            assert rel(Y[:, q], y) < 1e-13
+            assert rel(Y[:, q], o.matvec(np.ascontiguousarray(X[:, q]), om)) < 1e-12
+
+
 def test_c1_factors_match_oracle(c1):
     g, o = c1["g"], c1["o"]
     blocks = g.partition_blocks()
