@@ -184,6 +184,9 @@ int hmgpu_storage(hmgpu_ctx* ctx, hmgpu_storage_info* info);
 /* measured DFMA throughput of the device (TFLOP/s, 2 flops per FMA): the
  * fp64 roofline denominator of the assembly kernels */
 int hmgpu_fp64_peak(int device, double* tflops);
+/* measured fp64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s:
+   the peak the multi-RHS sweep is reported against */
+int hmgpu_dmma_peak(int device, double* tflops);
 
 /* CUDA-event timing of every kernel launch (off by default).  names are
  * "gather", "nearfield", "aca", "hmv_blocks", "hmv_reduce", "tail", ...

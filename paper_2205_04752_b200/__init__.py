@@ -3,14 +3,14 @@
 blocks, near-field fill and the H-matvec on sm_100a, behind the C ABI of
 include/hmgpu.h, with a host layer mirroring the reference's operator API.
 """
-from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflops, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
+from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflops, dmma_peak_tflops, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
                   AssemblyStats, BlockTerm, ClusterTree, ConfigError, DeviceError,
                   DimensionError, Error, GammaContributions, HMatrix, Mesh, MeshError,
                   Mode, amvm_multiply, assemble, device_count, gamma_contributions,
                   host_tree_and_partition)
 
 __all__ = [
-    "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
+    "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
     "AssemblyStats", "BlockTerm", "ClusterTree", "ConfigError", "DeviceError",
     "DimensionError", "Error", "GammaContributions", "HMatrix", "Mesh", "MeshError",
     "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",

@@ -88,6 +88,7 @@ _sig(gpu, "hmgpu_set_profiling", I, P, I)
 _sig(gpu, "hmgpu_kernel_times", I, P, C.c_char_p, DP, LLP, I)
 _sig(gpu, "hmgpu_storage", I, P, P)
 _sig(gpu, "hmgpu_fp64_peak", I, I, DP)
+_sig(gpu, "hmgpu_dmma_peak", I, I, DP)
 
 HMGPU_SYMBOLS = [
     "hmgpu_device_count", "hmgpu_create", "hmgpu_destroy", "hmgpu_last_error",
@@ -96,5 +97,5 @@ HMGPU_SYMBOLS = [
     "hmgpu_set_partition", "hmgpu_assemble", "hmgpu_ranks", "hmgpu_matvec",
     "hmgpu_promote", "hmgpu_extend", "hmgpu_tail_terms", "hmgpu_download_factor",
     "hmgpu_download_dense", "hmgpu_storage", "hmgpu_set_profiling",
-    "hmgpu_kernel_times", "hmgpu_fp64_peak",
+    "hmgpu_kernel_times", "hmgpu_fp64_peak", "hmgpu_dmma_peak",
 ]

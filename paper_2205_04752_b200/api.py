@@ -498,6 +498,16 @@ def random_vector(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
     return out
 
 
+def dmma_peak_tflops(device: int = 0) -> float:
+    """Measured fp64 tensor-core (DMMA) throughput of the device: the roofline
+    denominator of the multi-RHS sweep."""
+    v = C.c_double()
+    st = _lib.gpu.hmgpu_dmma_peak(device, C.byref(v))
+    if st:
+        raise DeviceError("hmgpu_dmma_peak failed", st)
+    return v.value
+
+
 def fp64_peak_tflops(device: int = 0) -> float:
     """Measured DFMA throughput of the device (fp64 roofline denominator)."""
     v = C.c_double()

@@ -1958,6 +1958,41 @@ int hmgpu_fp64_peak(int device, double* tflops) {
   return HMGPU_OK;
 }
 
+int hmgpu_dmma_peak(int device, double* tflops) {
+  if (!tflops) return HMGPU_ERR_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return HMGPU_ERR_NODEVICE;
+  if (device < 0 || device >= count) return HMGPU_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return HMGPU_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return HMGPU_ERR_OOM;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = sms * 8, iters = 1 << 12;
+  dmma_peak_kernel<<<grid, 256>>>(out, 64);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    dmma_peak_kernel<<<grid, 256>>>(out, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    best = std::min(best, ms);
+  }
+  const cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  if (e != cudaSuccess) return HMGPU_ERR_CUDA;
+  const double flops = 512.0 * 8.0 * iters * (double)grid * 8.0;  // 8 warps per CTA
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return HMGPU_OK;
+}
+
 int hmgpu_set_profiling(hmgpu_ctx* c, int on) {
   return guard(c, [&] { c->prof = on != 0; });
 }

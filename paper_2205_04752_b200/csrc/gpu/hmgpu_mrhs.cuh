@@ -314,4 +314,21 @@ hmv16_leaf_kernel(const int2* __restrict__ tiles, int ntiles,
   }
 }
 
+// fp64 tensor-core peak probe: eight independent DMMA chains per warp
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  const double a = 1.0 + lane * 1e-9, b = 1e-9;
+  double d[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) d[q][0] = d[q][1] = q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dmma(d[q][0], d[q][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += d[q][0] + d[q][1];
+  if (s == 12345.678) out[0] = s;  // practically never; keeps the chains live
+}
+
 }  // namespace hmgpu
