@@ -323,29 +323,34 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+// Max / arg-max of non-negative doubles with the integer reduction unit
+// (redux.sync): for x >= 0 the IEEE bit pattern is monotonic, so the max is
+// found on the high then the low 32 bits.  Exact (no arithmetic on values).
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
+  const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+  return ((unsigned long long)hi << 32) | lo;
 }
-// first-max arg-max: larger value wins, ties go to the smaller index
+// max of v >= 0 over the warp
+__device__ __forceinline__ double warp_max(double v) {
+  return __longlong_as_double((long long)warp_max_u64((unsigned long long)__double_as_longlong(v)));
+}
+// first-max arg-max: larger val wins, ties go to the smaller index; lanes
+// without a candidate carry val < 0 (and idx -1).  val >= 0 otherwise.
 __device__ __forceinline__ void warp_argmax(double& val, int& idx, double& aux) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double v2 = __shfl_xor_sync(0xffffffffu, val, o);
-    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-    const double a2 = __shfl_xor_sync(0xffffffffu, aux, o);
-    if (v2 > val || (v2 == val && i2 >= 0 && (idx < 0 || i2 < idx))) {
-      val = v2;
-      idx = i2;
-      aux = a2;
-    }
-  }
+  const unsigned long long key =
+      val >= 0.0 ? (unsigned long long)__double_as_longlong(val) + 1ull : 0ull;
+  const unsigned long long mk = warp_max_u64(key);
+  const bool win = key == mk;
+  const int mi = __reduce_min_sync(0xffffffffu, win ? idx : 0x7fffffff);
+  const unsigned bal = __ballot_sync(0xffffffffu, win && idx == mi);
+  const int src = __ffs(bal) - 1;
+  aux = __shfl_sync(0xffffffffu, aux, src);
+  val = __shfl_sync(0xffffffffu, val, src);
+  idx = mi;
 }
 __device__ __forceinline__ int warp_min_int(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  return __reduce_min_sync(0xffffffffu, v);
 }
 
 // Residual of one row (is_row) or one column of the block, one warp:
@@ -360,9 +365,24 @@ struct LineStats {
   int pj, nq;
 };
 
+// Entry source of the ACA: evaluates the kernel from the geometry in HBM.
+// (A variant that evaluated small blocks whole into shared memory first,
+// all six components together, was measured slower: the per-step chain of
+// small blocks is dominated by the factor loads and warp reductions, and the
+// CTA-per-block occupancy was lower.)
 template <int KIND>
-__device__ __forceinline__ LineStats residual_line(const Geom& g, int row0, int col0, int comp,
-                                                   bool is_row, int fix,
+struct EvalSrc {
+  const Geom& g;
+  int row0, col0, comp;
+  __device__ __forceinline__ double operator()(bool is_row, int fix, int t, int& nq) const {
+    const int i = is_row ? row0 + fix : row0 + t;
+    const int j = is_row ? col0 + t : col0 + fix;
+    return entry_k<KIND>(g, i, j, comp, nq);
+  }
+};
+
+template <class SRC>
+__device__ __forceinline__ LineStats residual_line(const SRC& src, bool is_row, int fix,
                                                    const double* __restrict__ W, int ldw,
                                                    const double* __restrict__ X, int ldx,
                                                    int len, int k, double* __restrict__ out,
@@ -370,26 +390,21 @@ __device__ __forceinline__ LineStats residual_line(const Geom& g, int row0, int 
   LineStats st{0.0, -1.0, 0.0, 0.0, -1, 0};
   for (int base = 0; base < len; base += 128) {
     const int nb = min(4, (len - base + 31) >> 5);  // warp-uniform
+    double v[4];
+    bool ok[4];
     // phase A: the kernel entries of up to 4 columns per lane (arithmetic
     // only; parked in this lane's shared-memory slots)
 #pragma unroll 1
     for (int s = 0; s < nb; ++s) {
       const int t = base + 32 * s + lane;
-      double a = 0.0;
-      if (t < len) {
-        const int i = is_row ? row0 + fix : row0 + t;
-        const int j = is_row ? col0 + t : col0 + fix;
-        a = entry_k<KIND>(g, i, j, comp, st.nq);
-      }
-      ebuf[32 * s + lane] = a;
+      ebuf[32 * s + lane] = t < len ? src(is_row, fix, t, st.nq) : 0.0;
     }
     // phase B: the low-rank correction, four independent columns per lane so
     // that eight panel loads are in flight per lane
-    double v[4];
-    bool ok[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      ok[s] = s < nb && base + 32 * s + lane < len;
+      const int t = base + 32 * s + lane;
+      ok[s] = s < nb && t < len;
       v[s] = ok[s] ? ebuf[32 * s + lane] : 0.0;
       if (ok[s]) st.rs = fmax(st.rs, fabs(v[s]));
     }
@@ -505,8 +520,8 @@ __device__ __forceinline__ double cross_terms(const double* __restrict__ uk,
 // sf < 0 disables the accuracy test (extension mode).  The candidate row
 // residual is built in V(:,k) and the column residual in U(:,k); both are
 // only committed (k += 1) when the step is accepted.
-template <int KIND>
-__device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
+template <class SRC>
+__device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
                              double* __restrict__ V, int2* __restrict__ piv,
                              uint8_t* __restrict__ Z, double sf, int lane, int& nq_acc,
                              double* __restrict__ ebuf) {
@@ -550,8 +565,8 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
       const bool is_row = pass == 0;
-      const LineStats ls = residual_line<KIND>(
-          g, s.row0, s.col0, s.comp, is_row, fix, is_row ? U : V, is_row ? m : n,
+      const LineStats ls = residual_line(
+          src, is_row, fix, is_row ? U : V, is_row ? m : n,
           is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, lane);
       nq_acc += ls.nq;
       s.entries += is_row ? n : m;
@@ -599,14 +614,13 @@ __device__ int aca_step_warp(const Geom& g, Item& s, double* __restrict__ U,
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
 //   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
 // One call site of the step for all phases (code size).
-template <int KIND>
-__device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
+template <class SRC>
+__device__ void aca_item_warp(const SRC& src, Item& s, Item* __restrict__ items, int idx,
                               double* __restrict__ arena, int2* __restrict__ pivots,
                               uint8_t* __restrict__ cons, double sf_run,
                               long long max_rank, int lookahead,
                               int* __restrict__ overflow, int lane,
                               double* __restrict__ ebuf) {
-  Item s = items[idx];
   double* U = arena + s.u_off;
   double* V = arena + s.v_off;
   int2* piv = pivots + s.p_off;
@@ -624,7 +638,7 @@ __device__ void aca_item_warp(const Geom& g, Item* __restrict__ items, int idx,
         s.status = ST_OVERFLOW;
         break;
       }
-      st = aca_step_warp<KIND>(g, s, U, V, piv, Z, run ? sf_run : -1.0, lane, nq_acc, ebuf);
+      st = aca_step_warp(src, s, U, V, piv, Z, run ? sf_run : -1.0, lane, nq_acc, ebuf);
       if (st == STOP_NONE) {
         if (!run) s.steps_left--;
         continue;
@@ -678,8 +692,11 @@ aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
     if (lane == 0) t = atomicAdd(counter, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nlist) return;
-    aca_item_warp<KIND>(g, items, list[t], arena, pivots, cons, sf_run, max_rank,
-                        lookahead, overflow, lane, ebuf);
+    const int idx = list[t];
+    Item s = items[idx];
+    const EvalSrc<KIND> src{g, s.row0, s.col0, s.comp};
+    aca_item_warp(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead,
+                  overflow, lane, ebuf);
   }
 }
 
