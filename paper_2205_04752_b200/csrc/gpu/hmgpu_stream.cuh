@@ -453,28 +453,67 @@ hmv_warp_kernel(WarpStreamParams P) {
   }
 }
 
-// per leaf: y(p) = sum over covering job rows (fixed order)
+// per leaf: y(p) = sum over covering job rows (fixed order).  The leaf's
+// entries are staged in shared memory once; each thread sums its (row, r)
+// over them with eight independent partial-row loads in flight.
 template <int NOUT>
-__global__ void hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin,
-                                       const int* __restrict__ leaf_end,
-                                       const int* __restrict__ leaf_ptr,
-                                       const LeafEntry* __restrict__ entries, int nleaves,
-                                       const double* __restrict__ ypart,
-                                       const int* __restrict__ rperm, int nrows,
-                                       double* __restrict__ y) {
+__global__ void __launch_bounds__(128)
+hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin, const int* __restrict__ leaf_end,
+                       const int* __restrict__ leaf_ptr,
+                       const LeafEntry* __restrict__ entries, int nleaves,
+                       const double* __restrict__ ypart, const int* __restrict__ rperm,
+                       int nrows, double* __restrict__ y) {
+  constexpr int EC = 256;  // entries staged per round
+  __shared__ LeafEntry se[EC];
   for (int L = blockIdx.x; L < nleaves; L += gridDim.x) {
     const int b0 = leaf_begin[L], b1 = leaf_end[L];
     const int e0 = leaf_ptr[L], e1 = leaf_ptr[L + 1];
     const int cnt = (b1 - b0) * NOUT;
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const int r = t % NOUT;
-      const int i = t / NOUT;
-      double s = 0.0;
-      for (int e = e0; e < e1; ++e) {
-        const LeafEntry en = entries[e];
-        if (i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
+    double acc[2] = {0.0, 0.0};  // threads cover up to 256 (row, r) pairs per leaf
+    for (int c0 = e0; c0 < e1; c0 += EC) {
+      const int ne = min(EC, e1 - c0);
+      __syncthreads();
+      for (int q = threadIdx.x; q < ne; q += blockDim.x) se[q] = entries[c0 + q];
+      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = threadIdx.x + h * blockDim.x;
+        if (t >= cnt) continue;
+        const int r = t % NOUT, i = t / NOUT;
+        double s = acc[h];
+        int e = 0;
+        for (; e + 8 <= ne; e += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const LeafEntry en = se[e + u];
+            v[u] = (i >= en.lo && i < en.hi) ? ypart[(en.slot + (i - en.lo)) * NOUT + r] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; e < ne; ++e) {
+          const LeafEntry en = se[e];
+          if (i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
+        }
+        acc[h] = s;
       }
-      y[(long long)r * nrows + rperm[b0 + i]] = s;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = threadIdx.x + h * blockDim.x;
+      if (t < cnt) y[(long long)(t % NOUT) * nrows + rperm[b0 + t / NOUT]] = acc[h];
+    }
+    if (cnt > 2 * (int)blockDim.x) {  // leaves wider than 256 (row, r) pairs
+      for (int t = 2 * blockDim.x + threadIdx.x; t < cnt; t += blockDim.x) {
+        const int r = t % NOUT, i = t / NOUT;
+        double s = 0.0;
+        for (int e = e0; e < e1; ++e) {
+          const LeafEntry en = entries[e];
+          if (i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
+        }
+        y[(long long)r * nrows + rperm[b0 + i]] = s;
+      }
     }
   }
 }
