@@ -1,6 +1,7 @@
 """Per-source-line instruction / stall shares of one kernel in an ncu report,
 mapping SASS offsets to lines with nvdisasm -g of the built library
-(development helper).  usage: ncu_src_lines.py <rep> <lib.so> <kernel-substr> [top]"""
+(development helper).
+usage: ncu_src_lines.py <rep> <lib.so> <mangled-substr> [top] [launch-skip] [name-regex]"""
 import collections, csv, io, os, re, subprocess, sys, tempfile
 rep, lib, pat = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
@@ -20,7 +21,11 @@ for l in txt.split("\n"):
     if fn and pat in fn:
         m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
         if m: ins[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+skip = sys.argv[5] if len(sys.argv) > 5 else "0"
+kre = sys.argv[6] if len(sys.argv) > 6 else pat  # demangled-name regex for ncu
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                      "--kernel-name", "regex:" + kre, "--launch-skip", skip,
+                      "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]; data = rows[2:]
