@@ -167,6 +167,20 @@ int hmgpu_extend(hmgpu_ctx* ctx, int n, const int* comp_block, int steps);
  * rows in internal order.  Two-call protocol: with meta == NULL returns the
  * number of terms and total values; then fills meta rows
  * [comp, block, n_occ, off] and vals.  x is a host pointer. */
+/* Device-resident estimator of the adaptive matvec (Algorithm 2; replaces
+   gamma_contributions + mark_blocks, amvm.cpp:46-184, and the promote /
+   extend_lookahead calls of amvm_multiply, amvm.cpp:255-266):
+   hmgpu_amvm_estimate   tail terms, difference (optional host copy, rows in
+                         external component-major order) and gamma = ||difference||
+   hmgpu_amvm_mark       theta-marking walk on the device; gamma(P_k), count
+   hmgpu_amvm_refine     promote + extend_lookahead(steps) of the marked
+                         (comp, block) pairs (optional host copy of the pairs)
+   Whole (unsharded) operators only. */
+int hmgpu_amvm_estimate(hmgpu_ctx* ctx, const double* x, double* gamma, double* difference);
+int hmgpu_amvm_mark(hmgpu_ctx* ctx, double theta, int c_sp, long long m_rows,
+                    long long n_cols, double* gamma_pk, int* n_marked);
+int hmgpu_amvm_refine(hmgpu_ctx* ctx, int steps, int* comp_block);
+
 int hmgpu_tail_terms(hmgpu_ctx* ctx, const double* x, int* n_terms,
                      long long* n_vals, long long* meta4, double* vals);
 

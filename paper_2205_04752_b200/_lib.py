@@ -97,5 +97,6 @@ HMGPU_SYMBOLS = [
     "hmgpu_set_partition", "hmgpu_assemble", "hmgpu_ranks", "hmgpu_matvec",
     "hmgpu_promote", "hmgpu_extend", "hmgpu_tail_terms", "hmgpu_download_factor",
     "hmgpu_download_dense", "hmgpu_storage", "hmgpu_set_profiling",
-    "hmgpu_kernel_times", "hmgpu_fp64_peak", "hmgpu_dmma_peak",
+    "hmgpu_kernel_times", "hmgpu_fp64_peak", "hmgpu_dmma_peak", "hmgpu_amvm_estimate",
+    "hmgpu_amvm_mark", "hmgpu_amvm_refine",
 ]

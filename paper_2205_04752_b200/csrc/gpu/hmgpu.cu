@@ -21,12 +21,14 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "hmgpu.h"
 #include "hmgpu_device.cuh"
 #include "hmgpu_stream.cuh"
 #include "hmgpu_mrhs.cuh"
+#include "hmgpu_amvm.cuh"
 
 using namespace hmgpu;
 
@@ -265,6 +267,21 @@ struct hmgpu_ctx {
   DBuf<double> d_sarena, d_zpart;
   DBuf<LeafEntry> d_pentries;
 
+  // ---- device-resident AMVM estimator (hmgpu_amvm.cuh) ----
+  bool am_geom_valid = false;
+  DBuf<int> d_row_leaf, d_sortp, d_tix, d_term_bi, d_cnt, d_ptr, d_lists, d_order, d_idx,
+      d_marked, d_nm, d_mids;
+  DBuf<long long> d_spoff, d_eptr, d_eidx, d_ecnt;
+  DBuf<double> d_eval;
+  DBuf<TailTerm> d_aterms;
+  DBuf<double> d_aout, d_diff, d_resid, d_nsq, d_sc;
+  DBuf<unsigned long long> d_keys, d_keys2;
+  DBuf<unsigned char> d_inset, d_cub;
+  int am_nterms = 0;
+  long long am_nvals = 0;
+  bool am_have_estimate = false;
+  std::vector<int> marked_ids;
+
   // ---- multi-RHS (16 per pass, fp64 tensor cores) plan ----
   bool p16_valid = false;
   int p16_mode = -1;
@@ -307,6 +324,11 @@ struct hmgpu_ctx {
     d_pentries.free(); d_pleaf_ptr.free();
     d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
     d_rk16.free(); d_tiles16.free();
+    d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
+    d_ptr.free(); d_lists.free(); d_order.free(); d_idx.free(); d_marked.free(); d_nm.free();
+    d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
+    d_resid.free(); d_nsq.free(); d_sc.free(); d_keys.free(); d_keys2.free();
+    d_inset.free(); d_cub.free(); d_eptr.free(); d_eidx.free(); d_eval.free(); d_ecnt.free();
     if (stream) cudaStreamSynchronize(stream);
     if (pool) cudaMemPoolDestroy(pool);
     g_pool = nullptr;
@@ -741,6 +763,8 @@ void build_matvec(hmgpu_ctx* c) {
   c->d_leaf_end.upload(c->leaf_end, c->stream);
   c->d_leaf_ptr.upload(c->leaf_ptr, c->stream);
   c->d_leaf_blk.upload(c->leaf_blk, c->stream);
+  c->am_geom_valid = false;
+  c->am_have_estimate = false;
   c->d_leaf_prow.upload(c->leaf_prow, c->stream);
   c->sync();
 }
@@ -1731,21 +1755,103 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
   });
 }
 
+namespace {
+void promote_ids(hmgpu_ctx* c, const std::vector<int>& ids) {
+  if (ids.empty()) return;
+  c->d_list.upload(ids, c->stream);
+  c->timed("promote", [&] {
+    promote_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
+        c->d_items.p, c->d_list.p, (int)ids.size());
+  });
+  for (int i : ids) c->items[i].kcur = c->items[i].k;
+  c->plan_valid = false;
+  c->p16_valid = false;
+  c->sync();
+}
+
+void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  if (ids.empty() || steps == 0) return;
+  if (c->kind == KIND_KELVIN) upload_rules(c);
+  c->d_list.upload(ids, c->stream);
+  c->timed("prep_extend", [&] {
+    prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
+        c->d_items.p, c->d_list.p, (int)ids.size(), steps);
+  });
+  c->sync();
+  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+    return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
+  });
+  run_aca(c, ids, nullptr);
+  download_items(c);
+  refresh_matvec_ranks(c);
+  c->plan_valid = false;
+  c->p16_valid = false;
+}
+
+// per-partition tables of the estimator: leaf of every internal row, and per
+// matvec block its local rows in ascending external order
+void build_amvm_geometry(hmgpu_ctx* c) {
+  if (c->am_geom_valid) return;
+  std::vector<int> row_leaf(std::max(c->n_rows, 1), 0);
+  for (size_t l = 0; l < c->leaf_begin.size(); ++l)
+    for (int p = c->leaf_begin[l]; p < c->leaf_end[l]; ++p) row_leaf[p] = (int)l;
+  std::vector<long long> spoff(std::max(c->n_mv, 1), 0);
+  std::vector<int> sortp;
+  std::map<std::pair<int, int>, long long> seen;  // (row0, m) -> offset
+  for (int bi = 0; bi < c->n_mv; ++bi) {
+    const MvBlock& mb = c->mvb[bi];
+    if (mb.dense) continue;
+    auto key = std::make_pair(mb.row0, mb.m);
+    auto f = seen.find(key);
+    if (f != seen.end()) {
+      spoff[bi] = f->second;
+      continue;
+    }
+    const long long off = (long long)sortp.size();
+    std::vector<int> loc(mb.m);
+    std::iota(loc.begin(), loc.end(), 0);
+    std::sort(loc.begin(), loc.end(), [&](int a, int b) {
+      return c->rperm[mb.row0 + a] < c->rperm[mb.row0 + b];
+    });
+    sortp.insert(sortp.end(), loc.begin(), loc.end());
+    seen[key] = off;
+    spoff[bi] = off;
+  }
+  if (sortp.empty()) sortp.push_back(0);
+  c->d_row_leaf.upload(row_leaf, c->stream);
+  c->d_spoff.upload(spoff, c->stream);
+  c->d_sortp.upload(sortp, c->stream);
+  c->sync();
+  c->am_geom_valid = true;
+}
+
+AmvmGeom amvm_geom(hmgpu_ctx* c) {
+  AmvmGeom a{};
+  a.row_leaf = c->d_row_leaf.p;
+  a.leaf_begin = c->d_leaf_begin.p;
+  a.leaf_ptr = c->d_leaf_ptr.p;
+  a.leaf_blk = c->d_leaf_blk.p;
+  a.blocks = c->d_mvb.p;
+  a.rperm = c->d_rperm.p;
+  a.tix = c->d_tix.p;
+  a.terms = c->d_aterms.p;
+  a.term_bi = c->d_term_bi.p;
+  a.sortp = c->d_sortp.p;
+  a.spoff = c->d_spoff.p;
+  a.out = c->d_aout.p;
+  a.N = c->n_rows;
+  a.grid = c->NC == 6 ? 1 : 0;
+  return a;
+}
+}  // namespace
+
 int hmgpu_promote(hmgpu_ctx* c, int n, const int* comp_block) {
   return guard(c, [&] {
     if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
     if (n < 0 || (n > 0 && !comp_block)) fail(HMGPU_ERR_INVALID, "bad pairs");
-    std::vector<int> ids = items_from_pairs(c, n, comp_block);
-    if (ids.empty()) return;
-    c->d_list.upload(ids, c->stream);
-    c->timed("promote", [&] {
-      promote_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
-          c->d_items.p, c->d_list.p, (int)ids.size());
-    });
-    for (int i : ids) c->items[i].kcur = c->items[i].k;
-    c->plan_valid = false;
-    c->p16_valid = false;
-    c->sync();
+    promote_ids(c, items_from_pairs(c, n, comp_block));
   });
 }
 
@@ -1754,25 +1860,187 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
     if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
     if (n < 0 || (n > 0 && !comp_block) || steps < 0)
       fail(HMGPU_ERR_INVALID, "bad extend arguments");
-    std::vector<int> ids = items_from_pairs(c, n, comp_block);
-    std::sort(ids.begin(), ids.end());
-    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-    if (ids.empty() || steps == 0) return;
-    if (c->kind == KIND_KELVIN) upload_rules(c);
-    c->d_list.upload(ids, c->stream);
-    c->timed("prep_extend", [&] {
-      prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
-          c->d_items.p, c->d_list.p, (int)ids.size(), steps);
+    extend_ids(c, items_from_pairs(c, n, comp_block), steps);
+  });
+}
+
+int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* difference) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (!x || !gamma) fail(HMGPU_ERR_INVALID, "null x / gamma");
+    if (c->row_begin != 0 || c->row_end != c->n_rows)
+      fail(HMGPU_ERR_INVALID, "the estimator needs the whole operator (no shard)");
+    build_amvm_geometry(c);
+    // terms: (comp, block) with a look-ahead tail, component-major, blocks
+    // ascending (amvm.cpp:135-150)
+    std::vector<TailTerm> terms;
+    std::vector<int> term_bi;
+    std::vector<int> tix(c->items.size(), -1);
+    for (int q = 0; q < c->NC; ++q)
+      for (int bi = 0; bi < c->n_mv; ++bi) {
+        const MvBlock& mb = c->mvb[bi];
+        if (mb.dense) continue;
+        const Item& it = c->items[mb.item0 + q];
+        if (it.k <= it.kcur) continue;
+        const int nocc = (c->NC == 6 && c_comp_host_r(q) != c_comp_host_c(q)) ? 2 : 1;
+        tix[mb.item0 + q] = (int)terms.size();
+        terms.push_back({mb.item0 + q, nocc, 0});
+        term_bi.push_back(bi);
+      }
+    long long off = 0;
+    for (TailTerm& t : terms) {
+      t.off = off;
+      off += (long long)t.nocc * c->items[t.item].m;
+    }
+    c->am_nterms = (int)terms.size();
+    c->am_nvals = off;
+    const long long M = (long long)c->ndof_rows();
+    c->d_diff.ensure((size_t)M);
+    c->d_sc.ensure(4);
+    if (terms.empty()) {
+      c->d_aterms.ensure(1);
+      c->d_term_bi.ensure(1);
+    } else {
+      c->d_aterms.upload(terms, c->stream);
+      c->d_term_bi.upload(term_bi, c->stream);
+    }
+    if (tix.empty()) c->d_tix.ensure(1);
+    else c->d_tix.upload(tix, c->stream);
+    c->d_aout.ensure((size_t)std::max<long long>(off, 1));
+    const long long nx = c->ndof_cols();
+    c->d_x.ensure((size_t)nx);
+    CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    gather_x(c, c->d_x.p, 1);
+    if (!terms.empty())
+      c->timed("tail", [&] {
+        const int grid = grid_for(c, ((long long)terms.size() + 7) / 8, 8);
+        if (c->NC == 6)
+          tail_kernel<3><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, (int)terms.size(),
+                                                     c->d_items.p, c->d_arena.p, c->d_xi.p,
+                                                     c->d_aout.p, 1);
+        else
+          tail_kernel<1><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, (int)terms.size(),
+                                                     c->d_items.p, c->d_arena.p, c->d_xi.p,
+                                                     c->d_aout.p, 0);
+      });
+    const AmvmGeom a = amvm_geom(c);
+    c->timed("amvm_diff", [&] {
+      amvm_diff_kernel<<<(c->n_rows + 127) / 128, 128, 0, c->stream>>>(a, c->d_diff.p);
     });
+    amvm_sumsq_kernel<<<1, 32, 0, c->stream>>>(c->d_diff.p, M, c->d_sc.p);
+    CK(cudaGetLastError());
+    double sc[2];
+    CK(cudaMemcpyAsync(sc, c->d_sc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (difference)
+      CK(cudaMemcpyAsync(difference, c->d_diff.p, M * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
     c->sync();
-    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
-      return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
+    *gamma = sc[1];
+    c->am_have_estimate = true;
+  });
+}
+
+int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long long n_cols,
+                    double* gamma_pk, int* n_marked) {
+  return guard(c, [&] {
+    if (!c->am_have_estimate) fail(HMGPU_ERR_STATE, "hmgpu_amvm_estimate first");
+    if (!gamma_pk || !n_marked) fail(HMGPU_ERR_INVALID, "null outputs");
+    const long long M = (long long)c->ndof_rows();
+    const int nt = c->am_nterms;
+    c->marked_ids.clear();
+    const AmvmGeom a = amvm_geom(c);
+    const double csp_mn = (double)c_sp * (double)m_rows * (double)n_cols;
+    c->d_nsq.ensure((size_t)std::max(nt, 1));
+    c->d_cnt.ensure((size_t)M + 1);
+    c->d_ptr.ensure((size_t)M + 1);
+    c->d_lists.ensure((size_t)std::max<long long>(c->am_nvals, 1));
+    c->d_keys.ensure((size_t)M);
+    c->d_keys2.ensure((size_t)M);
+    c->d_idx.ensure((size_t)M);
+    c->d_order.ensure((size_t)M);
+    c->d_resid.ensure((size_t)M);
+    c->d_inset.ensure((size_t)std::max(nt, 1));
+    c->d_marked.ensure((size_t)std::max(nt, 1));
+    c->d_mids.ensure((size_t)std::max(nt, 1));
+    c->d_nm.ensure(1);
+    // term entries (ascending output index) and |term|^2
+    c->d_eptr.ensure((size_t)nt + 1);
+    c->d_eidx.ensure((size_t)std::max<long long>(c->am_nvals, 1));
+    c->d_eval.ensure((size_t)std::max<long long>(c->am_nvals, 1));
+    if (nt > 0) {
+      c->d_ecnt.ensure((size_t)nt + 1);
+      CK(cudaMemsetAsync(c->d_ecnt.p + nt, 0, sizeof(long long), c->stream));
+      amvm_entries_kernel<<<(nt + 127) / 128, 128, 0, c->stream>>>(
+          a, c->d_items.p, nt, 0, c->d_ecnt.p, nullptr, nullptr, nullptr, nullptr);
+      size_t tbe = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tbe, c->d_ecnt.p, c->d_eptr.p, nt + 1,
+                                       c->stream));
+      c->d_cub.ensure(tbe);
+      CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, tbe, c->d_ecnt.p, c->d_eptr.p, nt + 1,
+                                       c->stream));
+      amvm_entries_kernel<<<(nt + 127) / 128, 128, 0, c->stream>>>(
+          a, c->d_items.p, nt, 1, nullptr, c->d_eptr.p, c->d_eidx.p, c->d_eval.p, c->d_nsq.p);
+    }
+    const int gr = (c->n_rows + 127) / 128;
+    CK(cudaMemsetAsync(c->d_cnt.p, 0, (M + 1) * sizeof(int), c->stream));
+    amvm_cand_kernel<<<gr, 128, 0, c->stream>>>(a, c->d_sc.p, theta, csp_mn, 0, c->d_cnt.p,
+                                                nullptr, nullptr);
+    size_t tb1 = 0, tb2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb1, c->d_cnt.p, c->d_ptr.p, (int)(M + 1),
+                                     c->stream));
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb2, c->d_keys.p, c->d_keys2.p,
+                                                 c->d_idx.p, c->d_order.p, (int)M, 0, 64,
+                                                 c->stream));
+    c->d_cub.ensure(std::max(tb1, tb2));
+    CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, tb1, c->d_cnt.p, c->d_ptr.p, (int)(M + 1),
+                                     c->stream));
+    amvm_cand_kernel<<<gr, 128, 0, c->stream>>>(a, c->d_sc.p, theta, csp_mn, 1, c->d_cnt.p,
+                                                c->d_ptr.p, c->d_lists.p);
+    amvm_keys_kernel<<<(int)((M + 255) / 256), 256, 0, c->stream>>>(c->d_diff.p, M,
+                                                                     c->d_keys.p, c->d_idx.p);
+    CK(cub::DeviceRadixSort::SortPairsDescending(c->d_cub.p, tb2, c->d_keys.p, c->d_keys2.p,
+                                                 c->d_idx.p, c->d_order.p, (int)M, 0, 64,
+                                                 c->stream));
+    CK(cudaMemcpyAsync(c->d_resid.p, c->d_diff.p, M * sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_inset.p, 0, (size_t)std::max(nt, 1), c->stream));
+    c->timed("amvm_walk", [&] {
+      amvm_walk_kernel<<<1, 32, 0, c->stream>>>(c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p,
+                                                c->d_lists.p, c->d_eptr.p, c->d_eidx.p,
+                                                c->d_eval.p, c->d_nsq.p, c->d_resid.p,
+                                                c->d_inset.p, c->d_marked.p, c->d_nm.p,
+                                                c->d_sc.p + 2);
     });
-    run_aca(c, ids, nullptr);
-    download_items(c);
-    refresh_matvec_ranks(c);
-    c->plan_valid = false;
-    c->p16_valid = false;
+    if (nt > 0)
+      amvm_items_kernel<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_aterms.p, c->d_marked.p,
+                                                                 c->d_nm.p, c->d_mids.p);
+    CK(cudaGetLastError());
+    int nm = 0;
+    double pk = 0.0;
+    CK(cudaMemcpyAsync(&nm, c->d_nm.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&pk, c->d_sc.p + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    c->marked_ids.resize(nm);
+    if (nm > 0)
+      CK(cudaMemcpyAsync(c->marked_ids.data(), c->d_mids.p, nm * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    *n_marked = nm;
+    *gamma_pk = pk;
+  });
+}
+
+int hmgpu_amvm_refine(hmgpu_ctx* c, int steps, int* comp_block) {
+  return guard(c, [&] {
+    if (steps < 0) fail(HMGPU_ERR_INVALID, "bad steps");
+    if (comp_block)
+      for (size_t q = 0; q < c->marked_ids.size(); ++q) {
+        comp_block[2 * q] = c->items[c->marked_ids[q]].comp;
+        comp_block[2 * q + 1] = c->items[c->marked_ids[q]].block;
+      }
+    promote_ids(c, c->marked_ids);
+    extend_ids(c, c->marked_ids, steps);
+    c->am_have_estimate = false;
   });
 }
 

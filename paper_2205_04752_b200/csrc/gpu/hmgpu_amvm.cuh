@@ -1,0 +1,272 @@
+// Device-resident error estimator and marking of the adaptive H-matvec
+// (Algorithm 2 of the paper).  One sweep of
+// amvm_multiply keeps everything on the device except a handful of scalars:
+//
+//   tail_kernel          t_b = U[:, k:K] (V[:, k:K]^T x_s) per (comp, block)
+//                        with a look-ahead tail (apply_range, aca.cpp:7-11)
+//   amvm_diff_kernel     difference(r) = sum of the terms at output row r, in
+//                        term order (gamma_contributions, amvm.cpp:46-125)
+//   amvm_entries_kernel  each term's entries in ascending output index and
+//                        |term|^2 (the sorted sparse terms of amvm.cpp:105-122)
+//   amvm_cand_kernel     per output row the terms with |value| >= tau, in
+//                        term order (the marking CSR, amvm.cpp:131-160)
+//   (CUB)                rows stably sorted by |difference| descending
+//   amvm_walk_kernel     the greedy walk until ||residual|| <= (1-theta) gamma
+//                        (amvm.cpp:160-184), gamma(P_k)
+//
+// Every floating-point reduction is restated in the oracle's order (term
+// order per row; ascending output index inside a term; sequential sums over
+// rows), so gamma, the marked set and gamma(P_k) are bit-identical to the
+// CPU oracle (tests/test_gpu_parity.py, tests/test_gpu_fullsize.py).
+//
+// Terms are (component, block) pairs with K > k, in component-major, block-
+// ascending order; an output row is (rb, p): block-row rb of the 3x3 grid and
+// internal row p, external index rb * N + rperm[p].  The blocks covering p
+// are the leaf entries of p's leaf (leaf_blk, ascending block order).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace hmgpu {
+
+struct AmvmGeom {
+  const int* row_leaf;     // internal row -> leaf
+  const int* leaf_begin;
+  const int* leaf_ptr;
+  const int2* leaf_blk;    // (matvec block, row offset of the leaf in the block)
+  const MvBlock* blocks;
+  const int* rperm;
+  const int* tix;          // item -> term index or -1
+  const TailTerm* terms;
+  const int* term_bi;      // term -> matvec block
+  const int* sortp;        // per matvec block: local rows in ascending rperm order
+  const long long* spoff;  // matvec block -> offset into sortp
+  const double* out;       // tail values [off + o * m + i]
+  int N;                   // rows of one component block (internal rows)
+  int grid;                // 1: 3x3 Kelvin grid (6 components), 0: scalar
+};
+
+// occurrence of component c in block-row rb: 0 (rows R, x_C), 1 (rows C, x_R)
+__device__ __forceinline__ int amvm_occ(int grid, int c, int rb) {
+  if (!grid) return 0;
+  const int R = c_comp_r[c], C = c_comp_c[c];
+  if (R == rb) return 0;
+  if (C == rb && R != C) return 1;
+  return -1;
+}
+
+// visits the terms at output row (rb, p) in term order: f(term, value)
+template <class F>
+__device__ __forceinline__ void amvm_row_terms(const AmvmGeom& a, int rb, int p, F&& f) {
+  const int L = a.row_leaf[p];
+  const int e0 = a.leaf_ptr[L], e1 = a.leaf_ptr[L + 1];
+  const int ncomp = a.grid ? 6 : 1;
+  for (int c = 0; c < ncomp; ++c) {
+    const int o = amvm_occ(a.grid, c, rb);
+    if (o < 0) continue;
+    for (int e = e0; e < e1; ++e) {
+      const int2 be = a.leaf_blk[e];
+      const MvBlock& b = a.blocks[be.x];
+      if (b.dense) continue;
+      const int t = a.tix[b.item0 + c];
+      if (t < 0) continue;
+      const int i = p - b.row0;
+      const double v = a.out[a.terms[t].off + (long long)o * b.m + i];
+      f(t, v);
+    }
+  }
+}
+
+__global__ void amvm_diff_kernel(AmvmGeom a, double* __restrict__ diff) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.N) return;
+  const int nrb = a.grid ? 3 : 1;
+  for (int rb = 0; rb < nrb; ++rb) {
+    double s = 0.0;
+    amvm_row_terms(a, rb, p, [&](int, double v) {
+      if (a.grid && v == 0.0) return;  // the occurrence scatter skips zeros
+      s += v;
+    });
+    diff[(long long)rb * a.N + a.rperm[p]] = s;
+  }
+}
+
+// one thread: s = sum_i d_i^2 in index order; out[0] = s, out[1] = sqrt(s)
+__global__ void amvm_sumsq_kernel(const double* __restrict__ d, long long n,
+                                  double* __restrict__ out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double s = 0.0;
+  for (long long i = 0; i < n; ++i) s += d[i] * d[i];
+  out[0] = s;
+  out[1] = sqrt(s);
+}
+
+// calls f(ext_index, value) over a term's entries in ascending output index
+template <class F>
+__device__ __forceinline__ void amvm_term_entries(const AmvmGeom& a, const Item* items,
+                                                  int t, F&& f) {
+  const TailTerm tt = a.terms[t];
+  const MvBlock& b = a.blocks[a.term_bi[t]];
+  const int comp = items[tt.item].comp;
+  const int* sp = a.sortp + a.spoff[a.term_bi[t]];
+  for (int o = 0; o < tt.nocc; ++o) {
+    const int rb = a.grid ? (o == 0 ? c_comp_r[comp] : c_comp_c[comp]) : 0;
+    const double* v = a.out + tt.off + (long long)o * b.m;
+    for (int q = 0; q < b.m; ++q) {
+      const int i = sp[q];
+      const double x = v[i];
+      if (a.grid && x == 0.0) continue;
+      f((long long)rb * a.N + a.rperm[b.row0 + i], x);
+    }
+  }
+}
+
+// pass 0: nnz[t] = entries of term t (zeros skipped on the grid);
+// pass 1: the entries (ascending output index) at eptr[t] and |term|^2
+__global__ void amvm_entries_kernel(AmvmGeom a, const Item* __restrict__ items, int nterms,
+                                    int pass, long long* __restrict__ nnz,
+                                    const long long* __restrict__ eptr,
+                                    long long* __restrict__ eidx, double* __restrict__ eval,
+                                    double* __restrict__ nsq) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nterms) return;
+  if (pass == 0) {
+    long long n = 0;
+    amvm_term_entries(a, items, t, [&](long long, double) { ++n; });
+    nnz[t] = n;
+    return;
+  }
+  long long e = eptr[t];
+  double s = 0.0;
+  amvm_term_entries(a, items, t, [&](long long i, double v) {
+    eidx[e] = i;
+    eval[e] = v;
+    ++e;
+    s += v * v;
+  });
+  nsq[t] = s;
+}
+
+// tau = (1 - theta) gamma / sqrt(c_sp M N) (amvm.cpp:138-140), from the device gamma
+__device__ __forceinline__ double amvm_tau(const double* sc, double theta, double csp_mn) {
+  return (1.0 - theta) * sc[1] / sqrt(csp_mn);
+}
+
+// pass 0: cnt[r] = number of terms with |value| >= tau at output row r;
+// pass 1: their term indices in term order at lists[ptr[r] ...]
+__global__ void amvm_cand_kernel(AmvmGeom a, const double* __restrict__ sc, double theta,
+                                 double csp_mn, int pass, int* __restrict__ cnt,
+                                 const int* __restrict__ ptr, int* __restrict__ lists) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.N) return;
+  const double tau = amvm_tau(sc, theta, csp_mn);
+  const int nrb = a.grid ? 3 : 1;
+  for (int rb = 0; rb < nrb; ++rb) {
+    const long long r = (long long)rb * a.N + a.rperm[p];
+    int n = 0;
+    int* dst = pass ? lists + ptr[r] : nullptr;
+    amvm_row_terms(a, rb, p, [&](int t, double v) {
+      if (a.grid && v == 0.0) return;
+      if (fabs(v) >= tau) {
+        if (pass) dst[n] = t;
+        ++n;
+      }
+    });
+    if (!pass) cnt[r] = n;
+  }
+}
+
+// sort keys: |difference| bit patterns (monotonic for x >= 0)
+__global__ void amvm_keys_kernel(const double* __restrict__ d, long long n,
+                                 unsigned long long* __restrict__ keys, int* __restrict__ idx) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (unsigned long long)__double_as_longlong(fabs(d[i]));
+  idx[i] = (int)i;
+}
+
+// The greedy walk (amvm.cpp:160-184), one warp: rows in order, their
+// candidate terms in order; each new term updates ||residual||^2 by
+// |term|^2 - 2 (residual . term) -- the dot product summed sequentially in
+// entry order like the reference's loop (products formed 32 at a time in
+// parallel, then added in order by shuffles) -- and the residual itself.
+__global__ void __launch_bounds__(32)
+amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restrict__ order,
+                 long long nrows, const int* __restrict__ ptr, const int* __restrict__ lists,
+                 const long long* __restrict__ eptr, const long long* __restrict__ eidx,
+                 const double* __restrict__ eval, const double* __restrict__ nsq,
+                 double* __restrict__ residual, unsigned char* __restrict__ in_set,
+                 int* __restrict__ marked, int* __restrict__ n_marked,
+                 double* __restrict__ out_pk) {
+  const int lane = threadIdx.x & 31;
+  const double target = (1.0 - theta) * sc[1];
+  const double target_sq = target * target;
+  double res_sq = sc[0];
+  int nm = 0;
+  bool done = res_sq <= target_sq;
+  // rows 32 at a time: their indices and candidate ranges in one load each
+  for (long long q0 = 0; q0 < nrows && !done; q0 += 32) {
+    int rc0 = 0, rc1 = 0;
+    if (q0 + lane < nrows) {
+      const int r = order[q0 + lane];
+      rc0 = ptr[r];
+      rc1 = ptr[r + 1];
+    }
+    const int nrow = (int)min(32LL, nrows - q0);
+    for (int j = 0; j < nrow && !done; ++j) {
+      const int c0 = __shfl_sync(0xffffffffu, rc0, j);
+      const int c1 = __shfl_sync(0xffffffffu, rc1, j);
+      for (int cb = c0; cb < c1 && !done; cb += 32) {
+        // this row's candidates (terms are unique within a row): which are new
+        int t_l = -1;
+        if (cb + lane < c1) {
+          t_l = lists[cb + lane];
+          if (in_set[t_l]) t_l = -1;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, t_l >= 0);
+        while (todo && !done) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int t = __shfl_sync(0xffffffffu, t_l, src);
+          __syncwarp();
+          if (lane == 0) {
+            in_set[t] = 1;
+            marked[nm] = t;
+          }
+          ++nm;
+          const long long e0 = eptr[t], e1 = eptr[t + 1];
+          double dot = 0.0;
+          for (long long b = e0; b < e1; b += 32) {
+            const long long e = b + lane;
+            double pr = 0.0;
+            if (e < e1) pr = residual[eidx[e]] * eval[e];
+            const int cnt = (int)min(32LL, e1 - b);
+            for (int k = 0; k < cnt; ++k) dot += __shfl_sync(0xffffffffu, pr, k);
+          }
+          res_sq += nsq[t] - 2.0 * dot;
+          __syncwarp();
+          for (long long e = e0 + lane; e < e1; e += 32) residual[eidx[e]] -= eval[e];
+          __syncwarp();
+          if (res_sq <= target_sq) done = true;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    *n_marked = nm;
+    double s = 0.0;
+    for (long long i = 0; i < nrows; ++i) s += residual[i] * residual[i];
+    *out_pk = sqrt(s);
+  }
+}
+
+// marked term -> work item
+__global__ void amvm_items_kernel(const TailTerm* __restrict__ terms,
+                                  const int* __restrict__ marked, const int* __restrict__ n,
+                                  int* __restrict__ ids) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < *n) ids[q] = terms[marked[q]].item;
+}
+
+}  // namespace hmgpu

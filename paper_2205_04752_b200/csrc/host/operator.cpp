@@ -1,5 +1,8 @@
 #include "operator.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -429,35 +432,51 @@ std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
   return marked;
 }
 
-// Algorithm 2 (amvm.cpp:199-268)
+// Algorithm 2 (amvm.cpp:199-268).  The estimator, the marking walk and the
+// refinement run on the device (hmgpu_amvm_*); the host only sees gamma,
+// gamma(P_k), the marked count and the difference vector (for e_hat).
 std::vector<double> amvm_multiply(HOperator& op, const double* x,
                                   const AmvmConfig& cfg, AmvmReport& report) {
   if (cfg.theta <= 0.0 || cfg.theta >= 1.0)
     throw Error("amvm_multiply: theta must lie in (0,1)");
   if (cfg.eps_amvm <= 0.0) throw Error("amvm_multiply: eps_amvm must be positive");
+  if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
+    throw ConfigError("amvm_multiply: sharded operators are not supported");
   using clk = std::chrono::steady_clock;
   report = AmvmReport{};
   report.c_sp = std::max(1, sparsity_constant(op.partition()));
   const long long M = op.rows();
-  std::vector<double> b(M), b_hat_prev;
+  std::vector<double> b(M), b_hat_prev, diff(M);
   op.matvec(x, b.data(), 1, Mode::Current);
+  static const bool verbose = std::getenv("HMGPU_VERBOSE") != nullptr;
+  auto lap = [&](const char* what, clk::time_point& t) {
+    if (!verbose) return;
+    const auto now = clk::now();
+    std::fprintf(stderr, "[amvm] %-10s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  };
   for (int k = 0;; ++k) {
     const auto t0 = clk::now();
-    GammaContributions g = gamma_contributions(op, x);
+    auto tl = t0;
+    double gamma = 0.0;
+    check_status(op.gpu(), hmgpu_amvm_estimate(op.gpu(), x, &gamma, diff.data()),
+                 "hmgpu_amvm_estimate");
+    lap("gamma", tl);
     if (!b_hat_prev.empty()) {
       double s = 0.0;
       for (long long i = 0; i < M; ++i) {
-        const double d = b[i] + g.difference[i] - b_hat_prev[i];
+        const double d = b[i] + diff[i] - b_hat_prev[i];
         s += d * d;
       }
       report.iterations.back().e_hat = std::sqrt(s);
     }
     AmvmIteration it;
     it.k = k;
-    it.gamma = g.gamma;
+    it.gamma = gamma;
     it.cumulative_pivots = op.total_pivots();
     it.storage_mb = op.storage_mb_current();
-    if (g.gamma <= cfg.eps_amvm) {
+    if (gamma <= cfg.eps_amvm) {
       it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
       report.iterations.push_back(it);
       report.termination = "tolerance";
@@ -471,18 +490,23 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
       report.converged = false;
       return b;
     }
-    Real gpk = 0.0;
-    const auto marked = mark_blocks(g, cfg.theta, report.c_sp, M, op.cols(), &gpk);
+    double gpk = 0.0;
+    int nm = 0;
+    if (gamma > 0.0)
+      check_status(op.gpu(),
+                   hmgpu_amvm_mark(op.gpu(), cfg.theta, report.c_sp, M, op.cols(), &gpk, &nm),
+                   "hmgpu_amvm_mark");
+    lap("mark", tl);
     it.gamma_pk = gpk;
-    it.marked = static_cast<int>(marked.size());
+    it.marked = nm;
     b_hat_prev.resize(M);
-    for (long long i = 0; i < M; ++i) b_hat_prev[i] = b[i] + g.difference[i];
-    std::vector<std::pair<int, int>> cb;
-    cb.reserve(marked.size());
-    for (int t : marked) cb.emplace_back(g.terms[t].comp, g.terms[t].block);
-    op.promote(cb);
-    op.extend_lookahead(cb, cfg.lookahead_steps);
+    for (long long i = 0; i < M; ++i) b_hat_prev[i] = b[i] + diff[i];
+    if (nm > 0)
+      check_status(op.gpu(), hmgpu_amvm_refine(op.gpu(), cfg.lookahead_steps, nullptr),
+                   "hmgpu_amvm_refine");
+    lap("refine", tl);
     op.matvec(x, b.data(), 1, Mode::Current);
+    lap("matvec", tl);
     it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
     report.iterations.push_back(it);
   }
