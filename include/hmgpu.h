@@ -177,6 +177,10 @@ int hmgpu_extend(hmgpu_ctx* ctx, int n, const int* comp_block, int steps);
                          (comp, block) pairs (optional host copy of the pairs)
    Whole (unsharded) operators only. */
 int hmgpu_amvm_estimate(hmgpu_ctx* ctx, const double* x, double* gamma, double* difference);
+/* direct != 0: 1-RHS matvecs sweep the blocks in place instead of building the
+   packed stream plan (for one matvec per rank change, as in the adaptive loop;
+   the plan pays off from the second matvec on the same ranks) */
+int hmgpu_set_matvec_policy(hmgpu_ctx* ctx, int direct);
 int hmgpu_amvm_mark(hmgpu_ctx* ctx, double theta, int c_sp, long long m_rows,
                     long long n_cols, double* gamma_pk, int* n_marked);
 int hmgpu_amvm_refine(hmgpu_ctx* ctx, int steps, int* comp_block);

@@ -98,5 +98,5 @@ HMGPU_SYMBOLS = [
     "hmgpu_promote", "hmgpu_extend", "hmgpu_tail_terms", "hmgpu_download_factor",
     "hmgpu_download_dense", "hmgpu_storage", "hmgpu_set_profiling",
     "hmgpu_kernel_times", "hmgpu_fp64_peak", "hmgpu_dmma_peak", "hmgpu_amvm_estimate",
-    "hmgpu_amvm_mark", "hmgpu_amvm_refine",
+    "hmgpu_amvm_mark", "hmgpu_amvm_refine", "hmgpu_set_matvec_policy",
 ]

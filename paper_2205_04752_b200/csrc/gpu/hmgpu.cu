@@ -269,6 +269,7 @@ struct hmgpu_ctx {
 
   // ---- device-resident AMVM estimator (hmgpu_amvm.cuh) ----
   bool am_geom_valid = false;
+  bool mv_direct = false;  // hmgpu_set_matvec_policy: 1-RHS matvecs without a stream plan
   DBuf<int> d_row_leaf, d_sortp, d_tix, d_term_bi, d_cnt, d_ptr, d_lists, d_order, d_idx,
       d_marked, d_nm, d_mids;
   DBuf<long long> d_spoff, d_eptr, d_eidx, d_ecnt;
@@ -1700,10 +1701,15 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
         return;
       }
     }
-    bool streamed = !force_v1;
+    bool streamed = !force_v1 && !(c->mv_direct && nrhs == 1);
     if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
       try {
+        const auto tp = std::chrono::steady_clock::now();
         build_plan(c, mode, nrhs);
+        if (verbose())
+          std::fprintf(stderr, "[hmgpu] build_plan %9.2f ms\n",
+                       std::chrono::duration<double, std::milli>(
+                           std::chrono::steady_clock::now() - tp).count());
       } catch (const Fail& f) {
         if (f.code != HMGPU_ERR_INVALID) throw;
         streamed = false;  // ranks / widths beyond the stream layout: block sweep
@@ -1864,6 +1870,10 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
   });
 }
 
+int hmgpu_set_matvec_policy(hmgpu_ctx* c, int direct) {
+  return guard(c, [&] { c->mv_direct = direct != 0; });
+}
+
 int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* difference) {
   return guard(c, [&] {
     if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
@@ -1950,6 +1960,15 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
     c->marked_ids.clear();
     const AmvmGeom a = amvm_geom(c);
     const double csp_mn = (double)c_sp * (double)m_rows * (double)n_cols;
+    auto wall0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+      if (!verbose()) return;
+      c->sync();
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[hmgpu] mark %-10s %9.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - wall0).count());
+      wall0 = now;
+    };
     c->d_nsq.ensure((size_t)std::max(nt, 1));
     c->d_cnt.ensure((size_t)M + 1);
     c->d_ptr.ensure((size_t)M + 1);
@@ -1981,6 +2000,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
       amvm_entries_kernel<<<(nt + 127) / 128, 128, 0, c->stream>>>(
           a, c->d_items.p, nt, 1, nullptr, c->d_eptr.p, c->d_eidx.p, c->d_eval.p, c->d_nsq.p);
     }
+    phase("entries");
     const int gr = (c->n_rows + 127) / 128;
     CK(cudaMemsetAsync(c->d_cnt.p, 0, (M + 1) * sizeof(int), c->stream));
     amvm_cand_kernel<<<gr, 128, 0, c->stream>>>(a, c->d_sc.p, theta, csp_mn, 0, c->d_cnt.p,
@@ -2001,6 +2021,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
     CK(cub::DeviceRadixSort::SortPairsDescending(c->d_cub.p, tb2, c->d_keys.p, c->d_keys2.p,
                                                  c->d_idx.p, c->d_order.p, (int)M, 0, 64,
                                                  c->stream));
+    phase("cand+sort");
     CK(cudaMemcpyAsync(c->d_resid.p, c->d_diff.p, M * sizeof(double),
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_inset.p, 0, (size_t)std::max(nt, 1), c->stream));
@@ -2011,6 +2032,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
                                                 c->d_inset.p, c->d_marked.p, c->d_nm.p,
                                                 c->d_sc.p + 2);
     });
+    phase("walk");
     if (nt > 0)
       amvm_items_kernel<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_aterms.p, c->d_marked.p,
                                                                  c->d_nm.p, c->d_mids.p);

@@ -234,19 +234,53 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
             marked[nm] = t;
           }
           ++nm;
-          const long long e0 = eptr[t], e1 = eptr[t + 1];
+          const long long e0 = eptr[t];
+          const int n = (int)(eptr[t + 1] - e0);
           double dot = 0.0;
-          for (long long b = e0; b < e1; b += 32) {
-            const long long e = b + lane;
-            double pr = 0.0;
-            if (e < e1) pr = residual[eidx[e]] * eval[e];
-            const int cnt = (int)min(32LL, e1 - b);
-            for (int k = 0; k < cnt; ++k) dot += __shfl_sync(0xffffffffu, pr, k);
+          if (n <= 64) {
+            // the term in registers: two entries per lane, read once
+            const bool a0 = lane < n, a1 = lane + 32 < n;
+            const long long i0 = a0 ? eidx[e0 + lane] : 0;
+            const long long i1 = a1 ? eidx[e0 + lane + 32] : 0;
+            const double v0 = a0 ? eval[e0 + lane] : 0.0;
+            const double v1 = a1 ? eval[e0 + lane + 32] : 0.0;
+            const double r0 = a0 ? residual[i0] : 0.0;
+            const double r1 = a1 ? residual[i1] : 0.0;
+            const double p0 = r0 * v0, p1 = r1 * v1;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const double s = __shfl_sync(0xffffffffu, p0, k);
+              if (k < n) dot += s;
+            }
+            if (n > 32) {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const double s = __shfl_sync(0xffffffffu, p1, k);
+                if (32 + k < n) dot += s;
+              }
+            }
+            res_sq += nsq[t] - 2.0 * dot;
+            if (a0) residual[i0] = r0 - v0;
+            if (a1) residual[i1] = r1 - v1;
+            __syncwarp();
+          } else {
+            const long long e1 = e0 + n;
+            for (long long b = e0; b < e1; b += 32) {
+              const long long e = b + lane;
+              double pr = 0.0;
+              if (e < e1) pr = residual[eidx[e]] * eval[e];
+              const int cnt = (int)min(32LL, e1 - b);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const double s = __shfl_sync(0xffffffffu, pr, k);
+                if (k < cnt) dot += s;
+              }
+            }
+            res_sq += nsq[t] - 2.0 * dot;
+            __syncwarp();
+            for (long long e = e0 + lane; e < e1; e += 32) residual[eidx[e]] -= eval[e];
+            __syncwarp();
           }
-          res_sq += nsq[t] - 2.0 * dot;
-          __syncwarp();
-          for (long long e = e0 + lane; e < e1; e += 32) residual[eidx[e]] -= eval[e];
-          __syncwarp();
           if (res_sq <= target_sq) done = true;
         }
       }

@@ -447,6 +447,13 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
   report.c_sp = std::max(1, sparsity_constant(op.partition()));
   const long long M = op.rows();
   std::vector<double> b(M), b_hat_prev, diff(M);
+  // one matvec per rank change: sweep the blocks in place instead of
+  // re-packing the stream plan each sweep (hmgpu_set_matvec_policy)
+  struct DirectMatvec {
+    hmgpu_ctx* c;
+    explicit DirectMatvec(hmgpu_ctx* cc) : c(cc) { hmgpu_set_matvec_policy(c, 1); }
+    ~DirectMatvec() { hmgpu_set_matvec_policy(c, 0); }
+  } direct(op.gpu());
   op.matvec(x, b.data(), 1, Mode::Current);
   static const bool verbose = std::getenv("HMGPU_VERBOSE") != nullptr;
   auto lap = [&](const char* what, clk::time_point& t) {
