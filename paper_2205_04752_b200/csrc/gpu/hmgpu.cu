@@ -1906,7 +1906,7 @@ int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* di
     c->am_nvals = off;
     const long long M = (long long)c->ndof_rows();
     c->d_diff.ensure((size_t)M);
-    c->d_sc.ensure(4);
+    c->d_sc.ensure(8);
     if (terms.empty()) {
       c->d_aterms.ensure(1);
       c->d_term_bi.ensure(1);
@@ -2026,13 +2026,21 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_inset.p, 0, (size_t)std::max(nt, 1), c->stream));
     c->timed("amvm_walk", [&] {
-      amvm_walk_kernel<<<1, 32, 0, c->stream>>>(c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p,
+      const int wsmem = 3 * kWalkSmem * (int)sizeof(double);
+      CK(cudaFuncSetAttribute(amvm_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              wsmem));
+      amvm_walk_kernel<<<1, 32, wsmem, c->stream>>>(c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p,
                                                 c->d_lists.p, c->d_eptr.p, c->d_eidx.p,
                                                 c->d_eval.p, c->d_nsq.p, c->d_resid.p,
                                                 c->d_inset.p, c->d_marked.p, c->d_nm.p,
                                                 c->d_sc.p + 2);
     });
     phase("walk");
+    if (verbose()) {
+      double st[2];
+      CK(cudaMemcpy(st, c->d_sc.p + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[hmgpu] walk rows %.0f candidates %.0f\n", st[0], st[1]);
+    }
     if (nt > 0)
       amvm_items_kernel<<<(nt + 255) / 256, 256, 0, c->stream>>>(c->d_aterms.p, c->d_marked.p,
                                                                  c->d_nm.p, c->d_mids.p);

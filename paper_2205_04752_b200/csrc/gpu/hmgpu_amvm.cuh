@@ -91,12 +91,26 @@ __global__ void amvm_diff_kernel(AmvmGeom a, double* __restrict__ diff) {
   }
 }
 
-// one thread: s = sum_i d_i^2 in index order; out[0] = s, out[1] = sqrt(s)
+// s = sum_i d_i^2 in index order (one thread adds; loads 16 ahead)
+__device__ __forceinline__ double seq_sumsq(const double* __restrict__ d, long long n) {
+  double s = 0.0;
+  long long i = 0;
+  for (; i + 16 <= n; i += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = d[i + u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += v[u] * v[u];
+  }
+  for (; i < n; ++i) s += d[i] * d[i];
+  return s;
+}
+
+// one thread: out[0] = sum_i d_i^2 (index order), out[1] = sqrt
 __global__ void amvm_sumsq_kernel(const double* __restrict__ d, long long n,
                                   double* __restrict__ out) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  double s = 0.0;
-  for (long long i = 0; i < n; ++i) s += d[i] * d[i];
+  const double s = seq_sumsq(d, n);
   out[0] = s;
   out[1] = sqrt(s);
 }
@@ -190,6 +204,98 @@ __global__ void amvm_keys_kernel(const double* __restrict__ d, long long n,
 // |term|^2 - 2 (residual . term) -- the dot product summed sequentially in
 // entry order like the reference's loop (products formed 32 at a time in
 // parallel, then added in order by shuffles) -- and the residual itself.
+// Software-pipelined: the next new term is found and its entries loaded
+// while the current one is applied (only its residual gather must wait).
+
+// the walk's term sequence: rows 32 at a time, each row's candidates 32 at
+// a time, terms already in the set skipped (warp-uniform control flow)
+struct WalkGen {
+  const int* order;
+  long long nrows;
+  const int* ptr;
+  const int* lists;
+  const unsigned char* in_set;
+  int lane;
+  long long q0, rows_seen, cands;
+  int rc0, rc1, nrow, j, c1, cb, t_l;
+  unsigned todo;
+
+  __device__ __forceinline__ void init() {
+    q0 = -32;
+    rows_seen = cands = 0;
+    rc0 = rc1 = nrow = 0;
+    j = -1;
+    c1 = cb = 0;
+    t_l = -1;
+    todo = 0u;
+  }
+  __device__ __forceinline__ int next() {
+    for (;;) {
+      if (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        return __shfl_sync(0xffffffffu, t_l, src);
+      }
+      if (cb < c1) {  // next candidate chunk of the current row
+        t_l = -1;
+        if (cb + lane < c1) {
+          t_l = lists[cb + lane];
+          if (in_set[t_l]) t_l = -1;
+        }
+        todo = __ballot_sync(0xffffffffu, t_l >= 0);
+        cb += 32;
+        continue;
+      }
+      if (++j >= nrow) {  // next chunk of rows
+        q0 += 32;
+        if (q0 >= nrows) return -1;
+        rc0 = rc1 = 0;
+        if (q0 + lane < nrows) {
+          const int r = order[q0 + lane];
+          rc0 = ptr[r];
+          rc1 = ptr[r + 1];
+        }
+        nrow = (int)min(32LL, nrows - q0);
+        j = 0;
+      }
+      cb = __shfl_sync(0xffffffffu, rc0, j);
+      c1 = __shfl_sync(0xffffffffu, rc1, j);
+      ++rows_seen;
+      cands += c1 - cb;
+    }
+  }
+};
+
+// a term's entries, held in registers when it has at most 64
+struct WalkTerm {
+  long long e0, i0, i1;
+  int n;
+  double nsq, v0, v1;
+};
+
+__device__ __forceinline__ WalkTerm walk_load(int t, int lane, const long long* eptr,
+                                              const long long* eidx, const double* eval,
+                                              const double* nsq) {
+  WalkTerm w{};
+  if (t < 0) return w;
+  w.e0 = eptr[t];
+  w.n = (int)(eptr[t + 1] - w.e0);
+  w.nsq = nsq[t];
+  if (w.n <= 64) {
+    if (lane < w.n) {
+      w.i0 = eidx[w.e0 + lane];
+      w.v0 = eval[w.e0 + lane];
+    }
+    if (lane + 32 < w.n) {
+      w.i1 = eidx[w.e0 + lane + 32];
+      w.v1 = eval[w.e0 + lane + 32];
+    }
+  }
+  return w;
+}
+
+constexpr int kWalkSmem = 4096;  // entries of a term staged in shared memory
+
 __global__ void __launch_bounds__(32)
 amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restrict__ order,
                  long long nrows, const int* __restrict__ ptr, const int* __restrict__ lists,
@@ -198,100 +304,101 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
                  double* __restrict__ residual, unsigned char* __restrict__ in_set,
                  int* __restrict__ marked, int* __restrict__ n_marked,
                  double* __restrict__ out_pk) {
+  extern __shared__ double wsm[];  // [3][kWalkSmem]: indices, values, residuals
   const int lane = threadIdx.x & 31;
   const double target = (1.0 - theta) * sc[1];
   const double target_sq = target * target;
   double res_sq = sc[0];
   int nm = 0;
-  bool done = res_sq <= target_sq;
-  // rows 32 at a time: their indices and candidate ranges in one load each
-  for (long long q0 = 0; q0 < nrows && !done; q0 += 32) {
-    int rc0 = 0, rc1 = 0;
-    if (q0 + lane < nrows) {
-      const int r = order[q0 + lane];
-      rc0 = ptr[r];
-      rc1 = ptr[r + 1];
+  WalkGen G{order, nrows, ptr, lists, in_set, lane};
+  G.init();
+  int t = res_sq <= target_sq ? -1 : G.next();
+  WalkTerm w = walk_load(t, lane, eptr, eidx, eval, nsq);
+  while (t >= 0) {
+    __syncwarp();
+    if (lane == 0) {
+      in_set[t] = 1;
+      marked[nm] = t;
     }
-    const int nrow = (int)min(32LL, nrows - q0);
-    for (int j = 0; j < nrow && !done; ++j) {
-      const int c0 = __shfl_sync(0xffffffffu, rc0, j);
-      const int c1 = __shfl_sync(0xffffffffu, rc1, j);
-      for (int cb = c0; cb < c1 && !done; cb += 32) {
-        // this row's candidates (terms are unique within a row): which are new
-        int t_l = -1;
-        if (cb + lane < c1) {
-          t_l = lists[cb + lane];
-          if (in_set[t_l]) t_l = -1;
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, t_l >= 0);
-        while (todo && !done) {
-          const int src = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int t = __shfl_sync(0xffffffffu, t_l, src);
-          __syncwarp();
-          if (lane == 0) {
-            in_set[t] = 1;
-            marked[nm] = t;
-          }
-          ++nm;
-          const long long e0 = eptr[t];
-          const int n = (int)(eptr[t + 1] - e0);
-          double dot = 0.0;
-          if (n <= 64) {
-            // the term in registers: two entries per lane, read once
-            const bool a0 = lane < n, a1 = lane + 32 < n;
-            const long long i0 = a0 ? eidx[e0 + lane] : 0;
-            const long long i1 = a1 ? eidx[e0 + lane + 32] : 0;
-            const double v0 = a0 ? eval[e0 + lane] : 0.0;
-            const double v1 = a1 ? eval[e0 + lane + 32] : 0.0;
-            const double r0 = a0 ? residual[i0] : 0.0;
-            const double r1 = a1 ? residual[i1] : 0.0;
-            const double p0 = r0 * v0, p1 = r1 * v1;
+    ++nm;
+    __syncwarp();
+    const int tn = G.next();  // look ahead (t is in the set already)
+    const WalkTerm wn = walk_load(tn, lane, eptr, eidx, eval, nsq);
+    double dot = 0.0;
+    if (w.n <= 64) {
+      const bool a0 = lane < w.n, a1 = lane + 32 < w.n;
+      const double r0 = a0 ? residual[w.i0] : 0.0;
+      const double r1 = a1 ? residual[w.i1] : 0.0;
+      const double p0 = r0 * w.v0, p1 = r1 * w.v1;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const double s = __shfl_sync(0xffffffffu, p0, k);
-              if (k < n) dot += s;
-            }
-            if (n > 32) {
+      for (int k = 0; k < 32; ++k) {
+        const double s = __shfl_sync(0xffffffffu, p0, k);
+        if (k < w.n) dot += s;
+      }
+      if (w.n > 32) {
 #pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                const double s = __shfl_sync(0xffffffffu, p1, k);
-                if (32 + k < n) dot += s;
-              }
-            }
-            res_sq += nsq[t] - 2.0 * dot;
-            if (a0) residual[i0] = r0 - v0;
-            if (a1) residual[i1] = r1 - v1;
-            __syncwarp();
-          } else {
-            const long long e1 = e0 + n;
-            for (long long b = e0; b < e1; b += 32) {
-              const long long e = b + lane;
-              double pr = 0.0;
-              if (e < e1) pr = residual[eidx[e]] * eval[e];
-              const int cnt = (int)min(32LL, e1 - b);
-#pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                const double s = __shfl_sync(0xffffffffu, pr, k);
-                if (k < cnt) dot += s;
-              }
-            }
-            res_sq += nsq[t] - 2.0 * dot;
-            __syncwarp();
-            for (long long e = e0 + lane; e < e1; e += 32) residual[eidx[e]] -= eval[e];
-            __syncwarp();
-          }
-          if (res_sq <= target_sq) done = true;
+        for (int k = 0; k < 32; ++k) {
+          const double s = __shfl_sync(0xffffffffu, p1, k);
+          if (32 + k < w.n) dot += s;
         }
       }
+      res_sq += w.nsq - 2.0 * dot;
+      if (a0) residual[w.i0] = r0 - w.v0;
+      if (a1) residual[w.i1] = r1 - w.v1;
+    } else if (w.n <= kWalkSmem) {
+      // staged in shared memory: every load of the term in flight at once
+      long long* si = reinterpret_cast<long long*>(wsm);
+      double* sv = wsm + kWalkSmem;
+      double* sr = wsm + 2 * kWalkSmem;
+#pragma unroll 4
+      for (int e = lane; e < w.n; e += 32) {
+        si[e] = eidx[w.e0 + e];
+        sv[e] = eval[w.e0 + e];
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int e = lane; e < w.n; e += 32) sr[e] = residual[si[e]];
+      __syncwarp();
+      for (int b = 0; b < w.n; b += 32) {
+        const double pr = b + lane < w.n ? sr[b + lane] * sv[b + lane] : 0.0;
+        const int cnt = min(32, w.n - b);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double s = __shfl_sync(0xffffffffu, pr, k);
+          if (k < cnt) dot += s;
+        }
+      }
+      res_sq += w.nsq - 2.0 * dot;
+#pragma unroll 4
+      for (int e = lane; e < w.n; e += 32) residual[si[e]] = sr[e] - sv[e];
+    } else {
+      const long long e1 = w.e0 + w.n;
+      for (long long b = w.e0; b < e1; b += 32) {
+        const long long e = b + lane;
+        double pr = 0.0;
+        if (e < e1) pr = residual[eidx[e]] * eval[e];
+        const int cnt = (int)min(32LL, e1 - b);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double s = __shfl_sync(0xffffffffu, pr, k);
+          if (k < cnt) dot += s;
+        }
+      }
+      res_sq += w.nsq - 2.0 * dot;
+      __syncwarp();
+      for (long long e = w.e0 + lane; e < e1; e += 32) residual[eidx[e]] -= eval[e];
     }
+    __syncwarp();
+    if (res_sq <= target_sq) break;
+    t = tn;
+    w = wn;
   }
   __syncwarp();
   if (lane == 0) {
     *n_marked = nm;
-    double s = 0.0;
-    for (long long i = 0; i < nrows; ++i) s += residual[i] * residual[i];
-    *out_pk = sqrt(s);
+    out_pk[0] = sqrt(seq_sumsq(residual, nrows));
+    out_pk[1] = (double)G.rows_seen;  // walk statistics (verbose runs)
+    out_pk[2] = (double)G.cands;
   }
 }
 
