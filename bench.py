@@ -438,6 +438,22 @@ def run_ours(args, cfg):
                      (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None},
         "kernel_ms": {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kt.items()},
     }
+    if args.config == "c4" and world == 1:
+        # the adaptive matvec of config 4 (Algorithm 2): full-mode assembly at
+        # eps 1e-2, theta 0.7, eps_amvm 1e-6, look-ahead 2, 5 sweeps; the
+        # estimator, marking walk and refinement run on the device
+        st4 = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep = h.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, lookahead_steps=2,
+                                 max_iterations=5)
+        amvm_s = time.perf_counter() - t0
+        line["amvm"] = {"seconds": amvm_s, "sweeps": len(rep.iterations),
+                        "termination": rep.termination,
+                        "gamma": [float(i.gamma) for i in rep.iterations],
+                        "marked": [int(i.marked) for i in rep.iterations],
+                        "ms_per_sweep": [float(i.ms) for i in rep.iterations],
+                        "assembly_ms": st4.ms_total}
     if res is not None:
         line["cpu_baseline"] = res["cpu_baseline"]
         line["assembly"]["cpu_entries_per_s"] = res["assembly"]["value"]
