@@ -778,11 +778,13 @@ void refresh_matvec_ranks(hmgpu_ctx* c) {
 
 
 // ---- streamed matvec plan (warp-private jobs, hmgpu_stream.cuh) -------------
-// Default geometry of the warp pipelines (tuned on B200: 7 warps per SM,
-// two 12 KB stages each; larger stages beat deeper rings).  HMGPU_MV_CFG=
+// Default geometry of the warp pipelines (tuned on B200 with
+// scripts/mv_sweep.sh: 12 warps per SM, two 7 KB stages each, 4.7 KB of job
+// scratch -- more warps hide the FMA/shared-memory latency of the FUSED jobs;
+// deeper rings and scratch below ~4.5 KB lost).  HMGPU_MV_CFG=
 // "warps,stages,stage_doubles,scratch_doubles" overrides it for tuning.
 struct MvCfg {
-  int warps = 7, ns = 2, stage = 1536, scratch = 1024;
+  int warps = 12, ns = 2, stage = 896, scratch = 600;
 };
 MvCfg mv_cfg() {
   static MvCfg cfg = [] {
@@ -1198,8 +1200,8 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     return;                                                   \
   }
     c->timed(name, [&] {
-      HMV_CASE(7, 2) HMV_CASE(6, 2) HMV_CASE(8, 2) HMV_CASE(5, 3) HMV_CASE(4, 3)
-      HMV_CASE(6, 3) HMV_CASE(5, 2) HMV_CASE(4, 4)
+      HMV_CASE(12, 2) HMV_CASE(8, 2) HMV_CASE(10, 2) HMV_CASE(14, 2) HMV_CASE(16, 2)
+      HMV_CASE(7, 2)
       fail(HMGPU_ERR_INVALID, "HMGPU_MV_CFG: unsupported (warps, stages)");
     });
 #undef HMV_CASE

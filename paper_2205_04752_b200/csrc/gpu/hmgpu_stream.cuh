@@ -279,43 +279,72 @@ __device__ __forceinline__ void urows(const double* U, int m, int ncol, const do
   }
 }
 
-// dense chunk columns [0, ncol): D[j][c][i] (column stride cp), x rows xs
+// dense chunk columns [0, ncol): D[j][c][i] (column stride cp), x rows xs.
+// Two accumulator sets (even / odd columns) so that the three-deep FMA
+// chains of consecutive columns overlap.
 template <int NC>
 __device__ __forceinline__ void drows(const double* D, int m, int cp, int ncol,
                                       const double* xs, int lane, double* y) {
   const bool r0 = lane < m, r1 = lane + 32 < m;
-  double a0 = 0, a1 = 0, a2 = 0, c0 = 0, c1 = 0, c2 = 0;
-  for (int j = 0; j < ncol; ++j) {
+  double a[2][3] = {{0, 0, 0}, {0, 0, 0}}, c[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  int j = 0;
+  for (; j + 1 < ncol; j += 2) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double* d = D + (j + h) * cp;
+      const double2 x01 = *reinterpret_cast<const double2*>(xs + 4 * (j + h));
+      const double x2 = xs[4 * (j + h) + 2];
+      if (NC == 6) {
+        const double p00 = r0 ? d[lane] : 0.0, p01 = r0 ? d[m + lane] : 0.0,
+                     p02 = r0 ? d[2 * m + lane] : 0.0, p11 = r0 ? d[3 * m + lane] : 0.0,
+                     p12 = r0 ? d[4 * m + lane] : 0.0, p22 = r0 ? d[5 * m + lane] : 0.0;
+        a[h][0] = fma(p00, x01.x, fma(p01, x01.y, fma(p02, x2, a[h][0])));
+        a[h][1] = fma(p01, x01.x, fma(p11, x01.y, fma(p12, x2, a[h][1])));
+        a[h][2] = fma(p02, x01.x, fma(p12, x01.y, fma(p22, x2, a[h][2])));
+        if (r1) {
+          const int i = lane + 32;
+          const double q00 = d[i], q01 = d[m + i], q02 = d[2 * m + i], q11 = d[3 * m + i],
+                       q12 = d[4 * m + i], q22 = d[5 * m + i];
+          c[h][0] = fma(q00, x01.x, fma(q01, x01.y, fma(q02, x2, c[h][0])));
+          c[h][1] = fma(q01, x01.x, fma(q11, x01.y, fma(q12, x2, c[h][1])));
+          c[h][2] = fma(q02, x01.x, fma(q12, x01.y, fma(q22, x2, c[h][2])));
+        }
+      } else {
+        a[h][0] = fma(r0 ? d[lane] : 0.0, x01.x, a[h][0]);
+        c[h][0] = fma(r1 ? d[lane + 32] : 0.0, x01.x, c[h][0]);
+      }
+    }
+  }
+  if (j < ncol) {
     const double* d = D + j * cp;
     const double2 x01 = *reinterpret_cast<const double2*>(xs + 4 * j);
     const double x2 = xs[4 * j + 2];
     if (NC == 6) {
-      // y_r += sum_s A_(r,s) x_s with A_(r,s) = component (min(r,s), max(r,s))
       const double p00 = r0 ? d[lane] : 0.0, p01 = r0 ? d[m + lane] : 0.0,
                    p02 = r0 ? d[2 * m + lane] : 0.0, p11 = r0 ? d[3 * m + lane] : 0.0,
                    p12 = r0 ? d[4 * m + lane] : 0.0, p22 = r0 ? d[5 * m + lane] : 0.0;
-      a0 = fma(p00, x01.x, fma(p01, x01.y, fma(p02, x2, a0)));
-      a1 = fma(p01, x01.x, fma(p11, x01.y, fma(p12, x2, a1)));
-      a2 = fma(p02, x01.x, fma(p12, x01.y, fma(p22, x2, a2)));
+      a[0][0] = fma(p00, x01.x, fma(p01, x01.y, fma(p02, x2, a[0][0])));
+      a[0][1] = fma(p01, x01.x, fma(p11, x01.y, fma(p12, x2, a[0][1])));
+      a[0][2] = fma(p02, x01.x, fma(p12, x01.y, fma(p22, x2, a[0][2])));
       if (r1) {
         const int i = lane + 32;
         const double q00 = d[i], q01 = d[m + i], q02 = d[2 * m + i], q11 = d[3 * m + i],
                      q12 = d[4 * m + i], q22 = d[5 * m + i];
-        c0 = fma(q00, x01.x, fma(q01, x01.y, fma(q02, x2, c0)));
-        c1 = fma(q01, x01.x, fma(q11, x01.y, fma(q12, x2, c1)));
-        c2 = fma(q02, x01.x, fma(q12, x01.y, fma(q22, x2, c2)));
+        c[0][0] = fma(q00, x01.x, fma(q01, x01.y, fma(q02, x2, c[0][0])));
+        c[0][1] = fma(q01, x01.x, fma(q11, x01.y, fma(q12, x2, c[0][1])));
+        c[0][2] = fma(q02, x01.x, fma(q12, x01.y, fma(q22, x2, c[0][2])));
       }
     } else {
-      a0 = fma(r0 ? d[lane] : 0.0, x01.x, a0);
-      c0 = fma(r1 ? d[lane + 32] : 0.0, x01.x, c0);
+      a[0][0] = fma(r0 ? d[lane] : 0.0, x01.x, a[0][0]);
+      c[0][0] = fma(r1 ? d[lane + 32] : 0.0, x01.x, c[0][0]);
     }
   }
-  y[0] += a0;
-  y[1] += a1;
-  y[2] += a2;
-  y[3] += c0;
-  y[4] += c1;
-  y[5] += c2;
+  y[0] += a[0][0] + a[1][0];
+  y[1] += a[0][1] + a[1][1];
+  y[2] += a[0][2] + a[1][2];
+  y[3] += c[0][0] + c[1][0];
+  y[4] += c[0][1] + c[1][1];
+  y[5] += c[0][2] + c[1][2];
 }
 
 // Warp-private pipelines: WARPS warps per CTA, each with NS stages of
