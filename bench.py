@@ -251,7 +251,9 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    # torchrun (RANK set) or N > 1: the NCCL protocol runs even for one rank
+    # (HMB_BENCH_NO_DIST=1 disables it for a single process)
+    if world > 1 or ("RANK" in os.environ and not os.environ.get("HMB_BENCH_NO_DIST")):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
