@@ -89,6 +89,7 @@ _sig(gpu, "hmgpu_kernel_times", I, P, C.c_char_p, DP, LLP, I)
 _sig(gpu, "hmgpu_storage", I, P, P)
 _sig(gpu, "hmgpu_fp64_peak", I, I, DP)
 _sig(gpu, "hmgpu_dmma_peak", I, I, DP)
+_sig(gpu, "hmgpu_set_matvec_policy", I, P, I)
 
 HMGPU_SYMBOLS = [
     "hmgpu_device_count", "hmgpu_create", "hmgpu_destroy", "hmgpu_last_error",

@@ -301,6 +301,13 @@ class HMatrix:
     def gpu_ctx(self):
         return _h.hmb_op_gpu(self._h)
 
+    def set_matvec_policy(self, direct: bool) -> None:
+        """direct=True: 1-RHS matvecs sweep the blocks in place (no stream
+        plan; for one matvec per rank change), False: the packed stream plan."""
+        st = _lib.gpu.hmgpu_set_matvec_policy(self.gpu_ctx, 1 if direct else 0)
+        if st:
+            raise DeviceError("hmgpu_set_matvec_policy failed", st)
+
     # ---- tree / partition ----
     def tree(self, which: int = 0) -> ClusterTree:
         nn, dep, sz = C.c_int(), C.c_int(), C.c_int()

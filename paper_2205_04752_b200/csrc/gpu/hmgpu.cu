@@ -292,7 +292,8 @@ struct hmgpu_ctx {
   DBuf<Z16Sum> d_zs16;
   DBuf<long long> d_zb16;
   DBuf<int> d_rk16;
-  DBuf<int2> d_tiles16;
+  DBuf<int2> d_tiles16, d_zp2, d_zp4;
+  int n_zp2 = 0, n_zp4 = 0;
   DBuf<double> d_zpart16, d_xi16;
   DBuf<int> d_pleaf_ptr;
   std::vector<int> p_leaf_ptr;
@@ -324,7 +325,7 @@ struct hmgpu_ctx {
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
     d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
-    d_rk16.free(); d_tiles16.free();
+    d_rk16.free(); d_tiles16.free(); d_zp2.free(); d_zp4.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
     d_ptr.free(); d_lists.free(); d_order.free(); d_idx.free(); d_marked.free(); d_nm.free();
     d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
@@ -1105,6 +1106,16 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       zt.push_back({bi, z * JC, std::min(JC, mb.n - z * JC), z, zb[bi]});
     if (nz > 1) zsum.push_back({zb[bi], K * 32, nz});
   }
+  // phase-1 work: (task, component) pairs, rank <= 16 and > 16 separately
+  std::vector<int2> p2, p4;
+  for (size_t ti = 0; ti < zt.size(); ++ti) {
+    const int bi = zt[ti].blk;
+    for (int q = 0; q < 6; ++q) {
+      const int k = rk[8 * bi + q];
+      if (k == 0) continue;
+      (k <= 16 ? p2 : p4).push_back(make_int2((int)ti, q));
+    }
+  }
   std::vector<int2> tiles;
   for (size_t l = 0; l < c->leaf_begin.size(); ++l) {
     const int rows = c->leaf_end[l] - c->leaf_begin[l];
@@ -1115,6 +1126,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->d_zb16.upload(zb, c->stream);
   c->d_rk16.upload(rk, c->stream);
   c->d_tiles16.upload(tiles, c->stream);
+  if (!p2.empty()) c->d_zp2.upload(p2, c->stream);
+  if (!p4.empty()) c->d_zp4.upload(p4, c->stream);
+  c->n_zp2 = (int)p2.size();
+  c->n_zp4 = (int)p4.size();
   c->d_zpart16.ensure((size_t)std::max<long long>(zsize, 1));
   c->d_xi16.ensure((size_t)c->n_cols * 48);
   c->n_z16 = (int)zt.size();
@@ -1137,9 +1152,14 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
     });
     if (c->n_z16 > 0)
       c->timed("hmv16_z", [&] {
-        hmv16_z_kernel<<<grid_for(c, c->n_z16, 8), 192, 0, c->stream>>>(
-            c->d_z16.p, c->n_z16, c->d_mvb.p, c->d_items.p, c->d_rk16.p, c->d_arena.p,
-            c->d_xi16.p, c->d_zpart16.p);
+        if (c->n_zp2 > 0)
+          hmv16_z_kernel<2><<<grid_for(c, (c->n_zp2 + 7) / 8, 8), 256, 0, c->stream>>>(
+              c->d_zp2.p, c->n_zp2, c->d_z16.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p,
+              c->d_arena.p, c->d_xi16.p, c->d_zpart16.p);
+        if (c->n_zp4 > 0)
+          hmv16_z_kernel<4><<<grid_for(c, (c->n_zp4 + 7) / 8, 8), 256, 0, c->stream>>>(
+              c->d_zp4.p, c->n_zp4, c->d_z16.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p,
+              c->d_arena.p, c->d_xi16.p, c->d_zpart16.p);
       });
     if (c->n_zs16 > 0)
       c->timed("hmv16_zsum", [&] {

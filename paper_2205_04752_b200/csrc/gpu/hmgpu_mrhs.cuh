@@ -69,22 +69,28 @@ __global__ void gather16_kernel(const double* __restrict__ x, double* __restrict
 // Rank table of the plan: rk[8 * bi + c] = rank of component c of matvec
 // block bi in the plan's mode, rk[8 * bi + 6] = their sum.
 
-// phase 1: warp (task, component); no shared memory, no block barriers.  The
-// six warps of a CTA take the six components of one task, so the chunk's x
-// rows are shared through L1.
-__global__ void __launch_bounds__(192)
-hmv16_z_kernel(const Z16Task* __restrict__ tasks, int ntasks,
+// phase 1: one warp per (task, component) pair; no shared memory, no block
+// barriers.  NMT = 8-row m-tiles of V^T held in registers: the pairs with
+// rank <= 16 (almost all) run the NMT = 2 instance, which needs half the
+// registers and so keeps twice as many warps (loads) in flight.  Pairs are
+// ordered by task, so neighbouring warps share the chunk's x rows in L1.
+template <int NMT>
+__global__ void __launch_bounds__(256)
+hmv16_z_kernel(const int2* __restrict__ pairs, int npairs, const Z16Task* __restrict__ tasks,
                const MvBlock* __restrict__ blocks, const Item* __restrict__ items,
                const int* __restrict__ rk, const double* __restrict__ arena,
                const double* __restrict__ xi, double* __restrict__ zpart) {
-  const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
   constexpr int Rs[6] = {0, 0, 0, 1, 1, 2}, Cs[6] = {0, 1, 2, 1, 2, 2};
-  for (int ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
-    const Z16Task tk = tasks[ti];
+  for (int w = gw; w < npairs; w += nw) {
+    const int2 pc = pairs[w];
+    const Z16Task tk = tasks[pc.x];
+    const int c = pc.y;
     const int* r8 = rk + 8 * tk.blk;
     const int k = r8[c];
-    if (k == 0) continue;
     int kpre = 0;
     for (int q = 0; q < c; ++q) kpre += r8[q];
     const int K = r8[6];
@@ -94,24 +100,24 @@ hmv16_z_kernel(const Z16Task* __restrict__ tasks, int ntasks,
     const double* V = arena + items[b.item0 + c].v_off + tk.j0;
     const double* xb = xi + (long long)(b.col0 + tk.j0) * 48 + g;
     double* zp = zpart + tk.zbase + (long long)tk.zi * K * 32;
-    for (int lg = 0; lg < k; lg += 32) {
-      double acc[4][2][2][2];
+    for (int lg = 0; lg < k; lg += 8 * NMT) {
+      double acc[NMT][2][2][2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < NMT; ++a)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int xr = 0; xr < 2; ++xr) acc[a][nt][xr][0] = acc[a][nt][xr][1] = 0.0;
-      const int nmt = min(4, (k - lg + 7) >> 3);  // warp-uniform
+      const int nmt = min(NMT, (k - lg + 7) >> 3);  // warp-uniform
       // ZK k-steps (4 ZK columns) of A and B fragments issued before the MMAs
       for (int j16 = 0; j16 < tk.jlen; j16 += 4 * ZK) {
-        double a[ZK][4], bc[ZK][2], br[ZK][2];
+        double a[ZK][NMT], bc[ZK][2], br[ZK][2];
 #pragma unroll
         for (int st = 0; st < ZK; ++st) {
           const int j = j16 + 4 * st + t;
           const bool jok = j < tk.jlen;
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
+          for (int mt = 0; mt < NMT; ++mt) {
             const int l = lg + mt * 8 + g;
             a[st][mt] = (mt < nmt && l < k && jok) ? V[(long long)l * b.n + j] : 0.0;
           }
@@ -125,7 +131,7 @@ hmv16_z_kernel(const Z16Task* __restrict__ tasks, int ntasks,
         for (int st = 0; st < ZK; ++st) {
           if (j16 + 4 * st >= tk.jlen) break;  // warp-uniform
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
+          for (int mt = 0; mt < NMT; ++mt) {
             if (mt < nmt) {
               dmma(acc[mt][0][0][0], acc[mt][0][0][1], a[st][mt], bc[st][0]);
               dmma(acc[mt][1][0][0], acc[mt][1][0][1], a[st][mt], bc[st][1]);
@@ -138,7 +144,7 @@ hmv16_z_kernel(const Z16Task* __restrict__ tasks, int ntasks,
         }
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
+      for (int mt = 0; mt < NMT; ++mt) {
         const int l = lg + mt * 8 + g;
         if (mt < nmt && l < k) {
           double* row = zp + (long long)(kpre + l) * 32 + 2 * t;

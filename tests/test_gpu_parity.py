@@ -112,6 +112,22 @@ def test_c1_multi_rhs_dmma_sweep(c1, nrhs):
             assert rel(Y[:, q], o.matvec(np.ascontiguousarray(X[:, q]), om)) < 1e-12
 
 
+def test_c1_direct_matvec_policy(c1):
+    """One-shot matvecs after a rank change sweep the blocks in place (no
+    stream plan); same product within rounding of the summation order."""
+    g, o = c1["g"], c1["o"]
+    x = RV(3 * 1280, 11)
+    y_plan = g.matvec(x)
+    g.set_matvec_policy(True)
+    try:
+        y_direct = g.matvec(x)
+        assert (y_direct == g.matvec(x)).all()
+    finally:
+        g.set_matvec_policy(False)
+    assert rel(y_direct, y_plan) < 1e-13
+    assert rel(y_direct, o.matvec(x)) < 1e-12
+
+
 def test_c1_factors_match_oracle(c1):
     g, o = c1["g"], c1["o"]
     blocks = g.partition_blocks()
