@@ -150,6 +150,10 @@ struct PinnedVec {
     p[n++] = v;
   }
   void clear() { n = 0; }
+  void resize(size_t c) {  // contents unspecified (filled by a download)
+    reserve(c);
+    n = c;
+  }
   size_t size() const { return n; }
   bool empty() const { return n == 0; }
   T* data() { return p; }
@@ -293,6 +297,7 @@ struct hmgpu_ctx {
   DBuf<long long> d_zb16;
   DBuf<int> d_rk16;
   DBuf<int2> d_tiles16, d_zp2, d_zp4;
+  DBuf<AdmBlock> d_ablocks;
   int n_zp2 = 0, n_zp4 = 0;
   DBuf<double> d_zpart16, d_xi16;
   DBuf<int> d_pleaf_ptr;
@@ -325,7 +330,7 @@ struct hmgpu_ctx {
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
     d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
-    d_rk16.free(); d_tiles16.free(); d_zp2.free(); d_zp4.free();
+    d_rk16.free(); d_tiles16.free(); d_zp2.free(); d_zp4.free(); d_ablocks.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
     d_ptr.free(); d_lists.free(); d_order.free(); d_idx.free(); d_marked.free(); d_nm.free();
     d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
@@ -1501,6 +1506,8 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     c->piv_used = 0;
     c->dense_used = 0;
     long long cons_used = 0;
+    const int NCq = c->NC;
+    std::vector<AdmBlock> ablocks;
     // release the previous assembly before sizing this one
     c->d_arena.free();
     c->d_dense.free();
@@ -1537,31 +1544,25 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       if (rn[0] < c->row_begin || rn[1] > c->row_end) continue;
       const int m = rn[1] - rn[0], n = cn[1] - cn[0];
       if (B[2]) {
-        c->item_of_block[b] = (int)c->items.size();
+        // the NC items of this block are generated on the device from one
+        // record (items_init_kernel); offsets assigned here in item order
+        c->item_of_block[b] = (int)(NCq * ablocks.size());
         const long long capr = std::min<long long>(max_rank, std::min(m, n));
         const int cap = (int)std::min<long long>(capr, cap_init);
-        for (int q = 0; q < c->NC; ++q) {
-          Item it{};
-          it.m = m;
-          it.n = n;
-          it.row0 = rn[0];
-          it.col0 = cn[0];
-          it.comp = q;
-          it.cap = cap;
-          it.block = b;
-          it.phase = initial_rank >= 0 ? PH_INIT : PH_RUN;
-          it.steps_left = initial_rank >= 0 ? initial_rank : 0;
-          it.last_stop = STOP_NONE;
-          it.u_off = c->arena_used;
-          c->arena_used += align2((long long)m * cap);
-          it.v_off = c->arena_used;
-          c->arena_used += align2((long long)n * cap);
-          it.p_off = c->piv_used;
-          c->piv_used += std::max(cap, 1);
-          it.z_off = cons_used;
-          cons_used += align16(m);
-          c->items.push_back(it);
-        }
+        AdmBlock ab{};
+        ab.m = m;
+        ab.n = n;
+        ab.row0 = rn[0];
+        ab.col0 = cn[0];
+        ab.block = b;
+        ab.cap = cap;
+        ab.u_base = c->arena_used;
+        ab.p_base = c->piv_used;
+        ab.z_base = cons_used;
+        c->arena_used += (long long)NCq * (align2((long long)m * cap) + align2((long long)n * cap));
+        c->piv_used += (long long)NCq * std::max(cap, 1);
+        cons_used += (long long)NCq * align16(m);
+        ablocks.push_back(ab);
       } else {
         c->dense_of_block[b] = (int)c->dblocks.size();
         DenseBlock db{m, n, rn[0], cn[0], c->dense_used};
@@ -1573,8 +1574,17 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     const double want = 8.0 * (double)c->arena_used * 1.3;
     const size_t arena_cap = want < 0.85 * avail ? (size_t)(c->arena_used * 1.3)
                                                  : (size_t)c->arena_used;
+    c->items.resize((size_t)NCq * ablocks.size());  // mirror filled by download_items
     phase("items");
-    c->d_items.upload(c->items.data(), c->items.size(), c->stream);
+    c->d_items.ensure(std::max<size_t>(c->items.size(), 1));
+    if (!ablocks.empty()) {
+      c->d_ablocks.upload(ablocks, c->stream);
+      items_init_kernel<<<(int)((ablocks.size() * NCq + 255) / 256), 256, 0, c->stream>>>(
+          c->d_ablocks.p, (int)ablocks.size(), NCq,
+          initial_rank >= 0 ? PH_INIT : PH_RUN, initial_rank >= 0 ? initial_rank : 0,
+          c->d_items.p);
+      CK(cudaGetLastError());
+    }
     c->d_arena.alloc(arena_cap + 2);
     c->d_piv.alloc((size_t)(c->piv_used * 1.3) + 1);
     c->d_cons.alloc((size_t)cons_used + 16);
@@ -1600,16 +1610,19 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     CK(cudaEventRecord(tn1, c->stream));
 
     phase("nearfield");
-    // ACA, largest blocks first (stable counting sort on m + n)
+    // ACA, largest blocks first (stable counting sort of the blocks on m + n;
+    // a block's items stay in component order)
     std::vector<int> list(c->items.size());
     {
       int kmax_mn = 0;
-      for (const Item& it : c->items) kmax_mn = std::max(kmax_mn, it.m + it.n);
+      for (const AdmBlock& ab : ablocks) kmax_mn = std::max(kmax_mn, ab.m + ab.n);
       std::vector<int> cnt(kmax_mn + 2, 0);
-      for (const Item& it : c->items) ++cnt[kmax_mn - (it.m + it.n) + 1];
+      for (const AdmBlock& ab : ablocks) ++cnt[kmax_mn - (ab.m + ab.n) + 1];
       for (int k = 1; k <= kmax_mn + 1; ++k) cnt[k] += cnt[k - 1];
-      for (size_t t = 0; t < c->items.size(); ++t)
-        list[cnt[kmax_mn - (c->items[t].m + c->items[t].n)]++] = (int)t;
+      for (size_t a = 0; a < ablocks.size(); ++a) {
+        const int pos = cnt[kmax_mn - (ablocks[a].m + ablocks[a].n)]++;
+        for (int q = 0; q < NCq; ++q) list[(size_t)pos * NCq + q] = (int)(a * NCq + q);
+      }
     }
     int relaunch = 0;
     run_aca(c, list, &relaunch);

@@ -318,6 +318,42 @@ struct __align__(16) Item {
 };
 static_assert(sizeof(Item) == 128, "Item layout");
 
+// one admissible block's record from which its NC work items are generated
+// on the device (offsets of item q: U at u_base + q (align2(m cap) +
+// align2(n cap)), V right after its U, pivots p_base + q max(cap, 1),
+// consumed mask z_base + q align16(m))
+struct AdmBlock {
+  int m, n, row0, col0;
+  int block, cap, pad0, pad1;
+  long long u_base, p_base, z_base;
+};
+
+__global__ void items_init_kernel(const AdmBlock* __restrict__ ab, int nab, int nc,
+                                  int phase, int steps_left, Item* __restrict__ items) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nab * nc) return;
+  const int a = t / nc, q = t - a * nc;
+  const AdmBlock b = ab[a];
+  const long long su = ((long long)b.m * b.cap + 1) & ~1LL;
+  const long long sv = ((long long)b.n * b.cap + 1) & ~1LL;
+  Item it{};
+  it.m = b.m;
+  it.n = b.n;
+  it.row0 = b.row0;
+  it.col0 = b.col0;
+  it.comp = q;
+  it.cap = b.cap;
+  it.block = b.block;
+  it.phase = phase;
+  it.steps_left = steps_left;
+  it.last_stop = 0;  // STOP_NONE
+  it.u_off = b.u_base + (long long)q * (su + sv);
+  it.v_off = it.u_off + su;
+  it.p_off = b.p_base + (long long)q * max(b.cap, 1);
+  it.z_off = b.z_base + (long long)q * ((b.m + 15) & ~15);
+  items[t] = it;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
