@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
 #include <new>
 #include <numeric>
@@ -268,6 +269,8 @@ struct hmgpu_ctx {
   DBuf<int> d_pwoff;
   int p_woff_base[2] = {0, 0}, p_chunk_base[2] = {0, 0};
   int p_nwarps = 0, p_njb = 0;
+  int p_nwarps_pass[2] = {0, 0};
+  size_t p_smem_pass[2] = {0, 0};
   DBuf<double> d_sarena, d_zpart;
   DBuf<LeafEntry> d_pentries;
 
@@ -792,27 +795,30 @@ void refresh_matvec_ranks(hmgpu_ctx* c) {
 struct MvCfg {
   int warps = 12, ns = 2, stage = 896, scratch = 600;
 };
-MvCfg mv_cfg() {
-  static MvCfg cfg = [] {
-    MvCfg c;
-    if (const char* e = std::getenv("HMGPU_MV_CFG")) {
-      int w, n, s, k;
-      if (std::sscanf(e, "%d,%d,%d,%d", &w, &n, &s, &k) == 4) {
-        c.warps = w;
-        c.ns = n;
-        c.stage = s;
-        c.scratch = k;
-      }
-    }
-    return c;
-  }();
-  return cfg;
+// pass 0 (FUSED / DENSE / VSPLIT jobs) and pass 1 (USPLIT); HMGPU_MV_CFG sets
+// both, HMGPU_MV_CFG_A / HMGPU_MV_CFG_B one pass
+MvCfg parse_mv_cfg(const char* e, MvCfg c) {
+  int w, n, s, k;
+  if (e && std::sscanf(e, "%d,%d,%d,%d", &w, &n, &s, &k) == 4) {
+    c.warps = w;
+    c.ns = n;
+    c.stage = s;
+    c.scratch = k;
+  }
+  return c;
+}
+MvCfg mv_cfg(int pass) {
+  static const MvCfg both = parse_mv_cfg(std::getenv("HMGPU_MV_CFG"), MvCfg{});
+  static const MvCfg a = parse_mv_cfg(std::getenv("HMGPU_MV_CFG_A"), both);
+  static const MvCfg b = parse_mv_cfg(std::getenv("HMGPU_MV_CFG_B"), both);
+  return pass == 0 ? a : b;
 }
 
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
-  const MvCfg cfg = mv_cfg();
+  const MvCfg cfg = mv_cfg(0), cfgB = mv_cfg(1);
   const int kStageData = cfg.stage - 16;  // data + aux after the descriptor header
+  const int kStageDataB = cfgB.stage - 16;
   const int kMaxKFused = (cfg.scratch - 256) / 4;  // scratch: x (256) + W (4 K)
   const int NC = c->NC;
   std::vector<WJob> ja, jb;
@@ -964,7 +970,8 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     // USPLIT row tiles over component groups whose W fits the warp scratch
     for (int q0 = 0; q0 < NC;) {
       int q1 = q0, kg = 0;
-      while (q1 < NC && 4 * (kg + k[q1]) <= cfg.scratch && 4 * (kg + k[q1]) <= kStageData / 2)
+      while (q1 < NC && 4 * (kg + k[q1]) <= cfgB.scratch &&
+             4 * (kg + k[q1]) <= kStageDataB / 2)
         kg += k[q1++];
       if (q1 == q0) fail(HMGPU_ERR_INVALID, "rank too large for the streamed matvec");
       if (kg == 0) {
@@ -983,8 +990,8 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         j.out = slots;
         std::copy(gkp, gkp + 8, j.kp);
         std::vector<WChunk> chs;
-        const int first_cols = std::max(1, (kStageData - 4 * kg) / rt);
-        const int cols = std::max(1, kStageData / rt);
+        const int first_cols = std::max(1, (kStageDataB - 4 * kg) / rt);
+        const int cols = std::max(1, kStageDataB / rt);
         for (int g0 = 0; g0 < kg;) {
           const int g1 = std::min(kg, g0 + (g0 == 0 ? first_cols : cols));
           const long long off = alen;
@@ -1020,11 +1027,11 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   };
   // job table (pass A then pass B, each largest first) and, per pass, a
   // warp-major chunk table for the static round-robin job -> warp mapping
-  const int NWARPS = c->sm_count * cfg.warps;
   std::vector<WJob> jobs;
   std::vector<WChunk> chunks;
   std::vector<int> woff;
   for (int pass = 0; pass < 2; ++pass) {
+    const int NWARPS = c->sm_count * (pass == 0 ? cfg.warps : cfgB.warps);
     auto& J = pass == 0 ? ja : jb;
     auto& C = pass == 0 ? ca : cb;
     const std::vector<int> ord = order(C);
@@ -1042,8 +1049,9 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       }
     }
     woff.push_back((int)chunks.size() - c->p_chunk_base[pass]);
+    c->p_nwarps_pass[pass] = NWARPS;
   }
-  c->p_nwarps = NWARPS;
+  c->p_nwarps = c->p_nwarps_pass[0];
   std::vector<LeafEntry> entries;
   c->p_leaf_ptr.assign(nl + 1, 0);
   for (int l = 0; l < nl; ++l) {
@@ -1074,6 +1082,8 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   c->p_zslots = wslots;
   c->p_arena_len = alen;
   c->p_smem = sizeof(double) * (size_t)cfg.warps * (cfg.ns * cfg.stage + cfg.scratch);
+  c->p_smem_pass[0] = c->p_smem;
+  c->p_smem_pass[1] = sizeof(double) * (size_t)cfgB.warps * (cfgB.ns * cfgB.stage + cfgB.scratch);
   c->plan_mode = mode;
   c->plan_nrhs = nrhs;
   c->plan_valid = true;
@@ -1203,20 +1213,20 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
   P.wout = c->d_zpart.p;
   P.win = c->d_zpart.p;
   P.ypart = c->d_ypart.p;
-  const MvCfg cfg = mv_cfg();
-  P.stage = cfg.stage;
-  P.scratch = cfg.scratch;
   P.jobs = c->d_pjobs.p;
-  P.nwarps = c->p_nwarps;
   auto run = [&](int pass, int count, const char* name) {
     if (count <= 0) return;
+    const MvCfg cfg = mv_cfg(pass);
+    P.stage = cfg.stage;
+    P.scratch = cfg.scratch;
+    P.nwarps = c->p_nwarps_pass[pass];
     P.chunks = c->d_pchunks.p + c->p_chunk_base[pass];
     P.woff = c->d_pwoff.p + c->p_woff_base[pass];
-    const int g = c->p_nwarps / cfg.warps;  // the layout's grid: one CTA per SM
+    const int g = P.nwarps / cfg.warps;  // the layout's grid: one CTA per SM
+    const size_t smem = c->p_smem_pass[pass];
     auto go = [&](auto kernel) {
-      CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)c->p_smem));
-      kernel<<<g, cfg.warps * 32, c->p_smem, c->stream>>>(P);
+      CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kernel<<<g, cfg.warps * 32, smem, c->stream>>>(P);
     };
 #define HMV_CASE(W, S)                                        \
   if (cfg.warps == W && cfg.ns == S) {                        \
