@@ -339,3 +339,43 @@ def test_gpu_amvm_kelvin_ellipsoid_matches_oracle():
     gk, gl, _, _ = g.ranks()
     ok, ol, _, _ = o.ranks()
     assert (gk == ok).all() and (gl == ol).all()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_block_row_shards_on_one_device(c1, world):
+    """The multi-GPU decomposition run shard by shard on one
+    device: every shard assembles the blocks of its row range and its matvec
+    fills only its rows, so the sum of the shard products (the all-reduce of
+    bench.py) equals the whole operator's product, and every owned block has
+    the whole operator's ranks."""
+    g = c1["g"]
+    mesh = hm.Mesh.icosphere(3)
+    x = RV(3 * 1280, 5)
+    X = np.asfortranarray(np.stack([RV(3 * 1280, 40 + s) for s in range(3)], axis=1))
+    y_full = g.matvec(x)
+    Y_full = g.matvec(X)
+    k_full, kl_full, _, _ = g.ranks()
+    y = np.zeros_like(y_full)
+    Y = np.zeros_like(Y_full)
+    owned = np.zeros(k_full.shape[1], dtype=int)
+    for r in range(world):
+        s = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0, shard=(r, world))
+        s.assemble(eps=1e-4, beta=0.8, lookahead=2)
+        ys = s.matvec(x)
+        rb, re = s.row_range
+        t = s.tree()
+        rows = t.perm[rb:re]
+        mask = np.zeros(1280, dtype=bool)
+        mask[rows] = True
+        full_mask = np.tile(mask, 3)
+        assert (ys[~full_mask] == 0.0).all()  # only the shard's rows
+        y += ys
+        Y += s.matvec(X)  # the tensor-core multi-RHS sweep on a shard
+        k, kl, _, _ = s.ranks()
+        mine = k[0] >= 0
+        owned += mine
+        assert (k[:, mine] == k_full[:, mine]).all() and (kl[:, mine] == kl_full[:, mine]).all()
+    adm = k_full[0] >= 0
+    assert (owned[adm] == 1).all()
+    assert rel(y, y_full) < 1e-15
+    assert rel(Y, Y_full) < 1e-15
