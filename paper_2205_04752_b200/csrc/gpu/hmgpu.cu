@@ -2071,7 +2071,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_inset.p, 0, (size_t)std::max(nt, 1), c->stream));
     c->timed("amvm_walk", [&] {
-      const int wsmem = 3 * kWalkSmem * (int)sizeof(double);
+      const int wsmem = 4 * kWalkSmem * (int)sizeof(double);
       CK(cudaFuncSetAttribute(amvm_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               wsmem));
       amvm_walk_kernel<<<1, 32, wsmem, c->stream>>>(c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p,

@@ -295,7 +295,6 @@ __device__ __forceinline__ WalkTerm walk_load(int t, int lane, const long long* 
 }
 
 constexpr int kWalkSmem = 4096;  // entries of a term staged in shared memory
-
 __global__ void __launch_bounds__(32)
 amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restrict__ order,
                  long long nrows, const int* __restrict__ ptr, const int* __restrict__ lists,
@@ -304,7 +303,7 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
                  double* __restrict__ residual, unsigned char* __restrict__ in_set,
                  int* __restrict__ marked, int* __restrict__ n_marked,
                  double* __restrict__ out_pk) {
-  extern __shared__ double wsm[];  // [3][kWalkSmem]: indices, values, residuals
+  extern __shared__ double wsm[];  // [4][kWalkSmem]: indices, values, residuals, products
   const int lane = threadIdx.x & 31;
   const double target = (1.0 - theta) * sc[1];
   const double target_sq = target * target;
@@ -346,10 +345,12 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
       if (a0) residual[w.i0] = r0 - w.v0;
       if (a1) residual[w.i1] = r1 - w.v1;
     } else if (w.n <= kWalkSmem) {
-      // staged in shared memory: every load of the term in flight at once
+      // staged in shared memory: every load of the term in flight at once;
+      // the products are formed in parallel and lane 0 adds them in order
       long long* si = reinterpret_cast<long long*>(wsm);
       double* sv = wsm + kWalkSmem;
       double* sr = wsm + 2 * kWalkSmem;
+      double* sp = wsm + 3 * kWalkSmem;
 #pragma unroll 4
       for (int e = lane; e < w.n; e += 32) {
         si[e] = eidx[w.e0 + e];
@@ -357,17 +358,26 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
       }
       __syncwarp();
 #pragma unroll 4
-      for (int e = lane; e < w.n; e += 32) sr[e] = residual[si[e]];
-      __syncwarp();
-      for (int b = 0; b < w.n; b += 32) {
-        const double pr = b + lane < w.n ? sr[b + lane] * sv[b + lane] : 0.0;
-        const int cnt = min(32, w.n - b);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const double s = __shfl_sync(0xffffffffu, pr, k);
-          if (k < cnt) dot += s;
-        }
+      for (int e = lane; e < w.n; e += 32) {
+        const double r = residual[si[e]];
+        sr[e] = r;
+        sp[e] = r * sv[e];
       }
+      __syncwarp();
+      if (lane == 0) {
+        double d = 0.0;
+        int e = 0;
+        for (; e + 8 <= w.n; e += 8) {
+          double p[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p[u] = sp[e + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) d += p[u];
+        }
+        for (; e < w.n; ++e) d += sp[e];
+        dot = d;
+      }
+      dot = __shfl_sync(0xffffffffu, dot, 0);
       res_sq += w.nsq - 2.0 * dot;
 #pragma unroll 4
       for (int e = lane; e < w.n; e += 32) residual[si[e]] = sr[e] - sv[e];
