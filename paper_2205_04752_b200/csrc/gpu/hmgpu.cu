@@ -16,12 +16,14 @@
 #include <cstring>
 #include <array>
 #include <map>
+#include <mutex>
 #include <new>
 #include <numeric>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -59,6 +61,19 @@ struct Fail {
 thread_local cudaMemPool_t g_pool = nullptr;
 thread_local cudaStream_t g_stream = nullptr;
 
+// every live context's pool and stream: on an out-of-memory the idle memory
+// of all of them goes back to the device (trim is safe against in-use blocks)
+std::mutex g_pools_mu;
+std::vector<std::pair<cudaMemPool_t, cudaStream_t>> g_pools;
+
+void reclaim_idle_memory() {
+  std::lock_guard<std::mutex> lk(g_pools_mu);
+  for (auto& ps : g_pools) {
+    cudaStreamSynchronize(ps.second);
+    cudaMemPoolTrimTo(ps.first, 0);
+  }
+}
+
 void* pool_alloc(size_t bytes) {
   void* p = nullptr;
   if (!g_pool) {
@@ -66,10 +81,10 @@ void* pool_alloc(size_t bytes) {
     return p;
   }
   cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, g_pool, g_stream);
-  if (e == cudaErrorMemoryAllocation) {  // give the pool's idle memory back, retry
+  if (e == cudaErrorMemoryAllocation) {  // give the pools' idle memory back, retry
     (void)cudaGetLastError();
     CK(cudaStreamSynchronize(g_stream));
-    CK(cudaMemPoolTrimTo(g_pool, 0));
+    reclaim_idle_memory();
     e = cudaMallocFromPoolAsync(&p, bytes, g_pool, g_stream);
   }
   CK(e);
@@ -167,6 +182,148 @@ struct PinnedVec {
   const T* end() const { return p + n; }
 };
 
+// The ACA factor arena: a virtual-address range reserved once (as large as
+// the device memory) into which physical memory is mapped on demand
+// (cuMemCreate / cuMemMap), so capacity regrow and AMVM refinement extend it
+// in place -- no copy of the arena and no old + new peak.  Driver entry
+// points come from cudaGetDriverEntryPoint (no link-time libcuda).
+struct VmmApi {
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  bool ok = false;
+};
+const VmmApi& vmm_api() {
+  static const VmmApi api = [] {
+    VmmApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    a.ok = get("cuMemAddressReserve", (void**)&a.reserve) &&
+           get("cuMemAddressFree", (void**)&a.addr_free) &&
+           get("cuMemCreate", (void**)&a.create) && get("cuMemRelease", (void**)&a.release) &&
+           get("cuMemMap", (void**)&a.map) && get("cuMemUnmap", (void**)&a.unmap) &&
+           get("cuMemSetAccess", (void**)&a.set_access) &&
+           get("cuMemGetAllocationGranularity", (void**)&a.granularity);
+    return a;
+  }();
+  return api;
+}
+
+#define CU(x)                                                                  \
+  do {                                                                         \
+    CUresult r_ = (x);                                                         \
+    if (r_ != CUDA_SUCCESS)                                                    \
+      throw Fail{r_ == CUDA_ERROR_OUT_OF_MEMORY ? HMGPU_ERR_OOM : HMGPU_ERR_CUDA, \
+                 std::string(#x) + ": CUresult " + std::to_string((int)r_)};  \
+  } while (0)
+
+struct VArena {
+  double* p = nullptr;
+  size_t n = 0;  // mapped capacity in doubles
+  CUdeviceptr base = 0;
+  size_t va = 0, mapped = 0, gran = 0;
+  int device = -1;
+  std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks;
+
+  VArena() = default;
+  VArena(VArena&& o) noexcept { *this = std::move(o); }
+  VArena(const VArena&) = delete;
+  VArena& operator=(const VArena&) = delete;
+  VArena& operator=(VArena&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(base, o.base);
+    std::swap(va, o.va);
+    std::swap(mapped, o.mapped);
+    std::swap(gran, o.gran);
+    std::swap(device, o.device);
+    std::swap(chunks, o.chunks);
+    return *this;
+  }
+  ~VArena() { free(); }
+
+  CUmemAllocationProp prop() const {
+    CUmemAllocationProp pr{};
+    pr.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    pr.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    pr.location.id = device;
+    return pr;
+  }
+  // capacity for `count` doubles: maps more physical memory at the end
+  void ensure(size_t count, int dev) {
+    const VmmApi& api = vmm_api();
+    if (!api.ok) fail(HMGPU_ERR_CUDA, "virtual memory management entry points unavailable");
+    if (count == 0) count = 1;
+    if (count <= n) return;
+    if (!base) {
+      device = dev;
+      const CUmemAllocationProp pr = prop();
+      CU(api.granularity(&gran, &pr, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      va = (total_b + gran - 1) / gran * gran;
+      CU(api.reserve(&base, va, 0, 0, 0));
+      p = reinterpret_cast<double*>(base);
+    }
+    const size_t want = count * sizeof(double);
+    if (want > va) fail(HMGPU_ERR_OOM, "arena larger than the device memory");
+    // grow by at least 1/8 of the mapped size (fewer, larger chunks)
+    size_t delta = std::max(want - mapped, mapped / 8);
+    delta = std::min((delta + gran - 1) / gran * gran, va - mapped);
+    const CUmemAllocationProp pr = prop();
+    CUmemGenericAllocationHandle hnd;
+    CUresult rc = api.create(&hnd, delta, &pr, 0);
+    if (rc == CUDA_ERROR_OUT_OF_MEMORY) {  // idle pool memory back to the device, retry
+      reclaim_idle_memory();
+      rc = api.create(&hnd, delta, &pr, 0);
+    }
+    CU(rc);
+    CUresult r = api.map(base + mapped, delta, 0, hnd, 0);
+    if (r != CUDA_SUCCESS) {
+      api.release(hnd);
+      CU(r);
+    }
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = api.set_access(base + mapped, delta, &acc, 1);
+    if (r != CUDA_SUCCESS) {
+      api.unmap(base + mapped, delta);
+      api.release(hnd);
+      CU(r);
+    }
+    chunks.push_back({hnd, delta});
+    mapped += delta;
+    n = mapped / sizeof(double);
+  }
+  // releases everything (callers synchronise the stream first)
+  void free() {
+    if (!base) return;
+    const VmmApi& api = vmm_api();
+    size_t off = 0;
+    for (auto& ch : chunks) {
+      api.unmap(base + off, ch.second);
+      api.release(ch.first);
+      off += ch.second;
+    }
+    chunks.clear();
+    api.addr_free(base, va);
+    base = 0;
+    p = nullptr;
+    n = 0;
+    mapped = va = 0;
+  }
+};
+
 struct KTime {
   double ms = 0.0;
   long long launches = 0;
@@ -232,7 +389,8 @@ struct hmgpu_ctx {
   std::vector<int> dense_of_block;
   std::vector<DenseBlock> dblocks;
   DBuf<Item> d_items;
-  DBuf<double> d_arena;
+  VArena d_arena;                 // U/V factors (growable in place)
+  VArena spare_arena;             // the other arena of the compaction, kept mapped
   long long arena_used = 0;
   DBuf<int2> d_piv;
   long long piv_used = 0;
@@ -324,7 +482,8 @@ struct hmgpu_ctx {
     }
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     d_rowpt.free(); d_colpt.free(); d_tri.free(); d_A.free();
-    d_rperm.free(); d_cperm.free(); d_items.free(); d_arena.free();
+    if (stream) cudaStreamSynchronize(stream);
+    d_rperm.free(); d_cperm.free(); d_items.free(); d_arena.free(); spare_arena.free();
     d_piv.free(); d_cons.free(); d_dense.free(); d_dblocks.free();
     d_counter.free(); d_overflow.free(); d_list.free(); d_mvb.free();
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
@@ -340,6 +499,14 @@ struct hmgpu_ctx {
     d_resid.free(); d_nsq.free(); d_sc.free(); d_keys.free(); d_keys2.free();
     d_inset.free(); d_cub.free(); d_eptr.free(); d_eidx.free(); d_eval.free(); d_ecnt.free();
     if (stream) cudaStreamSynchronize(stream);
+    if (pool) {
+      std::lock_guard<std::mutex> lk(g_pools_mu);
+      for (size_t i = 0; i < g_pools.size(); ++i)
+        if (g_pools[i].first == pool) {
+          g_pools.erase(g_pools.begin() + i);
+          break;
+        }
+    }
     if (pool) cudaMemPoolDestroy(pool);
     g_pool = nullptr;
     g_stream = nullptr;
@@ -508,14 +675,8 @@ void upload_rules(hmgpu_ctx* c) {
 void arena_reserve(hmgpu_ctx* c, long long extra_doubles, long long extra_piv) {
   const long long need = c->arena_used + extra_doubles;
   if (need > (long long)c->d_arena.n) {
-    DBuf<double> nb;
-    nb.alloc((size_t)std::max<long long>(need, (long long)(c->d_arena.n * 3 / 2)));
-    if (c->arena_used)
-      CK(cudaMemcpyAsync(nb.p, c->d_arena.p, c->arena_used * sizeof(double),
-                         cudaMemcpyDeviceToDevice, c->stream));
-    c->sync();
-    c->d_arena.free();
-    c->d_arena = nb;
+    c->sync();  // mapping is synchronous with the host
+    c->d_arena.ensure((size_t)need, c->device);
   }
   const long long needp = c->piv_used + extra_piv;
   if (needp > (long long)c->d_piv.n) {
@@ -653,7 +814,7 @@ void compact(hmgpu_ctx* c, int slack) {
   usz.free();
   psz.free();
   const long long used = last[0] + last[1], usedp = last[2] + last[3];
-  const size_t free_b = avail_bytes();
+  const size_t free_b = avail_bytes() + c->spare_arena.mapped;
   if (8.0 * (double)used + 8.0 * (double)usedp > 0.9 * (double)free_b) {
     uoff.free();
     poff.free();
@@ -661,8 +822,8 @@ void compact(hmgpu_ctx* c, int slack) {
     download_items(c);  // not enough room for the packed copy: keep the loose arena
     return;
   }
-  DBuf<double> na;
-  na.alloc((size_t)used + 2);
+  VArena na = std::move(c->spare_arena);  // reuse the previous mapping
+  na.ensure((size_t)used + 2, c->device);
   DBuf<int2> npv;
   npv.alloc((size_t)usedp + 1);
   c->timed("compact", [&] {
@@ -673,8 +834,14 @@ void compact(hmgpu_ctx* c, int slack) {
   uoff.free();
   poff.free();
   caps.free();
-  c->d_arena.free();
-  c->d_arena = na;
+  c->d_arena = std::move(na);  // `na` now holds the loose arena: kept mapped
+  // for the next assembly while at least half of the device stays free
+  {
+    size_t fb = 0, tb = 0;
+    CK(cudaMemGetInfo(&fb, &tb));
+    if ((double)fb >= 0.5 * (double)tb) c->spare_arena = std::move(na);
+    else na.free();
+  }
   c->arena_used = used;
   c->d_piv.free();
   c->d_piv = npv;
@@ -1323,6 +1490,10 @@ int hmgpu_create(int device, hmgpu_ctx** out) {
     CK(cudaMemPoolCreate(&c->pool, &props));
     unsigned long long keep = ~0ULL;
     CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    {
+      std::lock_guard<std::mutex> lk(g_pools_mu);
+      g_pools.push_back({c->pool, c->stream});
+    }
     g_pool = c->pool;
     g_stream = c->stream;
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -1519,7 +1690,10 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     const int NCq = c->NC;
     std::vector<AdmBlock> ablocks;
     // release the previous assembly before sizing this one
-    c->d_arena.free();
+    c->sync();
+    // both arenas stay mapped across assemblies; the larger one takes the
+    // loose layout (the other is the compaction target)
+    if (c->spare_arena.n > c->d_arena.n) std::swap(c->spare_arena, c->d_arena);
     c->d_dense.free();
     c->d_piv.free();
     c->d_cons.free();
@@ -1539,7 +1713,8 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       else dense_total += n * align2((long long)c->NC * m);
     }
     c->sync();
-    const size_t free_b = avail_bytes();
+    // mapped arenas are reused by this assembly
+    const size_t free_b = avail_bytes() + c->d_arena.mapped + c->spare_arena.mapped;
     const double avail =
         (double)free_b - 8.0 * (double)dense_total - 4.0 * (1 << 30);
     int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
@@ -1580,10 +1755,9 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         c->dblocks.push_back(db);
       }
     }
-    // headroom at the arena end for relocated (regrown) items
-    const double want = 8.0 * (double)c->arena_used * 1.3;
-    const size_t arena_cap = want < 0.85 * avail ? (size_t)(c->arena_used * 1.3)
-                                                 : (size_t)c->arena_used;
+    // small headroom at the arena end for relocated (regrown) items; the
+    // arena grows in place beyond it (VArena)
+    const size_t arena_cap = (size_t)(c->arena_used * 1.02) + 1024;
     c->items.resize((size_t)NCq * ablocks.size());  // mirror filled by download_items
     phase("items");
     c->d_items.ensure(std::max<size_t>(c->items.size(), 1));
@@ -1595,7 +1769,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
           c->d_items.p);
       CK(cudaGetLastError());
     }
-    c->d_arena.alloc(arena_cap + 2);
+    c->d_arena.ensure(arena_cap + 2, c->device);
     c->d_piv.alloc((size_t)(c->piv_used * 1.3) + 1);
     c->d_cons.alloc((size_t)cons_used + 16);
     CK(cudaMemsetAsync(c->d_cons.p, 0, cons_used + 16, c->stream));
