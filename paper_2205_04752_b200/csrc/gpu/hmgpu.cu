@@ -429,7 +429,7 @@ struct hmgpu_ctx {
   int p_nwarps = 0, p_njb = 0;
   int p_nwarps_pass[2] = {0, 0};
   size_t p_smem_pass[2] = {0, 0};
-  DBuf<double> d_sarena, d_zpart;
+  DBuf<double> d_zpart;
   DBuf<LeafEntry> d_pentries;
 
   // ---- device-resident AMVM estimator (hmgpu_amvm.cuh) ----
@@ -489,7 +489,7 @@ struct hmgpu_ctx {
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
     d_leaf_ptr.free(); d_leaf_prow.free(); d_leaf_blk.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
-    d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_sarena.free(); d_zpart.free();
+    d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
     d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
     d_rk16.free(); d_tiles16.free(); d_zp2.free(); d_zp4.free(); d_ablocks.free();
@@ -834,14 +834,8 @@ void compact(hmgpu_ctx* c, int slack) {
   uoff.free();
   poff.free();
   caps.free();
-  c->d_arena = std::move(na);  // `na` now holds the loose arena: kept mapped
-  // for the next assembly while at least half of the device stays free
-  {
-    size_t fb = 0, tb = 0;
-    CK(cudaMemGetInfo(&fb, &tb));
-    if ((double)fb >= 0.5 * (double)tb) c->spare_arena = std::move(na);
-    else na.free();
-  }
+  c->d_arena = std::move(na);       // `na` now holds the loose arena: kept
+  c->spare_arena = std::move(na);   // mapped, it hosts the matvec stream arena
   c->arena_used = used;
   c->d_piv.free();
   c->d_piv = npv;
@@ -983,14 +977,40 @@ MvCfg mv_cfg(int pass) {
 
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
+  auto tp0 = std::chrono::steady_clock::now();
+  auto pphase = [&](const char* what) {
+    if (!verbose()) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hmgpu] plan %-10s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp0).count());
+    tp0 = now;
+  };
   const MvCfg cfg = mv_cfg(0), cfgB = mv_cfg(1);
   const int kStageData = cfg.stage - 16;  // data + aux after the descriptor header
   const int kStageDataB = cfgB.stage - 16;
   const int kMaxKFused = (cfg.scratch - 256) / 4;  // scratch: x (256) + W (4 K)
   const int NC = c->NC;
   std::vector<WJob> ja, jb;
-  std::vector<std::vector<WChunk>> ca, cb;  // chunks per job
+  // chunks per job, flat (CSR over the pass's jobs)
+  struct ChunkCSR {
+    std::vector<WChunk> flat;
+    std::vector<long long> ptr{0};
+    std::vector<long long> size;  // streamed doubles per job
+    void add(const std::vector<WChunk>& chs) {
+      long long s = 0;
+      for (const WChunk& ch : chs) s += ch.len + 4LL * ch.aux_len;
+      flat.insert(flat.end(), chs.begin(), chs.end());
+      ptr.push_back((long long)flat.size());
+      size.push_back(s);
+    }
+  } ca, cb;
+  std::vector<WChunk> chs;  // the current job's chunks (reused)
   std::vector<PackDesc> packs;
+  ja.reserve(c->mvb.size() * 2);
+  ca.flat.reserve(c->mvb.size() * 6);
+  ca.ptr.reserve(c->mvb.size() * 2);
+  ca.size.reserve(c->mvb.size() * 2);
+  packs.reserve(c->mvb.size() * 12);
   long long alen = 0, slots = 0, wslots = 0;
   const int nl = (int)c->leaf_begin.size();
   std::vector<std::vector<LeafEntry>> lists(nl);
@@ -1040,7 +1060,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.n = n;
       j.ncols = n;
       j.out = slots;
-      std::vector<WChunk> chs;
+      chs.clear();
       for (int g0 = 0; g0 < n; g0 += cpc) {
         const int g1 = std::min(n, g0 + cpc);
         chs.push_back(chunk(mb.dense_off + (long long)g0 * cp, (g1 - g0) * cp, 1,
@@ -1049,7 +1069,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       add_rows(mb.row0, m, slots);
       slots += m;
       ja.push_back(j);
-      ca.push_back(chs);
+      ca.add(chs);
       continue;
     }
     int k[6] = {0, 0, 0, 0, 0, 0};
@@ -1071,7 +1091,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.ncols = K;
       j.out = slots;
       std::copy(kp, kp + 8, j.kp);
-      std::vector<WChunk> chs;
+      chs.clear();
       // V part: row-major [j][g] chunks over whole columns, x rides along
       const int vcpc = std::max(1, (kStageData - 4 * n) / n);
       for (int g0 = 0; g0 < K; g0 += vcpc) {
@@ -1106,7 +1126,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       add_rows(mb.row0, m, slots);
       slots += m;
       ja.push_back(j);
-      ca.push_back(chs);
+      ca.add(chs);
       continue;
     }
     // split block: VSPLIT column groups of each component -> W (global)
@@ -1123,7 +1143,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         j.ncols = nc;
         j.comp = q;
         j.out = wbase + kp[q] + l0;
-        std::vector<WChunk> chs;
+        chs.clear();
         for (int r0 = 0; r0 < n; r0 += rpc) {
           const int r1 = std::min(n, r0 + rpc);
           const long long off =
@@ -1131,7 +1151,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
           chs.push_back(chunk(off, (r1 - r0) * nc, 0, WA_X, mb.col0 + r0, r1 - r0, r0, r1, 0));
         }
         ja.push_back(j);
-        ca.push_back(chs);
+        ca.add(chs);
       }
     }
     // USPLIT row tiles over component groups whose W fits the warp scratch
@@ -1156,7 +1176,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         j.ncols = kg;
         j.out = slots;
         std::copy(gkp, gkp + 8, j.kp);
-        std::vector<WChunk> chs;
+        chs.clear();
         const int first_cols = std::max(1, (kStageDataB - 4 * kg) / rt);
         const int cols = std::max(1, kStageDataB / rt);
         for (int g0 = 0; g0 < kg;) {
@@ -1177,68 +1197,80 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         add_rows(mb.row0 + i0, rt, slots);
         slots += rt;
         jb.push_back(j);
-        cb.push_back(chs);
+        cb.add(chs);
       }
       q0 = q1;
     }
   }
-  // order each pass by size (largest first) and lay out the chunk table
-  auto order = [](const std::vector<std::vector<WChunk>>& cs) {
-    std::vector<int> o(cs.size());
-    std::iota(o.begin(), o.end(), 0);
-    std::vector<long long> sz(cs.size(), 0);
-    for (size_t i = 0; i < cs.size(); ++i)
-      for (const WChunk& ch : cs[i]) sz[i] += ch.len + 4LL * ch.aux_len;
-    std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return sz[a] > sz[b]; });
+  // order each pass by size (largest first; stable counting sort on the
+  // streamed size) and lay out the chunk table
+  auto order = [](const ChunkCSR& cs) {
+    const size_t nj = cs.size.size();
+    long long smax = 0;
+    for (long long s : cs.size) smax = std::max(smax, s);
+    std::vector<int> cnt((size_t)smax + 2, 0), o(nj);
+    for (long long s : cs.size) ++cnt[(size_t)(smax - s) + 1];
+    for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+    for (size_t i = 0; i < nj; ++i) o[cnt[(size_t)(smax - cs.size[i])]++] = (int)i;
     return o;
   };
+  pphase("blocks");
   // job table (pass A then pass B, each largest first) and, per pass, a
   // warp-major chunk table for the static round-robin job -> warp mapping
   std::vector<WJob> jobs;
-  std::vector<WChunk> chunks;
   std::vector<int> woff;
+  const size_t nchunks_total = ca.flat.size() + cb.flat.size();
+  std::vector<WChunk> chunk_table(nchunks_total);
+  WChunk* chunks = chunk_table.data();
+  size_t nch = 0;
   for (int pass = 0; pass < 2; ++pass) {
     const int NWARPS = c->sm_count * (pass == 0 ? cfg.warps : cfgB.warps);
     auto& J = pass == 0 ? ja : jb;
-    auto& C = pass == 0 ? ca : cb;
+    const ChunkCSR& C = pass == 0 ? ca : cb;
     const std::vector<int> ord = order(C);
     const int jbase = (int)jobs.size();
     for (int idx : ord) jobs.push_back(J[idx]);
     c->p_woff_base[pass] = (int)woff.size();
-    c->p_chunk_base[pass] = (int)chunks.size();
+    c->p_chunk_base[pass] = (int)nch;
     for (int w = 0; w < NWARPS; ++w) {
-      woff.push_back((int)chunks.size() - c->p_chunk_base[pass]);
+      woff.push_back((int)(nch - c->p_chunk_base[pass]));
       for (int q = w; q < (int)ord.size(); q += NWARPS) {
-        for (WChunk ch : C[ord[q]]) {
+        for (long long k = C.ptr[ord[q]]; k < C.ptr[ord[q] + 1]; ++k) {
+          WChunk ch = C.flat[k];
           ch.job = jbase + q;
-          chunks.push_back(ch);
+          chunks[nch++] = ch;
         }
       }
     }
-    woff.push_back((int)chunks.size() - c->p_chunk_base[pass]);
+    woff.push_back((int)(nch - c->p_chunk_base[pass]));
     c->p_nwarps_pass[pass] = NWARPS;
   }
   c->p_nwarps = c->p_nwarps_pass[0];
+  pphase("layout");
   std::vector<LeafEntry> entries;
   c->p_leaf_ptr.assign(nl + 1, 0);
   for (int l = 0; l < nl; ++l) {
     entries.insert(entries.end(), lists[l].begin(), lists[l].end());
     c->p_leaf_ptr[l + 1] = (int)entries.size();
   }
-  c->d_sarena.free();
-  c->d_sarena.alloc((size_t)alen + 2);
+  pphase("entries");
+  // the stream arena lives in the idle arena of the last compaction (the
+  // loose ACA layout): no new device memory is mapped for it in steady state
+  c->sync();
+  c->spare_arena.ensure((size_t)alen + 2, c->device);
   if (!packs.empty()) {
     DBuf<PackDesc> d_packs;
     d_packs.upload(packs, c->stream);
     c->timed("pack", [&] {
       pack_kernel<<<grid_for(c, ((long long)packs.size() + 7) / 8, 16), 256, 0, c->stream>>>(
-          d_packs.p, (int)packs.size(), c->d_arena.p, c->d_sarena.p);
+          d_packs.p, (int)packs.size(), c->d_arena.p, c->spare_arena.p);
     });
     c->sync();
     d_packs.free();
   }
+  pphase("pack");
   c->d_pjobs.upload(jobs, c->stream);
-  c->d_pchunks.upload(chunks, c->stream);
+  c->d_pchunks.upload(chunks, nch, c->stream);
   c->d_pwoff.upload(woff, c->stream);
   c->d_pentries.upload(entries, c->stream);
   c->d_pleaf_ptr.upload(c->p_leaf_ptr, c->stream);
@@ -1255,10 +1287,11 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   c->plan_nrhs = nrhs;
   c->plan_valid = true;
   c->sync();
+  pphase("upload");
   if (verbose())
     std::fprintf(stderr, "[hmgpu] plan: jobs=%d (pass A %zu, USPLIT %zu) chunks=%zu "
                          "arena=%.3f GB slots=%lld wslots=%lld entries=%zu smem=%zu B\n",
-                 c->p_ntasks, ja.size(), jb.size(), chunks.size(), 8.0 * alen / 1e9, slots,
+                 c->p_ntasks, ja.size(), jb.size(), nch, 8.0 * alen / 1e9, slots,
                  wslots, entries.size(), c->p_smem);
 }
 
@@ -1374,7 +1407,7 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
   c->d_zpart.ensure((size_t)std::max<long long>(1, c->p_zslots * 4));
   WarpStreamParams P{};
   P.chunks = c->d_pchunks.p;
-  P.arena = c->d_sarena.p;
+  P.arena = c->spare_arena.p;  // the packed stream arena
   P.dense = c->d_dense.p;
   P.xi = c->d_xi.p;
   P.wout = c->d_zpart.p;
