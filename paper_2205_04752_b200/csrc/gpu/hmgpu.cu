@@ -733,19 +733,32 @@ void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>&
 
 // runs the ACA state machines of `list` to completion, regrowing the column
 // capacity of items that run out of it (resume is exact: same state)
-void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches) {
+// items with m + n at or above this run CTA-cooperatively (aca_kernel)
+int aca_cta_min() {
+  static const int v = [] {
+    const char* e = std::getenv("HMGPU_ACA_CTA_MIN");
+    return e ? std::atoi(e) : 2048;
+  }();
+  return v;
+}
+
+// `list` is ordered by m + n (largest first); mn(idx) gives an item's m + n
+template <class MN>
+void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
   const double sf = c->eps * (1.0 - c->beta) / (1.0 + c->eps);  // aca.cpp:114
   int passes = 0;
   while (!list.empty()) {
     c->d_list.upload(list, c->stream);
-    CK(cudaMemsetAsync(c->d_counter.p, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->d_counter.p, 0, 2 * sizeof(int), c->stream));
     CK(cudaMemsetAsync(c->d_overflow.p, 0, sizeof(int), c->stream));
+    int nbig = 0;
+    while (nbig < (int)list.size() && mn(list[nbig]) >= aca_cta_min()) ++nbig;
     const int nwarps = (int)list.size();
-    const int grid = grid_for(c, (nwarps + 7) / 8, 16);
+    const int grid = grid_for(c, std::max(nbig, (nwarps + 7) / 8), 16);
     c->timed("aca", [&] {
       auto go = [&](auto kernel) {
-        kernel<<<grid, 256, 0, c->stream>>>(
-            c->geom, c->d_items.p, c->d_list.p, (int)list.size(), c->d_counter.p,
+        kernel<<<grid, ACA_NT, 0, c->stream>>>(
+            c->geom, c->d_items.p, c->d_list.p, (int)list.size(), nbig, c->d_counter.p,
             c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
             c->d_overflow.p);
       };
@@ -1530,7 +1543,7 @@ int hmgpu_create(int device, hmgpu_ctx** out) {
     g_pool = c->pool;
     g_stream = c->stream;
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
-    c->d_counter.alloc(1);
+    c->d_counter.alloc(2);
     c->d_overflow.alloc(1);
     c->d_nq.alloc(1);
     c->rules.far_ratio = 4.0;
@@ -1842,7 +1855,41 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       }
     }
     int relaunch = 0;
-    run_aca(c, list, &relaunch);
+    auto mn_of = [&](int idx) { return ablocks[idx / NCq].m + ablocks[idx / NCq].n; };
+    static const bool split = std::getenv("HMGPU_ACA_CLASSES") != nullptr;
+    if (split && !list.empty()) {
+      // diagnostic: the ACA run class by class (m + n ranges, largest first)
+      // with one event pair per class; the results are the same
+      size_t s0 = 0;
+      while (s0 < list.size()) {
+        const AdmBlock& a0 = ablocks[list[s0] / NCq];
+        int lo = 1;
+        while (2 * lo <= a0.m + a0.n) lo *= 2;
+        size_t s1 = s0;
+        while (s1 < list.size()) {
+          const AdmBlock& a1 = ablocks[list[s1] / NCq];
+          if (a1.m + a1.n < lo) break;
+          ++s1;
+        }
+        std::vector<int> sub(list.begin() + s0, list.begin() + s1);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, c->stream));
+        run_aca(c, sub, &relaunch, mn_of);
+        CK(cudaEventRecord(e1, c->stream));
+        c->sync();
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        std::fprintf(stderr, "[hmgpu] aca class m+n in [%d,%d): items=%zu ms=%.3f\n", lo,
+                     2 * lo, sub.size(), ms);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        s0 = s1;
+      }
+    } else {
+      run_aca(c, list, &relaunch, mn_of);
+    }
     phase("aca");
     compact(c, 0);
     phase("compact");
@@ -2041,7 +2088,7 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
     return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
   });
-  run_aca(c, ids, nullptr);
+  run_aca(c, ids, nullptr, [&](int idx) { return c->items[idx].m + c->items[idx].n; });
   download_items(c);
   refresh_matvec_ranks(c);
   c->plan_valid = false;

@@ -1,10 +1,16 @@
 // Device side of the B200 H-matrix hot path: fused Kelvin / Newton / dense
-// entry providers, batched warp-per-block ACA, near-field fill, H-matvec
+// entry providers, batched ACA (warp or CTA per item), near-field fill, H-matvec
 // sweep and look-ahead tail products.  fp64 throughout (sm_100a).
 #pragma once
 
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#ifndef HMGPU_RUNROLL
+#define HMGPU_RUNROLL 2
+#endif
+#define HM_PRAGMA(x) _Pragma(#x)
+#define HM_UNROLL(n) HM_PRAGMA(unroll n)
 
 namespace hmgpu {
 
@@ -422,41 +428,45 @@ __device__ __forceinline__ LineStats residual_line(const SRC& src, bool is_row, 
                                                    const double* __restrict__ W, int ldw,
                                                    const double* __restrict__ X, int ldx,
                                                    int len, int k, double* __restrict__ out,
-                                                   double* __restrict__ ebuf, int lane) {
+                                                   double* __restrict__ ebuf, int lane,
+                                                   int nt) {
+  // nt threads (one warp, or the CTA for the largest items); element t is
+  // handled by thread t % nt, the lane-strided order of the canonical sums
   LineStats st{0.0, -1.0, 0.0, 0.0, -1, 0};
-  for (int base = 0; base < len; base += 128) {
-    const int nb = min(4, (len - base + 31) >> 5);  // warp-uniform
+  for (int base = 0; base < len; base += 4 * nt) {
+    const int rem = len - base;  // group-uniform; nb = min(4, ceil(rem / nt))
+    const int nb = rem > 3 * nt ? 4 : rem > 2 * nt ? 3 : rem > nt ? 2 : 1;
     double v[4];
     bool ok[4];
     // phase A: the kernel entries of up to 4 columns per lane (arithmetic
     // only; parked in this lane's shared-memory slots)
 #pragma unroll 1
     for (int s = 0; s < nb; ++s) {
-      const int t = base + 32 * s + lane;
-      ebuf[32 * s + lane] = t < len ? src(is_row, fix, t, st.nq) : 0.0;
+      const int t = base + nt * s + lane;
+      ebuf[nt * s + lane] = t < len ? src(is_row, fix, t, st.nq) : 0.0;
     }
     // phase B: the low-rank correction, four independent columns per lane so
     // that eight panel loads are in flight per lane
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      const int t = base + 32 * s + lane;
+      const int t = base + nt * s + lane;
       ok[s] = s < nb && t < len;
-      v[s] = ok[s] ? ebuf[32 * s + lane] : 0.0;
+      v[s] = ok[s] ? ebuf[nt * s + lane] : 0.0;
       if (ok[s]) st.rs = fmax(st.rs, fabs(v[s]));
     }
     const double* xb = X + base + lane;
-#pragma unroll 2
+HM_UNROLL(HMGPU_RUNROLL)
     for (int l = 0; l < k; ++l) {
       const double w = -W[(long long)l * ldw + fix];
       const double* xl = xb + (long long)l * ldx;
 #pragma unroll
       for (int s = 0; s < 4; ++s)
-        if (ok[s]) v[s] = fma(w, xl[32 * s], v[s]);
+        if (ok[s]) v[s] = fma(w, xl[nt * s], v[s]);
     }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       if (!ok[s]) continue;
-      const int t = base + 32 * s + lane;
+      const int t = base + nt * s + lane;
       out[t] = v[s];
       st.sq = fma(v[s], v[s], st.sq);
       if (fabs(v[s]) > st.pm) {
@@ -552,16 +562,187 @@ __device__ __forceinline__ double cross_terms(const double* __restrict__ uk,
   return cross;
 }
 
-// One ACA step of aca_step (aca.cpp:41-102) executed by one warp.
+// ---------------------------------------------------------------------------
+// Work groups of the ACA.  An item (block, component) is run either by one
+// warp (gsize 32, gtid = lane) or, for the largest blocks, by the whole CTA
+// (gsize ACA_NT, gtid = threadIdx.x): a single warp on a block with m + n in
+// the thousands was latency-bound on its panel loads and made the largest
+// items the critical path of the assembly (config 3: 196 ms for the 192
+// items with m + n >= 16384 run alone).  Both modes give the same bits: the
+// max / arg-max reductions are exact, and the CTA mode forms the canonical
+// lane-strided sums (||u||^2, ||v||^2, u.U(:,l), v.V(:,l)) with one warp per
+// sum from the stored line, in the warp mode's order.
+constexpr int ACA_NT = 256;
+constexpr int ACA_NW = ACA_NT / 32;
+
+struct AcaShared {
+  double ebuf[4 * ACA_NT];   // entry slots: warp mode [warp][4][32], CTA mode [4][ACA_NT]
+  double du[ACA_NT], dv[ACA_NT];  // CTA mode: per-l dots of the cross terms
+  double rd[ACA_NW], ra[ACA_NW];
+  long long rl[ACA_NW];
+  int ri[ACA_NW];
+  double uu, vv;
+  int t;
+};
+
+struct Grp {
+  int tid, size;
+  __device__ __forceinline__ bool cta() const { return size > 32; }
+  __device__ __forceinline__ int lane() const { return tid & 31; }
+  __device__ __forceinline__ int warp() const { return tid >> 5; }
+};
+
+__device__ __forceinline__ void gsync(const Grp& g) {
+  if (g.cta()) __syncthreads();
+  else __syncwarp();
+}
+
+__device__ __forceinline__ double grp_max(double v, const Grp& g, AcaShared& sh) {
+  v = warp_max(v);
+  if (!g.cta()) return v;
+  if (g.lane() == 0) sh.rd[g.warp()] = v;
+  __syncthreads();
+  double r = sh.rd[0];
+#pragma unroll
+  for (int w = 1; w < ACA_NW; ++w) r = fmax(r, sh.rd[w]);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ int grp_min_int(int v, const Grp& g, AcaShared& sh) {
+  v = warp_min_int(v);
+  if (!g.cta()) return v;
+  if (g.lane() == 0) sh.ri[g.warp()] = v;
+  __syncthreads();
+  int r = sh.ri[0];
+#pragma unroll
+  for (int w = 1; w < ACA_NW; ++w) r = min(r, sh.ri[w]);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ long long grp_sum_ll(long long t, const Grp& g, AcaShared& sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (!g.cta()) return t;
+  if (g.lane() == 0) sh.rl[g.warp()] = t;
+  __syncthreads();
+  long long r = 0;
+#pragma unroll
+  for (int w = 0; w < ACA_NW; ++w) r += sh.rl[w];
+  __syncthreads();
+  return r;
+}
+
+// first-max arg-max over the group (larger value, then smaller index)
+__device__ __forceinline__ void grp_argmax(double& val, int& idx, double& aux, const Grp& g,
+                                           AcaShared& sh) {
+  warp_argmax(val, idx, aux);
+  if (!g.cta()) return;
+  if (g.lane() == 0) {
+    sh.rd[g.warp()] = val;
+    sh.ri[g.warp()] = idx;
+    sh.ra[g.warp()] = aux;
+  }
+  __syncthreads();
+  double bv = sh.rd[0], ba = sh.ra[0];
+  int bi = sh.ri[0];
+#pragma unroll
+  for (int w = 1; w < ACA_NW; ++w) {
+    const double v = sh.rd[w];
+    const int i = sh.ri[w];
+    if (v > bv || (v == bv && i >= 0 && (bi < 0 || i < bi))) {
+      bv = v;
+      bi = i;
+      ba = sh.ra[w];
+    }
+  }
+  __syncthreads();
+  val = bv;
+  idx = bi;
+  aux = ba;
+}
+
+// canonical lane-strided dot (warp order, as warp_sum of fma partials)
+__device__ __forceinline__ double warp_dot(const double* __restrict__ a,
+                                           const double* __restrict__ b, int len, int lane) {
+  double p = 0.0;
+  for (int r = lane; r < len; r += 32) p = fma(a[r], b[r], p);
+  return warp_sum(p);
+}
+
+// CTA mode: ||u||^2 and ||v||^2 (warps 0 and 1) and the dots u.U(:,l),
+// v.V(:,l) of the cross terms (l spread over the warps), each a canonical
+// warp-order sum of the stored line; cross = sum_l du_l dv_l in l order.
+__device__ double cta_norms_cross(const double* __restrict__ uk, const double* __restrict__ U,
+                                  int m, const double* __restrict__ vk,
+                                  const double* __restrict__ V, int n, int k, const Grp& g,
+                                  AcaShared& sh, double& uu, double& vv) {
+  const int lane = g.lane(), w = g.warp();
+  __syncthreads();  // the line is complete
+  if (w == 0) {
+    const double t = warp_dot(uk, uk, m, lane);
+    if (lane == 0) sh.uu = t;
+  } else if (w == 1) {
+    const double t = warp_dot(vk, vk, n, lane);
+    if (lane == 0) sh.vv = t;
+  }
+  double cross = 0.0;
+  for (int l0 = 0; l0 < k; l0 += ACA_NT) {
+    const int l1 = min(k, l0 + ACA_NT);
+    // two l per pass share the loads of the line
+    for (int l = l0 + w; l < l1; l += 2 * ACA_NW) {
+      const int la = l, lb = l + ACA_NW;
+      const bool hb = lb < l1;
+      const double* Ua = U + (long long)la * m;
+      const double* Ub = U + (long long)(hb ? lb : la) * m;
+      const double* Va = V + (long long)la * n;
+      const double* Vb = V + (long long)(hb ? lb : la) * n;
+      double pa = 0.0, pb = 0.0, qa = 0.0, qb = 0.0;
+      for (int r = lane; r < m; r += 32) {
+        const double x = uk[r];
+        pa = fma(x, Ua[r], pa);
+        pb = fma(x, Ub[r], pb);
+      }
+      for (int c = lane; c < n; c += 32) {
+        const double x = vk[c];
+        qa = fma(x, Va[c], qa);
+        qb = fma(x, Vb[c], qb);
+      }
+      pa = warp_sum(pa);
+      qa = warp_sum(qa);
+      pb = warp_sum(pb);
+      qb = warp_sum(qb);
+      if (lane == 0) {
+        sh.du[la - l0] = pa;
+        sh.dv[la - l0] = qa;
+        if (hb) {
+          sh.du[lb - l0] = pb;
+          sh.dv[lb - l0] = qb;
+        }
+      }
+    }
+    __syncthreads();
+    for (int l = l0; l < l1; ++l) cross = fma(sh.du[l - l0], sh.dv[l - l0], cross);
+    __syncthreads();
+  }
+  if (k == 0) __syncthreads();
+  uu = sh.uu;
+  vv = sh.vv;
+  return cross;
+}
+
+// One ACA step of aca_step (aca.cpp:41-102) executed by one group.
 // sf < 0 disables the accuracy test (extension mode).  The candidate row
 // residual is built in V(:,k) and the column residual in U(:,k); both are
 // only committed (k += 1) when the step is accepted.
 template <class SRC>
-__device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
-                             double* __restrict__ V, int2* __restrict__ piv,
-                             uint8_t* __restrict__ Z, double sf, int lane, int& nq_acc,
-                             double* __restrict__ ebuf) {
+__device__ int aca_step(const SRC& src, Item& s, double* __restrict__ U,
+                        double* __restrict__ V, int2* __restrict__ piv,
+                        uint8_t* __restrict__ Z, double sf, const Grp& g, int& nq_acc,
+                        double* __restrict__ ebuf, AcaShared& sh) {
   const int m = s.m, n = s.n, k = s.k;
+  const int tid = g.tid, gs = g.size;
   for (;;) {
     if (s.nconsumed == m) return STOP_EXH;
     s.steps++;
@@ -569,17 +750,17 @@ __device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
     int i;
     if (k == 0) {
       int first = 0x7fffffff;
-      for (int r = lane; r < m; r += 32)
+      for (int r = tid; r < m; r += gs)
         if (!Z[r]) {
           first = r;
           break;
         }
-      i = warp_min_int(first);
+      i = grp_min_int(first, g, sh);
     } else {
       const double* ul = U + (long long)(k - 1) * m;
       double best = -1.0, aux = 0.0;
       int bi = -1;
-      for (int r = lane; r < m; r += 32) {
+      for (int r = tid; r < m; r += gs) {
         if (Z[r]) continue;
         const double mag = fabs(ul[r]);
         if (mag > best) {
@@ -587,7 +768,7 @@ __device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
           bi = r;
         }
       }
-      warp_argmax(best, bi, aux);
+      grp_argmax(best, bi, aux, g, sh);
       i = bi;
     }
     // --- row of the residual: v = A(i,:) - sum_l U(i,l) V(:,l), then the
@@ -603,26 +784,27 @@ __device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
       const bool is_row = pass == 0;
       const LineStats ls = residual_line(
           src, is_row, fix, is_row ? U : V, is_row ? m : n,
-          is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, lane);
+          is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, tid, gs);
       nq_acc += ls.nq;
       s.entries += is_row ? n : m;
       if (!is_row) {
-        uu = warp_sum(ls.sq);
+        if (!g.cta()) uu = warp_sum(ls.sq);
         break;
       }
-      const double row_scale = warp_max(ls.rs);
+      const double row_scale = grp_max(ls.rs, g, sh);
       double pm = ls.pm, pv = ls.pv;
       int pj = ls.pj;
-      warp_argmax(pm, pj, pv);
-      if (lane == 0) Z[i] = 1;
+      grp_argmax(pm, pj, pv, g, sh);
+      if (tid == 0) Z[i] = 1;
       s.nconsumed++;
-      __syncwarp();
+      gsync(g);
       if (pm <= 1e-14 * row_scale || row_scale == 0.0) {  // vanishing
         vanished = true;
         break;
       }
       j = pj;
-      for (int c = lane; c < n; c += 32) {
+      // thread t owns elements t mod gs of the line (as in residual_line)
+      for (int c = tid; c < n; c += gs) {
         const double t = vk[c] / pv;
         vk[c] = t;
         vv = fma(t, t, vv);
@@ -630,17 +812,22 @@ __device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
       fix = j;
     }
     if (vanished) continue;
-    vv = warp_sum(vv);
+    double cross = 0.0;
+    if (g.cta()) {
+      cross = cta_norms_cross(uk, U, m, vk, V, n, k, g, sh, uu, vv);
+    } else {
+      vv = warp_sum(vv);
+    }
     if (sf >= 0.0 && sqrt(uu) * sqrt(vv) <= sf * sqrt(fmax(s.frob_sq, 0.0))) {
-      __syncwarp();
+      gsync(g);
       return STOP_INEQ;
     }
     // ||S_k||^2 = ||S_{k-1}||^2 + 2 sum_l (u.u_l)(v.v_l) + ||u||^2 ||v||^2
-    const double cross = cross_terms(uk, U, m, vk, V, n, k, lane);
+    if (!g.cta()) cross = cross_terms(uk, U, m, vk, V, n, k, g.lane());
     s.frob_sq += 2.0 * cross + uu * vv;
-    if (lane == 0) piv[k] = make_int2(i, j);
+    if (tid == 0) piv[k] = make_int2(i, j);
     s.k = k + 1;
-    __syncwarp();
+    gsync(g);
     return STOP_NONE;
   }
 }
@@ -649,14 +836,13 @@ __device__ int aca_step_warp(const SRC& src, Item& s, double* __restrict__ U,
 //   PH_RUN  aca_run to the stopping rule (aca.cpp:106-124)
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
 //   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
-// One call site of the step for all phases (code size).
+// One call site of the step for all phases and both group modes (code size).
 template <class SRC>
-__device__ void aca_item_warp(const SRC& src, Item& s, Item* __restrict__ items, int idx,
-                              double* __restrict__ arena, int2* __restrict__ pivots,
-                              uint8_t* __restrict__ cons, double sf_run,
-                              long long max_rank, int lookahead,
-                              int* __restrict__ overflow, int lane,
-                              double* __restrict__ ebuf) {
+__device__ void aca_item(const SRC& src, Item& s, Item* __restrict__ items, int idx,
+                         double* __restrict__ arena, int2* __restrict__ pivots,
+                         uint8_t* __restrict__ cons, double sf_run, long long max_rank,
+                         int lookahead, int* __restrict__ overflow, const Grp& g,
+                         double* __restrict__ ebuf, AcaShared& sh) {
   double* U = arena + s.u_off;
   double* V = arena + s.v_off;
   int2* piv = pivots + s.p_off;
@@ -674,7 +860,7 @@ __device__ void aca_item_warp(const SRC& src, Item& s, Item* __restrict__ items,
         s.status = ST_OVERFLOW;
         break;
       }
-      st = aca_step_warp(src, s, U, V, piv, Z, run ? sf_run : -1.0, lane, nq_acc, ebuf);
+      st = aca_step(src, s, U, V, piv, Z, run ? sf_run : -1.0, g, nq_acc, ebuf, sh);
       if (st == STOP_NONE) {
         if (!run) s.steps_left--;
         continue;
@@ -700,39 +886,51 @@ __device__ void aca_item_warp(const SRC& src, Item& s, Item* __restrict__ items,
       }
     }
   }
-  __syncwarp();
-  {
-    long long t = nq_acc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    s.nq_sum += t;
-  }
-  if (lane == 0) {
+  gsync(g);
+  s.nq_sum += grp_sum_ll(nq_acc, g, sh);
+  if (g.tid == 0) {
     items[idx] = s;
     if (s.status == ST_OVERFLOW) atomicAdd(overflow, 1);
   }
 }
 
-// warps pull items from `list` (largest first) through a global counter
+// Persistent kernel.  list[0, nbig) (the largest items; the list is sorted
+// by m + n, largest first) is run CTA by CTA through counter[0]; then every
+// warp pulls single items from list[nbig, nlist) through counter[1].  One
+// call site of the item machine for both modes.
 template <int KIND, int MINB = 2>
-__global__ void __launch_bounds__(256, MINB)
-aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list,
-           int nlist, int* __restrict__ counter, double* __restrict__ arena,
+__global__ void __launch_bounds__(ACA_NT, MINB)
+aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list, int nlist,
+           int nbig, int* __restrict__ counter, double* __restrict__ arena,
            int2* __restrict__ pivots, uint8_t* __restrict__ cons, double sf_run,
            long long max_rank, int lookahead, int* __restrict__ overflow) {
-  __shared__ double ebuf_all[8][128];  // per-warp entry slots (residual_line)
-  const int lane = threadIdx.x & 31;
-  double* ebuf = ebuf_all[threadIdx.x >> 5];
+  __shared__ AcaShared sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool cta_mode = nbig > 0;
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(counter, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= nlist) return;
+    int t;
+    if (cta_mode) {
+      if (threadIdx.x == 0) sh.t = atomicAdd(counter, 1);
+      __syncthreads();
+      t = sh.t;
+      __syncthreads();
+      if (t >= nbig) {
+        cta_mode = false;
+        continue;
+      }
+    } else {
+      t = 0;
+      if (lane == 0) t = nbig + atomicAdd(counter + 1, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= nlist) return;
+    }
+    const Grp grp = cta_mode ? Grp{(int)threadIdx.x, ACA_NT} : Grp{lane, 32};
+    double* ebuf = cta_mode ? sh.ebuf : sh.ebuf + 128 * warp;
     const int idx = list[t];
     Item s = items[idx];
     const EvalSrc<KIND> src{g, s.row0, s.col0, s.comp};
-    aca_item_warp(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead,
-                  overflow, lane, ebuf);
+    aca_item(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead, overflow,
+             grp, ebuf, sh);
   }
 }
 
