@@ -485,6 +485,238 @@ struct Kelvin {
 };
 
 // ---------------------------------------------------------------------------
+// Galerkin pair quadrature (proj/src/quadrature.cpp:127-338) and the scalar
+// Galerkin kernels V_Delta, V_kl (proj/src/kernels.cpp:75-149), SURVEY.md 8f
+// rank 2.  PairCase numbering as quadrature.hpp:28.
+// component (r,c) of the symmetric 3x3 grids, row-major upper triangle
+static const int kCompR[6] = {0, 0, 0, 1, 1, 2};
+static const int kCompC[6] = {0, 1, 2, 1, 2, 2};
+enum PairCase { kDisjoint = 0, kVertex = 1, kEdge = 2, kIdentical = 3 };
+
+// classify_pair (quadrature.cpp:127-156): identical, shared edge traversed
+// in opposite directions, shared vertex, disjoint; rotations put the shared
+// simplex first.
+static int classify_pair(const std::array<int, 3>& a, const std::array<int, 3>& b,
+                         int& rot_a, int& rot_b) {
+  rot_a = rot_b = 0;
+  if (a == b) return kIdentical;
+  for (int rt = 0; rt < 3; ++rt)
+    for (int rs = 0; rs < 3; ++rs)
+      if (b[rs] == a[(rt + 1) % 3] && b[(rs + 1) % 3] == a[rt]) {
+        rot_a = rt;
+        rot_b = rs;
+        return kEdge;
+      }
+  for (int rt = 0; rt < 3; ++rt)
+    for (int rs = 0; rs < 3; ++rs)
+      if (a[rt] == b[rs]) {
+        rot_a = rt;
+        rot_b = rs;
+        return kVertex;
+      }
+  return kDisjoint;
+}
+// test_vertex_perm / trial_vertex_perm (quadrature.cpp:158-166)
+static std::array<int, 3> test_vertex_perm(int rot) {
+  return {rot, (rot + 1) % 3, (rot + 2) % 3};
+}
+static std::array<int, 3> trial_vertex_perm(int c, int rot) {
+  std::array<int, 3> p = {rot, (rot + 1) % 3, (rot + 2) % 3};
+  if (c == kEdge) std::swap(p[0], p[1]);
+  return p;
+}
+
+struct PairRule {
+  std::vector<Real> xr1, xr2, yr1, yr2, w;
+};
+
+// Sauter-Schwab maps [0,1]^4 -> pairs of reference coordinates
+// (quadrature.cpp:177-286), same expressions and association
+static void ss_map(int c, Real xi, Real e1, Real e2, Real e3, int s, Real* p) {
+  Real& x1 = p[0];
+  Real& x2 = p[1];
+  Real& y1 = p[2];
+  Real& y2 = p[3];
+  Real& jac = p[4];
+  if (c == kIdentical) {
+    jac = xi * xi * xi * e1 * e1 * e2;
+    switch (s) {
+      case 0: x1 = xi * e1 * (1 - e2); x2 = xi * (1 - e1 * (1 - e2));
+              y1 = xi * e1 * (1 - e2 * e3); y2 = xi * (1 - e1); break;
+      case 1: x1 = xi * e1 * (1 - e2 * e3); x2 = xi * (1 - e1);
+              y1 = xi * e1 * (1 - e2); y2 = xi * (1 - e1 * (1 - e2)); break;
+      case 2: x1 = xi * (1 - e1 * (1 - e2 * (1 - e3))); x2 = xi * e1 * (1 - e2 * (1 - e3));
+              y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2); break;
+      case 3: x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2);
+              y1 = xi * (1 - e1 * (1 - e2 * (1 - e3))); y2 = xi * e1 * (1 - e2 * (1 - e3)); break;
+      case 4: x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2 * e3);
+              y1 = xi * (1 - e1 * (1 - e2)); y2 = xi * e1 * (1 - e2); break;
+      default: x1 = xi * (1 - e1 * (1 - e2)); x2 = xi * e1 * (1 - e2);
+               y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2 * e3); break;
+    }
+  } else if (c == kEdge) {
+    jac = xi * xi * xi * e1 * e1;
+    switch (s) {
+      case 0: x1 = xi * (1 - e1 * e3); x2 = xi * e1 * e3;
+              y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2); break;
+      case 1: x1 = xi * (1 - e1); x2 = xi * e1;
+              y1 = xi * (1 - e1 * e2); y2 = xi * e1 * e2 * (1 - e3); jac *= e2; break;
+      case 2: x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2);
+              y1 = xi * (1 - e1 * e2 * e3); y2 = xi * e1 * e2 * e3; jac *= e2; break;
+      case 3: x1 = xi * (1 - e1 * e2); x2 = xi * e1 * e2 * (1 - e3);
+              y1 = xi * (1 - e1); y2 = xi * e1; jac *= e2; break;
+      default: x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2 * e3);
+               y1 = xi * (1 - e1 * e2); y2 = xi * e1 * e2; jac *= e2; break;
+    }
+  } else {
+    jac = xi * xi * xi * e2;
+    if (s == 0) {
+      x1 = xi * (1 - e1); x2 = xi * e1; y1 = xi * e2 * (1 - e3); y2 = xi * e2 * e3;
+    } else {
+      x1 = xi * e2 * (1 - e3); x2 = xi * e2 * e3; y1 = xi * (1 - e1); y2 = xi * e1;
+    }
+  }
+}
+
+// build_pair_rule (quadrature.cpp:290-336): disjoint = tensor product of
+// two triangle rules (test point outer); singular = simplices x n^4
+// Gauss-Legendre with the weight jac * w0 * w1 * w2 * w3 (left to right)
+static PairRule build_pair_rule(int c, int order) {
+  PairRule r;
+  if (c == kDisjoint) {
+    const Rule t = gauss_rule(order);
+    const size_t n = t.w.size();
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = 0; j < n; ++j) {
+        r.xr1.push_back(t.a[i]);
+        r.xr2.push_back(t.b[i]);
+        r.yr1.push_back(t.a[j]);
+        r.yr2.push_back(t.b[j]);
+        r.w.push_back(t.w[i] * t.w[j]);
+      }
+    return r;
+  }
+  const int ns = c == kIdentical ? 6 : c == kEdge ? 5 : 2;
+  std::vector<Real> gx, gw;
+  gauss_legendre_01(order, gx, gw);
+  const int n = order;
+  Real p[5];
+  for (int s = 0; s < ns; ++s)
+    for (int i0 = 0; i0 < n; ++i0)
+      for (int i1 = 0; i1 < n; ++i1)
+        for (int i2 = 0; i2 < n; ++i2)
+          for (int i3 = 0; i3 < n; ++i3) {
+            ss_map(c, gx[i0], gx[i1], gx[i2], gx[i3], s, p);
+            r.xr1.push_back(p[0]);
+            r.xr2.push_back(p[1]);
+            r.yr1.push_back(p[2]);
+            r.yr2.push_back(p[3]);
+            r.w.push_back(p[4] * gw[i0] * gw[i1] * gw[i2] * gw[i3]);
+          }
+  return r;
+}
+
+// Galerkin V_Delta / V_kl entries with QuadratureConfig defaults
+// (kernels.hpp:44-52: disjoint_order 4, singular_order 7, identical_bump 2,
+// far 4, mid 1.5, near 0.75).  Canonical evaluation order (parity contract
+// with the device, as for colloc_single): points by explicit fma from the
+// rotated corners, 1/|x-y| by rsqrt_canon, 1/(4 pi) and 4 area_i area_j
+// factored out of the pair sum.
+//   comp 0..5: V_kl for (k,l) = kCompR/kCompC (V_lk aliases V_kl,
+//              operators.cpp:226-233); comp 6: V_Delta
+struct Galerkin {
+  const Mesh* mesh = nullptr;
+  PairRule disjoint[7];  // by triangle-rule order (2, 4, 5 used)
+  PairRule singular[4];  // by PairCase (orders 7, 7, 9)
+  explicit Galerkin(const Mesh* m) : mesh(m) {
+    for (int o : {2, 4, 5}) disjoint[o] = build_pair_rule(kDisjoint, o);
+    singular[kVertex] = build_pair_rule(kVertex, 7);
+    singular[kEdge] = build_pair_rule(kEdge, 7);
+    singular[kIdentical] = build_pair_rule(kIdentical, 9);
+  }
+
+  // disjoint_order (kernels.cpp:75-85)
+  int disjoint_order(int ti, int tj) const {
+    const Real di = mesh->diam[ti], dj = mesh->diam[tj];
+    const Real dmax = std::max(di, dj);
+    const Real gap = norm3(sub(mesh->centroids[ti], mesh->centroids[tj])) - 0.5 * (di + dj);
+    if (gap >= 4.0 * dmax) return 2;
+    if (gap >= 1.5 * dmax) return 4;
+    if (gap >= 0.75 * dmax) return 4;
+    return 5;
+  }
+
+  const PairRule& rule_for(int ti, int tj, int& pc, int& rt, int& rs) const {
+    pc = classify_pair(mesh->triangles[ti], mesh->triangles[tj], rt, rs);
+    return pc == kDisjoint ? disjoint[disjoint_order(ti, tj)] : singular[pc];
+  }
+
+  // all seven components of one pair (integrate_pair, kernels.cpp:95-128):
+  // out7[0..5] = V_kl, out7[6] = V_Delta
+  void entry7(int i, int j, Real* out7) const {
+    if (i > j) std::swap(i, j);  // kernels.cpp:132-133, 141 (exact symmetry)
+    int pc, rt, rs;
+    const PairRule& r = rule_for(i, j, pc, rt, rs);
+    const auto xp = test_vertex_perm(rt);
+    const auto yp = trial_vertex_perm(pc, rs);
+    const Vec3 x0 = mesh->corner(i, xp[0]), x1 = mesh->corner(i, xp[1]),
+               x2 = mesh->corner(i, xp[2]);
+    const Vec3 y0 = mesh->corner(j, yp[0]), y1 = mesh->corner(j, yp[1]),
+               y2 = mesh->corner(j, yp[2]);
+    const Vec3 ex1 = sub(x1, x0), ex2 = sub(x2, x0), ey1 = sub(y1, y0), ey2 = sub(y2, y0);
+    Real ad = 0.0, akl[6] = {0, 0, 0, 0, 0, 0};
+    for (size_t q = 0; q < r.w.size(); ++q) {
+      const Real a1 = r.xr1[q], a2 = r.xr2[q], b1 = r.yr1[q], b2 = r.yr2[q];
+      Real d[3];
+      for (int c = 0; c < 3; ++c)
+        d[c] = std::fma(a2, ex2[c], std::fma(a1, ex1[c], x0[c])) -
+               std::fma(b2, ey2[c], std::fma(b1, ey1[c], y0[c]));
+      const Real ri = rsqrt_canon(std::fma(d[2], d[2], std::fma(d[1], d[1], d[0] * d[0])));
+      const Real wr = r.w[q] * ri;
+      const Real w3 = wr * ri * ri;
+      ad = ad + wr;
+      for (int k = 0; k < 6; ++k) akl[k] = std::fma(w3, d[kCompR[k]] * d[kCompC[k]], akl[k]);
+    }
+    const Real f = 4.0 * mesh->areas[i] * mesh->areas[j] * (1.0 / (4.0 * M_PI));
+    for (int k = 0; k < 6; ++k) out7[k] = f * akl[k];
+    out7[6] = f * ad;
+  }
+  Real entry(int i, int j, int comp) const {
+    Real o[7];
+    entry7(i, j, o);
+    return o[comp];
+  }
+  // the literal form of integrate_pair with the reference's integrand
+  // (acc += w f(x, y), 4 area area acc) -- checks the canonical order only
+  Real entry_literal(int i, int j, int comp) const {
+    if (i > j) std::swap(i, j);
+    int pc, rt, rs;
+    const PairRule& r = rule_for(i, j, pc, rt, rs);
+    const auto xp = test_vertex_perm(rt);
+    const auto yp = trial_vertex_perm(pc, rs);
+    Vec3 X[3], Y[3];
+    for (int v = 0; v < 3; ++v) {
+      X[v] = mesh->corner(i, xp[v]);
+      Y[v] = mesh->corner(j, yp[v]);
+    }
+    Real acc = 0.0;
+    for (size_t q = 0; q < r.w.size(); ++q) {
+      Vec3 x, y;
+      for (int c = 0; c < 3; ++c) {
+        x[c] = X[0][c] + r.xr1[q] * (X[1][c] - X[0][c]) + r.xr2[q] * (X[2][c] - X[0][c]);
+        y[c] = Y[0][c] + r.yr1[q] * (Y[1][c] - Y[0][c]) + r.yr2[q] * (Y[2][c] - Y[0][c]);
+      }
+      const Vec3 d = sub(x, y);
+      const Real rr = norm3(d);
+      const Real f = comp == 6 ? 1.0 / (4.0 * M_PI * rr)
+                               : d[kCompR[comp]] * d[kCompC[comp]] / (4.0 * M_PI * rr * rr * rr);
+      acc += r.w[q] * f;
+    }
+    return 4.0 * mesh->areas[i] * mesh->areas[j] * acc;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // Entry oracles (proj/include/hmbem/aca.hpp:15-44)
 struct EntryOracle {
   virtual ~EntryOracle() = default;
@@ -520,6 +752,17 @@ struct KelvinComponentOracle : EntryOracle {
   long cols() const override { return k->mesh->nt(); }
   Real entry(long i, long j) const override {
     return k->entry(static_cast<int>(i), static_cast<int>(j), r, c);
+  }
+};
+
+// KernelOracle over V_kl (comp 0..5) or V_Delta (comp 6) (kernels.hpp:95-105)
+struct GalerkinComponentOracle : EntryOracle {
+  const Galerkin* g;
+  int comp;
+  long rows() const override { return g->mesh->nt(); }
+  long cols() const override { return g->mesh->nt(); }
+  Real entry(long i, long j) const override {
+    return g->entry(static_cast<int>(i), static_cast<int>(j), comp);
   }
 };
 
@@ -1111,8 +1354,6 @@ static std::unique_ptr<HMatrix> assemble(const Partition* p,
 // 3x3 Kelvin block grid: six component H-matrices over one partition, the
 // (c,r) cell aliasing (r,c) (proj/src/baca.cpp:669-687), matvec through the
 // BlockGrid case of matvec (proj/src/expr.cpp:197-215).
-static const int kCompR[6] = {0, 0, 0, 1, 1, 2};
-static const int kCompC[6] = {0, 1, 2, 1, 2, 2};
 static int comp_index(int r, int c) {
   const int lo = std::min(r, c), hi = std::max(r, c);
   static const int idx[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
@@ -1406,11 +1647,13 @@ struct Problem {
   Mesh mesh;
   Material mat;
   std::unique_ptr<Kelvin> kelvin;
+  std::unique_ptr<Galerkin> galerkin;
   std::vector<std::unique_ptr<EntryOracle>> oracles;
   Tree rows_tree, cols_tree;
   std::unique_ptr<Partition> part;
   Grid grid;
-  int kind = 0;  // 0 Kelvin centroid collocation, 1 Newton points, 2 dense
+  int kind = 0;  // 0 Kelvin centroid collocation, 1 Newton points, 2 dense,
+                 // 3 Galerkin V_kl grid, 4 Galerkin V_Delta
   long n = 0;
   double t_assemble = 0.0;
   long entries_counted = 0;
@@ -1573,6 +1816,74 @@ int or_problem_kelvin(int nv, const double* verts, int nt, const int* tris,
   });
 }
 
+// kinds 3 / 4: Galerkin scalar kernels on the triangle partition of
+// assemble_operators (operators.cpp:186-200, corner boxes, one tree):
+// which = 0 -> the six V_kl as a symmetric 3x3 grid, 1 -> V_Delta alone.
+int or_problem_galerkin(int nv, const double* verts, int nt, const int* tris, int which,
+                        int b_min, double eta, void** out) {
+  return guard([&] {
+    auto p = std::make_unique<Problem>();
+    p->kind = which == 0 ? 3 : 4;
+    p->mesh.vertices.resize(nv);
+    for (int v = 0; v < nv; ++v)
+      p->mesh.vertices[v] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]};
+    p->mesh.triangles.resize(nt);
+    for (int t = 0; t < nt; ++t)
+      p->mesh.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    finish_geometry(p->mesh);
+    p->galerkin = std::make_unique<Galerkin>(&p->mesh);
+    p->n = nt;
+    std::vector<Box> boxes(nt);
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k) boxes[t].absorb(p->mesh.corner(t, k));
+    p->rows_tree = build_cluster_tree(boxes, b_min);
+    p->part = std::make_unique<Partition>(
+        build_block_partition(&p->rows_tree, &p->rows_tree, eta));
+    const int nc = which == 0 ? 6 : 1;
+    for (int c = 0; c < nc; ++c) {
+      auto o = std::make_unique<GalerkinComponentOracle>();
+      o->g = p->galerkin.get();
+      o->comp = which == 0 ? c : 6;
+      p->oracles.push_back(std::move(o));
+    }
+    p->grid.ncomp = nc;
+    p->grid.nblk = nt;
+    *out = p.release();
+  });
+}
+
+// pair_rule(case, order) tables (quadrature.cpp:290-338); NULL arrays query n
+int or_pair_rule(int pc, int order, int* n, double* xr1, double* xr2, double* yr1,
+                 double* yr2, double* w) {
+  return guard([&] {
+    const PairRule r = build_pair_rule(pc, order);
+    *n = static_cast<int>(r.w.size());
+    if (!w) return;
+    for (size_t q = 0; q < r.w.size(); ++q) {
+      xr1[q] = r.xr1[q];
+      xr2[q] = r.xr2[q];
+      yr1[q] = r.yr1[q];
+      yr2[q] = r.yr2[q];
+      w[q] = r.w[q];
+    }
+  });
+}
+
+// classify_pair + vertex permutations (quadrature.cpp:127-166)
+int or_classify_pair(const int* a3, const int* b3, int* rot_a, int* rot_b, int* perm_a,
+                     int* perm_b) {
+  return guard([&] {
+    const std::array<int, 3> a = {a3[0], a3[1], a3[2]}, b = {b3[0], b3[1], b3[2]};
+    const int c = classify_pair(a, b, *rot_a, *rot_b);
+    const auto pa = test_vertex_perm(*rot_a), pb = trial_vertex_perm(c, *rot_b);
+    for (int k = 0; k < 3; ++k) {
+      perm_a[k] = pa[k];
+      perm_b[k] = pb[k];
+    }
+    *rot_a = c * 16 + *rot_a;  // case in the high bits
+  });
+}
+
 // kind 1: Newton kernel over points with point boxes or explicit boxes.
 // boxes6 == nullptr => point boxes.
 int or_problem_newton(int n, const double* pts, const double* boxes6,
@@ -1709,7 +2020,12 @@ int or_partition_json(void* h, char* buf, long* len) {
 int or_entry_literal(void* h, int comp, long i, long j, double* out) {
   return guard([&] {
     Problem* p = P(h);
-    if (p->kind != 0) throw Error("kelvin only");
+    if (p->kind == 3 || p->kind == 4) {
+      *out = p->galerkin->entry_literal(static_cast<int>(i), static_cast<int>(j),
+                                        p->kind == 4 ? 6 : comp);
+      return;
+    }
+    if (p->kind != 0) throw Error("kelvin or galerkin only");
     *out = p->kelvin->colloc_single_literal(p->mesh.centroids[i], kCompR[comp],
                                             kCompC[comp], static_cast<int>(j));
   });

@@ -126,6 +126,26 @@ def self_term_i1(v9, p) -> float:
     return out.value
 
 
+def pair_rule(case: int, order: int):
+    """pair_rule(PairCase, order) (quadrature.cpp:290-338); case 0 disjoint,
+    1 vertex, 2 edge, 3 identical.  Returns xr1, xr2, yr1, yr2, w."""
+    n = C.c_int()
+    _ck(lib().or_pair_rule(case, order, C.byref(n), None, None, None, None, None))
+    arr = [np.zeros(n.value) for _ in range(5)]
+    _ck(lib().or_pair_rule(case, order, C.byref(n), *[_p(a) for a in arr]))
+    return tuple(arr)
+
+
+def classify_pair(a, b):
+    """classify_pair + test/trial vertex perms (quadrature.cpp:127-166)."""
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    b = np.ascontiguousarray(b, dtype=np.int32)
+    ra, rb = C.c_int(), C.c_int()
+    pa, pb = np.zeros(3, np.int32), np.zeros(3, np.int32)
+    _ck(lib().or_classify_pair(_p(a), _p(b), C.byref(ra), C.byref(rb), _p(pa), _p(pb)))
+    return ra.value >> 4, ra.value & 15, rb.value, pa, pb
+
+
 def admissible(box_a, box_b, eta) -> bool:
     a = np.ascontiguousarray(box_a, dtype=np.float64).reshape(6)
     b = np.ascontiguousarray(box_b, dtype=np.float64).reshape(6)
@@ -156,6 +176,17 @@ class Problem:
         _ck(lib().or_problem_kelvin(len(v), _p(v), len(t), _p(t), D(E), D(nu), b_min,
                                     D(eta), C.byref(h)))
         return cls(h, 6, len(t))
+
+    @classmethod
+    def galerkin(cls, verts, tris, which=0, b_min=32, eta=1.0):
+        """Galerkin scalar kernels on the triangle partition: which = 0 the
+        six V_kl as the symmetric 3x3 grid, 1 V_Delta (kernels.cpp:130-149)."""
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32)
+        h = C.c_void_p()
+        _ck(lib().or_problem_galerkin(len(v), _p(v), len(t), _p(t), int(which), b_min,
+                                      D(eta), C.byref(h)))
+        return cls(h, 6 if which == 0 else 1, len(t))
 
     @classmethod
     def newton(cls, pts, boxes=None, diag=2.0, b_min=10, eta=0.8):
@@ -222,7 +253,8 @@ class Problem:
         return out
 
     def dense_grid(self) -> np.ndarray:
-        """Full 3N x 3N Kelvin collocation matrix, component-major."""
+        """Full 3N x 3N matrix of the 6-component grid (Kelvin collocation or
+        the Galerkin V_kl grid), component-major."""
         if self.ncomp == 1:
             return self.dense(0)
         n = self.n

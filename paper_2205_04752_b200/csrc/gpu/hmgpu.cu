@@ -737,7 +737,7 @@ void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>&
 int aca_cta_min() {
   static const int v = [] {
     const char* e = std::getenv("HMGPU_ACA_CTA_MIN");
-    return e ? std::atoi(e) : 2048;
+    return e ? std::atoi(e) : 1024;
   }();
   return v;
 }
@@ -762,9 +762,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
             c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
             c->d_overflow.p);
       };
-      static const bool occ3 = std::getenv("HMGPU_ACA_OCC3") != nullptr;
-      if (c->kind == KIND_KELVIN && occ3) go(aca_kernel<KIND_KELVIN, 3>);
-      else if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
+      if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
       else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
       else go(aca_kernel<KIND_DENSE>);
     });

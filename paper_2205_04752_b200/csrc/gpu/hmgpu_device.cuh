@@ -423,13 +423,13 @@ struct EvalSrc {
   }
 };
 
-template <class SRC>
+template <int NT, class SRC>
 __device__ __forceinline__ LineStats residual_line(const SRC& src, bool is_row, int fix,
                                                    const double* __restrict__ W, int ldw,
                                                    const double* __restrict__ X, int ldx,
                                                    int len, int k, double* __restrict__ out,
-                                                   double* __restrict__ ebuf, int lane,
-                                                   int nt) {
+                                                   double* __restrict__ ebuf, int lane) {
+  constexpr int nt = NT;
   // nt threads (one warp, or the CTA for the largest items); element t is
   // handled by thread t % nt, the lane-strided order of the canonical sums
   LineStats st{0.0, -1.0, 0.0, 0.0, -1, 0};
@@ -568,11 +568,16 @@ __device__ __forceinline__ double cross_terms(const double* __restrict__ uk,
 // (gsize ACA_NT, gtid = threadIdx.x): a single warp on a block with m + n in
 // the thousands was latency-bound on its panel loads and made the largest
 // items the critical path of the assembly (config 3: 196 ms for the 192
-// items with m + n >= 16384 run alone).  Both modes give the same bits: the
+// items with m + n >= 16384 run alone).  CTA of 128 threads, items with
+// m + n >= 1024 (HMGPU_ACA_CTA_MIN; measured against 256 / 512 threads and
+// 512 / 2048 / 4096).  Both modes give the same bits: the
 // max / arg-max reductions are exact, and the CTA mode forms the canonical
 // lane-strided sums (||u||^2, ||v||^2, u.U(:,l), v.V(:,l)) with one warp per
 // sum from the stored line, in the warp mode's order.
-constexpr int ACA_NT = 256;
+#ifndef HMGPU_ACA_NT
+#define HMGPU_ACA_NT 128
+#endif
+constexpr int ACA_NT = HMGPU_ACA_NT;
 constexpr int ACA_NW = ACA_NT / 32;
 
 struct AcaShared {
@@ -585,21 +590,23 @@ struct AcaShared {
   int t;
 };
 
+template <int NT>
 struct Grp {
-  int tid, size;
-  __device__ __forceinline__ bool cta() const { return size > 32; }
+  int tid;
+  static constexpr int size = NT;
+  __host__ __device__ static constexpr bool cta() { return NT > 32; }
   __device__ __forceinline__ int lane() const { return tid & 31; }
   __device__ __forceinline__ int warp() const { return tid >> 5; }
 };
 
-__device__ __forceinline__ void gsync(const Grp& g) {
+template <int NT>
+__device__ __forceinline__ void gsync(const Grp<NT>& g) {
   if (g.cta()) __syncthreads();
   else __syncwarp();
 }
 
-__device__ __forceinline__ double grp_max(double v, const Grp& g, AcaShared& sh) {
-  v = warp_max(v);
-  if (!g.cta()) return v;
+template <int NT>
+__device__ __forceinline__ double cta_max(double v, const Grp<NT>& g, AcaShared& sh) {
   if (g.lane() == 0) sh.rd[g.warp()] = v;
   __syncthreads();
   double r = sh.rd[0];
@@ -608,10 +615,14 @@ __device__ __forceinline__ double grp_max(double v, const Grp& g, AcaShared& sh)
   __syncthreads();
   return r;
 }
+template <int NT>
+__device__ __forceinline__ double grp_max(double v, const Grp<NT>& g, AcaShared& sh) {
+  v = warp_max(v);
+  return g.cta() ? cta_max(v, g, sh) : v;
+}
 
-__device__ __forceinline__ int grp_min_int(int v, const Grp& g, AcaShared& sh) {
-  v = warp_min_int(v);
-  if (!g.cta()) return v;
+template <int NT>
+__device__ __forceinline__ int cta_min_int(int v, const Grp<NT>& g, AcaShared& sh) {
   if (g.lane() == 0) sh.ri[g.warp()] = v;
   __syncthreads();
   int r = sh.ri[0];
@@ -620,8 +631,14 @@ __device__ __forceinline__ int grp_min_int(int v, const Grp& g, AcaShared& sh) {
   __syncthreads();
   return r;
 }
+template <int NT>
+__device__ __forceinline__ int grp_min_int(int v, const Grp<NT>& g, AcaShared& sh) {
+  v = warp_min_int(v);
+  return g.cta() ? cta_min_int(v, g, sh) : v;
+}
 
-__device__ __forceinline__ long long grp_sum_ll(long long t, const Grp& g, AcaShared& sh) {
+template <int NT>
+__device__ __forceinline__ long long grp_sum_ll(long long t, const Grp<NT>& g, AcaShared& sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (!g.cta()) return t;
@@ -635,10 +652,9 @@ __device__ __forceinline__ long long grp_sum_ll(long long t, const Grp& g, AcaSh
 }
 
 // first-max arg-max over the group (larger value, then smaller index)
-__device__ __forceinline__ void grp_argmax(double& val, int& idx, double& aux, const Grp& g,
-                                           AcaShared& sh) {
-  warp_argmax(val, idx, aux);
-  if (!g.cta()) return;
+template <int NT>
+__device__ __forceinline__ void cta_argmax(double& val, int& idx, double& aux, const Grp<NT>& g,
+                                        AcaShared& sh) {
   if (g.lane() == 0) {
     sh.rd[g.warp()] = val;
     sh.ri[g.warp()] = idx;
@@ -662,6 +678,12 @@ __device__ __forceinline__ void grp_argmax(double& val, int& idx, double& aux, c
   idx = bi;
   aux = ba;
 }
+template <int NT>
+__device__ __forceinline__ void grp_argmax(double& val, int& idx, double& aux, const Grp<NT>& g,
+                                           AcaShared& sh) {
+  warp_argmax(val, idx, aux);
+  if (g.cta()) cta_argmax(val, idx, aux, g, sh);
+}
 
 // canonical lane-strided dot (warp order, as warp_sum of fma partials)
 __device__ __forceinline__ double warp_dot(const double* __restrict__ a,
@@ -674,9 +696,10 @@ __device__ __forceinline__ double warp_dot(const double* __restrict__ a,
 // CTA mode: ||u||^2 and ||v||^2 (warps 0 and 1) and the dots u.U(:,l),
 // v.V(:,l) of the cross terms (l spread over the warps), each a canonical
 // warp-order sum of the stored line; cross = sum_l du_l dv_l in l order.
-__device__ double cta_norms_cross(const double* __restrict__ uk, const double* __restrict__ U,
+template <int NT>
+__device__ __forceinline__ double cta_norms_cross(const double* __restrict__ uk, const double* __restrict__ U,
                                   int m, const double* __restrict__ vk,
-                                  const double* __restrict__ V, int n, int k, const Grp& g,
+                                  const double* __restrict__ V, int n, int k, const Grp<NT>& g,
                                   AcaShared& sh, double& uu, double& vv) {
   const int lane = g.lane(), w = g.warp();
   __syncthreads();  // the line is complete
@@ -736,13 +759,14 @@ __device__ double cta_norms_cross(const double* __restrict__ uk, const double* _
 // sf < 0 disables the accuracy test (extension mode).  The candidate row
 // residual is built in V(:,k) and the column residual in U(:,k); both are
 // only committed (k += 1) when the step is accepted.
-template <class SRC>
-__device__ int aca_step(const SRC& src, Item& s, double* __restrict__ U,
+template <int NT, class SRC>
+__device__ __forceinline__ int aca_step(const SRC& src, Item& s, double* __restrict__ U,
                         double* __restrict__ V, int2* __restrict__ piv,
-                        uint8_t* __restrict__ Z, double sf, const Grp& g, int& nq_acc,
+                        uint8_t* __restrict__ Z, double sf, const Grp<NT>& g, int& nq_acc,
                         double* __restrict__ ebuf, AcaShared& sh) {
   const int m = s.m, n = s.n, k = s.k;
-  const int tid = g.tid, gs = g.size;
+  const int tid = g.tid;
+  constexpr int gs = NT;
   for (;;) {
     if (s.nconsumed == m) return STOP_EXH;
     s.steps++;
@@ -782,9 +806,9 @@ __device__ int aca_step(const SRC& src, Item& s, double* __restrict__ U,
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
       const bool is_row = pass == 0;
-      const LineStats ls = residual_line(
+      const LineStats ls = residual_line<NT>(
           src, is_row, fix, is_row ? U : V, is_row ? m : n,
-          is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, tid, gs);
+          is_row ? V : U, is_row ? n : m, is_row ? n : m, k, is_row ? vk : uk, ebuf, tid);
       nq_acc += ls.nq;
       s.entries += is_row ? n : m;
       if (!is_row) {
@@ -837,11 +861,11 @@ __device__ int aca_step(const SRC& src, Item& s, double* __restrict__ U,
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
 //   PH_EXT  aca_extend(steps_left) (aca.cpp:126-143)
 // One call site of the step for all phases and both group modes (code size).
-template <class SRC>
-__device__ void aca_item(const SRC& src, Item& s, Item* __restrict__ items, int idx,
+template <int NT, class SRC>
+__device__ __forceinline__ void aca_item(const SRC& src, Item& s, Item* __restrict__ items, int idx,
                          double* __restrict__ arena, int2* __restrict__ pivots,
                          uint8_t* __restrict__ cons, double sf_run, long long max_rank,
-                         int lookahead, int* __restrict__ overflow, const Grp& g,
+                         int lookahead, int* __restrict__ overflow, const Grp<NT>& g,
                          double* __restrict__ ebuf, AcaShared& sh) {
   double* U = arena + s.u_off;
   double* V = arena + s.v_off;
@@ -897,8 +921,8 @@ __device__ void aca_item(const SRC& src, Item& s, Item* __restrict__ items, int 
 // Persistent kernel.  list[0, nbig) (the largest items; the list is sorted
 // by m + n, largest first) is run CTA by CTA through counter[0]; then every
 // warp pulls single items from list[nbig, nlist) through counter[1].  One
-// call site of the item machine for both modes.
-template <int KIND, int MINB = 2>
+// item machine instance per mode.
+template <int KIND, int MINB = 512 / ACA_NT>
 __global__ void __launch_bounds__(ACA_NT, MINB)
 aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list, int nlist,
            int nbig, int* __restrict__ counter, double* __restrict__ arena,
@@ -924,13 +948,17 @@ aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list, int n
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= nlist) return;
     }
-    const Grp grp = cta_mode ? Grp{(int)threadIdx.x, ACA_NT} : Grp{lane, 32};
-    double* ebuf = cta_mode ? sh.ebuf : sh.ebuf + 128 * warp;
     const int idx = list[t];
     Item s = items[idx];
     const EvalSrc<KIND> src{g, s.row0, s.col0, s.comp};
-    aca_item(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead, overflow,
-             grp, ebuf, sh);
+    // the group size is a compile-time constant of each instance (a runtime
+    // stride cost the warp mode 13 % on config 2)
+    if (cta_mode)
+      aca_item(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead, overflow,
+               Grp<ACA_NT>{(int)threadIdx.x}, sh.ebuf, sh);
+    else
+      aca_item(src, s, items, idx, arena, pivots, cons, sf_run, max_rank, lookahead, overflow,
+               Grp<32>{lane}, sh.ebuf + 128 * warp, sh);  // [4][32] per warp
   }
 }
 

@@ -14,11 +14,20 @@ elif cfg == "c1":
 else:
     mesh, bmin, eps = hm.Mesh.voxel_cube(128, 0.0, 1.0), 64, 1e-5
 h = hm.HMatrix.kelvin(mesh, b_min=bmin, eta=1.0, device=0)
+ts, ka = [], []
+h.set_profiling(True)
 for r in range(reps):
     t = time.perf_counter()
+    h.kernel_times("aca", reset=True)
     st = h.assemble(eps=eps, beta=0.8)
+    ka.append(h.kernel_times("aca", reset=True)[0])
+    ts.append(st.ms_total)
     print(f"{cfg} run {r}: wall {1e3*(time.perf_counter()-t):.1f} ms  ms={st.ms_total:.2f} "
           f"near={st.ms_nearfield:.3f} entries={st.aca_entries}", flush=True)
+w = sorted(ts[1:] or ts)
+k = sorted(ka[1:] or ka)
+print(f"{cfg} summary: min {w[0]:.2f} median {w[len(w)//2]:.2f} ms (warm runs); "
+      f"aca kernel min {k[0]:.2f} median {k[len(k)//2]:.2f} ms", flush=True)
 x = np.random.default_rng(1).uniform(-1, 1, h.cols)
 y = h.matvec(x)
 print(cfg, "digest", hashlib.sha1(np.ascontiguousarray(y).tobytes()).hexdigest()[:16],

@@ -31,3 +31,10 @@ def separated_kernel_matrix(m, n, seed, rv):
             d = x[i] - y[j]
             a[i, j] = 1.0 / np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2])
     return a, x, y
+
+
+def doctest_approx(got: float, want: float, eps: float) -> bool:
+    """doctest::Approx(want).epsilon(eps) == got: |got - want| <
+    eps * (scale + max(|got|, |want|)) with the default scale 1 (the
+    comparison the reference's test suite uses)."""
+    return abs(got - want) < eps * (1.0 + max(abs(got), abs(want)))
