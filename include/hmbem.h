@@ -8,6 +8,8 @@
  *                       proj/tools/meshgen.cpp:27-83)
  *   hmb_op_kelvin       evaluate_interior's 3x3 grid of CollocSingleOracle
  *                       H-matrices at triangle centroids (baca.cpp:645-687)
+ *   hmb_op_galerkin     GalerkinKernels V_kl grid / V_Delta KernelOracle
+ *                       H-matrices (kernels.cpp:95-149, operators.cpp:218-235)
  *   hmb_op_newton/dense test fixtures (test_hmatrix.cpp:12-53, aca.hpp:34-44)
  *   hmb_tree_*, hmb_partition_*   ClusterTree / BlockPartition /
  *                       sparsity_constant / partition_to_json (cluster.hpp)
@@ -73,6 +75,11 @@ int hmb_admissible(const double* box_a6, const double* box_b6, double eta, int* 
 /* ---- operators (device < 0: host-only, tree and partition) ---- */
 int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
                   int device, int shard_rank, int shard_count, hmb_op** out);
+/* Galerkin scalar kernels on the triangle partition (assemble_operators,
+ * operators.cpp:186-235): which = 0 -> the six V_kl as the 3x3 grid,
+ * 1 -> V_Delta (kernels.cpp:130-149) */
+int hmb_op_galerkin(const hmb_mesh* m, int which, int b_min, double eta, int device,
+                    int shard_rank, int shard_count, hmb_op** out);
 int hmb_op_newton(int n, const double* pts, const double* boxes6, double diag,
                   int b_min, double eta, int device, hmb_op** out);
 int hmb_op_dense(int m, int n, const double* a_colmajor, const double* row_pts,

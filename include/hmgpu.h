@@ -12,6 +12,12 @@
  *                               proj/src/kernels.cpp:21-28,87-93,176-187),
  *                              fused into the kernels instead of a callback
  *   hmgpu_set_rule             gauss_rule(order) tables (proj/src/quadrature.cpp:55-95)
+ *   hmgpu_set_galerkin_geometry  KernelOracle over V_Delta / V_kl: GalerkinKernels::
+ *                              vdelta / vkl / integrate_pair / disjoint_order
+ *                              (proj/include/hmbem/kernels.hpp:95-105,
+ *                               proj/src/kernels.cpp:75-149), fused into the kernels
+ *   hmgpu_set_pair_rule        pair_rule(PairCase, order) Sauter-Schwab tables
+ *                              (proj/src/quadrature.cpp:290-338)
  *   hmgpu_set_points           test fixtures CentroidKernelOracle / PointKernelOracle
  *                              (proj/tests/test_hmatrix.cpp:12-28, test_amvm.cpp:9-22)
  *   hmgpu_set_dense_matrix     DenseOracle (proj/include/hmbem/aca.hpp:34-44)
@@ -119,6 +125,22 @@ int hmgpu_set_kelvin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
                               int n_tri, const int* tris,
                               const double* centroid, const double* area,
                               const double* diam, double E, double nu);
+/* Galerkin scalar kernels on the triangle x triangle partition of
+ * assemble_operators (operators.cpp:186-200): which = 0 -> the six V_kl as
+ * the symmetric 3x3 grid (components (k,l) = 00 01 02 11 12 22; V_lk
+ * aliases V_kl, operators.cpp:226-233), which = 1 -> V_Delta (one
+ * component).  Arrays as hmgpu_set_kelvin_geometry.  Disjoint pairs use the
+ * rule tiers of hmgpu_set_rule (0: order 2, 1: order 4, 2: order 5); touching
+ * pairs the tables of hmgpu_set_pair_rule. */
+int hmgpu_set_galerkin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
+                                int n_tri, const int* tris, const double* centroid,
+                                const double* area, const double* diam, int which);
+/* singular pair rule of PairCase pair_case (1 vertex, 2 edge, 3 identical):
+ * n points, reference coordinates on the rotated test (xr) and trial (yr)
+ * triangles and weights (PairRule, quadrature.hpp:44-52) */
+int hmgpu_set_pair_rule(hmgpu_ctx* ctx, int pair_case, int n, const double* xr1,
+                        const double* xr2, const double* yr1, const double* yr2,
+                        const double* w);
 /* scalar Newton kernel 1/|x_i - x_j| with entry `diag` where x_i == x_j */
 int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag);
 /* scalar explicit matrix, column-major m x n, external ids */

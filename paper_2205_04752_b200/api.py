@@ -276,6 +276,18 @@ class HMatrix:
         return cls(out)
 
     @classmethod
+    def galerkin(cls, mesh: Mesh, which: int = 0, b_min: int = 32, eta: float = 1.0,
+                 device: int = 0, shard: tuple = (0, 1)) -> "HMatrix":
+        """Galerkin scalar kernels over triangle pairs (GalerkinKernels,
+        kernels.cpp:95-149) on the triangle partition of assemble_operators
+        (operators.cpp:186-235): which = 0 -> the six V_kl as the symmetric
+        3x3 grid (3 N_t dofs), 1 -> V_Delta (N_t dofs)."""
+        out = C.c_void_p()
+        _check(_h.hmb_op_galerkin(mesh._h, int(which), b_min, eta, device, shard[0],
+                                  shard[1], C.byref(out)))
+        return cls(out)
+
+    @classmethod
     def newton(cls, points, boxes=None, diag: float = 2.0, b_min: int = 10,
                eta: float = 0.8, device: int = 0) -> "HMatrix":
         p = _f64(points).reshape(-1, 3)
@@ -497,6 +509,46 @@ class HMatrix:
 
 
 # ---- reference-style free functions ----------------------------------------
+class LameSingleLayer:
+    """V_h = (1+nu) / (2E (1-nu)) [ (3-4nu) diag3(V_Delta) + grid(V_kl) ]
+    (compose_Vh, proj/src/operators.cpp:97-105): the Galerkin single-layer
+    operator of the Lame equations from the two GPU H-matrices (the V_kl
+    grid and V_Delta, assembled with one partition), 3 N_t dofs
+    component-major."""
+
+    def __init__(self, mesh: Mesh, E: float = 1.0, nu: float = 0.3, b_min: int = 32,
+                 eta: float = 1.0, device: int = 0, shard: tuple = (0, 1)):
+        if E <= 0.0:
+            raise Error("lame_constants: E must be positive")
+        if not 0.0 < nu < 0.5:
+            raise Error("lame_constants: nu must lie in (0, 1/2)")
+        self.E, self.nu = E, nu
+        self.vkl = HMatrix.galerkin(mesh, 0, b_min, eta, device, shard)
+        self.vdelta = HMatrix.galerkin(mesh, 1, b_min, eta, device, shard)
+        self.nt = self.vdelta.rows
+
+    @property
+    def rows(self) -> int:
+        return 3 * self.nt
+
+    @property
+    def cols(self) -> int:
+        return 3 * self.nt
+
+    def assemble(self, cfg: Optional[AssemblyConfig] = None, **kw):
+        return self.vkl.assemble(cfg, **kw), self.vdelta.assemble(cfg, **kw)
+
+    def matvec(self, x, mode: Mode = Mode.Current) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.cols,):
+            raise DimensionError("V_h matvec: size")
+        s = 0.5 / self.E * (1.0 + self.nu) / (1.0 - self.nu)
+        yg = self.vkl.matvec(x, mode)
+        # diag3(V_Delta): the three component blocks as three right-hand sides
+        yd = self.vdelta.matvec(x.reshape(3, self.nt).T, mode).T.reshape(-1)
+        return s * ((3.0 - 4.0 * self.nu) * yd + yg)
+
+
 def random_vector(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
     """Seeded synthetic input: mt19937_64 + uniform [-1,1) (the reference's
     random_vector) or standard normal."""

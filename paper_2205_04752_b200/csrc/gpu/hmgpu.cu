@@ -362,6 +362,9 @@ struct hmgpu_ctx {
   double E = 1.0, nu = 0.3, diag = 2.0;
   RuleTable rules{};
   bool rules_set[3] = {false, false, false};
+  int gal_which = 0;                   // galerkin: 0 V_kl grid, 1 V_Delta
+  std::vector<double> prule[4];        // galerkin singular pair rules, SoA per case
+  int prule_n[4] = {0, 0, 0, 0};
 
   // ---- partition ----
   bool have_partition = false;
@@ -375,7 +378,9 @@ struct hmgpu_ctx {
 
   // ---- device geometry ----
   DBuf<double4> d_rowpt, d_colpt;
-  DBuf<double> d_tri, d_A;
+  DBuf<double> d_tri, d_A, d_prule;
+  DBuf<double4> d_vtx;
+  DBuf<int4> d_tvid;
   DBuf<int> d_rperm, d_cperm;
   Geom geom{};
 
@@ -600,9 +605,9 @@ void build_geometry(hmgpu_ctx* c) {
   c->d_cperm.upload(c->cperm, c->stream);
   g.rperm = c->d_rperm.p;
   g.cperm = c->d_cperm.p;
-  if (c->kind == KIND_KELVIN) {
+  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) {
     if (c->n_tri != c->n_rows || c->n_tri != c->n_cols)
-      fail(HMGPU_ERR_DIMENSION, "kelvin geometry does not match the partition");
+      fail(HMGPU_ERR_DIMENSION, "triangle geometry does not match the partition");
     std::vector<double4> rp(c->n_rows);
     for (int i = 0; i < c->n_rows; ++i) {
       const int t = c->rperm[i];
@@ -634,6 +639,38 @@ void build_geometry(hmgpu_ctx* c) {
     // c = (1+nu) / (8 pi E (1-nu)) in the reference's evaluation order
     g.cst = (1.0 + c->nu) / (8.0 * M_PI * c->E * (1.0 - c->nu));
     g.c34 = 3.0 - 4.0 * c->nu;
+    if (c->kind == KIND_GALERKIN) {
+      if (!c->same_tree) fail(HMGPU_ERR_DIMENSION, "galerkin needs one triangle tree");
+      std::vector<double4> vx(c->n_vert);
+      for (int v = 0; v < c->n_vert; ++v)
+        vx[v] = make_double4(c->verts[3LL * v], c->verts[3LL * v + 1], c->verts[3LL * v + 2], 0);
+      std::vector<int4> tv(c->n_rows);
+      for (int i = 0; i < c->n_rows; ++i) {
+        const int t = c->rperm[i];
+        tv[i] = make_int4(c->tris[3 * t], c->tris[3 * t + 1], c->tris[3 * t + 2], t);
+      }
+      long long total = 0;
+      for (int pc = 1; pc < 4; ++pc) {
+        if (c->prule_n[pc] == 0) fail(HMGPU_ERR_STATE, "galerkin pair rule missing");
+        g.pr_off[pc] = (int)total;
+        g.pr_n[pc] = c->prule_n[pc];
+        total += c->prule_n[pc];
+      }
+      std::vector<double> pr(5 * total);
+      for (int pc = 1; pc < 4; ++pc)
+        for (int f = 0; f < 5; ++f)
+          std::copy(c->prule[pc].begin() + (long long)f * c->prule_n[pc],
+                    c->prule[pc].begin() + (long long)(f + 1) * c->prule_n[pc],
+                    pr.begin() + f * total + g.pr_off[pc]);
+      c->d_vtx.upload(vx, c->stream);
+      c->d_tvid.upload(tv, c->stream);
+      c->d_prule.upload(pr, c->stream);
+      g.vtx = c->d_vtx.p;
+      g.tvid = c->d_tvid.p;
+      g.prule = c->d_prule.p;
+      g.prule_total = total;
+      g.gal_delta = c->gal_which;
+    }
   } else if (c->kind == KIND_NEWTON) {
     if (c->n_pts != c->n_rows || c->n_pts != c->n_cols)
       fail(HMGPU_ERR_DIMENSION, "points do not match the partition");
@@ -763,6 +800,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
             c->d_overflow.p);
       };
       if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
+      else if (c->kind == KIND_GALERKIN) go(aca_kernel<KIND_GALERKIN>);
       else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
       else go(aca_kernel<KIND_DENSE>);
     });
@@ -1625,6 +1663,45 @@ int hmgpu_set_kelvin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
   });
 }
 
+int hmgpu_set_galerkin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
+                                int n_tri, const int* tris, const double* centroid,
+                                const double* area, const double* diam, int which) {
+  return guard(ctx, [&] {
+    if (n_vert < 3 || n_tri < 1 || !verts || !tris || !centroid || !area || !diam)
+      fail(HMGPU_ERR_INVALID, "bad galerkin geometry");
+    if (which != 0 && which != 1) fail(HMGPU_ERR_INVALID, "which must be 0 (V_kl) or 1 (V_Delta)");
+    for (long long t = 0; t < 3LL * n_tri; ++t)
+      if (tris[t] < 0 || tris[t] >= n_vert)
+        fail(HMGPU_ERR_INVALID, "vertex index out of range");
+    ctx->kind = KIND_GALERKIN;
+    ctx->NC = which == 0 ? 6 : 1;
+    ctx->gal_which = which;
+    ctx->n_vert = n_vert;
+    ctx->n_tri = n_tri;
+    ctx->verts.assign(verts, verts + 3LL * n_vert);
+    ctx->tris.assign(tris, tris + 3LL * n_tri);
+    ctx->centroid.assign(centroid, centroid + 3LL * n_tri);
+    ctx->area.assign(area, area + n_tri);
+    ctx->diam.assign(diam, diam + n_tri);
+    ctx->assembled = false;
+  });
+}
+
+int hmgpu_set_pair_rule(hmgpu_ctx* ctx, int pair_case, int n, const double* xr1,
+                        const double* xr2, const double* yr1, const double* yr2,
+                        const double* w) {
+  return guard(ctx, [&] {
+    if (pair_case < 1 || pair_case > 3) fail(HMGPU_ERR_INVALID, "pair_case must be 1..3");
+    if (n < 1 || !xr1 || !xr2 || !yr1 || !yr2 || !w) fail(HMGPU_ERR_INVALID, "bad pair rule");
+    std::vector<double>& r = ctx->prule[pair_case];
+    r.resize(5LL * n);
+    const double* src[5] = {xr1, xr2, yr1, yr2, w};
+    for (int f = 0; f < 5; ++f) std::copy(src[f], src[f] + n, r.begin() + (long long)f * n);
+    ctx->prule_n[pair_case] = n;
+    ctx->assembled = false;
+  });
+}
+
 int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag) {
   return guard(ctx, [&] {
     if (n < 1 || !pts) fail(HMGPU_ERR_INVALID, "bad points");
@@ -1693,7 +1770,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         fail(HMGPU_ERR_INVALID, "aca_run: beta must be in (0,1)");
     }
     if (lookahead < 0 || max_rank < 1) fail(HMGPU_ERR_INVALID, "bad lookahead/max_rank");
-    if (c->kind == KIND_KELVIN) upload_rules(c);
+    if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) upload_rules(c);
     build_geometry(c);
     c->eps = eps;
     c->beta = beta_stop;
@@ -2076,7 +2153,7 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::sort(ids.begin(), ids.end());
   ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
   if (ids.empty() || steps == 0) return;
-  if (c->kind == KIND_KELVIN) upload_rules(c);
+  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) upload_rules(c);
   c->d_list.upload(ids, c->stream);
   c->timed("prep_extend", [&] {
     prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(

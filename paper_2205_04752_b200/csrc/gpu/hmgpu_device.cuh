@@ -30,7 +30,7 @@ __constant__ RuleTable c_rules;
 __constant__ int c_comp_r[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_comp_c[6] = {0, 1, 2, 1, 2, 2};
 
-enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2 };
+enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2, KIND_GALERKIN = 3 };
 
 // Per-problem geometry, passed by value to every kernel.
 struct Geom {
@@ -47,6 +47,13 @@ struct Geom {
   double cst;               // (1+nu) / (8 pi E (1-nu))      (kernels.cpp:24)
   double c34;               // 3 - 4 nu
   double diag;              // newton diagonal value
+  // galerkin (V_Delta / V_kl, kernels.cpp:95-149)
+  const double4* vtx;       // mesh vertices, global ids
+  const int4* tvid;         // per internal triangle: global vertex ids, w = external id
+  const double* prule;      // singular pair rules, SoA [5][total] (xr1 xr2 yr1 yr2 w)
+  long long prule_total;
+  int pr_off[4], pr_n[4];   // per PairCase (1 vertex, 2 edge, 3 identical)
+  int gal_delta;            // 1: the context holds V_Delta (one component)
 };
 
 // ---------------------------------------------------------------------------
@@ -267,6 +274,194 @@ __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
   out6[5] = f * fma(g.c34, ad, a22);
 }
 
+// ---------------------------------------------------------------------------
+// Galerkin scalar kernels: V_Delta = (1/4pi) int int
+// 1/|x-y| and V_kl = (1/4pi) int int (x_k-y_k)(x_l-y_l)/|x-y|^3 over pairs of
+// triangles (integrate_pair, proj/src/kernels.cpp:95-149) with the pair
+// rules of quadrature.cpp:127-338: disjoint pairs a tensor product of two
+// triangle rules (order 2 / 4 / 5 by distance, disjoint_order kernels.cpp:
+// 75-85; the tiers of c_rules), touching pairs the Sauter-Schwab tables.
+// Canonical order shared bit for bit with oracle/hmbem_oracle.cpp Galerkin
+// (points by explicit fma from the rotated corners, rsqrt_canon, 4 area_i
+// area_j / (4 pi) factored out).  Components: 0..5 V_kl (c_comp_r/c_comp_c),
+// 6 V_Delta.
+
+// classify_pair (quadrature.cpp:127-156) on global vertex ids; returns the
+// case and the rotations
+__device__ __forceinline__ int gal_classify(const int4& a, const int4& b, int& ra, int& rb) {
+  const int A[3] = {a.x, a.y, a.z}, B[3] = {b.x, b.y, b.z};
+  ra = rb = 0;
+  if (A[0] == B[0] && A[1] == B[1] && A[2] == B[2]) return 3;
+#pragma unroll
+  for (int rt = 0; rt < 3; ++rt)
+#pragma unroll
+    for (int rs = 0; rs < 3; ++rs)
+      if (B[rs] == A[(rt + 1) % 3] && B[(rs + 1) % 3] == A[rt]) {
+        ra = rt;
+        rb = rs;
+        return 2;
+      }
+#pragma unroll
+  for (int rt = 0; rt < 3; ++rt)
+#pragma unroll
+    for (int rs = 0; rs < 3; ++rs)
+      if (A[rt] == B[rs]) {
+        ra = rt;
+        rb = rs;
+        return 1;
+      }
+  return 0;
+}
+
+// disjoint_order (kernels.cpp:75-85) as a tier of c_rules: 0 (order 2) if
+// gap >= 4 dmax, 1 (order 4) if gap >= 0.75 dmax (the mid and near tiers
+// share order 4), else 2 (order 5); IEEE operations in the oracle's order
+__device__ __forceinline__ int gal_tier(const TriRef& Ti, const TriRef& Tj) {
+  const double di = Ti[13], dj = Tj[13];
+  const double dmax = fmax(di, dj);
+  const double dx = __dsub_rn(Ti[9], Tj[9]), dy = __dsub_rn(Ti[10], Tj[10]),
+               dz = __dsub_rn(Ti[11], Tj[11]);
+  const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                          __dmul_rn(dz, dz)));
+  const double gap = __dsub_rn(nrm, __dmul_rn(0.5, __dadd_rn(di, dj)));
+  if (gap >= __dmul_rn(4.0, dmax)) return 0;
+  if (gap >= __dmul_rn(0.75, dmax)) return 1;
+  return 2;
+}
+
+struct GalPair {
+  double x0[3], ex1[3], ex2[3], y0[3], ey1[3], ey2[3];
+  double scale;  // 4 area_i area_j (1 / (4 pi))
+  int pc, tier;
+};
+
+// the canonical pair setup: orientation by external triangle id
+// (kernels.cpp:132-133, 141), classification, rotated corners.  TOUCH =
+// false: the caller guarantees a disjoint pair (admissible blocks).
+template <bool TOUCH>
+__device__ __forceinline__ GalPair gal_setup(const Geom& g, int i, int j) {
+  int4 a = g.tvid[i], b = g.tvid[j];
+  int ii = i, jj = j;
+  if (a.w > b.w) {
+    const int4 t = a;
+    a = b;
+    b = t;
+    ii = j;
+    jj = i;
+  }
+  GalPair P;
+  int ra = 0, rb = 0;
+  P.pc = TOUCH ? gal_classify(a, b, ra, rb) : 0;
+  const TriRef Ti = tri_ref(g, ii), Tj = tri_ref(g, jj);
+  P.tier = P.pc == 0 ? gal_tier(Ti, Tj) : 0;
+  const int A[3] = {a.x, a.y, a.z}, B[3] = {b.x, b.y, b.z};
+  // test_vertex_perm(ra) / trial_vertex_perm(pc, rb) (quadrature.cpp:158-166)
+  const int xp0 = ra, xp1 = (ra + 1) % 3, xp2 = (ra + 2) % 3;
+  int yp0 = rb, yp1 = (rb + 1) % 3;
+  const int yp2 = (rb + 2) % 3;
+  if (P.pc == 2) {
+    const int t = yp0;
+    yp0 = yp1;
+    yp1 = t;
+  }
+  const double4 X0 = g.vtx[A[xp0]], X1 = g.vtx[A[xp1]], X2 = g.vtx[A[xp2]];
+  const double4 Y0 = g.vtx[B[yp0]], Y1 = g.vtx[B[yp1]], Y2 = g.vtx[B[yp2]];
+  P.x0[0] = X0.x; P.x0[1] = X0.y; P.x0[2] = X0.z;
+  P.y0[0] = Y0.x; P.y0[1] = Y0.y; P.y0[2] = Y0.z;
+  P.ex1[0] = X1.x - X0.x; P.ex1[1] = X1.y - X0.y; P.ex1[2] = X1.z - X0.z;
+  P.ex2[0] = X2.x - X0.x; P.ex2[1] = X2.y - X0.y; P.ex2[2] = X2.z - X0.z;
+  P.ey1[0] = Y1.x - Y0.x; P.ey1[1] = Y1.y - Y0.y; P.ey1[2] = Y1.z - Y0.z;
+  P.ey2[0] = Y2.x - Y0.x; P.ey2[1] = Y2.y - Y0.y; P.ey2[2] = Y2.z - Y0.z;
+  P.scale = 4.0 * Ti[12] * Tj[12] * (1.0 / (4.0 * M_PI));
+  return P;
+}
+
+// one quadrature point of component COMP (0..5 V_kl, 6 V_Delta, -1 all)
+template <int COMP>
+__device__ __forceinline__ void gal_point(const GalPair& P, double a1, double a2, double b1,
+                                          double b2, double w, double& ad, double* akl) {
+  double d[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    d[c] = fma(a2, P.ex2[c], fma(a1, P.ex1[c], P.x0[c])) -
+           fma(b2, P.ey2[c], fma(b1, P.ey1[c], P.y0[c]));
+  const double ri = rsqrt_canon(fma(d[2], d[2], fma(d[1], d[1], d[0] * d[0])));
+  const double wr = w * ri;
+  if (COMP == 6 || COMP < 0) ad = ad + wr;
+  if (COMP != 6) {
+    const double w3 = wr * ri * ri;
+    if (COMP >= 0) {
+      akl[0] = fma(w3, d[COMP == 0 || COMP == 1 || COMP == 2 ? 0 : (COMP == 5 ? 2 : 1)] *
+                           d[COMP == 0 ? 0 : (COMP == 1 || COMP == 3 ? 1 : 2)],
+                   akl[0]);
+    } else {
+      akl[0] = fma(w3, d[0] * d[0], akl[0]);
+      akl[1] = fma(w3, d[0] * d[1], akl[1]);
+      akl[2] = fma(w3, d[0] * d[2], akl[2]);
+      akl[3] = fma(w3, d[1] * d[1], akl[3]);
+      akl[4] = fma(w3, d[1] * d[2], akl[4]);
+      akl[5] = fma(w3, d[2] * d[2], akl[5]);
+    }
+  }
+}
+
+// pair sum in rule order (disjoint: test point outer, trial inner, weight
+// w_i w_j; touching: the table order)
+template <int COMP>
+__device__ __forceinline__ void gal_sum(const Geom& g, const GalPair& P, double& ad,
+                                        double* akl, int& nq_acc) {
+  if (P.pc == 0) {
+    const int t = P.tier;
+    const int n = c_rules.n[t];
+    nq_acc += n * n;
+#pragma unroll 1
+    for (int qi = 0; qi < n; ++qi) {
+      const double a1 = c_rules.a[t][qi], a2 = c_rules.b[t][qi], wi = c_rules.w[t][qi];
+#pragma unroll 1
+      for (int qj = 0; qj < n; ++qj)
+        gal_point<COMP>(P, a1, a2, c_rules.a[t][qj], c_rules.b[t][qj], wi * c_rules.w[t][qj],
+                        ad, akl);
+    }
+  } else {
+    const int n = g.pr_n[P.pc];
+    const double* r = g.prule + g.pr_off[P.pc];
+    const long long T = g.prule_total;
+    nq_acc += n;
+#pragma unroll 1
+    for (int q = 0; q < n; ++q)
+      gal_point<COMP>(P, r[q], r[T + q], r[2 * T + q], r[3 * T + q], r[4 * T + q], ad, akl);
+  }
+}
+
+// one component (ACA rows / columns); comp 0..5 = V_kl, 6 = V_Delta
+template <bool TOUCH>
+__device__ __forceinline__ double galerkin_entry1(const Geom& g, int i, int j, int comp,
+                                                  int& nq_acc) {
+  const GalPair P = gal_setup<TOUCH>(g, i, j);
+  double ad = 0.0, akl[1] = {0.0};
+  switch (comp) {  // group-uniform
+    case 0: gal_sum<0>(g, P, ad, akl, nq_acc); break;
+    case 1: gal_sum<1>(g, P, ad, akl, nq_acc); break;
+    case 2: gal_sum<2>(g, P, ad, akl, nq_acc); break;
+    case 3: gal_sum<3>(g, P, ad, akl, nq_acc); break;
+    case 4: gal_sum<4>(g, P, ad, akl, nq_acc); break;
+    case 5: gal_sum<5>(g, P, ad, akl, nq_acc); break;
+    default: gal_sum<6>(g, P, ad, akl, nq_acc); return P.scale * ad;
+  }
+  return P.scale * akl[0];
+}
+
+// all seven components of a pair (near-field fill): out7[0..5] V_kl, [6] V_Delta
+__device__ __forceinline__ void galerkin_entry7(const Geom& g, int i, int j, double* out7,
+                                                int& nq_acc) {
+  const GalPair P = gal_setup<true>(g, i, j);
+  double ad = 0.0, akl[6] = {0, 0, 0, 0, 0, 0};
+  gal_sum<-1>(g, P, ad, akl, nq_acc);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) out7[k] = P.scale * akl[k];
+  out7[6] = P.scale * ad;
+}
+
 // Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact
 __device__ __forceinline__ double newton_entry(const Geom& g, int i, int j) {
   const double4 a = g.rowpt[i];
@@ -287,6 +482,7 @@ __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
                                          int comp) {
   int nq = 0;
   if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq);
+  if (g.kind == KIND_GALERKIN) return galerkin_entry1<true>(g, i, j, g.gal_delta ? 6 : comp, nq);
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -297,6 +493,8 @@ template <int KIND>
 __device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
                                           int& nq_acc) {
   if (KIND == KIND_KELVIN) return kelvin_entry1<false>(g, i, j, comp, nq_acc);
+  if (KIND == KIND_GALERKIN)
+    return galerkin_entry1<false>(g, i, j, g.gal_delta ? 6 : comp, nq_acc);
   if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -989,6 +1187,11 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
         double e[6];
         if (g.kind == KIND_KELVIN) {
           kelvin_entry6(g, b.row0 + i, b.col0 + j, e, nq_acc);
+        } else if (g.kind == KIND_GALERKIN) {
+          double e7[7];
+          galerkin_entry7(g, b.row0 + i, b.col0 + j, e7, nq_acc);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) e[c] = e7[c];
         } else {
           const double v = entry1(g, b.row0 + i, b.col0 + j, 0);
 #pragma unroll
@@ -996,6 +1199,10 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
         }
 #pragma unroll
         for (int c = 0; c < 6; ++c) D[(long long)j * cp + c * b.m + i] = e[c];
+      } else if (g.kind == KIND_GALERKIN) {
+        double e7[7];
+        galerkin_entry7(g, b.row0 + i, b.col0 + j, e7, nq_acc);
+        D[(long long)j * cp + i] = e7[6];
       } else {
         D[(long long)j * cp + i] = entry1(g, b.row0 + i, b.col0 + j, 0);
       }

@@ -50,7 +50,7 @@ struct Shard {
 
 class HOperator {
  public:
-  enum Kind { Kelvin = 0, Newton = 1, Dense = 2 };
+  enum Kind { Kelvin = 0, Newton = 1, Dense = 2, Galerkin = 3 };
 
   // Kelvin single-layer collocation at triangle centroids: one cluster tree
   // over the triangle support boxes for rows and columns
@@ -58,6 +58,13 @@ class HOperator {
                                            int b_min, Real eta, int device,
                                            Shard shard = {},
                                            QuadratureConfig qc = {});
+  // Galerkin scalar kernels on the triangle partition of assemble_operators
+  // (operators.cpp:186-200, 218-235): which = 0 the six V_kl as the 3x3
+  // grid, 1 V_Delta (GalerkinKernels::vkl / vdelta, kernels.cpp:130-149)
+  static std::unique_ptr<HOperator> galerkin(const Mesh& mesh, int which, int b_min,
+                                             Real eta, int device, Shard shard = {},
+                                             QuadratureConfig qc = {},
+                                             GalerkinQuadrature gq = {});
   // scalar Newton kernel over points; boxes == nullptr => point boxes
   static std::unique_ptr<HOperator> newton(const std::vector<V3>& pts,
                                            const std::vector<Box>* boxes,

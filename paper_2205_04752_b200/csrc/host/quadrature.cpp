@@ -77,6 +77,90 @@ TriangleRule gauss_rule(int order) {
   return ob.finish(order);
 }
 
+void gauss_legendre_01(int n, std::vector<double>& x, std::vector<double>& w) {
+  if (n < 1) throw Error("gauss_legendre_01: n must be positive");
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  // Newton on P_n from the Chebyshev-like guess, symmetric pairs mapped to [0,1]
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p_cur = 1.0, p_prev = 0.0;
+      for (int j = 0; j < n; ++j) {
+        const double p_old = p_prev;
+        p_prev = p_cur;
+        p_cur = ((2.0 * j + 1.0) * z * p_prev - j * p_old) / (j + 1.0);
+      }
+      dp = n * (z * p_cur - p_prev) / (z * z - 1.0);
+      const double step = p_cur / dp;
+      z -= step;
+      if (std::abs(step) < 1e-16) break;
+    }
+    const double wi = 1.0 / ((1.0 - z * z) * dp * dp);
+    x[i] = 0.5 * (1.0 - z);
+    x[n - 1 - i] = 0.5 * (1.0 + z);
+    w[i] = w[n - 1 - i] = wi;
+  }
+}
+
+namespace {
+
+// the subdomain maps [0,1]^4 -> (x1, x2, y1, y2) and the Jacobian; each
+// expression as the reference writes it (the rounding is the rule)
+void ss_point(int pc, int s, double xi, double e1, double e2, double e3, double* p) {
+  double& x1 = p[0];
+  double& x2 = p[1];
+  double& y1 = p[2];
+  double& y2 = p[3];
+  double& jac = p[4];
+  if (pc == 3) {  // identical, 6 simplices
+    jac = xi * xi * xi * e1 * e1 * e2;
+    if (s == 0) { x1 = xi * e1 * (1 - e2); x2 = xi * (1 - e1 * (1 - e2)); y1 = xi * e1 * (1 - e2 * e3); y2 = xi * (1 - e1); }
+    if (s == 1) { x1 = xi * e1 * (1 - e2 * e3); x2 = xi * (1 - e1); y1 = xi * e1 * (1 - e2); y2 = xi * (1 - e1 * (1 - e2)); }
+    if (s == 2) { x1 = xi * (1 - e1 * (1 - e2 * (1 - e3))); x2 = xi * e1 * (1 - e2 * (1 - e3)); y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2); }
+    if (s == 3) { x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2); y1 = xi * (1 - e1 * (1 - e2 * (1 - e3))); y2 = xi * e1 * (1 - e2 * (1 - e3)); }
+    if (s == 4) { x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2 * e3); y1 = xi * (1 - e1 * (1 - e2)); y2 = xi * e1 * (1 - e2); }
+    if (s == 5) { x1 = xi * (1 - e1 * (1 - e2)); x2 = xi * e1 * (1 - e2); y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2 * e3); }
+  } else if (pc == 2) {  // shared edge, 5 simplices
+    jac = xi * xi * xi * e1 * e1;
+    if (s == 0) { x1 = xi * (1 - e1 * e3); x2 = xi * e1 * e3; y1 = xi * (1 - e1); y2 = xi * e1 * (1 - e2); }
+    if (s == 1) { x1 = xi * (1 - e1); x2 = xi * e1; y1 = xi * (1 - e1 * e2); y2 = xi * e1 * e2 * (1 - e3); }
+    if (s == 2) { x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2); y1 = xi * (1 - e1 * e2 * e3); y2 = xi * e1 * e2 * e3; }
+    if (s == 3) { x1 = xi * (1 - e1 * e2); x2 = xi * e1 * e2 * (1 - e3); y1 = xi * (1 - e1); y2 = xi * e1; }
+    if (s == 4) { x1 = xi * (1 - e1); x2 = xi * e1 * (1 - e2 * e3); y1 = xi * (1 - e1 * e2); y2 = xi * e1 * e2; }
+    if (s > 0) jac *= e2;
+  } else {  // shared vertex, 2 simplices
+    jac = xi * xi * xi * e2;
+    if (s == 0) { x1 = xi * (1 - e1); x2 = xi * e1; y1 = xi * e2 * (1 - e3); y2 = xi * e2 * e3; }
+    else { x1 = xi * e2 * (1 - e3); x2 = xi * e2 * e3; y1 = xi * (1 - e1); y2 = xi * e1; }
+  }
+}
+
+}  // namespace
+
+PairRuleTable singular_pair_rule(int pair_case, int order) {
+  if (pair_case < 1 || pair_case > 3) throw Error("singular_pair_rule: bad pair case");
+  std::vector<double> gx, gw;
+  gauss_legendre_01(order, gx, gw);
+  const int simplices = pair_case == 3 ? 6 : pair_case == 2 ? 5 : 2;
+  PairRuleTable r;
+  double p[5];
+  for (int s = 0; s < simplices; ++s)
+    for (int a = 0; a < order; ++a)
+      for (int b = 0; b < order; ++b)
+        for (int c = 0; c < order; ++c)
+          for (int d = 0; d < order; ++d) {
+            ss_point(pair_case, s, gx[a], gx[b], gx[c], gx[d], p);
+            r.xr1.push_back(p[0]);
+            r.xr2.push_back(p[1]);
+            r.yr1.push_back(p[2]);
+            r.yr2.push_back(p[3]);
+            r.w.push_back(p[4] * gw[a] * gw[b] * gw[c] * gw[d]);
+          }
+  return r;
+}
+
 int QuadratureConfig::tier_order(int tier) const {
   if (tier == 0) return std::min(disjoint_order, 2);
   if (tier == 1) return disjoint_order;

@@ -25,4 +25,21 @@ struct QuadratureConfig {
   int tier_order(int tier) const;
 };
 
+// n-point Gauss-Legendre on [0, 1] (quadrature.cpp:97-125)
+void gauss_legendre_01(int n, std::vector<double>& x, std::vector<double>& w);
+
+// Sauter-Schwab pair rule of a touching pair (PairCase 1 vertex, 2 edge,
+// 3 identical; quadrature.cpp:168-338): `order` Gauss-Legendre points per
+// dimension of [0,1]^4 on each subdomain simplex
+struct PairRuleTable {
+  std::vector<double> xr1, xr2, yr1, yr2, w;
+};
+PairRuleTable singular_pair_rule(int pair_case, int order);
+
+// GalerkinKernels' QuadratureConfig defaults (kernels.hpp:44-52)
+struct GalerkinQuadrature {
+  int singular_order = 7;
+  int identical_bump = 2;
+};
+
 }  // namespace hmb
