@@ -243,6 +243,56 @@ def weighted_entries(h):
 
 
 # ---------------------------------------------------------------------------
+def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
+    """SURVEY.md 8f rank 2 on the same mesh: the Galerkin V_Delta and V_kl
+    H-matrices (pair quadrature with Sauter-Schwab rules for touching pairs)
+    assembled by the same engine, and the Lame single-layer V_h matvec
+    (compose_Vh) on device pointers.  Secondary object of the c2 line."""
+    vh = hm.LameSingleLayer(mesh, 1.0, 0.3, b_min=cfg["b_min"], eta=cfg["eta"],
+                            device=device)
+    best = None
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sk, sd = vh.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        wall = time.perf_counter() - t0
+        if best is None or wall < best[0]:
+            best = (wall, sk, sd)
+    wall, sk, sd = best
+    nt = vh.nt
+    x = hm.random_vector(3 * nt, cfg["seed"], "uniform")
+    xd = torch.tensor(x, dtype=torch.float64, device=f"cuda:{device}")
+    yg = torch.zeros(3 * nt, dtype=torch.float64, device=f"cuda:{device}")
+    yd = torch.zeros(3 * nt, dtype=torch.float64, device=f"cuda:{device}")
+    s = 0.5 / vh.E * (1.0 + vh.nu) / (1.0 - vh.nu)
+    c34 = 3.0 - 4.0 * vh.nu
+
+    def vh_step():
+        vh.vkl.matvec_ptr(xd.data_ptr(), yg.data_ptr(), 1)
+        vh.vdelta.matvec_ptr(xd.data_ptr(), yd.data_ptr(), 3)  # diag3: 3 RHS
+        torch.cuda.synchronize()
+        return s * (c34 * yd + yg)
+
+    y = vh_step()
+    for _ in range(3):
+        vh_step()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        vh_step()
+    ms = (time.perf_counter() - t0) / reps * 1e3
+    y_host = vh.matvec(x)
+    entries = sk.aca_entries + sk.dense_entries + sd.aca_entries + sd.dense_entries
+    return {"operator": "V_h = (1+nu)/(2E(1-nu)) [(3-4nu) diag3(V_Delta) + grid(V_kl)]",
+            "assembly_ms_device": sk.ms_total + sd.ms_total, "assembly_ms_wall": wall * 1e3,
+            "entries": entries, "entries_per_s": entries / ((sk.ms_total + sd.ms_total) * 1e-3),
+            "nearfield_ms": sk.ms_nearfield + sd.ms_nearfield,
+            "pivots": sk.pivots + sd.pivots,
+            "storage_mb": vh.vkl.storage()["mb_current"] + vh.vdelta.storage()["mb_current"],
+            "matvec_ms_wall": ms, "matvec_dofs_per_s": 3 * nt / (ms * 1e-3),
+            "matvec_check_rel": float(np.linalg.norm(y.cpu().numpy() - y_host) /
+                                      np.linalg.norm(y_host))}
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2205_04752_b200 as hm
@@ -456,6 +506,8 @@ def run_ours(args, cfg):
                         "marked": [int(i.marked) for i in rep.iterations],
                         "ms_per_sweep": [float(i.ms) for i in rep.iterations],
                         "assembly_ms": st4.ms_total}
+    if args.config == "c2" and world == 1 and not args.no_galerkin:
+        line["galerkin"] = galerkin_leg(hm, torch, mesh, cfg, device)
     if res is not None:
         line["cpu_baseline"] = res["cpu_baseline"]
         line["assembly"]["cpu_entries_per_s"] = res["assembly"]["value"]
@@ -475,6 +527,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-galerkin", action="store_true",
+                    help="skip the Galerkin V_h object of the c2 line")
     ap.add_argument("--nrhs", type=int, default=0,
                     help="override the config's number of right-hand sides")
     args = ap.parse_args()

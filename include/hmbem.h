@@ -10,6 +10,7 @@
  *                       H-matrices at triangle centroids (baca.cpp:645-687)
  *   hmb_op_galerkin     GalerkinKernels V_kl grid / V_Delta KernelOracle
  *                       H-matrices (kernels.cpp:95-149, operators.cpp:218-235)
+ *   hmb_op_kdelta       K_Delta KernelOracle H-matrix, triangles x nodes
  *   hmb_op_newton/dense test fixtures (test_hmatrix.cpp:12-53, aca.hpp:34-44)
  *   hmb_tree_*, hmb_partition_*   ClusterTree / BlockPartition /
  *                       sparsity_constant / partition_to_json (cluster.hpp)
@@ -80,6 +81,10 @@ int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
  * 1 -> V_Delta (kernels.cpp:130-149) */
 int hmb_op_galerkin(const hmb_mesh* m, int which, int b_min, double eta, int device,
                     int shard_rank, int shard_count, hmb_op** out);
+/* K_Delta on the triangle x node partition (kernels.cpp:151-167): rows
+ * triangles, columns vertices */
+int hmb_op_kdelta(const hmb_mesh* m, int b_min, double eta, int device, int shard_rank,
+                  int shard_count, hmb_op** out);
 int hmb_op_newton(int n, const double* pts, const double* boxes6, double diag,
                   int b_min, double eta, int device, hmb_op** out);
 int hmb_op_dense(int m, int n, const double* a_colmajor, const double* row_pts,

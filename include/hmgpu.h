@@ -16,6 +16,8 @@
  *                              vdelta / vkl / integrate_pair / disjoint_order
  *                              (proj/include/hmbem/kernels.hpp:95-105,
  *                               proj/src/kernels.cpp:75-149), fused into the kernels
+ *   hmgpu_set_kdelta_geometry  KernelOracle over K_Delta: GalerkinKernels::kdelta
+ *                              (proj/src/kernels.cpp:151-167), triangles x nodes
  *   hmgpu_set_pair_rule        pair_rule(PairCase, order) Sauter-Schwab tables
  *                              (proj/src/quadrature.cpp:290-338)
  *   hmgpu_set_points           test fixtures CentroidKernelOracle / PointKernelOracle
@@ -135,6 +137,13 @@ int hmgpu_set_kelvin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
 int hmgpu_set_galerkin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
                                 int n_tri, const int* tris, const double* centroid,
                                 const double* area, const double* diam, int which);
+/* K_Delta (kernels.cpp:151-167): triangles x vertices on the triangle x
+ * node partition (node boxes = union of the incident triangles' boxes,
+ * operators.cpp:190-200); normals n_tri x 3 as load_mesh computes them.
+ * Uses the rule tiers and pair rules like hmgpu_set_galerkin_geometry. */
+int hmgpu_set_kdelta_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts, int n_tri,
+                              const int* tris, const double* centroid, const double* area,
+                              const double* diam, const double* normals);
 /* singular pair rule of PairCase pair_case (1 vertex, 2 edge, 3 identical):
  * n points, reference coordinates on the rotated test (xr) and trial (yr)
  * triangles and weights (PairRule, quadrature.hpp:44-52) */

@@ -686,6 +686,88 @@ struct Galerkin {
     entry7(i, j, o);
     return o[comp];
   }
+
+  // K_Delta(i, node) = sum over the triangles tau of the node (ascending ids,
+  // load_mesh's vertex_triangles, mesh.cpp:245-247), tau != i, of
+  // integrate_pair(i, tau) of (x-y).n(tau) / (4 pi |x-y|^3) psi_node(y)
+  // (kernels.cpp:151-167; no orientation swap).  Canonical order: per pair
+  // sum_q fma(w / r^3, ((x-y).n) * bary_local, .), the 4 area area / (4 pi)
+  // scale per pair, pairs summed in tau order.
+  std::vector<std::vector<int>> vtri;
+  void build_vtri() {
+    vtri.assign(mesh->vertices.size(), {});
+    for (int t = 0; t < mesh->nt(); ++t)
+      for (int v : mesh->triangles[t]) vtri[v].push_back(t);
+  }
+  Real kdelta(int i, int node) const {
+    Real total = 0.0;
+    for (int tau : vtri[node]) {
+      if (tau == i) continue;
+      int local = 0;
+      while (mesh->triangles[tau][local] != node) ++local;
+      const Vec3& nrm = mesh->normals[tau];
+      int pc, rt, rs;
+      const PairRule& r = rule_for(i, tau, pc, rt, rs);
+      const auto xp = test_vertex_perm(rt);
+      const auto yp = trial_vertex_perm(pc, rs);
+      const Vec3 x0 = mesh->corner(i, xp[0]), x1 = mesh->corner(i, xp[1]),
+                 x2 = mesh->corner(i, xp[2]);
+      const Vec3 y0 = mesh->corner(tau, yp[0]), y1 = mesh->corner(tau, yp[1]),
+                 y2 = mesh->corner(tau, yp[2]);
+      const Vec3 ex1 = sub(x1, x0), ex2 = sub(x2, x0), ey1 = sub(y1, y0), ey2 = sub(y2, y0);
+      Real acc = 0.0;
+      for (size_t q = 0; q < r.w.size(); ++q) {
+        const Real a1 = r.xr1[q], a2 = r.xr2[q], b1 = r.yr1[q], b2 = r.yr2[q];
+        Real d[3];
+        for (int c = 0; c < 3; ++c)
+          d[c] = std::fma(a2, ex2[c], std::fma(a1, ex1[c], x0[c])) -
+                 std::fma(b2, ey2[c], std::fma(b1, ey1[c], y0[c]));
+        const Real ri = rsqrt_canon(std::fma(d[2], d[2], std::fma(d[1], d[1], d[0] * d[0])));
+        const Real w3 = r.w[q] * ri * ri * ri;
+        const Real dn = std::fma(d[2], nrm[2], std::fma(d[1], nrm[1], d[0] * nrm[0]));
+        // barycentric of y w.r.t. the original vertex order (kernels.cpp:119-123)
+        const Real bv = local == yp[0] ? (1.0 - b1) - b2 : local == yp[1] ? b1 : b2;
+        acc = std::fma(w3, dn * bv, acc);
+      }
+      total += 4.0 * mesh->areas[i] * mesh->areas[tau] * (1.0 / (4.0 * M_PI)) * acc;
+    }
+    return total;
+  }
+  // literal form (kernels.cpp:151-167 with integrate_pair's loop)
+  Real kdelta_literal(int i, int node) const {
+    Real total = 0.0;
+    for (int tau : vtri[node]) {
+      if (tau == i) continue;
+      int local = 0;
+      while (mesh->triangles[tau][local] != node) ++local;
+      int pc, rt, rs;
+      const PairRule& r = rule_for(i, tau, pc, rt, rs);
+      const auto xp = test_vertex_perm(rt);
+      const auto yp = trial_vertex_perm(pc, rs);
+      Vec3 X[3], Y[3];
+      for (int v = 0; v < 3; ++v) {
+        X[v] = mesh->corner(i, xp[v]);
+        Y[v] = mesh->corner(tau, yp[v]);
+      }
+      Real acc = 0.0;
+      for (size_t q = 0; q < r.w.size(); ++q) {
+        Vec3 x, y;
+        for (int c = 0; c < 3; ++c) {
+          x[c] = X[0][c] + r.xr1[q] * (X[1][c] - X[0][c]) + r.xr2[q] * (X[2][c] - X[0][c]);
+          y[c] = Y[0][c] + r.yr1[q] * (Y[1][c] - Y[0][c]) + r.yr2[q] * (Y[2][c] - Y[0][c]);
+        }
+        Real bary[3];
+        bary[yp[0]] = 1.0 - r.yr1[q] - r.yr2[q];
+        bary[yp[1]] = r.yr1[q];
+        bary[yp[2]] = r.yr2[q];
+        const Vec3 d = sub(x, y);
+        const Real rr = norm3(d);
+        acc += r.w[q] * (dot3(d, mesh->normals[tau]) / (4.0 * M_PI * rr * rr * rr) * bary[local]);
+      }
+      total += 4.0 * mesh->areas[i] * mesh->areas[tau] * acc;
+    }
+    return total;
+  }
   // the literal form of integrate_pair with the reference's integrand
   // (acc += w f(x, y), 4 area area acc) -- checks the canonical order only
   Real entry_literal(int i, int j, int comp) const {
@@ -763,6 +845,16 @@ struct GalerkinComponentOracle : EntryOracle {
   long cols() const override { return g->mesh->nt(); }
   Real entry(long i, long j) const override {
     return g->entry(static_cast<int>(i), static_cast<int>(j), comp);
+  }
+};
+
+// KernelOracle over K_Delta: triangles x nodes (kernels.hpp:95-105, 120)
+struct KDeltaOracle : EntryOracle {
+  const Galerkin* g;
+  long rows() const override { return g->mesh->nt(); }
+  long cols() const override { return static_cast<long>(g->mesh->vertices.size()); }
+  Real entry(long i, long j) const override {
+    return g->kdelta(static_cast<int>(i), static_cast<int>(j));
   }
 };
 
@@ -1852,6 +1944,42 @@ int or_problem_galerkin(int nv, const double* verts, int nt, const int* tris, in
   });
 }
 
+// kind 5: K_Delta on the triangle x node partition of assemble_operators
+// (operators.cpp:186-200): node boxes = union of the incident triangles'
+// corner boxes, separate row (triangle) and column (node) trees.
+int or_problem_kdelta(int nv, const double* verts, int nt, const int* tris, int b_min,
+                      double eta, void** out) {
+  return guard([&] {
+    auto p = std::make_unique<Problem>();
+    p->kind = 5;
+    p->mesh.vertices.resize(nv);
+    for (int v = 0; v < nv; ++v)
+      p->mesh.vertices[v] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]};
+    p->mesh.triangles.resize(nt);
+    for (int t = 0; t < nt; ++t)
+      p->mesh.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    finish_geometry(p->mesh);
+    p->galerkin = std::make_unique<Galerkin>(&p->mesh);
+    p->galerkin->build_vtri();
+    p->n = nt;
+    std::vector<Box> tb(nt), nb(nv);
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k) tb[t].absorb(p->mesh.corner(t, k));
+    for (int v = 0; v < nv; ++v)
+      for (int t : p->galerkin->vtri[v]) nb[v].absorb(tb[t]);
+    p->rows_tree = build_cluster_tree(tb, b_min);
+    p->cols_tree = build_cluster_tree(nb, b_min);
+    p->part = std::make_unique<Partition>(
+        build_block_partition(&p->rows_tree, &p->cols_tree, eta));
+    auto o = std::make_unique<KDeltaOracle>();
+    o->g = p->galerkin.get();
+    p->oracles.push_back(std::move(o));
+    p->grid.ncomp = 1;
+    p->grid.nblk = nt;
+    *out = p.release();
+  });
+}
+
 // pair_rule(case, order) tables (quadrature.cpp:290-338); NULL arrays query n
 int or_pair_rule(int pc, int order, int* n, double* xr1, double* xr2, double* yr1,
                  double* yr2, double* w) {
@@ -2020,6 +2148,10 @@ int or_partition_json(void* h, char* buf, long* len) {
 int or_entry_literal(void* h, int comp, long i, long j, double* out) {
   return guard([&] {
     Problem* p = P(h);
+    if (p->kind == 5) {
+      *out = p->galerkin->kdelta_literal(static_cast<int>(i), static_cast<int>(j));
+      return;
+    }
     if (p->kind == 3 || p->kind == 4) {
       *out = p->galerkin->entry_literal(static_cast<int>(i), static_cast<int>(j),
                                         p->kind == 4 ? 6 : comp);

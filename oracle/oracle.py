@@ -158,10 +158,11 @@ class Problem:
     """An oracle problem: tree + partition + (after assemble) the component
     H-matrices of the reference semantics."""
 
-    def __init__(self, handle, ncomp: int, n: int):
+    def __init__(self, handle, ncomp: int, n: int, ncols: int = -1):
         self._h = handle
         self.ncomp = ncomp
         self.n = n
+        self.ncols = n if ncols < 0 else ncols
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -189,6 +190,17 @@ class Problem:
         return cls(h, 6 if which == 0 else 1, len(t))
 
     @classmethod
+    def kdelta(cls, verts, tris, b_min=32, eta=1.0):
+        """K_Delta on the triangle x node partition (kernels.cpp:151-167,
+        operators.cpp:186-200): rows triangles, columns vertices."""
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32)
+        h = C.c_void_p()
+        _ck(lib().or_problem_kdelta(len(v), _p(v), len(t), _p(t), b_min, D(eta),
+                                    C.byref(h)))
+        return cls(h, 1, len(t), len(v))
+
+    @classmethod
     def newton(cls, pts, boxes=None, diag=2.0, b_min=10, eta=0.8):
         p = np.ascontiguousarray(pts, dtype=np.float64)
         b = None if boxes is None else np.ascontiguousarray(boxes, dtype=np.float64)
@@ -205,7 +217,7 @@ class Problem:
         h = C.c_void_p()
         _ck(lib().or_problem_dense(a.shape[0], a.shape[1], a.ctypes.data_as(C.c_void_p),
                                    _p(rp), _p(cp), b_min, D(eta), C.byref(h)))
-        return cls(h, 1, a.shape[0])
+        return cls(h, 1, a.shape[0], a.shape[1])
 
     @property
     def rows(self) -> int:
@@ -248,7 +260,7 @@ class Problem:
         return out.value
 
     def dense(self, comp: int = 0) -> np.ndarray:
-        out = np.zeros((self.n, self.n))
+        out = np.zeros((self.n, self.ncols))
         _ck(lib().or_dense(self._h, int(comp), _p(out)))
         return out
 

@@ -57,6 +57,7 @@ _sig(host, "hmb_gauss_rule", I, I, IP, P, P, P)
 _sig(host, "hmb_random_vector", I, LL, C.c_ulonglong, I, P)
 _sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_galerkin", I, P, I, I, D, I, I, I, C.POINTER(P))
+_sig(host, "hmb_op_kdelta", I, P, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_dense", I, I, I, P, P, P, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_free", None, P)

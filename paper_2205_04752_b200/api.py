@@ -288,6 +288,16 @@ class HMatrix:
         return cls(out)
 
     @classmethod
+    def kdelta(cls, mesh: Mesh, b_min: int = 32, eta: float = 1.0, device: int = 0,
+               shard: tuple = (0, 1)) -> "HMatrix":
+        """K_Delta (GalerkinKernels::kdelta, kernels.cpp:151-167) on the
+        triangle x node partition (operators.cpp:186-200): N_t x N_v."""
+        out = C.c_void_p()
+        _check(_h.hmb_op_kdelta(mesh._h, b_min, eta, device, shard[0], shard[1],
+                                C.byref(out)))
+        return cls(out)
+
+    @classmethod
     def newton(cls, points, boxes=None, diag: float = 2.0, b_min: int = 10,
                eta: float = 0.8, device: int = 0) -> "HMatrix":
         p = _f64(points).reshape(-1, 3)

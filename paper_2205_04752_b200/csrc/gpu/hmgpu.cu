@@ -363,6 +363,7 @@ struct hmgpu_ctx {
   RuleTable rules{};
   bool rules_set[3] = {false, false, false};
   int gal_which = 0;                   // galerkin: 0 V_kl grid, 1 V_Delta
+  std::vector<double> normals;         // K_Delta: unit normals per triangle
   std::vector<double> prule[4];        // galerkin singular pair rules, SoA per case
   int prule_n[4] = {0, 0, 0, 0};
 
@@ -380,7 +381,10 @@ struct hmgpu_ctx {
   DBuf<double4> d_rowpt, d_colpt;
   DBuf<double> d_tri, d_A, d_prule;
   DBuf<double4> d_vtx;
-  DBuf<int4> d_tvid;
+  DBuf<int4> d_tvid, d_tvx;
+  DBuf<double4> d_tce, d_tna;
+  DBuf<int> d_vtptr;
+  DBuf<int2> d_vttri;
   DBuf<int> d_rperm, d_cperm;
   Geom geom{};
 
@@ -671,6 +675,62 @@ void build_geometry(hmgpu_ctx* c) {
       g.prule_total = total;
       g.gal_delta = c->gal_which;
     }
+  } else if (c->kind == KIND_KDELTA) {
+    if (c->n_tri != c->n_rows || c->n_vert != c->n_cols)
+      fail(HMGPU_ERR_DIMENSION, "K_Delta geometry does not match the partition");
+    std::vector<double4> vx(c->n_vert), tce(c->n_tri), tna(c->n_tri);
+    for (int v = 0; v < c->n_vert; ++v)
+      vx[v] = make_double4(c->verts[3LL * v], c->verts[3LL * v + 1], c->verts[3LL * v + 2], 0);
+    std::vector<int4> tvx(c->n_tri), tv(c->n_rows);
+    for (int t = 0; t < c->n_tri; ++t) {
+      tvx[t] = make_int4(c->tris[3 * t], c->tris[3 * t + 1], c->tris[3 * t + 2], t);
+      tce[t] = make_double4(c->centroid[3 * t], c->centroid[3 * t + 1], c->centroid[3 * t + 2],
+                            c->diam[t]);
+      tna[t] = make_double4(c->normals[3 * t], c->normals[3 * t + 1], c->normals[3 * t + 2],
+                            c->area[t]);
+    }
+    for (int i = 0; i < c->n_rows; ++i) tv[i] = tvx[c->rperm[i]];
+    // vertex_triangles (mesh.cpp:245-247) per internal column, ascending ids
+    std::vector<std::vector<int2>> inc(c->n_vert);
+    for (int t = 0; t < c->n_tri; ++t)
+      for (int k = 0; k < 3; ++k) inc[c->tris[3 * t + k]].push_back(make_int2(t, k));
+    std::vector<int> ptr(c->n_cols + 1, 0);
+    std::vector<int2> lst;
+    for (int j = 0; j < c->n_cols; ++j) {
+      const auto& l = inc[c->cperm[j]];
+      lst.insert(lst.end(), l.begin(), l.end());
+      ptr[j + 1] = (int)lst.size();
+    }
+    long long total = 0;
+    for (int pc = 1; pc < 4; ++pc) {
+      if (c->prule_n[pc] == 0) fail(HMGPU_ERR_STATE, "galerkin pair rule missing");
+      g.pr_off[pc] = (int)total;
+      g.pr_n[pc] = c->prule_n[pc];
+      total += c->prule_n[pc];
+    }
+    std::vector<double> pr(5 * total);
+    for (int pc = 1; pc < 4; ++pc)
+      for (int f = 0; f < 5; ++f)
+        std::copy(c->prule[pc].begin() + (long long)f * c->prule_n[pc],
+                  c->prule[pc].begin() + (long long)(f + 1) * c->prule_n[pc],
+                  pr.begin() + f * total + g.pr_off[pc]);
+    c->d_vtx.upload(vx, c->stream);
+    c->d_tvid.upload(tv, c->stream);
+    c->d_tvx.upload(tvx, c->stream);
+    c->d_tce.upload(tce, c->stream);
+    c->d_tna.upload(tna, c->stream);
+    c->d_vtptr.upload(ptr, c->stream);
+    c->d_vttri.upload(lst, c->stream);
+    c->d_prule.upload(pr, c->stream);
+    g.vtx = c->d_vtx.p;
+    g.tvid = c->d_tvid.p;
+    g.tvx = c->d_tvx.p;
+    g.tce = c->d_tce.p;
+    g.tna = c->d_tna.p;
+    g.vt_ptr = c->d_vtptr.p;
+    g.vt_tri = c->d_vttri.p;
+    g.prule = c->d_prule.p;
+    g.prule_total = total;
   } else if (c->kind == KIND_NEWTON) {
     if (c->n_pts != c->n_rows || c->n_pts != c->n_cols)
       fail(HMGPU_ERR_DIMENSION, "points do not match the partition");
@@ -801,6 +861,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
       };
       if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
       else if (c->kind == KIND_GALERKIN) go(aca_kernel<KIND_GALERKIN>);
+      else if (c->kind == KIND_KDELTA) go(aca_kernel<KIND_KDELTA>);
       else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
       else go(aca_kernel<KIND_DENSE>);
     });
@@ -1687,6 +1748,29 @@ int hmgpu_set_galerkin_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts,
   });
 }
 
+int hmgpu_set_kdelta_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts, int n_tri,
+                              const int* tris, const double* centroid, const double* area,
+                              const double* diam, const double* normals) {
+  return guard(ctx, [&] {
+    if (n_vert < 3 || n_tri < 1 || !verts || !tris || !centroid || !area || !diam || !normals)
+      fail(HMGPU_ERR_INVALID, "bad K_Delta geometry");
+    for (long long t = 0; t < 3LL * n_tri; ++t)
+      if (tris[t] < 0 || tris[t] >= n_vert)
+        fail(HMGPU_ERR_INVALID, "vertex index out of range");
+    ctx->kind = KIND_KDELTA;
+    ctx->NC = 1;
+    ctx->n_vert = n_vert;
+    ctx->n_tri = n_tri;
+    ctx->verts.assign(verts, verts + 3LL * n_vert);
+    ctx->tris.assign(tris, tris + 3LL * n_tri);
+    ctx->centroid.assign(centroid, centroid + 3LL * n_tri);
+    ctx->area.assign(area, area + n_tri);
+    ctx->diam.assign(diam, diam + n_tri);
+    ctx->normals.assign(normals, normals + 3LL * n_tri);
+    ctx->assembled = false;
+  });
+}
+
 int hmgpu_set_pair_rule(hmgpu_ctx* ctx, int pair_case, int n, const double* xr1,
                         const double* xr2, const double* yr1, const double* yr2,
                         const double* w) {
@@ -1770,7 +1854,8 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         fail(HMGPU_ERR_INVALID, "aca_run: beta must be in (0,1)");
     }
     if (lookahead < 0 || max_rank < 1) fail(HMGPU_ERR_INVALID, "bad lookahead/max_rank");
-    if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) upload_rules(c);
+    if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA)
+      upload_rules(c);
     build_geometry(c);
     c->eps = eps;
     c->beta = beta_stop;
@@ -2153,7 +2238,8 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::sort(ids.begin(), ids.end());
   ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
   if (ids.empty() || steps == 0) return;
-  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) upload_rules(c);
+  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA)
+    upload_rules(c);
   c->d_list.upload(ids, c->stream);
   c->timed("prep_extend", [&] {
     prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(

@@ -30,7 +30,7 @@ __constant__ RuleTable c_rules;
 __constant__ int c_comp_r[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_comp_c[6] = {0, 1, 2, 1, 2, 2};
 
-enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2, KIND_GALERKIN = 3 };
+enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2, KIND_GALERKIN = 3, KIND_KDELTA = 4 };
 
 // Per-problem geometry, passed by value to every kernel.
 struct Geom {
@@ -54,6 +54,12 @@ struct Geom {
   long long prule_total;
   int pr_off[4], pr_n[4];   // per PairCase (1 vertex, 2 edge, 3 identical)
   int gal_delta;            // 1: the context holds V_Delta (one component)
+  // K_Delta (triangles x nodes, kernels.cpp:151-167): per external triangle
+  const int4* tvx;          // vertex ids, w = external id
+  const double4* tce;       // centroid, diameter
+  const double4* tna;       // unit normal, area
+  const int* vt_ptr;        // per internal column (node): its triangles in vt_tri
+  const int2* vt_tri;       // (triangle, local index of the node), ascending triangles
 };
 
 // ---------------------------------------------------------------------------
@@ -316,11 +322,10 @@ __device__ __forceinline__ int gal_classify(const int4& a, const int4& b, int& r
 // disjoint_order (kernels.cpp:75-85) as a tier of c_rules: 0 (order 2) if
 // gap >= 4 dmax, 1 (order 4) if gap >= 0.75 dmax (the mid and near tiers
 // share order 4), else 2 (order 5); IEEE operations in the oracle's order
-__device__ __forceinline__ int gal_tier(const TriRef& Ti, const TriRef& Tj) {
-  const double di = Ti[13], dj = Tj[13];
+__device__ __forceinline__ int gal_tier(double cix, double ciy, double ciz, double di,
+                                        double cjx, double cjy, double cjz, double dj) {
   const double dmax = fmax(di, dj);
-  const double dx = __dsub_rn(Ti[9], Tj[9]), dy = __dsub_rn(Ti[10], Tj[10]),
-               dz = __dsub_rn(Ti[11], Tj[11]);
+  const double dx = __dsub_rn(cix, cjx), dy = __dsub_rn(ciy, cjy), dz = __dsub_rn(ciz, cjz);
   const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                           __dmul_rn(dz, dz)));
   const double gap = __dsub_rn(nrm, __dmul_rn(0.5, __dadd_rn(di, dj)));
@@ -353,7 +358,8 @@ __device__ __forceinline__ GalPair gal_setup(const Geom& g, int i, int j) {
   int ra = 0, rb = 0;
   P.pc = TOUCH ? gal_classify(a, b, ra, rb) : 0;
   const TriRef Ti = tri_ref(g, ii), Tj = tri_ref(g, jj);
-  P.tier = P.pc == 0 ? gal_tier(Ti, Tj) : 0;
+  P.tier = P.pc == 0 ? gal_tier(Ti[9], Ti[10], Ti[11], Ti[13], Tj[9], Tj[10], Tj[11], Tj[13])
+                     : 0;
   const int A[3] = {a.x, a.y, a.z}, B[3] = {b.x, b.y, b.z};
   // test_vertex_perm(ra) / trial_vertex_perm(pc, rb) (quadrature.cpp:158-166)
   const int xp0 = ra, xp1 = (ra + 1) % 3, xp2 = (ra + 2) % 3;
@@ -462,6 +468,82 @@ __device__ __forceinline__ void galerkin_entry7(const Geom& g, int i, int j, dou
   out7[6] = P.scale * ad;
 }
 
+// K_Delta(i, node) = sum over the node's triangles tau != i (ascending) of
+// integrate_pair(i, tau) of (x-y).n(tau) / (4 pi |x-y|^3) psi_node(y)
+// (kernels.cpp:151-167, no orientation swap), in the oracle's canonical
+// order (Galerkin::kdelta): per pair sum_q fma(w / r^3, ((x-y).n) bary, .),
+// scaled by 4 area_i area_tau / (4 pi), pairs summed in tau order.
+// TOUCH = false: admissible blocks (no triangle of the node touches i).
+template <bool TOUCH>
+__device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int& nq_acc) {
+  const int4 a = g.tvid[i];
+  const double4 ca = g.tce[a.w], na = g.tna[a.w];
+  const int A[3] = {a.x, a.y, a.z};
+  double total = 0.0;
+  const int p1 = g.vt_ptr[j + 1];
+#pragma unroll 1
+  for (int p = g.vt_ptr[j]; p < p1; ++p) {
+    const int2 tl = g.vt_tri[p];
+    const int tau = tl.x, local = tl.y;
+    if (tau == a.w) continue;
+    const int4 b = g.tvx[tau];
+    int ra = 0, rb = 0;
+    const int pc = TOUCH ? gal_classify(a, b, ra, rb) : 0;
+    const double4 cb = g.tce[tau], nb = g.tna[tau];
+    const int B[3] = {b.x, b.y, b.z};
+    const int xp0 = ra, xp1 = (ra + 1) % 3, xp2 = (ra + 2) % 3;
+    int yp0 = rb, yp1 = (rb + 1) % 3;
+    const int yp2 = (rb + 2) % 3;
+    if (pc == 2) {
+      const int t = yp0;
+      yp0 = yp1;
+      yp1 = t;
+    }
+    const double4 X0 = g.vtx[A[xp0]], X1 = g.vtx[A[xp1]], X2 = g.vtx[A[xp2]];
+    const double4 Y0 = g.vtx[B[yp0]], Y1 = g.vtx[B[yp1]], Y2 = g.vtx[B[yp2]];
+    const double x0[3] = {X0.x, X0.y, X0.z}, y0[3] = {Y0.x, Y0.y, Y0.z};
+    const double ex1[3] = {X1.x - X0.x, X1.y - X0.y, X1.z - X0.z};
+    const double ex2[3] = {X2.x - X0.x, X2.y - X0.y, X2.z - X0.z};
+    const double ey1[3] = {Y1.x - Y0.x, Y1.y - Y0.y, Y1.z - Y0.z};
+    const double ey2[3] = {Y2.x - Y0.x, Y2.y - Y0.y, Y2.z - Y0.z};
+    // which rotated coordinate carries psi_node (kernels.cpp:119-123)
+    const int role = local == yp0 ? 0 : (local == yp1 ? 1 : 2);
+    double acc = 0.0;
+    auto point = [&](double a1, double a2, double b1, double b2, double w) {
+      double d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        d[c] = fma(a2, ex2[c], fma(a1, ex1[c], x0[c])) - fma(b2, ey2[c], fma(b1, ey1[c], y0[c]));
+      const double ri = rsqrt_canon(fma(d[2], d[2], fma(d[1], d[1], d[0] * d[0])));
+      const double w3 = w * ri * ri * ri;
+      const double dn = fma(d[2], nb.z, fma(d[1], nb.y, d[0] * nb.x));
+      const double bv = role == 0 ? (1.0 - b1) - b2 : (role == 1 ? b1 : b2);
+      acc = fma(w3, dn * bv, acc);
+    };
+    if (pc == 0) {
+      const int t = gal_tier(ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w);
+      const int n = c_rules.n[t];
+      nq_acc += n * n;
+#pragma unroll 1
+      for (int qi = 0; qi < n; ++qi) {
+        const double a1 = c_rules.a[t][qi], a2 = c_rules.b[t][qi], wi = c_rules.w[t][qi];
+#pragma unroll 1
+        for (int qj = 0; qj < n; ++qj)
+          point(a1, a2, c_rules.a[t][qj], c_rules.b[t][qj], wi * c_rules.w[t][qj]);
+      }
+    } else {
+      const int n = g.pr_n[pc];
+      const double* r = g.prule + g.pr_off[pc];
+      const long long T = g.prule_total;
+      nq_acc += n;
+#pragma unroll 1
+      for (int q = 0; q < n; ++q) point(r[q], r[T + q], r[2 * T + q], r[3 * T + q], r[4 * T + q]);
+    }
+    total += 4.0 * na.w * nb.w * (1.0 / (4.0 * M_PI)) * acc;
+  }
+  return total;
+}
+
 // Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact
 __device__ __forceinline__ double newton_entry(const Geom& g, int i, int j) {
   const double4 a = g.rowpt[i];
@@ -483,6 +565,7 @@ __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
   int nq = 0;
   if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq);
   if (g.kind == KIND_GALERKIN) return galerkin_entry1<true>(g, i, j, g.gal_delta ? 6 : comp, nq);
+  if (g.kind == KIND_KDELTA) return kdelta_entry<true>(g, i, j, nq);
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -495,6 +578,7 @@ __device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
   if (KIND == KIND_KELVIN) return kelvin_entry1<false>(g, i, j, comp, nq_acc);
   if (KIND == KIND_GALERKIN)
     return galerkin_entry1<false>(g, i, j, g.gal_delta ? 6 : comp, nq_acc);
+  if (KIND == KIND_KDELTA) return kdelta_entry<false>(g, i, j, nq_acc);
   if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }

@@ -241,6 +241,18 @@ int hmb_op_galerkin(const hmb_mesh* m, int which, int b_min, double eta, int dev
   });
 }
 
+int hmb_op_kdelta(const hmb_mesh* m, int b_min, double eta, int device, int shard_rank,
+                  int shard_count, hmb_op** out) {
+  return guard([&] {
+    need(m, "mesh");
+    need(out, "out");
+    auto op = std::make_unique<hmb_op>();
+    op->op = hmb::HOperator::kdelta(m->mesh, b_min, eta, device,
+                                    hmb::Shard{shard_rank, shard_count});
+    *out = op.release();
+  });
+}
+
 int hmb_op_newton(int n, const double* pts, const double* boxes6, double diag,
                   int b_min, double eta, int device, hmb_op** out) {
   return guard([&] {

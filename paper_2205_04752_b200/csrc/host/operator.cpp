@@ -195,6 +195,55 @@ std::unique_ptr<HOperator> HOperator::galerkin(const Mesh& mesh, int which, int 
   return op;
 }
 
+std::unique_ptr<HOperator> HOperator::kdelta(const Mesh& mesh, int b_min, Real eta,
+                                             int device, Shard shard, QuadratureConfig qc,
+                                             GalerkinQuadrature gq) {
+  if (mesh.centroids.size() != mesh.triangles.size())
+    throw MeshError("mesh geometry caches missing (call finish())");
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = KDelta;
+  op->ncomp_ = 1;
+  op->n_rows_ = mesh.nt();
+  op->n_cols_ = mesh.nv();
+  const std::vector<Box> tb = triangle_supports(mesh);
+  std::vector<Box> nb(mesh.nv());
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int k = 0; k < 3; ++k) nb[mesh.triangles[t][k]].absorb(tb[t]);
+  op->rows_ = std::make_unique<ClusterTree>(build_cluster_tree(tb, b_min));
+  op->cols_ = std::make_unique<ClusterTree>(build_cluster_tree(nb, b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  std::vector<double> verts(3 * mesh.nv()), cen(3 * mesh.nt()), nrm(3 * mesh.nt());
+  std::vector<int> tris(3 * mesh.nt());
+  for (int v = 0; v < mesh.nv(); ++v)
+    for (int d = 0; d < 3; ++d) verts[3 * v + d] = mesh.vertices[v][d];
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int d = 0; d < 3; ++d) {
+      tris[3 * t + d] = mesh.triangles[t][d];
+      cen[3 * t + d] = mesh.centroids[t][d];
+      nrm[3 * t + d] = mesh.normals[t][d];
+    }
+  op->check(hmgpu_set_kdelta_geometry(op->ctx_, mesh.nv(), verts.data(), mesh.nt(),
+                                      tris.data(), cen.data(), mesh.areas.data(),
+                                      mesh.diam.data(), nrm.data()),
+            "hmgpu_set_kdelta_geometry");
+  for (int tier = 0; tier < 3; ++tier) {
+    const TriangleRule r = gauss_rule(qc.tier_order(tier));
+    op->check(hmgpu_set_rule(op->ctx_, tier, static_cast<int>(r.w.size()), r.a.data(),
+                             r.b.data(), r.w.data()),
+              "hmgpu_set_rule");
+  }
+  for (int pc = 1; pc <= 3; ++pc) {
+    const PairRuleTable r = singular_pair_rule(
+        pc, gq.singular_order + (pc == 3 ? gq.identical_bump : 0));
+    op->check(hmgpu_set_pair_rule(op->ctx_, pc, static_cast<int>(r.w.size()), r.xr1.data(),
+                                  r.xr2.data(), r.yr1.data(), r.yr2.data(), r.w.data()),
+              "hmgpu_set_pair_rule");
+  }
+  return op;
+}
+
 std::unique_ptr<HOperator> HOperator::newton(const std::vector<V3>& pts,
                                              const std::vector<Box>* boxes,
                                              Real diag, int b_min, Real eta,

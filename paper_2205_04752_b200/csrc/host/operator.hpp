@@ -50,7 +50,7 @@ struct Shard {
 
 class HOperator {
  public:
-  enum Kind { Kelvin = 0, Newton = 1, Dense = 2, Galerkin = 3 };
+  enum Kind { Kelvin = 0, Newton = 1, Dense = 2, Galerkin = 3, KDelta = 4 };
 
   // Kelvin single-layer collocation at triangle centroids: one cluster tree
   // over the triangle support boxes for rows and columns
@@ -65,6 +65,12 @@ class HOperator {
                                              Real eta, int device, Shard shard = {},
                                              QuadratureConfig qc = {},
                                              GalerkinQuadrature gq = {});
+  // K_Delta on the triangle x node partition (operators.cpp:186-200):
+  // rows triangles, columns vertices (kernels.cpp:151-167)
+  static std::unique_ptr<HOperator> kdelta(const Mesh& mesh, int b_min, Real eta,
+                                           int device, Shard shard = {},
+                                           QuadratureConfig qc = {},
+                                           GalerkinQuadrature gq = {});
   // scalar Newton kernel over points; boxes == nullptr => point boxes
   static std::unique_ptr<HOperator> newton(const std::vector<V3>& pts,
                                            const std::vector<Box>* boxes,

@@ -125,3 +125,42 @@ def test_cta_mode_bit_identical(gal):
                          text=True, check=True).stdout.split()
     assert out[0] == y.tobytes().hex()
     assert out[1] == g.ranks()[1].tobytes().hex()
+
+
+@pytest.fixture(scope="module")
+def kdelta():
+    mesh = hm.Mesh.icosphere(3)
+    a = mesh.arrays()
+    eps = 1e-5
+    g = hm.HMatrix.kdelta(mesh, b_min=32, eta=1.0, device=0)
+    g.assemble(eps=eps, beta=0.8, lookahead=2)
+    o = orc.Problem.kdelta(a["vertices"], a["triangles"], b_min=32, eta=1.0)
+    o.assemble(eps=eps, beta=0.8, lookahead=2)
+    return dict(g=g, o=o, eps=eps)
+
+
+def test_kdelta_partition_and_nearfield(kdelta):
+    g, o = kdelta["g"], kdelta["o"]
+    assert g.partition_json() == o.partition_json()
+    rnodes, cnodes = g.tree(0).nodes, g.tree(1).nodes
+    for b, (rn, cn, adm, _) in enumerate(g.partition_blocks()):
+        if adm:
+            continue
+        m = rnodes[rn, 1] - rnodes[rn, 0]
+        n = cnodes[cn, 1] - cnodes[cn, 0]
+        assert (g.dense_block(0, b) == o.dense_block(0, b, m, n)).all(), b
+
+
+def test_kdelta_ranks_factors_matvec(kdelta):
+    g, o, eps = kdelta["g"], kdelta["o"], kdelta["eps"]
+    gk, gl, gc, _ = g.ranks()
+    ok, ol, oc, _ = o.ranks()
+    assert (gk == ok).all() and (gl == ol).all() and (gc == oc).all()
+    adm = np.nonzero(g.partition_blocks()[:, 2])[0]
+    for b in adm[:: max(1, len(adm) // 30)]:
+        fg, fo = g.factor(0, b), o.factor(0, b)
+        assert (fg["U"] == fo["U"]).all() and (fg["V"] == fo["V"]).all()
+    x = RV(g.cols, 2)
+    y = g.matvec(x)
+    assert rel(y, o.matvec(x)) <= 1e-12
+    assert rel(y, o.dense(0) @ x) <= 10 * eps

@@ -150,3 +150,93 @@ def test_galerkin_hmatrix_vs_dense(cube3):  # test_hmatrix.cpp:76-90 on V_Delta 
         y = p.matvec(x)
         yd = p.dense_grid() @ x
         assert np.linalg.norm(y - yd) <= 10 * eps * np.linalg.norm(yd)
+
+
+# ---------------------------------------------------------------------------
+# K_Delta (triangles x nodes, kernels.cpp:151-167)
+@pytest.fixture(scope="module")
+def kd3():
+    m = cube_mesh(3)
+    a = m.arrays()
+    return a, orc.Problem.kdelta(a["vertices"], a["triangles"], b_min=8, eta=1.0)
+
+
+def _vertex_triangles(T, nv):
+    vt = [[] for _ in range(nv)]
+    for t, tri in enumerate(T):
+        for v in tri:
+            vt[v].append(t)
+    return vt
+
+
+def _kdelta_bruteforce(V, T, i, node, vt):  # test_kernels.cpp:103-118
+    acc = 0.0
+    for tau in vt[node]:
+        if tau == i:
+            continue
+        local = list(T[tau]).index(node)
+        c = V[T[tau]]
+        e0, e1 = c[1] - c[0], c[2] - c[0]
+        nrm = np.cross(e0, e1)
+        nrm = nrm / np.linalg.norm(nrm)
+        a00, a01, a11 = e0 @ e0, e0 @ e1, e1 @ e1
+        det = a00 * a11 - a01 * a01
+
+        def k(X, Y, c=c, e0=e0, e1=e1, nrm=nrm, local=local):
+            d = X - Y
+            r = np.linalg.norm(d, axis=-1)
+            rel_ = Y - c[0]
+            b1 = (a11 * (rel_ @ e0) - a01 * (rel_ @ e1)) / det
+            b2 = (a00 * (rel_ @ e1) - a01 * (rel_ @ e0)) / det
+            bary = [1.0 - b1 - b2, b1, b2][local]
+            return (d @ nrm) / (4.0 * np.pi * r ** 3) * bary
+
+        acc += ref.bruteforce_pair_integral(V[T[i]], c, k, 8)
+    return acc
+
+
+def test_kdelta_separated_matches_subdivision(kd3):  # test_kernels.cpp:150-170
+    a, kd = kd3
+    V, T = a["vertices"], a["triangles"]
+    vt = _vertex_triangles(T, len(V))
+    checked = 0
+    for v in range(len(V)):
+        if checked >= 4:
+            break
+        if any(t == 0 or orc.classify_pair(T[0], T[t])[0] != 0 for t in vt[v]):
+            continue
+        want = _kdelta_bruteforce(V, T, 0, v, vt)
+        if abs(want) < 1e-12:
+            continue
+        assert doctest_approx(kd.entry(0, 0, v), want, 1e-6)
+        checked += 1
+    assert checked >= 3
+
+
+def test_kdelta_vanishes_on_coplanar_pairs(kd3):  # test_kernels.cpp:242-254
+    a, kd = kd3
+    V, T, N, Cc = a["vertices"], a["triangles"], a["normals"], a["centroids"]
+    vt = _vertex_triangles(T, len(V))
+    for t in range(len(T)):
+        node = T[t][0]
+        if all(np.linalg.norm(N[u] - N[t]) < 1e-14 and abs((Cc[u] - Cc[t]) @ N[t]) < 1e-14
+               for u in vt[node]):
+            assert abs(kd.entry(0, t, node)) < 1e-14
+            return
+    pytest.fail("no coplanar witness found")
+
+
+def test_kdelta_canonical_matches_literal_and_hmatrix(kd3):
+    a, kd = kd3
+    rng = np.random.default_rng(1)
+    D = kd.dense(0)
+    scale = np.abs(D).max()
+    for _ in range(40):
+        i = int(rng.integers(0, D.shape[0]))
+        j = int(rng.integers(0, D.shape[1]))
+        assert abs(kd.entry(0, i, j) - kd.entry_literal(0, i, j)) <= 1e-13 * scale
+    eps = 1e-6
+    kd.assemble(eps=eps, beta=0.8)
+    x = orc.random_vector(D.shape[1], 4)
+    y = kd.matvec(x)
+    assert np.linalg.norm(y - D @ x) <= 10 * eps * np.linalg.norm(D @ x)
