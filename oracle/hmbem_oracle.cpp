@@ -530,6 +530,18 @@ struct PairRule {
   std::vector<Real> xr1, xr2, yr1, yr2, w;
 };
 
+// 32 partial sums combined by the xor butterfly (the device's warp_sum)
+static Real butterfly32(const Real* p0) {
+  Real p[32];
+  std::copy(p0, p0 + 32, p);
+  for (int o = 16; o > 0; o >>= 1) {
+    Real q[32];
+    for (int l = 0; l < 32; ++l) q[l] = p[l] + p[l ^ o];
+    std::copy(q, q + 32, p);
+  }
+  return p[0];
+}
+
 // Sauter-Schwab maps [0,1]^4 -> pairs of reference coordinates
 // (quadrature.cpp:177-286), same expressions and association
 static void ss_map(int c, Real xi, Real e1, Real e2, Real e3, int s, Real* p) {
@@ -664,8 +676,14 @@ struct Galerkin {
     const Vec3 y0 = mesh->corner(j, yp[0]), y1 = mesh->corner(j, yp[1]),
                y2 = mesh->corner(j, yp[2]);
     const Vec3 ex1 = sub(x1, x0), ex2 = sub(x2, x0), ey1 = sub(y1, y0), ey2 = sub(y2, y0);
-    Real ad = 0.0, akl[6] = {0, 0, 0, 0, 0, 0};
+    // disjoint pairs: one sequential sum in rule order; touching pairs (the
+    // Sauter-Schwab tables, up to 39366 points): warp order, i.e. 32
+    // lane-strided partial sums (point q into partial q % 32, in order)
+    // combined by the xor butterfly, so that a warp shares one pair
+    const int nl = pc == kDisjoint ? 1 : 32;
+    Real ad[32] = {0}, akl[32][6] = {{0}};
     for (size_t q = 0; q < r.w.size(); ++q) {
+      const int l = static_cast<int>(q % nl);
       const Real a1 = r.xr1[q], a2 = r.xr2[q], b1 = r.yr1[q], b2 = r.yr2[q];
       Real d[3];
       for (int c = 0; c < 3; ++c)
@@ -674,12 +692,21 @@ struct Galerkin {
       const Real ri = rsqrt_canon(std::fma(d[2], d[2], std::fma(d[1], d[1], d[0] * d[0])));
       const Real wr = r.w[q] * ri;
       const Real w3 = wr * ri * ri;
-      ad = ad + wr;
-      for (int k = 0; k < 6; ++k) akl[k] = std::fma(w3, d[kCompR[k]] * d[kCompC[k]], akl[k]);
+      ad[l] = ad[l] + wr;
+      for (int k = 0; k < 6; ++k)
+        akl[l][k] = std::fma(w3, d[kCompR[k]] * d[kCompC[k]], akl[l][k]);
+    }
+    if (nl == 32) {
+      Real t[32];
+      ad[0] = butterfly32(ad);
+      for (int k = 0; k < 6; ++k) {
+        for (int l = 0; l < 32; ++l) t[l] = akl[l][k];
+        akl[0][k] = butterfly32(t);
+      }
     }
     const Real f = 4.0 * mesh->areas[i] * mesh->areas[j] * (1.0 / (4.0 * M_PI));
-    for (int k = 0; k < 6; ++k) out7[k] = f * akl[k];
-    out7[6] = f * ad;
+    for (int k = 0; k < 6; ++k) out7[k] = f * akl[0][k];
+    out7[6] = f * ad[0];
   }
   Real entry(int i, int j, int comp) const {
     Real o[7];
@@ -691,8 +718,9 @@ struct Galerkin {
   // load_mesh's vertex_triangles, mesh.cpp:245-247), tau != i, of
   // integrate_pair(i, tau) of (x-y).n(tau) / (4 pi |x-y|^3) psi_node(y)
   // (kernels.cpp:151-167; no orientation swap).  Canonical order: per pair
-  // sum_q fma(w / r^3, ((x-y).n) * bary_local, .), the 4 area area / (4 pi)
-  // scale per pair, pairs summed in tau order.
+  // sum_q fma(w / r^3, ((x-y).n) * bary_local, .) (warp order for touching
+  // pairs, as entry7), the 4 area area / (4 pi) scale per pair, pairs summed
+  // in tau order.
   std::vector<std::vector<int>> vtri;
   void build_vtri() {
     vtri.assign(mesh->vertices.size(), {});
@@ -715,7 +743,8 @@ struct Galerkin {
       const Vec3 y0 = mesh->corner(tau, yp[0]), y1 = mesh->corner(tau, yp[1]),
                  y2 = mesh->corner(tau, yp[2]);
       const Vec3 ex1 = sub(x1, x0), ex2 = sub(x2, x0), ey1 = sub(y1, y0), ey2 = sub(y2, y0);
-      Real acc = 0.0;
+      const int nl = pc == kDisjoint ? 1 : 32;  // warp order for touching pairs
+      Real part[32] = {0};
       for (size_t q = 0; q < r.w.size(); ++q) {
         const Real a1 = r.xr1[q], a2 = r.xr2[q], b1 = r.yr1[q], b2 = r.yr2[q];
         Real d[3];
@@ -727,8 +756,10 @@ struct Galerkin {
         const Real dn = std::fma(d[2], nrm[2], std::fma(d[1], nrm[1], d[0] * nrm[0]));
         // barycentric of y w.r.t. the original vertex order (kernels.cpp:119-123)
         const Real bv = local == yp[0] ? (1.0 - b1) - b2 : local == yp[1] ? b1 : b2;
-        acc = std::fma(w3, dn * bv, acc);
+        const int l = static_cast<int>(q % nl);
+        part[l] = std::fma(w3, dn * bv, part[l]);
       }
+      const Real acc = nl == 32 ? butterfly32(part) : part[0];
       total += 4.0 * mesh->areas[i] * mesh->areas[tau] * (1.0 / (4.0 * M_PI)) * acc;
     }
     return total;

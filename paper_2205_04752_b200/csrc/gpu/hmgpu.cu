@@ -1989,7 +1989,14 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     if (!c->dblocks.empty()) {
       c->timed("nearfield", [&] {
         const int grid = grid_for(c, (long long)c->dblocks.size(), 8);
-        if (c->NC == 6)
+        const bool gal = c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA;
+        if (gal && c->NC == 6)
+          nearfield_gal_kernel<6><<<grid, 256, 0, c->stream>>>(
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p, c->d_nq.p);
+        else if (gal)
+          nearfield_gal_kernel<1><<<grid, 256, 0, c->stream>>>(
+              c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p, c->d_nq.p);
+        else if (c->NC == 6)
           nearfield_kernel<6><<<grid, 256, 0, c->stream>>>(
               c->geom, c->d_dblocks.p, (int)c->dblocks.size(), c->d_dense.p, c->d_nq.p);
         else

@@ -292,6 +292,8 @@ __device__ __forceinline__ void kelvin_entry6(const Geom& g, int i, int j,
 // area_j / (4 pi) factored out).  Components: 0..5 V_kl (c_comp_r/c_comp_c),
 // 6 V_Delta.
 
+__device__ __forceinline__ double warp_sum(double v);
+
 // classify_pair (quadrature.cpp:127-156) on global vertex ids; returns the
 // case and the rotations
 __device__ __forceinline__ int gal_classify(const int4& a, const int4& b, int& ra, int& rb) {
@@ -412,10 +414,12 @@ __device__ __forceinline__ void gal_point(const GalPair& P, double a1, double a2
 }
 
 // pair sum in rule order (disjoint: test point outer, trial inner, weight
-// w_i w_j; touching: the table order)
-template <int COMP>
+// w_i w_j, one sequential sum; touching: the table in the canonical warp
+// order -- lane l accumulates points l, l + 32, ... and the 32 partials are
+// combined by the xor butterfly -- run by a whole warp, WARP = true)
+template <int COMP, bool WARP = false>
 __device__ __forceinline__ void gal_sum(const Geom& g, const GalPair& P, double& ad,
-                                        double* akl, int& nq_acc) {
+                                        double* akl, int& nq_acc, int lane = 0) {
   if (P.pc == 0) {
     const int t = P.tier;
     const int n = c_rules.n[t];
@@ -428,22 +432,29 @@ __device__ __forceinline__ void gal_sum(const Geom& g, const GalPair& P, double&
         gal_point<COMP>(P, a1, a2, c_rules.a[t][qj], c_rules.b[t][qj], wi * c_rules.w[t][qj],
                         ad, akl);
     }
-  } else {
+  } else if (WARP) {
     const int n = g.pr_n[P.pc];
     const double* r = g.prule + g.pr_off[P.pc];
     const long long T = g.prule_total;
-    nq_acc += n;
+    if (lane == 0) nq_acc += n;
 #pragma unroll 1
-    for (int q = 0; q < n; ++q)
+    for (int q = lane; q < n; q += 32)
       gal_point<COMP>(P, r[q], r[T + q], r[2 * T + q], r[3 * T + q], r[4 * T + q], ad, akl);
+    if (COMP == 6 || COMP < 0) ad = warp_sum(ad);
+    if (COMP < 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) akl[k] = warp_sum(akl[k]);
+    } else if (COMP != 6) {
+      akl[0] = warp_sum(akl[0]);
+    }
   }
 }
 
-// one component (ACA rows / columns); comp 0..5 = V_kl, 6 = V_Delta
-template <bool TOUCH>
+// one component of a disjoint pair (ACA rows / columns of admissible
+// blocks); comp 0..5 = V_kl, 6 = V_Delta
 __device__ __forceinline__ double galerkin_entry1(const Geom& g, int i, int j, int comp,
                                                   int& nq_acc) {
-  const GalPair P = gal_setup<TOUCH>(g, i, j);
+  const GalPair P = gal_setup<false>(g, i, j);
   double ad = 0.0, akl[1] = {0.0};
   switch (comp) {  // group-uniform
     case 0: gal_sum<0>(g, P, ad, akl, nq_acc); break;
@@ -457,12 +468,20 @@ __device__ __forceinline__ double galerkin_entry1(const Geom& g, int i, int j, i
   return P.scale * akl[0];
 }
 
-// all seven components of a pair (near-field fill): out7[0..5] V_kl, [6] V_Delta
+// all seven components of a pair (near-field fill): out7[0..5] V_kl, [6]
+// V_Delta.  WARP = false: a disjoint pair by one thread; true: any pair by a
+// whole warp (touching pairs in the warp order; every lane gets the result)
+template <bool WARP>
 __device__ __forceinline__ void galerkin_entry7(const Geom& g, int i, int j, double* out7,
-                                                int& nq_acc) {
-  const GalPair P = gal_setup<true>(g, i, j);
+                                                int& nq_acc, int lane) {
+  const GalPair P = gal_setup<WARP>(g, i, j);
   double ad = 0.0, akl[6] = {0, 0, 0, 0, 0, 0};
-  gal_sum<-1>(g, P, ad, akl, nq_acc);
+  if (WARP && P.pc == 0) {
+    int dummy = 0;
+    gal_sum<-1>(g, P, ad, akl, lane == 0 ? nq_acc : dummy);
+  } else {
+    gal_sum<-1, WARP>(g, P, ad, akl, nq_acc, lane);
+  }
 #pragma unroll
   for (int k = 0; k < 6; ++k) out7[k] = P.scale * akl[k];
   out7[6] = P.scale * ad;
@@ -473,9 +492,12 @@ __device__ __forceinline__ void galerkin_entry7(const Geom& g, int i, int j, dou
 // (kernels.cpp:151-167, no orientation swap), in the oracle's canonical
 // order (Galerkin::kdelta): per pair sum_q fma(w / r^3, ((x-y).n) bary, .),
 // scaled by 4 area_i area_tau / (4 pi), pairs summed in tau order.
-// TOUCH = false: admissible blocks (no triangle of the node touches i).
-template <bool TOUCH>
-__device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int& nq_acc) {
+// WARP = false: no triangle of the node touches i (admissible blocks, and
+// the near field's thread pass), one thread; true: a whole warp, touching
+// pairs summed in the canonical warp order (every lane gets the result).
+template <int WARP>
+__device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int& nq_acc,
+                                               int lane) {
   const int4 a = g.tvid[i];
   const double4 ca = g.tce[a.w], na = g.tna[a.w];
   const int A[3] = {a.x, a.y, a.z};
@@ -488,7 +510,7 @@ __device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int&
     if (tau == a.w) continue;
     const int4 b = g.tvx[tau];
     int ra = 0, rb = 0;
-    const int pc = TOUCH ? gal_classify(a, b, ra, rb) : 0;
+    const int pc = WARP ? gal_classify(a, b, ra, rb) : 0;
     const double4 cb = g.tce[tau], nb = g.tna[tau];
     const int B[3] = {b.x, b.y, b.z};
     const int xp0 = ra, xp1 = (ra + 1) % 3, xp2 = (ra + 2) % 3;
@@ -523,7 +545,7 @@ __device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int&
     if (pc == 0) {
       const int t = gal_tier(ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w);
       const int n = c_rules.n[t];
-      nq_acc += n * n;
+      if (!WARP || lane == 0) nq_acc += n * n;
 #pragma unroll 1
       for (int qi = 0; qi < n; ++qi) {
         const double a1 = c_rules.a[t][qi], a2 = c_rules.b[t][qi], wi = c_rules.w[t][qi];
@@ -535,13 +557,30 @@ __device__ __forceinline__ double kdelta_entry(const Geom& g, int i, int j, int&
       const int n = g.pr_n[pc];
       const double* r = g.prule + g.pr_off[pc];
       const long long T = g.prule_total;
-      nq_acc += n;
+      if (lane == 0) nq_acc += n;
 #pragma unroll 1
-      for (int q = 0; q < n; ++q) point(r[q], r[T + q], r[2 * T + q], r[3 * T + q], r[4 * T + q]);
+      for (int q = lane; q < n; q += 32)
+        point(r[q], r[T + q], r[2 * T + q], r[3 * T + q], r[4 * T + q]);
+      acc = warp_sum(acc);
     }
     total += 4.0 * na.w * nb.w * (1.0 / (4.0 * M_PI)) * acc;
   }
   return total;
+}
+
+// does the pair (row i, column j) need the touching-pair rules?
+__device__ __forceinline__ bool gal_touching(const Geom& g, int i, int j) {
+  int ra, rb;
+  return gal_classify(g.tvid[i], g.tvid[j], ra, rb) != 0;
+}
+__device__ __forceinline__ bool kd_touching(const Geom& g, int i, int j) {
+  const int4 a = g.tvid[i];
+  for (int p = g.vt_ptr[j]; p < g.vt_ptr[j + 1]; ++p) {
+    const int tau = g.vt_tri[p].x;
+    int ra, rb;
+    if (tau != a.w && gal_classify(a, g.tvx[tau], ra, rb) != 0) return true;
+  }
+  return false;
 }
 
 // Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact
@@ -564,8 +603,6 @@ __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
                                          int comp) {
   int nq = 0;
   if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq);
-  if (g.kind == KIND_GALERKIN) return galerkin_entry1<true>(g, i, j, g.gal_delta ? 6 : comp, nq);
-  if (g.kind == KIND_KDELTA) return kdelta_entry<true>(g, i, j, nq);
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -577,8 +614,8 @@ __device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
                                           int& nq_acc) {
   if (KIND == KIND_KELVIN) return kelvin_entry1<false>(g, i, j, comp, nq_acc);
   if (KIND == KIND_GALERKIN)
-    return galerkin_entry1<false>(g, i, j, g.gal_delta ? 6 : comp, nq_acc);
-  if (KIND == KIND_KDELTA) return kdelta_entry<false>(g, i, j, nq_acc);
+    return galerkin_entry1(g, i, j, g.gal_delta ? 6 : comp, nq_acc);
+  if (KIND == KIND_KDELTA) return kdelta_entry<0>(g, i, j, nq_acc, 0);
   if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -1271,11 +1308,6 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
         double e[6];
         if (g.kind == KIND_KELVIN) {
           kelvin_entry6(g, b.row0 + i, b.col0 + j, e, nq_acc);
-        } else if (g.kind == KIND_GALERKIN) {
-          double e7[7];
-          galerkin_entry7(g, b.row0 + i, b.col0 + j, e7, nq_acc);
-#pragma unroll
-          for (int c = 0; c < 6; ++c) e[c] = e7[c];
         } else {
           const double v = entry1(g, b.row0 + i, b.col0 + j, 0);
 #pragma unroll
@@ -1283,13 +1315,73 @@ nearfield_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
         }
 #pragma unroll
         for (int c = 0; c < 6; ++c) D[(long long)j * cp + c * b.m + i] = e[c];
-      } else if (g.kind == KIND_GALERKIN) {
-        double e7[7];
-        galerkin_entry7(g, b.row0 + i, b.col0 + j, e7, nq_acc);
-        D[(long long)j * cp + i] = e7[6];
       } else {
         D[(long long)j * cp + i] = entry1(g, b.row0 + i, b.col0 + j, 0);
       }
+    }
+  }
+  unsigned long long t = (unsigned long long)nq_acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(nq_total, t);
+}
+
+// Galerkin near field (V_kl grid: NC = 6, V_Delta / K_Delta: NC = 1): a
+// thread per disjoint pair (sequential sum), then a warp per touching pair
+// (the Sauter-Schwab tables, up to 39366 points, in the canonical warp
+// order).  Pairs are taken in chunks of GAL_CHUNK; the touching ones of a
+// chunk are listed in shared memory for the warp pass.
+constexpr int GAL_CHUNK = 1024;
+template <int NC>
+__global__ void __launch_bounds__(256)
+nearfield_gal_kernel(Geom g, const DenseBlock* __restrict__ blocks, int nblocks,
+                     double* __restrict__ dense, unsigned long long* __restrict__ nq_total) {
+  __shared__ int tlist[GAL_CHUNK];
+  __shared__ int tcount;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool kd = g.kind == KIND_KDELTA;
+  int nq_acc = 0;
+  for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
+    const DenseBlock b = blocks[bi];
+    const int mn = b.m * b.n;
+    const int cp = (b.m * NC + 1) & ~1;  // column pitch, 16-byte multiple
+    double* D = dense + b.off;
+    auto store = [&](int i, int j, const double* e7) {
+      if (NC == 6) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) D[(long long)j * cp + c * b.m + i] = e7[c];
+      } else {
+        D[(long long)j * cp + i] = e7[6];
+      }
+    };
+    for (int c0 = 0; c0 < mn; c0 += GAL_CHUNK) {
+      const int c1 = min(mn, c0 + GAL_CHUNK);
+      if (threadIdx.x == 0) tcount = 0;
+      __syncthreads();
+      for (int p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+        const int i = p % b.m, j = p / b.m;
+        const bool touch = kd ? kd_touching(g, b.row0 + i, b.col0 + j)
+                              : gal_touching(g, b.row0 + i, b.col0 + j);
+        if (touch) {
+          tlist[atomicAdd(&tcount, 1)] = p;
+          continue;
+        }
+        double e7[7];
+        if (kd) e7[6] = kdelta_entry<0>(g, b.row0 + i, b.col0 + j, nq_acc, lane);
+        else galerkin_entry7<false>(g, b.row0 + i, b.col0 + j, e7, nq_acc, lane);
+        store(i, j, e7);
+      }
+      __syncthreads();
+      const int nt = tcount;
+      for (int t = warp; t < nt; t += blockDim.x >> 5) {
+        const int p = tlist[t];
+        const int i = p % b.m, j = p / b.m;
+        double e7[7];
+        if (kd) e7[6] = kdelta_entry<1>(g, b.row0 + i, b.col0 + j, nq_acc, lane);
+        else galerkin_entry7<true>(g, b.row0 + i, b.col0 + j, e7, nq_acc, lane);
+        if (lane == 0) store(i, j, e7);
+      }
+      __syncthreads();
     }
   }
   unsigned long long t = (unsigned long long)nq_acc;
