@@ -62,6 +62,11 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
                  double* areas, double* normals, double* diam, int* dirichlet);
 void hmb_mesh_free(hmb_mesh* m);
 
+/* sparse transforms of build_sparse_ops (operators.cpp:7-95) in ELL form:
+ * n_tri rows x 3 slots (slot a = local vertex a, value 0 where the reference
+ * drops the entry).  which: 0 T12, 1 T13, 2 T23, 3 mass (area / 3). */
+int hmb_sparse_op(const hmb_mesh* m, int which, int* cols3, double* vals3);
+
 /* seeded synthetic input: kind 0 = uniform [-1,1) (mt19937_64, the
  * reference's random_vector, oracles.cpp:415-421), 1 = standard normal */
 int hmb_random_vector(long long n, unsigned long long seed, int kind, double* out);

@@ -18,6 +18,8 @@
  *                               proj/src/kernels.cpp:75-149), fused into the kernels
  *   hmgpu_set_kdelta_geometry  KernelOracle over K_Delta: GalerkinKernels::kdelta
  *                              (proj/src/kernels.cpp:151-167), triangles x nodes
+ *   hmgpu_ell3_spmv(_t)        SpMat products of the operator algebra (T12/T13/T23,
+ *                              mass; build_sparse_ops, proj/src/operators.cpp:7-95)
  *   hmgpu_set_pair_rule        pair_rule(PairCase, order) Sauter-Schwab tables
  *                              (proj/src/quadrature.cpp:290-338)
  *   hmgpu_set_points           test fixtures CentroidKernelOracle / PointKernelOracle
@@ -150,6 +152,19 @@ int hmgpu_set_kdelta_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts, i
 int hmgpu_set_pair_rule(hmgpu_ctx* ctx, int pair_case, int n, const double* xr1,
                         const double* xr2, const double* yr1, const double* yr2,
                         const double* w);
+/* Sparse transforms of the operator algebra (build_sparse_ops,
+ * operators.cpp:7-95) on the ctx's stream, DEVICE
+ * pointers: an ELL matrix with 3 slots per row (col3 / val3, rows x 3).
+ *   hmgpu_ell3_spmv:   y = alpha A x + beta y            (y: rows)
+ *   hmgpu_ell3_spmv_t: y = alpha A^T x + beta y          (y: cols), gathered
+ *                      per column over the inverse index tptr (cols + 1) /
+ *                      tslot (flat slot ids 3 r + a, ascending rows)
+ * beta == 0 does not read y. */
+int hmgpu_ell3_spmv(hmgpu_ctx* ctx, int rows, const int* col3, const double* val3,
+                    const double* x, double* y, double alpha, double beta);
+int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslot,
+                      const double* val3, const double* x, double* y, double alpha,
+                      double beta);
 /* scalar Newton kernel 1/|x_i - x_j| with entry `diag` where x_i == x_j */
 int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag);
 /* scalar explicit matrix, column-major m x n, external ids */

@@ -2011,6 +2011,40 @@ int or_problem_kdelta(int nv, const double* verts, int nt, const int* tris, int 
   });
 }
 
+// build_t_matrix (operators.cpp:8-33) / mass (operators.cpp:82-88) as a
+// dense row-major n_tri x n_vert array; which 0 T12, 1 T13, 2 T23, 3 mass
+int or_sparse_op(int nv, const double* verts, int nt, const int* tris, int which,
+                 double* dense) {
+  return guard([&] {
+    Mesh m;
+    m.vertices.resize(nv);
+    for (int v = 0; v < nv; ++v) m.vertices[v] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]};
+    m.triangles.resize(nt);
+    for (int t = 0; t < nt; ++t) m.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    finish_geometry(m);
+    std::fill(dense, dense + static_cast<long>(nt) * nv, 0.0);
+    const int kk[3] = {0, 0, 1}, ll[3] = {1, 2, 2};
+    for (int t = 0; t < nt; ++t) {
+      if (which == 3) {
+        for (int a = 0; a < 3; ++a)
+          dense[static_cast<long>(t) * nv + m.triangles[t][a]] += m.areas[t] / 3.0;
+        continue;
+      }
+      const int k = kk[which], l = ll[which];
+      const Vec3& n = m.normals[t];
+      const Real inv2a = 1.0 / (2.0 * m.areas[t]);
+      const Vec3 c[3] = {m.corner(t, 0), m.corner(t, 1), m.corner(t, 2)};
+      Vec3 g[3] = {cross3(n, sub(c[2], c[1])), cross3(n, sub(c[0], c[2])),
+                   cross3(n, sub(c[1], c[0]))};
+      for (int a = 0; a < 3; ++a) {
+        for (int d = 0; d < 3; ++d) g[a][d] *= inv2a;
+        const Real v = n[l] * g[a][k] - n[k] * g[a][l];
+        if (v != 0.0) dense[static_cast<long>(t) * nv + m.triangles[t][a]] += v;
+      }
+    }
+  });
+}
+
 // pair_rule(case, order) tables (quadrature.cpp:290-338); NULL arrays query n
 int or_pair_rule(int pc, int order, int* n, double* xr1, double* xr2, double* yr1,
                  double* yr2, double* w) {

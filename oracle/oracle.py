@@ -136,6 +136,16 @@ def pair_rule(case: int, order: int):
     return tuple(arr)
 
 
+def sparse_op(verts, tris, which: int) -> np.ndarray:
+    """build_sparse_ops (operators.cpp:7-95) as a dense n_tri x n_vert
+    matrix: which 0 T12, 1 T13, 2 T23, 3 mass."""
+    v = np.ascontiguousarray(verts, dtype=np.float64)
+    t = np.ascontiguousarray(tris, dtype=np.int32)
+    out = np.zeros((len(t), len(v)))
+    _ck(lib().or_sparse_op(len(v), _p(v), len(t), _p(t), int(which), _p(out)))
+    return out
+
+
 def classify_pair(a, b):
     """classify_pair + test/trial vertex perms (quadrature.cpp:127-166)."""
     a = np.ascontiguousarray(a, dtype=np.int32)

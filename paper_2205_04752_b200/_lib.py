@@ -58,6 +58,9 @@ _sig(host, "hmb_random_vector", I, LL, C.c_ulonglong, I, P)
 _sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_galerkin", I, P, I, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_kdelta", I, P, I, D, I, I, I, C.POINTER(P))
+_sig(host, "hmb_sparse_op", I, P, I, P, P)
+_sig(gpu, "hmgpu_ell3_spmv", I, P, I, P, P, P, P, D, D)
+_sig(gpu, "hmgpu_ell3_spmv_t", I, P, I, P, P, P, P, P, D, D)
 _sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_dense", I, I, I, P, P, P, I, D, I, C.POINTER(P))
 _sig(host, "hmb_op_free", None, P)

@@ -559,6 +559,204 @@ class LameSingleLayer:
         return s * ((3.0 - 4.0 * self.nu) * yd + yg)
 
 
+def lame_constants(E: float, nu: float):
+    """lambda = E nu / ((1+nu)(1-2nu)), mu = E / (2(1+nu)) (kernels.cpp:7-14)."""
+    if E <= 0.0:
+        raise Error("lame_constants: E must be positive")
+    if not 0.0 < nu < 0.5:
+        raise Error("lame_constants: nu must lie in (0, 1/2)")
+    return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), E / (2.0 * (1.0 + nu))
+
+
+class OperatorSet:
+    """assemble_operators / OperatorSet (operators.hpp:62-96, SURVEY.md 8f
+    ranks 2-3) on the device: the Galerkin H-matrices V_Delta, V_kl (3x3
+    grid) and K_Delta, the sparse transforms T12 / T13 / T23 / mass of
+    build_sparse_ops (ELL on the device, hmgpu_ell3_spmv), and the composed
+    discrete operators
+
+      V_h = (1+nu)/(2E(1-nu)) [(3-4nu) diag3(V_Delta) + grid(V_kl)]      3M x 3M
+      K_h = diag3(K_Delta) - diag3(V_Delta) T_h + 2 mu V_h T_h           3M x 3N
+      D_h = mu sum_k S_k' diag3(V_Delta) S_k + 2 mu T_h' diag3(V_Delta) T_h
+            - 4 mu^2 T_h' V_h T_h + mu [sum_k T_kj' V_Delta T_ki]_ij      3N x 3N
+
+    (compose_Vh / compose_Kh / compose_Dh, operators.cpp:97-158), evaluated
+    on device vectors (torch) through the H-matrix and SpMV entry points.
+    M = triangles, N = vertices, component-major."""
+
+    def __init__(self, mesh: Mesh, E: float = 1.0, nu: float = 0.3, b_min: int = 32,
+                 eta: float = 1.0, device: int = 0):
+        import torch
+        self._torch = torch
+        self.E, self.nu = E, nu
+        self.lam, self.mu = lame_constants(E, nu)
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.vkl = HMatrix.galerkin(mesh, 0, b_min, eta, device)
+        self.vdelta = HMatrix.galerkin(mesh, 1, b_min, eta, device)
+        self.kdelta = HMatrix.kdelta(mesh, b_min, eta, device)
+        self.m, self.n = mesh.num_triangles, mesh.num_vertices
+        self._ctx = self.vdelta.gpu_ctx
+        self._ell = []
+        for which in range(4):  # T12, T13, T23, mass
+            cols = np.zeros(3 * self.m, np.int32)
+            vals = np.zeros(3 * self.m)
+            _check(_h.hmb_sparse_op(mesh._h, which, _ptr(cols), _ptr(vals)))
+            # inverse index for the transpose: slots by vertex, ascending rows
+            order = np.argsort(cols, kind="stable").astype(np.int32)
+            tptr = np.zeros(self.n + 1, np.int32)
+            np.cumsum(np.bincount(cols, minlength=self.n), out=tptr[1:])
+            self._ell.append(tuple(torch.tensor(a, device=self.dev)
+                                   for a in (cols, vals, tptr, order)))
+
+    def assemble(self, cfg: Optional[AssemblyConfig] = None, **kw):
+        return (self.vkl.assemble(cfg, **kw), self.vdelta.assemble(cfg, **kw),
+                self.kdelta.assemble(cfg, **kw))
+
+    # ---- device building blocks (torch float64 tensors on self.dev) ----
+    def _sync(self):
+        self._torch.cuda.synchronize(self.dev)
+
+    def _spmv(self, which: int, x, transpose: bool = False, alpha: float = 1.0):
+        # the SpMV runs on the library's stream: synchronize on both sides
+        # with torch's (the compositions are not latency-critical)
+        cols, vals, tptr, slot = self._ell[which]
+        x = x.contiguous()
+        self._sync()
+        if transpose:
+            y = self._torch.empty(self.n, dtype=self._torch.float64, device=self.dev)
+            st = _lib.gpu.hmgpu_ell3_spmv_t(self._ctx, self.n, tptr.data_ptr(), slot.data_ptr(),
+                                            vals.data_ptr(), x.data_ptr(), y.data_ptr(),
+                                            alpha, 0.0)
+        else:
+            y = self._torch.empty(self.m, dtype=self._torch.float64, device=self.dev)
+            st = _lib.gpu.hmgpu_ell3_spmv(self._ctx, self.m, cols.data_ptr(), vals.data_ptr(),
+                                          x.data_ptr(), y.data_ptr(), alpha, 0.0)
+        if st != 0:
+            raise DeviceError(_lib.gpu.hmgpu_last_error(self._ctx).decode(), st)
+        self._sync()
+        return y
+
+    def _hmv(self, h: HMatrix, x, nrhs: int = 1):
+        """y = H x for nrhs columns stored back to back (column-major)."""
+        x = x.contiguous()
+        y = self._torch.empty(h.rows * nrhs, dtype=self._torch.float64, device=self.dev)
+        self._sync()
+        h.matvec_ptr(x.data_ptr(), y.data_ptr(), nrhs)
+        self._sync()
+        return y
+
+    # T_h = [0, T12, T13; -T12, 0, T23; -T13, -T23, 0] (operators.cpp:56-70)
+    _TH = ((None, (0, 1.0), (1, 1.0)), ((0, -1.0), None, (2, 1.0)),
+           ((1, -1.0), (2, -1.0), None))
+
+    def t_h(self, x):
+        """T_h x: 3N -> 3M."""
+        n = self.n
+        self._sync()
+        out = []
+        for i in range(3):
+            acc = None
+            for j in range(3):
+                e = self._TH[i][j]
+                if e is None:
+                    continue
+                y = self._spmv(e[0], x[j * n:(j + 1) * n], alpha=e[1])
+                acc = y if acc is None else acc + y
+            out.append(acc)
+        return self._torch.cat(out)
+
+    def t_h_t(self, z):
+        """T_h' z: 3M -> 3N."""
+        m = self.m
+        self._sync()
+        out = []
+        for j in range(3):
+            acc = None
+            for i in range(3):
+                e = self._TH[i][j]
+                if e is None:
+                    continue
+                y = self._spmv(e[0], z[i * m:(i + 1) * m], transpose=True, alpha=e[1])
+                acc = y if acc is None else acc + y
+            out.append(acc)
+        return self._torch.cat(out)
+
+    # S_1 = diag3(-T23), S_2 = diag3(T13), S_3 = diag3(T12) (operators.cpp:72-77)
+    _S = ((2, -1.0), (1, 1.0), (0, 1.0))
+
+    def s_k(self, k: int, x, transpose: bool = False):
+        w, a = self._S[k]
+        blk = self.m if transpose else self.n
+        self._sync()
+        return self._torch.cat([self._spmv(w, x[c * blk:(c + 1) * blk], transpose, a)
+                                for c in range(3)])
+
+    def vh_dev(self, x):
+        """V_h x on a device vector (3M)."""
+        s = 0.5 / self.E * (1.0 + self.nu) / (1.0 - self.nu)
+        yg = self._hmv(self.vkl, x)
+        yd = self._hmv(self.vdelta, x, 3)  # diag3(V_Delta): 3 RHS
+        return s * ((3.0 - 4.0 * self.nu) * yd + yg)
+
+    def kh_dev(self, x):
+        """K_h x (3N -> 3M) = diag3(K_Delta) x - diag3(V_Delta) T_h x + 2 mu V_h T_h x."""
+        t = self.t_h(x)
+        return (self._hmv(self.kdelta, x, 3) - self._hmv(self.vdelta, t, 3)
+                + 2.0 * self.mu * self.vh_dev(t))
+
+    def dh_dev(self, x):
+        """D_h x (3N -> 3N), compose_Dh (operators.cpp:114-158)."""
+        mu, n, m = self.mu, self.n, self.m
+        y = None
+        for k in range(3):
+            z = self.s_k(k, self._hmv(self.vdelta, self.s_k(k, x), 3), transpose=True)
+            y = mu * z if y is None else y + mu * z
+        t = self.t_h(x)
+        y = y + 2.0 * mu * self.t_h_t(self._hmv(self.vdelta, t, 3))
+        y = y - 4.0 * mu * mu * self.t_h_t(self.vh_dev(t))
+        # D'_ij = sum_k s1 s2 T_kj' V_Delta T_ki (T_kk = 0, T_lk = -T_kl)
+        def t_signed(k, l):
+            if k == l:
+                return None
+            return ({(0, 1): 0, (0, 2): 1, (1, 2): 2}[(min(k, l), max(k, l))],
+                    1.0 if k < l else -1.0)
+        dg = []
+        for i in range(3):
+            acc = None
+            for j in range(3):
+                for k in range(3):
+                    tkj, tki = t_signed(k, j), t_signed(k, i)
+                    if tkj is None or tki is None:
+                        continue
+                    self._sync()
+                    u = self._spmv(tki[0], x[j * n:(j + 1) * n])
+                    w = self._spmv(tkj[0], self._hmv(self.vdelta, u), transpose=True,
+                                   alpha=tkj[1] * tki[1])
+                    acc = w if acc is None else acc + w
+            dg.append(acc)
+        return y + mu * self._torch.cat(dg)
+
+    # ---- host-vector API (numpy in / out) ----
+    def _run(self, f, x, n_in):
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (n_in,):
+            raise DimensionError("operator matvec: size")
+        xd = self._torch.tensor(x, device=self.dev)
+        y = f(xd)
+        self._sync()
+        return y.cpu().numpy()
+
+    def vh(self, x):
+        return self._run(self.vh_dev, x, 3 * self.m)
+
+    def kh(self, x):
+        return self._run(self.kh_dev, x, 3 * self.n)
+
+    def dh(self, x):
+        return self._run(self.dh_dev, x, 3 * self.n)
+
+
 def random_vector(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
     """Seeded synthetic input: mt19937_64 + uniform [-1,1) (the reference's
     random_vector) or standard normal."""

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-HOST_SOURCES = ["geometry.cpp", "cluster.cpp", "quadrature.cpp", "operator.cpp",
+HOST_SOURCES = ["geometry.cpp", "cluster.cpp", "quadrature.cpp", "operator.cpp", "sparse_ops.cpp",
                 "capi.cpp"]
 
 

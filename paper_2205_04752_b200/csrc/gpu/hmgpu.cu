@@ -1786,6 +1786,61 @@ int hmgpu_set_pair_rule(hmgpu_ctx* ctx, int pair_case, int n, const double* xr1,
   });
 }
 
+// ---- sparse transforms of the operator algebra (build_sparse_ops, ---------
+// operators.cpp:7-95): ELL with 3 slots per triangle row; the transpose
+// gathers per vertex over the inverse index (ascending triangles), so both
+// directions are deterministic (no atomics).
+namespace {
+__global__ void ell3_spmv_kernel(int rows, const int* __restrict__ col,
+                                 const double* __restrict__ val, const double* __restrict__ x,
+                                 double* __restrict__ y, double alpha, double beta) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) s = fma(val[3 * r + a], x[col[3 * r + a]], s);
+    y[r] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * y[r]);
+  }
+}
+__global__ void ell3_spmv_t_kernel(int cols, const int* __restrict__ tptr,
+                                   const int* __restrict__ tslot, const double* __restrict__ val,
+                                   const double* __restrict__ x, double* __restrict__ y,
+                                   double alpha, double beta) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < cols; v += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = tptr[v]; p < tptr[v + 1]; ++p) {
+      const int e = tslot[p];
+      s = fma(val[e], x[e / 3], s);
+    }
+    y[v] = beta == 0.0 ? alpha * s : fma(alpha, s, beta * y[v]);
+  }
+}
+}  // namespace
+
+int hmgpu_ell3_spmv(hmgpu_ctx* ctx, int rows, const int* col3, const double* val3,
+                    const double* x, double* y, double alpha, double beta) {
+  return guard(ctx, [&] {
+    if (rows < 0 || (rows > 0 && (!col3 || !val3 || !x || !y)))
+      fail(HMGPU_ERR_INVALID, "bad ell3 spmv arguments");
+    if (rows == 0) return;
+    ell3_spmv_kernel<<<grid_for(ctx, (rows + 255) / 256), 256, 0, ctx->stream>>>(
+        rows, col3, val3, x, y, alpha, beta);
+    CK(cudaGetLastError());
+  });
+}
+
+int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslot,
+                      const double* val3, const double* x, double* y, double alpha,
+                      double beta) {
+  return guard(ctx, [&] {
+    if (cols < 0 || (cols > 0 && (!tptr || !tslot || !val3 || !x || !y)))
+      fail(HMGPU_ERR_INVALID, "bad ell3 transposed spmv arguments");
+    if (cols == 0) return;
+    ell3_spmv_t_kernel<<<grid_for(ctx, (cols + 255) / 256), 256, 0, ctx->stream>>>(
+        cols, tptr, tslot, val3, x, y, alpha, beta);
+    CK(cudaGetLastError());
+  });
+}
+
 int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag) {
   return guard(ctx, [&] {
     if (n < 1 || !pts) fail(HMGPU_ERR_INVALID, "bad points");

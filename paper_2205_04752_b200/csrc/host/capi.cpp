@@ -12,6 +12,7 @@
 #include "hmbem.h"
 #include "hmgpu.h"
 #include "operator.hpp"
+#include "sparse_ops.hpp"
 #include "quadrature.hpp"
 
 struct hmb_mesh {
@@ -175,6 +176,21 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
 }
 
 void hmb_mesh_free(hmb_mesh* m) { delete m; }
+
+int hmb_sparse_op(const hmb_mesh* m, int which, int* cols3, double* vals3) {
+  return guard([&] {
+    need(m, "mesh");
+    need(cols3, "cols3");
+    need(vals3, "vals3");
+    const hmb::Ell3 e = which == 0   ? hmb::build_t_matrix(m->mesh, 0, 1)
+                        : which == 1 ? hmb::build_t_matrix(m->mesh, 0, 2)
+                        : which == 2 ? hmb::build_t_matrix(m->mesh, 1, 2)
+                        : which == 3 ? hmb::build_mass_matrix(m->mesh)
+                                     : throw hmb::Error("hmb_sparse_op: which in 0..3");
+    std::copy(e.col.begin(), e.col.end(), cols3);
+    std::copy(e.val.begin(), e.val.end(), vals3);
+  });
+}
 
 int hmb_random_vector(long long n, unsigned long long seed, int kind, double* out) {
   return guard([&] {

@@ -164,3 +164,70 @@ def test_kdelta_ranks_factors_matvec(kdelta):
     y = g.matvec(x)
     assert rel(y, o.matvec(x)) <= 1e-12
     assert rel(y, o.dense(0) @ x) <= 10 * eps
+
+
+# ---------------------------------------------------------------------------
+# operator algebra: V_h, K_h, D_h on the device vs the
+# dense compositions of the oracle's matrices (operators.cpp:97-158)
+@pytest.fixture(scope="module")
+def opset():
+    mesh = hm.Mesh.icosphere(2)
+    a = mesh.arrays()
+    E, nu, eps = 1.0, 0.3, 1e-7
+    ops = hm.OperatorSet(mesh, E, nu, b_min=16, eta=1.0, device=0)
+    ops.assemble(eps=eps, beta=0.8)
+    V, T = a["vertices"], a["triangles"]
+    m, n = len(T), len(V)
+    lam, mu = hm.lame_constants(E, nu)
+    vd = orc.Problem.galerkin(V, T, 1, b_min=16, eta=1.0).dense(0)
+    vg = orc.Problem.galerkin(V, T, 0, b_min=16, eta=1.0).dense_grid()
+    kd = orc.Problem.kdelta(V, T, b_min=16, eta=1.0).dense(0)
+    t12, t13, t23 = (orc.sparse_op(V, T, w) for w in range(3))
+    Z = np.zeros((m, n))
+    Th = np.block([[Z, t12, t13], [-t12, Z, t23], [-t13, -t23, Z]])
+    D3 = np.kron(np.eye(3), vd)
+    Vh = 0.5 / E * (1 + nu) / (1 - nu) * ((3 - 4 * nu) * D3 + vg)
+    Kh = np.kron(np.eye(3), kd) - D3 @ Th + 2 * mu * Vh @ Th
+    S = [np.kron(np.eye(3), -t23), np.kron(np.eye(3), t13), np.kron(np.eye(3), t12)]
+    Dh = sum(mu * Sk.T @ D3 @ Sk for Sk in S) + 2 * mu * Th.T @ D3 @ Th \
+        - 4 * mu * mu * Th.T @ Vh @ Th
+    tl = {(0, 1): t12, (0, 2): t13, (1, 2): t23}
+    def ts(k, l):
+        return None if k == l else (1.0 if k < l else -1.0) * tl[(min(k, l), max(k, l))]
+    G = np.zeros((3 * n, 3 * n))
+    for i in range(3):
+        for j in range(3):
+            for k in range(3):
+                if k in (i, j):
+                    continue
+                G[i * n:(i + 1) * n, j * n:(j + 1) * n] += ts(k, j).T @ vd @ ts(k, i)
+    Dh = Dh + mu * G
+    return dict(ops=ops, Vh=Vh, Kh=Kh, Dh=Dh, m=m, n=n, eps=eps, t=(t12, t13, t23))
+
+
+def test_sparse_ops_match_oracle(opset):
+    ops, t = opset["ops"], opset["t"]
+    torch = pytest.importorskip("torch")
+    n = opset["n"]
+    x = RV(n, 11)
+    xd = torch.tensor(x, device="cuda")
+    for w in range(3):
+        y = ops._spmv(w, xd).cpu().numpy()
+        assert np.allclose(y, t[w] @ x, rtol=1e-13, atol=1e-13 * np.abs(t[w] @ x).max())
+        z = RV(opset["m"], 12)
+        yt = ops._spmv(w, torch.tensor(z, device="cuda"), transpose=True).cpu().numpy()
+        assert np.allclose(yt, t[w].T @ z, rtol=1e-13, atol=1e-13 * np.abs(t[w].T @ z).max())
+
+
+def test_composed_operators_match_dense(opset):
+    ops, eps = opset["ops"], opset["eps"]
+    m, n = opset["m"], opset["n"]
+    xm, xn = RV(3 * m, 13), RV(3 * n, 14)
+    assert rel(ops.vh(xm), opset["Vh"] @ xm) <= 10 * eps
+    assert rel(ops.kh(xn), opset["Kh"] @ xn) <= 100 * eps
+    assert rel(ops.dh(xn), opset["Dh"] @ xn) <= 100 * eps
+    # D_h is symmetric; constants are in its kernel (rigid translations)
+    Dh = opset["Dh"]
+    assert np.allclose(Dh, Dh.T, rtol=0, atol=1e-10 * np.abs(Dh).max())
+    ones = np.concatenate([np.ones(n), np.zeros(2 * n)])
+    assert np.linalg.norm(ops.dh(ones)) <= 1e-6 * np.linalg.norm(Dh) * np.sqrt(n)
