@@ -757,6 +757,253 @@ class OperatorSet:
         return self._run(self.dh_dev, x, 3 * self.n)
 
 
+@dataclasses.dataclass
+class BacaConfig:  # baca.hpp:11-23
+    theta: float = 0.8
+    alpha: float = 10.0
+    eps_baca: float = 1e-4
+    inner_tol0: float = 1e-1
+    inner_floor: float = 1e-12
+    lookahead_steps: int = 2
+    max_outer: int = 60
+    max_inner: int = 10000
+
+
+@dataclasses.dataclass
+class BacaIteration:  # baca.hpp:124-139 (reduced mode: V marks only)
+    k: int
+    ek: float
+    tail_norm: float
+    residual: float
+    inner_tol: float
+    inner_iterations: int
+    marked_v: int
+    storage_mb: float
+    wall_time_s: float
+
+
+@dataclasses.dataclass
+class BacaReport:
+    iterations: list
+    converged: bool
+    termination: str
+
+
+class VddPreconditioner:
+    """build_vdd_preconditioner (baca.cpp:104-192) for the all-Dirichlet
+    (reduced) system: the dense leaf-cluster diagonal blocks of V_h (all
+    three components, taken from the near-field blocks of the V_kl and
+    V_Delta contexts), Cholesky-factored on the device (batched), scaled by
+    eta = half the smallest Ritz value of C0^{-1} V_h from a 10-step
+    preconditioned Lanczos run, so that eta C0 stays spectrally below V_h."""
+
+    def __init__(self, ops: "OperatorSet"):
+        torch = ops._torch
+        self.ops = ops
+        m = ops.m
+        pref = 0.5 / ops.E * (1.0 + ops.nu) / (1.0 - ops.nu)
+        c34 = 3.0 - 4.0 * ops.nu
+        tree = ops.vdelta.tree(0)
+        blocks = ops.vdelta.partition_blocks()
+        diag = {int(r): b for b, (r, c, adm, _) in enumerate(blocks) if r == c and not adm}
+        idx = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 1): 3, (1, 2): 4, (2, 2): 5}
+        groups, mats = [], []
+        for leaf in tree.leaves():
+            b0, b1 = tree.nodes[leaf, 0], tree.nodes[leaf, 1]
+            members = tree.perm[b0:b1]
+            nm = len(members)
+            b = diag[int(leaf)]
+            dd = ops.vdelta.dense_block(0, b)
+            blk = np.zeros((3 * nm, 3 * nm))
+            for c1 in range(3):
+                for c2 in range(3):
+                    d = ops.vkl.dense_block(idx[(min(c1, c2), max(c1, c2))], b)
+                    if c1 == c2:
+                        d = d + c34 * dd
+                    blk[c1 * nm:(c1 + 1) * nm, c2 * nm:(c2 + 1) * nm] = pref * d
+            groups.append(np.concatenate([c * m + members for c in range(3)]))
+            mats.append(blk)
+        # batch by block size (leaves of one tree level share it)
+        self.batches = []
+        for size in sorted({len(g) for g in groups}):
+            sel = [i for i, g in enumerate(groups) if len(g) == size]
+            G = torch.tensor(np.stack([groups[i] for i in sel]), device=ops.dev)
+            A = torch.tensor(np.stack([mats[i] for i in sel]), device=ops.dev)
+            L = torch.linalg.cholesky(A)  # raises if a block is not SPD
+            self.batches.append((G, A, L))
+        self.eta = 1.0
+        self.eta = self._ritz_eta()
+
+    def solve(self, r):
+        torch = self.ops._torch
+        z = torch.zeros_like(r)
+        for G, _, L in self.batches:
+            z[G] = torch.cholesky_solve(r[G].unsqueeze(-1), L).squeeze(-1) / self.eta
+        return z
+
+    def apply(self, r):
+        torch = self.ops._torch
+        z = torch.zeros_like(r)
+        for G, A, _ in self.batches:
+            z[G] = self.eta * (A @ r[G].unsqueeze(-1)).squeeze(-1)
+        return z
+
+    def _ritz_eta(self) -> float:
+        torch = self.ops._torch
+        n = 3 * self.ops.m
+        i = torch.arange(n, dtype=torch.float64, device=self.ops.dev)
+        r = 0.5 + 0.5 * torch.cos(3 * i + 1)
+        z = self.solve(r)
+        p = z.clone()
+        rz = float(r @ z)
+        alphas, betas = [], []
+        for _ in range(10):
+            ap = self.ops.vh_dev(p)
+            pap = float(p @ ap)
+            if pap <= 0.0 or rz <= 0.0:
+                break
+            alpha = rz / pap
+            r = r - alpha * ap
+            z = self.solve(r)
+            rz_new = float(r @ z)
+            alphas.append(alpha)
+            betas.append(rz_new / rz)
+            rz = rz_new
+            p = z + betas[-1] * p
+            if np.sqrt(abs(rz)) < 1e-14:
+                break
+        if not alphas:
+            return 1.0
+        k = len(alphas)
+        tri = np.zeros((k, k))
+        for j in range(k):
+            tri[j, j] = 1.0 / alphas[j] + (betas[j - 1] / alphas[j - 1] if j > 0 else 0.0)
+            if j + 1 < k:
+                off = np.sqrt(max(betas[j], 0.0)) / alphas[j]
+                tri[j, j + 1] = tri[j + 1, j] = off
+        lam = float(np.linalg.eigvalsh(tri).min())
+        return 0.5 * lam if lam > 0 else 1.0
+
+
+def pcg_spd(ops: "OperatorSet", prec: VddPreconditioner, f, tol_abs: float, x0, max_iter: int):
+    """Preconditioned CG on V_h x = f (pcg_spd, baca.cpp:200-225); device vectors."""
+    x = x0.clone()
+    r = f - ops.vh_dev(x)
+    z = prec.solve(r)
+    p = z.clone()
+    rz = float(r @ z)
+    it = 0
+    while float(r.norm()) > tol_abs and it < max_iter:
+        ap = ops.vh_dev(p)
+        alpha = rz / float(p @ ap)
+        x = x + alpha * p
+        r = r - alpha * ap
+        z = prec.solve(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+        it += 1
+    res = float(r.norm())
+    return x, it, res
+
+
+def estimator_vh(ops: "OperatorSet", x):
+    """estimator_Ek of the reduced system (baca.cpp:401-456): the look-ahead
+    tail terms of V_h's leaf occurrences -- each V_kl block (grid embedding)
+    scaled by (1+nu)/(2E(1-nu)), each V_Delta block over its three diag3
+    occurrences scaled by that times (3-4nu) -- one term per (H-matrix,
+    block); E_k = sqrt(sum of the terms' norm_sq), diff = sum of the terms."""
+    m = ops.m
+    pref = 0.5 / ops.E * (1.0 + ops.nu) / (1.0 - ops.nu)
+    sd = pref * (3.0 - 4.0 * ops.nu)
+    xh = x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+    terms = []  # (h, comp, block, norm_sq)
+    diff = np.zeros(3 * m)
+    g = ops.vkl.gamma_contributions(xh)
+    for t in g.terms:
+        v = pref * t.val
+        np.add.at(diff, t.idx, v)
+        terms.append((ops.vkl, t.comp, t.block, float(v @ v)))
+    per_block = {}
+    for c in range(3):
+        gd = ops.vdelta.gamma_contributions(xh[c * m:(c + 1) * m])
+        for t in gd.terms:
+            v = sd * t.val
+            np.add.at(diff, c * m + t.idx, v)
+            per_block[t.block] = per_block.get(t.block, 0.0) + float(v @ v)
+    for b in sorted(per_block):
+        terms.append((ops.vdelta, 0, b, per_block[b]))
+    ek = float(np.sqrt(sum(t[3] for t in terms)))
+    return ek, terms, diff
+
+
+def doerfler_mark(terms, ek: float, theta: float):
+    """Minimal greedy Doerfler set (baca.cpp:458-476)."""
+    order = sorted(range(len(terms)), key=lambda i: -terms[i][3])  # stable
+    target = theta * theta * ek * ek
+    marked, acc = [], 0.0
+    for i in order:
+        if acc >= target:
+            break
+        marked.append(i)
+        acc += terms[i][3]
+    return marked
+
+
+def baca_solve(ops: "OperatorSet", f, cfg: Optional[BacaConfig] = None):
+    """baca_solve (baca.cpp:488-600) for the reduced all-Dirichlet system
+    V_h t = f: inner PCG under ||f - A_k x|| <= alpha ||(A_k - A_hat_k) x||,
+    estimator E_k, Doerfler marking (theta), promotion + look-ahead
+    extension of the marked blocks (phase 3 of the reference).  All
+    H-matrix work runs on the device.  Returns (x, BacaReport)."""
+    import time as _time
+    torch = ops._torch
+    cfg = cfg or BacaConfig()
+    if not 0.0 < cfg.theta < 1.0:
+        raise Error("baca_solve: theta must lie in (0,1)")
+    f = np.asarray(f, dtype=np.float64)
+    if f.shape != (3 * ops.m,):
+        raise DimensionError("baca_solve: rhs size")
+    fd = torch.tensor(f, device=ops.dev)
+    prec = VddPreconditioner(ops)
+    fnorm = float(np.linalg.norm(f))
+    floor_abs = cfg.inner_floor * max(fnorm, 1e-300)
+    x = torch.zeros_like(fd)
+    tol_abs = max(cfg.inner_tol0 * fnorm, floor_abs)
+    t0 = _time.perf_counter()
+    its = []
+    for k in range(cfg.max_outer + 1):
+        inner = 0
+        for _ in range(6):
+            x, n_it, res = pcg_spd(ops, prec, fd, tol_abs, x, cfg.max_inner)
+            inner += n_it
+            ek, terms, diff = estimator_vh(ops, x)
+            tail = float(np.linalg.norm(diff))
+            cond = cfg.alpha * tail
+            if res <= max(cond, floor_abs):
+                break
+            tol_abs = max(cond, floor_abs)
+        storage = (ops.vkl.storage_mb_current() + ops.vdelta.storage_mb_current())
+        it = BacaIteration(k, ek, tail, res, tol_abs, inner, 0, storage,
+                           _time.perf_counter() - t0)
+        if ek <= cfg.eps_baca:
+            its.append(it)
+            return x.cpu().numpy(), BacaReport(its, True, "tolerance")
+        if k >= cfg.max_outer:
+            its.append(it)
+            return x.cpu().numpy(), BacaReport(its, False, "max_outer")
+        marked = doerfler_mark(terms, ek, cfg.theta)
+        it.marked_v = len(marked)
+        for h in (ops.vkl, ops.vdelta):
+            pairs = [(terms[i][1], terms[i][2]) for i in marked if terms[i][0] is h]
+            if pairs:
+                h.promote(pairs)
+                h.extend_lookahead(pairs, cfg.lookahead_steps)
+        its.append(it)
+        tol_abs = max(tol_abs, floor_abs)
+    return x.cpu().numpy(), BacaReport(its, False, "max_outer")
+
+
 def random_vector(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
     """Seeded synthetic input: mt19937_64 + uniform [-1,1) (the reference's
     random_vector) or standard normal."""
