@@ -454,7 +454,10 @@ class HMatrix:
         return out
 
     # ---- adaptive matvec ----
-    def gamma_contributions(self, x) -> GammaContributions:
+    def gamma_contributions(self, x, term_data: bool = True) -> GammaContributions:
+        """term_data = False skips the per-term index/value downloads (the
+        terms then carry empty idx / val; gamma, difference and norm_sq are
+        complete)."""
         x = _f64(x)
         g = C.c_double()
         diff = np.zeros(self.rows)
@@ -467,9 +470,10 @@ class HMatrix:
         _check(_h.hmb_gamma_terms(self._h, _ptr(comp), _ptr(block), _ptr(nnz), _ptr(nsq)))
         terms = []
         for t in range(n):
-            idx = np.zeros(nnz[t], np.int64)
-            val = np.zeros(nnz[t])
-            _check(_h.hmb_gamma_term_data(self._h, t, _ptr(idx), _ptr(val)))
+            idx = np.zeros(nnz[t] if term_data else 0, np.int64)
+            val = np.zeros(nnz[t] if term_data else 0)
+            if term_data:
+                _check(_h.hmb_gamma_term_data(self._h, t, _ptr(idx), _ptr(val)))
             terms.append(BlockTerm(int(comp[t]), int(block[t]), idx, val, float(nsq[t])))
         return GammaContributions(g.value, diff, terms)
 
@@ -917,20 +921,19 @@ def estimator_vh(ops: "OperatorSet", x):
     pref = 0.5 / ops.E * (1.0 + ops.nu) / (1.0 - ops.nu)
     sd = pref * (3.0 - 4.0 * ops.nu)
     xh = x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+    # the scales enter linearly (diff) and squared (norm_sq), so only the
+    # per-context difference vectors and term norms are downloaded
     terms = []  # (h, comp, block, norm_sq)
-    diff = np.zeros(3 * m)
-    g = ops.vkl.gamma_contributions(xh)
+    g = ops.vkl.gamma_contributions(xh, term_data=False)
+    diff = pref * g.difference
     for t in g.terms:
-        v = pref * t.val
-        np.add.at(diff, t.idx, v)
-        terms.append((ops.vkl, t.comp, t.block, float(v @ v)))
+        terms.append((ops.vkl, t.comp, t.block, pref * pref * t.norm_sq))
     per_block = {}
     for c in range(3):
-        gd = ops.vdelta.gamma_contributions(xh[c * m:(c + 1) * m])
+        gd = ops.vdelta.gamma_contributions(xh[c * m:(c + 1) * m], term_data=False)
+        diff[c * m:(c + 1) * m] += sd * gd.difference
         for t in gd.terms:
-            v = sd * t.val
-            np.add.at(diff, c * m + t.idx, v)
-            per_block[t.block] = per_block.get(t.block, 0.0) + float(v @ v)
+            per_block[t.block] = per_block.get(t.block, 0.0) + sd * sd * t.norm_sq
     for b in sorted(per_block):
         terms.append((ops.vdelta, 0, b, per_block[b]))
     ek = float(np.sqrt(sum(t[3] for t in terms)))
