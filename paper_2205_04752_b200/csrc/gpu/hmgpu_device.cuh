@@ -1649,8 +1649,16 @@ __global__ void compact_kernel(Item* __restrict__ items, int n,
     const long long v0 = u0 + (((long long)it.m * caps[t] + 1) & ~1LL);
     const double* su = src + it.u_off;
     const double* sv = src + it.v_off;
-    for (long long e = lane; e < nu; e += 32) dst[u0 + e] = su[e];
-    for (long long e = lane; e < nv; e += 32) dst[v0 + e] = sv[e];
+    // every U / V region starts 16-byte aligned (align2 offsets): copy
+    // double2 pairs, then the odd tail element
+    auto copy2 = [&](double* d, const double* s_, long long len) {
+      const double2* s2 = reinterpret_cast<const double2*>(s_);
+      double2* d2 = reinterpret_cast<double2*>(d);
+      for (long long e = lane; e < len / 2; e += 32) d2[e] = s2[e];
+      if ((len & 1) && lane == 0) d[len - 1] = s_[len - 1];
+    };
+    copy2(dst + u0, su, nu);
+    copy2(dst + v0, sv, nv);
     for (int e = lane; e < it.k; e += 32) dpiv[poff[t] + e] = spiv[it.p_off + e];
     __syncwarp();
     if (lane == 0) {
