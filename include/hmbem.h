@@ -116,6 +116,9 @@ int hmb_assemble(hmb_op* op, double eps, double beta, int initial_rank,
                  int lookahead, long long max_rank, double* stats8);
 int hmb_matvec(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
                int device_ptrs);
+/* y = A^T x (HMatrix::matvec_transposed, hmatrix.cpp:47-72) */
+int hmb_matvec_transposed(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
+                          int device_ptrs);
 int hmb_ranks(const hmb_op* op, int* k_cur, int* k_look, int* consumed, int* last_stop);
 int hmb_promote(hmb_op* op, int n, const int* comp_block);
 int hmb_extend(hmb_op* op, int n, const int* comp_block, int steps);

@@ -32,6 +32,7 @@
  *   hmgpu_ranks                HBlock::current_rank / factor.rank() (hmatrix.hpp:31-39)
  *   hmgpu_matvec               HMatrix::matvec (hmatrix.cpp:22-45) composed by the
  *                              BlockGrid matvec (proj/src/expr.cpp:197-215)
+ *   hmgpu_matvec_transposed    HMatrix::matvec_transposed (hmatrix.cpp:47-72)
  *   hmgpu_promote              HMatrix::promote (hmatrix.cpp:95-97)
  *   hmgpu_extend               HMatrix::extend_lookahead (hmatrix.cpp:104-111)
  *   hmgpu_tail_terms           the apply_range(k_cur, k_look) products of
@@ -200,6 +201,13 @@ int hmgpu_ranks(hmgpu_ctx* ctx, int* k_cur, int* k_look, int* consumed,
  * pointers; host calls stage through pinned buffers. */
 int hmgpu_matvec(hmgpu_ctx* ctx, const double* x, double* y, int nrhs,
                  int mode, int ptr_kind);
+/* y = A^T x (HMatrix::matvec_transposed, proj/src/hmatrix.cpp:47-72; in the
+ * 3x3 grid the transpose of every cell): x over the rows (n_rows * 3 or
+ * n_rows dofs per RHS), y over the columns; nrhs columns back to back;
+ * deterministic (partial rows per block column range, fixed-order
+ * reduction per column leaf).  Block-row shards give partial products. */
+int hmgpu_matvec_transposed(hmgpu_ctx* ctx, const double* x, double* y, int nrhs,
+                            int mode, int ptr_kind);
 
 /* promote / extend work items given as (component, block) pairs */
 int hmgpu_promote(hmgpu_ctx* ctx, int n, const int* comp_block);

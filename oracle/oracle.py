@@ -339,7 +339,7 @@ class Problem:
 
     def matvec_transposed(self, x, mode=0) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = np.zeros(self.rows)
+        y = np.zeros(self.ncols * (3 if self.ncomp == 6 else 1))
         _ck(lib().or_matvec_transposed(self._h, _p(x), _p(y), mode))
         return y
 

@@ -73,6 +73,7 @@ _sig(host, "hmb_partition_blocks", I, P, P)
 _sig(host, "hmb_partition_json", I, P, C.c_char_p, LLP)
 _sig(host, "hmb_assemble", I, P, D, D, I, I, LL, P)
 _sig(host, "hmb_matvec", I, P, P, P, I, I, I)
+_sig(host, "hmb_matvec_transposed", I, P, P, P, I, I, I)
 _sig(host, "hmb_ranks", I, P, P, P, P, P)
 _sig(host, "hmb_promote", I, P, I, P)
 _sig(host, "hmb_extend", I, P, I, P, I)

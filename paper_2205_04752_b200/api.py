@@ -389,6 +389,20 @@ class HMatrix:
                              y.ctypes.data_as(C.c_void_p), nrhs, int(mode), 0))
         return y[:, 0].copy() if vec else y
 
+    def matvec_transposed(self, x, mode: Mode = Mode.Current) -> np.ndarray:
+        """y = A^T x (HMatrix::matvec_transposed, hmatrix.cpp:47-72)."""
+        x = np.asarray(x, dtype=np.float64)
+        vec = x.ndim == 1
+        xm = x.reshape(x.shape[0], -1)
+        if xm.shape[0] != self.rows:
+            raise DimensionError("HMatrix::matvec_transposed: size")
+        nrhs = xm.shape[1]
+        xf = np.asfortranarray(xm)
+        y = np.zeros((self.cols, nrhs), order="F")
+        _check(_h.hmb_matvec_transposed(self._h, xf.ctypes.data_as(C.c_void_p),
+                                        y.ctypes.data_as(C.c_void_p), nrhs, int(mode), 0))
+        return y[:, 0].copy() if vec else y
+
     def matvec_ptr(self, x_ptr: int, y_ptr: int, nrhs: int = 1,
                    mode: Mode = Mode.Current, device: bool = True) -> None:
         """y = A x on raw pointers (device pointers by default, e.g. torch

@@ -443,6 +443,13 @@ struct hmgpu_ctx {
 
   // ---- device-resident AMVM estimator (hmgpu_amvm.cuh) ----
   bool am_geom_valid = false;
+  // transposed matvec tables (column leaves), built on first use
+  bool t_valid = false;
+  int t_nleaves = 0;
+  long long t_rows = 0;
+  DBuf<long long> d_tprow, d_tleaf_prow;
+  DBuf<int> d_tleaf_begin, d_tleaf_end, d_tleaf_ptr;
+  DBuf<double> d_tpart, d_xr;
   bool mv_direct = false;  // hmgpu_set_matvec_policy: 1-RHS matvecs without a stream plan
   DBuf<int> d_row_leaf, d_sortp, d_tix, d_term_bi, d_cnt, d_ptr, d_lists, d_order, d_idx,
       d_marked, d_nm, d_mids;
@@ -1046,8 +1053,63 @@ void build_matvec(hmgpu_ctx* c) {
   c->d_leaf_blk.upload(c->leaf_blk, c->stream);
   c->am_geom_valid = false;
   c->am_have_estimate = false;
+  c->t_valid = false;
   c->d_leaf_prow.upload(c->leaf_prow, c->stream);
   c->sync();
+}
+
+// tables of the transposed matvec: a partial-row range per owned block over
+// its column cluster, and per column-tree leaf the covering blocks in block
+// order (deterministic reduction)
+void build_matvec_t(hmgpu_ctx* c) {
+  std::vector<long long> tprow(c->mvb.size());
+  long long t = 0;
+  for (size_t b = 0; b < c->mvb.size(); ++b) {
+    tprow[b] = t;
+    t += c->mvb[b].n;
+  }
+  c->t_rows = t;
+  std::vector<int> lb, le;
+  const int ncn = (int)c->cnodes.size() / 4;
+  for (int q = 0; q < ncn; ++q) {
+    const int* nd = &c->cnodes[4 * q];
+    if (nd[2] >= 0) continue;
+    lb.push_back(nd[0]);
+    le.push_back(nd[1]);
+  }
+  std::vector<int> ord(lb.size());
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return lb[a] < lb[b]; });
+  std::vector<int> b2(lb.size()), e2(lb.size());
+  for (size_t i = 0; i < ord.size(); ++i) {
+    b2[i] = lb[ord[i]];
+    e2[i] = le[ord[i]];
+  }
+  const int nl = (int)b2.size();
+  std::vector<std::vector<long long>> lists(nl);
+  for (size_t bi = 0; bi < c->mvb.size(); ++bi) {
+    const MvBlock& mb = c->mvb[bi];
+    int l0 = (int)(std::lower_bound(b2.begin(), b2.end(), mb.col0) - b2.begin());
+    for (int l = l0; l < nl && b2[l] < mb.col0 + mb.n; ++l) {
+      if (e2[l] > mb.col0 + mb.n)
+        fail(HMGPU_ERR_INVALID, "block columns do not align with column-tree leaves");
+      lists[l].push_back(tprow[bi] + (b2[l] - mb.col0));
+    }
+  }
+  std::vector<int> ptr(nl + 1, 0);
+  std::vector<long long> prow;
+  for (int l = 0; l < nl; ++l) {
+    ptr[l + 1] = ptr[l] + (int)lists[l].size();
+    prow.insert(prow.end(), lists[l].begin(), lists[l].end());
+  }
+  c->t_nleaves = nl;
+  c->d_tprow.upload(tprow, c->stream);
+  c->d_tleaf_begin.upload(b2, c->stream);
+  c->d_tleaf_end.upload(e2, c->stream);
+  c->d_tleaf_ptr.upload(ptr, c->stream);
+  c->d_tleaf_prow.upload(prow, c->stream);
+  c->sync();
+  c->t_valid = true;
 }
 
 // refresh kmax after rank changes (promote / extend)
@@ -2158,6 +2220,77 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       for (const DenseBlock& d : c->dblocks) flops += (double)c->NC * d.m * d.n;
       s.counted_flops = c->kind == KIND_KELVIN ? flops : 0.0;
       *stats = s;
+    }
+  });
+}
+
+int hmgpu_matvec_transposed(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
+                            int ptr_kind) {
+  return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+    if (!x || !y || nrhs < 1) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
+    if (mode != HMGPU_MODE_CURRENT && mode != HMGPU_MODE_LOOKAHEAD)
+      fail(HMGPU_ERR_INVALID, "bad mode");
+    check_ptr_kind(ptr_kind);
+    if (!c->t_valid) build_matvec_t(c);
+    const int NOUT = c->NC == 6 ? 3 : 1;
+    const long long nxr = (long long)c->n_rows * NOUT, nyc = (long long)c->n_cols * NOUT;
+    const double* dx = x;
+    double* dy = y;
+    DBuf<double> hx, hy;
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      hx.alloc((size_t)(nxr * nrhs));
+      hy.alloc((size_t)(nyc * nrhs));
+      CK(cudaMemcpyAsync(hx.p, x, nxr * nrhs * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+      dx = hx.p;
+      dy = hy.p;
+    }
+    c->d_xr.ensure((size_t)nxr);
+    c->d_tpart.ensure((size_t)std::max<long long>(c->t_rows * NOUT, 1));
+    const size_t smem = 2 * (size_t)std::max(c->kmax, 1) * sizeof(double);
+    for (int q = 0; q < nrhs; ++q) {
+      const int gg = grid_for(c, (nxr + 255) / 256);
+      if (NOUT == 3)
+        gather_kernel<3><<<gg, 256, 0, c->stream>>>(dx + q * nxr, c->d_xr.p, c->d_rperm.p,
+                                                     c->n_rows, 1);
+      else
+        gather_kernel<1><<<gg, 256, 0, c->stream>>>(dx + q * nxr, c->d_xr.p, c->d_rperm.p,
+                                                     c->n_rows, 1);
+      const int grid = grid_for(c, c->n_mv, 4);
+      if (c->NC == 6) {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(hmvt_blocks_kernel<6>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hmvt_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
+            c->d_mvb.p, c->n_mv, c->d_tprow.p, c->d_items.p, c->d_arena.p, c->d_dense.p,
+            c->d_xr.p, c->d_tpart.p, mode);
+      } else {
+        if (smem > 48 * 1024)
+          CK(cudaFuncSetAttribute(hmvt_blocks_kernel<1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        hmvt_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
+            c->d_mvb.p, c->n_mv, c->d_tprow.p, c->d_items.p, c->d_arena.p, c->d_dense.p,
+            c->d_xr.p, c->d_tpart.p, mode);
+      }
+      CK(cudaGetLastError());
+      const int gr = grid_for(c, c->t_nleaves, 8);
+      if (NOUT == 3)
+        hmv_reduce_kernel<3><<<gr, 128, 0, c->stream>>>(
+            c->d_tleaf_begin.p, c->d_tleaf_end.p, c->d_tleaf_ptr.p, c->d_tleaf_prow.p,
+            c->t_nleaves, c->d_tpart.p, c->d_cperm.p, c->n_cols, dy + q * nyc, 1);
+      else
+        hmv_reduce_kernel<1><<<gr, 128, 0, c->stream>>>(
+            c->d_tleaf_begin.p, c->d_tleaf_end.p, c->d_tleaf_ptr.p, c->d_tleaf_prow.p,
+            c->t_nleaves, c->d_tpart.p, c->d_cperm.p, c->n_cols, dy + q * nyc, 1);
+      CK(cudaGetLastError());
+    }
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      CK(cudaMemcpyAsync(y, hy.p, nyc * nrhs * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+      c->sync();
+      hx.free();
+      hy.free();
     }
   });
 }

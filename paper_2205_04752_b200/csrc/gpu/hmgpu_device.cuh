@@ -1510,6 +1510,92 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
   }
 }
 
+// Transposed H-matvec (HMatrix::matvec_transposed, proj/src/hmatrix.cpp:
+// 47-72) over the owned blocks: a CTA per block writes the partial rows of
+// its COLUMN range, tpart[(tprow + j) * NOUT + r]; the per-column-leaf pass
+// (hmv_reduce_kernel on the column tables) sums them in a fixed order.  In
+// the 3x3 grid the cell (R, C) transposed maps x_R to y_C and, for R != C,
+// its alias (C, R) maps x_C to y_R.  xr: x gathered to internal row order.
+template <int NC>
+__global__ void __launch_bounds__(256)
+hmvt_blocks_kernel(const MvBlock* __restrict__ blocks, int nblocks,
+                   const long long* __restrict__ tprow, const Item* __restrict__ items,
+                   const double* __restrict__ arena, const double* __restrict__ dense,
+                   const double* __restrict__ xr, double* __restrict__ tpart, int mode) {
+  constexpr int NOUT = NC == 6 ? 3 : 1;
+  extern __shared__ double zsm[];  // [2][kmax]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
+    const MvBlock b = blocks[bi];
+    double* out = tpart + tprow[bi] * NOUT;
+    const double* xs = xr + (long long)b.row0 * NOUT;
+    if (b.dense) {
+      const long long cp = (b.m * NC + 1) & ~1;
+      for (int j = threadIdx.x; j < b.n; j += blockDim.x) {
+        double acc[NOUT];
+#pragma unroll
+        for (int r = 0; r < NOUT; ++r) acc[r] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int R = NC == 6 ? c_comp_r[c] : 0, C = NC == 6 ? c_comp_c[c] : 0;
+          const double* D = dense + b.dense_off + j * cp + (long long)c * b.m;
+          double s1 = 0.0, s2 = 0.0;
+          for (int i = 0; i < b.m; ++i) {
+            s1 = fma(D[i], xs[i * NOUT + R], s1);
+            if (R != C) s2 = fma(D[i], xs[i * NOUT + C], s2);
+          }
+          acc[C] += s1;
+          if (R != C) acc[R] += s2;
+        }
+#pragma unroll
+        for (int r = 0; r < NOUT; ++r) out[(long long)j * NOUT + r] = acc[r];
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int c = 0; c < NC; ++c) {
+      const Item it = items[b.item0 + c];
+      const int k = mode ? it.k : it.kcur;
+      const int R = NC == 6 ? c_comp_r[c] : 0, C = NC == 6 ? c_comp_c[c] : 0;
+      const double* U = arena + it.u_off;
+      const double* V = arena + it.v_off;
+      // z_l = U(:,l) . x_R (and w_l = U(:,l) . x_C for the alias)
+      for (int l = warp; l < k; l += nwarps) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int i = lane; i < b.m; i += 32) {
+          const double u = U[(long long)l * b.m + i];
+          s1 = fma(u, xs[i * NOUT + R], s1);
+          if (R != C) s2 = fma(u, xs[i * NOUT + C], s2);
+        }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          zsm[l] = s1;
+          zsm[k + l] = s2;
+        }
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < b.n; j += blockDim.x) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int l = 0; l < k; ++l) {
+          const double v = V[(long long)l * b.n + j];
+          s1 = fma(v, zsm[l], s1);
+          if (R != C) s2 = fma(v, zsm[k + l], s2);
+        }
+        double* o = out + (long long)j * NOUT;
+        if (c == 0) {
+#pragma unroll
+          for (int r = 0; r < NOUT; ++r) o[r] = 0.0;
+        }
+        o[C] += s1;
+        if (R != C) o[R] += s2;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // per leaf: y(p) = sum over covering blocks (fixed order) of the partials
 template <int NOUT>
 __global__ void hmv_reduce_kernel(const int* __restrict__ leaf_begin,

@@ -428,6 +428,17 @@ int hmb_matvec(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
   });
 }
 
+int hmb_matvec_transposed(const hmb_op* op, const double* x, double* y, int nrhs, int mode,
+                          int device_ptrs) {
+  return guard([&] {
+    need(op, "op");
+    need(x, "x");
+    need(y, "y");
+    op->op->matvec_transposed(x, y, nrhs, mode ? hmb::Mode::Lookahead : hmb::Mode::Current,
+                              device_ptrs != 0);
+  });
+}
+
 int hmb_ranks(const hmb_op* op, int* k_cur, int* k_look, int* consumed, int* last_stop) {
   return guard([&] {
     need(op, "op");

@@ -339,6 +339,14 @@ void HOperator::matvec(const double* x, double* y, int nrhs, Mode mode,
         "hmgpu_matvec");
 }
 
+void HOperator::matvec_transposed(const double* x, double* y, int nrhs, Mode mode,
+                                  bool device_ptrs) const {
+  if (!assembled_) throw Error("matvec_transposed: operator not assembled");
+  check(hmgpu_matvec_transposed(ctx_, x, y, nrhs, static_cast<int>(mode),
+                                device_ptrs ? HMGPU_PTR_DEVICE : HMGPU_PTR_HOST),
+        "hmgpu_matvec_transposed");
+}
+
 std::vector<double> HOperator::matvec(const std::vector<double>& x, Mode mode) const {
   if (static_cast<long long>(x.size()) != cols())
     throw DimensionError("HMatrix::matvec: size");

@@ -104,6 +104,9 @@ class HOperator {
   void matvec(const double* x, double* y, int nrhs, Mode mode,
               bool device_ptrs = false) const;
   std::vector<double> matvec(const std::vector<double>& x, Mode mode) const;
+  // y = A^T x (HMatrix::matvec_transposed, hmatrix.cpp:47-72): x over rows
+  void matvec_transposed(const double* x, double* y, int nrhs, Mode mode,
+                         bool device_ptrs = false) const;
 
   void promote(const std::vector<std::pair<int, int>>& comp_block);
   void extend_lookahead(const std::vector<std::pair<int, int>>& comp_block,
