@@ -2605,6 +2605,135 @@ int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* di
   });
 }
 
+namespace {
+// the greedy marking walk, parallel and bit-identical (hmgpu_amvm.cuh,
+// walk_*_kernel): term sequence S by first appearance, then chunks of S
+// with per-row residual-before values, per-term dots, the sequential
+// res_sq scan and the residual update.  Writes d_marked / d_nm and
+// d_sc[2] = gamma(P_k) like amvm_walk_kernel.
+void parallel_walk(hmgpu_ctx* c, double theta, long long M, int nt) {
+  double sc2[2];
+  CK(cudaMemcpyAsync(sc2, c->d_sc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  const double target = (1.0 - theta) * sc2[1];
+  const double target_sq = target * target;
+  int nm = 0;
+  DBuf<long long> cnt, pre;
+  DBuf<unsigned long long> first, fsorted;
+  DBuf<int> tid, tS, count;
+  if (sc2[0] > target_sq && nt > 0 && M > 0) {
+    c->timed("amvm_walk", [&] {
+      cnt.alloc(M + 1);
+      pre.alloc(M + 1);
+      walk_cnt_kernel<<<(int)((M + 256) / 256), 256, 0, c->stream>>>(c->d_order.p, M,
+                                                                      c->d_ptr.p, cnt.p);
+      size_t tb = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, pre.p, (int)(M + 1), c->stream));
+      c->d_cub.ensure(tb);
+      CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, tb, cnt.p, pre.p, (int)(M + 1), c->stream));
+      first.alloc(nt);
+      fsorted.alloc(nt);
+      tid.alloc(nt);
+      tS.alloc(nt);
+      count.alloc(1);
+      CK(cudaMemsetAsync(first.p, 0xff, nt * sizeof(unsigned long long), c->stream));
+      CK(cudaMemsetAsync(count.p, 0, sizeof(int), c->stream));
+      walk_first_kernel<<<(int)((M + 255) / 256), 256, 0, c->stream>>>(
+          c->d_order.p, M, c->d_ptr.p, c->d_lists.p, pre.p, first.p);
+      walk_tids_kernel<<<(nt + 255) / 256, 256, 0, c->stream>>>(nt, tid.p, first.p, count.p);
+      tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, first.p, fsorted.p, tid.p, tS.p, nt, 0, 64,
+                                         c->stream));
+      c->d_cub.ensure(tb);
+      CK(cub::DeviceRadixSort::SortPairs(c->d_cub.p, tb, first.p, fsorted.p, tid.p, tS.p, nt, 0,
+                                         64, c->stream));
+    });
+    int L = 0;
+    CK(cudaMemcpyAsync(&L, count.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    DBuf<long long> sz, cumE;
+    sz.alloc(L + 1);
+    cumE.alloc(L + 1);
+    walk_sizes_kernel<<<(L + 256) / 256, 256, 0, c->stream>>>(tS.p, L, c->d_eptr.p, sz.p);
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, sz.p, cumE.p, L + 1, c->stream));
+    c->d_cub.ensure(tb);
+    CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, tb, sz.p, cumE.p, L + 1, c->stream));
+    std::vector<long long> hcum(L + 1);
+    CK(cudaMemcpyAsync(hcum.data(), cumE.p, (L + 1) * sizeof(long long),
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    int row_bits = 1;
+    while ((1LL << row_bits) <= M) ++row_bits;
+    const long long kEmax = 1LL << 24;
+    const int kTmax = 1 << 20;
+    DBuf<unsigned long long> keys, skeys;
+    DBuf<int> slots, sslots;
+    DBuf<long long> gslot;
+    DBuf<double> rb, dots, st;
+    st.alloc(2);
+    CK(cudaMemcpyAsync(st.p, c->d_sc.p, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    int k0 = 0;
+    bool stopped = false;
+    while (k0 < L && !stopped) {
+      int k1 = k0 + 1;
+      while (k1 < L && k1 - k0 < kTmax && hcum[k1 + 1] - hcum[k0] <= kEmax) ++k1;
+      const long long E = hcum[k1] - hcum[k0];
+      const int nk = k1 - k0;
+      c->timed("amvm_walk", [&] {
+        keys.ensure(E);
+        skeys.ensure(E);
+        slots.ensure(E);
+        sslots.ensure(E);
+        gslot.ensure(E);
+        rb.ensure(E);
+        dots.ensure(nk);
+        walk_build_kernel<<<(nk + 127) / 128, 128, 0, c->stream>>>(
+            tS.p, k0, k1, cumE.p, c->d_eptr.p, c->d_eidx.p, keys.p, slots.p, gslot.p);
+        size_t tbs = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tbs, keys.p, skeys.p, slots.p, sslots.p,
+                                           (int)E, 0, 22 + row_bits, c->stream));
+        c->d_cub.ensure(tbs);
+        CK(cub::DeviceRadixSort::SortPairs(c->d_cub.p, tbs, keys.p, skeys.p, slots.p,
+                                           sslots.p, (int)E, 0, 22 + row_bits, c->stream));
+        const int ge = (int)((E + 255) / 256);
+        walk_before_kernel<<<ge, 256, 0, c->stream>>>(skeys.p, sslots.p, E, gslot.p,
+                                                       c->d_eval.p, c->d_resid.p, rb.p);
+        walk_dot_kernel<<<(nk + 127) / 128, 128, 0, c->stream>>>(k0, k1, cumE.p, gslot.p,
+                                                                 c->d_eval.p, rb.p, dots.p);
+        walk_scan_kernel<<<1, 1, 0, c->stream>>>(tS.p, k0, k1, c->d_nsq.p, dots.p, target_sq,
+                                                 st.p);
+        walk_apply_kernel<<<ge, 256, 0, c->stream>>>(skeys.p, sslots.p, E, gslot.p,
+                                                      c->d_eval.p, rb.p, st.p, nk,
+                                                      c->d_resid.p);
+      });
+      double hst[2];
+      CK(cudaMemcpyAsync(hst, st.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      const int stop = (int)hst[1];
+      if (stop >= 0) {
+        nm = k0 + stop + 1;
+        stopped = true;
+      } else {
+        nm = k1;
+      }
+      k0 = k1;
+    }
+    CK(cudaMemcpyAsync(c->d_marked.p, tS.p, (size_t)nm * sizeof(int), cudaMemcpyDeviceToDevice,
+                       c->stream));
+    keys.free(); skeys.free(); slots.free(); sslots.free(); gslot.free(); rb.free();
+    dots.free(); st.free(); sz.free(); cumE.free();
+  }
+  CK(cudaMemcpyAsync(c->d_nm.p, &nm, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  // gamma(P_k): exact recomputation over the residual (amvm.cpp:181)
+  amvm_sumsq_kernel<<<1, 1, 0, c->stream>>>(c->d_resid.p, M, c->d_sc.p + 4);
+  CK(cudaMemcpyAsync(c->d_sc.p + 2, c->d_sc.p + 5, sizeof(double), cudaMemcpyDeviceToDevice,
+                     c->stream));
+  c->sync();
+  cnt.free(); pre.free(); first.free(); fsorted.free(); tid.free(); tS.free(); count.free();
+}
+}  // namespace
+
 int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long long n_cols,
                     double* gamma_pk, int* n_marked) {
   return guard(c, [&] {
@@ -2680,18 +2809,25 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
     CK(cudaMemcpyAsync(c->d_resid.p, c->d_diff.p, M * sizeof(double),
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemsetAsync(c->d_inset.p, 0, (size_t)std::max(nt, 1), c->stream));
-    c->timed("amvm_walk", [&] {
-      const int wsmem = 4 * kWalkSmem * (int)sizeof(double);
-      CK(cudaFuncSetAttribute(amvm_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              wsmem));
-      amvm_walk_kernel<<<1, 32, wsmem, c->stream>>>(c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p,
-                                                c->d_lists.p, c->d_eptr.p, c->d_eidx.p,
-                                                c->d_eval.p, c->d_nsq.p, c->d_resid.p,
-                                                c->d_inset.p, c->d_marked.p, c->d_nm.p,
-                                                c->d_sc.p + 2);
-    });
+    static const bool seq_walk = [] {
+      const char* e = std::getenv("HMGPU_AMVM_WALK");
+      return e && std::string(e) == "seq";
+    }();
+    if (seq_walk) {
+      c->timed("amvm_walk", [&] {
+        const int wsmem = 4 * kWalkSmem * (int)sizeof(double);
+        CK(cudaFuncSetAttribute(amvm_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                wsmem));
+        amvm_walk_kernel<<<1, 32, wsmem, c->stream>>>(
+            c->d_sc.p, theta, c->d_order.p, M, c->d_ptr.p, c->d_lists.p, c->d_eptr.p,
+            c->d_eidx.p, c->d_eval.p, c->d_nsq.p, c->d_resid.p, c->d_inset.p, c->d_marked.p,
+            c->d_nm.p, c->d_sc.p + 2);
+      });
+    } else {
+      parallel_walk(c, theta, M, nt);
+    }
     phase("walk");
-    if (verbose()) {
+    if (verbose() && seq_walk) {
       double st[2];
       CK(cudaMemcpy(st, c->d_sc.p + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost));
       std::fprintf(stderr, "[hmgpu] walk rows %.0f candidates %.0f\n", st[0], st[1]);

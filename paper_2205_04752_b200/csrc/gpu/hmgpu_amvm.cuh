@@ -412,6 +412,141 @@ amvm_walk_kernel(const double* __restrict__ sc, double theta, const int* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same greedy walk, parallel and bit-identical.  The walk's term
+// sequence S (rows in order, their candidates in order, each term at its
+// first appearance) does not depend on the residual; only the stopping
+// point does.  So: (1) S from the first-appearance position of every term
+// (atomicMin over the concatenated candidate lists, then a radix sort);
+// (2) per chunk of S, every entry's residual value BEFORE its term is
+// applied -- per output row the entries of the chunk's terms in S order,
+// subtracted sequentially from the carried residual (one thread per row
+// run of the (row, rank)-sorted entries: the reference's per-row order of
+// subtractions); (3) each term's dot = sum over its entries, in entry
+// order, of residual_before * value (the reference's loop, one thread per
+// term); (4) one thread scans res_sq += |term|^2 - 2 dot in S order and
+// stops at the first res_sq <= target; (5) the residual of every row takes
+// its value after the last applied entry.  Same operations, same order,
+// per row and per term as the sequential walk.
+__global__ void walk_cnt_kernel(const int* __restrict__ order, long long M,
+                                const int* __restrict__ ptr, long long* __restrict__ cnt) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q > M) return;
+  cnt[q] = q < M ? ptr[order[q] + 1] - ptr[order[q]] : 0;
+}
+__global__ void walk_first_kernel(const int* __restrict__ order, long long M,
+                                  const int* __restrict__ ptr, const int* __restrict__ lists,
+                                  const long long* __restrict__ pre,
+                                  unsigned long long* __restrict__ first) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= M) return;
+  const int r = order[q];
+  const int s0 = ptr[r], s1 = ptr[r + 1];
+  for (int s = s0; s < s1; ++s)
+    atomicMin(first + lists[s], (unsigned long long)(pre[q] + (s - s0)));
+}
+__global__ void walk_tids_kernel(int nt, int* __restrict__ tid, unsigned long long* __restrict__ first,
+                                 int* __restrict__ count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  tid[t] = t;
+  if (first[t] != ~0ull) atomicAdd(count, 1);
+}
+// entries of S's terms: sizes in S order (for the chunk offsets)
+__global__ void walk_sizes_kernel(const int* __restrict__ tS, int L,
+                                  const long long* __restrict__ eptr, long long* __restrict__ sz) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > L) return;
+  sz[k] = k < L ? eptr[tS[k] + 1] - eptr[tS[k]] : 0;
+}
+// chunk [k0, k1): one key (row << 22 | rank) per entry, the entry's global
+// position by chunk slot
+__global__ void walk_build_kernel(const int* __restrict__ tS, int k0, int k1,
+                                  const long long* __restrict__ cumE,
+                                  const long long* __restrict__ eptr,
+                                  const long long* __restrict__ eidx,
+                                  unsigned long long* __restrict__ keys, int* __restrict__ slots,
+                                  long long* __restrict__ gslot) {
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const int t = tS[k];
+  const long long base = cumE[k] - cumE[k0], e0 = eptr[t], n = eptr[t + 1] - e0;
+  for (long long e = 0; e < n; ++e) {
+    const long long sl = base + e;
+    keys[sl] = ((unsigned long long)eidx[e0 + e] << 22) | (unsigned long long)(k - k0);
+    slots[sl] = (int)sl;
+    gslot[sl] = e0 + e;
+  }
+}
+// (2): per row run of the sorted entries, the residual before each entry
+__global__ void walk_before_kernel(const unsigned long long* __restrict__ skeys,
+                                   const int* __restrict__ sslots, long long E,
+                                   const long long* __restrict__ gslot,
+                                   const double* __restrict__ eval,
+                                   const double* __restrict__ resid, double* __restrict__ rb) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const unsigned long long row = skeys[i] >> 22;
+  if (i > 0 && (skeys[i - 1] >> 22) == row) return;
+  double r = resid[row];
+  for (long long j = i; j < E && (skeys[j] >> 22) == row; ++j) {
+    const int sl = sslots[j];
+    rb[sl] = r;
+    r = r - eval[gslot[sl]];
+  }
+}
+// (3): dot of every chunk term, entry order
+__global__ void walk_dot_kernel(int k0, int k1, const long long* __restrict__ cumE,
+                                const long long* __restrict__ gslot,
+                                const double* __restrict__ eval, const double* __restrict__ rb,
+                                double* __restrict__ dots) {
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const long long b0 = cumE[k] - cumE[k0], b1 = cumE[k + 1] - cumE[k0];
+  double d = 0.0;
+  for (long long sl = b0; sl < b1; ++sl) d += rb[sl] * eval[gslot[sl]];
+  dots[k - k0] = d;
+}
+// (4): the sequential res_sq scan; st[0] = res_sq (in/out), st[1] = stop
+// rank within the chunk or -1
+__global__ void walk_scan_kernel(const int* __restrict__ tS, int k0, int k1,
+                                 const double* __restrict__ nsq, const double* __restrict__ dots,
+                                 double target_sq, double* __restrict__ st) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double res = st[0];
+  int stop = -1;
+  for (int k = k0; k < k1; ++k) {
+    res += nsq[tS[k]] - 2.0 * dots[k - k0];
+    if (res <= target_sq) {
+      stop = k - k0;
+      break;
+    }
+  }
+  st[0] = res;
+  st[1] = (double)stop;
+}
+// (5): rows take their value after the last applied entry (rank <= lim)
+__global__ void walk_apply_kernel(const unsigned long long* __restrict__ skeys,
+                                  const int* __restrict__ sslots, long long E,
+                                  const long long* __restrict__ gslot,
+                                  const double* __restrict__ eval, const double* __restrict__ rb,
+                                  const double* __restrict__ st, int nchunk,
+                                  double* __restrict__ resid) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const unsigned long long row = skeys[i] >> 22;
+  if (i > 0 && (skeys[i - 1] >> 22) == row) return;
+  const int stop = (int)st[1];
+  const unsigned long long lim = stop >= 0 ? (unsigned long long)stop : (unsigned long long)(nchunk - 1);
+  long long last = -1;
+  for (long long j = i; j < E && (skeys[j] >> 22) == row; ++j)
+    if ((skeys[j] & ((1ull << 22) - 1)) <= lim) last = j;
+  if (last >= 0) {
+    const int sl = sslots[last];
+    resid[row] = rb[sl] - eval[gslot[sl]];
+  }
+}
+
 // marked term -> work item
 __global__ void amvm_items_kernel(const TailTerm* __restrict__ terms,
                                   const int* __restrict__ marked, const int* __restrict__ n,
