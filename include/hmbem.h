@@ -81,6 +81,13 @@ int hmb_admissible(const double* box_a6, const double* box_b6, double eta, int* 
 /* ---- operators (device < 0: host-only, tree and partition) ---- */
 int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
                   int device, int shard_rank, int shard_count, hmb_op** out);
+/* the single-layer grid of evaluate_interior (baca.cpp:625-687): Kelvin
+ * collocation at npts points (rows, a tree over the point boxes) against the
+ * triangles (columns); points within min_distance_factor x the largest
+ * triangle diameter of the surface are rejected (baca.cpp:632-643) */
+int hmb_op_kelvin_points(const hmb_mesh* m, int npts, const double* pts, double E,
+                         double nu, int b_min, double eta, double min_distance_factor,
+                         int device, int shard_rank, int shard_count, hmb_op** out);
 /* Galerkin scalar kernels on the triangle partition (assemble_operators,
  * operators.cpp:186-235): which = 0 -> the six V_kl as the 3x3 grid,
  * 1 -> V_Delta (kernels.cpp:130-149) */

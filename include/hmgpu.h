@@ -11,6 +11,8 @@
  *                              (proj/include/hmbem/kernels.hpp:107-126,
  *                               proj/src/kernels.cpp:21-28,87-93,176-187),
  *                              fused into the kernels instead of a callback
+ *   hmgpu_set_eval_points      CollocSingleOracle at evaluate_interior's points
+ *                              (proj/src/baca.cpp:645-687)
  *   hmgpu_set_rule             gauss_rule(order) tables (proj/src/quadrature.cpp:55-95)
  *   hmgpu_set_galerkin_geometry  KernelOracle over V_Delta / V_kl: GalerkinKernels::
  *                              vdelta / vkl / integrate_pair / disjoint_order
@@ -166,6 +168,11 @@ int hmgpu_ell3_spmv(hmgpu_ctx* ctx, int rows, const int* col3, const double* val
 int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslot,
                       const double* val3, const double* x, double* y, double alpha,
                       double beta);
+/* Kelvin context only: collocation at n arbitrary evaluation points (the
+ * rows; CollocSingleOracle with evaluate_interior's points, kernels.hpp:
+ * 107-126, baca.cpp:645-687) instead of the triangle centroids; n = 0
+ * restores the centroids.  The partition's rows are then the points. */
+int hmgpu_set_eval_points(hmgpu_ctx* ctx, int n, const double* pts);
 /* scalar Newton kernel 1/|x_i - x_j| with entry `diag` where x_i == x_j */
 int hmgpu_set_points(hmgpu_ctx* ctx, int n, const double* pts, double diag);
 /* scalar explicit matrix, column-major m x n, external ids */

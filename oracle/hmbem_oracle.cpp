@@ -889,6 +889,19 @@ struct KDeltaOracle : EntryOracle {
   }
 };
 
+// CollocSingleOracle(r, c) at arbitrary evaluation points (kernels.hpp:107-126
+// as evaluate_interior uses it, baca.cpp:657-668)
+struct KelvinPointOracle : EntryOracle {
+  const Kelvin* k;
+  const std::vector<Vec3>* pts;
+  int r, c;
+  long rows() const override { return static_cast<long>(pts->size()); }
+  long cols() const override { return k->mesh->nt(); }
+  Real entry(long i, long j) const override {
+    return k->colloc_single((*pts)[i], r, c, static_cast<int>(j));
+  }
+};
+
 // Newton kernel over points with a bounded diagonal: CentroidKernelOracle /
 // PointKernelOracle fixtures (proj/tests/test_hmatrix.cpp:12-28,
 // proj/tests/test_amvm.cpp:9-22)
@@ -1486,6 +1499,7 @@ static int comp_index(int r, int c) {
 struct Grid {
   int ncomp = 1;           // 1 (scalar H-matrix) or 6 (Kelvin 3x3 grid)
   long nblk = 0;           // rows per grid cell
+  long ncol = 0;           // columns per grid cell (0: square, = nblk)
   std::vector<std::unique_ptr<HMatrix>> h;
   long rows() const { return ncomp == 6 ? 3 * nblk : nblk; }
 
@@ -1494,11 +1508,12 @@ struct Grid {
       h[0]->matvec(x, y, mode);
       return;
     }
+    const long nc = ncol > 0 ? ncol : nblk;
     std::vector<Real> tmp(nblk);
     std::fill(y, y + 3 * nblk, 0.0);
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
-        h[comp_index(i, j)]->matvec(x + j * nblk, tmp.data(), mode);
+        h[comp_index(i, j)]->matvec(x + j * nc, tmp.data(), mode);
         for (long p = 0; p < nblk; ++p) y[i * nblk + p] += tmp[p];
       }
   }
@@ -1771,6 +1786,7 @@ struct Problem {
   Material mat;
   std::unique_ptr<Kelvin> kelvin;
   std::unique_ptr<Galerkin> galerkin;
+  std::vector<Vec3> eval_pts;
   std::vector<std::unique_ptr<EntryOracle>> oracles;
   Tree rows_tree, cols_tree;
   std::unique_ptr<Partition> part;
@@ -1935,6 +1951,52 @@ int or_problem_kelvin(int nv, const double* verts, int nt, const int* tris,
     }
     p->grid.ncomp = 6;
     p->grid.nblk = nt;
+    *out = p.release();
+  });
+}
+
+// kind 6: the single-layer grid of evaluate_interior -- Kelvin collocation at
+// arbitrary points (rows: point-box tree; columns: the triangle tree),
+// partition (point tree, triangle tree, eta) (baca.cpp:645-653)
+int or_problem_kelvin_points(int nv, const double* verts, int nt, const int* tris, int npts,
+                             const double* pts, double E, double nu, int b_min, double eta,
+                             void** out) {
+  return guard([&] {
+    auto p = std::make_unique<Problem>();
+    p->kind = 6;
+    p->mesh.vertices.resize(nv);
+    for (int v = 0; v < nv; ++v)
+      p->mesh.vertices[v] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]};
+    p->mesh.triangles.resize(nt);
+    for (int t = 0; t < nt; ++t)
+      p->mesh.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    finish_geometry(p->mesh);
+    p->mat = {E, nu};
+    p->kelvin = std::make_unique<Kelvin>(&p->mesh, p->mat);
+    p->eval_pts.resize(npts);
+    std::vector<Box> pb(npts), tb(nt);
+    for (int i = 0; i < npts; ++i) {
+      p->eval_pts[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+      pb[i].absorb(p->eval_pts[i]);
+    }
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k) tb[t].absorb(p->mesh.corner(t, k));
+    p->n = npts;
+    p->rows_tree = build_cluster_tree(pb, b_min);
+    p->cols_tree = build_cluster_tree(tb, b_min);
+    p->part = std::make_unique<Partition>(
+        build_block_partition(&p->rows_tree, &p->cols_tree, eta));
+    for (int c = 0; c < 6; ++c) {
+      auto o = std::make_unique<KelvinPointOracle>();
+      o->k = p->kelvin.get();
+      o->pts = &p->eval_pts;
+      o->r = kCompR[c];
+      o->c = kCompC[c];
+      p->oracles.push_back(std::move(o));
+    }
+    p->grid.ncomp = 6;
+    p->grid.nblk = npts;
+    p->grid.ncol = nt;
     *out = p.release();
   });
 }

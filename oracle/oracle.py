@@ -200,6 +200,18 @@ class Problem:
         return cls(h, 6 if which == 0 else 1, len(t))
 
     @classmethod
+    def kelvin_points(cls, verts, tris, pts, E=1.0, nu=0.3, b_min=32, eta=1.0):
+        """evaluate_interior's single-layer grid: Kelvin collocation at
+        arbitrary points (baca.cpp:645-687)."""
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32)
+        p = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        h = C.c_void_p()
+        _ck(lib().or_problem_kelvin_points(len(v), _p(v), len(t), _p(t), len(p), _p(p), D(E),
+                                           D(nu), b_min, D(eta), C.byref(h)))
+        return cls(h, 6, len(p), len(t))
+
+    @classmethod
     def kdelta(cls, verts, tris, b_min=32, eta=1.0):
         """K_Delta on the triangle x node partition (kernels.cpp:151-167,
         operators.cpp:186-200): rows triangles, columns vertices."""
@@ -279,13 +291,13 @@ class Problem:
         the Galerkin V_kl grid), component-major."""
         if self.ncomp == 1:
             return self.dense(0)
-        n = self.n
-        A = np.zeros((3 * n, 3 * n))
+        n, nc = self.n, self.ncols
+        A = np.zeros((3 * n, 3 * nc))
         idx = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 1): 3, (1, 2): 4, (2, 2): 5}
         for (r, c), k in idx.items():
             blk = self.dense(k)
-            A[r * n:(r + 1) * n, c * n:(c + 1) * n] = blk
-            A[c * n:(c + 1) * n, r * n:(r + 1) * n] = blk
+            A[r * n:(r + 1) * n, c * nc:(c + 1) * nc] = blk
+            A[c * n:(c + 1) * n, r * nc:(r + 1) * nc] = blk
         return A
 
     def assemble(self, eps=1e-6, beta=0.8, initial_rank=-1, lookahead=2, max_rank=1 << 30):

@@ -276,6 +276,20 @@ class HMatrix:
         return cls(out)
 
     @classmethod
+    def kelvin_points(cls, mesh: Mesh, points, E: float = 1.0, nu: float = 0.3,
+                      b_min: int = 32, eta: float = 1.0, min_distance_factor: float = 0.5,
+                      device: int = 0, shard: tuple = (0, 1)) -> "HMatrix":
+        """The single-layer grid V~ of evaluate_interior (baca.cpp:625-687):
+        CollocSingleOracle(r, c) at arbitrary points (rows) against the
+        triangles (columns); 3 n_points x 3 N_t."""
+        p = _f64(points).reshape(-1, 3)
+        out = C.c_void_p()
+        _check(_h.hmb_op_kelvin_points(mesh._h, len(p), _ptr(p), E, nu, b_min, eta,
+                                       min_distance_factor, device, shard[0], shard[1],
+                                       C.byref(out)))
+        return cls(out)
+
+    @classmethod
     def galerkin(cls, mesh: Mesh, which: int = 0, b_min: int = 32, eta: float = 1.0,
                  device: int = 0, shard: tuple = (0, 1)) -> "HMatrix":
         """Galerkin scalar kernels over triangle pairs (GalerkinKernels,

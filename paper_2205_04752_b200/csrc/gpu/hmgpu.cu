@@ -364,6 +364,7 @@ struct hmgpu_ctx {
   bool rules_set[3] = {false, false, false};
   int gal_which = 0;                   // galerkin: 0 V_kl grid, 1 V_Delta
   std::vector<double> normals;         // K_Delta: unit normals per triangle
+  std::vector<double> eval_pts;        // Kelvin: evaluation points (empty: centroids)
   std::vector<double> prule[4];        // galerkin singular pair rules, SoA per case
   int prule_n[4] = {0, 0, 0, 0};
 
@@ -611,19 +612,22 @@ int grid_for(hmgpu_ctx* c, long long work, int per_sm = 8) {
 void build_geometry(hmgpu_ctx* c) {
   Geom g{};
   g.kind = c->kind;
-  g.same_tree = c->same_tree ? 1 : 0;
+  // evaluation points are never the column triangles' centroids (no self term)
+  g.same_tree = c->same_tree && c->eval_pts.empty() ? 1 : 0;
   c->d_rperm.upload(c->rperm, c->stream);
   c->d_cperm.upload(c->cperm, c->stream);
   g.rperm = c->d_rperm.p;
   g.cperm = c->d_cperm.p;
   if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN) {
-    if (c->n_tri != c->n_rows || c->n_tri != c->n_cols)
+    const bool pts = c->kind == KIND_KELVIN && !c->eval_pts.empty();
+    const long long nrow_geo = pts ? (long long)c->eval_pts.size() / 3 : c->n_tri;
+    if (nrow_geo != c->n_rows || c->n_tri != c->n_cols)
       fail(HMGPU_ERR_DIMENSION, "triangle geometry does not match the partition");
+    const double* rsrc = pts ? c->eval_pts.data() : c->centroid.data();
     std::vector<double4> rp(c->n_rows);
     for (int i = 0; i < c->n_rows; ++i) {
       const int t = c->rperm[i];
-      rp[i] = make_double4(c->centroid[3 * t], c->centroid[3 * t + 1],
-                           c->centroid[3 * t + 2], 0.0);
+      rp[i] = make_double4(rsrc[3LL * t], rsrc[3LL * t + 1], rsrc[3LL * t + 2], 0.0);
     }
     // tiles of 32 triangles x 16 field slots (TriRef in hmgpu_device.cuh)
     const long long ntile = (c->n_cols + 31) / 32;
@@ -1900,6 +1904,15 @@ int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslo
     ell3_spmv_t_kernel<<<grid_for(ctx, (cols + 255) / 256), 256, 0, ctx->stream>>>(
         cols, tptr, tslot, val3, x, y, alpha, beta);
     CK(cudaGetLastError());
+  });
+}
+
+int hmgpu_set_eval_points(hmgpu_ctx* ctx, int n, const double* pts) {
+  return guard(ctx, [&] {
+    if (ctx->kind != KIND_KELVIN) fail(HMGPU_ERR_STATE, "set the Kelvin geometry first");
+    if (n < 0 || (n > 0 && !pts)) fail(HMGPU_ERR_INVALID, "bad evaluation points");
+    ctx->eval_pts.assign(pts, pts + 3LL * n);
+    ctx->assembled = false;
   });
 }
 

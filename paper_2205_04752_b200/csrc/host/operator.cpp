@@ -1,5 +1,9 @@
 #include "operator.hpp"
 
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -136,6 +140,96 @@ std::unique_ptr<HOperator> HOperator::kelvin(const Mesh& mesh, Real E, Real nu,
                                       tris.data(), cen.data(), mesh.areas.data(),
                                       mesh.diam.data(), E, nu),
             "hmgpu_set_kelvin_geometry");
+  for (int tier = 0; tier < 3; ++tier) {
+    const TriangleRule r = gauss_rule(qc.tier_order(tier));
+    op->check(hmgpu_set_rule(op->ctx_, tier, static_cast<int>(r.w.size()), r.a.data(),
+                             r.b.data(), r.w.data()),
+              "hmgpu_set_rule");
+  }
+  op->check(hmgpu_set_tier_ratios(op->ctx_, qc.far_ratio, qc.mid_ratio),
+            "hmgpu_set_tier_ratios");
+  return op;
+}
+
+namespace {
+// distance from p to the triangle (a, b, c): the plane projection when it
+// falls inside, else the nearest edge point (validation threshold only)
+Real point_triangle_distance(const V3& p, const V3& a, const V3& b, const V3& c) {
+  auto sub = [](const V3& x, const V3& y) { return V3{x[0] - y[0], x[1] - y[1], x[2] - y[2]}; };
+  auto dot = [](const V3& x, const V3& y) { return x[0] * y[0] + x[1] * y[1] + x[2] * y[2]; };
+  auto seg = [&](const V3& u, const V3& v) {
+    const V3 d = sub(v, u), w = sub(p, u);
+    Real t = dot(w, d) / dot(d, d);
+    t = std::min(1.0, std::max(0.0, t));
+    const V3 q{u[0] + t * d[0] - p[0], u[1] + t * d[1] - p[1], u[2] + t * d[2] - p[2]};
+    return std::sqrt(dot(q, q));
+  };
+  const V3 e0 = sub(b, a), e1 = sub(c, a), w = sub(p, a);
+  const Real a00 = dot(e0, e0), a01 = dot(e0, e1), a11 = dot(e1, e1);
+  const Real det = a00 * a11 - a01 * a01;
+  const Real s = (a11 * dot(w, e0) - a01 * dot(w, e1)) / det;
+  const Real t = (a00 * dot(w, e1) - a01 * dot(w, e0)) / det;
+  if (s >= 0 && t >= 0 && s + t <= 1) {
+    const V3 q{a[0] + s * e0[0] + t * e1[0] - p[0], a[1] + s * e0[1] + t * e1[1] - p[1],
+               a[2] + s * e0[2] + t * e1[2] - p[2]};
+    return std::sqrt(dot(q, q));
+  }
+  return std::min({seg(a, b), seg(b, c), seg(c, a)});
+}
+}  // namespace
+
+std::unique_ptr<HOperator> HOperator::kelvin_points(const Mesh& mesh,
+                                                    const std::vector<V3>& points, Real E,
+                                                    Real nu, int b_min, Real eta, int device,
+                                                    Shard shard, Real min_distance_factor,
+                                                    QuadratureConfig qc) {
+  if (mesh.centroids.size() != mesh.triangles.size())
+    throw MeshError("mesh geometry caches missing (call finish())");
+  if (points.empty()) throw Error("evaluate_interior: no points");
+  if (E <= 0.0) throw Error("lame_constants: E must be positive");
+  if (nu <= 0.0 || nu >= 0.5) throw Error("lame_constants: nu must lie in (0, 1/2)");
+  Real max_diam = 0.0;
+  for (Real d : mesh.diam) max_diam = std::max(max_diam, d);
+  const Real min_dist = min_distance_factor * max_diam;
+  for (size_t i = 0; i < points.size(); ++i) {
+    Real d = std::numeric_limits<Real>::max();
+    for (int t = 0; t < mesh.nt() && d > min_dist; ++t)
+      d = std::min(d, point_triangle_distance(points[i], mesh.corner(t, 0), mesh.corner(t, 1),
+                                              mesh.corner(t, 2)));
+    if (d <= min_dist)
+      throw Error("evaluate_interior: point " + std::to_string(i) +
+                  " is closer to the surface than the quadrature threshold");
+  }
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = Kelvin;
+  op->ncomp_ = 6;
+  op->n_rows_ = static_cast<int>(points.size());
+  op->n_cols_ = mesh.nt();
+  std::vector<Box> pb(points.size());
+  for (size_t i = 0; i < points.size(); ++i) pb[i].absorb(points[i]);
+  op->rows_ = std::make_unique<ClusterTree>(build_cluster_tree(pb, b_min));
+  op->cols_ = std::make_unique<ClusterTree>(
+      build_cluster_tree(triangle_supports(mesh), b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  std::vector<double> verts(3 * mesh.nv()), cen(3 * mesh.nt()), ep(3 * points.size());
+  std::vector<int> tris(3 * mesh.nt());
+  for (int v = 0; v < mesh.nv(); ++v)
+    for (int d = 0; d < 3; ++d) verts[3 * v + d] = mesh.vertices[v][d];
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int d = 0; d < 3; ++d) {
+      tris[3 * t + d] = mesh.triangles[t][d];
+      cen[3 * t + d] = mesh.centroids[t][d];
+    }
+  for (size_t i = 0; i < points.size(); ++i)
+    for (int d = 0; d < 3; ++d) ep[3 * i + d] = points[i][d];
+  op->check(hmgpu_set_kelvin_geometry(op->ctx_, mesh.nv(), verts.data(), mesh.nt(),
+                                      tris.data(), cen.data(), mesh.areas.data(),
+                                      mesh.diam.data(), E, nu),
+            "hmgpu_set_kelvin_geometry");
+  op->check(hmgpu_set_eval_points(op->ctx_, static_cast<int>(points.size()), ep.data()),
+            "hmgpu_set_eval_points");
   for (int tier = 0; tier < 3; ++tier) {
     const TriangleRule r = gauss_rule(qc.tier_order(tier));
     op->check(hmgpu_set_rule(op->ctx_, tier, static_cast<int>(r.w.size()), r.a.data(),

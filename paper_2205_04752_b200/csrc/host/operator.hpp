@@ -58,6 +58,17 @@ class HOperator {
                                            int b_min, Real eta, int device,
                                            Shard shard = {},
                                            QuadratureConfig qc = {});
+  // The single-layer part of evaluate_interior (baca.cpp:625-687): Kelvin
+  // collocation at arbitrary points (rows: a tree over the point boxes;
+  // columns: the triangle tree), points closer to the surface than
+  // min_distance_factor x the largest triangle diameter rejected
+  // (baca.cpp:632-643)
+  static std::unique_ptr<HOperator> kelvin_points(const Mesh& mesh,
+                                                  const std::vector<V3>& points, Real E,
+                                                  Real nu, int b_min, Real eta, int device,
+                                                  Shard shard = {},
+                                                  Real min_distance_factor = 0.5,
+                                                  QuadratureConfig qc = {});
   // Galerkin scalar kernels on the triangle partition of assemble_operators
   // (operators.cpp:186-200, 218-235): which = 0 the six V_kl as the 3x3
   // grid, 1 V_Delta (GalerkinKernels::vkl / vdelta, kernels.cpp:130-149)
