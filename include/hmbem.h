@@ -87,7 +87,15 @@ int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
  * triangle diameter of the surface are rejected (baca.cpp:632-643) */
 int hmb_op_kelvin_points(const hmb_mesh* m, int npts, const double* pts, double E,
                          double nu, int b_min, double eta, double min_distance_factor,
-                         int device, int shard_rank, int shard_count, hmb_op** out);
+                         int disjoint_order, int device, int shard_rank, int shard_count,
+                         hmb_op** out);
+/* one cell (r, c) of evaluate_interior's double-layer grid W~
+ * (CollocDoubleOracle, kernels.cpp:189-210): points x vertices, partition
+ * point tree x node tree (baca.cpp:650-651) */
+int hmb_op_kelvin_double(const hmb_mesh* m, int npts, const double* pts, int r, int c,
+                         double E, double nu, int b_min, double eta,
+                         double min_distance_factor, int disjoint_order, int device,
+                         int shard_rank, int shard_count, hmb_op** out);
 /* Galerkin scalar kernels on the triangle partition (assemble_operators,
  * operators.cpp:186-235): which = 0 -> the six V_kl as the 3x3 grid,
  * 1 -> V_Delta (kernels.cpp:130-149) */

@@ -11,6 +11,8 @@
  *                              (proj/include/hmbem/kernels.hpp:107-126,
  *                               proj/src/kernels.cpp:21-28,87-93,176-187),
  *                              fused into the kernels instead of a callback
+ *   hmgpu_set_kdouble_geometry CollocDoubleOracle (colloc_double + kelvin_traction,
+ *                              proj/src/kernels.cpp:30-55,189-210), points x nodes
  *   hmgpu_set_eval_points      CollocSingleOracle at evaluate_interior's points
  *                              (proj/src/baca.cpp:645-687)
  *   hmgpu_set_rule             gauss_rule(order) tables (proj/src/quadrature.cpp:55-95)
@@ -168,6 +170,15 @@ int hmgpu_ell3_spmv(hmgpu_ctx* ctx, int rows, const int* col3, const double* val
 int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslot,
                       const double* val3, const double* x, double* y, double alpha,
                       double beta);
+/* One cell (r, c) of evaluate_interior's double-layer grid W~
+ * (CollocDoubleOracle / colloc_double, kernels.cpp:189-210, with
+ * kelvin_traction, kernels.cpp:30-55): rows = the evaluation points of
+ * hmgpu_set_eval_points, columns = the vertices (node patches); arrays as
+ * hmgpu_set_kdelta_geometry; rule tiers as the single layer. */
+int hmgpu_set_kdouble_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts, int n_tri,
+                               const int* tris, const double* centroid, const double* area,
+                               const double* diam, const double* normals, double E,
+                               double nu, int r, int c);
 /* Kelvin context only: collocation at n arbitrary evaluation points (the
  * rows; CollocSingleOracle with evaluate_interior's points, kernels.hpp:
  * 107-126, baca.cpp:645-687) instead of the triangle centroids; n = 0

@@ -364,12 +364,14 @@ struct Kelvin {
 
   // point_order with QuadratureConfig defaults disjoint_order = 4,
   // far_ratio = 4, mid_ratio = 1.5 (kernels.cpp:87-93, kernels.hpp:44-52)
+  int disjoint_order = 4;
+  void set_disjoint_order(int o) { disjoint_order = o; }
   int point_order(const Vec3& p, int tj) const {
     const Real dj = mesh->diam[tj];
     const Real gap = norm3(sub(p, mesh->centroids[tj])) - 0.5 * dj;
-    if (gap >= 4.0 * dj) return 2;
-    if (gap >= 1.5 * dj) return 4;
-    return 5;
+    if (gap >= 4.0 * dj) return std::min(disjoint_order, 2);
+    if (gap >= 1.5 * dj) return disjoint_order;
+    return std::min(disjoint_order + 1, 6);
   }
 
   // colloc_single: 2 area_j sum_q w_q S(p - y_q)_rc (kernels.cpp:176-187)
@@ -469,6 +471,87 @@ struct Kelvin {
     const int rr[6] = {0, 0, 0, 1, 1, 2}, cc[6] = {0, 1, 2, 1, 2, 2};
     for (int k = 0; k < 6; ++k)
       out6[k] = cst * ((rr[k] == cc[k] ? c34 * i1 : 0.0) + irc[rr[k]][cc[k]]);
+  }
+
+  // ---- double layer (colloc_double, kernels.cpp:189-210) ----------------
+  // kelvin_traction (kernels.cpp:30-55) in closed form: with x = y - p,
+  // n . x = nx, r = |x|:
+  //   T_ij = c [ ((2mu - 2 lambda (1-2nu)) n_i x_j + mu (1-k34) n_j x_i
+  //             + delta_ij mu (1-k34) nx) / r^3 - 6 mu x_i x_j nx / r^5 ]
+  // Canonical order (shared with the device): rsqrt_canon, explicit fma.
+  std::vector<std::vector<int>> vtri;  // vertex_triangles (mesh.cpp:245-247)
+  Real lam = 0.0, mu = 0.0;
+  void prepare_double() {
+    lame_constants(mat.E, mat.nu, lam, mu);
+    vtri.assign(mesh->vertices.size(), {});
+    for (int t = 0; t < mesh->nt(); ++t)
+      for (int v : mesh->triangles[t]) vtri[v].push_back(t);
+  }
+  Real colloc_double(const Vec3& p, int r, int c, int node) const {
+    const Real b1 = 2.0 * mu - 2.0 * lam * (1.0 - 2.0 * mat.nu);
+    const Real a2 = mu * (1.0 - c34());
+    const Real a6 = 6.0 * mu;
+    Real acc = 0.0;
+    for (int tau : vtri[node]) {
+      const Rule& rule = rules[point_order(p, tau)];
+      int local = 0;
+      while (mesh->triangles[tau][local] != node) ++local;
+      const Vec3 y0 = mesh->corner(tau, 0), y1 = mesh->corner(tau, 1),
+                 y2 = mesh->corner(tau, 2);
+      const Vec3 e1 = sub(y1, y0), e2 = sub(y2, y0);
+      const Vec3& n = mesh->normals[tau];
+      Real part = 0.0;
+      for (std::size_t q = 0; q < rule.w.size(); ++q) {
+        const Real a = rule.a[q], b = rule.b[q];
+        Real x[3];
+        for (int d = 0; d < 3; ++d) x[d] = std::fma(b, e2[d], std::fma(a, e1[d], y0[d])) - p[d];
+        const Real ri = rsqrt_canon(std::fma(x[2], x[2], std::fma(x[1], x[1], x[0] * x[0])));
+        const Real ri2 = ri * ri, ri3 = ri2 * ri, ri5 = ri3 * ri2;
+        const Real nx = std::fma(x[2], n[2], std::fma(x[1], n[1], x[0] * n[0]));
+        Real sv = std::fma(b1, n[r] * x[c], a2 * (n[c] * x[r]));
+        if (r == c) sv = std::fma(a2, nx, sv);
+        const Real v = std::fma(-(a6 * ri5), (x[r] * x[c]) * nx, ri3 * sv);
+        const Real psi = local == 0 ? (1.0 - a) - b : (local == 1 ? a : b);
+        part = std::fma(rule.w[q] * psi, v, part);
+      }
+      acc = acc + (2.0 * mesh->areas[tau] * cst()) * part;
+    }
+    return acc;
+  }
+  // the literal reference form (kelvin_traction per point) -- checks the
+  // canonical order only
+  Real colloc_double_literal(const Vec3& p, int r, int c, int node) const {
+    const Real cc = cst(), k34 = c34();
+    Real acc = 0.0;
+    for (int tau : vtri[node]) {
+      const Rule& rule = rules[point_order(p, tau)];
+      int local = 0;
+      while (mesh->triangles[tau][local] != node) ++local;
+      const Vec3 y0 = mesh->corner(tau, 0), y1 = mesh->corner(tau, 1),
+                 y2 = mesh->corner(tau, 2);
+      const Vec3& n = mesh->normals[tau];
+      Real part = 0.0;
+      for (std::size_t q = 0; q < rule.w.size(); ++q) {
+        const Real b1 = rule.a[q], b2 = rule.b[q];
+        Vec3 x;
+        for (int d = 0; d < 3; ++d)
+          x[d] = (y0[d] + b1 * (y1[d] - y0[d]) + b2 * (y2[d] - y0[d])) - p[d];
+        const Real rr = norm3(x), r3 = rr * rr * rr, r5 = r3 * rr * rr;
+        auto dU = [&](int k, int i, int j) {
+          Real v = -k34 * (i == j ? x[k] / r3 : 0.0);
+          v += ((i == k ? x[j] : 0.0) + (j == k ? x[i] : 0.0)) / r3;
+          v -= 3.0 * x[i] * x[j] * x[k] / r5;
+          return cc * v;
+        };
+        const Real div_j = -2.0 * cc * (1.0 - 2.0 * mat.nu) * x[c] / r3;
+        Real t = lam * n[r] * div_j;
+        for (int k = 0; k < 3; ++k) t += mu * n[k] * (dU(k, r, c) + dU(r, k, c));
+        const Real psi = local == 0 ? 1.0 - b1 - b2 : local == 1 ? b1 : b2;
+        part += rule.w[q] * t * psi;
+      }
+      acc += 2.0 * mesh->areas[tau] * part;
+    }
+    return acc;
   }
 
   // north-star entry: centroid collocation, A_rc[i,j]
@@ -899,6 +982,19 @@ struct KelvinPointOracle : EntryOracle {
   long cols() const override { return k->mesh->nt(); }
   Real entry(long i, long j) const override {
     return k->colloc_single((*pts)[i], r, c, static_cast<int>(j));
+  }
+};
+
+// CollocDoubleOracle(r, c) at arbitrary points (kernels.hpp:128-147):
+// points x nodes
+struct KelvinDoubleOracle : EntryOracle {
+  const Kelvin* k;
+  const std::vector<Vec3>* pts;
+  int r, c;
+  long rows() const override { return static_cast<long>(pts->size()); }
+  long cols() const override { return static_cast<long>(k->mesh->vertices.size()); }
+  Real entry(long i, long j) const override {
+    return k->colloc_double((*pts)[i], r, c, static_cast<int>(j));
   }
 };
 
@@ -2001,6 +2097,53 @@ int or_problem_kelvin_points(int nv, const double* verts, int nt, const int* tri
   });
 }
 
+// kind 7: one cell (r, c) of evaluate_interior's double-layer grid W~
+// (CollocDoubleOracle, points x nodes; partition point tree x node tree,
+// baca.cpp:650-651, 674-677); disjoint_order as QuadratureConfig
+int or_problem_kelvin_double(int nv, const double* verts, int nt, const int* tris, int npts,
+                             const double* pts, int r, int c, double E, double nu, int b_min,
+                             double eta, int disjoint_order, void** out) {
+  return guard([&] {
+    auto p = std::make_unique<Problem>();
+    p->kind = 7;
+    p->mesh.vertices.resize(nv);
+    for (int v = 0; v < nv; ++v)
+      p->mesh.vertices[v] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]};
+    p->mesh.triangles.resize(nt);
+    for (int t = 0; t < nt; ++t)
+      p->mesh.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    finish_geometry(p->mesh);
+    p->mat = {E, nu};
+    p->kelvin = std::make_unique<Kelvin>(&p->mesh, p->mat);
+    p->kelvin->set_disjoint_order(disjoint_order);
+    p->kelvin->prepare_double();
+    p->eval_pts.resize(npts);
+    std::vector<Box> pb(npts), tb(nt), nb(nv);
+    for (int i = 0; i < npts; ++i) {
+      p->eval_pts[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+      pb[i].absorb(p->eval_pts[i]);
+    }
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k) tb[t].absorb(p->mesh.corner(t, k));
+    for (int v = 0; v < nv; ++v)
+      for (int t : p->kelvin->vtri[v]) nb[v].absorb(tb[t]);
+    p->n = npts;
+    p->rows_tree = build_cluster_tree(pb, b_min);
+    p->cols_tree = build_cluster_tree(nb, b_min);
+    p->part = std::make_unique<Partition>(
+        build_block_partition(&p->rows_tree, &p->cols_tree, eta));
+    auto o = std::make_unique<KelvinDoubleOracle>();
+    o->k = p->kelvin.get();
+    o->pts = &p->eval_pts;
+    o->r = r;
+    o->c = c;
+    p->oracles.push_back(std::move(o));
+    p->grid.ncomp = 1;
+    p->grid.nblk = npts;
+    *out = p.release();
+  });
+}
+
 // kinds 3 / 4: Galerkin scalar kernels on the triangle partition of
 // assemble_operators (operators.cpp:186-200, corner boxes, one tree):
 // which = 0 -> the six V_kl as a symmetric 3x3 grid, 1 -> V_Delta alone.
@@ -2277,6 +2420,11 @@ int or_entry_literal(void* h, int comp, long i, long j, double* out) {
     Problem* p = P(h);
     if (p->kind == 5) {
       *out = p->galerkin->kdelta_literal(static_cast<int>(i), static_cast<int>(j));
+      return;
+    }
+    if (p->kind == 7) {
+      const auto* o = static_cast<const KelvinDoubleOracle*>(p->oracles[0].get());
+      *out = p->kelvin->colloc_double_literal(p->eval_pts[i], o->r, o->c, static_cast<int>(j));
       return;
     }
     if (p->kind == 3 || p->kind == 4) {

@@ -212,6 +212,20 @@ class Problem:
         return cls(h, 6, len(p), len(t))
 
     @classmethod
+    def kelvin_double(cls, verts, tris, pts, r, c, E=1.0, nu=0.3, b_min=32, eta=1.0,
+                      disjoint_order=4):
+        """One cell (r, c) of evaluate_interior's double-layer grid W~
+        (CollocDoubleOracle, kernels.cpp:189-210): points x nodes."""
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32)
+        p = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        h = C.c_void_p()
+        _ck(lib().or_problem_kelvin_double(len(v), _p(v), len(t), _p(t), len(p), _p(p), r, c,
+                                           D(E), D(nu), b_min, D(eta), disjoint_order,
+                                           C.byref(h)))
+        return cls(h, 1, len(p), len(v))
+
+    @classmethod
     def kdelta(cls, verts, tris, b_min=32, eta=1.0):
         """K_Delta on the triangle x node partition (kernels.cpp:151-167,
         operators.cpp:186-200): rows triangles, columns vertices."""

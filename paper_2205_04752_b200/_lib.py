@@ -57,7 +57,8 @@ _sig(host, "hmb_gauss_rule", I, I, IP, P, P, P)
 _sig(host, "hmb_random_vector", I, LL, C.c_ulonglong, I, P)
 _sig(host, "hmb_op_kelvin", I, P, D, D, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_galerkin", I, P, I, I, D, I, I, I, C.POINTER(P))
-_sig(host, "hmb_op_kelvin_points", I, P, I, P, D, D, I, D, D, I, I, I, C.POINTER(P))
+_sig(host, "hmb_op_kelvin_points", I, P, I, P, D, D, I, D, D, I, I, I, I, C.POINTER(P))
+_sig(host, "hmb_op_kelvin_double", I, P, I, P, I, I, D, D, I, D, D, I, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_kdelta", I, P, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_sparse_op", I, P, I, P, P)
 _sig(gpu, "hmgpu_ell3_spmv", I, P, I, P, P, P, P, D, D)

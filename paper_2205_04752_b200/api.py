@@ -278,15 +278,30 @@ class HMatrix:
     @classmethod
     def kelvin_points(cls, mesh: Mesh, points, E: float = 1.0, nu: float = 0.3,
                       b_min: int = 32, eta: float = 1.0, min_distance_factor: float = 0.5,
-                      device: int = 0, shard: tuple = (0, 1)) -> "HMatrix":
+                      device: int = 0, shard: tuple = (0, 1),
+                      disjoint_order: int = 4) -> "HMatrix":
         """The single-layer grid V~ of evaluate_interior (baca.cpp:625-687):
         CollocSingleOracle(r, c) at arbitrary points (rows) against the
         triangles (columns); 3 n_points x 3 N_t."""
         p = _f64(points).reshape(-1, 3)
         out = C.c_void_p()
         _check(_h.hmb_op_kelvin_points(mesh._h, len(p), _ptr(p), E, nu, b_min, eta,
-                                       min_distance_factor, device, shard[0], shard[1],
-                                       C.byref(out)))
+                                       min_distance_factor, disjoint_order, device, shard[0],
+                                       shard[1], C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def kelvin_double(cls, mesh: Mesh, points, r: int, c: int, E: float = 1.0,
+                      nu: float = 0.3, b_min: int = 32, eta: float = 1.0,
+                      min_distance_factor: float = 0.5, device: int = 0,
+                      shard: tuple = (0, 1), disjoint_order: int = 4) -> "HMatrix":
+        """Cell (r, c) of evaluate_interior's double-layer grid W~
+        (CollocDoubleOracle, kernels.cpp:189-210): n_points x N_v."""
+        p = _f64(points).reshape(-1, 3)
+        out = C.c_void_p()
+        _check(_h.hmb_op_kelvin_double(mesh._h, len(p), _ptr(p), int(r), int(c), E, nu, b_min,
+                                       eta, min_distance_factor, disjoint_order, device,
+                                       shard[0], shard[1], C.byref(out)))
         return cls(out)
 
     @classmethod
@@ -551,6 +566,43 @@ class HMatrix:
 
 
 # ---- reference-style free functions ----------------------------------------
+class InteriorEvaluator:
+    """evaluate_interior (baca.cpp:625-696): displacements at interior
+    points from the full Cauchy data, v = V~ t - W~ u, with the single-layer
+    grid V~ (one Kelvin context at the points) and the nine double-layer
+    cells W~_rc (points x nodes) as GPU H-matrices."""
+
+    def __init__(self, mesh: Mesh, points, E: float = 1.0, nu: float = 0.3, b_min: int = 32,
+                 eta: float = 1.0, min_distance_factor: float = 0.5, device: int = 0,
+                 disjoint_order: int = 4):
+        self.npts = len(_f64(points).reshape(-1, 3))
+        self.nt, self.nv = mesh.num_triangles, mesh.num_vertices
+        self.vt = HMatrix.kelvin_points(mesh, points, E, nu, b_min, eta, min_distance_factor,
+                                        device, disjoint_order=disjoint_order)
+        self.wt = [[HMatrix.kelvin_double(mesh, points, r, c, E, nu, b_min, eta,
+                                          min_distance_factor, device,
+                                          disjoint_order=disjoint_order)
+                    for c in range(3)] for r in range(3)]
+
+    def assemble(self, eps: float = 1e-6, lookahead: int = 2, beta: float = 0.8):
+        self.vt.assemble(eps=eps, beta=beta, lookahead=lookahead)
+        for row in self.wt:
+            for h in row:
+                h.assemble(eps=eps, beta=beta, lookahead=lookahead)
+
+    def evaluate(self, t_total, u_total) -> np.ndarray:
+        t = np.asarray(t_total, dtype=np.float64)
+        u = np.asarray(u_total, dtype=np.float64)
+        if t.shape != (3 * self.nt,) or u.shape != (3 * self.nv,):
+            raise DimensionError("evaluate_interior: Cauchy data size")
+        v = self.vt.matvec(t)
+        n = self.npts
+        for r in range(3):
+            for c in range(3):
+                v[r * n:(r + 1) * n] -= self.wt[r][c].matvec(u[c * self.nv:(c + 1) * self.nv])
+        return v
+
+
 class LameSingleLayer:
     """V_h = (1+nu) / (2E (1-nu)) [ (3-4nu) diag3(V_Delta) + grid(V_kl) ]
     (compose_Vh, proj/src/operators.cpp:97-105): the Galerkin single-layer

@@ -365,6 +365,7 @@ struct hmgpu_ctx {
   int gal_which = 0;                   // galerkin: 0 V_kl grid, 1 V_Delta
   std::vector<double> normals;         // K_Delta: unit normals per triangle
   std::vector<double> eval_pts;        // Kelvin: evaluation points (empty: centroids)
+  int dl_r = 0, dl_c = 0;              // double layer: grid cell
   std::vector<double> prule[4];        // galerkin singular pair rules, SoA per case
   int prule_n[4] = {0, 0, 0, 0};
 
@@ -686,9 +687,11 @@ void build_geometry(hmgpu_ctx* c) {
       g.prule_total = total;
       g.gal_delta = c->gal_which;
     }
-  } else if (c->kind == KIND_KDELTA) {
-    if (c->n_tri != c->n_rows || c->n_vert != c->n_cols)
-      fail(HMGPU_ERR_DIMENSION, "K_Delta geometry does not match the partition");
+  } else if (c->kind == KIND_KDELTA || c->kind == KIND_KDOUBLE) {
+    const bool dbl = c->kind == KIND_KDOUBLE;
+    const long long nrow_geo = dbl ? (long long)c->eval_pts.size() / 3 : c->n_tri;
+    if (nrow_geo != c->n_rows || c->n_vert != c->n_cols)
+      fail(HMGPU_ERR_DIMENSION, "node geometry does not match the partition");
     std::vector<double4> vx(c->n_vert), tce(c->n_tri), tna(c->n_tri);
     for (int v = 0; v < c->n_vert; ++v)
       vx[v] = make_double4(c->verts[3LL * v], c->verts[3LL * v + 1], c->verts[3LL * v + 2], 0);
@@ -700,7 +703,8 @@ void build_geometry(hmgpu_ctx* c) {
       tna[t] = make_double4(c->normals[3 * t], c->normals[3 * t + 1], c->normals[3 * t + 2],
                             c->area[t]);
     }
-    for (int i = 0; i < c->n_rows; ++i) tv[i] = tvx[c->rperm[i]];
+    if (!dbl)
+      for (int i = 0; i < c->n_rows; ++i) tv[i] = tvx[c->rperm[i]];
     // vertex_triangles (mesh.cpp:245-247) per internal column, ascending ids
     std::vector<std::vector<int2>> inc(c->n_vert);
     for (int t = 0; t < c->n_tri; ++t)
@@ -713,18 +717,42 @@ void build_geometry(hmgpu_ctx* c) {
       ptr[j + 1] = (int)lst.size();
     }
     long long total = 0;
-    for (int pc = 1; pc < 4; ++pc) {
-      if (c->prule_n[pc] == 0) fail(HMGPU_ERR_STATE, "galerkin pair rule missing");
-      g.pr_off[pc] = (int)total;
-      g.pr_n[pc] = c->prule_n[pc];
-      total += c->prule_n[pc];
+    std::vector<double> pr;
+    if (!dbl) {
+      for (int pc = 1; pc < 4; ++pc) {
+        if (c->prule_n[pc] == 0) fail(HMGPU_ERR_STATE, "galerkin pair rule missing");
+        g.pr_off[pc] = (int)total;
+        g.pr_n[pc] = c->prule_n[pc];
+        total += c->prule_n[pc];
+      }
+      pr.resize(5 * total);
+      for (int pc = 1; pc < 4; ++pc)
+        for (int f = 0; f < 5; ++f)
+          std::copy(c->prule[pc].begin() + (long long)f * c->prule_n[pc],
+                    c->prule[pc].begin() + (long long)(f + 1) * c->prule_n[pc],
+                    pr.begin() + f * total + g.pr_off[pc]);
+    } else {
+      std::vector<double4> rp(c->n_rows);
+      for (int i = 0; i < c->n_rows; ++i) {
+        const long long t = c->rperm[i];
+        rp[i] = make_double4(c->eval_pts[3 * t], c->eval_pts[3 * t + 1],
+                             c->eval_pts[3 * t + 2], 0.0);
+      }
+      c->d_rowpt.upload(rp, c->stream);
+      g.rowpt = c->d_rowpt.p;
+      // lame_constants (kernels.cpp:7-14) and the traction constants
+      const double lam = c->E * c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
+      const double mu = c->E / (2.0 * (1.0 + c->nu));
+      g.cst = (1.0 + c->nu) / (8.0 * M_PI * c->E * (1.0 - c->nu));
+      g.c34 = 3.0 - 4.0 * c->nu;
+      g.dl_b1 = 2.0 * mu - 2.0 * lam * (1.0 - 2.0 * c->nu);
+      g.dl_a2 = mu * (1.0 - g.c34);
+      g.dl_a6 = 6.0 * mu;
+      g.dl_r = c->dl_r;
+      g.dl_c = c->dl_c;
+      tv.assign(1, make_int4(0, 0, 0, 0));
+      pr.assign(5, 0.0);
     }
-    std::vector<double> pr(5 * total);
-    for (int pc = 1; pc < 4; ++pc)
-      for (int f = 0; f < 5; ++f)
-        std::copy(c->prule[pc].begin() + (long long)f * c->prule_n[pc],
-                  c->prule[pc].begin() + (long long)(f + 1) * c->prule_n[pc],
-                  pr.begin() + f * total + g.pr_off[pc]);
     c->d_vtx.upload(vx, c->stream);
     c->d_tvid.upload(tv, c->stream);
     c->d_tvx.upload(tvx, c->stream);
@@ -873,6 +901,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
       if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
       else if (c->kind == KIND_GALERKIN) go(aca_kernel<KIND_GALERKIN>);
       else if (c->kind == KIND_KDELTA) go(aca_kernel<KIND_KDELTA>);
+      else if (c->kind == KIND_KDOUBLE) go(aca_kernel<KIND_KDOUBLE>);
       else if (c->kind == KIND_NEWTON) go(aca_kernel<KIND_NEWTON>);
       else go(aca_kernel<KIND_DENSE>);
     });
@@ -1907,9 +1936,30 @@ int hmgpu_ell3_spmv_t(hmgpu_ctx* ctx, int cols, const int* tptr, const int* tslo
   });
 }
 
+int hmgpu_set_kdouble_geometry(hmgpu_ctx* ctx, int n_vert, const double* verts, int n_tri,
+                               const int* tris, const double* centroid, const double* area,
+                               const double* diam, const double* normals, double E,
+                               double nu, int r, int c) {
+  const int st = hmgpu_set_kdelta_geometry(ctx, n_vert, verts, n_tri, tris, centroid, area,
+                                           diam, normals);
+  if (st != HMGPU_OK) return st;
+  return guard(ctx, [&] {
+    if (E <= 0.0) fail(HMGPU_ERR_INVALID, "lame_constants: E must be positive");
+    if (nu <= 0.0 || nu >= 0.5)
+      fail(HMGPU_ERR_INVALID, "lame_constants: nu must lie in (0, 1/2)");
+    if (r < 0 || r > 2 || c < 0 || c > 2) fail(HMGPU_ERR_INVALID, "cell (r, c) in 0..2");
+    ctx->kind = KIND_KDOUBLE;
+    ctx->E = E;
+    ctx->nu = nu;
+    ctx->dl_r = r;
+    ctx->dl_c = c;
+  });
+}
+
 int hmgpu_set_eval_points(hmgpu_ctx* ctx, int n, const double* pts) {
   return guard(ctx, [&] {
-    if (ctx->kind != KIND_KELVIN) fail(HMGPU_ERR_STATE, "set the Kelvin geometry first");
+    if (ctx->kind != KIND_KELVIN && ctx->kind != KIND_KDOUBLE)
+      fail(HMGPU_ERR_STATE, "set the Kelvin / double-layer geometry first");
     if (n < 0 || (n > 0 && !pts)) fail(HMGPU_ERR_INVALID, "bad evaluation points");
     ctx->eval_pts.assign(pts, pts + 3LL * n);
     ctx->assembled = false;
@@ -1984,7 +2034,8 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         fail(HMGPU_ERR_INVALID, "aca_run: beta must be in (0,1)");
     }
     if (lookahead < 0 || max_rank < 1) fail(HMGPU_ERR_INVALID, "bad lookahead/max_rank");
-    if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA)
+    if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA ||
+        c->kind == KIND_KDOUBLE)
       upload_rules(c);
     build_geometry(c);
     c->eps = eps;
@@ -2446,7 +2497,8 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::sort(ids.begin(), ids.end());
   ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
   if (ids.empty() || steps == 0) return;
-  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA)
+  if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA ||
+      c->kind == KIND_KDOUBLE)
     upload_rules(c);
   c->d_list.upload(ids, c->stream);
   c->timed("prep_extend", [&] {

@@ -30,7 +30,8 @@ __constant__ RuleTable c_rules;
 __constant__ int c_comp_r[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_comp_c[6] = {0, 1, 2, 1, 2, 2};
 
-enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2, KIND_GALERKIN = 3, KIND_KDELTA = 4 };
+enum { KIND_KELVIN = 0, KIND_NEWTON = 1, KIND_DENSE = 2, KIND_GALERKIN = 3, KIND_KDELTA = 4,
+       KIND_KDOUBLE = 5 };
 
 // Per-problem geometry, passed by value to every kernel.
 struct Geom {
@@ -60,6 +61,9 @@ struct Geom {
   const double4* tna;       // unit normal, area
   const int* vt_ptr;        // per internal column (node): its triangles in vt_tri
   const int2* vt_tri;       // (triangle, local index of the node), ascending triangles
+  // double layer (colloc_double, kernels.cpp:189-210): cell (dl_r, dl_c)
+  int dl_r, dl_c;
+  double dl_b1, dl_a2, dl_a6;  // 2mu - 2lambda(1-2nu), mu(1-(3-4nu)), 6mu
 };
 
 // ---------------------------------------------------------------------------
@@ -583,6 +587,73 @@ __device__ __forceinline__ bool kd_touching(const Geom& g, int i, int j) {
   return false;
 }
 
+// ---------------------------------------------------------------------------
+// Double-layer collocation (CollocDoubleOracle / colloc_double, kernels.cpp:
+// 189-210): evaluation point i (rows) x node j (columns), the traction of
+// the Kelvin columns (kelvin_traction, kernels.cpp:30-55) in the closed form
+//   T_rc = c [ (b1 n_r x_c + a2 n_c x_r + delta_rc a2 (n.x)) / r^3
+//              - a6 x_r x_c (n.x) / r^5 ],  x = y - p,
+// times the hat function of the node, over the node's triangles in
+// ascending order; point_order tiers as colloc_single.  Canonical order
+// shared with oracle/hmbem_oracle.cpp Kelvin::colloc_double.
+__device__ __forceinline__ int kelvin_tier_c(double px, double py, double pz, double cx,
+                                             double cy, double cz, double dj) {
+  const double dx = __dsub_rn(px, cx), dy = __dsub_rn(py, cy), dz = __dsub_rn(pz, cz);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                              __dmul_rn(dz, dz));
+  const double t0 = (c_rules.far_ratio + 0.5) * dj, t1 = (c_rules.mid_ratio + 0.5) * dj;
+  const double s0 = t0 * t0, s1 = t1 * t1;
+  if (d2 > s0 * (1.0 + 1e-12)) return 0;
+  if (d2 < s0 * (1.0 - 1e-12)) {
+    if (d2 > s1 * (1.0 + 1e-12)) return 1;
+    if (d2 < s1 * (1.0 - 1e-12)) return 2;
+  }
+  return kelvin_tier_exact(d2, dj);
+}
+
+__device__ __forceinline__ double kdouble_entry(const Geom& g, int i, int j, int& nq_acc) {
+  const double4 p = g.rowpt[i];
+  const int R = g.dl_r, Cc = g.dl_c;
+  double acc = 0.0;
+  const int p1 = g.vt_ptr[j + 1];
+#pragma unroll 1
+  for (int pp = g.vt_ptr[j]; pp < p1; ++pp) {
+    const int2 tl = g.vt_tri[pp];
+    const int tau = tl.x, local = tl.y;
+    const int4 tv = g.tvx[tau];
+    const double4 ce = g.tce[tau], na = g.tna[tau];
+    const int tier = kelvin_tier_c(p.x, p.y, p.z, ce.x, ce.y, ce.z, ce.w);
+    const double4 Y0 = g.vtx[tv.x], Y1 = g.vtx[tv.y], Y2 = g.vtx[tv.z];
+    const double y0[3] = {Y0.x, Y0.y, Y0.z};
+    const double e1[3] = {Y1.x - Y0.x, Y1.y - Y0.y, Y1.z - Y0.z};
+    const double e2[3] = {Y2.x - Y0.x, Y2.y - Y0.y, Y2.z - Y0.z};
+    const double pv[3] = {p.x, p.y, p.z};
+    const double nn[3] = {na.x, na.y, na.z};
+    const double nr = sel3(R, na.x, na.y, na.z), nc = sel3(Cc, na.x, na.y, na.z);
+    const int n = c_rules.n[tier];
+    nq_acc += n;
+    double part = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < n; ++q) {
+      const double a = c_rules.a[tier][q], b = c_rules.b[tier][q], w = c_rules.w[tier][q];
+      double x[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) x[d] = fma(b, e2[d], fma(a, e1[d], y0[d])) - pv[d];
+      const double ri = rsqrt_canon(fma(x[2], x[2], fma(x[1], x[1], x[0] * x[0])));
+      const double ri2 = ri * ri, ri3 = ri2 * ri, ri5 = ri3 * ri2;
+      const double nx = fma(x[2], nn[2], fma(x[1], nn[1], x[0] * nn[0]));
+      const double xr = sel3(R, x[0], x[1], x[2]), xc = sel3(Cc, x[0], x[1], x[2]);
+      double sv = fma(g.dl_b1, nr * xc, g.dl_a2 * (nc * xr));
+      if (R == Cc) sv = fma(g.dl_a2, nx, sv);
+      const double v = fma(-(g.dl_a6 * ri5), (xr * xc) * nx, ri3 * sv);
+      const double psi = local == 0 ? (1.0 - a) - b : (local == 1 ? a : b);
+      part = fma(w * psi, v, part);
+    }
+    acc = acc + (2.0 * na.w * g.cst) * part;
+  }
+  return acc;
+}
+
 // Newton kernel: IEEE ops in the oracle's order, so entries are bit-exact
 __device__ __forceinline__ double newton_entry(const Geom& g, int i, int j) {
   const double4 a = g.rowpt[i];
@@ -603,6 +674,7 @@ __device__ __forceinline__ double entry1(const Geom& g, int i, int j,
                                          int comp) {
   int nq = 0;
   if (g.kind == KIND_KELVIN) return kelvin_entry1(g, i, j, comp, nq);
+  if (g.kind == KIND_KDOUBLE) return kdouble_entry(g, i, j, nq);
   if (g.kind == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }
@@ -616,6 +688,7 @@ __device__ __forceinline__ double entry_k(const Geom& g, int i, int j, int comp,
   if (KIND == KIND_GALERKIN)
     return galerkin_entry1(g, i, j, g.gal_delta ? 6 : comp, nq_acc);
   if (KIND == KIND_KDELTA) return kdelta_entry<0>(g, i, j, nq_acc, 0);
+  if (KIND == KIND_KDOUBLE) return kdouble_entry(g, i, j, nq_acc);
   if (KIND == KIND_NEWTON) return newton_entry(g, i, j);
   return dense_entry(g, i, j);
 }

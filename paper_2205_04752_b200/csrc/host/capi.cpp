@@ -247,17 +247,40 @@ int hmb_op_kelvin(const hmb_mesh* m, double E, double nu, int b_min, double eta,
 
 int hmb_op_kelvin_points(const hmb_mesh* m, int npts, const double* pts, double E,
                          double nu, int b_min, double eta, double min_distance_factor,
-                         int device, int shard_rank, int shard_count, hmb_op** out) {
+                         int disjoint_order, int device, int shard_rank, int shard_count,
+                         hmb_op** out) {
   return guard([&] {
     need(m, "mesh");
     need(pts, "pts");
     need(out, "out");
     std::vector<hmb::V3> p(npts);
     for (int i = 0; i < npts; ++i) p[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    hmb::QuadratureConfig qc;
+    qc.disjoint_order = disjoint_order;
     auto op = std::make_unique<hmb_op>();
     op->op = hmb::HOperator::kelvin_points(m->mesh, p, E, nu, b_min, eta, device,
                                            hmb::Shard{shard_rank, shard_count},
-                                           min_distance_factor);
+                                           min_distance_factor, qc);
+    *out = op.release();
+  });
+}
+
+int hmb_op_kelvin_double(const hmb_mesh* m, int npts, const double* pts, int r, int c,
+                         double E, double nu, int b_min, double eta,
+                         double min_distance_factor, int disjoint_order, int device,
+                         int shard_rank, int shard_count, hmb_op** out) {
+  return guard([&] {
+    need(m, "mesh");
+    need(pts, "pts");
+    need(out, "out");
+    std::vector<hmb::V3> p(npts);
+    for (int i = 0; i < npts; ++i) p[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    hmb::QuadratureConfig qc;
+    qc.disjoint_order = disjoint_order;
+    auto op = std::make_unique<hmb_op>();
+    op->op = hmb::HOperator::kelvin_double_points(m->mesh, p, r, c, E, nu, b_min, eta, device,
+                                                  hmb::Shard{shard_rank, shard_count},
+                                                  min_distance_factor, qc);
     *out = op.release();
   });
 }

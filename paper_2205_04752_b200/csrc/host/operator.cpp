@@ -178,16 +178,9 @@ Real point_triangle_distance(const V3& p, const V3& a, const V3& b, const V3& c)
 }
 }  // namespace
 
-std::unique_ptr<HOperator> HOperator::kelvin_points(const Mesh& mesh,
-                                                    const std::vector<V3>& points, Real E,
-                                                    Real nu, int b_min, Real eta, int device,
-                                                    Shard shard, Real min_distance_factor,
-                                                    QuadratureConfig qc) {
-  if (mesh.centroids.size() != mesh.triangles.size())
-    throw MeshError("mesh geometry caches missing (call finish())");
-  if (points.empty()) throw Error("evaluate_interior: no points");
-  if (E <= 0.0) throw Error("lame_constants: E must be positive");
-  if (nu <= 0.0 || nu >= 0.5) throw Error("lame_constants: nu must lie in (0, 1/2)");
+namespace {
+void check_interior_points(const Mesh& mesh, const std::vector<V3>& points,
+                           Real min_distance_factor) {
   Real max_diam = 0.0;
   for (Real d : mesh.diam) max_diam = std::max(max_diam, d);
   const Real min_dist = min_distance_factor * max_diam;
@@ -200,6 +193,76 @@ std::unique_ptr<HOperator> HOperator::kelvin_points(const Mesh& mesh,
       throw Error("evaluate_interior: point " + std::to_string(i) +
                   " is closer to the surface than the quadrature threshold");
   }
+}
+}  // namespace
+
+std::unique_ptr<HOperator> HOperator::kelvin_double_points(
+    const Mesh& mesh, const std::vector<V3>& points, int r, int c, Real E, Real nu, int b_min,
+    Real eta, int device, Shard shard, Real min_distance_factor, QuadratureConfig qc) {
+  if (mesh.normals.size() != mesh.triangles.size())
+    throw MeshError("mesh geometry caches missing (call finish())");
+  if (points.empty()) throw Error("evaluate_interior: no points");
+  if (E <= 0.0) throw Error("lame_constants: E must be positive");
+  if (nu <= 0.0 || nu >= 0.5) throw Error("lame_constants: nu must lie in (0, 1/2)");
+  if (r < 0 || r > 2 || c < 0 || c > 2) throw Error("double layer: cell (r, c) in 0..2");
+  check_interior_points(mesh, points, min_distance_factor);
+  std::unique_ptr<HOperator> op(new HOperator());
+  op->kind_ = Kelvin;
+  op->ncomp_ = 1;
+  op->n_rows_ = static_cast<int>(points.size());
+  op->n_cols_ = mesh.nv();
+  std::vector<Box> pb(points.size());
+  for (size_t i = 0; i < points.size(); ++i) pb[i].absorb(points[i]);
+  const std::vector<Box> tb = triangle_supports(mesh);
+  std::vector<Box> nb(mesh.nv());
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int k = 0; k < 3; ++k) nb[mesh.triangles[t][k]].absorb(tb[t]);
+  op->rows_ = std::make_unique<ClusterTree>(build_cluster_tree(pb, b_min));
+  op->cols_ = std::make_unique<ClusterTree>(build_cluster_tree(nb, b_min));
+  op->init_partition(eta, shard);
+  if (device < 0) return op;
+  op->check(hmgpu_create(device, &op->ctx_), "hmgpu_create");
+  std::vector<double> verts(3 * mesh.nv()), cen(3 * mesh.nt()), nrm(3 * mesh.nt()),
+      ep(3 * points.size());
+  std::vector<int> tris(3 * mesh.nt());
+  for (int v = 0; v < mesh.nv(); ++v)
+    for (int d = 0; d < 3; ++d) verts[3 * v + d] = mesh.vertices[v][d];
+  for (int t = 0; t < mesh.nt(); ++t)
+    for (int d = 0; d < 3; ++d) {
+      tris[3 * t + d] = mesh.triangles[t][d];
+      cen[3 * t + d] = mesh.centroids[t][d];
+      nrm[3 * t + d] = mesh.normals[t][d];
+    }
+  for (size_t i = 0; i < points.size(); ++i)
+    for (int d = 0; d < 3; ++d) ep[3 * i + d] = points[i][d];
+  op->check(hmgpu_set_kdouble_geometry(op->ctx_, mesh.nv(), verts.data(), mesh.nt(),
+                                       tris.data(), cen.data(), mesh.areas.data(),
+                                       mesh.diam.data(), nrm.data(), E, nu, r, c),
+            "hmgpu_set_kdouble_geometry");
+  op->check(hmgpu_set_eval_points(op->ctx_, static_cast<int>(points.size()), ep.data()),
+            "hmgpu_set_eval_points");
+  for (int tier = 0; tier < 3; ++tier) {
+    const TriangleRule rr = gauss_rule(qc.tier_order(tier));
+    op->check(hmgpu_set_rule(op->ctx_, tier, static_cast<int>(rr.w.size()), rr.a.data(),
+                             rr.b.data(), rr.w.data()),
+              "hmgpu_set_rule");
+  }
+  op->check(hmgpu_set_tier_ratios(op->ctx_, qc.far_ratio, qc.mid_ratio),
+            "hmgpu_set_tier_ratios");
+  return op;
+}
+
+std::unique_ptr<HOperator> HOperator::kelvin_points(const Mesh& mesh,
+                                                    const std::vector<V3>& points, Real E,
+                                                    Real nu, int b_min, Real eta, int device,
+                                                    Shard shard, Real min_distance_factor,
+                                                    QuadratureConfig qc) {
+  if (mesh.centroids.size() != mesh.triangles.size())
+    throw MeshError("mesh geometry caches missing (call finish())");
+  if (points.empty()) throw Error("evaluate_interior: no points");
+  if (E <= 0.0) throw Error("lame_constants: E must be positive");
+  if (nu <= 0.0 || nu >= 0.5) throw Error("lame_constants: nu must lie in (0, 1/2)");
+  check_interior_points(mesh, points, min_distance_factor);
   std::unique_ptr<HOperator> op(new HOperator());
   op->kind_ = Kelvin;
   op->ncomp_ = 6;

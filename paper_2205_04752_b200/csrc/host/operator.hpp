@@ -69,6 +69,13 @@ class HOperator {
                                                   Shard shard = {},
                                                   Real min_distance_factor = 0.5,
                                                   QuadratureConfig qc = {});
+  // one cell (r, c) of evaluate_interior's double-layer grid W~ (baca.cpp:
+  // 650-651, 674-677): CollocDoubleOracle at the points (rows, point tree)
+  // against the vertices (columns, node tree: union of incident triangle boxes)
+  static std::unique_ptr<HOperator> kelvin_double_points(
+      const Mesh& mesh, const std::vector<V3>& points, int r, int c, Real E, Real nu,
+      int b_min, Real eta, int device, Shard shard = {}, Real min_distance_factor = 0.5,
+      QuadratureConfig qc = {});
   // Galerkin scalar kernels on the triangle partition of assemble_operators
   // (operators.cpp:186-200, 218-235): which = 0 the six V_kl as the 3x3
   // grid, 1 V_Delta (GalerkinKernels::vkl / vdelta, kernels.cpp:130-149)
