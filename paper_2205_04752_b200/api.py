@@ -730,6 +730,16 @@ class OperatorSet:
         self._sync()
         return y
 
+    def _hmv_t(self, h: HMatrix, x, nrhs: int = 1):
+        """y = H^T x (HMatrix::matvec_transposed) for nrhs columns."""
+        x = x.contiguous()
+        y = self._torch.empty(h.cols * nrhs, dtype=self._torch.float64, device=self.dev)
+        self._sync()
+        _check(_h.hmb_matvec_transposed(h._h, C.c_void_p(x.data_ptr()),
+                                        C.c_void_p(y.data_ptr()), nrhs, 0, 1))
+        self._sync()
+        return y
+
     # T_h = [0, T12, T13; -T12, 0, T23; -T13, -T23, 0] (operators.cpp:56-70)
     _TH = ((None, (0, 1.0), (1, 1.0)), ((0, -1.0), None, (2, 1.0)),
            ((1, -1.0), (2, -1.0), None))
@@ -782,6 +792,21 @@ class OperatorSet:
         yg = self._hmv(self.vkl, x)
         yd = self._hmv(self.vdelta, x, 3)  # diag3(V_Delta): 3 RHS
         return s * ((3.0 - 4.0 * self.nu) * yd + yg)
+
+    def vh_t_dev(self, z):
+        """V_h^T z (the transpose of every leaf H-matrix; V_h^T = V_h up to
+        the ACA approximation)."""
+        s = 0.5 / self.E * (1.0 + self.nu) / (1.0 - self.nu)
+        yg = self._hmv_t(self.vkl, z)
+        yd = self._hmv_t(self.vdelta, z, 3)
+        return s * ((3.0 - 4.0 * self.nu) * yd + yg)
+
+    def kh_t_dev(self, z):
+        """K_h^T z (3M -> 3N) = diag3(K_Delta)^T z - T_h^T diag3(V_Delta)^T z
+        + 2 mu T_h^T V_h^T z (the transposed compose_Kh, as the reference's
+        transpose(K_ND) in the saddle system, baca.cpp:12-40)."""
+        return (self._hmv_t(self.kdelta, z, 3) - self.t_h_t(self._hmv_t(self.vdelta, z, 3))
+                + 2.0 * self.mu * self.t_h_t(self.vh_t_dev(z)))
 
     def kh_dev(self, x):
         """K_h x (3N -> 3M) = diag3(K_Delta) x - diag3(V_Delta) T_h x + 2 mu V_h T_h x."""
@@ -839,6 +864,9 @@ class OperatorSet:
 
     def dh(self, x):
         return self._run(self.dh_dev, x, 3 * self.n)
+
+    def kh_t(self, z):
+        return self._run(self.kh_t_dev, z, 3 * self.m)
 
 
 @dataclasses.dataclass

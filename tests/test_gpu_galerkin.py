@@ -226,6 +226,8 @@ def test_composed_operators_match_dense(opset):
     assert rel(ops.vh(xm), opset["Vh"] @ xm) <= 10 * eps
     assert rel(ops.kh(xn), opset["Kh"] @ xn) <= 100 * eps
     assert rel(ops.dh(xn), opset["Dh"] @ xn) <= 100 * eps
+    zm = RV(3 * m, 15)
+    assert rel(ops.kh_t(zm), opset["Kh"].T @ zm) <= 100 * eps
     # D_h is symmetric; constants are in its kernel (rigid translations)
     Dh = opset["Dh"]
     assert np.allclose(Dh, Dh.T, rtol=0, atol=1e-10 * np.abs(Dh).max())
