@@ -7,7 +7,8 @@ from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflo
                   AssemblyStats, BlockTerm, ClusterTree, ConfigError, DeviceError,
                   DimensionError, Error, GammaContributions, HMatrix, LameSingleLayer, Mesh,
                   OperatorSet, lame_constants, InteriorEvaluator, BacaConfig, BacaReport, VddPreconditioner,
-                  baca_solve, pcg_spd, estimator_vh, doerfler_mark,
+                  baca_solve, pcg_spd, estimator_vh, doerfler_mark, DofLayout, SaddleSystem,
+                  SolveStats, bpcg_solve,
                   MeshError, Mode, amvm_multiply, assemble, device_count, gamma_contributions,
                   host_tree_and_partition)
 
@@ -16,7 +17,8 @@ __all__ = [
     "AssemblyStats", "BlockTerm", "ClusterTree", "ConfigError", "DeviceError",
     "DimensionError", "Error", "GammaContributions", "HMatrix", "LameSingleLayer", "Mesh",
     "OperatorSet", "lame_constants", "InteriorEvaluator", "BacaConfig", "BacaReport", "VddPreconditioner",
-    "baca_solve", "pcg_spd", "estimator_vh", "doerfler_mark",
+    "baca_solve", "pcg_spd", "estimator_vh", "doerfler_mark", "DofLayout", "SaddleSystem",
+    "SolveStats", "bpcg_solve",
     "MeshError",
     "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",
     "host_tree_and_partition",

@@ -909,10 +909,18 @@ class VddPreconditioner:
     eta = half the smallest Ritz value of C0^{-1} V_h from a 10-step
     preconditioned Lanczos run, so that eta C0 stays spectrally below V_h."""
 
-    def __init__(self, ops: "OperatorSet"):
+    def __init__(self, ops: "OperatorSet", dirichlet=None, vdd=None):
+        """dirichlet: sorted Dirichlet triangle ids (None: all triangles);
+        vdd: the V_DD matvec on device vectors (default V_h)."""
         torch = ops._torch
         self.ops = ops
+        self._vdd = vdd or ops.vh_dev
         m = ops.m
+        rank = np.arange(m) if dirichlet is None else np.full(m, -1)
+        if dirichlet is not None:
+            rank[np.asarray(dirichlet)] = np.arange(len(dirichlet))
+        md = m if dirichlet is None else len(dirichlet)
+        self.n = 3 * md
         pref = 0.5 / ops.E * (1.0 + ops.nu) / (1.0 - ops.nu)
         c34 = 3.0 - 4.0 * ops.nu
         tree = ops.vdelta.tree(0)
@@ -922,18 +930,22 @@ class VddPreconditioner:
         groups, mats = [], []
         for leaf in tree.leaves():
             b0, b1 = tree.nodes[leaf, 0], tree.nodes[leaf, 1]
-            members = tree.perm[b0:b1]
+            # the Dirichlet members of the leaf (baca.cpp:113-127)
+            sel = np.nonzero(rank[tree.perm[b0:b1]] >= 0)[0]
+            if len(sel) == 0:
+                continue
+            members = tree.perm[b0:b1][sel]
             nm = len(members)
             b = diag[int(leaf)]
-            dd = ops.vdelta.dense_block(0, b)
+            dd = ops.vdelta.dense_block(0, b)[np.ix_(sel, sel)]
             blk = np.zeros((3 * nm, 3 * nm))
             for c1 in range(3):
                 for c2 in range(3):
-                    d = ops.vkl.dense_block(idx[(min(c1, c2), max(c1, c2))], b)
+                    d = ops.vkl.dense_block(idx[(min(c1, c2), max(c1, c2))], b)[np.ix_(sel, sel)]
                     if c1 == c2:
                         d = d + c34 * dd
                     blk[c1 * nm:(c1 + 1) * nm, c2 * nm:(c2 + 1) * nm] = pref * d
-            groups.append(np.concatenate([c * m + members for c in range(3)]))
+            groups.append(np.concatenate([c * md + rank[members] for c in range(3)]))
             mats.append(blk)
         # batch by block size (leaves of one tree level share it)
         self.batches = []
@@ -962,7 +974,7 @@ class VddPreconditioner:
 
     def _ritz_eta(self) -> float:
         torch = self.ops._torch
-        n = 3 * self.ops.m
+        n = self.n
         i = torch.arange(n, dtype=torch.float64, device=self.ops.dev)
         r = 0.5 + 0.5 * torch.cos(3 * i + 1)
         z = self.solve(r)
@@ -970,7 +982,7 @@ class VddPreconditioner:
         rz = float(r @ z)
         alphas, betas = [], []
         for _ in range(10):
-            ap = self.ops.vh_dev(p)
+            ap = self._vdd(p)
             pap = float(p @ ap)
             if pap <= 0.0 or rz <= 0.0:
                 break
@@ -995,6 +1007,266 @@ class VddPreconditioner:
                 tri[j, j + 1] = tri[j + 1, j] = off
         lam = float(np.linalg.eigvalsh(tri).min())
         return 0.5 * lam if lam > 0 else 1.0
+
+
+class DofLayout:
+    """classify_dofs (mesh.cpp:278-293): the Dirichlet triangles (sorted)
+    and the Neumann interior nodes (vertices none of whose triangles is
+    Dirichlet), component-major DOF index sets (operators.cpp:160-176)."""
+
+    def __init__(self, mesh: Mesh):
+        a = mesh.arrays()
+        T = a["triangles"]
+        d = a["dirichlet"].astype(bool)
+        self.num_triangles, self.num_nodes = len(T), len(a["vertices"])
+        self.dirichlet_triangle_ids = np.nonzero(d)[0]
+        touched = np.zeros(self.num_nodes, bool)
+        touched[T.reshape(-1)] = True
+        bad = np.zeros(self.num_nodes, bool)
+        bad[T[d].reshape(-1)] = True
+        self.neumann_interior_nodes = np.nonzero(touched & ~bad)[0]
+        m, n = self.num_triangles, self.num_nodes
+        self.t_dofs = np.concatenate([c * m + self.dirichlet_triangle_ids for c in range(3)])
+        self.u_dofs = np.concatenate([c * n + self.neumann_interior_nodes for c in range(3)])
+
+
+class SaddleSystem:
+    """assemble_saddle (baca.cpp:12-40): the Lame saddle system
+    [V_DD, -K_ND; K_ND^T, D_NN] over the Dirichlet-triangle and
+    Neumann-node DOFs, as restrictions of the device compositions of
+    OperatorSet (reduced to V_DD t = f_D when there is no Neumann node)."""
+
+    def __init__(self, ops: "OperatorSet", layout: DofLayout):
+        if len(layout.dirichlet_triangle_ids) == 0:
+            raise Error("assemble_saddle: empty Dirichlet part")
+        torch = ops._torch
+        self.ops, self.layout = ops, layout
+        self.t_idx = torch.tensor(layout.t_dofs, device=ops.dev)
+        self.u_idx = torch.tensor(layout.u_dofs, device=ops.dev)
+        self.nt, self.nu_ = len(layout.t_dofs), len(layout.u_dofs)
+        self.reduced = self.nu_ == 0
+
+    @property
+    def dim(self) -> int:
+        return self.nt + (0 if self.reduced else self.nu_)
+
+    def _embed(self, v, idx, n):
+        z = self.ops._torch.zeros(n, dtype=self.ops._torch.float64, device=self.ops.dev)
+        z[idx] = v
+        return z
+
+    def vdd(self, xt):
+        return self.ops.vh_dev(self._embed(xt, self.t_idx, 3 * self.ops.m))[self.t_idx]
+
+    def knd(self, xu):
+        return self.ops.kh_dev(self._embed(xu, self.u_idx, 3 * self.ops.n))[self.t_idx]
+
+    def knd_t(self, zt):
+        return self.ops.kh_t_dev(self._embed(zt, self.t_idx, 3 * self.ops.m))[self.u_idx]
+
+    def dnn(self, xu):
+        return self.ops.dh_dev(self._embed(xu, self.u_idx, 3 * self.ops.n))[self.u_idx]
+
+    def a(self, x):
+        """block2x2(vdd, knd, knd', dnn; 1, -1, 1, 1) applied to x = [t; u]."""
+        if self.reduced:
+            return self.vdd(x)
+        xt, xu = x[:self.nt], x[self.nt:]
+        return self.ops._torch.cat([self.vdd(xt) - self.knd(xu), self.knd_t(xt) + self.dnn(xu)])
+
+    def preconditioner(self) -> VddPreconditioner:
+        return VddPreconditioner(self.ops, self.layout.dirichlet_triangle_ids, self.vdd)
+
+    def rhs(self, g_neumann, g_dirichlet):
+        """assemble_rhs without AMVM (baca.cpp:42-76): the rows
+        [Dirichlet triangles; Neumann nodes] of
+        [-V_h, M/2 + K_h; M'/2 - K_h', -D_h] [g_N; g_D]."""
+        ops, torch = self.ops, self.ops._torch
+        gn = torch.tensor(np.asarray(g_neumann, dtype=np.float64), device=ops.dev)
+        gd = torch.tensor(np.asarray(g_dirichlet, dtype=np.float64), device=ops.dev)
+        if gn.shape[0] != 3 * ops.m or gd.shape[0] != 3 * ops.n:
+            raise DimensionError("assemble_rhs: boundary data size")
+        m, n = ops.m, ops.n
+        mass_gd = torch.cat([ops._spmv(3, gd[c * n:(c + 1) * n]) for c in range(3)])
+        mass_t_gn = torch.cat([ops._spmv(3, gn[c * m:(c + 1) * m], transpose=True)
+                               for c in range(3)])
+        top = -ops.vh_dev(gn) + (0.5 * mass_gd + ops.kh_dev(gd))
+        bottom = (0.5 * mass_t_gn - ops.kh_t_dev(gn)) - ops.dh_dev(gd)
+        f = torch.cat([top[self.t_idx], bottom[self.u_idx]])
+        return f.cpu().numpy()
+
+
+@dataclasses.dataclass
+class SolveStats:  # baca.hpp:91-96
+    iterations: int = 0
+    converged: bool = False
+    used_fallback: bool = False
+    residual: float = 0.0
+
+
+def _bpcg_core(sys: SaddleSystem, prec: VddPreconditioner, f, tol_abs, x0, max_iter):
+    """Bramble-Pasciak CG (baca.cpp:294-366) on [V, -K; -K', -D] with the
+    left transform P^{-1} = [C^{-1}, 0; -K' C^{-1}, -I] and the inner
+    product <x, y> = ((V - C) x_1, y_1) + x_2 . y_2."""
+    nt = sys.nt
+    torch = sys.ops._torch
+
+    def abar(v):
+        s = sys.a(v)
+        return torch.cat([s[:nt], -s[nt:]])
+
+    def ptrans(r):
+        z1 = prec.solve(r[:nt])
+        return torch.cat([z1, -sys.knd_t(z1) - r[nt:]])
+
+    def h_dot(a, b, v_a1):
+        return float(v_a1 @ b[:nt]) - float(prec.apply(a[:nt]) @ b[:nt]) + float(a[nt:] @ b[nt:])
+
+    bbar = torch.cat([f[:nt], -f[nt:]])
+    x = x0.clone()
+    r_orig = bbar - abar(x)
+    rhat = ptrans(r_orig)
+    p = rhat.clone()
+    v_rhat1 = sys.vdd(rhat[:nt])
+    rho = h_dot(rhat, rhat, v_rhat1)
+    st = SolveStats()
+    if rho < 0:
+        return x, st, True
+    while float(r_orig.norm()) > tol_abs and st.iterations < max_iter:
+        ap = abar(p)
+        q = ptrans(ap)
+        v_q1 = sys.vdd(q[:nt])
+        denom = h_dot(q, p, v_q1)
+        if denom <= 0:
+            return x, st, True
+        alpha = rho / denom
+        x = x + alpha * p
+        r_orig = r_orig - alpha * ap
+        rhat = rhat - alpha * q
+        v_rhat1 = v_rhat1 - alpha * v_q1
+        rho_new = h_dot(rhat, rhat, v_rhat1)
+        if rho_new < 0:
+            return x, st, True
+        p = rhat + (rho_new / rho) * p
+        rho = rho_new
+        st.iterations += 1
+    st.residual = float(r_orig.norm())
+    st.converged = st.residual <= tol_abs
+    return x, st, False
+
+
+def _minres(sys: SaddleSystem, prec: VddPreconditioner, f, tol_abs, x0, max_iter):
+    """Preconditioned MINRES on the symmetric form [-V, K; K', D]
+    (baca.cpp:227-292), the fallback solver."""
+    nt = sys.nt
+    torch = sys.ops._torch
+
+    def sym(v):
+        s = sys.a(v)
+        return torch.cat([-s[:nt], s[nt:]])
+
+    def pre(v):
+        return torch.cat([prec.solve(v[:nt]), v[nt:]])
+
+    b = torch.cat([-f[:nt], f[nt:]])
+    x = x0.clone()
+    r1 = b - sym(x)
+    y = pre(r1)
+    beta1 = float(r1 @ y)
+    st = SolveStats()
+    if beta1 < 0:
+        raise Error("minres: preconditioner not positive definite")
+    if beta1 == 0:
+        st.converged = True
+        return x, st
+    beta1 = np.sqrt(beta1)
+    eps_ln = dbar = oldb = 0.0
+    beta = phibar = beta1
+    cs, sn = -1.0, 0.0
+    r2 = r1.clone()
+    w = torch.zeros_like(x)
+    w2 = torch.zeros_like(x)
+    it = 0
+    while it < max_iter and phibar > tol_abs:
+        v = y / beta
+        y = sym(v)
+        if it > 0:
+            y = y - (beta / oldb) * r1
+        alfa = float(v @ y)
+        y = y - (alfa / beta) * r2
+        r1, r2 = r2, y
+        y = pre(r2)
+        oldb = beta
+        beta_sq = float(r2 @ y)
+        if beta_sq < 0:
+            raise Error("minres: preconditioner breakdown")
+        beta = np.sqrt(beta_sq)
+        oldeps = eps_ln
+        delta = cs * dbar + sn * alfa
+        gbar = sn * dbar - cs * alfa
+        eps_ln = sn * beta
+        dbar = -cs * beta
+        gamma = max(np.sqrt(gbar * gbar + beta * beta), 1e-30)
+        cs, sn = gbar / gamma, beta / gamma
+        phi = cs * phibar
+        phibar = sn * phibar
+        w1, w2 = w2, w
+        w = (v - oldeps * w1 - delta * w2) / gamma
+        x = x + phi * w
+        it += 1
+    st.iterations = it
+    st.residual = float((f - sys.a(x)).norm())
+    st.converged = st.residual <= tol_abs * 1.5
+    return x, st
+
+
+def bpcg_solve(sys: SaddleSystem, prec: VddPreconditioner, f, tol_abs: float, x0=None,
+               use_bpcg: bool = True, max_iter: int = 10000):
+    """bpcg_solve (baca.cpp:368-399): PCG in reduced mode, else
+    Bramble-Pasciak CG with the MINRES fallback on breakdown.  Device
+    vectors inside; f / x0 / result as numpy arrays.  Returns (x, stats)."""
+    torch = sys.ops._torch
+    f = np.asarray(f, dtype=np.float64)
+    if f.shape != (sys.dim,):
+        raise DimensionError("bpcg_solve: rhs size")
+    if np.linalg.norm(f) == 0.0:
+        return np.zeros(sys.dim), SolveStats(0, True, False, 0.0)
+    fd = torch.tensor(f, device=sys.ops.dev)
+    xd = torch.zeros_like(fd) if x0 is None else torch.tensor(np.asarray(x0, dtype=np.float64),
+                                                               device=sys.ops.dev)
+    if sys.reduced:
+        x, it, res = _pcg(sys.vdd, prec, fd, tol_abs, xd, max_iter)
+        return x.cpu().numpy(), SolveStats(it, res <= tol_abs, False, res)
+    if use_bpcg:
+        x, st, breakdown = _bpcg_core(sys, prec, fd, tol_abs, xd, max_iter)
+        if not breakdown:
+            return x.cpu().numpy(), st
+        y, st2 = _minres(sys, prec, fd, tol_abs, x, max_iter)
+        st2.iterations += st.iterations
+        st2.used_fallback = True
+        return y.cpu().numpy(), st2
+    x, st = _minres(sys, prec, fd, tol_abs, xd, max_iter)
+    return x.cpu().numpy(), st
+
+
+def _pcg(apply_a, prec: VddPreconditioner, f, tol_abs: float, x0, max_iter: int):
+    x = x0.clone()
+    r = f - apply_a(x)
+    z = prec.solve(r)
+    p = z.clone()
+    rz = float(r @ z)
+    it = 0
+    while float(r.norm()) > tol_abs and it < max_iter:
+        ap = apply_a(p)
+        alpha = rz / float(p @ ap)
+        x = x + alpha * p
+        r = r - alpha * ap
+        z = prec.solve(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+        it += 1
+    return x, it, float(r.norm())
 
 
 def pcg_spd(ops: "OperatorSet", prec: VddPreconditioner, f, tol_abs: float, x0, max_iter: int):
