@@ -282,6 +282,27 @@ def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
     ms = (time.perf_counter() - t0) / reps * 1e3
     y_host = vh.matvec(x)
     entries = sk.aca_entries + sk.dense_entries + sd.aca_entries + sd.dense_entries
+    # the composed operators of the operator algebra
+    # on device vectors: V_h, K_h (3N -> 3M), D_h (3N -> 3N)
+    ops_t = None
+    try:
+        ops = hm.OperatorSet(mesh, 1.0, 0.3, b_min=cfg["b_min"], eta=cfg["eta"], device=device)
+        so = ops.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        xn = torch.tensor(hm.random_vector(3 * ops.n, 3, "uniform"), device=f"cuda:{device}")
+        xm = torch.tensor(hm.random_vector(3 * ops.m, 4, "uniform"), device=f"cuda:{device}")
+        ops_t = {"assembly_ms_device": sum(st_.ms_total for st_ in so)}
+        for name, f_, v_ in (("vh", ops.vh_dev, xm), ("kh", ops.kh_dev, xn),
+                             ("dh", ops.dh_dev, xn), ("kh_t", ops.kh_t_dev, xm)):
+            f_(v_)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(5):
+                f_(v_)
+            torch.cuda.synchronize()
+            ops_t[name + "_ms_wall"] = (time.perf_counter() - t0) / 5 * 1e3
+        del ops
+    except Exception as e:  # informational
+        ops_t = {"error": str(e)}
     # CPU reference path (the oracle restatement, all host threads) beside
     # the device on a bounded sample: the icosphere L3 (1280 triangles)
     cpu = None
@@ -316,7 +337,8 @@ def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
             "matvec_ms_wall": ms, "matvec_dofs_per_s": 3 * nt / (ms * 1e-3),
             "matvec_check_rel": float(np.linalg.norm(y.cpu().numpy() - y_host) /
                                       np.linalg.norm(y_host)),
-            "cpu_baseline": cpu}
+            "cpu_baseline": cpu,
+            "operators": ops_t}
 
 
 def run_ours(args, cfg):

@@ -815,36 +815,52 @@ class OperatorSet:
                 + 2.0 * self.mu * self.vh_dev(t))
 
     def dh_dev(self, x):
-        """D_h x (3N -> 3N), compose_Dh (operators.cpp:114-158)."""
+        """D_h x (3N -> 3N), compose_Dh (operators.cpp:114-158).  All 24
+        V_Delta products of the sandwiches go through ONE multi-RHS H-matvec
+        (S_k x blocks, T_h x blocks -- shared with the diag3 part of V_h --
+        and the T_ki x_j of the D' grid)."""
+        torch = self._torch
         mu, n, m = self.mu, self.n, self.m
-        y = None
-        for k in range(3):
-            z = self.s_k(k, self._hmv(self.vdelta, self.s_k(k, x), 3), transpose=True)
-            y = mu * z if y is None else y + mu * z
+        # inputs of the V_Delta products, in order
+        ins = []
+        for k in range(3):  # S_k x: blocks c of diag3(+-T_w)
+            w, a = self._S[k]
+            ins += [self._spmv(w, x[c * n:(c + 1) * n], alpha=a) for c in range(3)]
         t = self.t_h(x)
-        y = y + 2.0 * mu * self.t_h_t(self._hmv(self.vdelta, t, 3))
-        y = y - 4.0 * mu * mu * self.t_h_t(self.vh_dev(t))
-        # D'_ij = sum_k s1 s2 T_kj' V_Delta T_ki (T_kk = 0, T_lk = -T_kl)
+        ins += [t[c * m:(c + 1) * m] for c in range(3)]
+
         def t_signed(k, l):
             if k == l:
                 return None
             return ({(0, 1): 0, (0, 2): 1, (1, 2): 2}[(min(k, l), max(k, l))],
                     1.0 if k < l else -1.0)
-        dg = []
+        grid = []  # (i, w_kj, sign) per D' product
         for i in range(3):
-            acc = None
             for j in range(3):
                 for k in range(3):
                     tkj, tki = t_signed(k, j), t_signed(k, i)
                     if tkj is None or tki is None:
                         continue
-                    self._sync()
-                    u = self._spmv(tki[0], x[j * n:(j + 1) * n])
-                    w = self._spmv(tkj[0], self._hmv(self.vdelta, u), transpose=True,
-                                   alpha=tkj[1] * tki[1])
-                    acc = w if acc is None else acc + w
-            dg.append(acc)
-        return y + mu * self._torch.cat(dg)
+                    ins.append(self._spmv(tki[0], x[j * n:(j + 1) * n]))
+                    grid.append((i, tkj[0], tkj[1] * tki[1]))
+        Y = self._hmv(self.vdelta, torch.cat(ins), len(ins)).view(len(ins), m)
+        # sum_k mu S_k' diag3(V_Delta) S_k x
+        y = None
+        for k in range(3):
+            w, a = self._S[k]
+            z = torch.cat([self._spmv(w, Y[3 * k + c], transpose=True, alpha=a)
+                           for c in range(3)])
+            y = mu * z if y is None else y + mu * z
+        vd_t = Y[9:12].reshape(-1)  # diag3(V_Delta) T_h x
+        y = y + 2.0 * mu * self.t_h_t(vd_t)
+        s = 0.5 / self.E * (1.0 + self.nu) / (1.0 - self.nu)
+        vh_t = s * ((3.0 - 4.0 * self.nu) * vd_t + self._hmv(self.vkl, t))
+        y = y - 4.0 * mu * mu * self.t_h_t(vh_t)
+        dg = [None, None, None]
+        for q, (i, w, sg) in enumerate(grid):
+            r = self._spmv(w, Y[12 + q], transpose=True, alpha=sg)
+            dg[i] = r if dg[i] is None else dg[i] + r
+        return y + mu * torch.cat(dg)
 
     # ---- host-vector API (numpy in / out) ----
     def _run(self, f, x, n_in):
