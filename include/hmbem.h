@@ -147,6 +147,9 @@ int hmb_dense_block(const hmb_op* op, int comp, int block, double* out);
 /* computes the estimator and keeps it in the operator for hmb_gamma_* */
 int hmb_gamma(hmb_op* op, const double* x, double* gamma, double* difference,
               int* n_terms);
+/* the same for the transposed occurrence: x over the rows, terms and
+ * difference over the columns (amvm.cpp:100-106); kept like hmb_gamma's */
+int hmb_gamma_t(hmb_op* op, const double* x, double* gamma, double* difference, int* n_terms);
 /* per term: comp, block, nnz, norm_sq */
 int hmb_gamma_terms(const hmb_op* op, int* comp, int* block, int* nnz, double* norm_sq);
 int hmb_gamma_term_data(const hmb_op* op, int t, long long* idx, double* val);

@@ -259,6 +259,12 @@ int hmgpu_amvm_refine(hmgpu_ctx* ctx, int steps, int* comp_block);
 
 int hmgpu_tail_terms(hmgpu_ctx* ctx, const double* x, int* n_terms,
                      long long* n_vals, long long* meta4, double* vals);
+/* the transposed tails V[:,k:K](U[:,k:K]^T x) of the transposed occurrences
+ * (gamma_contributions, amvm.cpp:100-106): x over the rows, per term nocc x n
+ * values over the block columns (internal order); grid occurrence 0 is the
+ * cell (R, C) (x_R -> component C), occurrence 1 its alias (x_C -> R) */
+int hmgpu_tail_terms_t(hmgpu_ctx* ctx, const double* x, int* n_terms,
+                       long long* n_vals, long long* meta4, double* vals);
 
 /* factor of (comp, block): U (m x K) and V (n x K) column-major, pivots
  * (K x 2, local), frob_sq; with U == NULL only the sizes are returned */

@@ -8,7 +8,7 @@ from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflo
                   DimensionError, Error, GammaContributions, HMatrix, LameSingleLayer, Mesh,
                   OperatorSet, lame_constants, InteriorEvaluator, BacaConfig, BacaReport, VddPreconditioner,
                   baca_solve, pcg_spd, estimator_vh, doerfler_mark, DofLayout, SaddleSystem,
-                  SolveStats, bpcg_solve,
+                  SolveStats, bpcg_solve, SaddleEstimator, baca_solve_saddle,
                   MeshError, Mode, amvm_multiply, assemble, device_count, gamma_contributions,
                   host_tree_and_partition)
 
@@ -18,7 +18,7 @@ __all__ = [
     "DimensionError", "Error", "GammaContributions", "HMatrix", "LameSingleLayer", "Mesh",
     "OperatorSet", "lame_constants", "InteriorEvaluator", "BacaConfig", "BacaReport", "VddPreconditioner",
     "baca_solve", "pcg_spd", "estimator_vh", "doerfler_mark", "DofLayout", "SaddleSystem",
-    "SolveStats", "bpcg_solve",
+    "SolveStats", "bpcg_solve", "SaddleEstimator", "baca_solve_saddle",
     "MeshError",
     "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",
     "host_tree_and_partition",

@@ -83,6 +83,7 @@ _sig(host, "hmb_storage", I, P, P)
 _sig(host, "hmb_factor", I, P, I, I, IP, IP, IP, IP, P, P, P, DP)
 _sig(host, "hmb_dense_block", I, P, I, I, P)
 _sig(host, "hmb_gamma", I, P, P, DP, P, IP)
+_sig(host, "hmb_gamma_t", I, P, P, DP, P, IP)
 _sig(host, "hmb_gamma_terms", I, P, P, P, P, P)
 _sig(host, "hmb_gamma_term_data", I, P, I, P, P)
 _sig(host, "hmb_mark", I, P, D, I, LL, LL, P, IP, DP)

@@ -497,15 +497,18 @@ class HMatrix:
         return out
 
     # ---- adaptive matvec ----
-    def gamma_contributions(self, x, term_data: bool = True) -> GammaContributions:
+    def gamma_contributions(self, x, term_data: bool = True,
+                            transposed: bool = False) -> GammaContributions:
         """term_data = False skips the per-term index/value downloads (the
         terms then carry empty idx / val; gamma, difference and norm_sq are
-        complete)."""
+        complete).  transposed: the transposed occurrence (x over the rows,
+        terms over the columns)."""
         x = _f64(x)
         g = C.c_double()
-        diff = np.zeros(self.rows)
+        diff = np.zeros(self.cols if transposed else self.rows)
         nt = C.c_int()
-        _check(_h.hmb_gamma(self._h, _ptr(x), C.byref(g), _ptr(diff), C.byref(nt)))
+        fn = _h.hmb_gamma_t if transposed else _h.hmb_gamma
+        _check(fn(self._h, _ptr(x), C.byref(g), _ptr(diff), C.byref(nt)))
         n = nt.value
         self._last_nterms = n
         comp, block, nnz = (np.zeros(n, np.int32) for _ in range(3))
@@ -676,6 +679,7 @@ class OperatorSet:
         self.lam, self.mu = lame_constants(E, nu)
         self.device = device
         self.dev = torch.device("cuda", device)
+        self._mesh = mesh
         self.vkl = HMatrix.galerkin(mesh, 0, b_min, eta, device)
         self.vdelta = HMatrix.galerkin(mesh, 1, b_min, eta, device)
         self.kdelta = HMatrix.kdelta(mesh, b_min, eta, device)
@@ -726,7 +730,7 @@ class OperatorSet:
         x = x.contiguous()
         y = self._torch.empty(h.rows * nrhs, dtype=self._torch.float64, device=self.dev)
         self._sync()
-        h.matvec_ptr(x.data_ptr(), y.data_ptr(), nrhs)
+        h.matvec_ptr(x.data_ptr(), y.data_ptr(), nrhs, getattr(self, "mode", Mode.Current))
         self._sync()
         return y
 
@@ -736,7 +740,8 @@ class OperatorSet:
         y = self._torch.empty(h.cols * nrhs, dtype=self._torch.float64, device=self.dev)
         self._sync()
         _check(_h.hmb_matvec_transposed(h._h, C.c_void_p(x.data_ptr()),
-                                        C.c_void_p(y.data_ptr()), nrhs, 0, 1))
+                                        C.c_void_p(y.data_ptr()), nrhs,
+                                        int(getattr(self, "mode", Mode.Current)), 1))
         self._sync()
         return y
 
@@ -1110,6 +1115,238 @@ class SaddleSystem:
         bottom = (0.5 * mass_t_gn - ops.kh_t_dev(gn)) - ops.dh_dev(gd)
         f = torch.cat([top[self.t_idx], bottom[self.u_idx]])
         return f.cpu().numpy()
+
+
+class SaddleEstimator:
+    """estimator_Ek of the mixed system (baca.cpp:401-456) over the
+    flattened leaf occurrences of V_DD, -K_ND, K_ND^T and D_NN
+    (flatten_occurrences, expr.cpp:424-498): per occurrence the device
+    computes every block's look-ahead tail (hmgpu_tail_terms / _t) on the
+    occurrence's input (suffix x), the host maps it through the prefix (the
+    restrictions, embeddings and T_h^T / S_k^T sandwiches, sparse) and sums
+    it per (H-matrix, block) within each occurrence list
+    (gamma_contributions, amvm.cpp:46-125); the K family merges the terms of
+    -K_ND and K_ND^T by adding their norms (add_terms, baca.cpp:406-432)."""
+
+    FAMILY = ("V", "K", "D")
+
+    def __init__(self, sys: "SaddleSystem"):
+        import scipy.sparse as sp
+        self.sys = sys
+        ops = sys.ops
+        m, n = ops.m, ops.n
+        L = sys.layout
+        self.nt, self.nu = sys.nt, sys.nu_
+        sel = lambda idx, N: sp.csr_matrix((np.ones(len(idx)), (np.arange(len(idx)), idx)),
+                                           shape=(len(idx), N))
+        self.St = sel(L.t_dofs, 3 * m)
+        self.Su = sel(L.u_dofs, 3 * n)
+        Tw = []
+        for which in range(3):
+            cols = np.zeros(3 * m, np.int32)
+            vals = np.zeros(3 * m)
+            _check(_h.hmb_sparse_op(ops._mesh._h, which, _ptr(cols), _ptr(vals)))
+            Tw.append(sp.csr_matrix((vals, (np.repeat(np.arange(m), 3), cols)), shape=(m, n)))
+        self.Tw = Tw
+        Z = None
+        blk = [[Z, Tw[0], Tw[1]], [-Tw[0], Z, Tw[2]], [-Tw[1], -Tw[2], Z]]
+        self.Th = sp.bmat(blk, format="csr")
+        self.Em = [sel(np.arange(m) + c * m, 3 * m).T.tocsr() for c in range(3)]  # 3m x m
+        self.En = [sel(np.arange(n) + c * n, 3 * n).T.tocsr() for c in range(3)]  # 3n x n
+        self.s = 0.5 / ops.E * (1.0 + ops.nu) / (1.0 - ops.nu)
+        self.c34 = 3.0 - 4.0 * ops.nu
+        self.mu = ops.mu
+
+    # occurrence lists: (h, transposed, coeff, suffix, prefix); suffix /
+    # prefix are sparse matrices (None = identity), h one of the contexts
+    def _vh_occ(self, coeff, suffix, prefix):
+        """the leaves of coeff * prefix V_h suffix (compose_Vh)."""
+        o = [(self.sys.ops.vkl, False, coeff * self.s, suffix, prefix)]
+        for c in range(3):
+            sf = self.Em[c].T @ suffix
+            pf = prefix @ self.Em[c]
+            o.append((self.sys.ops.vdelta, False, coeff * self.s * self.c34, sf, pf))
+        return o
+
+    def _kh_occ(self, coeff, suffix, prefix):
+        """the leaves of coeff * prefix K_h suffix (compose_Kh)."""
+        ops = self.sys.ops
+        o = []
+        for c in range(3):
+            o.append((ops.kdelta, False, coeff, self.En[c].T @ suffix, prefix @ self.Em[c]))
+        for c in range(3):
+            o.append((ops.vdelta, False, -coeff, self.Em[c].T @ self.Th @ suffix,
+                      prefix @ self.Em[c]))
+        o += self._vh_occ(2.0 * self.mu * coeff, self.Th @ suffix, prefix)
+        return o
+
+    def _dh_occ(self, suffix, prefix):
+        ops, mu = self.sys.ops, self.mu
+        o = []
+        S = ((2, -1.0), (1, 1.0), (0, 1.0))
+        for (w, a) in S:
+            for c in range(3):
+                o.append((ops.vdelta, False, mu, a * self.Tw[w] @ self.En[c].T @ suffix,
+                          prefix @ self.En[c] @ (a * self.Tw[w].T)))
+        for c in range(3):
+            o.append((ops.vdelta, False, 2.0 * mu, self.Em[c].T @ self.Th @ suffix,
+                      prefix @ self.Th.T @ self.Em[c]))
+        o += self._vh_occ(-4.0 * mu * mu, self.Th @ suffix, prefix @ self.Th.T)
+        ts = lambda k, l: None if k == l else ({(0, 1): 0, (0, 2): 1, (1, 2): 2}[
+            (min(k, l), max(k, l))], 1.0 if k < l else -1.0)
+        for i in range(3):
+            for j in range(3):
+                for k in range(3):
+                    tkj, tki = ts(k, j), ts(k, i)
+                    if tkj is None or tki is None:
+                        continue
+                    o.append((ops.vdelta, False, mu * tkj[1] * tki[1],
+                              self.Tw[tki[0]] @ self.En[j].T @ suffix,
+                              prefix @ self.En[i] @ self.Tw[tkj[0]].T))
+        return o
+
+    @staticmethod
+    def _transpose(occ):
+        return [(h, not tr, c, pf.T.tocsr(), sf.T.tocsr()) for (h, tr, c, sf, pf) in occ]
+
+    def _gamma(self, occ, x, out_dim):
+        """gamma_contributions over an occurrence list: {(h, comp, block):
+        dense vector over out_dim}, grouped by H-matrix (first appearance)."""
+        acc = {}
+        for (h, tr, coeff, suffix, prefix) in occ:
+            xin = suffix @ x
+            g = h.gamma_contributions(xin, term_data=True, transposed=tr)
+            for t in g.terms:
+                v = prefix[:, t.idx] @ (coeff * t.val)
+                key = (id(h), t.comp, t.block)
+                if key not in acc:
+                    acc[key] = (h, np.zeros(out_dim))
+                acc[key][1][:] += v
+        return acc
+
+    def estimate(self, x):
+        """(E_k, terms [(family, h, comp, block, norm_sq)], diff over [t; u])."""
+        import scipy.sparse as sp
+        nt, nu = self.nt, self.nu
+        x = np.asarray(x, dtype=np.float64)
+        xt, xu = x[:nt], x[nt:]
+        diff = np.zeros(nt + nu)
+        terms = []
+        vdd = self._vh_occ(1.0, self.St.T.tocsr(), self.St)
+        for key, (h, v) in self._gamma(vdd, xt, nt).items():
+            terms.append(("V", h, key[1], key[2], float(v @ v)))
+            diff[:nt] += v
+        if nu:
+            knd = self._kh_occ(1.0, self.Su.T.tocsr(), self.St)
+            k12 = [(h, tr, -c, sf, pf) for (h, tr, c, sf, pf) in knd]
+            k21 = self._transpose(knd)
+            kt = {}
+            for key, (h, v) in self._gamma(k12, xu, nt).items():
+                kt[key] = ["K", h, key[1], key[2], float(v @ v)]
+                diff[:nt] += v
+            for key, (h, v) in self._gamma(k21, xt, nu).items():
+                if key in kt:
+                    kt[key][4] += float(v @ v)
+                else:
+                    kt[key] = ["K", h, key[1], key[2], float(v @ v)]
+                diff[nt:] += v
+            terms += [tuple(t) for t in kt.values()]
+            dnn = self._dh_occ(self.Su.T.tocsr(), self.Su)
+            for key, (h, v) in self._gamma(dnn, xu, nu).items():
+                terms.append(("D", h, key[1], key[2], float(v @ v)))
+                diff[nt:] += v
+        ek = float(np.sqrt(sum(t[4] for t in terms)))
+        return ek, terms, diff
+
+
+def baca_solve_saddle(sys: "SaddleSystem", f, cfg: Optional[BacaConfig] = None):
+    """baca_solve (baca.cpp:488-600) for the mixed system: BPCG under the
+    adaptive accuracy condition, E_k over the V / K / D families, Doerfler
+    marking, and the refinement in the operator order -- (1) D_NN wholly,
+    (2) V_DD wholly plus the marked K blocks, (3) else the marked V blocks --
+    by promotion + look-ahead extension on the device.  Returns (x, report)
+    with per-sweep records (k, ek, tail_norm, residual, inner_tol,
+    inner_iterations, marked per family, phases)."""
+    import time as _time
+    cfg = cfg or BacaConfig()
+    if not 0.0 < cfg.theta < 1.0:
+        raise Error("baca_solve: theta must lie in (0,1)")
+    f = np.asarray(f, dtype=np.float64)
+    if f.shape != (sys.dim,):
+        raise DimensionError("baca_solve: rhs size")
+    ops = sys.ops
+    est = SaddleEstimator(sys)
+    prec = sys.preconditioner()
+    fnorm = float(np.linalg.norm(f))
+    floor_abs = cfg.inner_floor * max(fnorm, 1e-300)
+    x = np.zeros(sys.dim)
+    tol_abs = max(cfg.inner_tol0 * fnorm, floor_abs)
+    t0 = _time.perf_counter()
+    its = []
+
+    def all_blocks(h):  # every low-rank (comp, block) of a context
+        kc = h.ranks()[0]
+        return [(q, b) for q in range(kc.shape[0]) for b in range(kc.shape[1]) if kc[q, b] >= 0]
+
+    for k in range(cfg.max_outer + 1):
+        inner, used_fb = 0, False
+        for _ in range(6):
+            x, st = bpcg_solve(sys, prec, f, tol_abs, x)
+            inner += st.iterations
+            used_fb = used_fb or st.used_fallback
+            ek, terms, diff = est.estimate(x)
+            tail = float(np.linalg.norm(diff))
+            cond = cfg.alpha * tail
+            if st.residual <= max(cond, floor_abs):
+                break
+            tol_abs = max(cond, floor_abs)
+        it = dict(k=k, ek=ek, tail_norm=tail, residual=st.residual, inner_tol=tol_abs,
+                  inner_iterations=inner, used_fallback=used_fb, marked_v=0, marked_k=0,
+                  marked_d=0, phases=[], wall_time_s=_time.perf_counter() - t0)
+        if ek <= cfg.eps_baca:
+            its.append(it)
+            return x, BacaReport(its, True, "tolerance")
+        if k >= cfg.max_outer:
+            its.append(it)
+            return x, BacaReport(its, False, "max_outer")
+        order = sorted(range(len(terms)), key=lambda i: -terms[i][4])
+        target = cfg.theta * cfg.theta * ek * ek
+        marked, acc = [], 0.0
+        for i in order:
+            if acc >= target:
+                break
+            marked.append(i)
+            acc += terms[i][4]
+        fams = [terms[i][0] for i in marked]
+        it["marked_v"], it["marked_k"], it["marked_d"] = (fams.count("V"), fams.count("K"),
+                                                          fams.count("D"))
+        promo = {}
+        def add(h, comp, block):
+            promo.setdefault(id(h), (h, set()))[1].add((comp, block))
+        def add_all(hs):
+            for h in hs:
+                for (q, b) in all_blocks(h):
+                    add(h, q, b)
+        if it["marked_d"]:
+            it["phases"].append(1)
+            add_all([ops.vdelta, ops.vkl])  # the leaves of D_NN
+        if it["marked_k"]:
+            it["phases"].append(2)
+            add_all([ops.vdelta, ops.vkl])  # V_DD wholly
+            for i in marked:
+                if terms[i][0] == "K":
+                    add(terms[i][1], terms[i][2], terms[i][3])
+        if not it["marked_d"] and not it["marked_k"]:
+            it["phases"].append(3)
+            for i in marked:
+                add(terms[i][1], terms[i][2], terms[i][3])
+        for (h, pairs) in promo.values():
+            pairs = sorted(pairs)
+            h.promote(pairs)
+            h.extend_lookahead(pairs, cfg.lookahead_steps)
+        its.append(it)
+        tol_abs = max(tol_abs, floor_abs)
+    return x, BacaReport(its, False, "max_outer")
 
 
 @dataclasses.dataclass

@@ -2930,8 +2930,21 @@ int hmgpu_amvm_refine(hmgpu_ctx* c, int steps, int* comp_block) {
   });
 }
 
+namespace {
+int tail_terms_impl(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_vals,
+                    long long* meta4, double* vals, bool transposed);
+}
 int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_vals,
                      long long* meta4, double* vals) {
+  return tail_terms_impl(c, x, n_terms, n_vals, meta4, vals, false);
+}
+int hmgpu_tail_terms_t(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_vals,
+                       long long* meta4, double* vals) {
+  return tail_terms_impl(c, x, n_terms, n_vals, meta4, vals, true);
+}
+namespace {
+int tail_terms_impl(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_vals,
+                    long long* meta4, double* vals, bool transposed) {
   return guard(c, [&] {
     if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
     if (!n_terms || !n_vals) fail(HMGPU_ERR_INVALID, "null outputs");
@@ -2945,7 +2958,7 @@ int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_v
         if (it.k <= it.kcur) continue;
         const int nocc = (c->NC == 6 && c_comp_host_r(q) != c_comp_host_c(q)) ? 2 : 1;
         terms.push_back({i0 + q, nocc, off});
-        off += (long long)nocc * it.m;
+        off += (long long)nocc * (transposed ? it.n : it.m);
       }
     }
     // terms in component-major order (the by-H-matrix grouping of
@@ -2956,7 +2969,7 @@ int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_v
     off = 0;
     for (TailTerm& t : terms) {
       t.off = off;
-      off += (long long)t.nocc * c->items[t.item].m;
+      off += (long long)t.nocc * (transposed ? c->items[t.item].n : c->items[t.item].m);
     }
     *n_terms = (int)terms.size();
     *n_vals = off;
@@ -2970,18 +2983,38 @@ int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_v
       meta4[4 * t + 3] = terms[t].off;
     }
     if (terms.empty()) return;
-    const long long nx = c->ndof_cols();
+    const int NOUT = c->NC == 6 ? 3 : 1;
+    const long long nx = transposed ? (long long)c->n_rows * NOUT : c->ndof_cols();
     c->d_x.ensure((size_t)nx);
     CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice,
                        c->stream));
-    gather_x(c, c->d_x.p, 1);
+    if (transposed) {
+      c->d_xr.ensure((size_t)nx);
+      const int gg = grid_for(c, (nx + 255) / 256);
+      if (NOUT == 3)
+        gather_kernel<3><<<gg, 256, 0, c->stream>>>(c->d_x.p, c->d_xr.p, c->d_rperm.p,
+                                                     c->n_rows, 1);
+      else
+        gather_kernel<1><<<gg, 256, 0, c->stream>>>(c->d_x.p, c->d_xr.p, c->d_rperm.p,
+                                                     c->n_rows, 1);
+    } else {
+      gather_x(c, c->d_x.p, 1);
+    }
     DBuf<TailTerm> d_terms;
     d_terms.upload(terms, c->stream);
     DBuf<double> d_out;
     d_out.alloc((size_t)off);
     c->timed("tail", [&] {
       const int grid = grid_for(c, ((long long)terms.size() + 7) / 8, 8);
-      if (c->NC == 6)
+      if (transposed && c->NC == 6)
+        tail_t_kernel<3><<<grid, 256, 0, c->stream>>>(d_terms.p, (int)terms.size(),
+                                                     c->d_items.p, c->d_arena.p, c->d_xr.p,
+                                                     d_out.p, 1);
+      else if (transposed)
+        tail_t_kernel<1><<<grid, 256, 0, c->stream>>>(d_terms.p, (int)terms.size(),
+                                                     c->d_items.p, c->d_arena.p, c->d_xr.p,
+                                                     d_out.p, 0);
+      else if (c->NC == 6)
         tail_kernel<3><<<grid, 256, 0, c->stream>>>(d_terms.p, (int)terms.size(),
                                                    c->d_items.p, c->d_arena.p,
                                                    c->d_xi.p, d_out.p, 1);
@@ -2997,6 +3030,7 @@ int hmgpu_tail_terms(hmgpu_ctx* c, const double* x, int* n_terms, long long* n_v
     d_out.free();
   });
 }
+}  // namespace
 
 int hmgpu_download_factor(hmgpu_ctx* c, int comp, int block, int* m, int* n, int* K,
                           int* k_cur, double* U, double* V, int* piv, double* frob_sq) {

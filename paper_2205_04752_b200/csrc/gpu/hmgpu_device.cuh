@@ -1741,6 +1741,48 @@ __global__ void tail_kernel(const TailTerm* __restrict__ terms, int nterms,
   }
 }
 
+// transposed tails V[:,k:K](U[:,k:K]^T x) over the block columns (the
+// transposed occurrences of gamma_contributions, amvm.cpp:100-106): in the
+// grid the cell (R, C) maps x_R to columns of component C and its alias
+// (C, R) maps x_C to component R.  xr: x gathered to internal row order.
+template <int NOUT>
+__global__ void tail_t_kernel(const TailTerm* __restrict__ terms, int nterms,
+                              const Item* __restrict__ items,
+                              const double* __restrict__ arena,
+                              const double* __restrict__ xr, double* __restrict__ out,
+                              int is_grid) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < nterms; t += nw) {
+    const TailTerm tt = terms[t];
+    const Item it = items[tt.item];
+    const int rr = is_grid ? c_comp_r[it.comp] : 0;
+    const int cc = is_grid ? c_comp_c[it.comp] : 0;
+    const double* U = arena + it.u_off;
+    const double* V = arena + it.v_off;
+    double* o = out + tt.off;
+    for (int j = lane; j < tt.nocc * it.n; j += 32) o[j] = 0.0;
+    __syncwarp();
+    for (int l = it.kcur; l < it.k; ++l) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int i = lane; i < it.m; i += 32) {
+        const double u = U[(long long)l * it.m + i];
+        const double* xi = xr + (long long)(it.row0 + i) * NOUT;
+        s1 = fma(u, xi[rr], s1);
+        if (tt.nocc == 2) s2 = fma(u, xi[cc], s2);
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      for (int j = lane; j < it.n; j += 32) {
+        const double v = V[(long long)l * it.n + j];
+        o[j] = fma(v, s1, o[j]);
+        if (tt.nocc == 2) o[it.n + j] = fma(v, s2, o[it.n + j]);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // DFMA throughput probe (roofline denominator for the fp64 kernels): 8
 // independent FMA chains per thread, the result kept live.

@@ -564,6 +564,19 @@ int hmb_gamma(hmb_op* op, const double* x, double* gamma, double* difference,
   });
 }
 
+int hmb_gamma_t(hmb_op* op, const double* x, double* gamma, double* difference, int* n_terms) {
+  return guard([&] {
+    need(op, "op");
+    need(x, "x");
+    op->gamma = hmb::gamma_contributions_transposed(*op->op, x);
+    if (gamma) *gamma = op->gamma.gamma;
+    if (difference)
+      std::memcpy(difference, op->gamma.difference.data(),
+                  op->gamma.difference.size() * sizeof(double));
+    if (n_terms) *n_terms = static_cast<int>(op->gamma.terms.size());
+  });
+}
+
 int hmb_gamma_terms(const hmb_op* op, int* comp, int* block, int* nnz, double* norm_sq) {
   return guard([&] {
     need(op, "op");

@@ -633,6 +633,66 @@ GammaContributions gamma_contributions(const HOperator& op, const double* x) {
   return g;
 }
 
+// the transposed occurrences (gamma_contributions with occ.transposed,
+// amvm.cpp:100-106): per (comp, block) the tail V[:,k:K](U[:,k:K]^T x) over
+// the block columns (external column ids), grid occurrence 0 = cell (R, C)
+// transposed (x_R -> component C), 1 = its alias (x_C -> R)
+GammaContributions gamma_contributions_transposed(const HOperator& op, const double* x) {
+  if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
+    throw ConfigError("gamma_contributions: sharded operators are not supported");
+  GammaContributions g;
+  const long long NCOLS = op.cols();
+  const int N = op.col_tree().size();
+  g.difference.assign(NCOLS, 0.0);
+  int n_terms = 0;
+  long long n_vals = 0;
+  check_status(op.gpu(), hmgpu_tail_terms_t(op.gpu(), x, &n_terms, &n_vals, nullptr, nullptr),
+               "hmgpu_tail_terms_t");
+  std::vector<long long> meta(4LL * n_terms);
+  std::vector<double> vals(n_vals);
+  if (n_terms > 0)
+    check_status(op.gpu(),
+                 hmgpu_tail_terms_t(op.gpu(), x, &n_terms, &n_vals, meta.data(), vals.data()),
+                 "hmgpu_tail_terms_t");
+  const bool grid = op.ncomp() == 6;
+  const auto& cperm = op.col_tree().perm;
+  std::vector<std::pair<long long, double>> buf;
+  for (int t = 0; t < n_terms; ++t) {
+    const int comp = static_cast<int>(meta[4 * t]);
+    const int b = static_cast<int>(meta[4 * t + 1]);
+    const int nocc = static_cast<int>(meta[4 * t + 2]);
+    const long long off = meta[4 * t + 3];
+    const ClusterNode& cn = op.col_tree().nodes[op.partition().blocks[b].col_node];
+    const int n = cn.size();
+    buf.clear();
+    for (int o = 0; o < nocc; ++o) {
+      const int ob = grid ? (o == 0 ? kCompC[comp] : kCompR[comp]) : 0;
+      for (int j = 0; j < n; ++j) {
+        const double v = vals[off + static_cast<long long>(o) * n + j];
+        if (grid && v == 0.0) continue;
+        buf.emplace_back(static_cast<long long>(ob) * N + cperm[cn.begin + j], v);
+      }
+    }
+    if (buf.empty()) continue;
+    std::sort(buf.begin(), buf.end(),
+              [](const auto& a, const auto& b) { return a.first < b.first; });
+    BlockTerm term;
+    term.comp = comp;
+    term.block = b;
+    for (const auto& e : buf) {
+      term.idx.push_back(e.first);
+      term.val.push_back(e.second);
+      g.difference[e.first] += e.second;
+      term.norm_sq += e.second * e.second;
+    }
+    g.terms.push_back(std::move(term));
+  }
+  double s2 = 0.0;
+  for (double v : g.difference) s2 += v * v;
+  g.gamma = std::sqrt(s2);
+  return g;
+}
+
 // row-sorted greedy marking (amvm.cpp:131-184)
 std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
                              long long m_rows, long long n_cols, Real* gamma_pk_out) {

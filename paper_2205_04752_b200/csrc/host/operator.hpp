@@ -177,6 +177,8 @@ struct GammaContributions {  // amvm.hpp:27-31
 };
 
 GammaContributions gamma_contributions(const HOperator& op, const double* x);
+// the same for the transposed occurrence (x over the rows, terms over the columns)
+GammaContributions gamma_contributions_transposed(const HOperator& op, const double* x);
 std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
                              long long m_rows, long long n_cols,
                              Real* gamma_pk_out = nullptr);

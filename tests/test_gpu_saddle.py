@@ -112,3 +112,50 @@ def test_warm_starts_beat_cold(fx):  # test_baca.cpp:143-152
     _, warm = hm.bpcg_solve(fx["sys"], fx["prec"], f, 1e-3 * nf, x1)
     _, cold = hm.bpcg_solve(fx["sys"], fx["prec"], f, 1e-3 * nf)
     assert warm.iterations < cold.iterations
+
+
+@pytest.fixture(scope="module")
+def coarse():
+    """BacaFixture-like coarse system (test_baca.cpp:11-48): full-mode ACA at
+    a loose tolerance so that the look-ahead tails are large."""
+    mesh = hm.Mesh.voxel_cube(4, -1.0, 1.0)
+    mesh.label_dirichlet("x1>=1|x2<=-1|x3>=1")
+    ops = hm.OperatorSet(mesh, 1.0, 0.3, b_min=8, eta=1.0, device=0)
+    ops.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    return mesh, ops, hm.SaddleSystem(ops, hm.DofLayout(mesh))
+
+
+def test_estimator_aggregates_family_terms(coarse):  # test_baca.cpp:155-178
+    torch = pytest.importorskip("torch")
+    mesh, ops, sys = coarse
+    x = orc.random_vector(sys.dim, 31)
+    ek, terms, diff = hm.SaddleEstimator(sys).estimate(x)
+    assert ek == pytest.approx(np.sqrt(sum(t[4] for t in terms)), rel=1e-12)
+    xd = torch.tensor(x, device="cuda")
+    cur = sys.a(xd).cpu().numpy()
+    ops.mode = hm.Mode.Lookahead
+    try:
+        look = sys.a(xd).cpu().numpy()
+    finally:
+        ops.mode = hm.Mode.Current
+    want = look - cur
+    assert np.linalg.norm(diff - want) <= 1e-10 * (np.linalg.norm(want) + 1.0)
+    assert {t[0] for t in terms} == {"V", "K", "D"}  # all three families on a mixed mesh
+
+
+def test_baca_saddle_drives_estimator_below_tolerance(coarse, fx):  # test_baca.cpp:195-227
+    mesh, ops, sys = coarse
+    f = sys.rhs(fx["g_n"], fx["g_d"])
+    cfg = hm.BacaConfig(theta=0.8, alpha=10.0, eps_baca=3e-7, inner_tol0=1e-1)
+    x, rep = hm.baca_solve_saddle(sys, f, cfg)
+    assert rep.converged and rep.iterations[-1]["ek"] <= cfg.eps_baca
+    want = np.linalg.solve(fx["A"], fx["f"])
+    assert np.linalg.norm(x - want) <= 1e-3 * np.linalg.norm(want)
+    for it in rep.iterations:
+        if cfg.alpha * it["tail_norm"] > 1e-12 * np.linalg.norm(f):
+            assert it["residual"] <= max(cfg.alpha * it["tail_norm"], it["inner_tol"]) * (1 + 1e-10)
+        ph = it["phases"]
+        assert all(ph[i - 1] < ph[i] for i in range(1, len(ph)))  # D before K before V
+        if it["marked_d"] > 0:
+            assert ph and ph[0] == 1
+    assert len(rep.iterations) > 1
