@@ -62,6 +62,11 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
                  double* areas, double* normals, double* diam, int* dirichlet);
 void hmb_mesh_free(hmb_mesh* m);
 
+/* the touching-pair (Sauter-Schwab) rule uploaded to the device:
+ * pair_case 1 vertex, 2 edge, 3 identical; order = points per dimension
+ * (quadrature.cpp:168-338); NULL arrays query n */
+int hmb_pair_rule(int pair_case, int order, int* n, double* xr1, double* xr2, double* yr1,
+                  double* yr2, double* w);
 /* sparse transforms of build_sparse_ops (operators.cpp:7-95) in ELL form:
  * n_tri rows x 3 slots (slot a = local vertex a, value 0 where the reference
  * drops the entry).  which: 0 T12, 1 T13, 2 T23, 3 mass (area / 3). */

@@ -6,7 +6,7 @@ include/hmgpu.h, with a host layer mirroring the reference's operator API.
 from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflops, dmma_peak_tflops, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
                   AssemblyStats, BlockTerm, ClusterTree, ConfigError, DeviceError,
                   DimensionError, Error, GammaContributions, HMatrix, LameSingleLayer, Mesh,
-                  OperatorSet, lame_constants, InteriorEvaluator, BacaConfig, BacaReport, VddPreconditioner,
+                  OperatorSet, lame_constants, InteriorEvaluator, pair_rule, sparse_op, BacaConfig, BacaReport, VddPreconditioner,
                   baca_solve, pcg_spd, estimator_vh, doerfler_mark, DofLayout, SaddleSystem,
                   SolveStats, bpcg_solve, SaddleEstimator, baca_solve_saddle,
                   MeshError, Mode, amvm_multiply, assemble, device_count, gamma_contributions,
@@ -16,7 +16,7 @@ __all__ = [
     "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
     "AssemblyStats", "BlockTerm", "ClusterTree", "ConfigError", "DeviceError",
     "DimensionError", "Error", "GammaContributions", "HMatrix", "LameSingleLayer", "Mesh",
-    "OperatorSet", "lame_constants", "InteriorEvaluator", "BacaConfig", "BacaReport", "VddPreconditioner",
+    "OperatorSet", "lame_constants", "InteriorEvaluator", "pair_rule", "sparse_op", "BacaConfig", "BacaReport", "VddPreconditioner",
     "baca_solve", "pcg_spd", "estimator_vh", "doerfler_mark", "DofLayout", "SaddleSystem",
     "SolveStats", "bpcg_solve", "SaddleEstimator", "baca_solve_saddle",
     "MeshError",

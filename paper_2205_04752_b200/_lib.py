@@ -61,6 +61,7 @@ _sig(host, "hmb_op_kelvin_points", I, P, I, P, D, D, I, D, D, I, I, I, I, C.POIN
 _sig(host, "hmb_op_kelvin_double", I, P, I, P, I, I, D, D, I, D, D, I, I, I, I, C.POINTER(P))
 _sig(host, "hmb_op_kdelta", I, P, I, D, I, I, I, C.POINTER(P))
 _sig(host, "hmb_sparse_op", I, P, I, P, P)
+_sig(host, "hmb_pair_rule", I, I, I, IP, P, P, P, P, P)
 _sig(gpu, "hmgpu_ell3_spmv", I, P, I, P, P, P, P, D, D)
 _sig(gpu, "hmgpu_ell3_spmv_t", I, P, I, P, P, P, P, P, D, D)
 _sig(host, "hmb_op_newton", I, I, P, P, D, I, D, I, C.POINTER(P))

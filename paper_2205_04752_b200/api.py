@@ -646,6 +646,27 @@ class LameSingleLayer:
         return s * ((3.0 - 4.0 * self.nu) * yd + yg)
 
 
+def pair_rule(pair_case: int, order: int):
+    """The touching-pair rule the device uses (Sauter-Schwab, quadrature.cpp:
+    168-338): (xr1, xr2, yr1, yr2, w)."""
+    n = C.c_int()
+    _check(_h.hmb_pair_rule(int(pair_case), int(order), C.byref(n), None, None, None, None,
+                            None))
+    arr = [np.zeros(n.value) for _ in range(5)]
+    _check(_h.hmb_pair_rule(int(pair_case), int(order), C.byref(n), *[_ptr(a) for a in arr]))
+    return tuple(arr)
+
+
+def sparse_op(mesh: Mesh, which: int):
+    """build_sparse_ops in ELL form (operators.cpp:7-95): which 0 T12, 1 T13,
+    2 T23, 3 mass; returns (cols, vals), n_tri x 3 each."""
+    m = mesh.num_triangles
+    cols = np.zeros(3 * m, np.int32)
+    vals = np.zeros(3 * m)
+    _check(_h.hmb_sparse_op(mesh._h, int(which), _ptr(cols), _ptr(vals)))
+    return cols.reshape(m, 3), vals.reshape(m, 3)
+
+
 def lame_constants(E: float, nu: float):
     """lambda = E nu / ((1+nu)(1-2nu)), mu = E / (2(1+nu)) (kernels.cpp:7-14)."""
     if E <= 0.0:

@@ -177,6 +177,21 @@ int hmb_mesh_get(const hmb_mesh* m, double* verts, int* tris, double* centroids,
 
 void hmb_mesh_free(hmb_mesh* m) { delete m; }
 
+int hmb_pair_rule(int pair_case, int order, int* n, double* xr1, double* xr2, double* yr1,
+                  double* yr2, double* w) {
+  return guard([&] {
+    need(n, "n");
+    const hmb::PairRuleTable r = hmb::singular_pair_rule(pair_case, order);
+    *n = static_cast<int>(r.w.size());
+    if (!w) return;
+    std::copy(r.xr1.begin(), r.xr1.end(), xr1);
+    std::copy(r.xr2.begin(), r.xr2.end(), xr2);
+    std::copy(r.yr1.begin(), r.yr1.end(), yr1);
+    std::copy(r.yr2.begin(), r.yr2.end(), yr2);
+    std::copy(r.w.begin(), r.w.end(), w);
+  });
+}
+
 int hmb_sparse_op(const hmb_mesh* m, int which, int* cols3, double* vals3) {
   return guard([&] {
     need(m, "mesh");

@@ -195,3 +195,50 @@ def test_shards_cover_rows_disjointly():
         assert ranges[0][0] == 0 and ranges[-1][1] == m.num_triangles
         for a, b in zip(ranges, ranges[1:]):
             assert a[1] == b[0] and a[0] < a[1]
+
+
+# ---- Galerkin / operator-algebra host pieces vs the oracle -------
+@pytest.mark.parametrize("case,order", [(1, 7), (2, 7), (3, 9), (2, 5)])
+def test_pair_rules_match_oracle_bitwise(case, order):
+    got, ref = hm.pair_rule(case, order), orc.pair_rule(case, order)
+    for x, y in zip(got, ref):
+        assert (x == y).all()
+
+
+def test_sparse_ops_match_oracle_bitwise():
+    mesh = hm.Mesh.voxel_cube(3, -1.0, 1.0)
+    a = mesh.arrays()
+    for which in range(4):
+        cols, vals = hm.sparse_op(mesh, which)
+        dense = np.zeros((mesh.num_triangles, mesh.num_vertices))
+        for t in range(mesh.num_triangles):
+            for s in range(3):
+                dense[t, cols[t, s]] += vals[t, s]
+        assert (dense == orc.sparse_op(a["vertices"], a["triangles"], which)).all()
+
+
+def test_galerkin_and_kdelta_partitions_bit_exact():
+    mesh = hm.Mesh.icosphere(3)
+    a = mesh.arrays()
+    for which in (0, 1):
+        h = hm.HMatrix.galerkin(mesh, which, b_min=32, eta=1.0, device=-1)
+        o = orc.Problem.galerkin(a["vertices"], a["triangles"], which, b_min=32, eta=1.0)
+        assert h.partition_json() == o.partition_json()
+    h = hm.HMatrix.kdelta(mesh, b_min=32, eta=1.0, device=-1)
+    o = orc.Problem.kdelta(a["vertices"], a["triangles"], b_min=32, eta=1.0)
+    assert h.partition_json() == o.partition_json()
+    assert (h.rows, h.cols) == (mesh.num_triangles, mesh.num_vertices)
+
+
+def test_dof_layout_of_the_experiment_cube():
+    """classify_dofs (mesh.cpp:278-293) on make_cube_mesh's labelling."""
+    mesh = hm.Mesh.voxel_cube(4, -1.0, 1.0)
+    mesh.label_dirichlet("x1>=1|x2<=-1|x3>=1")
+    L = hm.DofLayout(mesh)
+    a = mesh.arrays()
+    d = a["dirichlet"].astype(bool)
+    assert (L.dirichlet_triangle_ids == np.nonzero(d)[0]).all()
+    T = a["triangles"]
+    for v in L.neumann_interior_nodes:
+        assert not d[(T == v).any(axis=1)].any()
+    assert len(L.t_dofs) == 3 * d.sum() and len(L.u_dofs) == 3 * len(L.neumann_interior_nodes)
