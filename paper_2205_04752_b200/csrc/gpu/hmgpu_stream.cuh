@@ -189,6 +189,54 @@ __device__ __forceinline__ void vdots(const double* V, int rl, int nrows, const 
   f2 += (a2[0] + a2[1]) + (a2[2] + a2[3]);
 }
 
+// vdots for the two columns col and col + 32 of one lane in a single sweep
+// over the rows (the x row loads shared); each column's arithmetic is that
+// of vdots (same accumulators, same order).  Used when a chunk has more
+// than 32 columns: one pass instead of two with the second mostly idle.
+template <int NC>
+__device__ __forceinline__ void vdots2(const double* V, int rl, int nrows, const double* xs,
+                                       int col, bool two, double* f) {
+  double a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
+  double b0[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0}, b2[4] = {0, 0, 0, 0};
+  const int col2 = two ? col + 32 : col;
+  int j = 0;
+  for (; j + 3 < nrows; j += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = V[(j + u) * rl + col];
+      const double w = V[(j + u) * rl + col2];
+      const double2 x01 = *reinterpret_cast<const double2*>(xs + 4 * (j + u));
+      a0[u] = fma(v, x01.x, a0[u]);
+      b0[u] = fma(w, x01.x, b0[u]);
+      if (NC == 6) {
+        const double x2 = xs[4 * (j + u) + 2];
+        a1[u] = fma(v, x01.y, a1[u]);
+        a2[u] = fma(v, x2, a2[u]);
+        b1[u] = fma(w, x01.y, b1[u]);
+        b2[u] = fma(w, x2, b2[u]);
+      }
+    }
+  }
+  for (; j < nrows; ++j) {
+    const double v = V[j * rl + col];
+    const double w = V[j * rl + col2];
+    a0[0] = fma(v, xs[4 * j], a0[0]);
+    b0[0] = fma(w, xs[4 * j], b0[0]);
+    if (NC == 6) {
+      a1[0] = fma(v, xs[4 * j + 1], a1[0]);
+      a2[0] = fma(v, xs[4 * j + 2], a2[0]);
+      b1[0] = fma(w, xs[4 * j + 1], b1[0]);
+      b2[0] = fma(w, xs[4 * j + 2], b2[0]);
+    }
+  }
+  f[0] = 0.0 + ((a0[0] + a0[1]) + (a0[2] + a0[3]));
+  f[1] = 0.0 + ((a1[0] + a1[1]) + (a1[2] + a1[3]));
+  f[2] = 0.0 + ((a2[0] + a2[1]) + (a2[2] + a2[3]));
+  f[3] = 0.0 + ((b0[0] + b0[1]) + (b0[2] + b0[3]));
+  f[4] = 0.0 + ((b1[0] + b1[1]) + (b1[2] + b1[3]));
+  f[5] = 0.0 + ((b2[0] + b2[1]) + (b2[2] + b2[3]));
+}
+
 // y rows (lane, lane + 32) += sum_g U[g][i] W[g][:] over columns [0, ncol)
 // of a column-major chunk with m rows
 template <int NC>
@@ -432,13 +480,32 @@ hmv_warp_kernel(WarpStreamParams P) {
       double* W = scratch + 256;
       if (ch.part == 0) {
         const int ncol = ch.g1 - ch.g0;
-        for (int g = lane; g < ncol; g += 32) {
-          double a = 0.0, b = 0.0, c = 0.0;
-          vdots<NC>(data, ncol, job.n, scratch, g, a, b, c);
-          double w[4];
-          weights<NC>(comp_of_col(job.kp, ch.g0 + g), a, b, c, w);
-          *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g)) = make_double2(w[0], w[1]);
-          *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g) + 2) = make_double2(w[2], w[3]);
+        if (ncol > 32 && ncol <= 64) {
+          // one sweep: lane takes columns lane and lane + 32
+          if (lane < ncol) {
+            const bool two = lane + 32 < ncol;
+            double f[6];
+            vdots2<NC>(data, ncol, job.n, scratch, lane, two, f);
+            double w[4];
+            weights<NC>(comp_of_col(job.kp, ch.g0 + lane), f[0], f[1], f[2], w);
+            *reinterpret_cast<double2*>(W + 4 * (ch.g0 + lane)) = make_double2(w[0], w[1]);
+            *reinterpret_cast<double2*>(W + 4 * (ch.g0 + lane) + 2) = make_double2(w[2], w[3]);
+            if (two) {
+              const int g = lane + 32;
+              weights<NC>(comp_of_col(job.kp, ch.g0 + g), f[3], f[4], f[5], w);
+              *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g)) = make_double2(w[0], w[1]);
+              *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g) + 2) = make_double2(w[2], w[3]);
+            }
+          }
+        } else {
+          for (int g = lane; g < ncol; g += 32) {
+            double a = 0.0, b = 0.0, c = 0.0;
+            vdots<NC>(data, ncol, job.n, scratch, g, a, b, c);
+            double w[4];
+            weights<NC>(comp_of_col(job.kp, ch.g0 + g), a, b, c, w);
+            *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g)) = make_double2(w[0], w[1]);
+            *reinterpret_cast<double2*>(W + 4 * (ch.g0 + g) + 2) = make_double2(w[2], w[3]);
+          }
         }
         __syncwarp();
       } else {
