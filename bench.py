@@ -161,6 +161,27 @@ def profile_traffic(config_name):
         return None
 
 
+def profile_pipes(config_name):
+    """fp64-pipe utilisation of the assembly kernels from the committed ncu
+    captures (the north star's counter for kernel evaluation): the ACA
+    kernel and the near-field fill, per config when captured."""
+    out = {}
+    for key, fname in (("aca_fp64_pipe_pct", f"ncu_r01_aca_{config_name}_final.json"),
+                       ("nearfield_fp64_pipe_pct", f"ncu_r01_{config_name}_assembly.json")):
+        try:
+            with open(os.path.join(ROOT, "profiles", fname)) as f:
+                launches = json.load(f)["launches"]
+        except (OSError, ValueError, KeyError):
+            continue
+        want = "aca_kernel" if key.startswith("aca") else "nearfield_kernel"
+        for l in launches:
+            if want in l.get("kernel", ""):
+                out[key] = l.get("fp64_pipe_pct")
+                out[key.replace("pct", "source")] = "profiles/" + fname
+                break
+    return out or None
+
+
 # ---------------------------------------------------------------------------
 def cpu_reference(args, cfg, emit_line: bool):
     """The reference path's CPU implementation (oracle port) on this config:
@@ -535,7 +556,8 @@ def run_ours(args, cfg):
                      "fp64_frac_kernels": best.counted_flops /
                      ((best_kt["aca"] + best_kt["nearfield"]) * 1e-3) / 1e12 / fp64_peak,
                      "nearfield_entries_per_s": best.dense_entries /
-                     (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None},
+                     (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None,
+                     "ncu": profile_pipes(args.config)},
         "kernel_ms": {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kt.items()},
     }
     if args.config == "c4" and world == 1:
