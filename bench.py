@@ -384,10 +384,11 @@ def run_ours(args, cfg):
     h = hm.HMatrix.kelvin(mesh, E=1.0, nu=0.3, b_min=cfg["b_min"], eta=cfg["eta"],
                           device=device, shard=(rank, world))
     n = h.cols
-    # ---- assembly (timed on the device, best of 2 after one warm-up) ----
+    # ---- assembly (timed on the device, best of 3 after one warm-up; the
+    # first assemblies of a process also map the factor arenas) ----
     asm = []
     h.set_profiling(True)
-    for _ in range(3):
+    for _ in range(4):
         for k in ("aca", "nearfield", "compact", "relocate"):
             h.kernel_times(k, reset=True)
         st = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
