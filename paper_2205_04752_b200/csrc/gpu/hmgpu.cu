@@ -446,6 +446,11 @@ struct hmgpu_ctx {
   // ---- device-resident AMVM estimator (hmgpu_amvm.cuh) ----
   bool am_geom_valid = false;
   // transposed matvec tables (column leaves), built on first use
+  // parallel marking walk: chunk buffers (hmgpu_amvm_mark)
+  DBuf<unsigned long long> w_keys, w_skeys;
+  DBuf<int> w_slots, w_sslots;
+  DBuf<long long> w_gslot;
+  DBuf<double> w_rb, w_dots;
   bool t_valid = false;
   int t_nleaves = 0;
   long long t_rows = 0;
@@ -516,6 +521,11 @@ struct hmgpu_ctx {
     d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
     d_resid.free(); d_nsq.free(); d_sc.free(); d_keys.free(); d_keys2.free();
     d_inset.free(); d_cub.free(); d_eptr.free(); d_eidx.free(); d_eval.free(); d_ecnt.free();
+    d_prule.free(); d_vtx.free(); d_tvid.free(); d_tvx.free(); d_tce.free(); d_tna.free();
+    d_vtptr.free(); d_vttri.free(); d_tprow.free(); d_tleaf_prow.free(); d_tleaf_begin.free();
+    d_tleaf_end.free(); d_tleaf_ptr.free(); d_tpart.free(); d_xr.free();
+    w_keys.free(); w_skeys.free(); w_slots.free(); w_sslots.free(); w_gslot.free();
+    w_rb.free(); w_dots.free();
     if (stream) cudaStreamSynchronize(stream);
     if (pool) {
       std::lock_guard<std::mutex> lk(g_pools_mu);
@@ -2732,11 +2742,35 @@ void parallel_walk(hmgpu_ctx* c, double theta, long long M, int nt) {
     while ((1LL << row_bits) <= M) ++row_bits;
     const long long kEmax = 1LL << 24;
     const int kTmax = 1 << 20;
-    DBuf<unsigned long long> keys, skeys;
-    DBuf<int> slots, sslots;
-    DBuf<long long> gslot;
-    DBuf<double> rb, dots, st;
+    // chunk buffers live in the context (sized once for the largest chunk:
+    // re-growing the pool on every sweep cost up to 0.3 s)
+    DBuf<unsigned long long>& keys = c->w_keys;
+    DBuf<unsigned long long>& skeys = c->w_skeys;
+    DBuf<int>& slots = c->w_slots;
+    DBuf<int>& sslots = c->w_sslots;
+    DBuf<long long>& gslot = c->w_gslot;
+    DBuf<double>& rb = c->w_rb;
+    DBuf<double>& dots = c->w_dots;
+    DBuf<double> st;
     st.alloc(2);
+    {
+      const long long emax = std::min<long long>(hcum[L], kEmax);
+      long long e1max = 0;
+      for (int a = 0, b = 0; a < L; a = b) {  // the largest chunk of this walk
+        b = a + 1;
+        while (b < L && b - a < kTmax && hcum[b + 1] - hcum[a] <= kEmax) ++b;
+        e1max = std::max(e1max, hcum[b] - hcum[a]);
+        if (e1max >= emax) break;
+      }
+      const size_t need = (size_t)std::max(e1max, 1LL);
+      keys.ensure(need);
+      skeys.ensure(need);
+      slots.ensure(need);
+      sslots.ensure(need);
+      gslot.ensure(need);
+      rb.ensure(need);
+      dots.ensure((size_t)std::min(L, kTmax) + 1);
+    }
     CK(cudaMemcpyAsync(st.p, c->d_sc.p, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     int k0 = 0;
     bool stopped = false;
@@ -2766,8 +2800,9 @@ void parallel_walk(hmgpu_ctx* c, double theta, long long M, int nt) {
                                                        c->d_eval.p, c->d_resid.p, rb.p);
         walk_dot_kernel<<<(nk + 127) / 128, 128, 0, c->stream>>>(k0, k1, cumE.p, gslot.p,
                                                                  c->d_eval.p, rb.p, dots.p);
-        walk_scan_kernel<<<1, 1, 0, c->stream>>>(tS.p, k0, k1, c->d_nsq.p, dots.p, target_sq,
-                                                 st.p);
+        walk_incr_kernel<<<(nk + 255) / 256, 256, 0, c->stream>>>(tS.p, k0, k1, c->d_nsq.p,
+                                                                  dots.p);
+        walk_scan_kernel<<<1, 1, 0, c->stream>>>(dots.p, nk, target_sq, st.p);
         walk_apply_kernel<<<ge, 256, 0, c->stream>>>(skeys.p, sslots.p, E, gslot.p,
                                                       c->d_eval.p, rb.p, st.p, nk,
                                                       c->d_resid.p);
@@ -2786,8 +2821,7 @@ void parallel_walk(hmgpu_ctx* c, double theta, long long M, int nt) {
     }
     CK(cudaMemcpyAsync(c->d_marked.p, tS.p, (size_t)nm * sizeof(int), cudaMemcpyDeviceToDevice,
                        c->stream));
-    keys.free(); skeys.free(); slots.free(); sslots.free(); gslot.free(); rb.free();
-    dots.free(); st.free(); sz.free(); cumE.free();
+    st.free(); sz.free(); cumE.free();
   }
   CK(cudaMemcpyAsync(c->d_nm.p, &nm, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   // gamma(P_k): exact recomputation over the residual (amvm.cpp:181)

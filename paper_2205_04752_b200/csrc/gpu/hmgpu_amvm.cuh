@@ -509,18 +509,35 @@ __global__ void walk_dot_kernel(int k0, int k1, const long long* __restrict__ cu
 }
 // (4): the sequential res_sq scan; st[0] = res_sq (in/out), st[1] = stop
 // rank within the chunk or -1
-__global__ void walk_scan_kernel(const int* __restrict__ tS, int k0, int k1,
-                                 const double* __restrict__ nsq, const double* __restrict__ dots,
-                                 double target_sq, double* __restrict__ st) {
+// the chunk's |term|^2 - 2 dot in S order, contiguous (parallel)
+__global__ void walk_incr_kernel(const int* __restrict__ tS, int k0, int k1,
+                                 const double* __restrict__ nsq, double* __restrict__ dots) {
+  const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  dots[k - k0] = nsq[tS[k]] - 2.0 * dots[k - k0];
+}
+__global__ void walk_scan_kernel(const double* __restrict__ incr, int n, double target_sq,
+                                 double* __restrict__ st) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   double res = st[0];
   int stop = -1;
-  for (int k = k0; k < k1; ++k) {
-    res += nsq[tS[k]] - 2.0 * dots[k - k0];
-    if (res <= target_sq) {
-      stop = k - k0;
-      break;
+  int k = 0;
+  // the increments are loaded 16 at a time ahead of the dependent adds
+  for (; k + 16 <= n && stop < 0; k += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = incr[k + u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (stop < 0) {
+        res += v[u];
+        if (res <= target_sq) stop = k + u;
+      }
     }
+  }
+  for (; k < n && stop < 0; ++k) {
+    res += incr[k];
+    if (res <= target_sq) stop = k;
   }
   st[0] = res;
   st[1] = (double)stop;
