@@ -844,6 +844,29 @@ void download_items(hmgpu_ctx* c) {
   c->sync();
 }
 
+// refreshes the host mirror of the items in `ids` only
+void download_items_subset(hmgpu_ctx* c, const std::vector<int>& ids) {
+  if (ids.empty()) return;
+  if (ids.size() * 4 > c->items.size()) {
+    download_items(c);
+    return;
+  }
+  DBuf<int> d_ids;
+  DBuf<Item> d_out;
+  d_ids.upload(ids, c->stream);
+  d_out.alloc(ids.size());
+  gather_items_kernel<<<(int)((ids.size() + 255) / 256), 256, 0, c->stream>>>(
+      c->d_items.p, d_ids.p, (int)ids.size(), d_out.p);
+  CK(cudaGetLastError());
+  std::vector<Item> h(ids.size());
+  CK(cudaMemcpyAsync(h.data(), d_out.p, ids.size() * sizeof(Item), cudaMemcpyDeviceToHost,
+                     c->stream));
+  c->sync();
+  for (size_t t = 0; t < ids.size(); ++t) c->items[ids[t]] = h[t];
+  d_ids.free();
+  d_out.free();
+}
+
 // moves `ids` to fresh storage at the arena end with `caps` columns
 void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>& caps) {
   if (ids.empty()) return;
@@ -921,7 +944,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
     c->sync();
     if (over == 0) break;
     ++passes;
-    download_items(c);
+    download_items_subset(c, list);
     std::vector<int> ids, caps;
     for (int idx : list) {
       const Item& it = c->items[idx];
@@ -2520,7 +2543,7 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
     return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
   });
   run_aca(c, ids, nullptr, [&](int idx) { return c->items[idx].m + c->items[idx].n; });
-  download_items(c);
+  download_items_subset(c, ids);
   refresh_matvec_ranks(c);
   c->plan_valid = false;
   c->p16_valid = false;
@@ -2610,59 +2633,83 @@ int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* di
     if (!x || !gamma) fail(HMGPU_ERR_INVALID, "null x / gamma");
     if (c->row_begin != 0 || c->row_end != c->n_rows)
       fail(HMGPU_ERR_INVALID, "the estimator needs the whole operator (no shard)");
+    auto wall0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+      if (!verbose()) return;
+      c->sync();
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[hmgpu] est  %-10s %9.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - wall0).count());
+      wall0 = now;
+    };
     build_amvm_geometry(c);
+    phase("geometry");
     // terms: (comp, block) with a look-ahead tail, component-major, blocks
-    // ascending (amvm.cpp:135-150)
-    std::vector<TailTerm> terms;
-    std::vector<int> term_bi;
-    std::vector<int> tix(c->items.size(), -1);
-    for (int q = 0; q < c->NC; ++q)
-      for (int bi = 0; bi < c->n_mv; ++bi) {
-        const MvBlock& mb = c->mvb[bi];
-        if (mb.dense) continue;
-        const Item& it = c->items[mb.item0 + q];
-        if (it.k <= it.kcur) continue;
-        const int nocc = (c->NC == 6 && c_comp_host_r(q) != c_comp_host_c(q)) ? 2 : 1;
-        tix[mb.item0 + q] = (int)terms.size();
-        terms.push_back({mb.item0 + q, nocc, 0});
-        term_bi.push_back(bi);
-      }
+    // ascending (amvm.cpp:135-150) -- generated on the device (flags, two
+    // CUB scans for the term index and the value offset)
+    const int nslot = c->NC * c->n_mv;
     long long off = 0;
-    for (TailTerm& t : terms) {
-      t.off = off;
-      off += (long long)t.nocc * c->items[t.item].m;
+    int nterms = 0;
+    {
+      DBuf<int> flag, pos;
+      DBuf<long long> size, offs;
+      flag.alloc(nslot + 1);
+      pos.alloc(nslot + 1);
+      size.alloc(nslot + 1);
+      offs.alloc(nslot + 1);
+      CK(cudaMemsetAsync(flag.p + nslot, 0, sizeof(int), c->stream));
+      CK(cudaMemsetAsync(size.p + nslot, 0, sizeof(long long), c->stream));
+      if (nslot > 0)
+        amvm_term_flags_kernel<<<(nslot + 255) / 256, 256, 0, c->stream>>>(
+            c->d_mvb.p, c->n_mv, c->NC, c->d_items.p, flag.p, size.p);
+      size_t t1 = 0, t2 = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, t1, flag.p, pos.p, nslot + 1, c->stream));
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, size.p, offs.p, nslot + 1, c->stream));
+      c->d_cub.ensure(std::max(t1, t2));
+      CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, t1, flag.p, pos.p, nslot + 1, c->stream));
+      CK(cub::DeviceScan::ExclusiveSum(c->d_cub.p, t2, size.p, offs.p, nslot + 1, c->stream));
+      CK(cudaMemcpyAsync(&nterms, pos.p + nslot, sizeof(int), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaMemcpyAsync(&off, offs.p + nslot, sizeof(long long), cudaMemcpyDeviceToHost,
+                         c->stream));
+      c->sync();
+      c->d_aterms.ensure((size_t)std::max(nterms, 1));
+      c->d_term_bi.ensure((size_t)std::max(nterms, 1));
+      c->d_tix.ensure(std::max<size_t>(c->items.size(), 1));
+      CK(cudaMemsetAsync(c->d_tix.p, 0xff, std::max<size_t>(c->items.size(), 1) * sizeof(int),
+                         c->stream));
+      if (nterms > 0)
+        amvm_term_write_kernel<<<(nslot + 255) / 256, 256, 0, c->stream>>>(
+            c->d_mvb.p, c->n_mv, c->NC, flag.p, pos.p, offs.p, c->d_aterms.p, c->d_term_bi.p,
+            c->d_tix.p);
+      CK(cudaGetLastError());
+      flag.free();
+      pos.free();
+      size.free();
+      offs.free();
     }
-    c->am_nterms = (int)terms.size();
+    c->am_nterms = nterms;
     c->am_nvals = off;
     const long long M = (long long)c->ndof_rows();
     c->d_diff.ensure((size_t)M);
     c->d_sc.ensure(8);
-    if (terms.empty()) {
-      c->d_aterms.ensure(1);
-      c->d_term_bi.ensure(1);
-    } else {
-      c->d_aterms.upload(terms, c->stream);
-      c->d_term_bi.upload(term_bi, c->stream);
-    }
-    if (tix.empty()) c->d_tix.ensure(1);
-    else c->d_tix.upload(tix, c->stream);
     c->d_aout.ensure((size_t)std::max<long long>(off, 1));
     const long long nx = c->ndof_cols();
     c->d_x.ensure((size_t)nx);
     CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     gather_x(c, c->d_x.p, 1);
-    if (!terms.empty())
+    phase("terms");
+    if (nterms > 0)
       c->timed("tail", [&] {
-        const int grid = grid_for(c, ((long long)terms.size() + 7) / 8, 8);
+        const int grid = grid_for(c, ((long long)nterms + 7) / 8, 8);
         if (c->NC == 6)
-          tail_kernel<3><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, (int)terms.size(),
-                                                     c->d_items.p, c->d_arena.p, c->d_xi.p,
-                                                     c->d_aout.p, 1);
+          tail_kernel<3><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, nterms, c->d_items.p,
+                                                     c->d_arena.p, c->d_xi.p, c->d_aout.p, 1);
         else
-          tail_kernel<1><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, (int)terms.size(),
-                                                     c->d_items.p, c->d_arena.p, c->d_xi.p,
-                                                     c->d_aout.p, 0);
+          tail_kernel<1><<<grid, 256, 0, c->stream>>>(c->d_aterms.p, nterms, c->d_items.p,
+                                                     c->d_arena.p, c->d_xi.p, c->d_aout.p, 0);
       });
+    phase("tail");
     const AmvmGeom a = amvm_geom(c);
     c->timed("amvm_diff", [&] {
       amvm_diff_kernel<<<(c->n_rows + 127) / 128, 128, 0, c->stream>>>(a, c->d_diff.p);
@@ -2675,6 +2722,7 @@ int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* di
       CK(cudaMemcpyAsync(difference, c->d_diff.p, M * sizeof(double), cudaMemcpyDeviceToHost,
                          c->stream));
     c->sync();
+    phase("diff+dl");
     *gamma = sc[1];
     c->am_have_estimate = true;
   });

@@ -77,6 +77,44 @@ __device__ __forceinline__ void amvm_row_terms(const AmvmGeom& a, int rb, int p,
   }
 }
 
+// the estimator's terms on the device: every (comp, block) with a
+// look-ahead tail, component-major, blocks ascending (amvm.cpp:135-150)
+__global__ void amvm_term_flags_kernel(const MvBlock* __restrict__ mvb, int n_mv, int nc,
+                                       const Item* __restrict__ items, int* __restrict__ flag,
+                                       long long* __restrict__ size) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * n_mv) return;
+  const int q = t / n_mv, bi = t - q * n_mv;
+  const MvBlock mb = mvb[bi];
+  int f = 0;
+  long long sz = 0;
+  if (!mb.dense) {
+    const Item& it = items[mb.item0 + q];
+    if (it.k > it.kcur) {
+      f = 1;
+      const int nocc = (nc == 6 && c_comp_r[q] != c_comp_c[q]) ? 2 : 1;
+      sz = (long long)nocc * it.m;
+    }
+  }
+  flag[t] = f;
+  size[t] = sz;
+}
+__global__ void amvm_term_write_kernel(const MvBlock* __restrict__ mvb, int n_mv, int nc,
+                                       const int* __restrict__ flag,
+                                       const int* __restrict__ pos,
+                                       const long long* __restrict__ off,
+                                       TailTerm* __restrict__ terms, int* __restrict__ term_bi,
+                                       int* __restrict__ tix) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * n_mv || !flag[t]) return;
+  const int q = t / n_mv, bi = t - q * n_mv;
+  const int item = mvb[bi].item0 + q;
+  const int k = pos[t];
+  terms[k] = TailTerm{item, (nc == 6 && c_comp_r[q] != c_comp_c[q]) ? 2 : 1, off[t]};
+  term_bi[k] = bi;
+  tix[item] = k;
+}
+
 __global__ void amvm_diff_kernel(AmvmGeom a, double* __restrict__ diff) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= a.N) return;

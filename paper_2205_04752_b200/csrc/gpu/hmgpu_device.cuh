@@ -1802,6 +1802,14 @@ __global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, 
 }
 
 // ---------------------------------------------------------------------------
+// a subset of the item table (partial host-mirror refresh)
+__global__ void gather_items_kernel(const Item* __restrict__ items, const int* __restrict__ ids,
+                                    int n, Item* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = items[ids[t]];
+}
+
+// ---------------------------------------------------------------------------
 // small state kernels
 __global__ void promote_kernel(Item* items, const int* idx, int n) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
