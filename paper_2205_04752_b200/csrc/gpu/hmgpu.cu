@@ -1263,14 +1263,6 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       lists[l].push_back(LeafEntry{slot + (lo - r_lo), lo - lb, hi - lb});
     }
   };
-  // packs rows x cols of a column-major source into the arena; returns the offset
-  auto pack = [&](long long src, int ld, int rows, int cols, int trans) {
-    const long long off = alen;
-    if (rows > 0 && cols > 0)
-      packs.push_back(PackDesc{src, alen, ld, trans ? cols : rows, rows, cols, trans, 0});
-    alen += align2((long long)rows * cols);
-    return off;
-  };
   auto chunk = [](long long src, int len, int src_kind, int aux_kind, long long aux,
                   int aux_len, int g0, int g1, int part) {
     WChunk ch{};
@@ -1367,30 +1359,37 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       ca.add(chs);
       continue;
     }
-    // split block: VSPLIT column groups of each component -> W (global)
+    // split block: VSPLIT groups of <= 64 consecutive columns of the K
+    // (component-major, balanced) -> W (global, the same slot order)
     const long long wbase = wslots;
     wslots += K;
-    for (int q = 0; q < NC; ++q) {
-      const Item& it = c->items[mb.item0 + q];
-      for (int l0 = 0; l0 < k[q]; l0 += 32) {
-        const int nc = std::min(32, k[q] - l0);
-        const int rpc = std::max(1, kStageData / (nc + 4));
-        WJob j{};
-        j.kind = WJ_VSPLIT;
-        j.n = n;
-        j.ncols = nc;
-        j.comp = q;
-        j.out = wbase + kp[q] + l0;
-        chs.clear();
-        for (int r0 = 0; r0 < n; r0 += rpc) {
-          const int r1 = std::min(n, r0 + rpc);
-          const long long off =
-              pack(it.v_off + r0 + (long long)l0 * n, n, r1 - r0, nc, 1);  // row-major
-          chs.push_back(chunk(off, (r1 - r0) * nc, 0, WA_X, mb.col0 + r0, r1 - r0, r0, r1, 0));
+    const int ngr = (K + 63) / 64, per = (K + ngr - 1) / ngr;
+    for (int g0 = 0; g0 < K; g0 += per) {
+      const int g1 = std::min(K, g0 + per), nc = g1 - g0;
+      const int rpc = std::max(1, kStageData / (nc + 4));
+      WJob j{};
+      j.kind = WJ_VSPLIT;
+      j.n = n;
+      j.ncols = nc;
+      j.comp = g0;
+      std::copy(kp, kp + 8, j.kp);
+      j.out = wbase + g0;
+      chs.clear();
+      for (int r0 = 0; r0 < n; r0 += rpc) {
+        const int r1 = std::min(n, r0 + rpc);
+        const long long off = alen;  // row-major [j][g] tile, per component piece
+        for (int q = 0; q < NC; ++q) {
+          const int a = std::max(g0, kp[q]), b = std::min(g1, kp[q + 1]);
+          if (a >= b) continue;
+          packs.push_back(PackDesc{c->items[mb.item0 + q].v_off + r0 +
+                                       (long long)(a - kp[q]) * n,
+                                   off + (a - g0), n, nc, r1 - r0, b - a, 1, 0});
         }
-        ja.push_back(j);
-        ca.add(chs);
+        alen += align2((long long)(r1 - r0) * nc);
+        chs.push_back(chunk(off, (r1 - r0) * nc, 0, WA_X, mb.col0 + r0, r1 - r0, r0, r1, 0));
       }
+      ja.push_back(j);
+      ca.add(chs);
     }
     // USPLIT row tiles over component groups whose W fits the warp scratch
     for (int q0 = 0; q0 < NC;) {

@@ -13,7 +13,9 @@
 //          per column the three dot products f_s = V_g . x_s give the
 //          weights W[g][r] = (R==r) f_C + (C==r, R!=C) f_R; U part packed
 //          column-major [g][i] (lane = row i): y_r += U[i,g] W[g][r]
-//   VSPLIT up to 32 columns of one component of a large block, all rows
+//   VSPLIT up to 64 consecutive columns of the K = sum k_c columns of a
+//          large block (across components, packed row-major [j][g] like
+//          FUSED; lane = column, a second column at lane + 32), all rows
 //          streamed in row chunks (x rows with each chunk); W to global
 //   USPLIT a <= 64-row tile of all components' U of a large block; W of
 //          the block from global with the first chunk
@@ -40,7 +42,7 @@ struct __align__(16) WJob {
   int n;           // FUSED/DENSE: block columns; VSPLIT: rows of V
   int ncols;       // FUSED/USPLIT: K = sum k_c; VSPLIT: columns (<= 32); DENSE: n
   int chunk0, nchunks;
-  int comp;        // VSPLIT: component of its columns
+  int comp;        // VSPLIT: first column (of the block's K) of the job
   int pad0;
   long long out;   // FUSED/USPLIT/DENSE: partial row slot; VSPLIT: W slot of column 0
   int kp[8];       // FUSED/USPLIT: component prefix sums of the K columns
@@ -457,8 +459,8 @@ hmv_warp_kernel(WarpStreamParams P) {
   };
   for (int s = 0; s < NS; ++s) issue(s, s);
 
-  double y[6] = {0, 0, 0, 0, 0, 0};     // rows lane, lane+32 x 3 outputs
-  double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // VSPLIT dot products
+  // rows lane, lane+32 x 3 outputs; VSPLIT: f_s of columns lane, lane+32
+  double y[6] = {0, 0, 0, 0, 0, 0};
   for (int consumed = 0; consumed < nch; ++consumed) {
     const int s = consumed % NS;
     mbar_wait(&bar[s], (uint32_t)((consumed / NS) & 1));
@@ -520,20 +522,34 @@ hmv_warp_kernel(WarpStreamParams P) {
       drows<NC>(data, job.m, cp, ch.g1 - ch.g0, scratch + 4 * ch.g0, lane, y);
       last = ch.g1 == job.n;
     } else {  // WJ_VSPLIT: rows [g0, g1) of V for this job's columns
-      if (lane < job.ncols) vdots<NC>(data, job.ncols, ch.g1 - ch.g0, aux, lane, f0, f1, f2);
+      const int ncol = job.ncols;
+      if (ncol > 32) {
+        double f[6];
+        vdots2<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, lane + 32 < ncol, f);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) y[r] += f[r];
+      } else if (lane < ncol) {
+        vdots<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, y[0], y[1], y[2]);
+      }
       last = ch.g1 == job.n;
     }
     // job epilogue (descriptor fields read before the stage is recycled)
     if (last) {
       if (kind == WJ_VSPLIT) {
-        if (lane < job.ncols) {
-          double w[4];
-          weights<NC>(job.comp, f0, f1, f2, w);
-          double* o = P.wout + (job.out + lane) * 4;
-          *reinterpret_cast<double2*>(o) = make_double2(w[0], w[1]);
-          *reinterpret_cast<double2*>(o + 2) = make_double2(w[2], w[3]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = lane + 32 * h;
+          if (l < job.ncols) {
+            double w[4];
+            weights<NC>(comp_of_col(job.kp, job.comp + l), y[3 * h], y[3 * h + 1],
+                        y[3 * h + 2], w);
+            double* o = P.wout + (job.out + l) * 4;
+            *reinterpret_cast<double2*>(o) = make_double2(w[0], w[1]);
+            *reinterpret_cast<double2*>(o + 2) = make_double2(w[2], w[3]);
+          }
         }
-        f0 = f1 = f2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) y[r] = 0.0;
       } else {
         double* yo = P.ypart + job.out * NOUT;
         if (lane < job.m)
