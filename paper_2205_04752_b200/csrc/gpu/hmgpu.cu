@@ -1684,11 +1684,11 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     const int nl = (int)c->leaf_begin.size();
     const int g = grid_for(c, nl, 16);
     if (NOUT == 3)
-      hmv_leaf_reduce_kernel<3><<<g, 128, 0, c->stream>>>(
+      hmv_leaf_reduce_kernel<3><<<g, LR_THREADS, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
           c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
     else
-      hmv_leaf_reduce_kernel<1><<<g, 128, 0, c->stream>>>(
+      hmv_leaf_reduce_kernel<1><<<g, LR_THREADS, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
           c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
   });

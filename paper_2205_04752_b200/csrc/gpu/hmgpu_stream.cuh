@@ -566,58 +566,36 @@ hmv_warp_kernel(WarpStreamParams P) {
 }
 
 // per leaf: y(p) = sum over covering job rows (fixed order).  The leaf's
-// entries are staged in shared memory once; each thread sums its (row, r)
-// over them with eight independent partial-row loads in flight.
+// entries are staged in shared memory; its (row, r) pairs are padded to a
+// power of two P2 and the CTA's LR_THREADS / P2 thread groups take the
+// entries round-robin (group h: entries h, h + G, ...; 8 partial-row loads
+// in flight per thread), then the group partials are added in group order
+// (deterministic).  The critical path is the entry count of the fullest
+// leaf divided by G.  Leaves wider than LR_THREADS pairs: one thread per pair.
+#ifndef HMV_LR_THREADS
+#define HMV_LR_THREADS 256
+#endif
+#ifndef HMV_LR_UNROLL
+#define HMV_LR_UNROLL 8
+#endif
+constexpr int LR_THREADS = HMV_LR_THREADS;
 template <int NOUT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(LR_THREADS)
 hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin, const int* __restrict__ leaf_end,
                        const int* __restrict__ leaf_ptr,
                        const LeafEntry* __restrict__ entries, int nleaves,
                        const double* __restrict__ ypart, const int* __restrict__ rperm,
                        int nrows, double* __restrict__ y) {
-  constexpr int EC = 256;  // entries staged per round
+  constexpr int EC = 512;  // entries staged per round
+  constexpr int U = HMV_LR_UNROLL;
   __shared__ LeafEntry se[EC];
+  __shared__ double red[LR_THREADS];
   for (int L = blockIdx.x; L < nleaves; L += gridDim.x) {
     const int b0 = leaf_begin[L], b1 = leaf_end[L];
     const int e0 = leaf_ptr[L], e1 = leaf_ptr[L + 1];
     const int cnt = (b1 - b0) * NOUT;
-    double acc[2] = {0.0, 0.0};  // threads cover up to 256 (row, r) pairs per leaf
-    for (int c0 = e0; c0 < e1; c0 += EC) {
-      const int ne = min(EC, e1 - c0);
-      __syncthreads();
-      for (int q = threadIdx.x; q < ne; q += blockDim.x) se[q] = entries[c0 + q];
-      __syncthreads();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int t = threadIdx.x + h * blockDim.x;
-        if (t >= cnt) continue;
-        const int r = t % NOUT, i = t / NOUT;
-        double s = acc[h];
-        int e = 0;
-        for (; e + 8 <= ne; e += 8) {
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const LeafEntry en = se[e + u];
-            v[u] = (i >= en.lo && i < en.hi) ? ypart[(en.slot + (i - en.lo)) * NOUT + r] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s += v[u];
-        }
-        for (; e < ne; ++e) {
-          const LeafEntry en = se[e];
-          if (i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
-        }
-        acc[h] = s;
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int t = threadIdx.x + h * blockDim.x;
-      if (t < cnt) y[(long long)(t % NOUT) * nrows + rperm[b0 + t / NOUT]] = acc[h];
-    }
-    if (cnt > 2 * (int)blockDim.x) {  // leaves wider than 256 (row, r) pairs
-      for (int t = 2 * blockDim.x + threadIdx.x; t < cnt; t += blockDim.x) {
+    if (cnt > LR_THREADS) {
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
         const int r = t % NOUT, i = t / NOUT;
         double s = 0.0;
         for (int e = e0; e < e1; ++e) {
@@ -626,7 +604,46 @@ hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin, const int* __restrict
         }
         y[(long long)r * nrows + rperm[b0 + i]] = s;
       }
+      continue;
     }
+    int P2 = 1;
+    while (P2 < cnt) P2 <<= 1;
+    const int G = LR_THREADS / P2;
+    const int p = threadIdx.x & (P2 - 1), h = threadIdx.x / P2;
+    const bool act = p < cnt;
+    const int r = p % NOUT, i = p / NOUT;
+    double s = 0.0;
+    for (int c0 = e0; c0 < e1; c0 += EC) {
+      const int ne = min(EC, e1 - c0);
+      __syncthreads();
+      for (int q = threadIdx.x; q < ne; q += blockDim.x) se[q] = entries[c0 + q];
+      __syncthreads();
+      int e = h;
+      for (; e + (U - 1) * G < ne; e += U * G) {
+        double v[U];
+        bool in[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // unconditional loads (clamped index): U in flight
+          const LeafEntry en = se[e + u * G];
+          in[u] = act && i >= en.lo && i < en.hi;
+          v[u] = __ldg(ypart + (in[u] ? (en.slot + (i - en.lo)) * NOUT + r : 0));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += in[u] ? v[u] : 0.0;
+      }
+      for (; e < ne; e += G) {
+        const LeafEntry en = se[e];
+        if (act && i >= en.lo && i < en.hi) s += ypart[(en.slot + (i - en.lo)) * NOUT + r];
+      }
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      double acc = red[threadIdx.x];
+      for (int g = 1; g < G; ++g) acc += red[g * P2 + threadIdx.x];
+      y[(long long)r * nrows + rperm[b0 + i]] = acc;
+    }
+    __syncthreads();
   }
 }
 
