@@ -1213,6 +1213,15 @@ MvCfg mv_cfg(int pass) {
   return pass == 0 ? a : b;
 }
 
+// HMGPU_MV_VROWS=0: FUSED V parts in column chunks only (A/B switch)
+bool vrows_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("HMGPU_MV_VROWS");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
   auto tp0 = std::chrono::steady_clock::now();
@@ -1322,9 +1331,28 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.out = slots;
       std::copy(kp, kp + 8, j.kp);
       chs.clear();
-      // V part: row-major [j][g] chunks over whole columns, x rides along
+      // V part, K <= 64: row chunks over all K columns (row-major [j][g]),
+      // x rows with each chunk -- every lane busy (two columns per lane
+      // above 32) instead of column chunks of the stage width
+      if (K <= 64 && !vrows_off()) {
+        j.vrows = 1;
+        const int rpc = std::max(1, kStageData / (K + 4));
+        for (int r0 = 0; r0 < n; r0 += rpc) {
+          const int r1 = std::min(n, r0 + rpc);
+          const long long off = alen;
+          for (int q = 0; q < NC; ++q) {
+            const int a = kp[q], b = kp[q + 1];
+            if (a >= b) continue;
+            packs.push_back(PackDesc{c->items[mb.item0 + q].v_off + r0, off + a, n, K, r1 - r0,
+                                     b - a, 1, 0});
+          }
+          alen += align2((long long)(r1 - r0) * K);
+          chs.push_back(chunk(off, (r1 - r0) * K, 0, WA_X, mb.col0 + r0, r1 - r0, r0, r1, 0));
+        }
+      }
+      // V part, K > 64: row-major [j][g] chunks over whole columns, x rides along
       const int vcpc = std::max(1, (kStageData - 4 * n) / n);
-      for (int g0 = 0; g0 < K; g0 += vcpc) {
+      for (int g0 = 0; g0 < K && !j.vrows; g0 += vcpc) {
         const int g1 = std::min(K, g0 + vcpc);
         // the chunk's columns may span components: pack per component piece
         const long long off = alen;

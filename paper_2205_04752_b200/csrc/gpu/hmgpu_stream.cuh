@@ -43,7 +43,7 @@ struct __align__(16) WJob {
   int ncols;       // FUSED/USPLIT: K = sum k_c; VSPLIT: columns (<= 32); DENSE: n
   int chunk0, nchunks;
   int comp;        // VSPLIT: first column (of the block's K) of the job
-  int pad0;
+  int vrows;       // FUSED: V part streamed in row chunks (K <= 64), x with each
   long long out;   // FUSED/USPLIT/DENSE: partial row slot; VSPLIT: W slot of column 0
   int kp[8];       // FUSED/USPLIT: component prefix sums of the K columns
 };
@@ -470,7 +470,7 @@ hmv_warp_kernel(WarpStreamParams P) {
     const double* data = st + kHdr;
     const double* aux = data + ch.len;
     const int kind = job.kind;
-    const bool first = ch.part == 0 && ch.g0 == 0 && kind != WJ_VSPLIT
+    const bool first = ch.part == 0 && ch.g0 == 0 && kind != WJ_VSPLIT && !job.vrows
                            ? true
                            : (kind == WJ_USPLIT && ch.g0 == 0);
     if (first) {  // keep the job's x / W for its later chunks
@@ -480,7 +480,34 @@ hmv_warp_kernel(WarpStreamParams P) {
     bool last;
     if (kind == WJ_FUSED) {
       double* W = scratch + 256;
-      if (ch.part == 0) {
+      if (ch.part == 0 && job.vrows) {
+        // rows [g0, g1) of V over all K <= 64 columns (as VSPLIT); f_s of
+        // columns lane, lane + 32 in y until the last row chunk gives W
+        const int ncol = job.ncols;
+        if (ncol > 32) {
+          double f[6];
+          vdots2<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, lane + 32 < ncol, f);
+#pragma unroll
+          for (int r = 0; r < 6; ++r) y[r] += f[r];
+        } else if (lane < ncol) {
+          vdots<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, y[0], y[1], y[2]);
+        }
+        if (ch.g1 == job.n) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int l = lane + 32 * h;
+            if (l < ncol) {
+              double w[4];
+              weights<NC>(comp_of_col(job.kp, l), y[3 * h], y[3 * h + 1], y[3 * h + 2], w);
+              *reinterpret_cast<double2*>(W + 4 * l) = make_double2(w[0], w[1]);
+              *reinterpret_cast<double2*>(W + 4 * l + 2) = make_double2(w[2], w[3]);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 6; ++r) y[r] = 0.0;
+          __syncwarp();
+        }
+      } else if (ch.part == 0) {
         const int ncol = ch.g1 - ch.g0;
         if (ncol > 32 && ncol <= 64) {
           // one sweep: lane takes columns lane and lane + 32
