@@ -1222,6 +1222,24 @@ bool vrows_off() {
   return off;
 }
 
+// streamed bytes (doubles) per chain unit of the matvec plan; 0 = automatic
+// (HMGPU_MV_UNIT overrides, for tuning)
+// HMGPU_MV_LAYOUT: 0 automatic, 1 contiguous runs, 2 round-robin units
+int mv_layout() {
+  static const int v = [] {
+    const char* e = std::getenv("HMGPU_MV_LAYOUT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+long long mv_unit_cap() {
+  static const long long v = [] {
+    const char* e = std::getenv("HMGPU_MV_UNIT");
+    return e ? std::max(0LL, std::atoll(e)) : 0LL;
+  }();
+  return v;
+}
+
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
   auto tp0 = std::chrono::steady_clock::now();
@@ -1298,15 +1316,13 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.m = m;
       j.n = n;
       j.ncols = n;
-      j.out = slots;
+      j.row0 = mb.row0;
       chs.clear();
       for (int g0 = 0; g0 < n; g0 += cpc) {
         const int g1 = std::min(n, g0 + cpc);
         chs.push_back(chunk(mb.dense_off + (long long)g0 * cp, (g1 - g0) * cp, 1,
                             g0 == 0 ? WA_X : WA_NONE, mb.col0, g0 == 0 ? n : 0, g0, g1, 0));
       }
-      add_rows(mb.row0, m, slots);
-      slots += m;
       ja.push_back(j);
       ca.add(chs);
       continue;
@@ -1328,7 +1344,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.m = m;
       j.n = n;
       j.ncols = K;
-      j.out = slots;
+      j.row0 = mb.row0;
       std::copy(kp, kp + 8, j.kp);
       chs.clear();
       // V part, K <= 64: row chunks over all K columns (row-major [j][g]),
@@ -1381,8 +1397,6 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         alen += align2((long long)m * (g1 - g0));
         chs.push_back(chunk(off, m * (g1 - g0), 0, WA_NONE, 0, 0, g0, g1, 1));
       }
-      add_rows(mb.row0, m, slots);
-      slots += m;
       ja.push_back(j);
       ca.add(chs);
       continue;
@@ -1402,6 +1416,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       j.comp = g0;
       std::copy(kp, kp + 8, j.kp);
       j.out = wbase + g0;
+      j.row0 = -1;
       chs.clear();
       for (int r0 = 0; r0 < n; r0 += rpc) {
         const int r1 = std::min(n, r0 + rpc);
@@ -1439,7 +1454,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
         j.kind = WJ_USPLIT;
         j.m = rt;
         j.ncols = kg;
-        j.out = slots;
+        j.row0 = mb.row0 + i0;
         std::copy(gkp, gkp + 8, j.kp);
         chs.clear();
         const int first_cols = std::max(1, (kStageDataB - 4 * kg) / rt);
@@ -1459,29 +1474,40 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
                               wbase + kp[q0], g0 == 0 ? kg : 0, g0, g1, 1));
           g0 = g1;
         }
-        add_rows(mb.row0 + i0, rt, slots);
-        slots += rt;
         jb.push_back(j);
         cb.add(chs);
       }
       q0 = q1;
     }
   }
-  // order each pass by size (largest first; stable counting sort on the
-  // streamed size) and lay out the chunk table
-  auto order = [](const ChunkCSR& cs) {
-    const size_t nj = cs.size.size();
-    long long smax = 0;
-    for (long long s : cs.size) smax = std::max(smax, s);
-    std::vector<int> cnt((size_t)smax + 2, 0), o(nj);
-    for (long long s : cs.size) ++cnt[(size_t)(smax - s) + 1];
-    for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
-    for (size_t i = 0; i < nj; ++i) o[cnt[(size_t)(smax - cs.size[i])]++] = (int)i;
-    return o;
-  };
   pphase("blocks");
-  // job table (pass A then pass B, each largest first) and, per pass, a
-  // warp-major chunk table for the static round-robin job -> warp mapping
+  // Job order per pass: the row jobs by (first row, rows) -- stable LSD
+  // counting sorts, so a block row's jobs are adjacent -- then the VSPLIT
+  // jobs.  Consecutive jobs on the same rows form chain units that one warp
+  // runs back to back, accumulating in registers and writing ONE partial
+  // row (the leaf pass then sums a few units per leaf instead of one partial
+  // row per block).
+  auto order = [&](const std::vector<WJob>& J) {
+    const size_t nj = J.size();
+    std::vector<int> a(nj), b(nj);
+    std::vector<int> cnt(66, 0);
+    for (size_t i = 0; i < nj; ++i) ++cnt[J[i].row0 < 0 ? 0 : 1 + std::min(J[i].m, 64)];
+    for (int k = 0, run = 0; k < 66; ++k) {
+      const int t = cnt[k];
+      cnt[k] = run;
+      run += t;
+    }
+    for (size_t i = 0; i < nj; ++i) a[cnt[J[i].row0 < 0 ? 0 : 1 + std::min(J[i].m, 64)]++] = (int)i;
+    std::vector<int> cr((size_t)c->n_rows + 2, 0);
+    for (int i : a) ++cr[J[i].row0 < 0 ? (size_t)c->n_rows + 1 : (size_t)J[i].row0];
+    for (size_t k = 0, run = 0; k < cr.size(); ++k) {
+      const int t = cr[k];
+      cr[k] = (int)run;
+      run += t;
+    }
+    for (int i : a) b[cr[J[i].row0 < 0 ? (size_t)c->n_rows + 1 : (size_t)J[i].row0]++] = i;
+    return b;
+  };
   std::vector<WJob> jobs;
   std::vector<int> woff;
   const size_t nchunks_total = ca.flat.size() + cb.flat.size();
@@ -1492,18 +1518,95 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     const int NWARPS = c->sm_count * (pass == 0 ? cfg.warps : cfgB.warps);
     auto& J = pass == 0 ? ja : jb;
     const ChunkCSR& C = pass == 0 ? ca : cb;
-    const std::vector<int> ord = order(C);
-    const int jbase = (int)jobs.size();
-    for (int idx : ord) jobs.push_back(J[idx]);
+    const std::vector<int> ord = order(J);
+    const size_t nj = ord.size();
+    long long total = 0;
+    for (int idx : ord) total += C.size[idx];
+    // Chain units: runs of row jobs on the same rows (VSPLIT jobs: one unit
+    // each).  Two layouts (measured):
+    //  * a warp's share of the pass >= 2 MB (C3, C4): each warp streams one
+    //    contiguous run of the order (1/NWARPS of the bytes, sequential
+    //    pages), units cut at run ends;
+    //  * smaller shares (C2: 1.6 MB, where one job is a sizeable part of a
+    //    share): units cut at ~1/16 of a share, dealt round-robin largest
+    //    first over the warps (the balance of a size-sorted round-robin).
+    const bool contiguous =
+        mv_layout() == 1 || (mv_layout() == 0 && total / NWARPS >= (2LL << 20) / 8);
+    const long long cap = contiguous ? (1LL << 62)
+                          : mv_unit_cap() > 0 ? mv_unit_cap()
+                                              : std::max<long long>(4096, total / NWARPS / 16);
+    std::vector<int> owner(nj, 0);
+    if (contiguous) {
+      const double share = std::max(1.0, (double)total / NWARPS);
+      long long cum = 0;
+      for (size_t t = 0; t < nj; ++t) {
+        const long long sz = C.size[ord[t]];
+        owner[t] = (int)std::min<double>(NWARPS - 1, std::floor((cum + 0.5 * sz) / share));
+        cum += sz;
+      }
+    }
+    std::vector<size_t> ubeg;  // unit u = ord positions [ubeg[u], ubeg[u + 1])
+    std::vector<long long> usize;
+    for (size_t t = 0; t < nj; ++t) {
+      const WJob& q = J[ord[t]];
+      const bool open = !ubeg.empty() && q.row0 >= 0 && usize.back() < cap &&
+                        owner[t] == owner[t - 1] && J[ord[t - 1]].row0 == q.row0 &&
+                        J[ord[t - 1]].m == q.m;
+      if (!open) {
+        ubeg.push_back(t);
+        usize.push_back(0);
+      }
+      usize.back() += C.size[ord[t]];
+    }
+    const size_t nu = ubeg.size();
+    ubeg.push_back(nj);
+    std::vector<int> uord(nu);  // units in emission order
+    std::iota(uord.begin(), uord.end(), 0);
+    std::vector<int> uwarp(nu);
+    if (contiguous) {
+      for (size_t u = 0; u < nu; ++u) uwarp[u] = owner[ubeg[u]];
+    } else {
+      std::stable_sort(uord.begin(), uord.end(),
+                       [&](int x, int y) { return usize[x] > usize[y]; });
+      for (size_t i = 0; i < nu; ++i) uwarp[uord[i]] = (int)(i % NWARPS);
+    }
+    std::vector<int> jpos(nj);  // ord position -> job table index
+    for (size_t i = 0; i < nu; ++i) {
+      const int u = uord[i];
+      for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t) {
+        jpos[t] = (int)jobs.size();
+        WJob jt = J[ord[t]];
+        if (jt.row0 >= 0) {
+          if (t == ubeg[u]) {  // the unit's partial row
+            add_rows(jt.row0, jt.m, slots);
+            slots += jt.m;
+          }
+          jt.out = slots - jt.m;
+          jt.chain = t + 1 < ubeg[u + 1];
+        }
+        jobs.push_back(jt);
+      }
+    }
+    // per warp, its units in emission order (CSR over warps)
+    std::vector<int> wptr(NWARPS + 1, 0), wunits(nu);
+    for (size_t u = 0; u < nu; ++u) ++wptr[uwarp[u] + 1];
+    for (int w = 0; w < NWARPS; ++w) wptr[w + 1] += wptr[w];
+    {
+      std::vector<int> fill(wptr.begin(), wptr.end() - 1);
+      for (size_t i = 0; i < nu; ++i) wunits[fill[uwarp[uord[i]]]++] = uord[i];
+    }
     c->p_woff_base[pass] = (int)woff.size();
     c->p_chunk_base[pass] = (int)nch;
     for (int w = 0; w < NWARPS; ++w) {
       woff.push_back((int)(nch - c->p_chunk_base[pass]));
-      for (int q = w; q < (int)ord.size(); q += NWARPS) {
-        for (long long k = C.ptr[ord[q]]; k < C.ptr[ord[q] + 1]; ++k) {
-          WChunk ch = C.flat[k];
-          ch.job = jbase + q;
-          chunks[nch++] = ch;
+      for (int k = wptr[w]; k < wptr[w + 1]; ++k) {
+        const int u = wunits[k];
+        for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t) {
+          for (long long q = C.ptr[ord[t]]; q < C.ptr[ord[t] + 1]; ++q) {
+            WChunk ch = C.flat[q];
+            ch.job = jpos[t];
+            chunks[nch++] = ch;
+          }
         }
       }
     }

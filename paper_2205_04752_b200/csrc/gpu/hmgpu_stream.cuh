@@ -41,10 +41,11 @@ struct __align__(16) WJob {
   int m;           // rows of the output tile (FUSED/USPLIT/DENSE); VSPLIT: 0
   int n;           // FUSED/DENSE: block columns; VSPLIT: rows of V
   int ncols;       // FUSED/USPLIT: K = sum k_c; VSPLIT: columns (<= 32); DENSE: n
-  int chunk0, nchunks;
+  int chain;       // row jobs: the warp's next job adds to the same rows (keep y)
+  int row0;        // row jobs: first internal row (host bookkeeping); VSPLIT: -1
   int comp;        // VSPLIT: first column (of the block's K) of the job
   int vrows;       // FUSED: V part streamed in row chunks (K <= 64), x with each
-  long long out;   // FUSED/USPLIT/DENSE: partial row slot; VSPLIT: W slot of column 0
+  long long out;   // FUSED/USPLIT/DENSE: partial row slot of its chain; VSPLIT: W slot of column 0
   int kp[8];       // FUSED/USPLIT: component prefix sums of the K columns
 };
 static_assert(sizeof(WJob) == 80, "WJob layout");
@@ -481,32 +482,41 @@ hmv_warp_kernel(WarpStreamParams P) {
     if (kind == WJ_FUSED) {
       double* W = scratch + 256;
       if (ch.part == 0 && job.vrows) {
-        // rows [g0, g1) of V over all K <= 64 columns (as VSPLIT); f_s of
-        // columns lane, lane + 32 in y until the last row chunk gives W
+        // rows [g0, g1) of V over all K <= 64 columns (as VSPLIT); the f_s
+        // of columns lane, lane + 32 add up in the lane's own W slots (y may
+        // hold the rows of a job chain) until the last row chunk gives W
         const int ncol = job.ncols;
+        double f[6] = {0, 0, 0, 0, 0, 0};
         if (ncol > 32) {
-          double f[6];
           vdots2<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, lane + 32 < ncol, f);
-#pragma unroll
-          for (int r = 0; r < 6; ++r) y[r] += f[r];
         } else if (lane < ncol) {
-          vdots<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, y[0], y[1], y[2]);
+          vdots<NC>(data, ncol, ch.g1 - ch.g0, aux, lane, f[0], f[1], f[2]);
         }
-        if (ch.g1 == job.n) {
+        const bool vlast = ch.g1 == job.n;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int l = lane + 32 * h;
-            if (l < ncol) {
+        for (int h = 0; h < 2; ++h) {
+          const int l = lane + 32 * h;
+          if (l < ncol) {
+            double* o = W + 4 * l;
+            double a0 = f[3 * h], a1 = f[3 * h + 1], a2 = f[3 * h + 2];
+            if (ch.g0 != 0) {
+              a0 = o[0] + a0;
+              a1 = o[1] + a1;
+              a2 = o[2] + a2;
+            }
+            if (vlast) {
               double w[4];
-              weights<NC>(comp_of_col(job.kp, l), y[3 * h], y[3 * h + 1], y[3 * h + 2], w);
-              *reinterpret_cast<double2*>(W + 4 * l) = make_double2(w[0], w[1]);
-              *reinterpret_cast<double2*>(W + 4 * l + 2) = make_double2(w[2], w[3]);
+              weights<NC>(comp_of_col(job.kp, l), a0, a1, a2, w);
+              *reinterpret_cast<double2*>(o) = make_double2(w[0], w[1]);
+              *reinterpret_cast<double2*>(o + 2) = make_double2(w[2], w[3]);
+            } else {
+              o[0] = a0;
+              o[1] = a1;
+              o[2] = a2;
             }
           }
-#pragma unroll
-          for (int r = 0; r < 6; ++r) y[r] = 0.0;
-          __syncwarp();
         }
+        if (vlast) __syncwarp();
       } else if (ch.part == 0) {
         const int ncol = ch.g1 - ch.g0;
         if (ncol > 32 && ncol <= 64) {
@@ -577,7 +587,7 @@ hmv_warp_kernel(WarpStreamParams P) {
         }
 #pragma unroll
         for (int r = 0; r < 6; ++r) y[r] = 0.0;
-      } else {
+      } else if (!job.chain) {
         double* yo = P.ypart + job.out * NOUT;
         if (lane < job.m)
           for (int r = 0; r < NOUT; ++r) yo[lane * NOUT + r] = y[r];

@@ -379,3 +379,30 @@ def test_block_row_shards_on_one_device(c1, world):
     assert (owned[adm] == 1).all()
     assert rel(y, y_full) < 1e-15
     assert rel(Y, Y_full) < 1e-15
+
+
+@pytest.mark.parametrize("layout", ["1", "2"])
+def test_stream_layouts_agree(c1, layout):
+    """Both job layouts of the streamed matvec (contiguous runs per warp,
+    round-robin chain units; HMGPU_MV_LAYOUT) give the product of this
+    process within rounding of the summation order, and each is
+    deterministic."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    y = c1["g"].matvec(c1["x"])
+    code = ("import sys, numpy as np; sys.path.insert(0, %r);"
+            "import paper_2205_04752_b200 as hm; from oracle import oracle as orc;"
+            "g = hm.HMatrix.kelvin(hm.Mesh.icosphere(3), E=1.0, nu=0.3, b_min=32, eta=1.0,"
+            " device=0); g.assemble(eps=1e-4, beta=0.8, lookahead=2);"
+            "x = orc.random_vector(3 * 1280, 0); a = g.matvec(x); b = g.matvec(x);"
+            "sys.stdout.write(a.tobytes().hex() + ' ' + b.tobytes().hex())" % root)
+    env = dict(os.environ, HMGPU_MV_LAYOUT=layout)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                         text=True, timeout=600, check=True).stdout.split()
+    a = np.frombuffer(bytes.fromhex(out[0]))
+    b = np.frombuffer(bytes.fromhex(out[1]))
+    assert (a == b).all()
+    assert rel(a, y) < 1e-13
+    assert rel(a, c1["o"].matvec(c1["x"])) < 10 * c1["eps"]
