@@ -1224,13 +1224,22 @@ bool vrows_off() {
 
 // streamed bytes (doubles) per chain unit of the matvec plan; 0 = automatic
 // (HMGPU_MV_UNIT overrides, for tuning)
-// HMGPU_MV_LAYOUT: 0 automatic, 1 contiguous runs, 2 round-robin units
-int mv_layout() {
-  static const int v = [] {
+// HMGPU_MV_LAYOUT (both passes), HMGPU_MV_LAYOUT_A / _B (one pass):
+// 0 automatic, 1 contiguous runs, 2 round-robin units
+int mv_layout(int pass) {
+  static const int both = [] {
     const char* e = std::getenv("HMGPU_MV_LAYOUT");
     return e ? std::atoi(e) : 0;
   }();
-  return v;
+  static const int a = [] {
+    const char* e = std::getenv("HMGPU_MV_LAYOUT_A");
+    return e ? std::atoi(e) : both;
+  }();
+  static const int b = [] {
+    const char* e = std::getenv("HMGPU_MV_LAYOUT_B");
+    return e ? std::atoi(e) : both;
+  }();
+  return pass == 0 ? a : b;
 }
 long long mv_unit_cap() {
   static const long long v = [] {
@@ -1531,7 +1540,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     //    share): units cut at ~1/16 of a share, dealt round-robin largest
     //    first over the warps (the balance of a size-sorted round-robin).
     const bool contiguous =
-        mv_layout() == 1 || (mv_layout() == 0 && total / NWARPS >= (2LL << 20) / 8);
+        mv_layout(pass) == 1 || (mv_layout(pass) == 0 && total / NWARPS >= (2LL << 20) / 8);
     const long long cap = contiguous ? (1LL << 62)
                           : mv_unit_cap() > 0 ? mv_unit_cap()
                                               : std::max<long long>(4096, total / NWARPS / 16);
