@@ -112,6 +112,9 @@ typedef struct hmgpu_storage_info {
   double mb_arena_allocated;  /* device bytes reserved for U,V */
   long long matvec_bytes;     /* algorithmic bytes of one MODE_CURRENT matvec, nrhs=1 */
   long long matvec_flops;     /* flops of one MODE_CURRENT matvec, nrhs=1 */
+  long long pivots;           /* sum of the look-ahead ranks k over the low-rank
+                               * (component, block) items: the reference's
+                               * cumulative pivot count (HMatrix::total_pivots) */
 } hmgpu_storage_info;
 
 int hmgpu_device_count(int* n);

@@ -280,6 +280,7 @@ struct VArena {
     delta = std::min((delta + gran - 1) / gran * gran, va - mapped);
     const CUmemAllocationProp pr = prop();
     CUmemGenericAllocationHandle hnd;
+    const auto tg0 = std::chrono::steady_clock::now();
     CUresult rc = api.create(&hnd, delta, &pr, 0);
     if (rc == CUDA_ERROR_OUT_OF_MEMORY) {  // idle pool memory back to the device, retry
       reclaim_idle_memory();
@@ -304,6 +305,11 @@ struct VArena {
     chunks.push_back({hnd, delta});
     mapped += delta;
     n = mapped / sizeof(double);
+    if (std::getenv("HMGPU_VERBOSE"))
+      std::fprintf(stderr, "[hmgpu] arena grow +%.2f GB -> %.2f GB, %.1f ms\n", delta / 1e9,
+                   mapped / 1e9,
+                   std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now() - tg0).count());
   }
   // releases everything (callers synchronise the stream first)
   void free() {
@@ -944,6 +950,9 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
     c->sync();
     if (over == 0) break;
     ++passes;
+    if (verbose())
+      std::fprintf(stderr, "[hmgpu] aca overflow: pass %d, %zu items in the launch\n", passes,
+                   list.size());
     download_items_subset(c, list);
     std::vector<int> ids, caps;
     for (int idx : list) {
@@ -3132,6 +3141,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
       CK(cudaMemcpyAsync(c->marked_ids.data(), c->d_mids.p, nm * sizeof(int),
                          cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+    phase("items");
     *n_marked = nm;
     *gamma_pk = pk;
   });
@@ -3302,17 +3312,58 @@ int hmgpu_download_dense(hmgpu_ctx* c, int comp, int block, double* out) {
   });
 }
 
+// per-item sums of hmgpu_storage on the device (the item table is 128 B per
+// (component, block): ~180 MB at config 4, a host scan took 16 ms per AMVM
+// sweep): current / tail entries, matvec flops, pivots; integer sums, so
+// the atomics are exact and order independent
+__global__ void storage_sums_kernel(const Item* __restrict__ items, int n, int nc,
+                                    unsigned long long* __restrict__ acc) {
+  unsigned long long cur = 0, tail = 0, fl = 0, piv = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const Item& it = items[i];
+    const unsigned long long mn = (unsigned long long)(it.m + it.n);
+    const unsigned long long kc = it.kcur > 0 ? it.kcur : 0, k = it.k > 0 ? it.k : 0;
+    const unsigned long long w = (nc == 6 && c_comp_r[it.comp] != c_comp_c[it.comp]) ? 2 : 1;
+    cur += kc * mn;
+    tail += (k > kc ? k - kc : 0) * mn;
+    fl += 2 * w * kc * mn;
+    piv += k;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cur += __shfl_xor_sync(0xffffffffu, cur, o);
+    tail += __shfl_xor_sync(0xffffffffu, tail, o);
+    fl += __shfl_xor_sync(0xffffffffu, fl, o);
+    piv += __shfl_xor_sync(0xffffffffu, piv, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, cur);
+    atomicAdd(acc + 1, tail);
+    atomicAdd(acc + 2, fl);
+    atomicAdd(acc + 3, piv);
+  }
+}
+
 int hmgpu_storage(hmgpu_ctx* c, hmgpu_storage_info* info) {
   return guard(c, [&] {
     if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
     if (!info) fail(HMGPU_ERR_INVALID, "null info");
     double cur = 0, tail = 0, dense = 0;
-    long long flops = 0;
-    for (const Item& it : c->items) {
-      cur += (double)it.kcur * (it.m + it.n);
-      tail += (double)(it.k - it.kcur) * (it.m + it.n);
-      const int w = (c->NC == 6 && c_comp_host_r(it.comp) != c_comp_host_c(it.comp)) ? 2 : 1;
-      flops += 2LL * w * it.kcur * (it.m + it.n);
+    long long flops = 0, pivots = 0;
+    const int ni = (int)c->items.size();
+    if (ni > 0) {
+      DBuf<unsigned long long> acc;
+      acc.alloc(4);
+      CK(cudaMemsetAsync(acc.p, 0, 4 * sizeof(unsigned long long), c->stream));
+      storage_sums_kernel<<<grid_for(c, (ni + 255) / 256, 4), 256, 0, c->stream>>>(
+          c->d_items.p, ni, c->NC, acc.p);
+      unsigned long long h[4];
+      CK(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      acc.free();
+      cur = (double)h[0];
+      tail = (double)h[1];
+      flops = (long long)h[2];
+      pivots = (long long)h[3];
     }
     for (const DenseBlock& d : c->dblocks) {
       for (int q = 0; q < c->NC; ++q) {
@@ -3329,6 +3380,7 @@ int hmgpu_storage(hmgpu_ctx* c, hmgpu_storage_info* info) {
     info->matvec_bytes = (long long)(8.0 * (cur + dense)) +
                          8LL * (c->ndof_cols() + c->ndof_rows());
     info->matvec_flops = flops;
+    info->pivots = pivots;
   });
 }
 

@@ -545,11 +545,9 @@ void HOperator::ranks(std::vector<int>& k_cur, std::vector<int>& k_look,
 }
 
 long long HOperator::total_pivots() const {
-  std::vector<int> kc, kl;
-  ranks(kc, kl);
-  long long p = 0;
-  for (int k : kl) p += k > 0 ? k : 0;
-  return p;
+  hmgpu_storage_info s{};
+  check(hmgpu_storage(ctx_, &s), "hmgpu_storage");
+  return s.pivots;
 }
 
 double HOperator::storage_mb_current() const {
@@ -803,8 +801,13 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
     AmvmIteration it;
     it.k = k;
     it.gamma = gamma;
-    it.cumulative_pivots = op.total_pivots();
-    it.storage_mb = op.storage_mb_current();
+    {
+      hmgpu_storage_info si{};  // one pass over the items for both figures
+      check_status(op.gpu(), hmgpu_storage(op.gpu(), &si), "hmgpu_storage");
+      it.cumulative_pivots = si.pivots;
+      it.storage_mb = si.mb_current;
+    }
+    lap("account", tl);
     if (gamma <= cfg.eps_amvm) {
       it.ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
       report.iterations.push_back(it);
