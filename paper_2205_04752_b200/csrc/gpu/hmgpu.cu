@@ -2681,6 +2681,22 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA ||
       c->kind == KIND_KDOUBLE)
     upload_rules(c);
+  {
+    // items that cannot take `steps` more columns move to a larger slot up
+    // front (growth as in run_aca's overflow path); the overflow path would
+    // spend a launch, a mirror download and then the same relocation
+    std::vector<int> rid, rcap;
+    for (int idx : ids) {
+      const Item& it = c->items[idx];
+      const long long capr = std::min<long long>(c->max_rank, std::min(it.m, it.n));
+      const long long need = std::min<long long>(capr, (long long)it.k + steps);
+      if (need <= it.cap) continue;
+      rid.push_back(idx);
+      rcap.push_back((int)std::min<long long>(
+          capr, std::max<long long>(need, std::max(2 * it.cap, it.cap + 8))));
+    }
+    relocate(c, rid, rcap);  // the mirror catches up with the download below
+  }
   c->d_list.upload(ids, c->stream);
   c->timed("prep_extend", [&] {
     prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
