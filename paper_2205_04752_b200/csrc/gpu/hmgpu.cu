@@ -2678,6 +2678,15 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::sort(ids.begin(), ids.end());
   ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
   if (ids.empty() || steps == 0) return;
+  auto w0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!verbose()) return;
+    c->sync();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hmgpu] extend %-9s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - w0).count());
+    w0 = now;
+  };
   if (c->kind == KIND_KELVIN || c->kind == KIND_GALERKIN || c->kind == KIND_KDELTA ||
       c->kind == KIND_KDOUBLE)
     upload_rules(c);
@@ -2697,6 +2706,7 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
     }
     relocate(c, rid, rcap);  // the mirror catches up with the download below
   }
+  phase("relocate");
   c->d_list.upload(ids, c->stream);
   c->timed("prep_extend", [&] {
     prep_extend_kernel<<<(int)(ids.size() + 255) / 256, 256, 0, c->stream>>>(
@@ -2706,9 +2716,13 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
     return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
   });
+  phase("prep");
   run_aca(c, ids, nullptr, [&](int idx) { return c->items[idx].m + c->items[idx].n; });
+  phase("aca");
   download_items_subset(c, ids);
+  phase("download");
   refresh_matvec_ranks(c);
+  phase("ranks");
   c->plan_valid = false;
   c->p16_valid = false;
 }

@@ -1504,7 +1504,7 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
   for (int oi = blockIdx.x; oi < nblocks; oi += gridDim.x) {
     const MvBlock b = blocks[order[oi]];
     double* yp = ypart + b.prow * NOUT * nrhs;
-    if (b.dense) {
+    if (b.dense && b.m > (int)blockDim.x) {  // wide near-field block: a thread per row
       for (int i = threadIdx.x; i < b.m; i += blockDim.x) {
         for (int q = 0; q < nrhs; ++q) {
           double acc[NOUT];
@@ -1531,6 +1531,52 @@ hmv_blocks_kernel(const MvBlock* __restrict__ blocks, const int* __restrict__ or
         }
       }
       __syncthreads();
+      continue;
+    }
+    if (b.dense) {
+      // thread (i, part): rows i < m, the P = blockDim / m parts take the
+      // column range in contiguous slices; the part sums are added in part
+      // order (deterministic) -- a near-field block has m <= 64 rows, so one
+      // thread per row would leave most of the CTA idle
+      __shared__ double dred[256 * NOUT];
+      const int P = max(1, min((int)blockDim.x / b.m, b.n));
+      const int per = (b.n + P - 1) / P;
+      const int i = threadIdx.x % b.m, part = threadIdx.x / b.m;
+      const bool act = part < P;
+      const int j0 = act ? part * per : 0, j1 = act ? min(b.n, j0 + per) : 0;
+      const long long cp = (b.m * NC + 1) & ~1;
+      for (int q = 0; q < nrhs; ++q) {
+        double acc[NOUT];
+#pragma unroll
+        for (int r = 0; r < NOUT; ++r) acc[r] = 0.0;
+        if (act) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const int rr = NC == 6 ? c_comp_r[c] : 0;
+            const int cc = NC == 6 ? c_comp_c[c] : 0;
+            const double* D = dense + b.dense_off + (long long)c * b.m + i;
+            double s1 = 0.0, s2 = 0.0;
+            for (int j = j0; j < j1; ++j) {
+              const double d = D[j * cp];
+              const double* xj = xi + ((long long)(b.col0 + j) * NOUT) * nrhs + q;
+              s1 = fma(d, xj[cc * nrhs], s1);
+              if (rr != cc) s2 = fma(d, xj[rr * nrhs], s2);
+            }
+            acc[rr] += s1;
+            if (rr != cc) acc[cc] += s2;
+          }
+#pragma unroll
+          for (int r = 0; r < NOUT; ++r) dred[(part * b.m + i) * NOUT + r] = acc[r];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < b.m * NOUT; t += blockDim.x) {
+          double s = dred[t];
+          for (int h = 1; h < P; ++h) s += dred[h * b.m * NOUT + t];
+          const int ii = t / NOUT, r = t % NOUT;
+          yp[((long long)ii * NOUT + r) * nrhs + q] = s;
+        }
+        __syncthreads();
+      }
       continue;
     }
     // low rank: per component z = V^T x_c (and w = V^T x_r), then U z

@@ -763,8 +763,10 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
   if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
     throw ConfigError("amvm_multiply: sharded operators are not supported");
   using clk = std::chrono::steady_clock;
+  const auto ts = clk::now();
   report = AmvmReport{};
   report.c_sp = std::max(1, sparsity_constant(op.partition()));
+  const auto ts1 = clk::now();
   const long long M = op.rows();
   std::vector<double> b(M), b_hat_prev, diff(M);
   // one matvec per rank change: sweep the blocks in place instead of
@@ -783,6 +785,10 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
                  std::chrono::duration<double, std::milli>(now - t).count());
     t = now;
   };
+  if (verbose)
+    std::fprintf(stderr, "[amvm] setup      %9.2f ms (c_sp %.2f ms)\n",
+                 std::chrono::duration<double, std::milli>(clk::now() - ts).count(),
+                 std::chrono::duration<double, std::milli>(ts1 - ts).count());
   for (int k = 0;; ++k) {
     const auto t0 = clk::now();
     auto tl = t0;
