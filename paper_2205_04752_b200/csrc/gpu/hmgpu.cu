@@ -876,6 +876,15 @@ void download_items_subset(hmgpu_ctx* c, const std::vector<int>& ids) {
 // moves `ids` to fresh storage at the arena end with `caps` columns
 void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>& caps) {
   if (ids.empty()) return;
+  auto w0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!verbose()) return;
+    c->sync();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hmgpu] relocate %-8s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - w0).count());
+    w0 = now;
+  };
   long long extra = 0, extrap = 0;
   std::vector<long long> nu(ids.size()), nv(ids.size()), np(ids.size());
   for (size_t t = 0; t < ids.size(); ++t) {
@@ -887,7 +896,9 @@ void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>&
     np[t] = c->piv_used + extrap;
     extrap += caps[t];
   }
+  phase("host");
   arena_reserve(c, extra, extrap);
+  phase("reserve");
   DBuf<int> d_ids, d_caps;
   DBuf<long long> d_nu, d_nv, d_np;
   d_ids.upload(ids, c->stream);
@@ -895,6 +906,7 @@ void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>&
   d_nu.upload(nu, c->stream);
   d_nv.upload(nv, c->stream);
   d_np.upload(np, c->stream);
+  phase("upload");
   c->timed("relocate", [&] {
     relocate_kernel<<<grid_for(c, (long long)ids.size() / 8 + 1), 256, 0, c->stream>>>(
         c->d_items.p, d_ids.p, d_nu.p, d_nv.p, d_np.p, d_caps.p, (int)ids.size(),
@@ -903,6 +915,7 @@ void relocate(hmgpu_ctx* c, const std::vector<int>& ids, const std::vector<int>&
   c->arena_used += extra;
   c->piv_used += extrap;
   c->sync();
+  phase("kernel");
   d_ids.free(); d_caps.free(); d_nu.free(); d_nv.free(); d_np.free();
 }
 
@@ -2713,15 +2726,23 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
         c->d_items.p, c->d_list.p, (int)ids.size(), steps);
   });
   c->sync();
-  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
-    return c->items[a].m + c->items[a].n > c->items[b].m + c->items[b].n;
-  });
+  {  // largest m + n first, stable: keys gathered once (the comparator's
+     // random reads of the 128-byte item table cost ~10 ms per sweep)
+    std::vector<std::pair<int, int>> kv(ids.size());
+    for (size_t t = 0; t < ids.size(); ++t)
+      kv[t] = {-(c->items[ids[t]].m + c->items[ids[t]].n), ids[t]};
+    std::stable_sort(kv.begin(), kv.end(),
+                     [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+                       return a.first < b.first;
+                     });
+    for (size_t t = 0; t < ids.size(); ++t) ids[t] = kv[t].second;
+  }
   phase("prep");
   run_aca(c, ids, nullptr, [&](int idx) { return c->items[idx].m + c->items[idx].n; });
   phase("aca");
   download_items_subset(c, ids);
   phase("download");
-  refresh_matvec_ranks(c);
+  for (int idx : ids) c->kmax = std::max(c->kmax, c->items[idx].k);  // k only grows here
   phase("ranks");
   c->plan_valid = false;
   c->p16_valid = false;
