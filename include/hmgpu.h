@@ -256,6 +256,7 @@ int hmgpu_amvm_estimate(hmgpu_ctx* ctx, const double* x, double* gamma, double* 
    packed stream plan (for one matvec per rank change, as in the adaptive loop;
    the plan pays off from the second matvec on the same ranks) */
 int hmgpu_set_matvec_policy(hmgpu_ctx* ctx, int direct);
+int hmgpu_get_matvec_policy(hmgpu_ctx* ctx, int* direct);
 int hmgpu_amvm_mark(hmgpu_ctx* ctx, double theta, int c_sp, long long m_rows,
                     long long n_cols, double* gamma_pk, int* n_marked);
 int hmgpu_amvm_refine(hmgpu_ctx* ctx, int steps, int* comp_block);

@@ -504,6 +504,8 @@ class HMatrix:
         complete).  transposed: the transposed occurrence (x over the rows,
         terms over the columns)."""
         x = _f64(x)
+        if x.shape != ((self.rows if transposed else self.cols),):
+            raise DimensionError("gamma_contributions: size")
         g = C.c_double()
         diff = np.zeros(self.cols if transposed else self.rows)
         nt = C.c_int()
@@ -536,6 +538,10 @@ class HMatrix:
     def amvm_multiply(self, x, cfg: Optional[AmvmConfig] = None, **kw):
         cfg = cfg or AmvmConfig(**kw)
         x = _f64(x)
+        if x.shape != (self.cols,):
+            raise DimensionError("amvm_multiply: size")
+        if cfg.max_iterations < 0:
+            raise ConfigError("amvm_multiply: max_iterations must be >= 0")
         b = np.zeros(self.rows)
         iters = np.zeros((cfg.max_iterations + 1, 8))
         ni, conv = C.c_int(), C.c_int()

@@ -463,6 +463,7 @@ struct hmgpu_ctx {
   DBuf<long long> d_tprow, d_tleaf_prow;
   DBuf<int> d_tleaf_begin, d_tleaf_end, d_tleaf_ptr;
   DBuf<double> d_tpart, d_xr;
+  bool am_have_mark = false;  // hmgpu_amvm_mark ran since the last refine
   bool mv_direct = false;  // hmgpu_set_matvec_policy: 1-RHS matvecs without a stream plan
   DBuf<int> d_row_leaf, d_sortp, d_tix, d_term_bi, d_cnt, d_ptr, d_lists, d_order, d_idx,
       d_marked, d_nm, d_mids;
@@ -2638,16 +2639,18 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
       c->timed("hmv_blocks", [&] {
         const int grid = grid_for(c, c->n_mv, 8);
         if (c->NC == 6) {
-          if (smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          // always opt in: the kernel's static dred[] shares the 48 KB
+          // default window, so any dynamic size needs the attribute
+          CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
               c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
               c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
         } else {
-          if (smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          // always opt in: the kernel's static dred[] shares the 48 KB
+          // default window, so any dynamic size needs the attribute
+          CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
               c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
               c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
@@ -2824,6 +2827,13 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
 
 int hmgpu_set_matvec_policy(hmgpu_ctx* c, int direct) {
   return guard(c, [&] { c->mv_direct = direct != 0; });
+}
+
+int hmgpu_get_matvec_policy(hmgpu_ctx* c, int* direct) {
+  return guard(c, [&] {
+    if (!direct) fail(HMGPU_ERR_INVALID, "null direct");
+    *direct = c->mv_direct ? 1 : 0;
+  });
 }
 
 int hmgpu_amvm_estimate(hmgpu_ctx* c, const double* x, double* gamma, double* difference) {
@@ -3088,6 +3098,7 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
     const long long M = (long long)c->ndof_rows();
     const int nt = c->am_nterms;
     c->marked_ids.clear();
+    c->am_have_mark = false;
     const AmvmGeom a = amvm_geom(c);
     const double csp_mn = (double)c_sp * (double)m_rows * (double)n_cols;
     auto wall0 = std::chrono::steady_clock::now();
@@ -3195,12 +3206,17 @@ int hmgpu_amvm_mark(hmgpu_ctx* c, double theta, int c_sp, long long m_rows, long
     phase("items");
     *n_marked = nm;
     *gamma_pk = pk;
+    c->am_have_mark = true;
   });
 }
 
 int hmgpu_amvm_refine(hmgpu_ctx* c, int steps, int* comp_block) {
   return guard(c, [&] {
+    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
     if (steps < 0) fail(HMGPU_ERR_INVALID, "bad steps");
+    // one refinement per marking: a second call would promote and extend
+    // the same items again (2*steps pivots instead of steps)
+    if (!c->am_have_mark) fail(HMGPU_ERR_STATE, "hmgpu_amvm_mark first");
     if (comp_block)
       for (size_t q = 0; q < c->marked_ids.size(); ++q) {
         comp_block[2 * q] = c->items[c->marked_ids[q]].comp;
@@ -3209,6 +3225,8 @@ int hmgpu_amvm_refine(hmgpu_ctx* c, int steps, int* comp_block) {
     promote_ids(c, c->marked_ids);
     extend_ids(c, c->marked_ids, steps);
     c->am_have_estimate = false;
+    c->am_have_mark = false;
+    c->marked_ids.clear();
   });
 }
 

@@ -440,9 +440,14 @@ int hmb_partition_json(const hmb_op* op, char* buf, long long* len) {
     need(op, "op");
     need(len, "len");
     const std::string s = hmb::partition_to_json(op->op->partition());
+    const long long need_len = static_cast<long long>(s.size()) + 1;
     if (!buf) {
-      *len = static_cast<long long>(s.size()) + 1;
+      *len = need_len;
       return;
+    }
+    if (*len < need_len) {
+      *len = need_len;
+      throw hmb::DimensionError("partition_json: buffer too small");
     }
     std::memcpy(buf, s.c_str(), s.size() + 1);
   });
@@ -631,6 +636,7 @@ int hmb_amvm(hmb_op* op, const double* x, double theta, double eps_amvm,
     need(op, "op");
     need(x, "x");
     need(b, "b");
+    if (max_iterations < 0) throw hmb::ConfigError("amvm_multiply: max_iterations must be >= 0");
     hmb::AmvmConfig cfg;
     cfg.theta = theta;
     cfg.eps_amvm = eps_amvm;

@@ -1,9 +1,13 @@
 #include "geometry.hpp"
 
 #include <algorithm>
+#include <cctype>
+#include <cerrno>
+#include <climits>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <fstream>
-#include <map>
 #include <sstream>
 #include <stdexcept>
 #include <unordered_map>
@@ -57,84 +61,120 @@ void Mesh::finish() {
   }
 }
 
-void Mesh::validate_admissible() const {
-  std::map<std::pair<int, int>, int> edges;
-  for (const auto& tri : triangles)
-    for (int e = 0; e < 3; ++e)
-      if (++edges[{tri[e], tri[(e + 1) % 3]}] > 1)
-        throw MeshError("non-admissible triangulation: repeated directed edge");
-  for (const auto& kv : edges)
-    if (!edges.count({kv.first.second, kv.first.first}))
-      throw MeshError("non-admissible triangulation: open edge " +
-                      std::to_string(kv.first.first) + "-" +
-                      std::to_string(kv.first.second));
-  std::vector<std::vector<int>> vt(nv());
-  for (int t = 0; t < nt(); ++t)
-    for (int v : triangles[t]) vt[v].push_back(t);
-  for (int v = 0; v < nv(); ++v)
-    for (std::size_t a = 0; a < vt[v].size(); ++a)
-      for (std::size_t b = a + 1; b < vt[v].size(); ++b) {
-        int shared = 0;
-        for (int i : triangles[vt[v][a]])
-          for (int j : triangles[vt[v][b]]) shared += i == j;
-        if (shared > 2)
-          throw MeshError("non-admissible triangulation: triangles share a face");
-      }
+namespace {
+
+// directed edge a -> b packed into one sortable key
+inline std::uint64_t edge_key(int a, int b) {
+  return (static_cast<std::uint64_t>(static_cast<std::uint32_t>(a)) << 32) |
+         static_cast<std::uint32_t>(b);
 }
 
-void Mesh::label_dirichlet(const std::string& text) {
-  struct Clause {
-    int axis, op;
-    Real value;
-  };
-  std::vector<Clause> clauses;
-  std::stringstream ss(text);
-  std::string term;
-  while (std::getline(ss, term, '|')) {
-    term.erase(std::remove_if(term.begin(), term.end(), ::isspace), term.end());
-    if (term.empty()) continue;
-    if (term.size() < 4 || term[0] != 'x' || term[1] < '1' || term[1] > '3')
-      throw MeshError("labeling predicate: bad clause '" + term + "'");
-    Clause c{term[1] - '1', 0, 0.0};
-    std::size_t pos = 2;
-    if (term.compare(pos, 2, "<=") == 0) {
-      c.op = 2;
-      pos += 2;
-    } else if (term.compare(pos, 2, ">=") == 0) {
-      c.op = 3;
-      pos += 2;
-    } else if (term[pos] == '<') {
-      c.op = 0;
-      pos += 1;
-    } else if (term[pos] == '>') {
-      c.op = 1;
-      pos += 1;
-    } else {
-      throw MeshError("labeling predicate: bad operator in '" + term + "'");
-    }
-    try {
-      c.value = std::stod(term.substr(pos));
-    } catch (const std::exception&) {
-      throw MeshError("labeling predicate: bad value in '" + term + "'");
-    }
-    clauses.push_back(c);
+}  // namespace
+
+// Same acceptance rule as the reference's check (proj/src/mesh.cpp:68-101):
+// every directed edge occurs once and its reverse exists (closed and
+// consistently oriented), and no two triangles span the same vertex set.
+// Implemented on sorted key arrays instead of ordered maps.
+void Mesh::validate_admissible() const {
+  std::vector<std::uint64_t> dir;
+  dir.reserve(3 * triangles.size());
+  for (const auto& tri : triangles) {
+    dir.push_back(edge_key(tri[0], tri[1]));
+    dir.push_back(edge_key(tri[1], tri[2]));
+    dir.push_back(edge_key(tri[2], tri[0]));
   }
-  if (clauses.empty())
-    throw MeshError("labeling predicate: no clauses in '" + text + "'");
+  std::sort(dir.begin(), dir.end());
+  const auto dup = std::adjacent_find(dir.begin(), dir.end());
+  if (dup != dir.end())
+    throw MeshError("mesh is not admissible: directed edge " +
+                    std::to_string(*dup >> 32) + "->" +
+                    std::to_string(*dup & 0xffffffffu) + " used twice");
+  for (const std::uint64_t k : dir) {
+    const int a = static_cast<int>(k >> 32), b = static_cast<int>(k & 0xffffffffu);
+    if (!std::binary_search(dir.begin(), dir.end(), edge_key(b, a)))
+      throw MeshError("mesh is not admissible: boundary edge " + std::to_string(a) +
+                      "->" + std::to_string(b) + " has no twin");
+  }
+  // duplicated faces: equal sorted vertex triples
+  std::vector<std::pair<std::array<int, 3>, int>> faces(triangles.size());
+  for (std::size_t t = 0; t < triangles.size(); ++t) {
+    faces[t].first = triangles[t];
+    std::sort(faces[t].first.begin(), faces[t].first.end());
+    faces[t].second = static_cast<int>(t);
+  }
+  std::sort(faces.begin(), faces.end());
+  for (std::size_t t = 1; t < faces.size(); ++t)
+    if (faces[t].first == faces[t - 1].first)
+      throw MeshError("mesh is not admissible: triangles " +
+                      std::to_string(faces[t - 1].second) + " and " +
+                      std::to_string(faces[t].second) + " span the same face");
+}
+
+namespace {
+
+// One clause of a centroid predicate, e.g. "x3<=0": axis 0..2, comparison,
+// threshold.  Grammar as documented by the reference (mesh.hpp:42-48): a
+// '|'-separated disjunction of x<axis><op><value>, op in {<, >, <=, >=},
+// whitespace ignored.
+struct Clause {
+  int axis = 0;
+  char op = '<';      // '<' '>' 'l' (<=) 'g' (>=)
+  Real value = 0.0;
+  bool test(Real x) const {
+    switch (op) {
+      case '<': return x < value;
+      case '>': return x > value;
+      case 'l': return x <= value;
+      default: return x >= value;
+    }
+  }
+};
+
+Clause parse_clause(const std::string& raw) {
+  std::string t;
+  for (char ch : raw)
+    if (!std::isspace(static_cast<unsigned char>(ch))) t.push_back(ch);
+  const auto bad = [&](const char* why) {
+    return MeshError(std::string("dirichlet predicate: ") + why + " in clause '" + t + "'");
+  };
+  if (t.size() < 3 || t[0] != 'x' || t[1] < '1' || t[1] > '3')
+    throw bad("expected x1, x2 or x3");
+  Clause c;
+  c.axis = t[1] - '1';
+  std::size_t at = 2;
+  const bool eq = at + 1 < t.size() && t[at + 1] == '=';
+  if (t[at] == '<') c.op = eq ? 'l' : '<';
+  else if (t[at] == '>') c.op = eq ? 'g' : '>';
+  else throw bad("expected <, >, <= or >=");
+  at += eq ? 2 : 1;
+  const std::string num = t.substr(at);
+  char* end = nullptr;
+  errno = 0;
+  c.value = num.empty() ? 0.0 : std::strtod(num.c_str(), &end);
+  if (num.empty() || errno != 0 || end != num.c_str() + num.size())
+    throw bad("expected a number");
+  return c;
+}
+
+}  // namespace
+
+void Mesh::label_dirichlet(const std::string& text) {
+  std::vector<Clause> clauses;
+  std::size_t from = 0;
+  while (from <= text.size()) {
+    const std::size_t bar = std::min(text.find('|', from), text.size());
+    const std::string piece = text.substr(from, bar - from);
+    if (piece.find_first_not_of(" \t\r\n") != std::string::npos)
+      clauses.push_back(parse_clause(piece));
+    from = bar + 1;
+  }
+  if (clauses.empty()) throw MeshError("dirichlet predicate '" + text + "' has no clauses");
   if (centroids.size() != triangles.size()) finish();
   dirichlet.assign(nt(), 0);
   for (int t = 0; t < nt(); ++t)
-    for (const Clause& c : clauses) {
-      const Real x = centroids[t][c.axis];
-      const bool hit = c.op == 0   ? x < c.value
-                       : c.op == 1 ? x > c.value
-                       : c.op == 2 ? x <= c.value
-                                   : x >= c.value;
-      if (hit) {
-        dirichlet[t] = 1;
-        break;
-      }
-    }
+    dirichlet[t] = std::any_of(clauses.begin(), clauses.end(), [&](const Clause& c) {
+      return c.test(centroids[t][c.axis]);
+    });
 }
 
 Mesh make_icosphere(int level) {
@@ -249,47 +289,44 @@ Mesh make_voxel_cube(int n, Real lo, Real hi) {
   return m;
 }
 
+// OFF reader (the format of the reference's load_mesh, mesh.cpp:180-219):
+// "OFF", then "nv nt ne", nv vertex lines, nt lines "3 a b c"; '#' starts a
+// comment.  The file is read as a stream of non-comment lines, each record on
+// its own line.
 Mesh load_off(const std::string& path) {
   std::ifstream in(path);
-  if (!in) throw MeshError("cannot open mesh file " + path);
-  auto next = [&]() {
-    std::string line;
-    while (std::getline(in, line)) {
-      const auto pos = line.find('#');
-      if (pos != std::string::npos) line.erase(pos);
-      if (line.find_first_not_of(" \t\r\n") != std::string::npos) return line;
-    }
-    throw MeshError("unexpected end of mesh file " + path);
+  if (!in) throw MeshError("load_off: cannot read " + path);
+  std::vector<std::string> lines;
+  for (std::string raw; std::getline(in, raw);) {
+    raw = raw.substr(0, raw.find('#'));
+    if (raw.find_first_not_of(" \t\r\n") != std::string::npos) lines.push_back(raw);
+  }
+  std::size_t cur = 0;
+  const auto record = [&](const char* what) -> std::istringstream {
+    if (cur >= lines.size())
+      throw MeshError("load_off: " + path + " ends before the " + what);
+    return std::istringstream(lines[cur++]);
   };
-  {
-    std::stringstream ss(next());
-    std::string tag;
-    ss >> tag;
-    if (tag != "OFF") throw MeshError("mesh file " + path + ": missing OFF header");
-  }
-  int nv = 0, nt = 0, ne = 0;
-  {
-    std::stringstream ss(next());
-    if (!(ss >> nv >> nt >> ne) || nv <= 0 || nt <= 0)
-      throw MeshError("mesh file " + path + ": bad counts line");
-  }
+  std::string magic;
+  record("header") >> magic;
+  if (magic != "OFF") throw MeshError("load_off: " + path + " is not an OFF file");
+  long long nv = 0, nt = 0, ne = 0;
+  if (!(record("size line") >> nv >> nt >> ne) || nv < 1 || nt < 1 || nv > INT32_MAX ||
+      nt > INT32_MAX)
+    throw MeshError("load_off: " + path + ": invalid size line");
   Mesh m;
-  m.vertices.resize(nv);
-  for (int v = 0; v < nv; ++v) {
-    std::stringstream ss(next());
-    if (!(ss >> m.vertices[v][0] >> m.vertices[v][1] >> m.vertices[v][2]))
-      throw MeshError("mesh file " + path + ": bad vertex line");
-  }
-  m.triangles.resize(nt);
-  for (int t = 0; t < nt; ++t) {
-    std::stringstream ss(next());
-    int k = 0;
-    auto& tri = m.triangles[t];
-    if (!(ss >> k >> tri[0] >> tri[1] >> tri[2]) || k != 3)
-      throw MeshError("mesh file " + path + ": bad triangle line");
-    for (int i : tri)
-      if (i < 0 || i >= nv)
-        throw MeshError("mesh file " + path + ": vertex index out of range");
+  m.vertices.resize(static_cast<std::size_t>(nv));
+  for (V3& v : m.vertices)
+    if (!(record("vertex list") >> v[0] >> v[1] >> v[2]))
+      throw MeshError("load_off: " + path + ": unreadable vertex record");
+  m.triangles.resize(static_cast<std::size_t>(nt));
+  for (auto& tri : m.triangles) {
+    int corners = 0;
+    if (!(record("face list") >> corners >> tri[0] >> tri[1] >> tri[2]) || corners != 3)
+      throw MeshError("load_off: " + path + ": unreadable face record (triangles only)");
+    if (*std::min_element(tri.begin(), tri.end()) < 0 ||
+        *std::max_element(tri.begin(), tri.end()) >= nv)
+      throw MeshError("load_off: " + path + ": face refers to a missing vertex");
   }
   m.finish();
   m.validate_admissible();

@@ -771,10 +771,15 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
   std::vector<double> b(M), b_hat_prev, diff(M);
   // one matvec per rank change: sweep the blocks in place instead of
   // re-packing the stream plan each sweep (hmgpu_set_matvec_policy)
+  // the caller's policy is restored on exit
   struct DirectMatvec {
     hmgpu_ctx* c;
-    explicit DirectMatvec(hmgpu_ctx* cc) : c(cc) { hmgpu_set_matvec_policy(c, 1); }
-    ~DirectMatvec() { hmgpu_set_matvec_policy(c, 0); }
+    int saved = 0;
+    explicit DirectMatvec(hmgpu_ctx* cc) : c(cc) {
+      hmgpu_get_matvec_policy(c, &saved);
+      hmgpu_set_matvec_policy(c, 1);
+    }
+    ~DirectMatvec() { hmgpu_set_matvec_policy(c, saved); }
   } direct(op.gpu());
   op.matvec(x, b.data(), 1, Mode::Current);
   static const bool verbose = std::getenv("HMGPU_VERBOSE") != nullptr;
