@@ -71,7 +71,8 @@ enum {
   HMGPU_ERR_CUDA = 3,      /* CUDA runtime / launch error */
   HMGPU_ERR_NODEVICE = 4,  /* no CUDA device visible */
   HMGPU_ERR_STATE = 5,     /* call out of order (e.g. matvec before assemble) */
-  HMGPU_ERR_DIMENSION = 6  /* size mismatch (reference: DimensionError) */
+  HMGPU_ERR_DIMENSION = 6, /* size mismatch (reference: DimensionError) */
+  HMGPU_ERR_COMM = 7       /* NCCL / transport failure (multi-GPU) */
 };
 
 enum {
@@ -280,6 +281,53 @@ int hmgpu_download_factor(hmgpu_ctx* ctx, int comp, int block, int* m, int* n,
 int hmgpu_download_dense(hmgpu_ctx* ctx, int comp, int block, double* out);
 
 int hmgpu_storage(hmgpu_ctx* ctx, hmgpu_storage_info* info);
+
+/* ---- multi-GPU block-row sharding --------------------
+ * One ctx per rank and device, each created with its shard's row range
+ * (hmgpu_set_partition row_begin / row_end; the ranges of all ranks must
+ * tile [0, n_rows) in rank order).  A communicator attached to the ctx makes
+ * hmgpu_matvec_dist the whole sharded product: x is broadcast from rank 0,
+ * every rank sweeps the blocks of its rows and writes its rows in internal
+ * order into a segment buffer, the segments (padded to the longest shard)
+ * are all-gathered, and every rank un-permutes the full y.  The reference
+ * runs the same product on one process (HMatrix::matvec, hmatrix.cpp:22-45,
+ * over the blocks assembled in parallel, hmatrix.cpp:147-186).
+ *
+ * Transports: NCCL (the library's own communicator from a unique id, or a
+ * caller's ncclComm_t borrowed), loaded at run time from libnccl.so.2 (the
+ * copy already in the process if there is one); or host callbacks on HOST
+ * buffers (any other transport, e.g. a test harness), which the library
+ * stages through pinned memory.  All collective calls of one product are
+ * issued on the ctx's stream; every rank must call hmgpu_matvec_dist with
+ * the same nrhs and mode. */
+typedef struct hmgpu_comm_ops {
+  /* in-place broadcast of `bytes` from rank `root`; returns 0 on success */
+  int (*broadcast)(void* user, void* buf, long long bytes, int root);
+  /* recv[r * bytes_per_rank ...] = send of rank r, for every rank r */
+  int (*allgather)(void* user, const void* send, void* recv, long long bytes_per_rank);
+  void* user;
+} hmgpu_comm_ops;
+
+/* 1 if libnccl.so.2 can be loaded (NCCL version in *version), else 0 */
+int hmgpu_nccl_available(int* available, int* version);
+/* ncclGetUniqueId: 128 bytes that rank 0 hands to every rank out of band */
+int hmgpu_nccl_unique_id(void* id128);
+/* create the ctx's own NCCL communicator (ncclCommInitRank; collective) */
+int hmgpu_comm_init_nccl(hmgpu_ctx* ctx, int nranks, int rank, const void* id128);
+/* borrow an existing ncclComm_t (not destroyed by the library) */
+int hmgpu_comm_set_nccl(hmgpu_ctx* ctx, void* nccl_comm, int nranks, int rank);
+/* host-callback transport (ops copied; ops->user must outlive the ctx) */
+int hmgpu_comm_set_ops(hmgpu_ctx* ctx, int nranks, int rank, const hmgpu_comm_ops* ops);
+int hmgpu_comm_clear(hmgpu_ctx* ctx);
+/* kind: 0 none, 1 NCCL (own), 2 NCCL (borrowed), 3 host callbacks; row
+ * ranges of all ranks (row_begin[nranks], row_end[nranks], may be NULL) */
+int hmgpu_comm_info(hmgpu_ctx* ctx, int* nranks, int* rank, int* kind, int* row_begin,
+                    int* row_end);
+/* y = A x on all ranks (see above).  x is read on rank 0 only (other ranks
+ * may pass NULL); y (dofs x nrhs, column-major, external order) is written
+ * on every rank.  ptr_kind as hmgpu_matvec. */
+int hmgpu_matvec_dist(hmgpu_ctx* ctx, const double* x, double* y, int nrhs, int mode,
+                      int ptr_kind);
 
 /* measured DFMA throughput of the device (TFLOP/s, 2 flops per FMA): the
  * fp64 roofline denominator of the assembly kernels */

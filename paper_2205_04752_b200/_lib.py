@@ -100,6 +100,26 @@ _sig(gpu, "hmgpu_storage", I, P, P)
 _sig(gpu, "hmgpu_fp64_peak", I, I, DP)
 _sig(gpu, "hmgpu_dmma_peak", I, I, DP)
 _sig(gpu, "hmgpu_set_matvec_policy", I, P, I)
+_sig(gpu, "hmgpu_get_matvec_policy", I, P, IP)
+# multi-GPU block-row shards
+_sig(gpu, "hmgpu_nccl_available", I, IP, IP)
+_sig(gpu, "hmgpu_nccl_unique_id", I, P)
+_sig(gpu, "hmgpu_comm_init_nccl", I, P, I, I, P)
+_sig(gpu, "hmgpu_comm_set_nccl", I, P, P, I, I)
+_sig(gpu, "hmgpu_comm_clear", I, P)
+_sig(gpu, "hmgpu_comm_info", I, P, IP, IP, IP, P, P)
+_sig(gpu, "hmgpu_matvec_dist", I, P, P, P, I, I, I)
+
+# hmgpu_comm_ops: host-callback transport
+BCAST_FN = C.CFUNCTYPE(C.c_int, P, P, C.c_longlong, C.c_int)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, P, P, P, C.c_longlong)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("broadcast", BCAST_FN), ("allgather", ALLGATHER_FN), ("user", P)]
+
+
+_sig(gpu, "hmgpu_comm_set_ops", I, P, I, I, C.POINTER(CommOps))
 
 HMGPU_SYMBOLS = [
     "hmgpu_device_count", "hmgpu_create", "hmgpu_destroy", "hmgpu_last_error",

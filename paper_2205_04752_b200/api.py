@@ -359,6 +359,78 @@ class HMatrix:
         if st:
             raise DeviceError("hmgpu_set_matvec_policy failed", st)
 
+    # ---- multi-GPU block-row shards ----
+    def _gpu_check(self, st: int) -> None:
+        if st:
+            raise DeviceError(_lib.gpu.hmgpu_last_error(self.gpu_ctx).decode(), st)
+
+    def attach_nccl(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        """The library's own NCCL communicator over the shards (collective:
+        every rank calls it with rank 0's nccl_unique_id())."""
+        uid = C.create_string_buffer(bytes(unique_id), 128)
+        self._gpu_check(_lib.gpu.hmgpu_comm_init_nccl(self.gpu_ctx, nranks, rank, uid))
+
+    def attach_comm(self, nranks: int, rank: int, broadcast, allgather) -> None:
+        """Host-callback transport: broadcast(buf: np.uint8 array, root) in
+        place, allgather(send: np.uint8 array, recv: np.uint8 array) with
+        recv = concatenation over ranks (e.g. torch.distributed gloo,
+        paper_2205_04752_b200.dist.torch_transport)."""
+        def bc(_user, buf, nbytes, root):
+            try:
+                broadcast(np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)),
+                                                (int(nbytes),)), int(root))
+                return 0
+            except Exception:  # reported as HMGPU_ERR_COMM
+                return 1
+
+        def ag(_user, send, recv, nbytes):
+            try:
+                s = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (int(nbytes),))
+                r = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                          (int(nbytes) * nranks,))
+                allgather(s, r)
+                return 0
+            except Exception:
+                return 1
+
+        ops = _lib.CommOps(_lib.BCAST_FN(bc), _lib.ALLGATHER_FN(ag), None)
+        self._comm_keep = ops  # the callbacks must outlive the communicator
+        self._gpu_check(_lib.gpu.hmgpu_comm_set_ops(self.gpu_ctx, nranks, rank, C.byref(ops)))
+
+    def comm_info(self) -> dict:
+        n, r, k = C.c_int(), C.c_int(), C.c_int()
+        self._gpu_check(_lib.gpu.hmgpu_comm_info(self.gpu_ctx, C.byref(n), C.byref(r),
+                                                 C.byref(k), None, None))
+        rb = np.zeros(n.value, np.int32)
+        re = np.zeros(n.value, np.int32)
+        self._gpu_check(_lib.gpu.hmgpu_comm_info(self.gpu_ctx, None, None, None, _ptr(rb),
+                                                 _ptr(re)))
+        return dict(nranks=n.value, rank=r.value,
+                    kind={0: "none", 1: "nccl", 2: "nccl (borrowed)", 3: "host"}[k.value],
+                    row_begin=rb, row_end=re)
+
+    def matvec_dist(self, x=None, mode: Mode = Mode.Current, nrhs: int = 1) -> np.ndarray:
+        """The whole product A x on every rank: x (read on rank 0 only) is
+        broadcast, each rank sweeps its block rows, the row segments are
+        all-gathered (hmgpu_matvec_dist)."""
+        y = np.zeros((self.rows, nrhs), order="F")
+        xp = None
+        if x is not None:
+            xf = np.asfortranarray(np.asarray(x, dtype=np.float64).reshape(self.cols, -1))
+            if xf.shape[1] != nrhs:
+                raise DimensionError("matvec_dist: nrhs")
+            xp = xf.ctypes.data_as(C.c_void_p)
+        self._gpu_check(_lib.gpu.hmgpu_matvec_dist(self.gpu_ctx, xp,
+                                                   y.ctypes.data_as(C.c_void_p), nrhs,
+                                                   int(mode), 0))
+        return y[:, 0].copy() if nrhs == 1 else y
+
+    def matvec_dist_ptr(self, x_ptr: int, y_ptr: int, nrhs: int = 1,
+                        mode: Mode = Mode.Current, device: bool = True) -> None:
+        self._gpu_check(_lib.gpu.hmgpu_matvec_dist(self.gpu_ctx, C.c_void_p(x_ptr or None),
+                                                   C.c_void_p(y_ptr), nrhs, int(mode),
+                                                   1 if device else 0))
+
     # ---- tree / partition ----
     def tree(self, which: int = 0) -> ClusterTree:
         nn, dep, sz = C.c_int(), C.c_int(), C.c_int()
@@ -572,6 +644,22 @@ class HMatrix:
         if st:
             raise DeviceError(_lib.gpu.hmgpu_last_error(self.gpu_ctx).decode(), st)
         return ms.value, n.value
+
+
+def nccl_available():
+    """(available, version) of the NCCL the library loads at run time."""
+    a, v = C.c_int(), C.c_int()
+    _lib.gpu.hmgpu_nccl_available(C.byref(a), C.byref(v))
+    return bool(a.value), v.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = _lib.gpu.hmgpu_nccl_unique_id(buf)
+    if st:
+        raise DeviceError("ncclGetUniqueId failed (" + ("NCCL not loadable" if st == 7
+                                                        else "error") + ")", st)
+    return buf.raw
 
 
 # ---- reference-style free functions ----------------------------------------

@@ -32,6 +32,7 @@
 #include "hmgpu_stream.cuh"
 #include "hmgpu_mrhs.cuh"
 #include "hmgpu_amvm.cuh"
+#include "hmgpu_dist.cuh"
 
 using namespace hmgpu;
 
@@ -494,6 +495,21 @@ struct hmgpu_ctx {
   DBuf<int> d_pleaf_ptr;
   std::vector<int> p_leaf_ptr;
 
+  // ---- multi-GPU block-row sharding (hmgpu_comm_*, hmgpu_matvec_dist) ----
+  int comm_kind = 0;  // 0 none, 1 NCCL (own), 2 NCCL (borrowed), 3 host callbacks
+  int comm_n = 1, comm_rank = 0;
+  ncclComm_t nccl = nullptr;
+  hmgpu_comm_ops comm_ops{};
+  std::vector<int> dist_rb, dist_len;  // row range of every rank
+  int dist_maxseg = 0;
+  DBuf<int> d_segperm, d_dist_rb, d_dist_len;
+  DBuf<double> d_ysend, d_yrecv;
+  PinnedVec<char> h_stage_a, h_stage_b;  // host-callback staging
+  // where the matvec writes its rows: (rperm, n_rows) = external y; the
+  // distributed product points this at the shard's segment map instead
+  const int* out_perm = nullptr;
+  int out_nrows = 0;
+
   // ---- profiling ----
   bool prof = false;
   std::map<std::string, KTime> times;
@@ -533,7 +549,9 @@ struct hmgpu_ctx {
     d_tleaf_end.free(); d_tleaf_ptr.free(); d_tpart.free(); d_xr.free();
     w_keys.free(); w_skeys.free(); w_slots.free(); w_sslots.free(); w_gslot.free();
     w_rb.free(); w_dots.free();
+    d_segperm.free(); d_dist_rb.free(); d_dist_len.free(); d_ysend.free(); d_yrecv.free();
     if (stream) cudaStreamSynchronize(stream);
+    if (comm_kind == 1 && nccl) nccl_api().CommDestroy(nccl);
     if (pool) {
       std::lock_guard<std::mutex> lk(g_pools_mu);
       for (size_t i = 0; i < g_pools.size(); ++i)
@@ -548,6 +566,8 @@ struct hmgpu_ctx {
     if (stream) cudaStreamDestroy(stream);
   }
 
+  const int* yperm() const { return out_perm ? out_perm : d_rperm.p; }
+  int ynrows() const { return out_perm ? out_nrows : n_rows; }
   int ndof_rows() const { return n_rows * (NC == 6 ? 3 : 1); }
   int ndof_cols() const { return n_cols * (NC == 6 ? 3 : 1); }
 
@@ -1785,8 +1805,8 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
       hmv16_leaf_kernel<<<grid_for(c, (c->n_tiles16 + 7) / 8, 8), 256, 0, c->stream>>>(
           c->d_tiles16.p, c->n_tiles16, c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p,
           c->d_leaf_blk.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p, c->d_zb16.p,
-          c->d_arena.p, c->d_dense.p, c->d_xi16.p, c->d_zpart16.p, c->d_rperm.p,
-          c->n_rows, dy, s0, nr);
+          c->d_arena.p, c->d_dense.p, c->d_xi16.p, c->d_zpart16.p, c->yperm(),
+          c->ynrows(), dy, s0, nr);
     });
   }
 }
@@ -1849,11 +1869,11 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     if (NOUT == 3)
       hmv_leaf_reduce_kernel<3><<<g, LR_THREADS, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
-          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
+          c->d_ypart.p, c->yperm(), c->ynrows(), dy);
     else
       hmv_leaf_reduce_kernel<1><<<g, LR_THREADS, 0, c->stream>>>(
           c->d_leaf_begin.p, c->d_leaf_end.p, c->d_pleaf_ptr.p, c->d_pentries.p, nl,
-          c->d_ypart.p, c->d_rperm.p, c->n_rows, dy);
+          c->d_ypart.p, c->yperm(), c->ynrows(), dy);
   });
 }
 
@@ -2570,15 +2590,100 @@ int hmgpu_ranks(hmgpu_ctx* c, int* k_cur, int* k_look, int* consumed, int* last_
   });
 }
 
+namespace {
+// y = A x over the owned block rows, DEVICE pointers; the rows are written
+// through (c->yperm(), c->ynrows()): external order by default (non-owned
+// rows zeroed), the shard's segment for the distributed product
+void matvec_local(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode) {
+  const int NOUT = c->NC == 6 ? 3 : 1;
+  if (!c->out_perm && (c->row_begin != 0 || c->row_end != c->n_rows))
+    CK(cudaMemsetAsync(dy, 0, (size_t)c->ndof_rows() * nrhs * sizeof(double), c->stream));
+  static const bool force_v1 = std::getenv("HMGPU_MATVEC_V1") != nullptr;
+  if (nrhs > 1 && c->NC == 6 && !force_v1) {
+    bool ok = true;
+    if (!c->p16_valid || c->p16_mode != mode) {
+      try {
+        build_plan16(c, mode);
+      } catch (const Fail& f) {
+        if (f.code != HMGPU_ERR_INVALID) throw;
+        ok = false;  // ranks beyond the shared-memory Z: block sweep below
+        c->p16_valid = false;
+      }
+    }
+    if (ok) {
+      launch_mrhs(c, dx, dy, nrhs, mode);
+      return;
+    }
+  }
+  bool streamed = !force_v1 && !(c->mv_direct && nrhs == 1);
+  if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
+    try {
+      const auto tp = std::chrono::steady_clock::now();
+      build_plan(c, mode, nrhs);
+      if (verbose())
+        std::fprintf(stderr, "[hmgpu] build_plan %9.2f ms\n",
+                     std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - tp).count());
+    } catch (const Fail& f) {
+      if (f.code != HMGPU_ERR_INVALID) throw;
+      streamed = false;  // ranks / widths beyond the stream layout: block sweep
+      c->plan_valid = false;
+    }
+  }
+  if (streamed) {
+    launch_stream(c, dx, dy, nrhs);
+    return;
+  }
+  gather_x(c, dx, nrhs);
+  c->d_ypart.ensure((size_t)std::max<long long>(1, c->part_rows * NOUT * nrhs));
+  const size_t smem = sizeof(double) * 2 * (size_t)c->kmax * nrhs;
+  if (smem > 200 * 1024) fail(HMGPU_ERR_INVALID, "rank x nrhs too large for matvec");
+  c->timed("hmv_blocks", [&] {
+    const int grid = grid_for(c, c->n_mv, 8);
+    // always opt in: the kernel's static dred[] shares the 48 KB default
+    // window, so any dynamic size needs the attribute
+    if (c->NC == 6) {
+      CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
+          c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+          c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+    } else {
+      CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
+          c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
+          c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
+    }
+  });
+  c->timed("hmv_reduce", [&] {
+    const int nl = (int)c->leaf_begin.size();
+    const int grid = grid_for(c, nl, 16);
+    if (c->NC == 6)
+      hmv_reduce_kernel<3><<<grid, 128, 0, c->stream>>>(
+          c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+          nl, c->d_ypart.p, c->yperm(), c->ynrows(), dy, nrhs);
+    else
+      hmv_reduce_kernel<1><<<grid, 128, 0, c->stream>>>(
+          c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
+          nl, c->d_ypart.p, c->yperm(), c->ynrows(), dy, nrhs);
+  });
+}
+
+void check_matvec_args(hmgpu_ctx* c, int nrhs, int mode, int ptr_kind) {
+  if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
+  if (nrhs < 1) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
+  if (mode != HMGPU_MODE_CURRENT && mode != HMGPU_MODE_LOOKAHEAD)
+    fail(HMGPU_ERR_INVALID, "bad mode");
+  check_ptr_kind(ptr_kind);
+}
+}  // namespace
+
 int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
                  int ptr_kind) {
   return guard(c, [&] {
-    if (!c->assembled) fail(HMGPU_ERR_STATE, "assemble first");
-    if (!x || !y || nrhs < 1) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
-    if (mode != HMGPU_MODE_CURRENT && mode != HMGPU_MODE_LOOKAHEAD)
-      fail(HMGPU_ERR_INVALID, "bad mode");
-    check_ptr_kind(ptr_kind);
-    const int NOUT = c->NC == 6 ? 3 : 1;
+    check_matvec_args(c, nrhs, mode, ptr_kind);
+    if (!x || !y) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
     const long long nx = (long long)c->ndof_cols() * nrhs;
     const long long ny = (long long)c->ndof_rows() * nrhs;
     const double* dx = x;
@@ -2591,84 +2696,252 @@ int hmgpu_matvec(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
       dx = c->d_x.p;
       dy = c->d_y.p;
     }
-    if (c->row_begin != 0 || c->row_end != c->n_rows)
-      CK(cudaMemsetAsync(dy, 0, ny * sizeof(double), c->stream));
-    static const bool force_v1 = std::getenv("HMGPU_MATVEC_V1") != nullptr;
-    if (nrhs > 1 && c->NC == 6 && !force_v1) {
-      bool ok = true;
-      if (!c->p16_valid || c->p16_mode != mode) {
-        try {
-          build_plan16(c, mode);
-        } catch (const Fail& f) {
-          if (f.code != HMGPU_ERR_INVALID) throw;
-          ok = false;  // ranks beyond the shared-memory Z: block sweep below
-          c->p16_valid = false;
-        }
-      }
-      if (ok) {
-        launch_mrhs(c, dx, dy, nrhs, mode);
-        if (ptr_kind == HMGPU_PTR_HOST) {
-          CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-          c->sync();
-        }
-        return;
-      }
+    matvec_local(c, dx, dy, nrhs, mode);
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
     }
-    bool streamed = !force_v1 && !(c->mv_direct && nrhs == 1);
-    if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
-      try {
-        const auto tp = std::chrono::steady_clock::now();
-        build_plan(c, mode, nrhs);
-        if (verbose())
-          std::fprintf(stderr, "[hmgpu] build_plan %9.2f ms\n",
-                       std::chrono::duration<double, std::milli>(
-                           std::chrono::steady_clock::now() - tp).count());
-      } catch (const Fail& f) {
-        if (f.code != HMGPU_ERR_INVALID) throw;
-        streamed = false;  // ranks / widths beyond the stream layout: block sweep
-        c->plan_valid = false;
+  });
+}
+
+// ---- multi-GPU block-row sharding ------------------------------------------
+namespace {
+#define NK(x)                                                                     \
+  do {                                                                            \
+    ncclResult_t r_ = (x);                                                        \
+    if (r_ != ncclSuccess)                                                        \
+      throw Fail{HMGPU_ERR_COMM, std::string(#x) + ": " + nccl_api().GetErrorString(r_)}; \
+  } while (0)
+
+NcclApi& need_nccl() {
+  NcclApi& a = nccl_api();
+  if (!a.ok) fail(HMGPU_ERR_COMM, a.why);
+  return a;
+}
+
+// in-place broadcast of a device buffer from `root`
+void comm_bcast(hmgpu_ctx* c, const void* send, void* dbuf, size_t bytes, int root) {
+  if (bytes == 0) return;
+  if (c->comm_kind == 1 || c->comm_kind == 2) {
+    NK(nccl_api().Broadcast(send ? send : dbuf, dbuf, bytes, ncclChar, root, c->nccl,
+                            c->stream));
+    return;
+  }
+  c->h_stage_a.resize(bytes);
+  if (c->comm_rank == root)
+    CK(cudaMemcpyAsync(c->h_stage_a.data(), send ? send : dbuf, bytes,
+                       cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (c->comm_ops.broadcast(c->comm_ops.user, c->h_stage_a.data(), (long long)bytes, root))
+    fail(HMGPU_ERR_COMM, "host broadcast callback failed");
+  CK(cudaMemcpyAsync(dbuf, c->h_stage_a.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+}
+
+// recv[r * bytes ...] = send of rank r (device buffers)
+void comm_allgather(hmgpu_ctx* c, const void* dsend, void* drecv, size_t bytes) {
+  if (c->comm_kind == 1 || c->comm_kind == 2) {
+    NK(nccl_api().AllGather(dsend, drecv, bytes, ncclChar, c->nccl, c->stream));
+    return;
+  }
+  c->h_stage_a.resize(bytes);
+  c->h_stage_b.resize(bytes * c->comm_n);
+  CK(cudaMemcpyAsync(c->h_stage_a.data(), dsend, bytes, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (c->comm_ops.allgather(c->comm_ops.user, c->h_stage_a.data(), c->h_stage_b.data(),
+                            (long long)bytes))
+    fail(HMGPU_ERR_COMM, "host allgather callback failed");
+  CK(cudaMemcpyAsync(drecv, c->h_stage_b.data(), bytes * c->comm_n, cudaMemcpyHostToDevice,
+                     c->stream));
+}
+
+// after a transport is attached: exchange the row ranges, check that they
+// tile the rows in rank order, build the segment map
+void comm_setup(hmgpu_ctx* c) {
+  const int n = c->comm_n;
+  DBuf<int> mine, all;
+  const int rr[2] = {c->row_begin, c->row_end};
+  mine.upload(rr, 2, c->stream);
+  all.ensure(2 * (size_t)n);
+  comm_allgather(c, mine.p, all.p, 2 * sizeof(int));
+  std::vector<int> h(2 * (size_t)n);
+  CK(cudaMemcpyAsync(h.data(), all.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost,
+                     c->stream));
+  c->sync();
+  mine.free();
+  all.free();
+  c->dist_rb.assign(n, 0);
+  c->dist_len.assign(n, 0);
+  int expect = 0, maxseg = 1;
+  for (int k = 0; k < n; ++k) {
+    if (h[2 * k] != expect || h[2 * k + 1] < h[2 * k])
+      fail(HMGPU_ERR_INVALID, "shard row ranges do not tile the rows in rank order");
+    c->dist_rb[k] = h[2 * k];
+    c->dist_len[k] = h[2 * k + 1] - h[2 * k];
+    maxseg = std::max(maxseg, c->dist_len[k]);
+    expect = h[2 * k + 1];
+  }
+  if (expect != c->n_rows) fail(HMGPU_ERR_INVALID, "shard row ranges do not cover the rows");
+  c->dist_maxseg = maxseg;
+  c->d_dist_rb.upload(c->dist_rb, c->stream);
+  c->d_dist_len.upload(c->dist_len, c->stream);
+  c->d_segperm.ensure((size_t)c->n_rows);
+  dist_segperm_kernel<<<grid_for(c, (c->n_rows + 255) / 256, 8), 256, 0, c->stream>>>(
+      c->d_segperm.p, c->n_rows, c->row_begin, c->row_end);
+  CK(cudaGetLastError());
+  c->sync();
+}
+
+void comm_reset(hmgpu_ctx* c) {
+  if (c->comm_kind == 1 && c->nccl) nccl_api().CommDestroy(c->nccl);
+  c->nccl = nullptr;
+  c->comm_kind = 0;
+  c->comm_n = 1;
+  c->comm_rank = 0;
+  c->comm_ops = hmgpu_comm_ops{};
+}
+
+void comm_args(hmgpu_ctx* c, int nranks, int rank) {
+  if (!c->have_partition) fail(HMGPU_ERR_STATE, "set the partition (with the shard) first");
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(HMGPU_ERR_INVALID, "bad nranks / rank");
+}
+}  // namespace
+
+int hmgpu_nccl_available(int* available, int* version) {
+  NcclApi& a = nccl_api();
+  if (available) *available = a.ok ? 1 : 0;
+  if (version) *version = a.version;
+  return HMGPU_OK;
+}
+
+int hmgpu_nccl_unique_id(void* id128) {
+  if (!id128) return HMGPU_ERR_INVALID;
+  NcclApi& a = nccl_api();
+  if (!a.ok) return HMGPU_ERR_COMM;
+  ncclUniqueId id;
+  if (a.GetUniqueId(&id) != ncclSuccess) return HMGPU_ERR_COMM;
+  std::memcpy(id128, &id, sizeof(id));
+  return HMGPU_OK;
+}
+
+int hmgpu_comm_init_nccl(hmgpu_ctx* c, int nranks, int rank, const void* id128) {
+  return guard(c, [&] {
+    comm_args(c, nranks, rank);
+    if (!id128) fail(HMGPU_ERR_INVALID, "null unique id");
+    NcclApi& a = need_nccl();
+    comm_reset(c);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm = nullptr;
+    NK(a.CommInitRank(&comm, nranks, id, rank));
+    c->nccl = comm;
+    c->comm_kind = 1;
+    c->comm_n = nranks;
+    c->comm_rank = rank;
+    comm_setup(c);
+  });
+}
+
+int hmgpu_comm_set_nccl(hmgpu_ctx* c, void* nccl_comm, int nranks, int rank) {
+  return guard(c, [&] {
+    comm_args(c, nranks, rank);
+    if (!nccl_comm) fail(HMGPU_ERR_INVALID, "null ncclComm_t");
+    need_nccl();
+    comm_reset(c);
+    c->nccl = static_cast<ncclComm_t>(nccl_comm);
+    c->comm_kind = 2;
+    c->comm_n = nranks;
+    c->comm_rank = rank;
+    comm_setup(c);
+  });
+}
+
+int hmgpu_comm_set_ops(hmgpu_ctx* c, int nranks, int rank, const hmgpu_comm_ops* ops) {
+  return guard(c, [&] {
+    comm_args(c, nranks, rank);
+    if (!ops || !ops->broadcast || !ops->allgather)
+      fail(HMGPU_ERR_INVALID, "comm ops need broadcast and allgather");
+    comm_reset(c);
+    c->comm_ops = *ops;
+    c->comm_kind = 3;
+    c->comm_n = nranks;
+    c->comm_rank = rank;
+    comm_setup(c);
+  });
+}
+
+int hmgpu_comm_clear(hmgpu_ctx* c) {
+  return guard(c, [&] { comm_reset(c); });
+}
+
+int hmgpu_comm_info(hmgpu_ctx* c, int* nranks, int* rank, int* kind, int* row_begin,
+                    int* row_end) {
+  return guard(c, [&] {
+    if (nranks) *nranks = c->comm_n;
+    if (rank) *rank = c->comm_rank;
+    if (kind) *kind = c->comm_kind;
+    if (c->comm_kind)
+      for (int k = 0; k < c->comm_n; ++k) {
+        if (row_begin) row_begin[k] = c->dist_rb[k];
+        if (row_end) row_end[k] = c->dist_rb[k] + c->dist_len[k];
       }
+  });
+}
+
+int hmgpu_matvec_dist(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
+                      int ptr_kind) {
+  return guard(c, [&] {
+    if (!c->comm_kind) fail(HMGPU_ERR_STATE, "no communicator attached (hmgpu_comm_*)");
+    check_matvec_args(c, nrhs, mode, ptr_kind);
+    if (!y || (c->comm_rank == 0 && !x)) fail(HMGPU_ERR_INVALID, "bad matvec arguments");
+    const int NOUT = c->NC == 6 ? 3 : 1;
+    const long long nx = (long long)c->ndof_cols() * nrhs;
+    const long long ny = (long long)c->ndof_rows() * nrhs;
+    // x from rank 0 into every rank's d_x (NCCL reads the root's x in place)
+    c->d_x.ensure((size_t)nx);
+    const double* root_src = nullptr;
+    if (c->comm_rank == 0) {
+      if (ptr_kind == HMGPU_PTR_HOST)
+        CK(cudaMemcpyAsync(c->d_x.p, x, nx * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
+      else
+        root_src = x;
     }
-    if (streamed) {
-      launch_stream(c, dx, dy, nrhs);
-    } else {
-      gather_x(c, dx, nrhs);
-      c->d_ypart.ensure((size_t)std::max<long long>(1, c->part_rows * NOUT * nrhs));
-      const size_t smem = sizeof(double) * 2 * (size_t)c->kmax * nrhs;
-      if (smem > 200 * 1024) fail(HMGPU_ERR_INVALID, "rank x nrhs too large for matvec");
-      c->timed("hmv_blocks", [&] {
-        const int grid = grid_for(c, c->n_mv, 8);
-        if (c->NC == 6) {
-          // always opt in: the kernel's static dred[] shares the 48 KB
-          // default window, so any dynamic size needs the attribute
-          CK(cudaFuncSetAttribute(hmv_blocks_kernel<6>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          hmv_blocks_kernel<6><<<grid, 256, smem, c->stream>>>(
-              c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
-              c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
-        } else {
-          // always opt in: the kernel's static dred[] shares the 48 KB
-          // default window, so any dynamic size needs the attribute
-          CK(cudaFuncSetAttribute(hmv_blocks_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          hmv_blocks_kernel<1><<<grid, 256, smem, c->stream>>>(
-              c->d_mvb.p, c->d_mvorder.p, c->n_mv, c->d_items.p, c->d_arena.p,
-              c->d_dense.p, c->d_xi.p, c->d_ypart.p, nrhs, mode);
-        }
-      });
-      c->timed("hmv_reduce", [&] {
-        const int nl = (int)c->leaf_begin.size();
-        const int grid = grid_for(c, nl, 16);
-        if (c->NC == 6)
-          hmv_reduce_kernel<3><<<grid, 128, 0, c->stream>>>(
-              c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
-              nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
-        else
-          hmv_reduce_kernel<1><<<grid, 128, 0, c->stream>>>(
-              c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p, c->d_leaf_prow.p,
-              nl, c->d_ypart.p, c->d_rperm.p, c->n_rows, dy, nrhs);
-      });
+    c->timed("dist_bcast", [&] {
+      comm_bcast(c, root_src, c->d_x.p, (size_t)nx * sizeof(double), 0);
+    });
+    // the shard's rows into its segment [nrhs][NOUT][maxseg]
+    const long long seg = (long long)nrhs * NOUT * c->dist_maxseg;
+    c->d_ysend.ensure((size_t)seg);
+    c->d_yrecv.ensure((size_t)seg * c->comm_n);
+    c->out_perm = c->d_segperm.p;
+    c->out_nrows = c->dist_maxseg;
+    try {
+      matvec_local(c, c->d_x.p, c->d_ysend.p, nrhs, mode);
+    } catch (...) {
+      c->out_perm = nullptr;
+      throw;
     }
+    c->out_perm = nullptr;
+    c->timed("dist_allgather", [&] {
+      comm_allgather(c, c->d_ysend.p, c->d_yrecv.p, (size_t)seg * sizeof(double));
+    });
+    double* dy = y;
+    if (ptr_kind == HMGPU_PTR_HOST) {
+      c->d_y.ensure((size_t)ny);
+      dy = c->d_y.p;
+    }
+    c->timed("dist_scatter", [&] {
+      const long long total = seg * c->comm_n;
+      const int g = grid_for(c, (total + 255) / 256, 16);
+      if (NOUT == 3)
+        dist_scatter_kernel<3><<<g, 256, 0, c->stream>>>(
+            c->d_yrecv.p, c->comm_n, nrhs, c->dist_maxseg, c->d_dist_rb.p, c->d_dist_len.p,
+            c->d_rperm.p, c->n_rows, dy);
+      else
+        dist_scatter_kernel<1><<<g, 256, 0, c->stream>>>(
+            c->d_yrecv.p, c->comm_n, nrhs, c->dist_maxseg, c->d_dist_rb.p, c->d_dist_len.p,
+            c->d_rperm.p, c->n_rows, dy);
+    });
     if (ptr_kind == HMGPU_PTR_HOST) {
       CK(cudaMemcpyAsync(y, dy, ny * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       c->sync();
