@@ -12,17 +12,24 @@ the timed region; assembly is timed separately and reported under
           timed with CUDA events on the library's stream, max over ranks
   e2e   : the same metric through the public API with pinned host buffers
           (H2D of x and D2H of y inside every timed step)
+  c3    : (default c2 line, 1 GPU) the same measurement on the largest
+          single-GPU config (voxel cube, 589,824 dofs, ~41 GB per step)
+
+Multi-GPU: `--gpus N` (N > 1) runs N ranks -- under torchrun as launched
+by the driver, or re-launched through torch.distributed.run when started
+as a single process.  Each rank holds the block rows of its shard; x is
+broadcast and y all-gathered by the library's own NCCL communicator
+(hmgpu_matvec_dist).  Fewer visible GPUs than N is an error.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
-        python bench.py --impl reference ...   (CPU oracle of the reference path)
-Multi-GPU (torchrun): block rows sharded over ranks, x broadcast and y
-summed (disjoint rows) with NCCL on the library's stream.
+        python bench.py --impl reference ...   (the reference's own code on the CPU)
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -53,38 +60,68 @@ CONFIGS = {
 }
 
 BETA_STOP = 0.8  # ACA stopping beta (partition eta = 1 is outside (0,1))
+# config 5 memory: one 1/8 block-row shard measured at 50 GB of factors + 10 GB
+# of near field + ~2 GB of matvec plans (scripts/c5_shard.py), i.e. ~500 GB for
+# the whole operator
+C5_BYTES_TOTAL = 8 * 62e9
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def make_mesh(hm, cfg):
+def config_dict(args, cfg, n_gpus):
+    """The workload description -- identical in both arms."""
+    return {"workload": args.config + ": " + cfg["desc"], "b_min": cfg["b_min"],
+            "eta": cfg["eta"], "eps_aca": cfg["eps"], "beta_stop": BETA_STOP, "lookahead": 2,
+            "nrhs": cfg["nrhs"],
+            "parallelism": f"block-row shards x{n_gpus}" if n_gpus > 1 else "1 device",
+            "l2": L2_NOTE.get(args.config, "")}
+
+
+# every step streams the whole stored operator (the matvec's compulsory bytes)
+L2_NOTE = {
+    "c1": "small case: the stored operator (~0.1 GB) is comparable to the 126 MB L2",
+    "c2": "inputs larger than L2: 3.9 GB of stored operator streamed per step",
+    "c3": "inputs larger than L2: ~41 GB of stored operator streamed per step",
+    "c4": "inputs larger than L2: the stored operator (GBs) streamed per step",
+    "c5": "inputs larger than L2: ~500 GB of stored operator over the shards per step",
+}
+
+
+# ---- inputs built without the product package (oracle generators) --------
+def mesh_arrays(cfg):
+    """(vertices, triangles, dirichlet mask) from the oracle's generators --
+    bit-identical to the product's (tests/test_host.py)."""
+    from oracle import oracle as orc
     kind, p = cfg["mesh"]
     if kind == "icosphere":
-        return hm.Mesh.icosphere(p)
-    if kind == "ellipsoid":
-        return hm.Mesh.ellipsoid(p, 2.0, 1.0, 0.5)
-    m = hm.Mesh.voxel_cube(p, 0.0, 1.0)
-    m.label_dirichlet("x3<=0")
-    return m
+        v, t = orc.icosphere(p)
+    elif kind == "ellipsoid":
+        v, t = orc.ellipsoid(p, 2.0, 1.0, 0.5)
+    else:
+        v, t = orc.voxel_surface(p, 0.0, 1.0)
+    cen = orc.mesh_geometry(v, t)["centroids"]
+    dirichlet = cen[:, 2] <= 0.0 if kind == "cube" else np.zeros(len(t), bool)
+    return v, t, cen, dirichlet
 
 
-def make_x(hm, cfg, mesh, n_dofs):
+def make_x(cfg, centroids, dirichlet, n_dofs):
+    """x of BASELINE.json's config (seeded; mt19937_64 streams)."""
+    from oracle import oracle as orc
     nrhs = cfg["nrhs"]
     kind = cfg["x"]
     if kind == "uniform":
-        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "uniform")
+        x = orc.random_vector(n_dofs * nrhs, cfg["seed"])
     elif kind == "normal":
-        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "normal")
+        x = orc.normal_vector(n_dofs * nrhs, cfg["seed"])
     elif kind == "normal_dirichlet0":
-        x = hm.random_vector(n_dofs * nrhs, cfg["seed"], "normal")
-        d = mesh.arrays()["dirichlet"].astype(bool)
-        x.reshape(nrhs, 3, -1)[:, :, d] = 0.0  # g_N extension (hmbem_cli.cpp:76-77)
+        x = orc.normal_vector(n_dofs * nrhs, cfg["seed"])
+        x.reshape(nrhs, 3, -1)[:, :, dirichlet] = 0.0  # g_N extension (hmbem_cli.cpp:76-77)
     else:  # Gaussian bump at (2,0,0), sigma 0.05, + 1e-3 uniform noise
-        c = mesh.arrays()["centroids"]
-        bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.05 ** 2))
-        x = np.tile(bump, 3) + 1e-3 * hm.random_vector(n_dofs, cfg["seed"], "uniform")
+        bump = np.exp(-np.sum((centroids - np.array([2.0, 0, 0])) ** 2, axis=1) /
+                      (2 * 0.05 ** 2))
+        x = np.tile(bump, 3) + 1e-3 * orc.random_vector(n_dofs, cfg["seed"])
     return np.asfortranarray(x.reshape(nrhs, n_dofs).T) if nrhs > 1 else x
 
 
@@ -150,100 +187,157 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def profile_traffic(config_name):
+def profile_traffic(config_name, nrhs):
     """dram bytes per matvec of the streamed kernels from the committed ncu
-    summary (profiles/ncu_<config>_matvec.json), if present."""
-    p = os.path.join(ROOT, "profiles", f"ncu_{config_name}_matvec.json")
+    summary (profiles/ncu_<config>[_nrhs16]_matvec.json), if present."""
+    name = f"ncu_{config_name}_matvec.json" if nrhs == 1 else \
+        f"ncu_{config_name}_nrhs{nrhs}_matvec.json"
     try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_matvec")
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_matvec"), "profiles/" + name
     except (OSError, ValueError):
-        return None
+        return None, None
 
 
 def profile_pipes(config_name):
     """fp64-pipe utilisation of the assembly kernels from the committed ncu
-    captures (the north star's counter for kernel evaluation): the ACA
-    kernel and the near-field fill, per config when captured."""
+    captures (the north star's counter for kernel evaluation)."""
     out = {}
-    for key, fname in (("aca_fp64_pipe_pct", f"ncu_r01_aca_{config_name}_final.json"),
-                       ("nearfield_fp64_pipe_pct", f"ncu_r01_{config_name}_assembly.json")):
-        try:
-            with open(os.path.join(ROOT, "profiles", fname)) as f:
-                launches = json.load(f)["launches"]
-        except (OSError, ValueError, KeyError):
-            continue
-        want = "aca_kernel" if key.startswith("aca") else "nearfield_kernel"
-        for l in launches:
-            if want in l.get("kernel", ""):
-                out[key] = l.get("fp64_pipe_pct")
-                out[key.replace("pct", "source")] = "profiles/" + fname
+    for key, fnames in (("aca_fp64_pipe_pct", (f"ncu_r02_aca_{config_name}.json",
+                                               f"ncu_r01_aca_{config_name}_final.json")),
+                        ("nearfield_fp64_pipe_pct", (f"ncu_r01_{config_name}_assembly.json",))):
+        for fname in fnames:
+            try:
+                with open(os.path.join(ROOT, "profiles", fname)) as f:
+                    launches = json.load(f)["launches"]
+            except (OSError, ValueError, KeyError):
+                continue
+            want = "aca_kernel" if key.startswith("aca") else "nearfield_kernel"
+            for l in launches:
+                if want in l.get("kernel", ""):
+                    out[key] = l.get("fp64_pipe_pct")
+                    out[key.replace("pct", "source")] = "profiles/" + fname
+                    break
+            if key in out:
                 break
     return out or None
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(args, cfg, emit_line: bool):
-    """The reference path's CPU implementation (oracle port) on this config:
-    assembly with all host threads (parallel_for over blocks) and the serial
-    H-matvec (hmatrix.cpp:22-45), each step one matvec."""
-    import paper_2205_04752_b200 as hm
+# the reference path on the host cores
+def cpu_reference(cfg, steps, warmup, sample_depth=0):
+    """The reference's own implementation of the path on this box's host
+    cores: oracle/_ref (proj/src hot-path sources compiled unmodified
+    against the API shim) when it was built, else the oracle port.
+    Assembly with every host thread (parallel_for over blocks,
+    hmatrix.cpp:147-186), then `steps` serial H-matvecs (hmatrix.cpp:22-45
+    is single-threaded) over the BlockGrid (expr.cpp:197-215).
+    sample_depth > 0 restricts the operator to the block rows of one
+    2^-depth subtree of the row tree (a bounded sample of large configs)."""
     from oracle import oracle as orc
-    mesh = make_mesh(hm, cfg)
-    a = mesh.arrays()
+    from oracle import ref
+    v, t, cen, dirichlet = mesh_arrays(cfg)
     cores = os.cpu_count() or 1
-    prob = orc.Problem.kelvin(a["vertices"], a["triangles"], 1.0, 0.3, cfg["b_min"], cfg["eta"])
-    t0 = time.perf_counter()
-    prob.assemble(eps=cfg["eps"], beta=BETA_STOP)
-    t_asm = time.perf_counter() - t0
-    _, entries = prob.assemble_time()
-    n = 3 * mesh.num_triangles
-    x = make_x(hm, cfg, mesh, n)
-    xs = x if x.ndim == 1 else x[:, 0]
-    times = []
-    steps = args.steps if emit_line else 3
-    warm = args.warmup if emit_line else 1
-    for it in range(warm + steps):
+    n = 3 * len(t)
+    x = make_x(cfg, cen, dirichlet, n)
+    xs = x if x.ndim == 1 else np.ascontiguousarray(x[:, 0])
+    if ref.available():
+        kind = "reference"
+        ref.set_threads(cores)
+        prob = ref.RefProblem(v, t, "kelvin", b_min=cfg["b_min"], eta=cfg["eta"])
+        rows = (0, len(t))
+        if sample_depth > 0:
+            rows = prob.subtree_rows(sample_depth)
+            prob.restrict_rows(*rows)
         t0 = time.perf_counter()
-        prob.matvec(xs)
+        prob.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        t_asm = time.perf_counter() - t0
+        entries = None
+        mv = prob.matvec
+    else:
+        kind = "port"
+        if sample_depth > 0:
+            raise RuntimeError("bounded samples need oracle/_ref")
+        orc.set_threads(cores)
+        prob = orc.Problem.kelvin(v, t, 1.0, 0.3, cfg["b_min"], cfg["eta"])
+        rows = (0, len(t))
+        t0 = time.perf_counter()
+        prob.assemble(eps=cfg["eps"], beta=BETA_STOP)
+        t_asm = time.perf_counter() - t0
+        _, entries = prob.assemble_time()
+        mv = prob.matvec
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        mv(xs)
         dt = time.perf_counter() - t0
-        if it >= warm:
+        if it >= warmup:
             times.append(dt)
     t_mv = float(np.mean(times))
-    value = n / t_mv
-    sample = (f"{cfg['desc']}: oracle assembly ({cores} threads, {t_asm:.1f} s) + "
-              f"{steps} serial H-matvecs (1 RHS, {t_mv * 1e3:.1f} ms each)")
-    out = {
-        "cpu_baseline": {"value": value, "unit": "dofs/s", "cores": 1, "kind": "port",
-                         "sample": sample, "ms_per_matvec": t_mv * 1e3},
-        "assembly": {"value": entries / t_asm, "unit": "entries/s", "cores": cores,
-                     "seconds": t_asm, "entries": entries},
-    }
-    return out, t_mv
+    sample_rows = 3 * (rows[1] - rows[0])
+    value = sample_rows / t_mv
+    what = "the reference's own code (oracle/_ref)" if kind == "reference" else \
+        "the oracle port of the reference"
+    frac = "" if sample_depth == 0 else \
+        f", block rows of 1 of 2^{sample_depth} row subtrees ({sample_rows} of {n} dofs)"
+    sample = (f"{cfg['desc']}{frac}: {what}; assembly on {cores} threads "
+              f"({t_asm:.1f} s), {steps} serial H-matvecs (1 RHS, {t_mv * 1e3:.1f} ms each)")
+    return {"value": value, "unit": "dofs/s", "cores": 1, "kind": kind, "sample": sample,
+            "ms_per_matvec": t_mv * 1e3, "assembly_s": t_asm, "assembly_cores": cores,
+            "assembly_entries": entries}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    res, t_mv = cpu_reference(args, cfg, emit_line=True)
-    v = res["cpu_baseline"]["value"]
+    depth = {"c3": 5, "c5": 9}.get(args.config, 0)
+    steps = args.steps
+    if args.config in ("c3", "c5"):  # keep the run within minutes
+        steps = min(steps, 5)
+    cb = cpu_reference(cfg, steps, args.warmup if depth == 0 else 1, depth)
+    v = cb["value"]
     line = {
         "metric": METRIC, "value": v, "unit": "dofs/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_mv * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_matvec"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": args.config + ": " + cfg["desc"], "b_min": cfg["b_min"],
-                   "eta": cfg["eta"], "eps_aca": cfg["eps"], "beta_stop": BETA_STOP,
-                   "nrhs": 1},
-        "cpu_baseline": res["cpu_baseline"],
-        "assembly_cpu": res["assembly"],
+        "data": "synthetic (seeded mesh + x; random_vector mt19937_64)", "impl": "reference",
+        "config": config_dict(args, cfg, args.gpus),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "assembly_cpu": {"seconds": cb["assembly_s"], "cores": cb["assembly_cores"]},
         "e2e": {"value": v, "unit": "dofs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def cpu_amvm_reference(cfg, max_iterations=5):
+    """config 4's adaptive matvec on the reference's own code (oracle/_ref):
+    full-mode assembly at eps 1e-2, then amvm_multiply (amvm.cpp:199-268)
+    with theta 0.7, eps_amvm 1e-6, look-ahead 2 -- all host threads for the
+    parallel parts (assembly, extensions), the rest serial as written."""
+    from oracle import ref
+    if not ref.available():
+        return None
+    v, t, cen, dirichlet = mesh_arrays(cfg)
+    x = make_x(cfg, cen, dirichlet, 3 * len(t))
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    prob = ref.RefProblem(v, t, "kelvin", b_min=cfg["b_min"], eta=cfg["eta"])
+    t0 = time.perf_counter()
+    prob.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+    t_asm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    b, it, conv = prob.amvm(x, theta=0.7, eps_amvm=1e-6, lookahead_steps=2,
+                            max_iterations=max_iterations)
+    t_amvm = time.perf_counter() - t0
+    return {"seconds": t_amvm, "assembly_s": t_asm, "cores": cores, "kind": "reference",
+            "sweeps": len(it), "gamma": [float(r[1]) for r in it],
+            "marked": [int(r[3]) for r in it], "converged": conv}
+
+
+# ---------------------------------------------------------------------------
 def weighted_entries(h):
     """sum_c w_c (sum_adm k_cb (m_b + n_b) + sum_dense m_b n_b), w_c = 1 on the
     diagonal components and 2 off it (each off-diagonal factor serves two x
@@ -263,7 +357,199 @@ def weighted_entries(h):
     return float((w * (lowrank + dense)).sum())
 
 
-# ---------------------------------------------------------------------------
+OUR_KERNELS = ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_reduce", "hmv_blocks",
+               "hmv16_z", "hmv16_zsum", "hmv16_leaf", "dist_scatter")
+COMM_OPS = ("dist_bcast", "dist_allgather")
+
+
+def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
+    """Assembly + K timed matvecs (+ e2e) of config `name` on this rank."""
+    nrhs = cfg["nrhs"]
+    if name == "c5":
+        free_b, total_b = torch.cuda.mem_get_info(device)
+        need = C5_BYTES_TOTAL / world
+        if need > 0.92 * total_b:
+            raise SystemExit(
+                f"config c5 needs ~{need / 1e9:.0f} GB per GPU at {world} GPU(s) "
+                f"(~{C5_BYTES_TOTAL / 1e9:.0f} GB in total, DESIGN.md 5); this device has "
+                f"{total_b / 1e9:.0f} GB -- run it with --gpus 4 or 8")
+    t0 = time.perf_counter()
+    kind, p = cfg["mesh"]
+    if kind == "icosphere":
+        mesh = hm.Mesh.icosphere(p)
+    elif kind == "ellipsoid":
+        mesh = hm.Mesh.ellipsoid(p, 2.0, 1.0, 0.5)
+    else:
+        mesh = hm.Mesh.voxel_cube(p, 0.0, 1.0)
+        mesh.label_dirichlet("x3<=0")
+    a = mesh.arrays()
+    h = hm.HMatrix.kelvin(mesh, E=1.0, nu=0.3, b_min=cfg["b_min"], eta=cfg["eta"],
+                          device=device, shard=(rank, world))
+    host_setup_s = time.perf_counter() - t0
+    n = h.cols
+    # ---- assembly (timed on the device, best of the repeats after the first;
+    # the first assemblies of a process also map the factor arenas) ----
+    reps = 4 if n < 1_000_000 else 2
+    asm = []
+    h.set_profiling(True)
+    for _ in range(reps):
+        for k in ("aca", "nearfield", "compact", "relocate"):
+            h.kernel_times(k, reset=True)
+        st = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
+        kt_asm = {k: h.kernel_times(k, reset=True)[0]
+                  for k in ("aca", "nearfield", "compact", "relocate")}
+        asm.append((st, kt_asm))
+    h.set_profiling(False)
+    best, best_kt = min(asm[1:], key=lambda q: q[0].ms_total)
+    storage = h.storage()
+    if world > 1:
+        from paper_2205_04752_b200.dist import exchange_unique_id
+        uid = exchange_unique_id(rank, hm.nccl_unique_id() if rank == 0 else None)
+        h.attach_nccl(world, rank, uid)
+
+    x = make_x(cfg, a["centroids"], a["dirichlet"].astype(bool), n)
+    xt = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x), dtype=torch.float64,
+                      device=f"cuda:{device}")
+    # library layout: dofs x nrhs column-major == nrhs x dofs row-major
+    yt = torch.zeros((nrhs, h.rows) if nrhs > 1 else h.rows, dtype=torch.float64,
+                     device=f"cuda:{device}")
+    stream = torch.cuda.ExternalStream(h.stream(), device=f"cuda:{device}")
+
+    def step():
+        if world > 1:
+            h.matvec_dist_ptr(xt.data_ptr() if rank == 0 else 0, yt.data_ptr(), nrhs)
+        else:
+            h.matvec_ptr(xt.data_ptr(), yt.data_ptr(), nrhs)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-kernel device times from a separate profiled pass (not the timed one)
+    h.set_profiling(True)
+    for k in OUR_KERNELS + COMM_OPS:
+        h.kernel_times(k, reset=True)
+    nprof = max(3, min(steps, 10))
+    for _ in range(nprof):
+        step()
+    torch.cuda.synchronize()
+    kt = {k: h.kernel_times(k, reset=True) for k in OUR_KERNELS + COMM_OPS}
+    h.set_profiling(False)
+    launches_per_step = sum(kt[k][1] for k in OUR_KERNELS) / nprof
+
+    # ---- timed region: K device-resident matvecs ----
+    clocks = ClockSampler(device)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)  # sampler warm-up
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        tt = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / steps
+    value = h.rows * nrhs / (ms_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers ----
+    xh = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x),
+                      dtype=torch.float64).pin_memory()
+    yh = torch.zeros(yt.shape, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        if world > 1:
+            h.matvec_dist_ptr(xh.data_ptr() if rank == 0 else 0, yh.data_ptr(), nrhs,
+                              device=False)
+        else:
+            h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
+
+    e2e_steps = max(3, min(steps, 20))
+    for _ in range(2):
+        e2e_step()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+
+    # ---- roofline of the dominant kernel (this rank's shard) ----
+    peak, peak_src = measured_peaks()
+    alg_bytes = storage["matvec_bytes"] + 8 * (nrhs - 1) * (h.rows + h.cols)
+    traffic, traffic_src = profile_traffic(name, nrhs) if world == 1 else (None, None)
+    if kt["hmv16_leaf"][1] > 0:
+        # 16 RHS per pass on the fp64 tensor cores: F = 2 nrhs sum_c w_c
+        # (sum_adm k (m + n) + sum_dense m n), w = 1 | 2 (SURVEY.md 8d)
+        ms_dom = (kt["hmv16_z"][0] + kt["hmv16_zsum"][0] + kt["hmv16_leaf"][0]) / nprof
+        flops = 2.0 * nrhs * weighted_entries(h)
+        dmma_peak = hm.dmma_peak_tflops(device)
+        achieved = flops / (ms_dom * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": "hmv16_z + hmv16_zsum + hmv16_leaf (DMMA)",
+                    "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+                    "frac": achieved / dmma_peak, "traffic": traffic,
+                    "peak_source": "measured (hmgpu_dmma_peak, fp64 m8n8k4 chains)",
+                    "algorithmic_flops_per_step": flops,
+                    "algorithmic_bytes_per_step": alg_bytes,
+                    "hbm_frac": alg_bytes / (ms_dom * 1e-3) / 1e9 / peak,
+                    "ms_kernel": ms_dom, "ms_matvec_device": ms_step}
+    else:
+        ms_stream = (kt["hmv_stream"][0] + kt["hmv_ypart"][0]) / nprof
+        ms_blocks = kt["hmv_blocks"][0] / nprof
+        ms_dom = ms_stream if ms_stream > 0 else ms_blocks
+        dom = "hmv_warp_kernel (pass A + pass B)" if ms_stream > 0 else "hmv_blocks_kernel"
+        achieved = alg_bytes / (ms_dom * 1e-3) / 1e9 if ms_dom > 0 else None
+        roofline = {"bound": "hbm", "kernel": dom,
+                    "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak if achieved else None,
+                    "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                    "algorithmic_bytes_per_step": alg_bytes,
+                    "ms_kernel": ms_dom, "ms_matvec_device": ms_step,
+                    "matvec_frac_incl_gather_reduce": alg_bytes / (ms_step * 1e-3) / 1e9 / peak}
+    if world > 1:
+        roofline["scope"] = f"rank {rank}'s shard ({h.row_range[1] - h.row_range[0]} rows)"
+        roofline["comm_ms"] = {k: kt[k][0] / nprof for k in COMM_OPS}
+    asm_s = best.ms_total * 1e-3
+    entries = best.aca_entries + best.dense_entries
+    fp64_peak = hm.fp64_peak_tflops(device)
+    res = {
+        "value": value, "ms_per_step": ms_step,
+        "roofline": roofline,
+        "e2e": {"value": h.rows * nrhs / e2e_s, "unit": "dofs/s",
+                "h2d_bytes_per_step": int(8 * h.cols * nrhs) if rank == 0 else 0,
+                "d2h_bytes_per_step": int(8 * h.rows * nrhs)},
+        "gpu_launches": int(round(steps * launches_per_step)),
+        "clocks": ck,
+        "assembly": {"value": entries / asm_s, "unit": "entries/s", "ms": best.ms_total,
+                     "kernel_ms": best_kt, "aca_entries": best.aca_entries,
+                     "dense_entries": best.dense_entries, "pivots": best.pivots,
+                     "storage_mb": storage["mb_current"],
+                     # counted flops: 30 n_q + 1 per component entry (SURVEY.md 8d)
+                     "counted_tflops": best.counted_flops / asm_s / 1e12,
+                     "fp64_peak_tflops_measured": fp64_peak,
+                     "fp64_frac": best.counted_flops / asm_s / 1e12 / fp64_peak,
+                     "fp64_frac_kernels": best.counted_flops /
+                     ((best_kt["aca"] + best_kt["nearfield"]) * 1e-3) / 1e12 / fp64_peak,
+                     "nearfield_entries_per_s": best.dense_entries /
+                     (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None,
+                     "ncu": profile_pipes(name)},
+        "kernel_ms": {k: (v[0] / nprof) for k, v in kt.items() if v[1]},
+        "host_setup_s": host_setup_s,
+    }
+    return res, h, x
+
+
 def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
     """SURVEY.md 8f rank 2 on the same mesh: the Galerkin V_Delta and V_kl
     H-matrices (pair quadrature with Sauter-Schwab rules for touching pairs)
@@ -303,8 +589,6 @@ def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
     ms = (time.perf_counter() - t0) / reps * 1e3
     y_host = vh.matvec(x)
     entries = sk.aca_entries + sk.dense_entries + sd.aca_entries + sd.dense_entries
-    # the composed operators of the operator algebra
-    # on device vectors: V_h, K_h (3N -> 3M), D_h (3N -> 3N)
     ops_t = None
     try:
         ops = hm.OperatorSet(mesh, 1.0, 0.3, b_min=cfg["b_min"], eta=cfg["eta"], device=device)
@@ -312,43 +596,18 @@ def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
         xn = torch.tensor(hm.random_vector(3 * ops.n, 3, "uniform"), device=f"cuda:{device}")
         xm = torch.tensor(hm.random_vector(3 * ops.m, 4, "uniform"), device=f"cuda:{device}")
         ops_t = {"assembly_ms_device": sum(st_.ms_total for st_ in so)}
-        for name, f_, v_ in (("vh", ops.vh_dev, xm), ("kh", ops.kh_dev, xn),
-                             ("dh", ops.dh_dev, xn), ("kh_t", ops.kh_t_dev, xm)):
+        for nm_, f_, v_ in (("vh", ops.vh_dev, xm), ("kh", ops.kh_dev, xn),
+                            ("dh", ops.dh_dev, xn), ("kh_t", ops.kh_t_dev, xm)):
             f_(v_)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(5):
                 f_(v_)
             torch.cuda.synchronize()
-            ops_t[name + "_ms_wall"] = (time.perf_counter() - t0) / 5 * 1e3
+            ops_t[nm_ + "_ms_wall"] = (time.perf_counter() - t0) / 5 * 1e3
         del ops
     except Exception as e:  # informational
         ops_t = {"error": str(e)}
-    # CPU reference path (the oracle restatement, all host threads) beside
-    # the device on a bounded sample: the icosphere L3 (1280 triangles)
-    cpu = None
-    try:
-        import os as _os
-        from oracle import oracle as orc
-        m3 = hm.Mesh.icosphere(3)
-        a3 = m3.arrays()
-        t0 = time.perf_counter()
-        for which in (0, 1):
-            p = orc.Problem.galerkin(a3["vertices"], a3["triangles"], which,
-                                     b_min=cfg["b_min"], eta=cfg["eta"])
-            p.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        cpu_s = time.perf_counter() - t0
-        g3 = hm.LameSingleLayer(m3, 1.0, 0.3, b_min=cfg["b_min"], eta=cfg["eta"],
-                                device=device)
-        g3.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        s3 = g3.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        gpu_ms = s3[0].ms_total + s3[1].ms_total
-        cpu = {"sample": "icosphere L3, 1280 triangles: V_kl grid + V_Delta assembly",
-               "cpu_s": cpu_s, "cores": _os.cpu_count(), "kind": "port",
-               "gpu_ms_device": gpu_ms, "speedup": cpu_s / (gpu_ms * 1e-3)}
-    except Exception as e:  # the CPU leg is informational
-        cpu = {"error": str(e)}
-
     return {"operator": "V_h = (1+nu)/(2E(1-nu)) [(3-4nu) diag3(V_Delta) + grid(V_kl)]",
             "assembly_ms_device": sk.ms_total + sd.ms_total, "assembly_ms_wall": wall * 1e3,
             "entries": entries, "entries_per_s": entries / ((sk.ms_total + sd.ms_total) * 1e-3),
@@ -358,8 +617,24 @@ def galerkin_leg(hm, torch, mesh, cfg, device, reps=20):
             "matvec_ms_wall": ms, "matvec_dofs_per_s": 3 * nt / (ms * 1e-3),
             "matvec_check_rel": float(np.linalg.norm(y.cpu().numpy() - y_host) /
                                       np.linalg.norm(y_host)),
-            "cpu_baseline": cpu,
             "operators": ops_t}
+
+
+def relaunch_multi(args):
+    """`--gpus N` started as one process: re-run under torch.distributed.run
+    with N ranks (one per GPU); refuse if fewer than N GPUs are visible."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) visible")
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def run_ours(args, cfg):
@@ -369,209 +644,63 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return 2
+    if torch.cuda.device_count() < (local + 1):
+        log(f"bench.py: rank {rank} needs GPU {local}, {torch.cuda.device_count()} visible")
+        return 2
     dist = None
-    # torchrun (RANK set) or N > 1: the NCCL protocol runs even for one rank
-    # (HMB_BENCH_NO_DIST=1 disables it for a single process)
-    if world > 1 or ("RANK" in os.environ and not os.environ.get("HMB_BENCH_NO_DIST")):
+    torch.cuda.set_device(local)
+    if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local
-    torch.cuda.set_device(device)
 
-    mesh = make_mesh(hm, cfg)
-    nrhs = cfg["nrhs"]
-    h = hm.HMatrix.kelvin(mesh, E=1.0, nu=0.3, b_min=cfg["b_min"], eta=cfg["eta"],
-                          device=device, shard=(rank, world))
-    n = h.cols
-    # ---- assembly (timed on the device, best of 3 after one warm-up; the
-    # first assemblies of a process also map the factor arenas) ----
-    asm = []
-    h.set_profiling(True)
-    for _ in range(4):
-        for k in ("aca", "nearfield", "compact", "relocate"):
-            h.kernel_times(k, reset=True)
-        st = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        kt_asm = {k: h.kernel_times(k, reset=True)[0]
-                  for k in ("aca", "nearfield", "compact", "relocate")}
-        asm.append((st, kt_asm))
-    h.set_profiling(False)
-    best, best_kt = min(asm[1:], key=lambda p: p[0].ms_total)
-    storage = h.storage()
-    fp64_peak = hm.fp64_peak_tflops(device)
-
-    x = make_x(hm, cfg, mesh, n)
-    xt = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x), dtype=torch.float64,
-                      device=f"cuda:{device}")
-    # library layout: dofs x nrhs column-major == nrhs x dofs row-major
-    yt = torch.zeros((nrhs, h.rows) if nrhs > 1 else h.rows, dtype=torch.float64,
-                     device=f"cuda:{device}")
-    stream = torch.cuda.ExternalStream(h.stream(), device=f"cuda:{device}")
-
-    def step():
-        with torch.cuda.stream(stream):
-            if dist is not None:
-                dist.broadcast(xt, src=0)
-            h.matvec_ptr(xt.data_ptr(), yt.data_ptr(), nrhs)
-            if dist is not None:
-                dist.all_reduce(yt)  # rows are disjoint across ranks: sum = gather
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    # per-kernel device times from a separate profiled pass (not the timed one)
-    h.set_profiling(True)
-    KNAMES = ("gather", "hmv_stream", "hmv_zreduce", "hmv_ypart", "hmv_reduce", "hmv_blocks",
-              "hmv16_z", "hmv16_zsum", "hmv16_leaf")
-    for k in KNAMES:
-        h.kernel_times(k, reset=True)
-    for _ in range(max(3, min(args.steps, 10))):
-        step()
-    torch.cuda.synchronize()
-    kt = {k: h.kernel_times(k, reset=True) for k in KNAMES}
-    h.set_profiling(False)
-
-    # ---- timed region: K device-resident matvecs ----
-    clocks = ClockSampler(device)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)  # sampler warm-up
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ck = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = h.rows * nrhs / (ms_step * 1e-3)
-
-    # ---- e2e through the public API with pinned host buffers ----
-    xh = torch.tensor(np.ascontiguousarray(x.T if x.ndim > 1 else x),
-                      dtype=torch.float64).pin_memory()
-    yh = torch.zeros(yt.shape, dtype=torch.float64).pin_memory()
-    e2e_steps = max(3, min(args.steps, 20))
-    for _ in range(2):
-        h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
-    if dist is not None:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        if dist is not None:  # host-driven: x from host on every rank, y reduced
-            h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
-            yd = yh.to(f"cuda:{device}", non_blocking=True)
-            dist.all_reduce(yd)
-            yh.copy_(yd)
-        else:
-            h.matvec_ptr(xh.data_ptr(), yh.data_ptr(), nrhs, device=False)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if dist is not None:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-
-    # ---- roofline of the dominant kernel ----
-    peak, peak_src = measured_peaks()
-    nsteps_prof = max(kt["gather"][1], 1)
-    alg_bytes = storage["matvec_bytes"] + 8 * (nrhs - 1) * (h.rows + h.cols)
-    traffic = profile_traffic(args.config) if nrhs == 1 else None
-    if kt["hmv16_leaf"][1] > 0:
-        # 16 RHS per pass on the fp64 tensor cores: flop-bound:
-        # F = 2 nrhs sum_c w_c (sum_adm k (m + n) + sum_dense m n), w = 1 | 2
-        ms_dom = (kt["hmv16_z"][0] + kt["hmv16_zsum"][0] + kt["hmv16_leaf"][0]) / nsteps_prof
-        flops = 2.0 * nrhs * weighted_entries(h)
-        dmma_peak = hm.dmma_peak_tflops(device)
-        achieved = flops / (ms_dom * 1e-3) / 1e12
-        roofline = {"bound": "tensor", "kernel": "hmv16_z + hmv16_zsum + hmv16_leaf (DMMA)",
-                     "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-                     "frac": achieved / dmma_peak, "traffic": traffic,
-                     "peak_source": "measured (hmgpu_dmma_peak, fp64 m8n8k4 chains)",
-                     "algorithmic_flops_per_step": flops,
-                     "algorithmic_bytes_per_step": alg_bytes,
-                     "hbm_frac": alg_bytes / (ms_dom * 1e-3) / 1e9 / peak,
-                     "ms_kernel": ms_dom, "ms_matvec_device": ms_step}
-        dom_launches = 4 * ((nrhs + 15) // 16)
-    else:
-        ms_stream = (kt["hmv_stream"][0] + kt["hmv_ypart"][0]) / max(kt["hmv_stream"][1], 1)
-        ms_blocks = kt["hmv_blocks"][0] / max(kt["hmv_blocks"][1], 1)
-        ms_dom = ms_stream if ms_stream > 0 else ms_blocks
-        dom_name = "hmv_stream_kernel (pass A + pass B)" if ms_stream > 0 else "hmv_blocks_kernel"
-        achieved = alg_bytes / (ms_dom * 1e-3) / 1e9 if ms_dom > 0 else None
-        roofline = {"bound": "hbm", "kernel": dom_name,
-                    "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak if achieved else None,
-                    "traffic": traffic, "peak_source": peak_src,
-                    "algorithmic_bytes_per_step": alg_bytes,
-                    "ms_kernel": ms_dom,
-                    "ms_matvec_device": ms_step,
-                    "matvec_frac_incl_gather_reduce": alg_bytes / (ms_step * 1e-3) / 1e9 / peak}
-        dom_launches = 3 + (kt["hmv_zreduce"][1] > 0) + (kt["hmv_ypart"][1] > 0)
-
-    res = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        res, _ = cpu_reference(args, cfg, emit_line=False)
-    # counted fp64 flops per entry: 30 n_q + 1 with n_q = 7 for
-    # near-field pairs; ACA entries mostly far (n_q = 3); report entries/s
-    asm_s = best.ms_total * 1e-3
-    entries = best.aca_entries + best.dense_entries
+    res, h, x = measure(hm, torch, args.config, cfg, args.steps, args.warmup, world, rank,
+                        device, dist)
     line = {
         "metric": METRIC,
-        "value": value,
+        "value": res["value"],
         "unit": "dofs/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms_step,
+        "ms_per_step": res["ms_per_step"],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded mesh + x; random_vector mt19937_64)",
-        "config": {"workload": args.config + ": " + cfg["desc"], "b_min": cfg["b_min"],
-                   "eta": cfg["eta"], "eps_aca": cfg["eps"], "beta_stop": BETA_STOP,
-                   "lookahead": 2, "nrhs": nrhs,
-                   "parallelism": f"block-row shards x{world}" if world > 1 else "1 GPU",
-                   "l2": f"inputs larger than L2: {alg_bytes / 1e9:.2f} GB streamed per step"},
-        "roofline": roofline,
-        "e2e": {"value": h.rows * nrhs / e2e_s, "unit": "dofs/s",
-                "h2d_bytes_per_step": int(8 * h.cols * nrhs),
-                "d2h_bytes_per_step": int(8 * h.rows * nrhs)},
-        "gpu_launches": int(args.steps * dom_launches),
-        "clocks": ck,
-        "assembly": {"value": entries / asm_s, "unit": "entries/s", "ms": best.ms_total,
-                     "kernel_ms": best_kt, "aca_entries": best.aca_entries,
-                     "dense_entries": best.dense_entries, "pivots": best.pivots,
-                     "storage_mb": storage["mb_current"],
-                     # counted flops: 30 n_q + 1 per component entry
-                     "counted_tflops": best.counted_flops / asm_s / 1e12,
-                     "fp64_peak_tflops_measured": fp64_peak,
-                     "fp64_frac": best.counted_flops / asm_s / 1e12 / fp64_peak,
-                     "fp64_frac_kernels": best.counted_flops /
-                     ((best_kt["aca"] + best_kt["nearfield"]) * 1e-3) / 1e12 / fp64_peak,
-                     "nearfield_entries_per_s": best.dense_entries /
-                     (best_kt["nearfield"] * 1e-3) if best_kt["nearfield"] else None,
-                     "ncu": profile_pipes(args.config)},
-        "kernel_ms": {k: (v[0] / v[1] if v[1] else 0.0) for k, v in kt.items()},
+        "config": config_dict(args, cfg, world),
+        "roofline": res["roofline"],
+        "e2e": res["e2e"],
+        "gpu_launches": res["gpu_launches"],
+        "clocks": res["clocks"],
+        "assembly": res["assembly"],
+        "kernel_ms": res["kernel_ms"],
     }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        depth = {"c3": 5, "c5": 9}.get(args.config, 0)
+        try:
+            cb = cpu_reference(cfg, 3, 1, depth)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["assembly"]["cpu_reference_s"] = cb["assembly_s"]
+            line["assembly"]["cpu_reference_cores"] = cb["assembly_cores"]
+        except Exception as e:
+            line["cpu_baseline"] = {"error": str(e)}
     if args.config == "c4" and world == 1:
         # the adaptive matvec of config 4 (Algorithm 2): full-mode assembly at
         # eps 1e-2, theta 0.7, eps_amvm 1e-6, look-ahead 2, 5 sweeps; the
         # estimator, marking walk and refinement run on the device.  One
-        # untimed run first (like the matvec warm-up: the estimator's term
-        # buffers, ~2 GB, come out of the stream-ordered pool on first use),
-        # then a fresh assembly and the timed run
+        # untimed run first (the estimator's term buffers come out of the
+        # stream-ordered pool on first use), then a fresh assembly and the
+        # timed run
+        import torch as _t
         h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
         h.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, lookahead_steps=2, max_iterations=5)
         st4 = h.assemble(eps=cfg["eps"], beta=BETA_STOP, lookahead=2)
-        torch.cuda.synchronize()
+        _t.cuda.synchronize()
         t0 = time.perf_counter()
         _, rep = h.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, lookahead_steps=2,
                                  max_iterations=5)
@@ -581,17 +710,42 @@ def run_ours(args, cfg):
                         "gamma": [float(i.gamma) for i in rep.iterations],
                         "marked": [int(i.marked) for i in rep.iterations],
                         "ms_per_sweep": [float(i.ms) for i in rep.iterations],
-                        "warmup_runs": 1,
-                        "assembly_ms": st4.ms_total}
+                        "warmup_runs": 1, "assembly_ms": st4.ms_total}
+        if not args.no_cpu:
+            try:
+                line["amvm"]["cpu_reference"] = cpu_amvm_reference(cfg)
+            except Exception as e:
+                line["amvm"]["cpu_reference"] = {"error": str(e)}
+    if args.config == "c2" and world == 1 and not args.no_c3:
+        # the largest single-GPU config beside the headline (its own
+        # measurement, roofline and committed ncu traffic)
+        del h
+        torch.cuda.synchronize()
+        try:
+            c3cfg = dict(CONFIGS["c3"])
+            r3, h3, _ = measure(hm, torch, "c3", c3cfg, min(args.steps, 10),
+                                args.warmup, 1, 0, device, None)
+            obj = {"workload": "c3: " + c3cfg["desc"], "value": r3["value"], "unit": "dofs/s",
+                   "ms_per_step": r3["ms_per_step"], "roofline": r3["roofline"],
+                   "e2e": r3["e2e"], "assembly": r3["assembly"],
+                   "kernel_ms": r3["kernel_ms"], "clocks": r3["clocks"]}
+            if not args.no_cpu:
+                try:
+                    cb = cpu_reference(c3cfg, 2, 1, 5)
+                    obj["cpu_baseline"] = {k: cb[k] for k in
+                                           ("value", "unit", "cores", "kind", "sample")}
+                except Exception as e:
+                    obj["cpu_baseline"] = {"error": str(e)}
+            line["c3"] = obj
+            del h3
+        except Exception as e:  # secondary object: never costs the headline line
+            line["c3"] = {"error": str(e)}
     if args.config == "c2" and world == 1 and not args.no_galerkin:
-        try:  # secondary object: never costs the headline line
+        try:
+            mesh = hm.Mesh.icosphere(5)
             line["galerkin"] = galerkin_leg(hm, torch, mesh, cfg, device)
         except Exception as e:
             line["galerkin"] = {"error": str(e)}
-    if res is not None:
-        line["cpu_baseline"] = res["cpu_baseline"]
-        line["assembly"]["cpu_entries_per_s"] = res["assembly"]["value"]
-        line["assembly"]["cpu_cores"] = res["assembly"]["cores"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -609,6 +763,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-galerkin", action="store_true",
                     help="skip the Galerkin V_h object of the c2 line")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the c3 object of the c2 line")
     ap.add_argument("--nrhs", type=int, default=0,
                     help="override the config's number of right-hand sides")
     args = ap.parse_args()
@@ -620,6 +776,8 @@ def main():
         cfg["nrhs"] = args.nrhs
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_multi(args)
     return run_ours(args, cfg)
 
 

@@ -1957,6 +1957,75 @@ int or_voxel_surface(int n, double lo, double hi, int* nv, int* nt,
   });
 }
 
+// Synthetic BASELINE meshes (the reference ships none):
+// unit icosphere -- the icosahedron refined `level` times by edge midpoints
+// projected to the sphere (20 * 4^level triangles, outward winding) -- and
+// the ellipsoid (icosphere scaled by the semi-axes).  Stated here so the
+// reference arm of bench.py and the tests build the inputs without the
+// product package; tests/test_host.py checks they equal the product's
+// generators bit for bit.
+static void icosphere_mesh(int level, Mesh& m) {
+  if (level < 0 || level > 10) throw std::runtime_error("icosphere level out of range");
+  const Real g = (1.0 + std::sqrt(5.0)) / 2.0;
+  std::vector<Vec3> v = {{-1, g, 0}, {1, g, 0},  {-1, -g, 0}, {1, -g, 0},
+                         {0, -1, g}, {0, 1, g},  {0, -1, -g}, {0, 1, -g},
+                         {g, 0, -1}, {g, 0, 1},  {-g, 0, -1}, {-g, 0, 1}};
+  auto unit = [](Vec3 p) {
+    const Real r = std::sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]);
+    for (int d = 0; d < 3; ++d) p[d] /= r;
+    return p;
+  };
+  for (Vec3& p : v) p = unit(p);
+  std::vector<std::array<int, 3>> f = {
+      {0, 11, 5}, {0, 5, 1},  {0, 1, 7},   {0, 7, 10}, {0, 10, 11},
+      {1, 5, 9},  {5, 11, 4}, {11, 10, 2}, {10, 7, 6}, {7, 1, 8},
+      {3, 9, 4},  {3, 4, 2},  {3, 2, 6},   {3, 6, 8},  {3, 8, 9},
+      {4, 9, 5},  {2, 4, 11}, {6, 2, 10},  {8, 6, 7},  {9, 8, 1}};
+  for (int l = 0; l < level; ++l) {
+    std::map<std::pair<int, int>, int> cache;
+    auto mid = [&](int a, int b) {
+      const auto key = std::make_pair(std::min(a, b), std::max(a, b));
+      const auto it = cache.find(key);
+      if (it != cache.end()) return it->second;
+      Vec3 q;
+      for (int d = 0; d < 3; ++d) q[d] = 0.5 * (v[a][d] + v[b][d]);
+      v.push_back(unit(q));
+      cache[key] = static_cast<int>(v.size()) - 1;
+      return static_cast<int>(v.size()) - 1;
+    };
+    std::vector<std::array<int, 3>> nf;
+    nf.reserve(4 * f.size());
+    for (const auto& t : f) {
+      const int ab = mid(t[0], t[1]), bc = mid(t[1], t[2]), ca = mid(t[2], t[0]);
+      nf.push_back({t[0], ab, ca});
+      nf.push_back({t[1], bc, ab});
+      nf.push_back({t[2], ca, bc});
+      nf.push_back({ab, bc, ca});
+    }
+    f.swap(nf);
+  }
+  m.vertices = std::move(v);
+  m.triangles = std::move(f);
+}
+
+// icosphere (ax = ay = az = 1) or ellipsoid; verts == nullptr queries sizes
+int or_ellipsoid(int level, double ax, double ay, double az, int* nv, int* nt,
+                 double* verts, int* tris) {
+  return guard([&] {
+    Mesh m;
+    icosphere_mesh(level, m);
+    *nv = static_cast<int>(m.vertices.size());
+    *nt = m.nt();
+    if (verts) {
+      const double s[3] = {ax, ay, az};
+      for (int v = 0; v < *nv; ++v)
+        for (int d = 0; d < 3; ++d) verts[3 * v + d] = m.vertices[v][d] * s[d];
+      for (int t = 0; t < *nt; ++t)
+        for (int d = 0; d < 3; ++d) tris[3 * t + d] = m.triangles[t][d];
+    }
+  });
+}
+
 // geometry caches: centroids, areas, normals, diameters (mesh.cpp:229-247)
 int or_mesh_geometry(int nv, const double* verts, int nt, const int* tris,
                      double* centroids, double* areas, double* normals,

@@ -96,6 +96,20 @@ def voxel_surface(n: int, lo: float, hi: float):
     return v, t
 
 
+def ellipsoid(level: int, ax: float = 1.0, ay: float = 1.0, az: float = 1.0):
+    """icosphere (semi-axes 1) or ellipsoid mesh: (vertices, triangles)"""
+    nv, nt = C.c_int(), C.c_int()
+    _ck(lib().or_ellipsoid(level, D(ax), D(ay), D(az), C.byref(nv), C.byref(nt), None, None))
+    v = np.zeros((nv.value, 3))
+    t = np.zeros((nt.value, 3), np.int32)
+    _ck(lib().or_ellipsoid(level, D(ax), D(ay), D(az), C.byref(nv), C.byref(nt), _p(v), _p(t)))
+    return v, t
+
+
+def icosphere(level: int):
+    return ellipsoid(level)
+
+
 def mesh_geometry(verts, tris):
     v = np.ascontiguousarray(verts, dtype=np.float64)
     t = np.ascontiguousarray(tris, dtype=np.int32)

@@ -111,6 +111,25 @@ class RefProblem:
         _ck(lib().hmr_tree(self._h, _p(perm), _p(nodes), _p(blocks)))
         return perm, nodes, blocks
 
+    def restrict_rows(self, row_begin: int, row_end: int) -> None:
+        """Keep only the block rows inside [row_begin, row_end) (internal
+        positions): a bounded sample of the operator for CPU timing."""
+        _ck(lib().hmr_restrict_rows(self._h, int(row_begin), int(row_end)))
+        nb = C.c_int()
+        _ck(lib().hmr_info(self._h, None, C.byref(nb), None, None, None))
+        self.num_blocks = nb.value
+
+    def subtree_rows(self, depth: int):
+        """[begin, end) of the row-tree node reached from the root by
+        `depth` first-child steps (a 2^-depth sample of the rows)."""
+        _, nodes, _ = self.tree()
+        nd = 0
+        for _ in range(depth):
+            if nodes[nd, 2] < 0:
+                break
+            nd = nodes[nd, 2]
+        return int(nodes[nd, 0]), int(nodes[nd, 1])
+
     def entry(self, comp: int, i: int, j: int) -> float:
         out = C.c_double()
         _ck(lib().hmr_entry(self._h, int(comp), int(i), int(j), C.byref(out)))

@@ -141,13 +141,15 @@ struct hmr_problem {
   GammaContributions gamma;
 };
 
+#define HMR_API __attribute__((visibility("default")))
+
 extern "C" {
 
-const char* hmr_last_error() { return g_err.c_str(); }
+HMR_API const char* hmr_last_error() { return g_err.c_str(); }
 
 // kind 0: Kelvin centroid collocation (6 components, 3x3 grid); kind 1: the
 // reference's Newton CentroidKernelOracle fixture (1 component).
-int hmr_create(int kind, int nv, const double* xyz, int nt, const int* tri, double E,
+HMR_API int hmr_create(int kind, int nv, const double* xyz, int nt, const int* tri, double E,
                double nu, int b_min, double eta, hmr_problem** out) {
   return guard([&] {
     if (!out || !xyz || !tri) throw Error("null argument");
@@ -208,14 +210,14 @@ int hmr_create(int kind, int nv, const double* xyz, int nt, const int* tri, doub
   });
 }
 
-void hmr_destroy(hmr_problem* p) { delete p; }
+HMR_API void hmr_destroy(hmr_problem* p) { delete p; }
 
-int hmr_set_threads(int n) {
+HMR_API int hmr_set_threads(int n) {
   thread_cap() = n;
   return 0;
 }
 
-int hmr_partition_json(const hmr_problem* p, char* buf, long long* len) {
+HMR_API int hmr_partition_json(const hmr_problem* p, char* buf, long long* len) {
   return guard([&] {
     const std::string s = partition_to_json(*p->part);
     if (!buf) {
@@ -227,7 +229,7 @@ int hmr_partition_json(const hmr_problem* p, char* buf, long long* len) {
   });
 }
 
-int hmr_info(const hmr_problem* p, int* n, int* n_blocks, int* ncomp, int* c_sp, int* n_nodes) {
+HMR_API int hmr_info(const hmr_problem* p, int* n, int* n_blocks, int* ncomp, int* c_sp, int* n_nodes) {
   return guard([&] {
     if (n) *n = p->tree->size();
     if (n_blocks) *n_blocks = static_cast<int>(p->part->blocks.size());
@@ -239,7 +241,7 @@ int hmr_info(const hmr_problem* p, int* n, int* n_blocks, int* ncomp, int* c_sp,
 
 // perm[n]; nodes[n_nodes][4] = begin, end, child0, child1; blocks[nb][4] =
 // row_node, col_node, admissible, level
-int hmr_tree(const hmr_problem* p, int* perm, int* nodes4, int* blocks4) {
+HMR_API int hmr_tree(const hmr_problem* p, int* perm, int* nodes4, int* blocks4) {
   return guard([&] {
     if (perm) std::copy(p->tree->perm.begin(), p->tree->perm.end(), perm);
     if (nodes4)
@@ -261,13 +263,31 @@ int hmr_tree(const hmr_problem* p, int* perm, int* nodes4, int* blocks4) {
   });
 }
 
-int hmr_entry(const hmr_problem* p, int comp, long long i, long long j, double* out) {
+// bounded CPU samples: keep only the blocks whose row cluster lies inside
+// the internal row range [row_begin, row_end) (one subtree of the row tree);
+// the reference's assemble / matvec then run on that block-row sample
+// (call before hmr_assemble)
+HMR_API int hmr_restrict_rows(hmr_problem* p, int row_begin, int row_end) {
+  return guard([&] {
+    BlockPartition q = *p->part;
+    q.blocks.clear();
+    for (const Block& b : p->part->blocks) {
+      const ClusterNode& rn = p->tree->nodes[b.row_node];
+      if (rn.begin >= row_begin && rn.end <= row_end) q.blocks.push_back(b);
+    }
+    p->part = std::make_shared<const BlockPartition>(std::move(q));
+    p->h.clear();
+    p->op.reset();
+  });
+}
+
+HMR_API int hmr_entry(const hmr_problem* p, int comp, long long i, long long j, double* out) {
   return guard([&] { *out = p->oracles.at(comp)->entry(i, j); });
 }
 
 // assemble(part, oracle, cfg) per component (hmatrix.cpp:147-186); the grid
 // expression as evaluate_interior builds it (baca.cpp:669-687)
-int hmr_assemble(hmr_problem* p, double eps, double beta, int initial_rank, int lookahead,
+HMR_API int hmr_assemble(hmr_problem* p, double eps, double beta, int initial_rank, int lookahead,
                  long long max_rank) {
   return guard([&] {
     AssemblyConfig cfg;
@@ -293,7 +313,7 @@ int hmr_assemble(hmr_problem* p, double eps, double beta, int initial_rank, int 
 }
 
 // kcur / klook [ncomp][n_blocks]; -1 on dense blocks
-int hmr_ranks(const hmr_problem* p, int* kcur, int* klook) {
+HMR_API int hmr_ranks(const hmr_problem* p, int* kcur, int* klook) {
   return guard([&] {
     if (p->h.empty()) throw Error("assemble first");
     const int nb = static_cast<int>(p->part->blocks.size());
@@ -307,7 +327,7 @@ int hmr_ranks(const hmr_problem* p, int* kcur, int* klook) {
 }
 
 // storage_mb_current summed over the components, total pivots
-int hmr_storage(const hmr_problem* p, double* mb_current, long long* pivots) {
+HMR_API int hmr_storage(const hmr_problem* p, double* mb_current, long long* pivots) {
   return guard([&] {
     double mb = 0.0;
     long long piv = 0;
@@ -321,7 +341,7 @@ int hmr_storage(const hmr_problem* p, double* mb_current, long long* pivots) {
 }
 
 // U (m x K, column-major), V (n x K), pivots [K][2]; two-call protocol
-int hmr_factor(const hmr_problem* p, int comp, int block, int* m, int* n, int* K, int* kcur,
+HMR_API int hmr_factor(const hmr_problem* p, int comp, int block, int* m, int* n, int* K, int* kcur,
                double* U, double* V, int* piv) {
   return guard([&] {
     const HBlock& hb = p->h.at(comp)->block(block);
@@ -342,7 +362,7 @@ int hmr_factor(const hmr_problem* p, int comp, int block, int* m, int* n, int* K
 
 // y = A x through the reference's expression matvec (expr.cpp:197-215,
 // hmatrix.cpp:22-45); mode 0 current, 1 look-ahead
-int hmr_matvec(const hmr_problem* p, const double* x, double* y, int mode) {
+HMR_API int hmr_matvec(const hmr_problem* p, const double* x, double* y, int mode) {
   return guard([&] {
     if (!p->op) throw Error("assemble first");
     const Index n = p->op->cols();
@@ -354,7 +374,7 @@ int hmr_matvec(const hmr_problem* p, const double* x, double* y, int mode) {
 }
 
 // gamma_contributions over the expression (amvm.cpp:46-129)
-int hmr_gamma(hmr_problem* p, const double* x, double* gamma, double* difference,
+HMR_API int hmr_gamma(hmr_problem* p, const double* x, double* gamma, double* difference,
               int* n_terms) {
   return guard([&] {
     const Index n = p->op->cols();
@@ -371,7 +391,7 @@ int hmr_gamma(hmr_problem* p, const double* x, double* gamma, double* difference
 
 // mark_blocks on the last gamma (amvm.cpp:131-184): marked term indices and
 // the (component, block) of every term
-int hmr_mark(hmr_problem* p, double theta, int* marked, int* n_marked, double* gamma_pk,
+HMR_API int hmr_mark(hmr_problem* p, double theta, int* marked, int* n_marked, double* gamma_pk,
              int* term_comp_block) {
   return guard([&] {
     const int c_sp = operator_sparsity_constant(p->op);
@@ -393,7 +413,7 @@ int hmr_mark(hmr_problem* p, double theta, int* marked, int* n_marked, double* g
 
 // amvm_multiply (amvm.cpp:199-268) on the expression; iters8 rows:
 // k, gamma, gamma_pk, marked, cumulative_pivots, storage_mb, e_hat, 0
-int hmr_amvm(hmr_problem* p, const double* x, double theta, double eps_amvm,
+HMR_API int hmr_amvm(hmr_problem* p, const double* x, double theta, double eps_amvm,
              int lookahead_steps, int max_iterations, double* b, double* iters8, int* n_iters,
              int* converged) {
   return guard([&] {

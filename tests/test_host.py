@@ -242,3 +242,24 @@ def test_dof_layout_of_the_experiment_cube():
     for v in L.neumann_interior_nodes:
         assert not d[(T == v).any(axis=1)].any()
     assert len(L.t_dofs) == 3 * d.sum() and len(L.u_dofs) == 3 * len(L.neumann_interior_nodes)
+
+
+# ---- inputs shared with the reference arm (no product import there) -------
+def test_oracle_mesh_generators_match_product_bitwise():
+    for level in (0, 2, 5):
+        v, t = orc.icosphere(level)
+        a = hm.Mesh.icosphere(level).arrays()
+        assert (v == a["vertices"]).all() and (t == a["triangles"]).all()
+    v, t = orc.ellipsoid(4, 2.0, 1.0, 0.5)
+    a = hm.Mesh.ellipsoid(4, 2.0, 1.0, 0.5).arrays()
+    assert (v == a["vertices"]).all() and (t == a["triangles"]).all()
+
+
+def test_random_vector_streams_match_oracle():
+    """hm.random_vector: mt19937_64 + uniform_real_distribution(-1,1) (the
+    reference's random_vector, proj/tests/oracles.cpp:415-421) and
+    std::normal_distribution, identical to the oracle's streams."""
+    for seed in (0, 1, 3):
+        assert (hm.random_vector(5000, seed, "uniform") == orc.random_vector(5000, seed)).all()
+    for seed in (2, 4):
+        assert (hm.random_vector(5000, seed, "normal") == orc.normal_vector(5000, seed)).all()
