@@ -2512,6 +2512,48 @@ int or_entry(void* h, int comp, long i, long j, double* out) {
   return guard([&] { *out = P(h)->oracles[comp]->entry(i, j); });
 }
 
+// rows of the exact product A x from oracle entries (Kelvin grid): for each
+// requested output dof r*N + i, exact = sum_c sum_j A_rc(i, j) x[c*N + j]
+// and mag = sum |A_rc(i, j) x[c*N + j]| -- the checker of the H-matvec at
+// sizes where no dense matrix fits (config 5); rows x 64 column chunks in
+// parallel, the chunk sums added in order
+int or_rows_dot(void* h, int n, const long* out_dofs, const double* x, double* exact,
+                double* mag) {
+  return guard([&] {
+    Problem* p = P(h);
+    if (p->oracles.size() != 6) throw Error("or_rows_dot: Kelvin problems only");
+    const long N = p->oracles[0]->cols();
+    const int kChunks = 64;
+    const int comp_of[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    std::vector<double> pe(static_cast<size_t>(n) * kChunks), pm(pe.size());
+    parallel_for(static_cast<long>(n) * kChunks, [&](long w) {
+      const long q = w / kChunks, ch = w % kChunks;
+      const long r = out_dofs[q] / N, i = out_dofs[q] % N;
+      const long j0 = N * ch / kChunks, j1 = N * (ch + 1) / kChunks;
+      double e = 0.0, a = 0.0;
+      for (int c = 0; c < 3; ++c) {
+        const EntryOracle& o = *p->oracles[comp_of[r][c]];
+        for (long j = j0; j < j1; ++j) {
+          const double t = o.entry(i, j) * x[c * N + j];
+          e += t;
+          a += std::abs(t);
+        }
+      }
+      pe[w] = e;
+      pm[w] = a;
+    });
+    for (int q = 0; q < n; ++q) {
+      double e = 0.0, a = 0.0;
+      for (int ch = 0; ch < kChunks; ++ch) {
+        e += pe[static_cast<size_t>(q) * kChunks + ch];
+        a += pm[static_cast<size_t>(q) * kChunks + ch];
+      }
+      exact[q] = e;
+      mag[q] = a;
+    }
+  });
+}
+
 // dense component matrix (row-major m x n); comp for Kelvin in 0..5
 int or_dense(void* h, int comp, double* out) {
   return guard([&] {

@@ -309,6 +309,15 @@ class Problem:
         _ck(lib().or_entry_literal(self._h, int(comp), C.c_long(i), C.c_long(j), C.byref(out)))
         return out.value
 
+    def rows_dot(self, out_dofs, x):
+        """(exact, mag) of the requested rows of A x from oracle entries
+        (Kelvin grid; output dof r*N + i)."""
+        d = np.ascontiguousarray(out_dofs, dtype=np.int64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        ex, mg = np.zeros(len(d)), np.zeros(len(d))
+        _ck(lib().or_rows_dot(self._h, len(d), _p(d), _p(x), _p(ex), _p(mg)))
+        return ex, mg
+
     def dense(self, comp: int = 0) -> np.ndarray:
         out = np.zeros((self.n, self.ncols))
         _ck(lib().or_dense(self._h, int(comp), _p(out)))

@@ -2,11 +2,17 @@
 
 config 2 (20,480 triangles): the whole oracle assembly fits in seconds, so
 ranks / pivots are compared for every (component, block) and the matvec
-against the oracle's.  config 3 (196,608 triangles): the oracle's full
-assembly would take minutes, so parity is by sampling (near-field entries,
-ACA of individual blocks re-run by the oracle, rows of A x from oracle
-entries) plus size-independent properties (linearity, determinism).
-config 4 (81,920 triangles): the adaptive matvec's record, sweep by sweep."""
+against the oracle's.  config 3 (196,608 triangles): the oracle's whole
+assembly on all host threads (~1-2 min, ~45 GB of host memory): every rank
+and the matvec; the reference's own code (oracle/_ref) on a 1/16 block-row
+sample; plus sampled near-field entries, ACA blocks, rows of A x from
+oracle entries and size-independent properties (linearity, determinism).
+config 4 (81,920 triangles): the adaptive matvec's record, sweep by sweep.
+config 5 (1,310,720 triangles, 16 RHS): one 1/8 block-row shard (the
+per-GPU share at 8 GPUs) -- partition, sampled ACA blocks, rows of A x from
+oracle entries, and every one of the 16 columns against the 1-RHS sweep."""
+import os
+
 import numpy as np
 import pytest
 
@@ -65,6 +71,54 @@ def test_config3_partition_and_sampled_aca(c3):
         kc, K, fs, _ = o.aca_block(comp, int(b), eps=1e-5, beta=0.8, lookahead=2)
         assert (gk[comp, b], gl[comp, b]) == (kc, K), (b, comp)
         assert g.factor(comp, int(b))["frob_sq"] == fs
+
+
+def test_config3_full_parity(c3):
+    """Every (component, block) rank of config 3 and the whole matvec
+    against the oracle's full assembly (all host threads)."""
+    g, o = c3["g"], c3["o"]
+    orc.set_threads(os.cpu_count() or 1)
+    o.assemble(eps=1e-5, beta=0.8, lookahead=2)
+    gk, gl, gc, _ = g.ranks()
+    ok, ol, oc, _ = o.ranks()
+    adm = ok >= 0
+    assert np.abs(gk[adm] - ok[adm]).max() <= 2 and np.abs(gl[adm] - ol[adm]).max() <= 2
+    assert (gk == ok).all() and (gl == ol).all() and (gc == oc).all()  # canonical: identical
+    assert g.storage()["mb_current"] == pytest.approx(o.storage()["mb_current"], rel=1e-12)
+    x = hm.random_vector(g.cols, 2, "normal")
+    assert rel(g.matvec(x), o.matvec(x)) < 1e-12
+    assert rel(g.matvec(x, hm.Mode.Lookahead), o.matvec(x, 1)) < 1e-12
+
+
+def test_config3_reference_code_sample(c3):
+    """The reference's own assemble / matvec (oracle/_ref) on the block rows
+    of one 1/16 subtree of config 3's row tree: ranks within +-2 (observed
+    identical) and those rows of A x within 10 eps_ACA (observed ~1e-15)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    g, mesh = c3["g"], c3["mesh"]
+    a = mesh.arrays()
+    ref.set_threads(os.cpu_count() or 1)
+    r = ref.RefProblem(a["vertices"], a["triangles"], "kelvin", b_min=64, eta=1.0)
+    rb, re = r.subtree_rows(4)
+    r.restrict_rows(rb, re)
+    r.assemble(eps=1e-5, beta=0.8, lookahead=2)
+    t = g.tree()
+    blocks = g.partition_blocks()
+    keep = np.nonzero((t.nodes[blocks[:, 0], 0] >= rb) & (t.nodes[blocks[:, 0], 1] <= re))[0]
+    rk, rl = r.ranks()
+    gk, gl, _, _ = g.ranks()
+    gk, gl = gk[:, keep], gl[:, keep]
+    adm = rk >= 0
+    assert np.abs(gk[adm] - rk[adm]).max() <= 2 and np.abs(gl[adm] - rl[adm]).max() <= 2
+    assert (gk == rk).all() and (gl == rl).all()
+    x = hm.random_vector(g.cols, 2, "normal")
+    N = mesh.num_triangles
+    rows = np.concatenate([c * N + t.perm[rb:re] for c in range(3)])
+    yr = r.matvec(x)[rows]
+    yg = g.matvec(x)[rows]
+    assert rel(yg, yr) <= 10 * 1e-5 and rel(yg, yr) < 1e-12
 
 
 def test_config3_sampled_nearfield(c3):
@@ -133,3 +187,49 @@ def test_config4_amvm_matches_oracle():
     gk, gl, _, _ = g.ranks()
     ok, ol, _, _ = o.ranks()
     assert (gk == ok).all() and (gl == ol).all()
+
+
+def test_config5_shard():
+    """Config 5's per-GPU share at 8 GPUs: block-row shard 0 of 8 of the
+    1,310,720-triangle icosphere (163,840 rows, ~60 GB on the device)."""
+    eps = 1e-5
+    mesh = hm.Mesh.icosphere(8)
+    a = mesh.arrays()
+    g = hm.HMatrix.kelvin(mesh, b_min=64, eta=1.0, device=0, shard=(0, 8))
+    g.assemble(eps=eps, beta=0.8, lookahead=2)
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=64, eta=1.0)
+    assert (g.partition_blocks() == o.blocks()).all()
+    t = g.tree()
+    assert (t.perm == o.tree()[2]).all()
+    rb, re = g.row_range
+    blocks = g.partition_blocks()
+    owned = (t.nodes[blocks[:, 0], 0] >= rb) & (t.nodes[blocks[:, 0], 1] <= re)
+    adm = np.nonzero(owned & (blocks[:, 2] == 1))[0]
+    gk, gl, _, _ = g.ranks()
+    assert (gk[:, owned & (blocks[:, 2] == 1)] >= 0).all()
+    assert (gk[:, ~owned] == -1).all()
+    # sampled ACA blocks re-run by the oracle: bit-identical state
+    sizes = t.nodes[blocks[adm, 0], 1] - t.nodes[blocks[adm, 0], 0]
+    rng = np.random.default_rng(5)
+    pick = list(adm[np.argsort(-sizes)[:4]]) + list(rng.choice(adm, 24, replace=False))
+    for b in pick:
+        comp = int(rng.integers(0, 6))
+        kc, K, fs, _ = o.aca_block(comp, int(b), eps=eps, beta=0.8, lookahead=2)
+        assert (gk[comp, b], gl[comp, b]) == (kc, K), (b, comp)
+        assert g.factor(comp, int(b))["frob_sq"] == fs
+    # 16 RHS (fp64 tensor-core sweep) against 16 single-RHS sweeps
+    n = g.cols
+    X = np.asfortranarray(hm.random_vector(n * 16, 4, "normal").reshape(16, n).T)
+    Y = g.matvec(X)
+    for q in range(16):
+        yq = g.matvec(np.ascontiguousarray(X[:, q]))
+        assert rel(Y[:, q], yq) < 1e-13, q
+    # rows of A x from oracle entries: the H-approximation within 10 eps
+    N = mesh.num_triangles
+    orc.set_threads(os.cpu_count() or 1)
+    own_rows = t.perm[rb:re]
+    dofs = np.concatenate([c * N + rng.choice(own_rows, 8, replace=False) for c in range(3)])
+    exact, mag = o.rows_dot(dofs, X[:, 0])
+    got = Y[dofs, 0]
+    assert np.all(np.abs(got - exact) <= 10 * eps * mag)
+    assert np.linalg.norm(got - exact) <= 10 * eps * np.linalg.norm(exact)
