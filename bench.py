@@ -680,15 +680,6 @@ def run_ours(args, cfg):
         "assembly": res["assembly"],
         "kernel_ms": res["kernel_ms"],
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        depth = {"c3": 5, "c5": 9}.get(args.config, 0)
-        try:
-            cb = cpu_reference(cfg, 3, 1, depth)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            line["assembly"]["cpu_reference_s"] = cb["assembly_s"]
-            line["assembly"]["cpu_reference_cores"] = cb["assembly_cores"]
-        except Exception as e:
-            line["cpu_baseline"] = {"error": str(e)}
     if args.config == "c4" and world == 1:
         # the adaptive matvec of config 4 (Algorithm 2): full-mode assembly at
         # eps 1e-2, theta 0.7, eps_amvm 1e-6, look-ahead 2, 5 sweeps; the
@@ -711,15 +702,10 @@ def run_ours(args, cfg):
                         "marked": [int(i.marked) for i in rep.iterations],
                         "ms_per_sweep": [float(i.ms) for i in rep.iterations],
                         "warmup_runs": 1, "assembly_ms": st4.ms_total}
-        if not args.no_cpu:
-            try:
-                line["amvm"]["cpu_reference"] = cpu_amvm_reference(cfg)
-            except Exception as e:
-                line["amvm"]["cpu_reference"] = {"error": str(e)}
     if args.config == "c2" and world == 1 and not args.no_c3:
         # the largest single-GPU config beside the headline (its own
         # measurement, roofline and committed ncu traffic)
-        del h
+        h = None
         torch.cuda.synchronize()
         try:
             c3cfg = dict(CONFIGS["c3"])
@@ -729,13 +715,6 @@ def run_ours(args, cfg):
                    "ms_per_step": r3["ms_per_step"], "roofline": r3["roofline"],
                    "e2e": r3["e2e"], "assembly": r3["assembly"],
                    "kernel_ms": r3["kernel_ms"], "clocks": r3["clocks"]}
-            if not args.no_cpu:
-                try:
-                    cb = cpu_reference(c3cfg, 2, 1, 5)
-                    obj["cpu_baseline"] = {k: cb[k] for k in
-                                           ("value", "unit", "cores", "kind", "sample")}
-                except Exception as e:
-                    obj["cpu_baseline"] = {"error": str(e)}
             line["c3"] = obj
             del h3
         except Exception as e:  # secondary object: never costs the headline line
@@ -746,6 +725,30 @@ def run_ours(args, cfg):
             line["galerkin"] = galerkin_leg(hm, torch, mesh, cfg, device)
         except Exception as e:
             line["galerkin"] = {"error": str(e)}
+    # ---- the CPU legs last: their host-memory churn (tens of GB allocated
+    # and returned) must not sit before any timed GPU region ----
+    if rank == 0 and world == 1 and not args.no_cpu:
+        h = None
+        depth = {"c3": 5, "c5": 9}.get(args.config, 0)
+        try:
+            cb = cpu_reference(cfg, 3, 1, depth)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["assembly"]["cpu_reference_s"] = cb["assembly_s"]
+            line["assembly"]["cpu_reference_cores"] = cb["assembly_cores"]
+        except Exception as e:
+            line["cpu_baseline"] = {"error": str(e)}
+        if isinstance(line.get("c3"), dict) and "value" in line["c3"]:
+            try:
+                cb = cpu_reference(dict(CONFIGS["c3"]), 2, 1, 5)
+                line["c3"]["cpu_baseline"] = {k: cb[k] for k in
+                                              ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:
+                line["c3"]["cpu_baseline"] = {"error": str(e)}
+        if "amvm" in line:
+            try:
+                line["amvm"]["cpu_reference"] = cpu_amvm_reference(cfg)
+            except Exception as e:
+                line["amvm"]["cpu_reference"] = {"error": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
