@@ -58,7 +58,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
                "-Xcompiler", "-ffp-contract=off", "-I", INC, "-shared", "-cudart",
                "static", "-o", gpu_so, os.path.join(GPU_SRC, "hmgpu.cu")]
         if verbose_ptxas:
-            cmd.insert(4, "-Xptxas=-v")
+            cmd.insert(3, "-Xptxas=-v")
         _run(cmd)
     host_so = os.path.join(LIB, "libhmbem.so")
     host_deps = _glob(HOST_SRC, (".cpp", ".hpp")) + [os.path.join(INC, "hmbem.h"),

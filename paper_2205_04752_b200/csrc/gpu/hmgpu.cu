@@ -479,19 +479,20 @@ struct hmgpu_ctx {
   bool am_have_estimate = false;
   std::vector<int> marked_ids;
 
-  // ---- multi-RHS (16 per pass, fp64 tensor cores) plan ----
+  // ---- multi-RHS (16 per pass, fp64 tensor cores) plan (hmgpu_mrhs.cuh) ----
   bool p16_valid = false;
   int p16_mode = -1;
-  int n_z16 = 0, n_zs16 = 0, n_tiles16 = 0;
-  long long p16_zsize = 0;
-  DBuf<Z16Task> d_z16;
-  DBuf<Z16Sum> d_zs16;
-  DBuf<long long> d_zb16;
-  DBuf<int> d_rk16;
-  DBuf<int2> d_tiles16, d_zp2, d_zp4;
+  int p16_ns = 2, p16_stage = 0, p16_ncta = 0;
+  long long p16_zsize = 0, p16_alen = 0;
+  int n_zch16 = 0, n_yst16 = 0;
+  DBuf<ZChunk16> d_zch16;
+  DBuf<ZTask16> d_ztask16;
+  DBuf<M16Stage> d_yst16;
+  DBuf<YItem16> d_yitem16;
+  DBuf<M16Copy> d_ycopy16;
+  DBuf<int> d_zcoff16, d_ycoff16;
+  DBuf<double> d_p16arena, d_z16buf, d_xp16;
   DBuf<AdmBlock> d_ablocks;
-  int n_zp2 = 0, n_zp4 = 0;
-  DBuf<double> d_zpart16, d_xi16;
   DBuf<int> d_pleaf_ptr;
   std::vector<int> p_leaf_ptr;
 
@@ -537,8 +538,9 @@ struct hmgpu_ctx {
     d_xi.free(); d_ypart.free();
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
-    d_z16.free(); d_zs16.free(); d_zb16.free(); d_zpart16.free(); d_xi16.free();
-    d_rk16.free(); d_tiles16.free(); d_zp2.free(); d_zp4.free(); d_ablocks.free();
+    d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free();
+    d_yitem16.free(); d_ycopy16.free();
+    d_p16arena.free(); d_z16buf.free(); d_xp16.free(); d_ablocks.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
     d_ptr.free(); d_lists.free(); d_order.free(); d_idx.free(); d_marked.free(); d_nm.free();
     d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
@@ -1715,99 +1717,483 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
                  wslots, entries.size(), c->p_smem);
 }
 
-// multi-RHS plan: phase-1 tasks per (admissible block, 128-column chunk),
-// the blocks' Z regions [nz][K][32]; phase 2 runs per leaf (leaf_blk)
+// ---- multi-RHS plan (hmgpu_mrhs.cuh) ----------------------------------------
+// HMGPU_M16_CFG="ns,stage": ring depth (3, 4, 6 or 9) and doubles per stage
+struct M16Cfg {
+  int ns = 3, stage = 4608;
+};
+M16Cfg m16_cfg() {
+  static const M16Cfg cfg = [] {
+    M16Cfg r;
+    int a, b;
+    const char* e = std::getenv("HMGPU_M16_CFG");
+    if (e && std::sscanf(e, "%d,%d", &a, &b) == 2) {
+      r.ns = a;
+      r.stage = b;
+    }
+    return r;
+  }();
+  return cfg;
+}
+
+// contiguous runs of work units over ncta CTAs with about equal bytes:
+// first[k] = first unit of CTA k, first[ncta] = number of units
+std::vector<int> split_runs(const std::vector<long long>& bytes, int ncta) {
+  long long total = 0;
+  for (long long b : bytes) total += b;
+  const double share = std::max(1.0, (double)total / ncta);
+  std::vector<int> first(ncta + 1, 0);
+  long long cum = 0;
+  int k = 0;
+  for (size_t u = 0; u < bytes.size(); ++u) {
+    const int owner =
+        (int)std::min<double>(ncta - 1, std::floor((cum + 0.5 * bytes[u]) / share));
+    while (k < owner) first[++k] = (int)u;
+    cum += bytes[u];
+  }
+  while (k < ncta) first[++k] = (int)bytes.size();
+  return first;
+}
+
+// Multi-RHS plan: phase-1 tasks (block, <= 64 l of its components) with
+// their column chunks, phase-2 stages per leaf, the p16 arena (current-rank
+// factors re-packed in stage order, zero padded to the conflict-free
+// pitches), the Z layout and the per-CTA runs of both passes.
 void build_plan16(hmgpu_ctx* c, int mode) {
-  std::vector<Z16Task> zt;
-  std::vector<Z16Sum> zsum;
-  std::vector<long long> zb(std::max(c->n_mv, 1), 0);
-  std::vector<int> rk(8 * (size_t)std::max(c->n_mv, 1), 0);
+  const M16Cfg cfg = m16_cfg();
+  if ((cfg.ns != 3 && cfg.ns != 4 && cfg.ns != 6 && cfg.ns != 9) || cfg.stage < 2048 || (cfg.stage & 3))
+    fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_CFG");
+  const int SD = cfg.stage - M16_HDR;  // data doubles per stage
+  const int nb = c->n_mv;
+  std::vector<std::array<int, 6>> rk(std::max(nb, 1)), zo(std::max(nb, 1));
+  std::vector<long long> zb(std::max(nb, 1), -1);
   long long zsize = 0;
-  for (int bi = 0; bi < c->n_mv; ++bi) {
+  for (int bi = 0; bi < nb; ++bi) {
     const MvBlock& mb = c->mvb[bi];
+    rk[bi].fill(0);
+    zo[bi].fill(0);
     if (mb.dense) continue;
-    int K = 0;
+    int K = 0, z4 = 0;
     for (int q = 0; q < 6; ++q) {
       const Item& it = c->items[mb.item0 + q];
-      rk[8 * bi + q] = mode ? it.k : it.kcur;
-      K += rk[8 * bi + q];
+      const int k = mode ? it.k : it.kcur;
+      if (k > 255) fail(HMGPU_ERR_INVALID, "rank above 255 for the multi-RHS sweep");
+      rk[bi][q] = k;
+      zo[bi][q] = z4;
+      z4 += (k + 3) & ~3;
+      K += k;
     }
-    rk[8 * bi + 6] = K;
     if (K == 0) continue;
-    const int nz = (mb.n + JC - 1) / JC;
     zb[bi] = zsize;
-    zsize += (long long)nz * K * 32;
-    for (int z = 0; z < nz; ++z)
-      zt.push_back({bi, z * JC, std::min(JC, mb.n - z * JC), z, zb[bi]});
-    if (nz > 1) zsum.push_back({zb[bi], K * 32, nz});
+    zsize += (long long)z4 * ZP;
   }
-  // phase-1 work: (task, component) pairs, rank <= 16 and > 16 separately
-  std::vector<int2> p2, p4;
-  for (size_t ti = 0; ti < zt.size(); ++ti) {
-    const int bi = zt[ti].blk;
-    for (int q = 0; q < 6; ++q) {
-      const int k = rk[8 * bi + q];
-      if (k == 0) continue;
-      (k <= 16 ? p2 : p4).push_back(make_int2((int)ti, q));
+  std::vector<PackDesc> packs;
+  long long alen = 0;
+
+  // ---- phase 1: tasks and their chunks
+  std::vector<ZTask16> tasks;
+  std::vector<ZChunk16> zch;
+  std::vector<long long> tbytes;
+  std::vector<int> tptr{0};
+  struct Seg {
+    int c, lo, hi;
+  };
+  std::vector<Seg> segs, grp;
+  for (int bi = 0; bi < nb; ++bi) {
+    if (zb[bi] < 0) continue;
+    const MvBlock& mb = c->mvb[bi];
+    const int n = mb.n;
+    segs.clear();
+    for (int q = 0; q < 6; ++q)
+      for (int lo = 0; lo < rk[bi][q]; lo += 64)
+        segs.push_back({q, lo, std::min(rk[bi][q], lo + 64)});
+    size_t si = 0;
+    while (si < segs.size()) {
+      grp.clear();
+      int L = 0;
+      while (si < segs.size() && grp.size() < 6 && L + (segs[si].hi - segs[si].lo) <= 64) {
+        L += segs[si].hi - segs[si].lo;
+        grp.push_back(segs[si++]);
+      }
+      ZTask16 tk{};
+      tk.zdst = zb[bi];
+      int vr = 0, grows[3] = {0, 0, 0}, gn[3] = {0, 0, 0};
+      static const int kR[6] = {0, 0, 0, 1, 1, 2}, kC[6] = {0, 1, 2, 1, 2, 2};
+      for (size_t e = 0; e < grp.size(); ++e) {
+        const Seg& sg = grp[e];
+        const int len = sg.hi - sg.lo, cr = kR[sg.c], cc = kC[sg.c];
+        tk.len[e] = (unsigned char)len;
+        tk.vrow[e] = (unsigned char)vr;
+        tk.zrow[e] = (short)(zo[bi][sg.c] + sg.lo);
+        vr += len;
+        // Z_c = V_c^T x_C (part 0); W_c = V_c^T x_R (part 1, off-diagonal)
+        tk.gent[cc][gn[cc]++] = (unsigned char)(e << 1);
+        grows[cc] += len;
+        if (cr != cc) {
+          tk.gent[cr][gn[cr]++] = (unsigned char)((e << 1) | 1);
+          grows[cr] += len;
+        }
+      }
+      tk.gtile[0] = 0;
+      for (int r = 0; r < 3; ++r) {
+        tk.gn[r] = (unsigned char)gn[r];
+        tk.grows[r] = (unsigned char)grows[r];
+        tk.gtile[r + 1] = (unsigned char)(tk.gtile[r] + (grows[r] + 7) / 8);
+      }
+      tk.ntiles = tk.gtile[3];
+      // widest chunk whose V^T and X rows fit one stage
+      int jc = std::min(n, 252);
+      while (jc > 4 && (long long)(L + XP) * cf_pitch(jc) > SD) jc -= 4;
+      if ((long long)(L + XP) * cf_pitch(jc) > SD)
+        fail(HMGPU_ERR_INVALID, "multi-RHS stage too small");
+      const int ti = (int)tasks.size();
+      tasks.push_back(tk);
+      long long by = 0;
+      const int nch = (n + jc - 1) / jc;
+      for (int q = 0; q < nch; ++q) {
+        const int j0 = q * jc, jj = std::min(jc, n - j0), Pp = cf_pitch(jj);
+        ZChunk16 ch{};
+        ch.vsrc = alen;
+        ch.vlen = L * Pp;
+        ch.xcol = mb.col0 + j0;
+        ch.P = Pp;
+        ch.task = ti;
+        ch.flags = (q == 0 ? 1 : 0) | (q == nch - 1 ? 2 : 0);
+        for (size_t e = 0; e < grp.size(); ++e) {
+          const Seg& sg = grp[e];
+          packs.push_back(PackDesc{c->items[mb.item0 + sg.c].v_off + (long long)sg.lo * n + j0,
+                                   alen + (long long)tk.vrow[e] * Pp, n, Pp, jj,
+                                   sg.hi - sg.lo, 0, 0});
+        }
+        alen += (long long)L * Pp;
+        by += (long long)L * Pp + (long long)Pp * XP;
+        zch.push_back(ch);
+      }
+      tbytes.push_back(by);
+      tptr.push_back((int)zch.size());
     }
   }
-  std::vector<int2> tiles;
-  for (size_t l = 0; l < c->leaf_begin.size(); ++l) {
-    const int rows = c->leaf_end[l] - c->leaf_begin[l];
-    for (int tt = 0; tt * 8 * TR < rows; ++tt) tiles.push_back(make_int2((int)l, tt));
+
+  // ---- phase 2: pieces per leaf, the covering blocks in leaf_blk order (each
+  // piece fits a stage after the item records)
+  const int SDY = cfg.stage - Y16_HDR;
+  // A/B switch (timing experiments): HMGPU_M16_SKIP=1 / 2 leaves out the
+  // near-field / low-rank pieces (wrong products)
+  static const int skip = [] {
+    const char* e = std::getenv("HMGPU_M16_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  std::vector<YStage16> yst;
+  std::vector<long long> lbytes;
+  std::vector<int> lptr{0};
+  const int nl = (int)c->leaf_begin.size();
+  for (int L = 0; L < nl; ++L) {
+    const int R = c->leaf_end[L] - c->leaf_begin[L];
+    if (R > 64) fail(HMGPU_ERR_INVALID, "leaf above 64 rows for the multi-RHS sweep");
+    const int PR = cf_pitch(R);
+    const size_t first = yst.size();
+    long long by = 0;
+    for (int e = c->leaf_ptr[L]; e < c->leaf_ptr[L + 1]; ++e) {
+      const int bi = c->leaf_blk[e].x, roff = c->leaf_blk[e].y;
+      const MvBlock& mb = c->mvb[bi];
+      if (mb.dense) {
+        if (skip == 1) continue;
+        const long long cp = align2(6LL * mb.m);
+        const int PD = cf_pitch(6 * mb.m);
+        const int jd = (SDY / (PD + XP)) & ~3;
+        if (jd < 4) fail(HMGPU_ERR_INVALID, "near-field block too tall for the multi-RHS stage");
+        for (int j0 = 0; j0 < mb.n; j0 += jd) {
+          const int jj = std::min(jd, mb.n - j0);
+          YStage16 d{};
+          d.kind = Y16_DENSE;
+          d.leaf = L;
+          d.R = R;
+          d.src = mb.dense_off + (long long)j0 * cp;
+          d.len = 6 * mb.m;
+          d.spitch = (int)cp;
+          d.PR = PD;
+          d.jd = jj;
+          d.src2 = mb.col0 + j0;
+          d.len2 = ((jj + 3) & ~3) * XP;
+          d.m = mb.m;
+          d.roff = roff;
+          yst.push_back(d);
+          by += (long long)jj * 6 * mb.m + d.len2;
+        }
+        continue;
+      }
+      if (zb[bi] < 0 || skip == 2) continue;
+      YStage16 d{};
+      bool open = false;
+      int used = 0;
+      auto flush = [&]() {
+        yst.push_back(d);
+        by += d.len + d.len2;
+        open = false;
+      };
+      for (int q = 0; q < 6; ++q) {
+        const int k = rk[bi][q], k4 = (k + 3) & ~3;
+        int lo = 0;
+        while (lo < k) {
+          if (!open) {
+            d = YStage16{};
+            d.kind = Y16_ADM;
+            d.leaf = L;
+            d.R = R;
+            d.PR = PR;
+            d.src = alen;
+            d.src2 = zb[bi] + (long long)(zo[bi][q] + lo) * ZP;
+            used = 0;
+            open = true;
+          }
+          const int left = SDY - used, rest = k - lo;
+          int take = rest;
+          if ((long long)rest * PR + (long long)(k4 - lo) * ZP > left)
+            take = std::min(rest - 1, left / (PR + ZP)) & ~3;
+          if (take <= 0) {
+            if (used == 0) fail(HMGPU_ERR_INVALID, "multi-RHS stage too small");
+            flush();
+            continue;
+          }
+          const int hi = lo + take;
+          d.lo[q] = (unsigned char)lo;
+          d.hi[q] = (unsigned char)hi;
+          packs.push_back(PackDesc{c->items[mb.item0 + q].u_off + (long long)lo * mb.m + roff,
+                                   alen, mb.m, PR, R, take, 0, 0});
+          alen += (long long)take * PR;
+          const int zrows = ((hi + 3) & ~3) - lo;
+          d.len += take * PR;
+          d.len2 += zrows * ZP;
+          used += take * PR + zrows * ZP;
+          lo = hi;
+          if (hi < k) flush();  // the component continues in the next stage
+        }
+      }
+      if (open) flush();
+    }
+    if (yst.size() == first) {  // no contribution: the leaf's rows are written as 0
+      YStage16 d{};
+      d.kind = Y16_ADM;
+      d.leaf = L;
+      d.R = R;
+      d.PR = PR;
+      yst.push_back(d);
+    }
+    yst[first].flags |= 1;
+    yst.back().flags |= 2;
+    lbytes.push_back(std::max<long long>(by, 1));
+    lptr.push_back((int)yst.size());
   }
-  c->d_z16.upload(zt, c->stream);
-  c->d_zs16.upload(zsum, c->stream);
-  c->d_zb16.upload(zb, c->stream);
-  c->d_rk16.upload(rk, c->stream);
-  c->d_tiles16.upload(tiles, c->stream);
-  if (!p2.empty()) c->d_zp2.upload(p2, c->stream);
-  if (!p4.empty()) c->d_zp4.upload(p4, c->stream);
-  c->n_zp2 = (int)p2.size();
-  c->n_zp4 = (int)p4.size();
-  c->d_zpart16.ensure((size_t)std::max<long long>(zsize, 1));
-  c->d_xi16.ensure((size_t)c->n_cols * 48);
-  c->n_z16 = (int)zt.size();
-  c->n_zs16 = (int)zsum.size();
-  c->n_tiles16 = (int)tiles.size();
+
+  // ---- per-CTA runs (up to 3 CTAs per SM, as many as their rings fit):
+  // phase 1 by tasks, phase 2 by leaves (a leaf's accumulators live in one
+  // CTA); within a CTA's leaves, consecutive pieces are packed into stages
+  // of up to Y16_MAXIT items, their records and bulk copies
+  const size_t ring_bytes = (size_t)cfg.ns * cfg.stage * sizeof(double);
+  const int per_sm = std::max(1, std::min(3, (int)((227 * 1024) / (ring_bytes + 1024))));
+  if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
+  const int ncta = c->sm_count * per_sm;
+  std::vector<int> zcoff(ncta + 1), ycoff(ncta + 1);
+  std::vector<M16Stage> ystages;
+  std::vector<YItem16> yitems;
+  std::vector<M16Copy> ycopies;
+  std::vector<unsigned char> ckind;  // copy source: 0 items, 1 p16 arena, 2 Z, 3 dense, 4 x
+  {
+    const std::vector<int> ft = split_runs(tbytes, ncta);
+    for (int k = 0; k <= ncta; ++k) zcoff[k] = tptr[ft[k]];
+    const std::vector<int> fl = split_runs(lbytes, ncta);
+    const int SD2 = cfg.stage - Y16_HDR;
+    auto plen = [](const YStage16& d) -> long long {
+      return d.kind == Y16_ADM ? (long long)d.len + d.len2 : (long long)d.jd * d.PR + d.len2;
+    };
+    auto copy = [&](int kind, long long src_bytes, long long dst, long long bytes) {
+      ycopies.push_back(M16Copy{(unsigned long long)src_bytes, (int)dst, (int)bytes});
+      ckind.push_back((unsigned char)kind);
+    };
+    for (int k = 0; k < ncta; ++k) {
+      ycoff[k] = (int)ystages.size();
+      const int p1 = lptr[fl[k + 1]];
+      for (int pi = lptr[fl[k]]; pi < p1;) {
+        int pe = pi;
+        long long used = 0;
+        while (pe < p1 && pe - pi < Y16_MAXIT && used + plen(yst[pe]) <= SD2)
+          used += plen(yst[pe++]);
+        if (pe == pi) fail(HMGPU_ERR_INVALID, "multi-RHS piece larger than a stage");
+        M16Stage st{};
+        st.cbeg = (int)ycopies.size();
+        st.nitems = pe - pi;
+        const size_t rec = yitems.size();
+        YItem16 cnt{};
+        cnt.kind = st.nitems;  // the count record (first int of the stage)
+        yitems.push_back(cnt);
+        copy(0, (long long)rec * (long long)sizeof(YItem16), 0,
+             (long long)sizeof(YItem16) * (1 + st.nitems));
+        long long off = Y16_HDR, bytes = (long long)sizeof(YItem16) * (1 + st.nitems);
+        for (int q = pi; q < pe; ++q) {
+          const YStage16& d = yst[q];
+          YItem16 it{};
+          it.kind = d.kind;
+          it.leaf = d.leaf;
+          it.flags = d.flags;
+          it.R = d.R;
+          it.PR = d.PR;
+          it.jd = d.jd;
+          it.m = d.m;
+          it.roff = d.roff;
+          std::copy(d.lo, d.lo + 6, it.lo);
+          std::copy(d.hi, d.hi + 6, it.hi);
+          it.off1 = (int)off;
+          if (d.kind == Y16_ADM) {
+            it.off2 = (int)(off + d.len);
+            if (d.len) copy(1, 8 * d.src, off, 8LL * d.len);
+            if (d.len2) copy(2, 8 * d.src2, off + d.len, 8LL * d.len2);
+          } else {
+            it.off2 = (int)(off + (long long)d.jd * d.PR);
+            for (int j = 0; j < d.jd; ++j)
+              copy(3, 8 * (d.src + (long long)j * d.spitch), off + (long long)j * d.PR,
+                   8LL * d.len);
+            copy(4, 8 * d.src2 * XP, it.off2, 8LL * d.len2);
+          }
+          bytes += d.kind == Y16_ADM ? 8LL * (d.len + d.len2)
+                                     : 8LL * ((long long)d.jd * d.len + d.len2);
+          off += plen(d);
+          yitems.push_back(it);
+        }
+        st.ncopies = (int)ycopies.size() - st.cbeg;
+        st.bytes = (int)bytes;
+        ystages.push_back(st);
+        pi = pe;
+      }
+    }
+    ycoff[ncta] = (int)ystages.size();
+  }
+  c->d_zch16.upload(zch, c->stream);
+  c->d_ztask16.upload(tasks, c->stream);
+  c->d_zcoff16.upload(zcoff, c->stream);
+  c->d_ycoff16.upload(ycoff, c->stream);
+  c->d_yst16.upload(ystages, c->stream);
+  c->d_yitem16.upload(yitems, c->stream);
+  c->d_z16buf.ensure((size_t)zsize + 2);
+  // rows past k_c of a component's last l-step stay zero (A is zero there)
+  CK(cudaMemsetAsync(c->d_z16buf.p, 0, ((size_t)zsize + 2) * sizeof(double), c->stream));
+  c->d_xp16.ensure(((size_t)c->n_cols + M16_XPAD) * XP);
+  CK(cudaMemsetAsync(c->d_xp16.p, 0, c->d_xp16.n * sizeof(double), c->stream));
+  c->d_p16arena.ensure((size_t)alen + 2);
+  CK(cudaMemsetAsync(c->d_p16arena.p, 0, ((size_t)alen + 2) * sizeof(double), c->stream));
+  {
+    const unsigned long long base[5] = {
+        (unsigned long long)c->d_yitem16.p, (unsigned long long)c->d_p16arena.p,
+        (unsigned long long)c->d_z16buf.p, (unsigned long long)c->d_dense.p,
+        (unsigned long long)c->d_xp16.p};
+    for (size_t q = 0; q < ycopies.size(); ++q) ycopies[q].src += base[ckind[q]];
+    c->d_ycopy16.upload(ycopies, c->stream);
+  }
+  if (!packs.empty()) {
+    DBuf<PackDesc> d_packs;
+    d_packs.upload(packs, c->stream);
+    c->timed("pack16", [&] {
+      pack_kernel<<<grid_for(c, ((long long)packs.size() + 7) / 8, 16), 256, 0, c->stream>>>(
+          d_packs.p, (int)packs.size(), c->d_arena.p, c->d_p16arena.p);
+    });
+    c->sync();
+    d_packs.free();
+  }
+  c->n_zch16 = (int)zch.size();
+  c->n_yst16 = (int)ystages.size();
+  c->p16_ns = cfg.ns;
+  c->p16_stage = cfg.stage;
+  c->p16_ncta = ncta;
   c->p16_zsize = zsize;
+  c->p16_alen = alen;
   c->p16_mode = mode;
   c->p16_valid = true;
   c->sync();
+  if (verbose())
+    std::fprintf(stderr, "[hmgpu] plan16: tasks=%zu chunks=%zu stages=%zu arena=%.3f GB "
+                         "Z=%.3f GB ctas=%d ring=%zu B\n",
+                 tasks.size(), zch.size(), ystages.size(), 8.0 * alen / 1e9, 8.0 * zsize / 1e9,
+                 ncta, ring_bytes);
+}
+
+template <int NS>
+void launch_m16(hmgpu_ctx* c, M16Params P, bool zpass) {
+  const size_t smem = (size_t)NS * c->p16_stage * sizeof(double);
+  if (zpass) {
+    CK(cudaFuncSetAttribute(hmv16_z_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    hmv16_z_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
+  } else {
+    CK(cudaFuncSetAttribute(hmv16_y_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    hmv16_y_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
+  }
+  CK(cudaGetLastError());
 }
 
 void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode) {
   (void)mode;  // the plan carries the mode's ranks
+  M16Params P{};
+  P.tasks = c->d_ztask16.p;
+  P.arena = c->d_p16arena.p;
+  P.dense = c->d_dense.p;
+  P.xp = c->d_xp16.p;
+  P.z = c->d_z16buf.p;
+  P.leaf_begin = c->d_leaf_begin.p;
+  P.rperm = c->yperm();
+  P.y = dy;
+  P.nrows = c->ynrows();
+  P.stage = c->p16_stage;
+  static const int dbg = [] {
+    const char* e = std::getenv("HMGPU_M16_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  P.dbg = dbg;
+  static DBuf<unsigned long long> prof;
+  if (dbg == 3) {
+    prof.ensure(8);
+    CK(cudaMemsetAsync(prof.p, 0, 64, c->stream));
+    P.prof = prof.p;
+  }
   for (int s0 = 0; s0 < nrhs; s0 += MR) {
     const int nr = std::min(MR, nrhs - s0);
+    P.s0 = s0;
+    P.nr = nr;
     c->timed("gather", [&] {
       const long long total = 48LL * c->n_cols;
       gather16_kernel<<<grid_for(c, (total + 255) / 256, 16), 256, 0, c->stream>>>(
-          dx, c->d_xi16.p, c->d_cperm.p, c->n_cols, s0, nr);
+          dx, c->d_xp16.p, c->d_cperm.p, c->n_cols, s0, nr);
     });
-    if (c->n_z16 > 0)
+    if (c->n_zch16 > 0)
       c->timed("hmv16_z", [&] {
-        if (c->n_zp2 > 0)
-          hmv16_z_kernel<2><<<grid_for(c, (c->n_zp2 + 7) / 8, 8), 256, 0, c->stream>>>(
-              c->d_zp2.p, c->n_zp2, c->d_z16.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p,
-              c->d_arena.p, c->d_xi16.p, c->d_zpart16.p);
-        if (c->n_zp4 > 0)
-          hmv16_z_kernel<4><<<grid_for(c, (c->n_zp4 + 7) / 8, 8), 256, 0, c->stream>>>(
-              c->d_zp4.p, c->n_zp4, c->d_z16.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p,
-              c->d_arena.p, c->d_xi16.p, c->d_zpart16.p);
-      });
-    if (c->n_zs16 > 0)
-      c->timed("hmv16_zsum", [&] {
-        hmv16_zsum_kernel<<<grid_for(c, c->n_zs16, 8), 256, 0, c->stream>>>(
-            c->d_zs16.p, c->n_zs16, c->d_zpart16.p);
+        P.desc = c->d_zch16.p;
+        P.coff = c->d_zcoff16.p;
+        switch (c->p16_ns) {
+          case 4: launch_m16<4>(c, P, true); break;
+          case 6: launch_m16<6>(c, P, true); break;
+          case 9: launch_m16<9>(c, P, true); break;
+          default: launch_m16<3>(c, P, true);
+        }
       });
     c->timed("hmv16_leaf", [&] {
-      hmv16_leaf_kernel<<<grid_for(c, (c->n_tiles16 + 7) / 8, 8), 256, 0, c->stream>>>(
-          c->d_tiles16.p, c->n_tiles16, c->d_leaf_begin.p, c->d_leaf_end.p, c->d_leaf_ptr.p,
-          c->d_leaf_blk.p, c->d_mvb.p, c->d_items.p, c->d_rk16.p, c->d_zb16.p,
-          c->d_arena.p, c->d_dense.p, c->d_xi16.p, c->d_zpart16.p, c->yperm(),
-          c->ynrows(), dy, s0, nr);
+      P.desc = c->d_yst16.p;
+      P.copies = c->d_ycopy16.p;
+      P.coff = c->d_ycoff16.p;
+      switch (c->p16_ns) {
+        case 4: launch_m16<4>(c, P, false); break;
+        case 6: launch_m16<6>(c, P, false); break;
+        case 9: launch_m16<9>(c, P, false); break;
+        default: launch_m16<3>(c, P, false);
+      }
     });
+  }
+  if (dbg == 3) {
+    unsigned long long h[8];
+    CK(cudaMemcpyAsync(h, prof.p, 64, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    std::fprintf(stderr, "[hmgpu] m16 cycles (sum over warps): z consumer wait %.3g work %.3g, "
+                 "producer wait %.3g issue %.3g; y consumer wait %.3g work %.3g, producer "
+                 "wait %.3g issue %.3g\n", (double)h[0], (double)h[1], (double)h[2], (double)h[3],
+                 (double)h[4], (double)h[5], (double)h[6], (double)h[7]);
   }
 }
 

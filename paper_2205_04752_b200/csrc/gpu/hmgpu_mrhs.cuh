@@ -1,23 +1,40 @@
 // Multi-right-hand-side H-matvec Y += A X for the 3x3 Kelvin grid, 16
 // right-hand sides per pass, on the fp64 tensor cores (DMMA,
-// mma.sync.m8n8k4.f64).  At 16 RHS every stored factor value feeds 32 (16
-// for the diagonal components) multiply-adds, so the sweep is no longer
-// HBM-bound: these are the "batched fp64 factor products" of the north star.
+// mma.sync.m8n8k4.f64).  At 16 RHS every stored factor value feeds 16
+// (diagonal components) or 32 (off-diagonal: applied to x_C and x_R)
+// multiply-adds, so the sweep needs the fp64 tensor pipe as much as HBM:
+// these are the "batched fp64 factor products" of the north star.
 //
-//   phase 1 (hmv16_z_kernel)  per admissible block and 128-column chunk:
-//            Z_c = V_c^T X_C and W_c = V_c^T X_R for the six components
-//            (one warp each)
-//   phase 1b (hmv16_zsum_kernel) chunks of wide blocks summed in order
-//   phase 2 (hmv16_leaf_kernel) per leaf of the row tree, over the blocks
-//            covering it in a fixed order: Y_R += U_c Z_c, Y_C += U_c W_c
-//            and, for near-field blocks,
-//            Y_R += D_c X_C, Y_C += D_c X_R; y written once per row
-//            (deterministic, no atomics, no partial rows).
+// Two persistent, TMA-fed passes; a CTA of 4 warps runs a ring of NS stages
+// in shared memory, every stage brought in by cp.async.bulk (one mbarrier
+// transaction per stage: descriptor + data), the warps compute DMMA from the
+// stage while the next one is in flight:
 //
-// Layouts: x gathered to xi16[(col * 3 + comp) * 16 + s] (internal column
-// order, zero-padded past nrhs).
-// Factors are read in place from the ACA arena (U: m x cap and V: n x cap,
-// column-major), near-field blocks from the dense arena ([j][c][i]).
+//   phase 1 (hmv16_z_kernel)  one task per (admissible block, group of
+//            component l-ranges, <= 64 l in all): Z_c = V_c^T X_C and
+//            W_c = V_c^T X_R accumulated in registers over the block's
+//            column chunks (all the group's components share the staged X
+//            rows: x is read once per block and chunk, not once per
+//            component), written once ([l][ZP] rows, no partial sums)
+//   phase 2 (hmv16_y_kernel)  one task per leaf of the row tree: for the
+//            blocks covering the leaf in a fixed order, Y_R += U_c Z_c,
+//            Y_C += U_c W_c (the block's Z staged once per leaf and shared
+//            by the 4 warps) and, for near-field blocks, Y_R += D_c X_C,
+//            Y_C += D_c X_R; y written once per row (deterministic, no
+//            atomics, no partial rows).
+//
+// Data (all chosen so that the DMMA fragment loads from shared memory are
+// free of bank conflicts: a half-warp (g, t) in [0,4)^2 reads element
+// t * pitch + g with pitch = 4 or 12 mod 16 doubles):
+//   gathered x   xp[col][XP]: (component r, RHS s) at r * 16 + s, 4 pad
+//   p16 arena    the current-rank factors re-packed at plan time:
+//                phase 1 V^T pieces [l][P] per (task, chunk), P = pitch of
+//                the chunk's columns (zero padded); phase 2 U pieces [l][PR]
+//                per (leaf, block, stage), PR = pitch of the leaf's rows
+//   Z            per block, per component c, ceil4(k_c) rows of ZP doubles:
+//                Z_c (16) | W_c (16) | pad
+//   near field   read in place (dense arena [j][c][i]), one bulk copy per
+//                column into a conflict-free pitch
 //
 // Reference: HMatrix::matvec with a multi-column Vec (proj/src/hmatrix.cpp:
 // 22-45) over the BlockGrid (proj/src/expr.cpp:197-215).
@@ -27,20 +44,94 @@
 
 namespace hmgpu {
 
-constexpr int MR = 16;   // right-hand sides per pass
-constexpr int JC = 128;  // columns per phase-1 task
-#ifndef HMV16_ZK
-#define HMV16_ZK 4
-#endif
-constexpr int ZK = HMV16_ZK;  // phase-1 k-steps of fragments in flight
+constexpr int MR = 16;          // right-hand sides per pass
+constexpr int XP = 52;          // doubles per gathered column
+constexpr int ZP = 36;          // doubles per Z row
+constexpr int M16_NW = 8;       // consumer warps per CTA
+constexpr int M16_NT = 32 * (M16_NW + 1);  // + one producer warp
+constexpr int M16_HDR = 16;     // doubles of stage header (descriptors)
+constexpr int M16_XPAD = 256;   // zero columns after the last gathered column
 
-struct Z16Task {
-  int blk, j0, jlen, zi;
-  long long zbase;  // doubles: the block's Z region [nz][K][32]
+// smallest pitch >= n, multiple of 4, = 4 or 12 mod 16 (conflict-free DMMA
+// fragment loads, 16-byte aligned rows)
+__host__ __device__ constexpr int cf_pitch(int n) {
+  return ((n + 3) & ~3) + ((((n + 3) & ~3) & 7) == 0 ? 4 : 0);
+}
+
+struct __align__(16) ZChunk16 {  // phase-1 stage (32 B)
+  long long vsrc;  // doubles into the p16 arena
+  int vlen;        // doubles of V^T (sum len * P)
+  int xcol;        // first gathered column of the chunk
+  int P;           // pitch = staged X rows
+  int task;
+  int flags;       // 1 first chunk of the task, 2 last
+  int pad;
 };
-struct Z16Sum {
-  long long zbase;
-  int len, nz;  // len = K * 32
+static_assert(sizeof(ZChunk16) == 32, "ZChunk16 layout");
+
+struct __align__(16) ZTask16 {  // phase-1 task (80 B)
+  long long zdst;            // doubles: the block's Z region
+  int ntiles, pad0;          // 8-row m-tiles over the three operand groups
+  short zrow[6];             // Z row (of the block) of each segment's first l
+  unsigned char len[6];      // l count of the segment (<= 64)
+  unsigned char vrow[6];     // first row of the segment in the staged V^T
+  unsigned char gent[3][6];  // operand group r (x_r): entries (segment << 1) | part
+  unsigned char gn[3];       // entries of group r
+  unsigned char grows[3];    // rows of group r
+  unsigned char gtile[4];    // first m-tile of group r (gtile[3] = ntiles)
+  int pad1[3];
+};
+static_assert(sizeof(ZTask16) == 80, "ZTask16 layout");
+
+enum { Y16_ADM = 0, Y16_DENSE = 1 };
+
+// phase-2 item: one low-rank block piece (l ranges of its components) or
+// one near-field column group, for one leaf; a stage carries up to
+// Y16_MAXIT of them (consecutive in leaf order, possibly across leaves)
+struct __align__(16) YItem16 {  // 64 B
+  int kind, leaf, flags, R;  // flags: 1 first item of the leaf, 2 last
+  int PR;                    // ADM: U pitch; DENSE: column pitch in shared memory
+  int off1, off2;            // stage offsets (doubles): ADM U, Z; DENSE D, X
+  int jd;                    // DENSE: columns
+  int m, roff, pad0, pad1;   // DENSE: block rows (component stride), first row of the leaf
+  unsigned char lo[6], hi[6];  // ADM: l range of each component
+  int pad2;
+};
+static_assert(sizeof(YItem16) == 64, "YItem16 layout");
+constexpr int Y16_MAXIT = 14;
+constexpr int Y16_HDR = 8 * (1 + Y16_MAXIT);  // doubles: count record + items
+
+// a stage of phase 2: its bulk copies (global source, stage offset, bytes)
+struct __align__(16) M16Stage {
+  int cbeg, ncopies, bytes, nitems;
+};
+struct __align__(16) M16Copy {
+  unsigned long long src;
+  int dst, bytes;  // dst in doubles from the stage start
+};
+
+// host-side piece of the phase-2 plan (one block piece / column group)
+struct YStage16 {
+  long long src, src2;
+  int len, len2, kind, leaf, flags, R, PR, jd, spitch, m, roff;
+  unsigned char lo[6], hi[6];
+};
+
+struct M16Params {
+  const void* desc;          // ZChunk16[] (phase 1) or M16Stage[] (phase 2)
+  const M16Copy* copies;     // phase 2
+  const ZTask16* tasks;
+  const int* coff;           // stages of CTA b: [coff[b], coff[b + 1])
+  const double* arena;       // p16 arena
+  const double* dense;
+  const double* xp;
+  double* z;
+  const int* leaf_begin;
+  const int* rperm;
+  double* y;
+  int nrows, s0, nr, stage;  // stage: doubles per stage (header included)
+  int dbg;                   // A/B: 1 = stream only (no compute), 2 = compute only
+  unsigned long long* prof;  // A/B (dbg 3): cycle counters of the stage loop
 };
 
 // D = A B + D, A 8x4 (row), B 4x8 (col), fp64; lane (g = lane/4, t = lane%4)
@@ -51,273 +142,359 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// xi16[(p * 3 + r) * 16 + s] = x[(s0 + s) * ndof + r * ncols + cperm[p]]
-__global__ void gather16_kernel(const double* __restrict__ x, double* __restrict__ xi,
+// xp[p * XP + r * 16 + s] = x[(s0 + s) * ndof + r * ncols + cperm[p]] (0 past nr)
+__global__ void gather16_kernel(const double* __restrict__ x, double* __restrict__ xp,
                                 const int* __restrict__ cperm, int ncols, int s0, int nr) {
   const long long ndof = 3LL * ncols;
-  const long long total = ndof * MR;
+  const long long total = (long long)ncols * 48;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int s = (int)(t & (MR - 1));
     const long long pr = t >> 4;
     const int r = (int)(pr % 3);
     const long long p = pr / 3;
-    xi[t] = s < nr ? x[(long long)(s0 + s) * ndof + r * (long long)ncols + cperm[p]] : 0.0;
+    xp[p * XP + r * 16 + s] =
+        s < nr ? x[(long long)(s0 + s) * ndof + r * (long long)ncols + cperm[p]] : 0.0;
   }
 }
 
-// Rank table of the plan: rk[8 * bi + c] = rank of component c of matvec
-// block bi in the plan's mode, rk[8 * bi + 6] = their sum.
+// ---------------------------------------------------------------------------
+// stage ring shared by both passes: warp 0 issues, all warps consume
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
-// phase 1: one warp per (task, component) pair; no shared memory, no block
-// barriers.  NMT = 8-row m-tiles of V^T held in registers: the pairs with
-// rank <= 16 (almost all) run the NMT = 2 instance, which needs half the
-// registers and so keeps twice as many warps (loads) in flight.  Pairs are
-// ordered by task, so neighbouring warps share the chunk's x rows in L1.
-template <int NMT>
-__global__ void __launch_bounds__(256)
-hmv16_z_kernel(const int2* __restrict__ pairs, int npairs, const Z16Task* __restrict__ tasks,
-               const MvBlock* __restrict__ blocks, const Item* __restrict__ items,
-               const int* __restrict__ rk, const double* __restrict__ arena,
-               const double* __restrict__ xi, double* __restrict__ zpart) {
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  constexpr int Rs[6] = {0, 0, 0, 1, 1, 2}, Cs[6] = {0, 1, 2, 1, 2, 2};
-  for (int w = gw; w < npairs; w += nw) {
-    const int2 pc = pairs[w];
-    const Z16Task tk = tasks[pc.x];
-    const int c = pc.y;
-    const int* r8 = rk + 8 * tk.blk;
-    const int k = r8[c];
-    int kpre = 0;
-    for (int q = 0; q < c; ++q) kpre += r8[q];
-    const int K = r8[6];
-    const MvBlock b = blocks[tk.blk];
-    const int R = Rs[c], C = Cs[c];
-    const bool two = R != C;
-    const double* V = arena + items[b.item0 + c].v_off + tk.j0;
-    const double* xb = xi + (long long)(b.col0 + tk.j0) * 48 + g;
-    double* zp = zpart + tk.zbase + (long long)tk.zi * K * 32;
-    for (int lg = 0; lg < k; lg += 8 * NMT) {
-      double acc[NMT][2][2][2];
-#pragma unroll
-      for (int a = 0; a < NMT; ++a)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int xr = 0; xr < 2; ++xr) acc[a][nt][xr][0] = acc[a][nt][xr][1] = 0.0;
-      const int nmt = min(NMT, (k - lg + 7) >> 3);  // warp-uniform
-      // ZK k-steps (4 ZK columns) of A and B fragments issued before the MMAs
-      for (int j16 = 0; j16 < tk.jlen; j16 += 4 * ZK) {
-        double a[ZK][NMT], bc[ZK][2], br[ZK][2];
-#pragma unroll
-        for (int st = 0; st < ZK; ++st) {
-          const int j = j16 + 4 * st + t;
-          const bool jok = j < tk.jlen;
-#pragma unroll
-          for (int mt = 0; mt < NMT; ++mt) {
-            const int l = lg + mt * 8 + g;
-            a[st][mt] = (mt < nmt && l < k && jok) ? V[(long long)l * b.n + j] : 0.0;
-          }
-          const double* xr = xb + (long long)j * 48;
-          bc[st][0] = jok ? xr[C * 16] : 0.0;
-          bc[st][1] = jok ? xr[C * 16 + 8] : 0.0;
-          br[st][0] = (jok && two) ? xr[R * 16] : 0.0;
-          br[st][1] = (jok && two) ? xr[R * 16 + 8] : 0.0;
-        }
-#pragma unroll
-        for (int st = 0; st < ZK; ++st) {
-          if (j16 + 4 * st >= tk.jlen) break;  // warp-uniform
-#pragma unroll
-          for (int mt = 0; mt < NMT; ++mt) {
-            if (mt < nmt) {
-              dmma(acc[mt][0][0][0], acc[mt][0][0][1], a[st][mt], bc[st][0]);
-              dmma(acc[mt][1][0][0], acc[mt][1][0][1], a[st][mt], bc[st][1]);
-              if (two) {
-                dmma(acc[mt][0][1][0], acc[mt][0][1][1], a[st][mt], br[st][0]);
-                dmma(acc[mt][1][1][0], acc[mt][1][1][1], a[st][mt], br[st][1]);
-              }
-            }
-          }
-        }
+// full[s]: the stage's bytes have landed (one arrival + tx bytes);
+// empty[s]: every consumer warp is done with the slot (M16_NW arrivals)
+template <int NS>
+__device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* empty,
+                                          int stage) {
+  // zero the ring once: every later read of a slot outside the current
+  // stage's data sees finite values (previous stages or zero), so fragment
+  // loads past a segment's end may run unpredicated when A is zero
+  for (int e = threadIdx.x; e < NS * stage; e += blockDim.x) sm[e] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], M16_NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+// Stage loop shared by both passes: a producer warp (the CTA's last) issues
+// stage j into slot j % NS as soon as every consumer warp released the
+// slot's previous stage, running up to NS stages ahead; the consumer warps
+// wait for each stage's bytes, compute, and release the slot.  issue(slot,
+// bar, j) loads the records of stage j + 1 after issuing stage j, so their
+// latency overlaps the wait for the next free slot.
+template <int NS, class ISSUE, class COMPUTE>
+__device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t* empty,
+                                           int stage, int n, ISSUE issue,
+                                           COMPUTE compute, int dbg = 0,
+                                           unsigned long long* prof = nullptr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tm = dbg == 3 && prof != nullptr;
+  long long t_wait = 0, t_work = 0;
+  if (warp == M16_NW) {
+    for (int j = 0; j < n; ++j) {
+      const int s = j % NS;
+      const long long t0 = tm ? clock64() : 0;
+      if (j >= NS) mbar_wait(&empty[s], (uint32_t)(((j / NS) - 1) & 1));
+      const long long t1 = tm ? clock64() : 0;
+      issue(sm + (long long)s * stage, &full[s], j);  // prefetches stage j + 1's records
+      if (tm) {
+        t_wait += t1 - t0;
+        t_work += clock64() - t1;
       }
+    }
+    if (tm && lane == 0) {
+      atomicAdd(prof + 2, (unsigned long long)t_wait);
+      atomicAdd(prof + 3, (unsigned long long)t_work);
+    }
+    return;
+  }
+  for (int i = 0; i < n; ++i) {
+    const int s = i % NS;
+    const long long t0 = tm ? clock64() : 0;
+    mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+    const long long t1 = tm ? clock64() : 0;
+    if (dbg != 1) compute(sm + (long long)s * stage);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tm) {
+      t_wait += t1 - t0;
+      t_work += clock64() - t1;
+    }
+  }
+  if (tm && lane == 0) {
+    atomicAdd(prof + 0, (unsigned long long)t_wait);
+    atomicAdd(prof + 1, (unsigned long long)t_work);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 1
+__device__ __forceinline__ void z16_issue(const M16Params& P, double* st, uint64_t* bar,
+                                          const ZChunk16& ch, const ZChunk16* gch, int lane) {
+  if (lane != 0) return;
+  const bool hdr = P.dbg == 2;  // A/B: descriptors only (compute on stale data)
+  const uint32_t vb = hdr ? 0u : (uint32_t)ch.vlen * 8u, xb = hdr ? 0u : (uint32_t)ch.P * XP * 8u;
+  fence_proxy_async();
+  mbar_expect_tx(bar, 32u + 80u + vb + xb);
+  bulk_g2s(st, gch, 32u, bar);
+  bulk_g2s(st + 4, P.tasks + ch.task, 80u, bar);
+  if (vb) bulk_g2s(st + M16_HDR, P.arena + ch.vsrc, vb, bar);
+  if (xb) bulk_g2s(st + M16_HDR + ch.vlen, P.xp + (long long)ch.xcol * XP, xb, bar);
+}
+
+template <int NS>
+__global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  ring_init<NS>(sm, full, empty, P.stage);
+  const ZChunk16* chunks = static_cast<const ZChunk16*>(P.desc);
+  const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
+  // m-tiles warp, warp + 8, warp + 16 of the task
+  double acc[3][2][2];
+  ZChunk16 nxt{};
+  if (warp == M16_NW && n > 0) nxt = chunks[c0];
+  auto issue = [&](double* st, uint64_t* bar, int j) {
+    const ZChunk16 cur = nxt;
+    if (j + 1 < n) nxt = chunks[c0 + j + 1];
+    z16_issue(P, st, bar, cur, chunks + c0 + j, lane);
+  };
+  auto compute = [&](double* st) {
+    const ZChunk16& ch = *reinterpret_cast<const ZChunk16*>(st);
+    const ZTask16& tk = *reinterpret_cast<const ZTask16*>(st + 4);
+    const double* sV = st + M16_HDR;
+    const double* sX = sV + ch.vlen;
+    const int Pp = ch.P;
+    if (ch.flags & 1) {
 #pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) {
-        const int l = lg + mt * 8 + g;
-        if (mt < nmt && l < k) {
-          double* row = zp + (long long)(kpre + l) * 32 + 2 * t;
+      for (int q = 0; q < 3; ++q)
 #pragma unroll
-          for (int xr = 0; xr < 2; ++xr)
+        for (int nt = 0; nt < 2; ++nt) acc[q][nt][0] = acc[q][nt][1] = 0.0;
+    }
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-              *reinterpret_cast<double2*>(row + xr * 16 + nt * 8) =
-                  make_double2(acc[mt][nt][xr][0], acc[mt][nt][xr][1]);
-        }
+    for (int q = 0; q < 3; ++q) {
+      const int p = warp + M16_NW * q;
+      if (p >= tk.ntiles) break;  // warp-uniform
+      // operand group r (rows multiply x_r), this lane's row rho of it ->
+      // (segment, part, l): Z_c (part 0) if C_c = r, W_c (part 1) if R_c = r
+      const int r = p >= tk.gtile[2] ? 2 : (p >= tk.gtile[1] ? 1 : 0);
+      const int rho = (p - tk.gtile[r]) * 8 + g;
+      const bool valid = rho < tk.grows[r];
+      int cum = 0, e = 0, seg = 0;
+      for (; e < tk.gn[r]; ++e) {
+        seg = tk.gent[r][e] >> 1;
+        if (rho < cum + tk.len[seg]) break;
+        cum += tk.len[seg];
+      }
+      if (!valid) seg = tk.gent[r][0] >> 1;
+      const int l = valid ? rho - cum : 0;
+      const double* A0 = sV + (tk.vrow[seg] + l) * Pp + t;
+      const double* X0 = sX + t * XP + r * 16 + g;
+#pragma unroll 4
+      for (int kk = 0; kk < Pp; kk += 4) {
+        const double u = A0[kk];
+        const double a = valid ? u : 0.0;
+        const double* x0 = X0 + kk * XP;
+        dmma(acc[q][0][0], acc[q][0][1], a, x0[0]);
+        dmma(acc[q][1][0], acc[q][1][1], a, x0[8]);
+      }
+      if ((ch.flags & 2) && valid) {  // last chunk: this lane's Z row
+        const int part = tk.gent[r][e] & 1;
+        double* zr = P.z + tk.zdst + (long long)(tk.zrow[seg] + l) * ZP + part * 16 + 2 * t;
+        *reinterpret_cast<double2*>(zr) = make_double2(acc[q][0][0], acc[q][0][1]);
+        *reinterpret_cast<double2*>(zr + 8) = make_double2(acc[q][1][0], acc[q][1][1]);
+      }
+    }
+  };
+  stage_loop<NS>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof);
+}
+
+// ---------------------------------------------------------------------------
+// phase 2
+// issue one phase-2 stage whose records the producer warp holds: the stage
+// (every lane) and its first 32 copies (lane q: copy q)
+__device__ __forceinline__ void y16_issue(const M16Params& P, double* st, uint64_t* bar,
+                                          const M16Stage& d, const M16Copy& mine, int lane) {
+  const bool hdr = P.dbg == 2;  // A/B: the item records only (compute on stale data)
+  if (lane == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, hdr ? (uint32_t)(64 * (1 + d.nitems)) : (uint32_t)d.bytes);
+  }
+  __syncwarp();
+  const int nc = hdr ? 1 : d.ncopies;  // copy 0 is the item records
+  if (lane < nc) {
+    fence_proxy_async();
+    bulk_g2s(st + mine.dst, reinterpret_cast<const void*>(mine.src), (uint32_t)mine.bytes, bar);
+  }
+  for (int q = lane + 32; q < nc; q += 32) {
+    const M16Copy cp = P.copies[d.cbeg + q];
+    fence_proxy_async();
+    bulk_g2s(st + cp.dst, reinterpret_cast<const void*>(cp.src), (uint32_t)cp.bytes, bar);
+  }
+}
+
+// Y rows of the warp's row tile += U_c [Z_c | W_c] over the item's l range
+// of component c = (RR, CC), for NH RHS halves (NH = 1: the half at the
+// caller's offset into Z, accumulated in acc[..][0])
+template <int RR, int CC, int NH>
+__device__ __forceinline__ void y16_adm(const double* sU, int PR, const double* sZ, int lo,
+                                        int hi, int rt, int g, int t,
+                                        double (&acc)[3][2][2]) {
+  const double* ur = sU + t * PR + rt * 8 + g;
+  const double* zr = sZ + t * ZP + g;
+#pragma unroll 2
+  for (int l0 = lo; l0 < hi; l0 += 4) {
+    const double u = ur[0];
+    const double a = l0 + t < hi ? u : 0.0;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
+      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
+    }
+    ur += 4 * PR;
+    zr += 4 * ZP;
+  }
+}
+
+// one phase-2 item for the warp's row tile rt; hoff = first RHS of the half
+// (NH = 1) or 0 (NH = 2)
+template <int NH>
+__device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int rt, int hoff,
+                                         int g, int t, double (&acc)[3][2][2]) {
+  if (d.kind == Y16_ADM) {
+    const double* sU = st + d.off1;
+    const double* sZ = st + d.off2 + hoff;
+    int uo = 0, zo = 0;
+#define Y16_COMP(CI, RR, CC)                                                              \
+  {                                                                                       \
+    const int lo = d.lo[CI], hi = d.hi[CI];                                               \
+    if (lo < hi) {                                                                        \
+      y16_adm<RR, CC, NH>(sU + uo, d.PR, sZ + zo, lo, hi, rt, g, t, acc);                \
+      uo += (hi - lo) * d.PR;                                                             \
+      zo += (((hi + 3) & ~3) - lo) * ZP;                                                  \
+    }                                                                                     \
+  }
+    Y16_COMP(0, 0, 0)
+    Y16_COMP(1, 0, 1)
+    Y16_COMP(2, 0, 2)
+    Y16_COMP(3, 1, 1)
+    Y16_COMP(4, 1, 2)
+    Y16_COMP(5, 2, 2)
+#undef Y16_COMP
+    return;
+  }
+  // near field: D [j][c][i] (column pitch PR, component stride m, the leaf's
+  // rows from roff), x rows after the columns
+  const double* sD = st + d.off1 + d.roff + rt * 8 + g;
+  const double* sX = st + d.off2 + hoff + g;
+  const int m = d.m, PD = d.PR;
+  constexpr int Rs[6] = {0, 0, 0, 1, 1, 2}, Cs[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll 1
+  for (int j0 = 0; j0 < d.jd; j0 += 4) {
+    const int j = j0 + t;
+    const bool ok = j < d.jd;
+    const double* xr = sX + j * XP;
+    const double* dr = sD + j * PD;
+    double a[6];
+#pragma unroll
+    for (int cc = 0; cc < 6; ++cc) {
+      const double v = dr[cc * m];
+      a[cc] = ok ? v : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      const double bx[3] = {xr[8 * h], xr[16 + 8 * h], xr[32 + 8 * h]};
+#pragma unroll
+      for (int cc = 0; cc < 6; ++cc) {
+        dmma(acc[Rs[cc]][h][0], acc[Rs[cc]][h][1], a[cc], bx[Cs[cc]]);
+        if (Rs[cc] != Cs[cc]) dmma(acc[Cs[cc]][h][0], acc[Cs[cc]][h][1], a[cc], bx[Rs[cc]]);
       }
     }
   }
 }
 
-// phase 1b: Z of blocks wider than one chunk = sum of its chunks, in order
-__global__ void hmv16_zsum_kernel(const Z16Sum* __restrict__ sums, int nsums,
-                                  double* __restrict__ zpart) {
-  for (int si = blockIdx.x; si < nsums; si += gridDim.x) {
-    const Z16Sum s = sums[si];
-    double* z = zpart + s.zbase;
-    for (int e = threadIdx.x; e < s.len; e += blockDim.x) {
-      double v = z[e];
-      for (int q = 1; q < s.nz; ++q) v += z[(long long)q * s.len + e];
-      z[e] = v;
-    }
-  }
-}
-
-// phase 2, per group of TR 8-row tiles of a leaf of the row tree
-// (tiles[w] = (leaf, group)): one warp visits the blocks covering the leaf in
-// a fixed order (leaf_blk) and accumulates in registers, so y is written once
-// per row: no partial rows, no reduction pass, no atomics, no block barriers.
-// Each Z / x fragment loaded feeds TR row tiles.
-#ifndef HMV16_TR
-#define HMV16_TR 2
-#endif
-#ifndef HMV16_KS
-#define HMV16_KS 4
-#endif
-constexpr int TR = HMV16_TR;  // row tiles per warp
-constexpr int KS = HMV16_KS;  // k-steps of fragments in flight
-
-__global__ void __launch_bounds__(256)
-hmv16_leaf_kernel(const int2* __restrict__ tiles, int ntiles,
-                  const int* __restrict__ leaf_begin, const int* __restrict__ leaf_end,
-                  const int* __restrict__ leaf_ptr, const int2* __restrict__ leaf_blk,
-                  const MvBlock* __restrict__ blocks, const Item* __restrict__ items,
-                  const int* __restrict__ rk, const long long* __restrict__ zbase,
-                  const double* __restrict__ arena, const double* __restrict__ dense,
-                  const double* __restrict__ xi, const double* __restrict__ zpart,
-                  const int* __restrict__ rperm, int nrows, double* __restrict__ y, int s0,
-                  int nr) {
-  const int lane = threadIdx.x & 31;
+// Leaves of at most 64 rows (8 row tiles): warp w takes row tile w with both
+// RHS halves, or, for leaves of at most 32 rows, row tile w % 4 with RHS
+// half w / 4.
+template <int NS>
+__global__ void __launch_bounds__(M16_NT, 3) hmv16_y_kernel(M16Params P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  constexpr int Rs[6] = {0, 0, 0, 1, 1, 2}, Cs[6] = {0, 1, 2, 1, 2, 2};
-  for (int w = gw; w < ntiles; w += nw) {
-    const int2 lt = tiles[w];
-    const int b0 = leaf_begin[lt.x];
-    const int rows = leaf_end[lt.x] - b0;
-    const int r0 = lt.y * 8 * TR;  // first row of the group within the leaf
-    const int ntr = min(TR, (rows - r0 + 7) >> 3);  // warp-uniform
-    bool iok[TR];
-#pragma unroll
-    for (int q = 0; q < TR; ++q) iok[q] = q < ntr && r0 + 8 * q + g < rows;
-    double acc[TR][3][2][2];
-#pragma unroll
-    for (int q = 0; q < TR; ++q)
+  ring_init<NS>(sm, full, empty, P.stage);
+  const M16Stage* stages = static_cast<const M16Stage*>(P.desc);
+  const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
+  double acc[3][2][2];  // [output component][RHS half][pair]
+  const long long ndof = 3LL * P.nrows;
+  // producer state: the records of stage j (rec0, its copies cp0) and j + 1
+  // (rec1); issuing stage j loads stage j + 1's copies and stage j + 2's
+  // record, so no load sits on the issue path
+  M16Stage rec0{}, rec1{};
+  M16Copy cp0{};
+  if (warp == M16_NW) {
+    if (n > 0) rec0 = stages[c0];
+    if (n > 1) rec1 = stages[c0 + 1];
+    if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
+  }
+  auto issue = [&](double* st, uint64_t* bar, int j) {
+    const M16Stage cur = rec0;
+    const M16Copy mine = cp0;
+    rec0 = rec1;
+    if (j + 1 < n && lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
+    if (j + 2 < n) rec1 = stages[c0 + j + 2];
+    y16_issue(P, st, bar, cur, mine, lane);
+  };
+  auto compute = [&](double* st) {
+    const int nit = *reinterpret_cast<const int*>(st);
+    const YItem16* items = reinterpret_cast<const YItem16*>(st) + 1;
+    for (int it = 0; it < nit; ++it) {
+    const YItem16& d = items[it];
+    const int RT = (d.R + 7) >> 3;
+    const bool split = RT <= 4;
+    const int rt = split ? (warp & 3) : warp;
+    const int h0 = split ? (warp >> 2) : 0;
+    if (d.flags & 1) {
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[q][r][nt][0] = acc[q][r][nt][1] = 0.0;
-    const int e1 = leaf_ptr[lt.x + 1];
-    for (int e = leaf_ptr[lt.x]; e < e1; ++e) {
-      const int2 be = leaf_blk[e];
-      const MvBlock b = blocks[be.x];
-      const int i = be.y + r0 + g;  // row of tile 0 within the block
-      if (!b.dense) {
-        const int* r8 = rk + 8 * be.x;
-        const double* z = zpart + zbase[be.x] + g;
-        int kp = 0;
+        for (int h = 0; h < 2; ++h) acc[r][h][0] = acc[r][h][1] = 0.0;
+    }
+    if (rt < RT) {  // warp-uniform
+      if (split) y16_item<1>(d, st, rt, 8 * h0, g, t, acc);
+      else y16_item<2>(d, st, rt, 0, g, t, acc);
+      if (d.flags & 2) {  // the leaf is complete: y rows, external order
+        const int b0 = P.leaf_begin[d.leaf];
+        const int i = rt * 8 + g;
+        if (i < d.R) {
+          const long long row = P.rperm[b0 + i];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const int k = r8[c];
-          const int R = Rs[c], C = Cs[c];
-          const double* U = arena + items[b.item0 + c].u_off + i;
-          const double* zc = z + (long long)kp * 32;
-          kp += k;
-          for (int l0 = 0; l0 < k; l0 += 4 * KS) {  // KS k-steps in flight
-            double a[KS][TR], zz[KS][4];
+          for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int st = 0; st < KS; ++st) {
-              const int l = l0 + 4 * st + t;
-              const bool lok = l < k;
+            for (int h = 0; h < 2; ++h) {
+              if (split && h > 0) continue;
 #pragma unroll
-              for (int q = 0; q < TR; ++q)
-                a[st][q] = (lok && iok[q]) ? U[(long long)l * b.m + 8 * q] : 0.0;
-              const double* zr = zc + (long long)l * 32;
-              zz[st][0] = lok ? zr[0] : 0.0;
-              zz[st][1] = lok ? zr[8] : 0.0;
-              zz[st][2] = (lok && R != C) ? zr[16] : 0.0;
-              zz[st][3] = (lok && R != C) ? zr[24] : 0.0;
-            }
-#pragma unroll
-            for (int st = 0; st < KS; ++st) {
-              if (l0 + 4 * st >= k) break;  // warp-uniform
-#pragma unroll
-              for (int q = 0; q < TR; ++q) {
-                if (q >= ntr) break;
-                dmma(acc[q][R][0][0], acc[q][R][0][1], a[st][q], zz[st][0]);
-                dmma(acc[q][R][1][0], acc[q][R][1][1], a[st][q], zz[st][1]);
-                if (R != C) {
-                  dmma(acc[q][C][0][0], acc[q][C][0][1], a[st][q], zz[st][2]);
-                  dmma(acc[q][C][1][0], acc[q][C][1][1], a[st][q], zz[st][3]);
-                }
+              for (int e = 0; e < 2; ++e) {
+                const int sx = (split ? 8 * h0 : 8 * h) + 2 * t + e;
+                if (sx < P.nr)
+                  P.y[(long long)(P.s0 + sx) * ndof + r * (long long)P.nrows + row] =
+                      acc[r][h][e];
               }
             }
-          }
-        }
-      } else {
-        const long long cp = (6LL * b.m + 1) & ~1LL;
-        const double* D = dense + b.dense_off + i;
-        const double* xb = xi + (long long)b.col0 * 48 + g;
-        for (int j0 = 0; j0 < b.n; j0 += 4) {
-          const int j = j0 + t;
-          const bool jok = j < b.n;
-          double bx[3][2];
-          const double* xr = xb + (long long)j * 48;
-#pragma unroll
-          for (int xc = 0; xc < 3; ++xc) {
-            bx[xc][0] = jok ? xr[xc * 16] : 0.0;
-            bx[xc][1] = jok ? xr[xc * 16 + 8] : 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < TR; ++q) {
-            if (q >= ntr) break;
-            double a[6];
-#pragma unroll
-            for (int c = 0; c < 6; ++c)
-              a[c] = (jok && iok[q]) ? D[(long long)j * cp + (long long)c * b.m + 8 * q] : 0.0;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-              const int R = Rs[c], C = Cs[c];
-              dmma(acc[q][R][0][0], acc[q][R][0][1], a[c], bx[C][0]);
-              dmma(acc[q][R][1][0], acc[q][R][1][1], a[c], bx[C][1]);
-              if (R != C) {
-                dmma(acc[q][C][0][0], acc[q][C][0][1], a[c], bx[R][0]);
-                dmma(acc[q][C][1][0], acc[q][C][1][1], a[c], bx[R][1]);
-              }
-            }
-          }
         }
       }
     }
-    const long long ndof = 3LL * nrows;
-#pragma unroll
-    for (int q = 0; q < TR; ++q) {
-      if (!iok[q]) continue;
-      const long long row = rperm[b0 + r0 + 8 * q + g];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int s = nt * 8 + 2 * t + hh;
-            if (s < nr)
-              y[(long long)(s0 + s) * ndof + r * (long long)nrows + row] = acc[q][r][nt][hh];
-          }
     }
-  }
+  };
+  stage_loop<NS>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof ? P.prof + 4 : nullptr);
 }
 
 // fp64 tensor-core peak probe: eight independent DMMA chains per warp

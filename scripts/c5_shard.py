@@ -23,7 +23,7 @@ for it in range(3):
     t = time.perf_counter()
     Y = h.matvec(X)
     print("matvec", nrhs, "rhs", round((time.perf_counter() - t) * 1e3, 1), "ms", flush=True)
-for k in ("gather", "hmv16_z", "hmv16_zsum", "hmv16_leaf"):
+for k in ("gather", "hmv16_z", "hmv16_leaf", "pack16"):
     ms, n = h.kernel_times(k, reset=True)
     print(f"  {k:12s} {ms / max(n, 1):.3f} ms/launch")
 x = np.ascontiguousarray(X[:, 0])

@@ -15,7 +15,7 @@ X = np.asfortranarray(hm.random_vector(h.cols * nrhs, 2, "normal").reshape(nrhs,
 h.set_profiling(True)
 for it in range(3):
     Y = h.matvec(X)
-names = ["gather", "hmv16_z", "hmv16_zsum", "hmv16_leaf"]
+names = ["gather", "hmv16_z", "hmv16_leaf", "pack16"]
 for k in names:
     ms, n = h.kernel_times(k, reset=True)
     print(f"{k:12s} {ms / max(n, 1) * 1:.3f} ms/launch  ({n} launches)")
