@@ -18,7 +18,9 @@
  *   hmb_matvec          matvec(BlockGrid, x, Mode)  (expr.cpp:197-215)
  *   hmb_promote/extend  HMatrix::promote / extend_lookahead
  *   hmb_gamma/hmb_mark  gamma_contributions / mark_blocks (amvm.hpp:36-48)
- *   hmb_amvm            amvm_multiply               (amvm.hpp:67-71)
+ *   hmb_amvm            amvm_multiply               (amvm.hpp:67-71); on a block-row
+ *                       shard with a communicator: the sharded loop
+ *   hmb_mark_sharded    mark_blocks across block-row shards (amvm.cpp:131-184)
  *
  * Status convention: 0 = ok, otherwise an hmbem error class
  * (1 Error, 2 MeshError, 3 ConfigError, 4 DimensionError, 5 DeviceError);
@@ -160,6 +162,22 @@ int hmb_gamma_terms(const hmb_op* op, int* comp, int* block, int* nnz, double* n
 int hmb_gamma_term_data(const hmb_op* op, int t, long long* idx, double* val);
 int hmb_mark(const hmb_op* op, double theta, int c_sp, long long m_rows,
              long long n_cols, int* marked, int* n_marked, double* gamma_pk);
+/* mark_blocks (amvm.cpp:131-184) over block-row shards: every rank passes its
+ * own terms (CSR: term t's rows idx[term_ptr[t] .. term_ptr[t+1]), values
+ * val), the WHOLE difference vector and the flags of its rows; the ranks
+ * exchange their marking events through `allgather` (recv[r * bytes ...] =
+ * send of rank r; returns 0 on success) and each gets its marked terms
+ * (indices into its own list), the count over all ranks and gamma(P_k) --
+ * the unsharded walk's result, bit for bit.  A sharded hmb_amvm runs this
+ * between its ranks (the library's communicator). */
+typedef int (*hmb_allgather_fn)(void* user, const void* send, void* recv,
+                                long long bytes_per_rank);
+int hmb_mark_sharded(int n_terms, const long long* term_ptr, const long long* idx,
+                     const double* val, const double* difference,
+                     const unsigned char* own_rows, long long m_rows, long long n_cols,
+                     double theta, int c_sp, int nranks, int rank,
+                     hmb_allgather_fn allgather, void* user, int* marked, int* n_marked,
+                     int* n_marked_total, double* gamma_pk);
 /* iterations as rows of 8 doubles [k, gamma, gamma_pk, marked,
  * cumulative_pivots, storage_mb, e_hat, ms]; iters8 holds max_iterations+1 rows */
 int hmb_amvm(hmb_op* op, const double* x, double theta, double eps_amvm,

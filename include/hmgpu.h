@@ -251,7 +251,9 @@ int hmgpu_extend(hmgpu_ctx* ctx, int n, const int* comp_block, int steps);
    hmgpu_amvm_mark       theta-marking walk on the device; gamma(P_k), count
    hmgpu_amvm_refine     promote + extend_lookahead(steps) of the marked
                          (comp, block) pairs (optional host copy of the pairs)
-   Whole (unsharded) operators only. */
+   Whole (unsharded) operators only; a block-row shard with a communicator
+   runs the adaptive loop through the term-level API (hmb_amvm, operator.cpp
+   amvm_multiply_sharded). */
 int hmgpu_amvm_estimate(hmgpu_ctx* ctx, const double* x, double* gamma, double* difference);
 /* direct != 0: 1-RHS matvecs sweep the blocks in place instead of building the
    packed stream plan (for one matvec per rank change, as in the adaptive loop;
@@ -323,6 +325,11 @@ int hmgpu_comm_clear(hmgpu_ctx* ctx);
  * ranges of all ranks (row_begin[nranks], row_end[nranks], may be NULL) */
 int hmgpu_comm_info(hmgpu_ctx* ctx, int* nranks, int* rank, int* kind, int* row_begin,
                     int* row_end);
+/* all-gather of HOST buffers over the ctx's communicator (collective):
+ * recv[r * bytes_per_rank ...] = send of rank r (the sharded adaptive
+ * matvec exchanges its estimator and marking events with it) */
+int hmgpu_comm_allgather(hmgpu_ctx* ctx, const void* send, void* recv,
+                         long long bytes_per_rank);
 /* y = A x on all ranks (see above).  x is read on rank 0 only (other ranks
  * may pass NULL); y (dofs x nrhs, column-major, external order) is written
  * on every rank.  ptr_kind as hmgpu_matvec. */

@@ -10,7 +10,8 @@ from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflo
                   baca_solve, pcg_spd, estimator_vh, doerfler_mark, DofLayout, SaddleSystem,
                   SolveStats, bpcg_solve, SaddleEstimator, baca_solve_saddle,
                   MeshError, Mode, amvm_multiply, assemble, device_count, gamma_contributions,
-                  host_tree_and_partition, nccl_available, nccl_unique_id)
+                  host_tree_and_partition, nccl_available, nccl_unique_id,
+                  mark_blocks_sharded)
 
 __all__ = [
     "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
@@ -21,5 +22,5 @@ __all__ = [
     "SolveStats", "bpcg_solve", "SaddleEstimator", "baca_solve_saddle",
     "MeshError",
     "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",
-    "host_tree_and_partition", "nccl_available", "nccl_unique_id",
+    "host_tree_and_partition", "nccl_available", "nccl_unique_id", "mark_blocks_sharded",
 ]

@@ -115,6 +115,11 @@ BCAST_FN = C.CFUNCTYPE(C.c_int, P, P, C.c_longlong, C.c_int)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, P, P, P, C.c_longlong)
 
 
+_sig(host, "hmb_mark_sharded", I, I, P, P, P, P, P, LL, LL, D, I, I, I, ALLGATHER_FN, P, P,
+     IP, IP, DP)
+_sig(gpu, "hmgpu_comm_allgather", I, P, P, P, LL)
+
+
 class CommOps(C.Structure):
     _fields_ = [("broadcast", BCAST_FN), ("allgather", ALLGATHER_FN), ("user", P)]
 

@@ -646,6 +646,47 @@ class HMatrix:
         return ms.value, n.value
 
 
+def mark_blocks_sharded(terms, difference, own_rows, theta: float, c_sp: int, m_rows: int,
+                        n_cols: int, nranks: int, rank: int, allgather):
+    """mark_blocks (amvm.cpp:131-184) across block-row shards (hmb_mark_sharded).
+    terms: this rank's BlockTerms (rows of its shard); difference: the whole
+    difference vector; own_rows: bool flags of this rank's rows; allgather as
+    HMatrix.attach_comm's (np.uint8 send / recv arrays, recv = concatenation
+    over ranks).  Returns (this rank's marked term indices, marked count over
+    all ranks, gamma(P_k)) -- the unsharded walk's result bit for bit."""
+    diff = _f64(difference)
+    if diff.shape != (m_rows,):
+        raise DimensionError("mark_blocks: difference size")
+    own = np.ascontiguousarray(np.asarray(own_rows, dtype=np.uint8))
+    if own.shape != (m_rows,):
+        raise DimensionError("mark_blocks: own_rows size")
+    ptr = np.zeros(len(terms) + 1, np.int64)
+    for t, term in enumerate(terms):
+        ptr[t + 1] = ptr[t] + len(term.idx)
+    idx = np.ascontiguousarray(np.concatenate([np.asarray(t.idx, np.int64) for t in terms])
+                               if terms else np.zeros(1, np.int64))
+    val = np.ascontiguousarray(np.concatenate([np.asarray(t.val, np.float64) for t in terms])
+                               if terms else np.zeros(1))
+
+    def ag(_user, send, recv, nbytes):
+        try:
+            s = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (int(nbytes),))
+            r = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                      (int(nbytes) * nranks,))
+            allgather(s, r)
+            return 0
+        except Exception:
+            return 1
+
+    cb = _lib.ALLGATHER_FN(ag)
+    marked = np.zeros(max(1, len(terms)), np.int32)
+    nm, nt, gpk = C.c_int(), C.c_int(), C.c_double()
+    _check(_h.hmb_mark_sharded(len(terms), _ptr(ptr), _ptr(idx), _ptr(val), _ptr(diff),
+                               _ptr(own), m_rows, n_cols, theta, c_sp, nranks, rank, cb,
+                               None, _ptr(marked), C.byref(nm), C.byref(nt), C.byref(gpk)))
+    return marked[: nm.value].copy(), nt.value, gpk.value
+
+
 def nccl_available():
     """(available, version) of the NCCL the library loads at run time."""
     a, v = C.c_int(), C.c_int()

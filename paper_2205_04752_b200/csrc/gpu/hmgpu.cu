@@ -3273,6 +3273,31 @@ int hmgpu_comm_info(hmgpu_ctx* c, int* nranks, int* rank, int* kind, int* row_be
   });
 }
 
+int hmgpu_comm_allgather(hmgpu_ctx* c, const void* send, void* recv,
+                         long long bytes_per_rank) {
+  return guard(c, [&] {
+    if (!c->comm_kind) fail(HMGPU_ERR_STATE, "no communicator attached (hmgpu_comm_*)");
+    if (bytes_per_rank < 0 || (bytes_per_rank > 0 && (!send || !recv)))
+      fail(HMGPU_ERR_INVALID, "bad all-gather arguments");
+    if (bytes_per_rank == 0) return;
+    const size_t b = (size_t)bytes_per_rank;
+    if (c->comm_kind == 3) {  // host callbacks work on host buffers directly
+      if (c->comm_ops.allgather(c->comm_ops.user, send, recv, bytes_per_rank))
+        fail(HMGPU_ERR_COMM, "allgather callback failed");
+      return;
+    }
+    DBuf<char> ds, dr;
+    ds.alloc(b);
+    dr.alloc(b * c->comm_n);
+    CK(cudaMemcpyAsync(ds.p, send, b, cudaMemcpyHostToDevice, c->stream));
+    comm_allgather(c, ds.p, dr.p, b);
+    CK(cudaMemcpyAsync(recv, dr.p, b * c->comm_n, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    ds.free();
+    dr.free();
+  });
+}
+
 int hmgpu_matvec_dist(hmgpu_ctx* c, const double* x, double* y, int nrhs, int mode,
                       int ptr_kind) {
   return guard(c, [&] {

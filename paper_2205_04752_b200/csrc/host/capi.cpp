@@ -629,6 +629,48 @@ int hmb_mark(const hmb_op* op, double theta, int c_sp, long long m_rows, long lo
   });
 }
 
+int hmb_mark_sharded(int n_terms, const long long* term_ptr, const long long* idx,
+                     const double* val, const double* difference,
+                     const unsigned char* own_rows, long long m_rows, long long n_cols,
+                     double theta, int c_sp, int nranks, int rank,
+                     hmb_allgather_fn allgather, void* user, int* marked, int* n_marked,
+                     int* n_marked_total, double* gamma_pk) {
+  return guard([&] {
+    need(difference, "difference");
+    need(own_rows, "own_rows");
+    if (!allgather) throw hmb::Error("mark_blocks: no all-gather");
+    if (n_terms < 0 || m_rows < 0 || nranks < 1 || rank < 0 || rank >= nranks)
+      throw hmb::DimensionError("mark_blocks: bad sizes");
+    if (n_terms > 0) {
+      need(term_ptr, "term_ptr");
+      need(idx, "idx");
+      need(val, "val");
+    }
+    hmb::GammaContributions g;
+    g.difference.assign(difference, difference + m_rows);
+    g.terms.resize(n_terms);
+    for (int t = 0; t < n_terms; ++t) {
+      hmb::BlockTerm& term = g.terms[t];
+      for (long long e = term_ptr[t]; e < term_ptr[t + 1]; ++e) {
+        if (idx[e] < 0 || idx[e] >= m_rows) throw hmb::DimensionError("mark_blocks: row index");
+        term.idx.push_back(idx[e]);
+        term.val.push_back(val[e]);
+        term.norm_sq += val[e] * val[e];
+      }
+    }
+    std::vector<char> own(own_rows, own_rows + m_rows);
+    const hmb::AllGather ag = [&](const void* send, void* recv, long long bytes) {
+      if (allgather(user, send, recv, bytes)) throw hmb::Error("mark_blocks: all-gather failed");
+    };
+    int total = 0;
+    const auto mk = hmb::mark_blocks_sharded(g, own, theta, c_sp, m_rows, n_cols, ag, nranks,
+                                             rank, gamma_pk, &total);
+    if (n_marked) *n_marked = static_cast<int>(mk.size());
+    if (n_marked_total) *n_marked_total = total;
+    if (marked) std::memcpy(marked, mk.data(), mk.size() * sizeof(int));
+  });
+}
+
 int hmb_amvm(hmb_op* op, const double* x, double theta, double eps_amvm,
              int lookahead_steps, int max_iterations, double* b, double* iters8,
              int* n_iters, int* converged) {

@@ -573,9 +573,21 @@ long long HOperator::matvec_bytes() const {
 // into sparse terms over the operator's output rows exactly as the
 // occurrence scatter does (grid cells carry an embedding prefix, so zero
 // values are skipped there, amvm.cpp:112-116).
+namespace {
+GammaContributions gamma_contributions_rows(const HOperator& op, const double* x);
+}
+
 GammaContributions gamma_contributions(const HOperator& op, const double* x) {
   if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
     throw ConfigError("gamma_contributions: sharded operators are not supported");
+  return gamma_contributions_rows(op, x);
+}
+
+namespace {
+// the estimator terms of the blocks the operator holds: every block for a
+// whole operator, the shard's block rows for a shard (difference nonzero on
+// its rows only)
+GammaContributions gamma_contributions_rows(const HOperator& op, const double* x) {
   GammaContributions g;
   const long long M = op.rows();
   const int N = op.row_tree().size();
@@ -630,6 +642,7 @@ GammaContributions gamma_contributions(const HOperator& op, const double* x) {
   g.gamma = std::sqrt(s);
   return g;
 }
+}  // namespace
 
 // the transposed occurrences (gamma_contributions with occ.transposed,
 // amvm.cpp:100-106): per (comp, block) the tail V[:,k:K](U[:,k:K]^T x) over
@@ -752,6 +765,244 @@ std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
   return marked;
 }
 
+// mark_blocks (amvm.cpp:131-184) over ranks that each hold the terms of
+// their own rows (g.difference: the whole difference vector, every rank's
+// rows; own: this rank's rows).  The walk visits the rows in ONE global
+// order (|diff| descending, stable) and stops once the global residual
+// reaches the target; a term lives on the rank owning its block's rows and
+// only terms on the same rows change each other's residual contribution, so
+// each rank walks its own rows in the global order without stopping and
+// records per term Delta = ||term||^2 - 2 <residual, term>; the events of
+// all ranks merged by row position are the unsharded walk's res_sq updates
+// bit for bit, and the stopping event fixes every rank's marked terms.
+// Returns this rank's marked term indices; gamma(P_k) and the marked count
+// over all ranks through the out-parameters.
+std::vector<int> mark_blocks_sharded(const GammaContributions& g, const std::vector<char>& own,
+                                     Real theta, int c_sp, long long m_rows, long long n_cols,
+                                     const AllGather& allgather, int nranks, int rank,
+                                     Real* gamma_pk_out, int* n_marked_out) {
+  const long long M = m_rows;
+  std::vector<int> marked;
+  std::vector<double> residual = g.difference;
+  int n_marked = 0;
+  double gamma2 = 0.0;
+  for (double v : g.difference) gamma2 += v * v;
+  const double gamma = std::sqrt(gamma2);
+  if (gamma > 0.0) {
+    const double threshold =
+        (1.0 - theta) * gamma /
+        std::sqrt(static_cast<double>(c_sp) * static_cast<double>(M) *
+                  static_cast<double>(n_cols));
+    const double target = (1.0 - theta) * gamma;
+    const double target_sq = target * target;
+    std::vector<int> cnt(M + 1, 0);
+    for (const BlockTerm& t : g.terms)
+      for (std::size_t i = 0; i < t.idx.size(); ++i)
+        if (std::abs(t.val[i]) >= threshold) ++cnt[t.idx[i] + 1];
+    for (long long r = 0; r < M; ++r) cnt[r + 1] += cnt[r];
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1), lists(cnt[M]);
+    for (std::size_t t = 0; t < g.terms.size(); ++t)
+      for (std::size_t i = 0; i < g.terms[t].idx.size(); ++i)
+        if (std::abs(g.terms[t].val[i]) >= threshold)
+          lists[fill[g.terms[t].idx[i]]++] = static_cast<int>(t);
+    std::vector<long long> order(M);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](long long a, long long b) {
+      return std::abs(g.difference[a]) > std::abs(g.difference[b]);
+    });
+    double res_sq = 0.0;
+    for (double v : residual) res_sq += v * v;
+    struct Ev {
+      long long pos;
+      double delta;
+    };
+    std::vector<Ev> ev;
+    std::vector<int> ev_term;
+    {
+      std::vector<double> rl = g.difference;
+      std::vector<char> in_set(g.terms.size(), 0);
+      for (long long p = 0; p < M; ++p) {
+        const long long row = order[p];
+        for (int e = cnt[row]; e < cnt[row + 1]; ++e) {
+          const int t = lists[e];
+          if (in_set[t]) continue;
+          in_set[t] = 1;
+          const BlockTerm& term = g.terms[t];
+          double dot = 0.0;
+          for (std::size_t i = 0; i < term.idx.size(); ++i) dot += rl[term.idx[i]] * term.val[i];
+          ev.push_back(Ev{p, term.norm_sq - 2.0 * dot});
+          ev_term.push_back(t);
+          for (std::size_t i = 0; i < term.idx.size(); ++i) rl[term.idx[i]] -= term.val[i];
+        }
+      }
+    }
+    // every rank's events, merged by row position (a row's events come from
+    // one rank, in that rank's walk order)
+    long long ne = static_cast<long long>(ev.size());
+    std::vector<long long> counts(nranks);
+    allgather(&ne, counts.data(), static_cast<long long>(sizeof(long long)));
+    long long maxne = 1;
+    for (long long q : counts) maxne = std::max(maxne, q);
+    std::vector<Ev> send(maxne, Ev{-1, 0.0}), all(static_cast<size_t>(maxne) * nranks);
+    std::copy(ev.begin(), ev.end(), send.begin());
+    allgather(send.data(), all.data(), maxne * static_cast<long long>(sizeof(Ev)));
+    std::vector<long long> cur(nranks, 0);
+    if (res_sq > target_sq) {
+      for (;;) {
+        int best = -1;
+        for (int r = 0; r < nranks; ++r)
+          if (cur[r] < counts[r] &&
+              (best < 0 || all[static_cast<size_t>(r) * maxne + cur[r]].pos <
+                               all[static_cast<size_t>(best) * maxne + cur[best]].pos))
+            best = r;
+        if (best < 0) break;  // every event taken: the walk ran out of terms
+        res_sq += all[static_cast<size_t>(best) * maxne + cur[best]].delta;
+        ++cur[best];
+        ++n_marked;
+        if (res_sq <= target_sq) break;
+      }
+    }
+    for (long long e = 0; e < cur[rank]; ++e) {
+      const BlockTerm& term = g.terms[ev_term[e]];
+      marked.push_back(ev_term[e]);
+      for (std::size_t i = 0; i < term.idx.size(); ++i) residual[term.idx[i]] -= term.val[i];
+    }
+  }
+  // gamma(P_k): the residual rows of every rank, summed in row order
+  for (long long i = 0; i < M; ++i)
+    if (!own[i]) residual[i] = 0.0;
+  std::vector<double> all(static_cast<size_t>(M) * nranks);
+  allgather(residual.data(), all.data(), M * static_cast<long long>(sizeof(double)));
+  double rs = 0.0;
+  for (long long i = 0; i < M; ++i) {
+    double v = 0.0;
+    for (int r = 0; r < nranks; ++r) v += all[static_cast<size_t>(r) * M + i];
+    rs += v * v;
+  }
+  if (gamma_pk_out) *gamma_pk_out = std::sqrt(rs);
+  if (n_marked_out) *n_marked_out = n_marked;
+  return marked;
+}
+
+// Algorithm 2 over a block-row shard: every rank holds the
+// blocks of its rows; the ranks exchange (hmgpu_comm_allgather, collective)
+// the estimator's difference vector (disjoint rows: their sum is exact), the
+// storage figures, and the marking events.  The marking walk of
+// mark_blocks (amvm.cpp:131-184) visits the rows in ONE global order (|diff|
+// descending, stable) and stops once the global residual reaches the
+// target; a term lives on the rank owning its block's rows, and only terms
+// on the same rows change each other's residual contribution, so each rank
+// walks its own rows in the global order without stopping and records, per
+// term, Delta = ||term||^2 - 2 <residual, term>; the merged event stream
+// (by global row position) is the unsharded walk's sequence of res_sq
+// updates, bit for bit, and the stopping event picks every rank's marked
+// set.  x must be given on every rank (the product is hmgpu_matvec_dist).
+std::vector<double> amvm_multiply_sharded(HOperator& op, const double* x,
+                                          const AmvmConfig& cfg, AmvmReport& report) {
+  hmgpu_ctx* c = op.gpu();
+  int nranks = 0, rank = 0, kind = 0;
+  check_status(c, hmgpu_comm_info(c, &nranks, &rank, &kind, nullptr, nullptr),
+               "hmgpu_comm_info");
+  if (!kind)
+    throw ConfigError("amvm_multiply: a sharded operator needs a communicator (hmgpu_comm_*)");
+  report = AmvmReport{};
+  report.c_sp = std::max(1, sparsity_constant(op.partition()));
+  const long long M = op.rows();
+  const int N = op.row_tree().size();
+  const AllGather allgather = [c](const void* send, void* recv, long long bytes) {
+    check_status(c, hmgpu_comm_allgather(c, send, recv, bytes), "hmgpu_comm_allgather");
+  };
+  // rows of this shard (external dof ids)
+  std::vector<char> own(M, 0);
+  {
+    const auto& perm = op.row_tree().perm;
+    const int nout = static_cast<int>(M / N);
+    for (int p = op.row_begin(); p < op.row_end(); ++p)
+      for (int r = 0; r < nout; ++r) own[static_cast<long long>(r) * N + perm[p]] = 1;
+  }
+  // every rank's rows, one vector: the ranks' rows are disjoint
+  auto combine = [&](std::vector<double>& v) {
+    std::vector<double> all(static_cast<size_t>(M) * nranks);
+    allgather(v.data(), all.data(), M * static_cast<long long>(sizeof(double)));
+    for (long long i = 0; i < M; ++i) {
+      double s = 0.0;
+      for (int r = 0; r < nranks; ++r) s += all[static_cast<size_t>(r) * M + i];
+      v[i] = s;
+    }
+  };
+  auto storage = [&](long long& pivots, double& mb) {
+    hmgpu_storage_info si{};
+    check_status(c, hmgpu_storage(c, &si), "hmgpu_storage");
+    struct {
+      long long p;
+      double mb;
+    } mine{si.pivots, si.mb_current};
+    std::vector<decltype(mine)> all(nranks);
+    allgather(&mine, all.data(), static_cast<long long>(sizeof(mine)));
+    pivots = 0;
+    mb = 0.0;
+    for (const auto& a : all) {
+      pivots += a.p;
+      mb += a.mb;
+    }
+  };
+  std::vector<double> b(M), b_hat_prev;
+  auto matvec = [&] {
+    check_status(c, hmgpu_matvec_dist(c, x, b.data(), 1, HMGPU_MODE_CURRENT, HMGPU_PTR_HOST),
+                 "hmgpu_matvec_dist");
+  };
+  matvec();
+  for (int k = 0;; ++k) {
+    const auto t0 = std::chrono::steady_clock::now();
+    GammaContributions g = gamma_contributions_rows(op, x);
+    combine(g.difference);
+    double s2 = 0.0;
+    for (double v : g.difference) s2 += v * v;
+    const double gamma = std::sqrt(s2);
+    if (!b_hat_prev.empty()) {
+      double s = 0.0;
+      for (long long i = 0; i < M; ++i) {
+        const double d = b[i] + g.difference[i] - b_hat_prev[i];
+        s += d * d;
+      }
+      report.iterations.back().e_hat = std::sqrt(s);
+    }
+    AmvmIteration it;
+    it.k = k;
+    it.gamma = gamma;
+    storage(it.cumulative_pivots, it.storage_mb);
+    auto finish = [&](const char* why, bool conv) {
+      it.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count();
+      report.iterations.push_back(it);
+      report.termination = why;
+      report.converged = conv;
+      return b;
+    };
+    if (gamma <= cfg.eps_amvm) return finish("tolerance", true);
+    if (k >= cfg.max_iterations) return finish("max_iterations", false);
+    // ---- marking (mark_blocks, amvm.cpp:131-184) across the ranks
+    std::vector<std::pair<int, int>> mine_marked;
+    int n_marked = 0;
+    double gpk = 0.0;
+    for (int t : mark_blocks_sharded(g, own, cfg.theta, report.c_sp, M, op.cols(), allgather,
+                                     nranks, rank, &gpk, &n_marked))
+      mine_marked.emplace_back(g.terms[t].comp, g.terms[t].block);
+    it.gamma_pk = gpk;
+    it.marked = n_marked;
+    b_hat_prev.resize(M);
+    for (long long i = 0; i < M; ++i) b_hat_prev[i] = b[i] + g.difference[i];
+    if (!mine_marked.empty()) {
+      op.promote(mine_marked);
+      op.extend_lookahead(mine_marked, cfg.lookahead_steps);
+    }
+    matvec();
+    it.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                .count();
+    report.iterations.push_back(it);
+  }
+}
+
 // Algorithm 2 (amvm.cpp:199-268).  The estimator, the marking walk and the
 // refinement run on the device (hmgpu_amvm_*); the host only sees gamma,
 // gamma(P_k), the marked count and the difference vector (for e_hat).
@@ -761,7 +1012,7 @@ std::vector<double> amvm_multiply(HOperator& op, const double* x,
     throw Error("amvm_multiply: theta must lie in (0,1)");
   if (cfg.eps_amvm <= 0.0) throw Error("amvm_multiply: eps_amvm must be positive");
   if (op.row_begin() != 0 || op.row_end() != op.row_tree().size())
-    throw ConfigError("amvm_multiply: sharded operators are not supported");
+    return amvm_multiply_sharded(op, x, cfg, report);
   using clk = std::chrono::steady_clock;
   const auto ts = clk::now();
   report = AmvmReport{};

@@ -14,6 +14,7 @@
 
 #include <memory>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "cluster.hpp"
@@ -182,6 +183,15 @@ GammaContributions gamma_contributions_transposed(const HOperator& op, const dou
 std::vector<int> mark_blocks(const GammaContributions& g, Real theta, int c_sp,
                              long long m_rows, long long n_cols,
                              Real* gamma_pk_out = nullptr);
+
+// recv[r * bytes ...] = send of rank r, for every rank (collective)
+using AllGather = std::function<void(const void* send, void* recv, long long bytes)>;
+// mark_blocks over block-row shards: g holds this rank's terms and the whole
+// difference vector, own flags this rank's rows; returns its marked terms
+std::vector<int> mark_blocks_sharded(const GammaContributions& g, const std::vector<char>& own,
+                                     Real theta, int c_sp, long long m_rows, long long n_cols,
+                                     const AllGather& allgather, int nranks, int rank,
+                                     Real* gamma_pk_out, int* n_marked_out);
 
 struct AmvmIteration {  // amvm.hpp:50-58
   int k = 0;

@@ -86,3 +86,76 @@ def test_shard_ranges_align_with_blocks():
         assert (rows_owned == 1).all()
     with pytest.raises(hm.ConfigError):
         hm.HMatrix.kelvin(hm.Mesh.icosphere(1), b_min=32, device=-1, shard=(0, 8))
+
+
+def _mark_worker(rank, world, port, outdir, theta):
+    """One rank of the sharded marking walk (hmb_mark_sharded): the oracle's
+    estimator terms of the blocks on this rank's rows, the whole difference
+    vector, the events exchanged over gloo."""
+    import paper_2205_04752_b200 as hm
+    from paper_2205_04752_b200.dist import torch_transport
+    from oracle import oracle as orc
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    mesh = hm.Mesh.ellipsoid(3, 2.0, 1.0, 0.5)
+    a = mesh.arrays()
+    N = mesh.num_triangles
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=16, eta=1.0)
+    o.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    c = a["centroids"]
+    bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.1 ** 2))
+    x = np.tile(bump, 3) + 1e-3 * orc.random_vector(3 * N, 3)
+    gamma, diff, terms = o.gamma(x)
+    op = hm.HMatrix.kelvin(mesh, b_min=16, eta=1.0, device=-1, shard=(rank, world))
+    rb, re = op.row_range
+    t = op.tree()
+    blocks = op.partition_blocks()
+    own = np.zeros(3 * N, dtype=bool)
+    for r in range(3):
+        own[r * N + t.perm[rb:re]] = True
+    mine = [i for i, term in enumerate(terms)
+            if t.nodes[blocks[term["block"], 0], 0] >= rb and
+            t.nodes[blocks[term["block"], 0], 1] <= re]
+    local = [hm.BlockTerm(terms[i]["comp"], terms[i]["block"], terms[i]["idx"],
+                          terms[i]["val"], terms[i]["norm_sq"]) for i in mine]
+    _, allgather = torch_transport()
+    marked, total, gpk = hm.mark_blocks_sharded(local, diff, own, theta,
+                                                op.sparsity_constant, 3 * N, 3 * N, world,
+                                                rank, allgather)
+    np.save(os.path.join(outdir, f"m{rank}.npy"),
+            np.array([[mine[i] for i in marked], total, gpk, len(mine)], dtype=object),
+            allow_pickle=True)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,theta", [(2, 0.7), (3, 0.5), (4, 0.9)])
+def test_sharded_marking_matches_unsharded_walk(tmp_path, world, theta):
+    """hmb_mark_sharded (the marking step of the sharded adaptive matvec) on
+    CPU ranks over gloo: the union of the ranks' marked terms, the marked
+    count and gamma(P_k) equal the oracle's unsharded mark_blocks bit for bit,
+    and every term belongs to exactly one rank."""
+    import paper_2205_04752_b200 as hm
+    from oracle import oracle as orc
+
+    port = _free_port()
+    mp.spawn(_mark_worker, args=(world, port, str(tmp_path), theta), nprocs=world, join=True)
+    outs = [np.load(tmp_path / f"m{r}.npy", allow_pickle=True) for r in range(world)]
+    mesh = hm.Mesh.ellipsoid(3, 2.0, 1.0, 0.5)
+    a = mesh.arrays()
+    N = mesh.num_triangles
+    o = orc.Problem.kelvin(a["vertices"], a["triangles"], b_min=16, eta=1.0)
+    o.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    c = a["centroids"]
+    bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.1 ** 2))
+    x = np.tile(bump, 3) + 1e-3 * orc.random_vector(3 * N, 3)
+    _, _, terms = o.gamma(x)
+    op = hm.HMatrix.kelvin(mesh, b_min=16, eta=1.0, device=-1)
+    ref_marked, ref_gpk = o.mark(theta, op.sparsity_constant, 3 * N, 3 * N, len(terms))
+    assert len(ref_marked) > 0
+    union = sorted(i for r in range(world) for i in outs[r][0])
+    assert union == sorted(ref_marked.tolist())
+    assert sum(outs[r][3] for r in range(world)) == len(terms)
+    for r in range(world):
+        assert outs[r][1] == len(ref_marked)
+        assert outs[r][2] == ref_gpk

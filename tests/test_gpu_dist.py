@@ -109,3 +109,69 @@ def test_matvec_dist_single_rank_nccl():
     assert h.comm_info()["kind"] == "nccl"
     x = orc.random_vector(h.cols, 3)
     assert (h.matvec_dist(x) == h.matvec(x)).all()
+
+
+def _amvm_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    import paper_2205_04752_b200 as hm
+    from paper_2205_04752_b200.dist import torch_transport
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    mesh, x = _amvm_case()
+    h = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0, shard=(rank, world))
+    h.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    h.attach_comm(world, rank, *torch_transport())
+    b, rep = h.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, max_iterations=5)
+    gk, gl, _, _ = h.ranks()
+    np.save(os.path.join(outdir, f"a{rank}.npy"),
+            np.array([b, [(r.gamma, r.gamma_pk, r.marked, r.cumulative_pivots, r.storage_mb,
+                           r.e_hat) for r in rep.iterations], gk, gl], dtype=object),
+            allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _amvm_case():
+    import paper_2205_04752_b200 as hm
+    mesh = hm.Mesh.ellipsoid(4, 2.0, 1.0, 0.5)
+    c = mesh.arrays()["centroids"]
+    bump = np.exp(-np.sum((c - np.array([2.0, 0, 0])) ** 2, axis=1) / (2 * 0.05 ** 2))
+    x = np.tile(bump, 3) + 1e-3 * hm.random_vector(3 * len(c), 3)
+    return mesh, x
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_amvm_sharded_world_on_one_gpu(tmp_path, world):
+    """The adaptive matvec on block-row shards: the ranks
+    exchange the estimator's difference vector and the marking events; the
+    record (gamma, marked count, cumulative pivots of every sweep) must be
+    the unsharded operator's, bit for bit, every block's ranks after the
+    loop the unsharded ones, and b the same product."""
+    import torch.multiprocessing as mp
+    import paper_2205_04752_b200 as hm
+
+    port = _free_port()
+    mp.spawn(_amvm_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    outs = [np.load(tmp_path / f"a{r}.npy", allow_pickle=True) for r in range(world)]
+    mesh, x = _amvm_case()
+    full = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+    full.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    bf, rep = full.amvm_multiply(x, theta=0.7, eps_amvm=1e-6, max_iterations=5)
+    fk, fl, _, _ = full.ranks()
+    its = [(r.gamma, r.gamma_pk, r.marked, r.cumulative_pivots, r.storage_mb)
+           for r in rep.iterations]
+    assert sum(r.marked for r in rep.iterations) > 0
+    for r in range(world):
+        b, rit, gk, gl = outs[r]
+        assert len(rit) == len(its)
+        for a, e in zip(rit, its):
+            assert a[0] == e[0] and a[2] == e[2] and a[3] == e[3], (r, a, e)
+            assert a[1] == pytest.approx(e[1], rel=1e-12)
+            assert a[4] == pytest.approx(e[4], rel=1e-12)
+        assert np.linalg.norm(b - bf) <= 1e-13 * np.linalg.norm(bf)
+        own = gk >= 0
+        assert (gk[own] == fk[own]).all() and (gl[own] == fl[own]).all()
+    # every low-rank (comp, block) is owned by exactly one rank
+    owned = sum((outs[r][2] >= 0).astype(int) for r in range(world))
+    assert (owned[fk >= 0] == 1).all()
