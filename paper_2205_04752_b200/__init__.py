@@ -11,7 +11,8 @@ from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflo
                   SolveStats, bpcg_solve, SaddleEstimator, baca_solve_saddle,
                   MeshError, Mode, amvm_multiply, assemble, device_count, gamma_contributions,
                   host_tree_and_partition, nccl_available, nccl_unique_id,
-                  mark_blocks_sharded)
+                  mark_blocks_sharded, amvm_multiply_occurrences, rhs_occurrences,
+                  assemble_rhs)
 
 __all__ = [
     "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
@@ -23,4 +24,5 @@ __all__ = [
     "MeshError",
     "Mode", "amvm_multiply", "assemble", "device_count", "gamma_contributions",
     "host_tree_and_partition", "nccl_available", "nccl_unique_id", "mark_blocks_sharded",
+    "amvm_multiply_occurrences", "rhs_occurrences", "assemble_rhs",
 ]

@@ -1415,6 +1415,156 @@ class SaddleEstimator:
         return ek, terms, diff
 
 
+def amvm_multiply_occurrences(occurrences, matvec, x, out_dim: int, n_cols: int,
+                              cfg: Optional[AmvmConfig] = None, h_order=None, **kw):
+    """amvm_multiply (amvm.cpp:199-268) over an operator EXPRESSION given by
+    its flattened H-leaf occurrences (flatten_occurrences, expr.cpp:424-510):
+    occurrences = [(h, transposed, coeff, suffix, prefix)] with h an HMatrix
+    context (every component of a grid context is one H-matrix of the
+    reference), suffix / prefix sparse (None = identity); matvec(x) the
+    expression's product at the current ranks (numpy in / out).  Per sweep:
+    gamma_contributions over the occurrences (amvm.cpp:46-125: every
+    occurrence's device look-ahead tail on suffix x, mapped through prefix and
+    coeff, summed per (H-matrix, block), terms grouped by H-matrix in
+    h_order (the expression's first-appearance order, (context, comp) pairs;
+    default: the order of the occurrence list) then block), the marking walk
+    (mark_blocks, amvm.cpp:131-184, on the library's host walk), promotion +
+    look-ahead extension of the marked blocks on the device, and the
+    product again.  Returns (b, AmvmReport)."""
+    import time as _time
+    cfg = cfg or AmvmConfig(**kw)
+    if not 0.0 < cfg.theta < 1.0:
+        raise ConfigError("amvm_multiply: theta must lie in (0,1)")
+    if cfg.eps_amvm <= 0.0:
+        raise ConfigError("amvm_multiply: eps_amvm must be positive")
+    if cfg.max_iterations < 0:
+        raise ConfigError("amvm_multiply: max_iterations must be >= 0")
+    x = _f64(x)
+    if x.shape != (n_cols,):
+        raise DimensionError("amvm_multiply: size")
+    ctxs = []
+    for o in occurrences:
+        if all(o[0] is not h for h in ctxs):
+            ctxs.append(o[0])
+    if h_order is None:
+        h_order = [(h, q) for h in ctxs for q in range(6 if h.ncomp == 6 else 1)]
+    rank_of = {(id(h), q): i for i, (h, q) in enumerate(h_order)}
+    # operator_sparsity_constant: the largest c_sp over the distinct partitions
+    c_sp = max([1] + [h.sparsity_constant for h in ctxs])
+
+    def one_world(send, recv):
+        recv[:] = send
+
+    def estimate():
+        acc = {}
+        for (h, tr, coeff, suffix, prefix) in occurrences:
+            xin = x if suffix is None else suffix @ x
+            g = h.gamma_contributions(xin, term_data=True, transposed=tr)
+            for t in g.terms:
+                if prefix is None:
+                    v = np.zeros(out_dim)
+                    v[t.idx] = coeff * t.val
+                else:
+                    v = prefix[:, t.idx] @ (coeff * t.val)
+                key = (rank_of[(id(h), t.comp)], t.block)
+                if key not in acc:
+                    acc[key] = (h, t.comp, t.block, np.zeros(out_dim))
+                acc[key][3][:] += v
+        terms = []
+        diff = np.zeros(out_dim)
+        for key in sorted(acc):
+            h, comp, block, v = acc[key]
+            idx = np.nonzero(v)[0]
+            if len(idx) == 0:
+                continue
+            terms.append(BlockTerm(comp, block, idx.astype(np.int64), v[idx],
+                                   float(v[idx] @ v[idx])))
+            terms[-1].ctx = h
+            diff[idx] += v[idx]  # term by term, as amvm.cpp:111-115
+        return terms, diff
+
+    t_start = _time.perf_counter()
+    b = _f64(matvec(x))
+    b_hat_prev = None
+    its = []
+    for k in range(cfg.max_iterations + 1):
+        t0 = _time.perf_counter()
+        terms, diff = estimate()
+        # sequential sum in row order (difference.norm(), amvm.cpp:124);
+        # numpy's sum is pairwise
+        gamma = float(np.sqrt(np.cumsum(diff * diff)[-1])) if out_dim else 0.0
+        if b_hat_prev is not None:
+            its[-1].e_hat = float(np.linalg.norm(b + diff - b_hat_prev))
+        pivots = sum(h.total_pivots() for h in ctxs)
+        storage = sum(h.storage_mb_current() for h in ctxs)
+        it = AmvmIteration(k, gamma, 0.0, 0, pivots, storage, -1.0, 0.0)
+        if gamma <= cfg.eps_amvm or k >= cfg.max_iterations:
+            it.ms = 1e3 * (_time.perf_counter() - t0)
+            its.append(it)
+            conv = gamma <= cfg.eps_amvm
+            return b, AmvmReport(its, "tolerance" if conv else "max_iterations", conv, c_sp)
+        marked, n_marked, gpk = mark_blocks_sharded(terms, diff, np.ones(out_dim, bool),
+                                                    cfg.theta, c_sp, out_dim, n_cols, 1, 0,
+                                                    one_world)
+        it.gamma_pk, it.marked = gpk, n_marked
+        b_hat_prev = b + diff
+        by_ctx = {}
+        for t in marked:
+            by_ctx.setdefault(id(terms[t].ctx), (terms[t].ctx, []))[1].append(
+                (terms[t].comp, terms[t].block))
+        for h, pairs in by_ctx.values():
+            h.promote(pairs)
+            h.extend_lookahead(pairs, cfg.lookahead_steps)
+        b = _f64(matvec(x))
+        it.ms = 1e3 * (_time.perf_counter() - t0)
+        its.append(it)
+    raise AssertionError("unreachable")
+
+
+def rhs_occurrences(sys: "SaddleSystem"):
+    """The flattened H-leaf occurrences of rhs_operator (baca.cpp:42-55):
+    rows [Dirichlet-triangle dofs; Neumann-node dofs] of
+    [-V_h, M/2 + K_h; M'/2 - K_h', -D_h] over x = [g_N; g_D] (the mass
+    matrix is sparse and carries no H-leaf), and the H-matrices in the
+    expression's first-appearance order: V_Delta (in -V_h's diag3), the six
+    V_kl components, K_Delta."""
+    import scipy.sparse as sp
+    est = SaddleEstimator(sys)
+    ops = sys.ops
+    m3, n3 = 3 * ops.m, 3 * ops.n
+    nt, nu = sys.nt, sys.nu_
+    out = nt + nu
+    P0 = sp.vstack([est.St, sp.csr_matrix((nu, m3))]).tocsr()        # top rows
+    P1 = sp.vstack([sp.csr_matrix((nt, n3)), est.Su]).tocsr()        # bottom rows
+    Rn = sp.hstack([sp.identity(m3), sp.csr_matrix((m3, n3))]).tocsr()  # g_N
+    Rd = sp.hstack([sp.csr_matrix((n3, m3)), sp.identity(n3)]).tocsr()  # g_D
+    neg = lambda occ: [(h, tr, -c, sf, pf) for (h, tr, c, sf, pf) in occ]
+    occ = neg(est._vh_occ(1.0, Rn, P0))                                # -V_h g_N
+    occ += est._kh_occ(1.0, Rd, P0)                                    # +K_h g_D
+    occ += est._transpose(neg(est._kh_occ(1.0, P1.T.tocsr(), Rn.T.tocsr())))  # -K_h' g_N
+    occ += neg(est._dh_occ(Rd, P1))                                    # -D_h g_D
+    order = [(ops.vdelta, 0)] + [(ops.vkl, q) for q in range(6)] + [(ops.kdelta, 0)]
+    return occ, order, out, m3 + n3
+
+
+def assemble_rhs(sys: "SaddleSystem", g_neumann, g_dirichlet, amvm: bool = False,
+                 amvm_cfg: Optional[AmvmConfig] = None):
+    """assemble_rhs (baca.cpp:57-76): f = rhs_operator [g_N; g_D], through the
+    adaptive matvec over the composite operator when amvm is set (the paper's
+    Table 3 workload).  Returns (f, AmvmReport or None)."""
+    gn = _f64(g_neumann)
+    gd = _f64(g_dirichlet)
+    if gn.shape != (3 * sys.ops.m,) or gd.shape != (3 * sys.ops.n,):
+        raise DimensionError("assemble_rhs: boundary data size")
+    if not amvm:
+        return sys.rhs(gn, gd), None
+    occ, order, out, ncols = rhs_occurrences(sys)
+    m3 = 3 * sys.ops.m
+    return amvm_multiply_occurrences(occ, lambda v: sys.rhs(v[:m3], v[m3:]),
+                                     np.concatenate([gn, gd]), out, ncols,
+                                     amvm_cfg or AmvmConfig(), h_order=order)
+
+
 def baca_solve_saddle(sys: "SaddleSystem", f, cfg: Optional[BacaConfig] = None):
     """baca_solve (baca.cpp:488-600) for the mixed system: BPCG under the
     adaptive accuracy condition, E_k over the V / K / D families, Doerfler
