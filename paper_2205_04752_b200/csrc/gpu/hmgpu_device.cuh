@@ -115,7 +115,13 @@ __device__ __forceinline__ int kelvin_tier(double px, double py, double pz,
 // and restated operation for operation by the oracle (oracle/hmbem_oracle.cpp
 // rsqrt_canon), so entries stay bit-identical; about 4x cheaper than the
 // IEEE division of an IEEE square root.
+// HMGPU_FAST_ENTRY (measurement builds only, scripts/aca_fast_ab.py): the
+// CUDA math library's rsqrt instead (hardware seed + Newton), to price the
+// bit-exact contract; its results are not bit-identical to the oracle.
 __device__ __forceinline__ double rsqrt_canon(double x) {
+#ifdef HMGPU_FAST_ENTRY
+  return rsqrt(x);
+#endif
   const long long i = 0x5fe6eb50c7b537a9LL - (__double_as_longlong(x) >> 1);
   double y = __longlong_as_double(i);
   const double h = 0.5 * x;
