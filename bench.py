@@ -637,6 +637,63 @@ def relaunch_multi(args):
     return subprocess.call(cmd)
 
 
+def mrhs_leg(hm, torch, h, steps, warmup, device, name):
+    """16 right-hand sides on an assembled operator (config 5's batched
+    product, measured at config 3): device-timed sweeps with 16 normal(0,1)
+    RHS (seed 4), the fp64 tensor-core roofline of the two passes, and the
+    committed ncu traffic of the same workload."""
+    nrhs = 16
+    X = hm.random_vector(h.cols * nrhs, 4, "normal").reshape(nrhs, h.cols)
+    xt = torch.tensor(X, dtype=torch.float64, device=f"cuda:{device}")
+    yt = torch.zeros((nrhs, h.rows), dtype=torch.float64, device=f"cuda:{device}")
+    stream = torch.cuda.ExternalStream(h.stream(), device=f"cuda:{device}")
+
+    def step():
+        h.matvec_ptr(xt.data_ptr(), yt.data_ptr(), nrhs)
+
+    for _ in range(max(warmup, 2)):
+        step()
+    torch.cuda.synchronize()
+    h.set_profiling(True)
+    for k in OUR_KERNELS:
+        h.kernel_times(k, reset=True)
+    nprof = 3
+    for _ in range(nprof):
+        step()
+    torch.cuda.synchronize()
+    kt = {k: h.kernel_times(k, reset=True) for k in OUR_KERNELS}
+    h.set_profiling(False)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / steps
+    ms_dom = (kt["hmv16_z"][0] + kt["hmv16_leaf"][0]) / nprof
+    flops = 2.0 * nrhs * weighted_entries(h)
+    dmma_peak = hm.dmma_peak_tflops(device)
+    peak, peak_src = measured_peaks()
+    alg_bytes = h.storage()["matvec_bytes"] + 8 * (nrhs - 1) * (h.rows + h.cols)
+    traffic, traffic_src = profile_traffic(name, nrhs)
+    achieved = flops / (ms_dom * 1e-3) / 1e12
+    return {"nrhs": nrhs, "value": h.rows * nrhs / (ms_step * 1e-3), "unit": "dof-RHS/s",
+            "ms_per_step": ms_step,
+            "kernel_ms": {k: kt[k][0] / nprof for k in ("gather", "hmv16_z", "hmv16_leaf")},
+            "roofline": {"bound": "tensor",
+                         "kernel": "hmv16_z_kernel + hmv16_y_kernel (DMMA, TMA-fed)",
+                         "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+                         "frac": achieved / dmma_peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "peak_source": "measured (hmgpu_dmma_peak, fp64 m8n8k4 chains)",
+                         "algorithmic_flops_per_step": flops,
+                         "algorithmic_bytes_per_step": alg_bytes,
+                         "hbm_frac": alg_bytes / (ms_dom * 1e-3) / 1e9 / peak,
+                         "hbm_peak_source": peak_src, "ms_kernel": ms_dom}}
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2205_04752_b200 as hm
@@ -715,6 +772,11 @@ def run_ours(args, cfg):
                    "ms_per_step": r3["ms_per_step"], "roofline": r3["roofline"],
                    "e2e": r3["e2e"], "assembly": r3["assembly"],
                    "kernel_ms": r3["kernel_ms"], "clocks": r3["clocks"]}
+            try:
+                obj["nrhs16"] = mrhs_leg(hm, torch, h3, min(args.steps, 10), args.warmup,
+                                         device, "c3")
+            except Exception as e:
+                obj["nrhs16"] = {"error": str(e)}
             line["c3"] = obj
             del h3
         except Exception as e:  # secondary object: never costs the headline line

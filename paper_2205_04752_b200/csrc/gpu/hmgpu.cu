@@ -491,7 +491,7 @@ struct hmgpu_ctx {
   DBuf<YItem16> d_yitem16;
   DBuf<M16Copy> d_ycopy16;
   DBuf<int> d_zcoff16, d_ycoff16;
-  DBuf<double> d_p16arena, d_z16buf, d_xp16;
+  DBuf<double> d_z16buf, d_xp16;
   DBuf<AdmBlock> d_ablocks;
   DBuf<int> d_pleaf_ptr;
   std::vector<int> p_leaf_ptr;
@@ -540,7 +540,7 @@ struct hmgpu_ctx {
     d_pentries.free(); d_pleaf_ptr.free();
     d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free();
     d_yitem16.free(); d_ycopy16.free();
-    d_p16arena.free(); d_z16buf.free(); d_xp16.free(); d_ablocks.free();
+    d_z16buf.free(); d_xp16.free(); d_ablocks.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
     d_ptr.free(); d_lists.free(); d_order.free(); d_idx.free(); d_marked.free(); d_nm.free();
     d_mids.free(); d_spoff.free(); d_aterms.free(); d_aout.free(); d_diff.free();
@@ -1296,6 +1296,7 @@ long long mv_unit_cap() {
 
 void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   if (nrhs != 1) fail(HMGPU_ERR_INVALID, "streamed matvec: single right-hand side");
+  c->p16_valid = false;  // the stream arena takes the spare arena the p16 plan used
   auto tp0 = std::chrono::steady_clock::now();
   auto pphase = [&](const char* what) {
     if (!verbose()) return;
@@ -1719,8 +1720,8 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
 
 // ---- multi-RHS plan (hmgpu_mrhs.cuh) ----------------------------------------
 // HMGPU_M16_CFG="ns,stage": ring depth (3, 4, 6 or 9) and doubles per stage
-struct M16Cfg {
-  int ns = 3, stage = 4608;
+struct M16Cfg {  // measured on config 3: 3 x 3072 (3 CTAs / SM) best
+  int ns = 3, stage = 3072;
 };
 M16Cfg m16_cfg() {
   static const M16Cfg cfg = [] {
@@ -2078,11 +2079,16 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   CK(cudaMemsetAsync(c->d_z16buf.p, 0, ((size_t)zsize + 2) * sizeof(double), c->stream));
   c->d_xp16.ensure(((size_t)c->n_cols + M16_XPAD) * XP);
   CK(cudaMemsetAsync(c->d_xp16.p, 0, c->d_xp16.n * sizeof(double), c->stream));
-  c->d_p16arena.ensure((size_t)alen + 2);
-  CK(cudaMemsetAsync(c->d_p16arena.p, 0, ((size_t)alen + 2) * sizeof(double), c->stream));
+  // the packed factors live in the idle compaction arena, like the 1-RHS
+  // stream arena (no new device memory in steady state; at most one of the
+  // two plans is valid at a time)
+  c->sync();
+  c->plan_valid = false;
+  c->spare_arena.ensure((size_t)alen + 2, c->device);
+  CK(cudaMemsetAsync(c->spare_arena.p, 0, ((size_t)alen + 2) * sizeof(double), c->stream));
   {
     const unsigned long long base[5] = {
-        (unsigned long long)c->d_yitem16.p, (unsigned long long)c->d_p16arena.p,
+        (unsigned long long)c->d_yitem16.p, (unsigned long long)c->spare_arena.p,
         (unsigned long long)c->d_z16buf.p, (unsigned long long)c->d_dense.p,
         (unsigned long long)c->d_xp16.p};
     for (size_t q = 0; q < ycopies.size(); ++q) ycopies[q].src += base[ckind[q]];
@@ -2093,7 +2099,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     d_packs.upload(packs, c->stream);
     c->timed("pack16", [&] {
       pack_kernel<<<grid_for(c, ((long long)packs.size() + 7) / 8, 16), 256, 0, c->stream>>>(
-          d_packs.p, (int)packs.size(), c->d_arena.p, c->d_p16arena.p);
+          d_packs.p, (int)packs.size(), c->d_arena.p, c->spare_arena.p);
     });
     c->sync();
     d_packs.free();
@@ -2134,7 +2140,7 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
   (void)mode;  // the plan carries the mode's ranks
   M16Params P{};
   P.tasks = c->d_ztask16.p;
-  P.arena = c->d_p16arena.p;
+  P.arena = c->spare_arena.p;  // the packed p16 arena
   P.dense = c->d_dense.p;
   P.xp = c->d_xp16.p;
   P.z = c->d_z16buf.p;
