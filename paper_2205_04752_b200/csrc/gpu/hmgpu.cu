@@ -2008,17 +2008,37 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       return d.kind == Y16_ADM ? (long long)d.len + d.len2 : (long long)d.jd * d.PR + d.len2;
     };
     auto copy = [&](int kind, long long src_bytes, long long dst, long long bytes) {
-      ycopies.push_back(M16Copy{(unsigned long long)src_bytes, (int)dst, (int)bytes});
+      // Z (2) and x (4) are re-read by many stages: kept in L2 (evict last)
+      const int keep = (kind == 2 || kind == 4) ? M16_KEEP : 0;
+      ycopies.push_back(M16Copy{(unsigned long long)src_bytes, (int)dst | keep, (int)bytes});
       ckind.push_back((unsigned char)kind);
     };
+    // leaves per CTA: contiguous runs of about equal bytes, or (default)
+    // cyclic -- leaf i on CTA i mod ncta, so the CTAs work on a window of
+    // neighbouring leaves at any time and the Z of the blocks above them is
+    // read from L2 by all of them (HMGPU_M16_YORDER=runs for the runs)
+    static const bool yruns = [] {
+      const char* e = std::getenv("HMGPU_M16_YORDER");
+      return e && std::string(e) == "runs";
+    }();
+    std::vector<std::vector<int>> cleaves(ncta);
+    for (int k = 0; k < ncta; ++k)
+      if (yruns)
+        for (int L = fl[k]; L < fl[k + 1]; ++L) cleaves[k].push_back(L);
+    if (!yruns)
+      for (int L = 0; L < nl; ++L) cleaves[L % ncta].push_back(L);
+    std::vector<int> cpieces;
     for (int k = 0; k < ncta; ++k) {
       ycoff[k] = (int)ystages.size();
-      const int p1 = lptr[fl[k + 1]];
-      for (int pi = lptr[fl[k]]; pi < p1;) {
+      cpieces.clear();
+      for (int L : cleaves[k])
+        for (int q = lptr[L]; q < lptr[L + 1]; ++q) cpieces.push_back(q);
+      const int p1 = (int)cpieces.size();
+      for (int pi = 0; pi < p1;) {
         int pe = pi;
         long long used = 0;
-        while (pe < p1 && pe - pi < Y16_MAXIT && used + plen(yst[pe]) <= SD2)
-          used += plen(yst[pe++]);
+        while (pe < p1 && pe - pi < Y16_MAXIT && used + plen(yst[cpieces[pe]]) <= SD2)
+          used += plen(yst[cpieces[pe++]]);
         if (pe == pi) fail(HMGPU_ERR_INVALID, "multi-RHS piece larger than a stage");
         M16Stage st{};
         st.cbeg = (int)ycopies.size();
@@ -2031,7 +2051,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
              (long long)sizeof(YItem16) * (1 + st.nitems));
         long long off = Y16_HDR, bytes = (long long)sizeof(YItem16) * (1 + st.nitems);
         for (int q = pi; q < pe; ++q) {
-          const YStage16& d = yst[q];
+          const YStage16& d = yst[cpieces[q]];
           YItem16 it{};
           it.kind = d.kind;
           it.leaf = d.leaf;

@@ -107,8 +107,10 @@ struct __align__(16) M16Stage {
 };
 struct __align__(16) M16Copy {
   unsigned long long src;
-  int dst, bytes;  // dst in doubles from the stage start
+  int dst, bytes;  // dst in doubles from the stage start (| M16_KEEP: evict last in L2)
 };
+constexpr int M16_KEEP = 1 << 30;
+constexpr int M16_DST_MASK = M16_KEEP - 1;
 
 // host-side piece of the phase-2 plan (one block piece / column group)
 struct YStage16 {
@@ -133,6 +135,27 @@ struct M16Params {
   int dbg;                   // A/B: 1 = stream only (no compute), 2 = compute only
   unsigned long long* prof;  // A/B (dbg 3): cycle counters of the stage loop
 };
+
+// L2 eviction policies for the bulk copies: the streamed factors and
+// near-field columns are read once per pass (evict first), the gathered x
+// rows and the blocks' Z are re-read by many stages (evict last), so the
+// stream does not push them out of L2
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 // D = A B + D, A 8x4 (row), B 4x8 (col), fp64; lane (g = lane/4, t = lane%4)
 // holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1]
@@ -245,8 +268,10 @@ __device__ __forceinline__ void z16_issue(const M16Params& P, double* st, uint64
   mbar_expect_tx(bar, 32u + 80u + vb + xb);
   bulk_g2s(st, gch, 32u, bar);
   bulk_g2s(st + 4, P.tasks + ch.task, 80u, bar);
-  if (vb) bulk_g2s(st + M16_HDR, P.arena + ch.vsrc, vb, bar);
-  if (xb) bulk_g2s(st + M16_HDR + ch.vlen, P.xp + (long long)ch.xcol * XP, xb, bar);
+  if (vb) bulk_g2s_hint(st + M16_HDR, P.arena + ch.vsrc, vb, bar, l2_policy(false));
+  if (xb)
+    bulk_g2s_hint(st + M16_HDR + ch.vlen, P.xp + (long long)ch.xcol * XP, xb, bar,
+                  l2_policy(true));
 }
 
 template <int NS>
@@ -258,8 +283,13 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
   ring_init<NS>(sm, full, empty, P.stage);
   const ZChunk16* chunks = static_cast<const ZChunk16*>(P.desc);
   const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
-  // m-tiles warp, warp + 8, warp + 16 of the task
+  // m-tiles warp, warp + 8, warp + 16 of the task; their rows are resolved
+  // once per task (the task's first chunk) and kept in registers
   double acc[3][2][2];
+  int ntl = 0;                 // this warp's m-tiles in the task
+  int arow[3] = {0, 0, 0};     // this lane's row in the staged V^T (its tile's)
+  int xcol[3] = {0, 0, 0};     // its operand group r: x columns 16 r ..
+  int zdst[3] = {-1, -1, -1};  // its Z row * ZP + part * 16 (-1: padding row)
   ZChunk16 nxt{};
   if (warp == M16_NW && n > 0) nxt = chunks[c0];
   auto issue = [&](double* st, uint64_t* bar, int j) {
@@ -274,41 +304,53 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
     const double* sX = sV + ch.vlen;
     const int Pp = ch.P;
     if (ch.flags & 1) {
+      ntl = 0;
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[q][nt][0] = acc[q][nt][1] = 0.0;
+      for (int q = 0; q < 3; ++q) {
+        acc[q][0][0] = acc[q][0][1] = acc[q][1][0] = acc[q][1][1] = 0.0;
+        const int p = warp + M16_NW * q;
+        if (p >= tk.ntiles) continue;
+        ntl = q + 1;
+        // operand group r (rows multiply x_r), this lane's row rho of it ->
+        // (segment, part, l): Z_c (part 0) if C_c = r, W_c (part 1) if R_c = r
+        const int r = p >= tk.gtile[2] ? 2 : (p >= tk.gtile[1] ? 1 : 0);
+        const int rho = (p - tk.gtile[r]) * 8 + g;
+        int cum = 0, e = 0, seg = tk.gent[r][0] >> 1;
+        for (; e < tk.gn[r]; ++e) {
+          seg = tk.gent[r][e] >> 1;
+          if (rho < cum + tk.len[seg]) break;
+          cum += tk.len[seg];
+        }
+        xcol[q] = r * 16;
+        if (rho < tk.grows[r]) {
+          const int l = rho - cum;
+          arow[q] = tk.vrow[seg] + l;
+          zdst[q] = (tk.zrow[seg] + l) * ZP + (tk.gent[r][e] & 1) * 16;
+        } else {
+          arow[q] = -1;
+          zdst[q] = -1;
+        }
+      }
     }
+    const double* X0 = sX + t * XP + g;
+    // k-steps outer, the warp's tiles inner: 2 ntl independent DMMA chains
+#pragma unroll 2
+    for (int kk = 0; kk < Pp; kk += 4) {
+      const double* xk = X0 + kk * XP;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int p = warp + M16_NW * q;
-      if (p >= tk.ntiles) break;  // warp-uniform
-      // operand group r (rows multiply x_r), this lane's row rho of it ->
-      // (segment, part, l): Z_c (part 0) if C_c = r, W_c (part 1) if R_c = r
-      const int r = p >= tk.gtile[2] ? 2 : (p >= tk.gtile[1] ? 1 : 0);
-      const int rho = (p - tk.gtile[r]) * 8 + g;
-      const bool valid = rho < tk.grows[r];
-      int cum = 0, e = 0, seg = 0;
-      for (; e < tk.gn[r]; ++e) {
-        seg = tk.gent[r][e] >> 1;
-        if (rho < cum + tk.len[seg]) break;
-        cum += tk.len[seg];
+      for (int q = 0; q < 3; ++q) {
+        if (q >= ntl) break;  // warp-uniform
+        const double u = sV[(arow[q] < 0 ? 0 : arow[q]) * Pp + kk + t];
+        const double a = arow[q] < 0 ? 0.0 : u;
+        dmma(acc[q][0][0], acc[q][0][1], a, xk[xcol[q]]);
+        dmma(acc[q][1][0], acc[q][1][1], a, xk[xcol[q] + 8]);
       }
-      if (!valid) seg = tk.gent[r][0] >> 1;
-      const int l = valid ? rho - cum : 0;
-      const double* A0 = sV + (tk.vrow[seg] + l) * Pp + t;
-      const double* X0 = sX + t * XP + r * 16 + g;
-#pragma unroll 4
-      for (int kk = 0; kk < Pp; kk += 4) {
-        const double u = A0[kk];
-        const double a = valid ? u : 0.0;
-        const double* x0 = X0 + kk * XP;
-        dmma(acc[q][0][0], acc[q][0][1], a, x0[0]);
-        dmma(acc[q][1][0], acc[q][1][1], a, x0[8]);
-      }
-      if ((ch.flags & 2) && valid) {  // last chunk: this lane's Z row
-        const int part = tk.gent[r][e] & 1;
-        double* zr = P.z + tk.zdst + (long long)(tk.zrow[seg] + l) * ZP + part * 16 + 2 * t;
+    }
+    if (ch.flags & 2) {  // last chunk: this lane's Z rows
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (q >= ntl || zdst[q] < 0) continue;
+        double* zr = P.z + tk.zdst + zdst[q] + 2 * t;
         *reinterpret_cast<double2*>(zr) = make_double2(acc[q][0][0], acc[q][0][1]);
         *reinterpret_cast<double2*>(zr + 8) = make_double2(acc[q][1][0], acc[q][1][1]);
       }
@@ -332,12 +374,14 @@ __device__ __forceinline__ void y16_issue(const M16Params& P, double* st, uint64
   const int nc = hdr ? 1 : d.ncopies;  // copy 0 is the item records
   if (lane < nc) {
     fence_proxy_async();
-    bulk_g2s(st + mine.dst, reinterpret_cast<const void*>(mine.src), (uint32_t)mine.bytes, bar);
+    bulk_g2s_hint(st + (mine.dst & M16_DST_MASK), reinterpret_cast<const void*>(mine.src),
+                  (uint32_t)mine.bytes, bar, l2_policy(mine.dst & M16_KEEP));
   }
   for (int q = lane + 32; q < nc; q += 32) {
     const M16Copy cp = P.copies[d.cbeg + q];
     fence_proxy_async();
-    bulk_g2s(st + cp.dst, reinterpret_cast<const void*>(cp.src), (uint32_t)cp.bytes, bar);
+    bulk_g2s_hint(st + (cp.dst & M16_DST_MASK), reinterpret_cast<const void*>(cp.src),
+                  (uint32_t)cp.bytes, bar, l2_policy(cp.dst & M16_KEEP));
   }
 }
 
