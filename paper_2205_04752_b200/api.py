@@ -861,44 +861,62 @@ class OperatorSet:
     def _sync(self):
         self._torch.cuda.synchronize(self.dev)
 
+    def _lib_stream(self, handle: int):
+        """torch view of a context's stream (cached)."""
+        cache = self.__dict__.setdefault("_streams", {})
+        if handle not in cache:
+            cache[handle] = self._torch.cuda.ExternalStream(handle, device=self.dev)
+        return cache[handle]
+
+    def _on_lib(self, handle: int, fn, *tensors):
+        """Run a library call on the context's stream, ordered after torch's
+        current stream and before its later work by events (no host
+        synchronisation); the tensors are recorded on the library stream for
+        the caching allocator."""
+        torch = self._torch
+        ls = self._lib_stream(handle)
+        cur = torch.cuda.current_stream(self.dev)
+        ls.wait_stream(cur)
+        for t in tensors:
+            t.record_stream(ls)
+        st = fn()
+        cur.wait_stream(ls)
+        return st
+
     def _spmv(self, which: int, x, transpose: bool = False, alpha: float = 1.0):
-        # the SpMV runs on the library's stream: synchronize on both sides
-        # with torch's (the compositions are not latency-critical)
         cols, vals, tptr, slot = self._ell[which]
         x = x.contiguous()
-        self._sync()
         if transpose:
             y = self._torch.empty(self.n, dtype=self._torch.float64, device=self.dev)
-            st = _lib.gpu.hmgpu_ell3_spmv_t(self._ctx, self.n, tptr.data_ptr(), slot.data_ptr(),
-                                            vals.data_ptr(), x.data_ptr(), y.data_ptr(),
-                                            alpha, 0.0)
+            fn = lambda: _lib.gpu.hmgpu_ell3_spmv_t(
+                self._ctx, self.n, tptr.data_ptr(), slot.data_ptr(), vals.data_ptr(),
+                x.data_ptr(), y.data_ptr(), alpha, 0.0)
         else:
             y = self._torch.empty(self.m, dtype=self._torch.float64, device=self.dev)
-            st = _lib.gpu.hmgpu_ell3_spmv(self._ctx, self.m, cols.data_ptr(), vals.data_ptr(),
-                                          x.data_ptr(), y.data_ptr(), alpha, 0.0)
+            fn = lambda: _lib.gpu.hmgpu_ell3_spmv(
+                self._ctx, self.m, cols.data_ptr(), vals.data_ptr(), x.data_ptr(),
+                y.data_ptr(), alpha, 0.0)
+        st = self._on_lib(self.vdelta.stream(), fn, x, y)
         if st != 0:
             raise DeviceError(_lib.gpu.hmgpu_last_error(self._ctx).decode(), st)
-        self._sync()
         return y
 
     def _hmv(self, h: HMatrix, x, nrhs: int = 1):
         """y = H x for nrhs columns stored back to back (column-major)."""
         x = x.contiguous()
         y = self._torch.empty(h.rows * nrhs, dtype=self._torch.float64, device=self.dev)
-        self._sync()
-        h.matvec_ptr(x.data_ptr(), y.data_ptr(), nrhs, getattr(self, "mode", Mode.Current))
-        self._sync()
+        self._on_lib(h.stream(), lambda: h.matvec_ptr(
+            x.data_ptr(), y.data_ptr(), nrhs, getattr(self, "mode", Mode.Current)), x, y)
         return y
 
     def _hmv_t(self, h: HMatrix, x, nrhs: int = 1):
         """y = H^T x (HMatrix::matvec_transposed) for nrhs columns."""
         x = x.contiguous()
         y = self._torch.empty(h.cols * nrhs, dtype=self._torch.float64, device=self.dev)
-        self._sync()
-        _check(_h.hmb_matvec_transposed(h._h, C.c_void_p(x.data_ptr()),
-                                        C.c_void_p(y.data_ptr()), nrhs,
-                                        int(getattr(self, "mode", Mode.Current)), 1))
-        self._sync()
+        st = self._on_lib(h.stream(), lambda: _h.hmb_matvec_transposed(
+            h._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), nrhs,
+            int(getattr(self, "mode", Mode.Current)), 1), x, y)
+        _check(st)
         return y
 
     # T_h = [0, T12, T13; -T12, 0, T23; -T13, -T23, 0] (operators.cpp:56-70)
@@ -908,7 +926,6 @@ class OperatorSet:
     def t_h(self, x):
         """T_h x: 3N -> 3M."""
         n = self.n
-        self._sync()
         out = []
         for i in range(3):
             acc = None
@@ -924,7 +941,6 @@ class OperatorSet:
     def t_h_t(self, z):
         """T_h' z: 3M -> 3N."""
         m = self.m
-        self._sync()
         out = []
         for j in range(3):
             acc = None
@@ -943,7 +959,6 @@ class OperatorSet:
     def s_k(self, k: int, x, transpose: bool = False):
         w, a = self._S[k]
         blk = self.m if transpose else self.n
-        self._sync()
         return self._torch.cat([self._spmv(w, x[c * blk:(c + 1) * blk], transpose, a)
                                 for c in range(3)])
 
