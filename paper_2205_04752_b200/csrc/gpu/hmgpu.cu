@@ -1224,11 +1224,6 @@ void build_matvec_t(hmgpu_ctx* c) {
 }
 
 // refresh kmax after rank changes (promote / extend)
-void refresh_matvec_ranks(hmgpu_ctx* c) {
-  c->kmax = 1;
-  for (const Item& it : c->items) c->kmax = std::max(c->kmax, it.k);
-}
-
 
 // ---- streamed matvec plan (warp-private jobs, hmgpu_stream.cuh) -------------
 // Default geometry of the warp pipelines (tuned on B200 with
