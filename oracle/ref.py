@@ -193,3 +193,54 @@ class RefProblem:
         _ck(lib().hmr_amvm(self._h, _p(x), theta, eps_amvm, lookahead_steps, max_iterations,
                            _p(b), _p(iters), C.byref(ni), C.byref(conv)))
         return b, iters[: ni.value].copy(), bool(conv.value)
+
+
+class RefOperatorSet:
+    """assemble_operators (operators.cpp:187-245) by the reference's code on
+    a labelled mesh (load_mesh with a centroid predicate), and the
+    right-hand-side operator of assemble_rhs (baca.cpp:42-76): its product
+    at the current ranks and its adaptive matvec (amvm_multiply over the
+    flattened expression)."""
+
+    def __init__(self, verts, tris, predicate: str, E=1.0, nu=0.3, b_min=8, eta=1.0,
+                 eps=1e-6, beta_stop=0.8, lookahead=2):
+        L = lib()
+        L.hmr_ops_create.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_char_p,
+                                     C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
+                                     C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.hmr_ops_destroy.argtypes = [C.c_void_p]
+        L.hmr_ops_rhs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.hmr_ops_rhs_amvm.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                       C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]
+        v = np.ascontiguousarray(verts, dtype=np.float64)
+        t = np.ascontiguousarray(tris, dtype=np.int32)
+        h = C.c_void_p()
+        rows, cols = C.c_longlong(), C.c_longlong()
+        _ck(L.hmr_ops_create(len(v), _p(v), len(t), _p(t), predicate.encode(), E, nu, b_min,
+                             eta, eps, beta_stop, lookahead, C.byref(h), C.byref(rows),
+                             C.byref(cols)))
+        self._h = h
+        self.rows, self.cols = rows.value, cols.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hmr_ops_destroy(self._h)
+            self._h = None
+
+    def rhs(self, g_neumann, g_dirichlet) -> np.ndarray:
+        x = np.ascontiguousarray(np.concatenate([g_neumann, g_dirichlet]), dtype=np.float64)
+        f = np.zeros(self.rows)
+        _ck(lib().hmr_ops_rhs(self._h, _p(x), _p(f)))
+        return f
+
+    def rhs_amvm(self, g_neumann, g_dirichlet, theta=0.7, eps_amvm=1e-6, lookahead_steps=2,
+                 max_iterations=100):
+        x = np.ascontiguousarray(np.concatenate([g_neumann, g_dirichlet]), dtype=np.float64)
+        f = np.zeros(self.rows)
+        iters = np.zeros((max_iterations + 1, 8))
+        ni, conv = C.c_int(), C.c_int()
+        _ck(lib().hmr_ops_rhs_amvm(self._h, _p(x), theta, eps_amvm, lookahead_steps,
+                                   max_iterations, _p(f), _p(iters), C.byref(ni),
+                                   C.byref(conv)))
+        return f, iters[: ni.value].copy(), bool(conv.value)

@@ -1,7 +1,7 @@
 // oracle/_ref driver -- TEST INFRASTRUCTURE ONLY.
 //
 // A C ABI over the reference's OWN hot-path code (/root/reference/proj/src/
-// {quadrature,mesh,cluster,kernels,aca,hmatrix,expr,amvm}.cpp compiled
+// {quadrature,mesh,cluster,kernels,aca,hmatrix,expr,amvm,operators}.cpp compiled
 // unmodified against oracle/ref_shim/, see oracle/Makefile).  It builds the
 // north-star matrix the way the reference would: load_mesh (mesh.cpp:180-
 // 219) for the geometry caches, one cluster tree over the triangle support
@@ -33,6 +33,7 @@
 #include "hmbem/hmatrix.hpp"
 #include "hmbem/kernels.hpp"
 #include "hmbem/mesh.hpp"
+#include "hmbem/operators.hpp"
 #include "hmbem/parallel.hpp"
 
 using namespace hmbem;
@@ -140,6 +141,62 @@ struct hmr_problem {
   ExprPtr op;  // BlockGrid (Kelvin) or the single leaf (Newton)
   GammaContributions gamma;
 };
+
+// The Galerkin operator set of the mixed problem (assemble_operators,
+// operators.cpp:187-245) and the right-hand-side operator of assemble_rhs.
+struct hmr_ops {
+  std::shared_ptr<SurfaceMesh> mesh;
+  OperatorSet ops;
+  ExprPtr rhs;
+};
+
+namespace {
+// rhs_operator (baca.cpp:42-55), restated: baca.cpp (preconditioner, BPCG,
+// BACA) is not part of _ref, its composition of the right-hand side is
+// these lines
+ExprPtr rhs_operator_ref(const OperatorSet& ops) {
+  const DofLayout& layout = ops.layout;
+  const ExprPtr mass = leaf(ops.sparse.mass_d3);
+  const ExprPtr top = sum({scale(0.5, mass), ops.kh});
+  const ExprPtr bottom = sum({scale(0.5, transpose(mass)), scale(-1.0, transpose(ops.kh))});
+  const ExprPtr full = block2x2(scale(-1.0, ops.vh), top, bottom, scale(-1.0, ops.dh));
+  const Index m3 = 3 * static_cast<Index>(layout.num_triangles);
+  std::vector<Index> rows = dirichlet_triangle_dofs(layout);
+  for (Index u : neumann_node_dofs(layout)) rows.push_back(m3 + u);
+  return compose({leaf(selection_matrix(rows, full->rows())), full});
+}
+
+std::shared_ptr<SurfaceMesh> load_off_mesh(int nv, const double* xyz, int nt, const int* tri,
+                                           const std::string& predicate) {
+  char path[] = "/tmp/hmr_meshXXXXXX";
+  const int fd = mkstemp(path);
+  if (fd < 0) throw Error("mkstemp failed");
+  close(fd);
+  {
+    std::ofstream f(path);
+    f << "OFF\n" << nv << " " << nt << " 0\n";
+    char buf[96];
+    for (int v = 0; v < nv; ++v) {
+      std::snprintf(buf, sizeof buf, "%.17g %.17g %.17g\n", xyz[3 * v], xyz[3 * v + 1],
+                    xyz[3 * v + 2]);
+      f << buf;
+    }
+    for (int t = 0; t < nt; ++t)
+      f << "3 " << tri[3 * t] << " " << tri[3 * t + 1] << " " << tri[3 * t + 2] << "\n";
+  }
+  BoundaryLabeling lab;
+  lab.dirichlet_predicate = predicate;
+  std::shared_ptr<SurfaceMesh> mesh;
+  try {
+    mesh = std::make_shared<SurfaceMesh>(load_mesh(path, lab));
+  } catch (...) {
+    std::remove(path);
+    throw;
+  }
+  std::remove(path);
+  return mesh;
+}
+}  // namespace
 
 #define HMR_API __attribute__((visibility("default")))
 
@@ -408,6 +465,74 @@ HMR_API int hmr_mark(hmr_problem* p, double theta, int* marked, int* n_marked, d
         term_comp_block[2 * t] = comp;
         term_comp_block[2 * t + 1] = p->gamma.terms[t].block;
       }
+  });
+}
+
+// assemble_operators on the labelled mesh (full-mode ACA at eps, beta_stop
+// for the stopping rule, eta for admissibility); sizes of the RHS operator
+HMR_API int hmr_ops_create(int nv, const double* xyz, int nt, const int* tri,
+                           const char* predicate, double E, double nu, int b_min, double eta,
+                           double eps, double beta_stop, int lookahead, hmr_ops** out,
+                           long long* rows, long long* cols) {
+  return guard([&] {
+    if (!out || !xyz || !tri || !predicate) throw Error("null argument");
+    auto p = std::make_unique<hmr_ops>();
+    p->mesh = load_off_mesh(nv, xyz, nt, tri, predicate);
+    OperatorConfig cfg;
+    cfg.clustering.b_min = b_min;
+    cfg.clustering.beta = eta;
+    cfg.eps_aca = eps;
+    cfg.beta_stop = beta_stop;
+    cfg.lookahead = lookahead;
+    p->ops = assemble_operators(p->mesh, make_material(E, nu), cfg);
+    p->rhs = rhs_operator_ref(p->ops);
+    if (rows) *rows = p->rhs->rows();
+    if (cols) *cols = p->rhs->cols();
+    *out = p.release();
+  });
+}
+
+HMR_API void hmr_ops_destroy(hmr_ops* p) { delete p; }
+
+// f = rhs_operator x at the current ranks (assemble_rhs without AMVM)
+HMR_API int hmr_ops_rhs(const hmr_ops* p, const double* x, double* f) {
+  return guard([&] {
+    Vec xv(p->rhs->cols());
+    std::copy(x, x + xv.size(), xv.data());
+    const Vec y = matvec(*p->rhs, xv, Mode::Current);
+    std::copy(y.data(), y.data() + y.size(), f);
+  });
+}
+
+// assemble_rhs with opt.amvm (baca.cpp:57-76): amvm_multiply over the RHS
+// operator; iters8 as hmr_amvm
+HMR_API int hmr_ops_rhs_amvm(hmr_ops* p, const double* x, double theta, double eps_amvm,
+                             int lookahead_steps, int max_iterations, double* f,
+                             double* iters8, int* n_iters, int* converged) {
+  return guard([&] {
+    Vec xv(p->rhs->cols());
+    std::copy(x, x + xv.size(), xv.data());
+    AmvmConfig cfg;
+    cfg.theta = theta;
+    cfg.eps_amvm = eps_amvm;
+    cfg.lookahead_steps = lookahead_steps;
+    cfg.max_iterations = max_iterations;
+    auto [res, rep] = amvm_multiply(p->rhs, xv, cfg);
+    std::copy(res.data(), res.data() + res.size(), f);
+    *n_iters = static_cast<int>(rep.iterations.size());
+    *converged = rep.converged ? 1 : 0;
+    for (std::size_t i = 0; i < rep.iterations.size(); ++i) {
+      const auto& it = rep.iterations[i];
+      double* r = iters8 + 8 * i;
+      r[0] = it.k;
+      r[1] = it.gamma;
+      r[2] = it.gamma_pk;
+      r[3] = it.marked;
+      r[4] = static_cast<double>(it.cumulative_pivots);
+      r[5] = it.storage_mb;
+      r[6] = it.e_hat;
+      r[7] = 0.0;
+    }
   });
 }
 

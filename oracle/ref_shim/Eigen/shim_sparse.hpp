@@ -168,6 +168,12 @@ class SparseMatrix {
     }
     return r;
   }
+  // -A (SpMat(-t23) in build_sparse_ops, operators.cpp:77)
+  friend SparseMatrix operator-(const SparseMatrix& a) {
+    SparseMatrix r = a;
+    for (double& v : r.val_) v = -v;
+    return r;
+  }
   friend SparseMatrix operator*(double s, const SparseMatrix& a) {
     SparseMatrix r = a;
     for (double& v : r.val_) v = s * v;

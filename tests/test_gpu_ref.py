@@ -91,3 +91,35 @@ def test_amvm_vs_reference_code():
         assert it.cumulative_pivots == int(rr[4])
         assert it.gamma == pytest.approx(rr[1], rel=1e-10)
     assert rel(bg, br) < 1e-12
+
+
+def test_rhs_amvm_vs_reference_code():
+    """assemble_rhs with the adaptive matvec (baca.cpp:57-76) over the
+    composite right-hand-side operator, against the reference's own
+    assemble_operators + amvm_multiply (oracle/_ref): the product before any
+    sweep, every sweep's marked count and cumulative pivots, gamma, and the
+    final right-hand side."""
+    pytest.importorskip("torch")
+    from oracle import oracle as orc
+    from tests.test_gpu_amvm_expr import _mesh
+    mesh = _mesh()
+    a = mesh.arrays()
+    R = ref.RefOperatorSet(a["vertices"], a["triangles"], "x1>=1|x2<=-1|x3>=1", b_min=8,
+                           eta=1.0, eps=1e-2, beta_stop=0.8, lookahead=2)
+    ops = hm.OperatorSet(mesh, 1.0, 0.3, b_min=8, eta=1.0, device=0)
+    ops.assemble(eps=1e-2, beta=0.8, lookahead=2)
+    sys = hm.SaddleSystem(ops, hm.DofLayout(mesh))
+    gn = orc.random_vector(3 * mesh.num_triangles, 11)
+    gd = orc.random_vector(3 * mesh.num_vertices, 12)
+    f0 = sys.rhs(gn, gd)
+    fr0 = R.rhs(gn, gd)
+    assert np.linalg.norm(f0 - fr0) <= 1e-12 * np.linalg.norm(fr0)
+    f, rep = hm.assemble_rhs(sys, gn, gd, amvm=True,
+                             amvm_cfg=hm.AmvmConfig(theta=0.7, eps_amvm=1e-7,
+                                                    max_iterations=40))
+    fr, it, conv = R.rhs_amvm(gn, gd, theta=0.7, eps_amvm=1e-7, max_iterations=40)
+    assert rep.converged == conv and len(rep.iterations) == len(it)
+    for ours, theirs in zip(rep.iterations, it):
+        assert ours.marked == int(theirs[3]) and ours.cumulative_pivots == int(theirs[4])
+        assert ours.gamma == pytest.approx(theirs[1], rel=1e-9)
+    assert np.linalg.norm(f - fr) <= 1e-12 * np.linalg.norm(fr)

@@ -243,3 +243,21 @@ def test_symmetric_mesh_ties_stay_within_the_bars():
     assert np.linalg.norm(br - bt) <= 1.5 * itr[-1, 1]
     assert np.linalg.norm(bo - bt) <= 1.5 * ito[-1, 1]
     assert rel(bo, br) <= 1e-4
+
+
+def test_reference_rhs_operator_matches_dense():
+    """The reference's own operator set (assemble_operators, operators.cpp,
+    in oracle/_ref) and its rhs_operator (baca.cpp:42-55): the product at
+    eps 1e-8 equals the dense composition of the oracle's Galerkin matrices
+    within the ACA tolerance (pins the driver's composition and the shim's
+    sparse algebra before the GPU comparison in test_gpu_ref.py)."""
+    from tests.test_gpu_amvm_expr import _dense_rhs, _mesh
+    mesh = _mesh()
+    a = mesh.arrays()
+    R = ref.RefOperatorSet(a["vertices"], a["triangles"], "x1>=1|x2<=-1|x3>=1", b_min=8,
+                           eta=1.0, eps=1e-8)
+    gn = orc.random_vector(3 * mesh.num_triangles, 11)
+    gd = orc.random_vector(3 * mesh.num_vertices, 12)
+    f = R.rhs(gn, gd)
+    fd = _dense_rhs(mesh, gn, gd)
+    assert np.linalg.norm(f - fd) <= 1e-6 * np.linalg.norm(fd)
