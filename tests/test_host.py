@@ -263,3 +263,24 @@ def test_random_vector_streams_match_oracle():
         assert (hm.random_vector(5000, seed, "uniform") == orc.random_vector(5000, seed)).all()
     for seed in (2, 4):
         assert (hm.random_vector(5000, seed, "normal") == orc.normal_vector(5000, seed)).all()
+
+
+def test_random_vector_stream_matches_oracle_and_golden():
+    """hm.random_vector (hmb_random_vector) is the reference test suite's
+    random_vector (proj/tests/oracles.cpp:414-420: std::mt19937_64 seeded
+    with `seed`, uniform_real_distribution(-1, 1)) -- equal to the oracle's
+    restatement bit for bit, and to committed values of the stream (seed 0);
+    the normal variant (std::normal_distribution) likewise."""
+    import paper_2205_04752_b200 as hm
+    from oracle import oracle as orc
+    for seed in (0, 1, 2, 3, 4, 12345):
+        for n in (1, 7, 1000):
+            assert (hm.random_vector(n, seed) == orc.random_vector(n, seed)).all()
+            assert (hm.random_vector(n, seed, "normal") == orc.normal_vector(n, seed)).all()
+    golden = [-0.6804132732590783, 0.9842904192596575, -0.9208619483102687,
+              0.19498932538934355]
+    assert hm.random_vector(4, 0).tolist() == golden
+    assert hm.random_vector(3, 4, "normal").tolist() == [
+        -0.2361666787221914, 1.460615509829741, -0.6497372926308559]
+    # the stream is a prefix stream: longer vectors extend shorter ones
+    assert (hm.random_vector(100, 7)[:10] == hm.random_vector(10, 7)).all()
