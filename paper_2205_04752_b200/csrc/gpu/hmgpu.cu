@@ -1896,8 +1896,11 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         if (skip == 1) continue;
         const long long cp = align2(6LL * mb.m);
         const int PD = cf_pitch(6 * mb.m);
-        const int jd = (SDY / (PD + XP)) & ~3;
-        if (jd < 4) fail(HMGPU_ERR_INVALID, "near-field block too tall for the multi-RHS stage");
+        // as many columns as fit with their x rows (ceil4 of them); any
+        // count: the last k-step is predicated
+        int jd = SDY / (PD + XP) + 1;
+        while (jd > 0 && (long long)jd * PD + (long long)((jd + 3) & ~3) * XP > SDY) --jd;
+        if (jd < 1) fail(HMGPU_ERR_INVALID, "near-field block too tall for the multi-RHS stage");
         for (int j0 = 0; j0 < mb.n; j0 += jd) {
           const int jj = std::min(jd, mb.n - j0);
           YStage16 d{};
