@@ -483,6 +483,7 @@ struct hmgpu_ctx {
   bool p16_valid = false;
   int p16_mode = -1;
   int p16_ns = 2, p16_stage = 0, p16_ncta = 0;
+  int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8;
   long long p16_zsize = 0, p16_alen = 0;
   int n_zch16 = 0, n_yst16 = 0;
   DBuf<ZChunk16> d_zch16;
@@ -1717,15 +1718,26 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
 // HMGPU_M16_CFG="ns,stage": ring depth (3, 4, 6 or 9) and doubles per stage
 struct M16Cfg {  // measured on config 3: 3 x 3072 (3 CTAs / SM) best
   int ns = 3, stage = 3072;
+  // phase 1 (HMGPU_M16_ZCFG="ns,stage,warps"): its own ring and consumer
+  // warps (8 or 12)
+  int zns = 3, zstage = 3072, znw = 8;
 };
 M16Cfg m16_cfg() {
   static const M16Cfg cfg = [] {
     M16Cfg r;
-    int a, b;
+    int a, b, w;
     const char* e = std::getenv("HMGPU_M16_CFG");
     if (e && std::sscanf(e, "%d,%d", &a, &b) == 2) {
       r.ns = a;
       r.stage = b;
+      r.zns = a;
+      r.zstage = b;
+    }
+    const char* z = std::getenv("HMGPU_M16_ZCFG");
+    if (z && std::sscanf(z, "%d,%d,%d", &a, &b, &w) == 3) {
+      r.zns = a;
+      r.zstage = b;
+      r.znw = w;
     }
     return r;
   }();
@@ -1759,7 +1771,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   const M16Cfg cfg = m16_cfg();
   if ((cfg.ns != 3 && cfg.ns != 4 && cfg.ns != 6 && cfg.ns != 9) || cfg.stage < 2048 || (cfg.stage & 3))
     fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_CFG");
-  const int SD = cfg.stage - M16_HDR;  // data doubles per stage
+  if ((cfg.zns != 3 && cfg.zns != 4) || (cfg.znw != 8 && cfg.znw != 12) || cfg.zstage < 2048 ||
+      (cfg.zstage & 3))
+    fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_ZCFG");
+  const int SD = cfg.zstage - M16_HDR;  // phase-1 data doubles per stage
   const int nb = c->n_mv;
   std::vector<std::array<int, 6>> rk(std::max(nb, 1)), zo(std::max(nb, 1));
   std::vector<long long> zb(std::max(nb, 1), -1);
@@ -1992,14 +2007,19 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   const int per_sm = std::max(1, std::min(3, (int)((227 * 1024) / (ring_bytes + 1024))));
   if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
   const int ncta = c->sm_count * per_sm;
-  std::vector<int> zcoff(ncta + 1), ycoff(ncta + 1);
+  const size_t zring_bytes = (size_t)cfg.zns * cfg.zstage * sizeof(double);
+  if (zring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_ZCFG ring too large");
+  const int zcta_sm = std::max(1, std::min(cfg.znw == 8 ? 3 : 2,
+                                           (int)((227 * 1024) / (zring_bytes + 1024))));
+  const int nctaz = c->sm_count * zcta_sm;
+  std::vector<int> zcoff(nctaz + 1), ycoff(ncta + 1);
   std::vector<M16Stage> ystages;
   std::vector<YItem16> yitems;
   std::vector<M16Copy> ycopies;
   std::vector<unsigned char> ckind;  // copy source: 0 items, 1 p16 arena, 2 Z, 3 dense, 4 x
   {
-    const std::vector<int> ft = split_runs(tbytes, ncta);
-    for (int k = 0; k <= ncta; ++k) zcoff[k] = tptr[ft[k]];
+    const std::vector<int> ft = split_runs(tbytes, nctaz);
+    for (int k = 0; k <= nctaz; ++k) zcoff[k] = tptr[ft[k]];
     const std::vector<int> fl = split_runs(lbytes, ncta);
     const int SD2 = cfg.stage - Y16_HDR;
     auto plen = [](const YStage16& d) -> long long {
@@ -2127,6 +2147,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_ns = cfg.ns;
   c->p16_stage = cfg.stage;
   c->p16_ncta = ncta;
+  c->p16_nctaz = nctaz;
+  c->p16_zns = cfg.zns;
+  c->p16_zstage = cfg.zstage;
+  c->p16_znw = cfg.znw;
   c->p16_zsize = zsize;
   c->p16_alen = alen;
   c->p16_mode = mode;
@@ -2140,17 +2164,20 @@ void build_plan16(hmgpu_ctx* c, int mode) {
 }
 
 template <int NS>
-void launch_m16(hmgpu_ctx* c, M16Params P, bool zpass) {
+void launch_m16(hmgpu_ctx* c, M16Params P) {  // phase 2
   const size_t smem = (size_t)NS * c->p16_stage * sizeof(double);
-  if (zpass) {
-    CK(cudaFuncSetAttribute(hmv16_z_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    hmv16_z_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
-  } else {
-    CK(cudaFuncSetAttribute(hmv16_y_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    hmv16_y_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
-  }
+  CK(cudaFuncSetAttribute(hmv16_y_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  hmv16_y_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
+  CK(cudaGetLastError());
+}
+template <int NS, int NW>
+void launch_m16z(hmgpu_ctx* c, M16Params P) {  // phase 1
+  const size_t smem = (size_t)NS * c->p16_zstage * sizeof(double);
+  CK(cudaFuncSetAttribute(hmv16_z_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  P.stage = c->p16_zstage;
+  hmv16_z_kernel<NS, NW><<<c->p16_nctaz, 32 * (NW + 1), smem, c->stream>>>(P);
   CK(cudaGetLastError());
 }
 
@@ -2191,22 +2218,22 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
       c->timed("hmv16_z", [&] {
         P.desc = c->d_zch16.p;
         P.coff = c->d_zcoff16.p;
-        switch (c->p16_ns) {
-          case 4: launch_m16<4>(c, P, true); break;
-          case 6: launch_m16<6>(c, P, true); break;
-          case 9: launch_m16<9>(c, P, true); break;
-          default: launch_m16<3>(c, P, true);
-        }
+        const int key = c->p16_zns * 100 + c->p16_znw;
+        if (key == 412) launch_m16z<4, 12>(c, P);
+        else if (key == 408) launch_m16z<4, 8>(c, P);
+        else if (key == 312) launch_m16z<3, 12>(c, P);
+        else launch_m16z<3, 8>(c, P);
       });
     c->timed("hmv16_leaf", [&] {
       P.desc = c->d_yst16.p;
       P.copies = c->d_ycopy16.p;
       P.coff = c->d_ycoff16.p;
+      P.stage = c->p16_stage;
       switch (c->p16_ns) {
-        case 4: launch_m16<4>(c, P, false); break;
-        case 6: launch_m16<6>(c, P, false); break;
-        case 9: launch_m16<9>(c, P, false); break;
-        default: launch_m16<3>(c, P, false);
+        case 4: launch_m16<4>(c, P); break;
+        case 6: launch_m16<6>(c, P); break;
+        case 9: launch_m16<9>(c, P); break;
+        default: launch_m16<3>(c, P);
       }
     });
   }

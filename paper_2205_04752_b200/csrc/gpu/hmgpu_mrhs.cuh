@@ -189,7 +189,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // full[s]: the stage's bytes have landed (one arrival + tx bytes);
 // empty[s]: every consumer warp is done with the slot (M16_NW arrivals)
-template <int NS>
+template <int NS, int NW = M16_NW>
 __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* empty,
                                           int stage) {
   // zero the ring once: every later read of a slot outside the current
@@ -199,7 +199,7 @@ __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], M16_NW);
+      mbar_init(&empty[s], NW);
     }
     mbar_fence_init();
   }
@@ -212,7 +212,7 @@ __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* 
 // wait for each stage's bytes, compute, and release the slot.  issue(slot,
 // bar, j) loads the records of stage j + 1 after issuing stage j, so their
 // latency overlaps the wait for the next free slot.
-template <int NS, class ISSUE, class COMPUTE>
+template <int NS, int NW = M16_NW, class ISSUE, class COMPUTE>
 __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t* empty,
                                            int stage, int n, ISSUE issue,
                                            COMPUTE compute, int dbg = 0,
@@ -220,7 +220,7 @@ __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t*
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tm = dbg == 3 && prof != nullptr;
   long long t_wait = 0, t_work = 0;
-  if (warp == M16_NW) {
+  if (warp == NW) {
     for (int j = 0; j < n; ++j) {
       const int s = j % NS;
       const long long t0 = tm ? clock64() : 0;
@@ -274,13 +274,14 @@ __device__ __forceinline__ void z16_issue(const M16Params& P, double* st, uint64
                   l2_policy(true));
 }
 
-template <int NS>
-__global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
+// NW consumer warps (+ one producer warp)
+template <int NS, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 2) hmv16_z_kernel(M16Params P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  ring_init<NS>(sm, full, empty, P.stage);
+  ring_init<NS, NW>(sm, full, empty, P.stage);
   const ZChunk16* chunks = static_cast<const ZChunk16*>(P.desc);
   const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
   // m-tiles warp, warp + 8, warp + 16 of the task; their rows are resolved
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
   int xcol[3] = {0, 0, 0};     // its operand group r: x columns 16 r ..
   int zdst[3] = {-1, -1, -1};  // its Z row * ZP + part * 16 (-1: padding row)
   ZChunk16 nxt{};
-  if (warp == M16_NW && n > 0) nxt = chunks[c0];
+  if (warp == NW && n > 0) nxt = chunks[c0];
   auto issue = [&](double* st, uint64_t* bar, int j) {
     const ZChunk16 cur = nxt;
     if (j + 1 < n) nxt = chunks[c0 + j + 1];
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         acc[q][0][0] = acc[q][0][1] = acc[q][1][0] = acc[q][1][1] = 0.0;
-        const int p = warp + M16_NW * q;
+        const int p = warp + NW * q;
         if (p >= tk.ntiles) continue;
         ntl = q + 1;
         // operand group r (rows multiply x_r), this lane's row rho of it ->
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_z_kernel(M16Params P) {
       }
     }
   };
-  stage_loop<NS>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof);
+  stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof);
 }
 
 // ---------------------------------------------------------------------------
