@@ -2756,7 +2756,13 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     const size_t free_b = avail_bytes() + c->d_arena.mapped + c->spare_arena.mapped;
     const double avail =
         (double)free_b - 8.0 * (double)dense_total - 4.0 * (1 << 30);
-    int cap_init = (initial_rank >= 0 ? initial_rank : 24) + lookahead;
+    // full mode: 24 columns before the look-ahead unless HMGPU_ACA_CAP0 says
+    // otherwise (items that need more are relocated and resumed)
+    static const int cap0 = [] {
+      const char* e = std::getenv("HMGPU_ACA_CAP0");
+      return e ? std::max(1, std::atoi(e)) : 24;
+    }();
+    int cap_init = (initial_rank >= 0 ? initial_rank : cap0) + lookahead;
     if (initial_rank < 0 && sum_mn > 0) {
       const long long fit = (long long)(0.55 * avail / (8.0 * (double)sum_mn));
       cap_init = (int)std::max<long long>(lookahead + 6, std::min<long long>(cap_init, fit));
