@@ -406,3 +406,46 @@ def test_stream_layouts_agree(c1, layout):
     assert (a == b).all()
     assert rel(a, y) < 1e-13
     assert rel(a, c1["o"].matvec(c1["x"])) < 10 * c1["eps"]
+
+
+def test_multi_rhs_plans_share_the_spare_arena_and_follow_rank_changes():
+    """The 16-RHS plan packs its factors into the same idle arena as the
+    1-RHS stream plan: alternating the two keeps every product right, and a
+    refinement (promote + extend) invalidates both plans."""
+    mesh = hm.Mesh.icosphere(3)
+    g = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+    g.assemble(eps=1e-3, beta=0.8, lookahead=2)
+    n = g.cols
+    X = np.asfortranarray(np.stack([RV(n, 200 + s) for s in range(16)], axis=1))
+
+    def cols():
+        return np.stack([g.matvec(np.ascontiguousarray(X[:, q])) for q in range(16)], axis=1)
+
+    Y1 = g.matvec(X)
+    C1 = cols()
+    Y2 = g.matvec(X)
+    assert (Y1 == Y2).all() and rel(Y1, C1) < 1e-13
+    kc, kl, _, _ = g.ranks()
+    pairs = [(q, b) for q in range(6) for b in range(kc.shape[1])
+             if kc[q, b] >= 0 and kl[q, b] > kc[q, b]][::3]
+    assert pairs
+    g.promote(pairs)
+    g.extend_lookahead(pairs, 2)
+    Y3 = g.matvec(X)
+    C3 = cols()
+    assert rel(Y3, C3) < 1e-13 and rel(Y3, Y1) > 1e-12  # the new ranks are used
+
+
+def test_multi_rhs_large_leaves_fall_back_to_the_block_sweep():
+    """Leaves above 64 rows are outside the TMA-fed sweep's tiling: the
+    product runs on the block-sweep kernel and stays the same product."""
+    mesh = hm.Mesh.icosphere(3)
+    g = hm.HMatrix.kelvin(mesh, b_min=96, eta=1.0, device=0)
+    g.assemble(eps=1e-4, beta=0.8, lookahead=2)
+    t = g.tree()
+    leaves = t.nodes[t.nodes[:, 2] < 0]
+    assert (leaves[:, 1] - leaves[:, 0]).max() > 64
+    X = np.asfortranarray(np.stack([RV(g.cols, 300 + s) for s in range(16)], axis=1))
+    Y = g.matvec(X)
+    for q in (0, 7, 15):
+        assert rel(Y[:, q], g.matvec(np.ascontiguousarray(X[:, q]))) < 1e-13
