@@ -483,7 +483,7 @@ struct hmgpu_ctx {
   bool p16_valid = false;
   int p16_mode = -1;
   int p16_ns = 2, p16_stage = 0, p16_ncta = 0;
-  int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8;
+  int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8, p16_ynw = 8;
   long long p16_zsize = 0, p16_alen = 0;
   int n_zch16 = 0, n_yst16 = 0;
   DBuf<ZChunk16> d_zch16;
@@ -1721,6 +1721,7 @@ struct M16Cfg {  // measured on config 3: 3 x 3072 (3 CTAs / SM) b
   // phase 1 (HMGPU_M16_ZCFG="ns,stage,warps"): its own ring and consumer
   // warps (8 or 12)
   int zns = 3, zstage = 3072, znw = 8;
+  int ynw = 8;  // phase-2 consumer warps (HMGPU_M16_YNW: 8 or 16, 16 = one CTA per SM)
 };
 M16Cfg m16_cfg() {
   static const M16Cfg cfg = [] {
@@ -1733,6 +1734,8 @@ M16Cfg m16_cfg() {
       r.zns = a;
       r.zstage = b;
     }
+    const char* yw = std::getenv("HMGPU_M16_YNW");
+    if (yw) r.ynw = std::atoi(yw) == 16 ? 16 : 8;
     const char* z = std::getenv("HMGPU_M16_ZCFG");
     if (z && std::sscanf(z, "%d,%d,%d", &a, &b, &w) == 3) {
       r.zns = a;
@@ -2004,7 +2007,8 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   // CTA); within a CTA's leaves, consecutive pieces are packed into stages
   // of up to Y16_MAXIT items, their records and bulk copies
   const size_t ring_bytes = (size_t)cfg.ns * cfg.stage * sizeof(double);
-  const int per_sm = std::max(1, std::min(3, (int)((227 * 1024) / (ring_bytes + 1024))));
+  const int per_sm = cfg.ynw == 16 ? 1
+                     : std::max(1, std::min(3, (int)((227 * 1024) / (ring_bytes + 1024))));
   if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
   const int ncta = c->sm_count * per_sm;
   const size_t zring_bytes = (size_t)cfg.zns * cfg.zstage * sizeof(double);
@@ -2151,6 +2155,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_zns = cfg.zns;
   c->p16_zstage = cfg.zstage;
   c->p16_znw = cfg.znw;
+  c->p16_ynw = cfg.ynw;
   c->p16_zsize = zsize;
   c->p16_alen = alen;
   c->p16_mode = mode;
@@ -2163,12 +2168,12 @@ void build_plan16(hmgpu_ctx* c, int mode) {
                  ncta, ring_bytes);
 }
 
-template <int NS>
+template <int NS, int NW = 8>
 void launch_m16(hmgpu_ctx* c, M16Params P) {  // phase 2
   const size_t smem = (size_t)NS * c->p16_stage * sizeof(double);
-  CK(cudaFuncSetAttribute(hmv16_y_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(hmv16_y_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
-  hmv16_y_kernel<NS><<<c->p16_ncta, M16_NT, smem, c->stream>>>(P);
+  hmv16_y_kernel<NS, NW><<<c->p16_ncta, 32 * (NW + 1), smem, c->stream>>>(P);
   CK(cudaGetLastError());
 }
 template <int NS, int NW>
@@ -2229,11 +2234,17 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
       P.copies = c->d_ycopy16.p;
       P.coff = c->d_ycoff16.p;
       P.stage = c->p16_stage;
-      switch (c->p16_ns) {
-        case 4: launch_m16<4>(c, P); break;
-        case 6: launch_m16<6>(c, P); break;
-        case 9: launch_m16<9>(c, P); break;
-        default: launch_m16<3>(c, P);
+      if (c->p16_ynw == 16) {
+        if (c->p16_ns == 6) launch_m16<6, 16>(c, P);
+        else if (c->p16_ns == 9) launch_m16<9, 16>(c, P);
+        else launch_m16<4, 16>(c, P);
+      } else {
+        switch (c->p16_ns) {
+          case 4: launch_m16<4>(c, P); break;
+          case 6: launch_m16<6>(c, P); break;
+          case 9: launch_m16<9>(c, P); break;
+          default: launch_m16<3>(c, P);
+        }
       }
     });
   }

@@ -466,16 +466,17 @@ __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int
   }
 }
 
-// Leaves of at most 64 rows (8 row tiles): warp w takes row tile w with both
-// RHS halves, or, for leaves of at most 32 rows, row tile w % 4 with RHS
-// half w / 4.
-template <int NS>
-__global__ void __launch_bounds__(M16_NT, 3) hmv16_y_kernel(M16Params P) {
+// Leaves of at most 64 rows (8 row tiles).  NW = 8 consumer warps: warp w
+// takes row tile w with both RHS halves, or, for leaves of at most 32 rows,
+// row tile w % 4 with RHS half w / 4.  NW = 16: row tile w % 8, RHS half
+// w / 8 (or, for leaves of at most 32 rows, the 8 spare warps idle).
+template <int NS, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 1) hmv16_y_kernel(M16Params P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  ring_init<NS>(sm, full, empty, P.stage);
+  ring_init<NS, NW>(sm, full, empty, P.stage);
   const M16Stage* stages = static_cast<const M16Stage*>(P.desc);
   const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
   double acc[3][2][2];  // [output component][RHS half][pair]
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_y_kernel(M16Params P) {
   // record, so no load sits on the issue path
   M16Stage rec0{}, rec1{};
   M16Copy cp0{};
-  if (warp == M16_NW) {
+  if (warp == NW) {
     if (n > 0) rec0 = stages[c0];
     if (n > 1) rec1 = stages[c0 + 1];
     if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
@@ -504,9 +505,9 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_y_kernel(M16Params P) {
     for (int it = 0; it < nit; ++it) {
     const YItem16& d = items[it];
     const int RT = (d.R + 7) >> 3;
-    const bool split = RT <= 4;
-    const int rt = split ? (warp & 3) : warp;
-    const int h0 = split ? (warp >> 2) : 0;
+    const bool split = NW == 16 || RT <= 4;
+    const int rt = NW == 16 ? (warp & 7) : (split ? (warp & 3) : warp);
+    const int h0 = NW == 16 ? (warp >> 3) : (split ? (warp >> 2) : 0);
     if (d.flags & 1) {
 #pragma unroll
       for (int r = 0; r < 3; ++r)
@@ -539,7 +540,8 @@ __global__ void __launch_bounds__(M16_NT, 3) hmv16_y_kernel(M16Params P) {
     }
     }
   };
-  stage_loop<NS>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof ? P.prof + 4 : nullptr);
+  stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg,
+                     P.prof ? P.prof + 4 : nullptr);
 }
 
 // fp64 tensor-core peak probe: eight independent DMMA chains per warp
