@@ -1320,7 +1320,10 @@ __device__ __forceinline__ void aca_item(const SRC& src, Item& s, Item* __restri
 // by m + n, largest first) is run CTA by CTA through counter[0]; then every
 // warp pulls single items from list[nbig, nlist) through counter[1].  One
 // item machine instance per mode.
-template <int KIND, int MINB = 512 / ACA_NT>
+#ifndef HMGPU_ACA_MINB
+#define HMGPU_ACA_MINB (512 / ACA_NT)
+#endif
+template <int KIND, int MINB = HMGPU_ACA_MINB>
 __global__ void __launch_bounds__(ACA_NT, MINB)
 aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list, int nlist,
            int nbig, int* __restrict__ counter, double* __restrict__ arena,
