@@ -871,14 +871,14 @@ class OperatorSet:
     def _on_lib(self, handle: int, fn, *tensors):
         """Run a library call on the context's stream, ordered after torch's
         current stream and before its later work by events (no host
-        synchronisation); the tensors are recorded on the library stream for
-        the caching allocator."""
+        synchronisation).  The tensors are not record_stream'ed on the
+        library stream: torch's stream waits for the call, so any reuse of
+        their memory on it comes after the library's work -- and a recorded
+        event would outlive the context's stream at interpreter exit."""
         torch = self._torch
         ls = self._lib_stream(handle)
         cur = torch.cuda.current_stream(self.dev)
         ls.wait_stream(cur)
-        for t in tensors:
-            t.record_stream(ls)
         st = fn()
         cur.wait_stream(ls)
         return st
