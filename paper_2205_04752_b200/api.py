@@ -1471,33 +1471,47 @@ def amvm_multiply_occurrences(occurrences, matvec, x, out_dim: int, n_cols: int,
         recv[:] = send
 
     def estimate():
+        # per (H-matrix, block): the contributions of its occurrences in
+        # occurrence order, (output index, value) pairs -- the Accum of
+        # amvm.cpp:14-41, summed per index in that order (np.add.at is
+        # unbuffered and runs in input order)
         acc = {}
         for (h, tr, coeff, suffix, prefix) in occurrences:
             xin = x if suffix is None else suffix @ x
             g = h.gamma_contributions(xin, term_data=True, transposed=tr)
             for t in g.terms:
+                w = coeff * np.asarray(t.val)
                 if prefix is None:
-                    v = np.zeros(out_dim)
-                    v[t.idx] = coeff * t.val
+                    idx, val = np.asarray(t.idx, np.int64), w
                 else:
-                    v = prefix[:, t.idx] @ (coeff * t.val)
+                    # prefix column by column (block rows ascending), each
+                    # column's nonzeros in row order: value * (coeff * y_r)
+                    sub = prefix[:, t.idx].tocoo()
+                    o = np.lexsort((sub.row, sub.col))
+                    idx = sub.row[o].astype(np.int64)
+                    val = sub.data[o] * w[sub.col[o]]
+                    keep = w[sub.col[o]] != 0.0
+                    idx, val = idx[keep], val[keep]
                 key = (rank_of[(id(h), t.comp)], t.block)
                 if key not in acc:
-                    acc[key] = (h, t.comp, t.block, np.zeros(out_dim))
-                acc[key][3][:] += v
+                    acc[key] = (h, t.comp, t.block, [], [])
+                acc[key][3].append(idx)
+                acc[key][4].append(val)
         terms = []
         diff = np.zeros(out_dim)
         for key in sorted(acc):
-            h, comp, block, v = acc[key]
-            idx = np.nonzero(v)[0]
-            if len(idx) == 0:
+            h, comp, block, il, vl = acc[key]
+            ci, cv = np.concatenate(il), np.concatenate(vl)
+            if len(ci) == 0:
                 continue
-            terms.append(BlockTerm(comp, block, idx.astype(np.int64), v[idx],
-                                   float(v[idx] @ v[idx])))
+            uniq, inv = np.unique(ci, return_inverse=True)
+            v = np.zeros(len(uniq))
+            np.add.at(v, inv, cv)
+            terms.append(BlockTerm(comp, block, uniq.astype(np.int64), v,
+                                   float(np.cumsum(v * v)[-1])))
             terms[-1].ctx = h
-            diff[idx] += v[idx]  # term by term, as amvm.cpp:111-115
+            diff[uniq] += v  # term by term, as amvm.cpp:111-115
         return terms, diff
-
     t_start = _time.perf_counter()
     b = _f64(matvec(x))
     b_hat_prev = None
