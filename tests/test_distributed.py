@@ -159,3 +159,49 @@ def test_sharded_marking_matches_unsharded_walk(tmp_path, world, theta):
     for r in range(world):
         assert outs[r][1] == len(ref_marked)
         assert outs[r][2] == ref_gpk
+
+
+def test_mark_sharded_argument_errors():
+    """hmb_mark_sharded validates its sizes and reports a failing all-gather
+    as the library's error (no crash)."""
+    import paper_2205_04752_b200 as hm
+    term = hm.BlockTerm(0, 0, np.array([0, 2], np.int64), np.array([1.0, -2.0]), 5.0)
+    diff = np.array([1.0, 0.0, -2.0])
+    with pytest.raises(hm.DimensionError):
+        hm.mark_blocks_sharded([term], diff[:2], np.ones(3, bool), 0.7, 1, 3, 3, 1, 0,
+                               lambda s, r: None)
+    with pytest.raises(hm.DimensionError):
+        hm.mark_blocks_sharded([term], diff, np.ones(2, bool), 0.7, 1, 3, 3, 1, 0,
+                               lambda s, r: None)
+
+    def broken(s, r):
+        raise RuntimeError("transport down")
+
+    with pytest.raises(hm.Error):
+        hm.mark_blocks_sharded([term], diff, np.ones(3, bool), 0.7, 1, 3, 3, 2, 0, broken)
+    # one rank, a trivial all-gather: the unsharded walk (every term marked
+    # once the target needs it)
+    marked, total, gpk = hm.mark_blocks_sharded(
+        [term], diff, np.ones(3, bool), 0.7, 1, 3, 3, 1, 0,
+        lambda s, r: r.__setitem__(slice(None), s))
+    assert list(marked) == [0] and total == 1 and gpk == 0.0
+    # rank index out of range
+    with pytest.raises(hm.Error):
+        hm.mark_blocks_sharded([term], diff, np.ones(3, bool), 0.7, 1, 3, 3, 2, 2,
+                               lambda s, r: None)
+
+
+def test_amvm_occurrences_config_errors():
+    import paper_2205_04752_b200 as hm
+    with pytest.raises(hm.ConfigError):
+        hm.amvm_multiply_occurrences([], lambda v: v, np.zeros(3), 3, 3,
+                                     hm.AmvmConfig(theta=1.0))
+    with pytest.raises(hm.ConfigError):
+        hm.amvm_multiply_occurrences([], lambda v: v, np.zeros(3), 3, 3,
+                                     hm.AmvmConfig(eps_amvm=0.0))
+    with pytest.raises(hm.DimensionError):
+        hm.amvm_multiply_occurrences([], lambda v: v, np.zeros(2), 3, 3, hm.AmvmConfig())
+    # no H-leaf at all: gamma = 0, the product itself
+    b, rep = hm.amvm_multiply_occurrences([], lambda v: 2.0 * v, np.ones(3), 3, 3,
+                                          hm.AmvmConfig())
+    assert (b == 2.0).all() and rep.converged and rep.iterations[0].gamma == 0.0
