@@ -954,6 +954,16 @@ int aca_cta_min() {
   return v;
 }
 
+// CTAs that take the CTA-cooperative items: all (default) or
+// HMGPU_ACA_BIG_CTAS per SM
+int aca_big_ctas(hmgpu_ctx* c, int grid) {
+  static const int per_sm = [] {
+    const char* e = std::getenv("HMGPU_ACA_BIG_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return per_sm > 0 ? std::min(grid, per_sm * c->sm_count) : grid;
+}
+
 // `list` is ordered by m + n (largest first); mn(idx) gives an item's m + n
 template <class MN>
 void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
@@ -972,7 +982,7 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
         kernel<<<grid, ACA_NT, 0, c->stream>>>(
             c->geom, c->d_items.p, c->d_list.p, (int)list.size(), nbig, c->d_counter.p,
             c->d_arena.p, c->d_piv.p, c->d_cons.p, sf, c->max_rank, c->lookahead,
-            c->d_overflow.p);
+            c->d_overflow.p, aca_big_ctas(c, grid));
       };
       if (c->kind == KIND_KELVIN) go(aca_kernel<KIND_KELVIN>);
       else if (c->kind == KIND_GALERKIN) go(aca_kernel<KIND_GALERKIN>);

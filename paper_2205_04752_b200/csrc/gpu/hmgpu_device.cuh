@@ -1328,10 +1328,13 @@ __global__ void __launch_bounds__(ACA_NT, MINB)
 aca_kernel(Geom g, Item* __restrict__ items, const int* __restrict__ list, int nlist,
            int nbig, int* __restrict__ counter, double* __restrict__ arena,
            int2* __restrict__ pivots, uint8_t* __restrict__ cons, double sf_run,
-           long long max_rank, int lookahead, int* __restrict__ overflow) {
+           long long max_rank, int lookahead, int* __restrict__ overflow, int big_ctas) {
   __shared__ AcaShared sh;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  bool cta_mode = nbig > 0;
+  // only the first big_ctas CTAs take the CTA-cooperative items (fewer of
+  // them in flight keeps their factor panels in L2); the others start with
+  // the single-warp items
+  bool cta_mode = nbig > 0 && (int)blockIdx.x < big_ctas;
   for (;;) {
     int t;
     if (cta_mode) {
