@@ -977,6 +977,17 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
     while (nbig < (int)list.size() && mn(list[nbig]) >= aca_cta_min()) ++nbig;
     const int nwarps = (int)list.size();
     const int grid = grid_for(c, std::max(nbig, (nwarps + 7) / 8), 16);
+    // HMGPU_ACA_TRACE=<file>: per-item completion times of this launch
+    // (diagnostics: item size, mode and end time relative to the first)
+    static const char* trace = std::getenv("HMGPU_ACA_TRACE");
+    DBuf<unsigned long long> d_trace;
+    if (trace) {
+      d_trace.alloc(c->items.size());
+      CK(cudaMemsetAsync(d_trace.p, 0, c->items.size() * 8, c->stream));
+      unsigned long long* pt = d_trace.p;
+      CK(cudaMemcpyToSymbolAsync(g_aca_trace, &pt, sizeof(pt), 0, cudaMemcpyHostToDevice,
+                                 c->stream));
+    }
     c->timed("aca", [&] {
       auto go = [&](auto kernel) {
         kernel<<<grid, ACA_NT, 0, c->stream>>>(
@@ -995,6 +1006,25 @@ void run_aca(hmgpu_ctx* c, std::vector<int> list, int* relaunches, MN&& mn) {
     CK(cudaMemcpyAsync(&over, c->d_overflow.p, sizeof(int), cudaMemcpyDeviceToHost,
                        c->stream));
     c->sync();
+    if (trace) {
+      std::vector<unsigned long long> tt(c->items.size());
+      CK(cudaMemcpy(tt.data(), d_trace.p, tt.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long* nullp = nullptr;
+      CK(cudaMemcpyToSymbol(g_aca_trace, &nullp, sizeof(nullp)));
+      unsigned long long t0 = ~0ull;
+      for (int idx : list)
+        if (tt[idx]) t0 = std::min(t0, tt[idx]);
+      if (FILE* f = std::fopen(trace, passes == 0 ? "w" : "a")) {
+        std::fprintf(f, "# pass %d nbig %d grid %d\n", passes, nbig, grid);
+        for (size_t q = 0; q < list.size(); ++q) {
+          const int idx = list[q];
+          std::fprintf(f, "%d %d %d %d %.3f\n", (int)q, c->items[idx].m, c->items[idx].n,
+                       (int)(q < (size_t)nbig), tt[idx] ? (tt[idx] - t0) * 1e-6 : -1.0);
+        }
+        std::fclose(f);
+      }
+      d_trace.free();
+    }
     if (over == 0) break;
     ++passes;
     if (verbose())
@@ -2788,6 +2818,32 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
       const long long fit = (long long)(0.55 * avail / (8.0 * (double)sum_mn));
       cap_init = (int)std::max<long long>(lookahead + 6, std::min<long long>(cap_init, fit));
     }
+    // the largest blocks carry the highest ranks: they start with extra
+    // columns when memory allows, so they rarely overflow into the
+    // relocation pass (a second launch over a few large items, poorly
+    // parallel: 11.5 ms of config 3's 287 ms ACA before this)
+    static const int big_mn = [] {
+      const char* e = std::getenv("HMGPU_ACA_BIG_MN");
+      return e ? std::atoi(e) : 8192;
+    }();
+    static const int big_extra = [] {
+      const char* e = std::getenv("HMGPU_ACA_BIG_EXTRA");
+      return e ? std::max(0, std::atoi(e)) : 24;
+    }();
+    int cap_big = cap_init;
+    if (initial_rank < 0 && big_extra > 0) {
+      long long sum_mn_big = 0;
+      for (int b = 0; b < c->n_blocks; ++b) {
+        const int* B = &c->blocks[4 * b];
+        const int* rn = &c->rnodes[4 * B[0]];
+        const int* cn = &c->cnodes[4 * B[1]];
+        if (!B[2] || rn[0] < c->row_begin || rn[1] > c->row_end) continue;
+        const long long mn = (rn[1] - rn[0]) + (cn[1] - cn[0]);
+        if (mn >= big_mn) sum_mn_big += mn * c->NC;
+      }
+      if (8.0 * ((double)sum_mn * cap_init + (double)sum_mn_big * big_extra) <= 0.55 * avail)
+        cap_big = cap_init + big_extra;
+    }
     for (int b = 0; b < c->n_blocks; ++b) {
       const int* B = &c->blocks[4 * b];
       const int* rn = &c->rnodes[4 * B[0]];
@@ -2799,7 +2855,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
         // record (items_init_kernel); offsets assigned here in item order
         c->item_of_block[b] = (int)(NCq * ablocks.size());
         const long long capr = std::min<long long>(max_rank, std::min(m, n));
-        const int cap = (int)std::min<long long>(capr, cap_init);
+        const int cap = (int)std::min<long long>(capr, m + n >= big_mn ? cap_big : cap_init);
         AdmBlock ab{};
         ab.m = m;
         ab.n = n;

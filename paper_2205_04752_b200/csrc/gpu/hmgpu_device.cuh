@@ -1254,6 +1254,9 @@ __device__ __forceinline__ int aca_step(const SRC& src, Item& s, double* __restr
   }
 }
 
+// per-item completion times of the last ACA launch (null = off)
+__device__ unsigned long long* g_aca_trace = nullptr;
+
 // Runs one item's state machine until done or out of column capacity:
 //   PH_RUN  aca_run to the stopping rule (aca.cpp:106-124)
 //   PH_INIT coarse mode: aca_extend(initial_rank) (hmatrix.cpp:156-158)
@@ -1312,6 +1315,11 @@ __device__ __forceinline__ void aca_item(const SRC& src, Item& s, Item* __restri
   s.nq_sum += grp_sum_ll(nq_acc, g, sh);
   if (g.tid == 0) {
     items[idx] = s;
+    if (g_aca_trace) {  // diagnostics (HMGPU_ACA_TRACE): item end time, ns
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      g_aca_trace[idx] = ns;
+    }
     if (s.status == ST_OVERFLOW) atomicAdd(overflow, 1);
   }
 }
