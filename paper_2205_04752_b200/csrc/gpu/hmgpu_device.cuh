@@ -1929,7 +1929,17 @@ __global__ void compact_kernel(Item* __restrict__ items, int n,
     auto copy2 = [&](double* d, const double* s_, long long len) {
       const double2* s2 = reinterpret_cast<const double2*>(s_);
       double2* d2 = reinterpret_cast<double2*>(d);
-      for (long long e = lane; e < len / 2; e += 32) d2[e] = s2[e];
+      // four 16-byte loads in flight per lane before their stores
+      const long long h = len / 2;
+      long long e = lane;
+      for (; e + 96 < h; e += 128) {
+        const double2 a = s2[e], b = s2[e + 32], c = s2[e + 64], f = s2[e + 96];
+        d2[e] = a;
+        d2[e + 32] = b;
+        d2[e + 64] = c;
+        d2[e + 96] = f;
+      }
+      for (; e < h; e += 32) d2[e] = s2[e];
       if ((len & 1) && lane == 0) d[len - 1] = s_[len - 1];
     };
     copy2(dst + u0, su, nu);
