@@ -17,6 +17,8 @@
 #include <array>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <exception>
 #include <new>
 #include <numeric>
 #include <stdexcept>
@@ -342,6 +344,30 @@ struct PendingEv {
 };
 
 long long align2(long long v) { return (v + 1) & ~1LL; }
+
+// vector allocator whose resize() leaves trivial elements uninitialized (the
+// plan tables are filled right after, in parallel: no serial zero-fill and
+// the first-touch page faults spread over the filling threads)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using fast_vector = std::vector<T, NoInitAlloc<T>>;
 inline int c_comp_host_r(int q) {
   static const int r[6] = {0, 0, 0, 1, 1, 2};
   return r[q];
@@ -1346,12 +1372,12 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   const int kStageDataB = cfgB.stage - 16;
   const int kMaxKFused = (cfg.scratch - 256) / 4;  // scratch: x (256) + W (4 K)
   const int NC = c->NC;
-  std::vector<WJob> ja, jb;
+  fast_vector<WJob> ja, jb;
   // chunks per job, flat (CSR over the pass's jobs)
   struct ChunkCSR {
-    std::vector<WChunk> flat;
-    std::vector<long long> ptr{0};
-    std::vector<long long> size;  // streamed doubles per job
+    fast_vector<WChunk> flat;
+    fast_vector<long long> ptr{0};
+    fast_vector<long long> size;  // streamed doubles per job
     void add(const std::vector<WChunk>& chs) {
       long long s = 0;
       for (const WChunk& ch : chs) s += ch.len + 4LL * ch.aux_len;
@@ -1361,7 +1387,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     }
   } ca, cb;
   std::vector<WChunk> chs;  // the current job's chunks (reused)
-  std::vector<PackDesc> packs;
+  fast_vector<PackDesc> packs;
   ja.reserve(c->mvb.size() * 2);
   ca.flat.reserve(c->mvb.size() * 6);
   ca.ptr.reserve(c->mvb.size() * 2);
@@ -1395,7 +1421,29 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     ch.part = part;
     return ch;
   };
-  for (const MvBlock& mb : c->mvb) {
+  // the blocks' jobs, chunks and pack descriptors, built by host threads over
+  // contiguous block ranges with local arena / W-slot offsets, then
+  // concatenated in range order with the offsets shifted (the same tables as
+  // one sequential pass)
+  struct Local {
+    fast_vector<WJob> ja, jb;
+    ChunkCSR ca, cb;
+    fast_vector<PackDesc> packs;
+    std::vector<WChunk> chs;
+    long long alen = 0, wslots = 0;
+    std::exception_ptr err;
+  };
+  auto run_range = [&](Local& Lc, size_t b0, size_t b1) {
+    auto& ja = Lc.ja;
+    auto& jb = Lc.jb;
+    auto& ca = Lc.ca;
+    auto& cb = Lc.cb;
+    auto& packs = Lc.packs;
+    auto& chs = Lc.chs;
+    long long& alen = Lc.alen;
+    long long& wslots = Lc.wslots;
+    for (size_t bi = b0; bi < b1; ++bi) {
+      const MvBlock& mb = c->mvb[bi];
     const int m = mb.m, n = mb.n;
     if (mb.dense) {
       if (m > 64 || n > 64)
@@ -1570,6 +1618,92 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       }
       q0 = q1;
     }
+      }
+  };
+  {
+    const size_t nb = c->mvb.size();
+    const int nthr = (int)std::max<size_t>(
+        1, std::min<size_t>({(size_t)std::max(1u, std::thread::hardware_concurrency()),
+                             (size_t)16, nb / 2048 + 1}));
+    std::vector<Local> loc(nthr);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthr; ++t) {
+      const size_t b0 = nb * t / nthr, b1 = nb * (t + 1) / nthr;
+      auto work = [&, t, b0, b1] {
+        try {
+          run_range(loc[t], b0, b1);
+        } catch (...) {
+          loc[t].err = std::current_exception();
+        }
+      };
+      if (t + 1 < nthr) pool.emplace_back(work);
+      else work();
+    }
+    for (auto& th : pool) th.join();
+    for (auto& Lc : loc)
+      if (Lc.err) std::rethrow_exception(Lc.err);
+    // offsets of every thread's part in the concatenated tables, then each
+    // thread shifts and copies its own part (in parallel)
+    struct Off {
+      size_t ja, jb, caf, cap, cbf, cbp, pk;
+      long long alen, wslots;
+    };
+    std::vector<Off> off(nthr + 1);
+    off[0] = Off{0, 0, 0, 1, 0, 1, 0, 0, 0};
+    for (int t = 0; t < nthr; ++t) {
+      const Local& Lc = loc[t];
+      off[t + 1] = Off{off[t].ja + Lc.ja.size(), off[t].jb + Lc.jb.size(),
+                       off[t].caf + Lc.ca.flat.size(), off[t].cap + Lc.ca.ptr.size() - 1,
+                       off[t].cbf + Lc.cb.flat.size(), off[t].cbp + Lc.cb.ptr.size() - 1,
+                       off[t].pk + Lc.packs.size(), off[t].alen + Lc.alen,
+                       off[t].wslots + Lc.wslots};
+    }
+    const Off& tot = off[nthr];
+    ja.resize(tot.ja);
+    jb.resize(tot.jb);
+    ca.flat.resize(tot.caf);
+    ca.ptr.resize(tot.cap);
+    ca.size.resize(tot.cap - 1);
+    cb.flat.resize(tot.cbf);
+    cb.ptr.resize(tot.cbp);
+    cb.size.resize(tot.cbp - 1);
+    packs.resize(tot.pk);
+    ca.ptr[0] = 0;
+    cb.ptr[0] = 0;
+    auto place = [&](int t) {
+      Local& Lc = loc[t];
+      const Off& o = off[t];
+      for (size_t i = 0; i < Lc.ja.size(); ++i) {
+        WJob j = Lc.ja[i];
+        if (j.kind == WJ_VSPLIT) j.out += o.wslots;
+        ja[o.ja + i] = j;
+      }
+      std::copy(Lc.jb.begin(), Lc.jb.end(), jb.begin() + o.jb);
+      auto put = [&](ChunkCSR& dst, const ChunkCSR& src, size_t fo, size_t po) {
+        for (size_t i = 0; i < src.flat.size(); ++i) {
+          WChunk ch = src.flat[i];
+          if (ch.src_kind == 0) ch.src += o.alen;
+          if (ch.aux_kind == WA_W) ch.aux += o.wslots;
+          dst.flat[fo + i] = ch;
+        }
+        for (size_t i = 1; i < src.ptr.size(); ++i) dst.ptr[po + i - 1] = (long long)fo + src.ptr[i];
+        std::copy(src.size.begin(), src.size.end(), dst.size.begin() + (po - 1));
+      };
+      put(ca, Lc.ca, o.caf, o.cap);
+      put(cb, Lc.cb, o.cbf, o.cbp);
+      for (size_t i = 0; i < Lc.packs.size(); ++i) {
+        PackDesc pd = Lc.packs[i];
+        pd.dst += o.alen;
+        packs[o.pk + i] = pd;
+      }
+      Lc = Local{};
+    };
+    pool.clear();
+    for (int t = 0; t + 1 < nthr; ++t) pool.emplace_back(place, t);
+    place(nthr - 1);
+    for (auto& th : pool) th.join();
+    alen = tot.alen;
+    wslots = tot.wslots;
   }
   pphase("blocks");
   // Job order per pass: the row jobs by (first row, rows) -- stable LSD
@@ -1578,7 +1712,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   // runs back to back, accumulating in registers and writing ONE partial
   // row (the leaf pass then sums a few units per leaf instead of one partial
   // row per block).
-  auto order = [&](const std::vector<WJob>& J) {
+  auto order = [&](const fast_vector<WJob>& J) {
     const size_t nj = J.size();
     std::vector<int> a(nj), b(nj);
     std::vector<int> cnt(66, 0);
@@ -1602,7 +1736,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   std::vector<WJob> jobs;
   std::vector<int> woff;
   const size_t nchunks_total = ca.flat.size() + cb.flat.size();
-  std::vector<WChunk> chunk_table(nchunks_total);
+  fast_vector<WChunk> chunk_table(nchunks_total);
   WChunk* chunks = chunk_table.data();
   size_t nch = 0;
   for (int pass = 0; pass < 2; ++pass) {
@@ -1686,22 +1820,47 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       std::vector<int> fill(wptr.begin(), wptr.end() - 1);
       for (size_t i = 0; i < nu; ++i) wunits[fill[uwarp[uord[i]]]++] = uord[i];
     }
+    pphase(pass == 0 ? "layout A/u" : "layout B/u");
     c->p_woff_base[pass] = (int)woff.size();
     c->p_chunk_base[pass] = (int)nch;
+    // per warp its chunk count, the offsets, then the copies by host
+    // threads over warp ranges (the table is the sequential one)
+    std::vector<long long> wstart(NWARPS + 1, 0);
     for (int w = 0; w < NWARPS; ++w) {
-      woff.push_back((int)(nch - c->p_chunk_base[pass]));
+      long long cnt = 0;
       for (int k = wptr[w]; k < wptr[w + 1]; ++k) {
         const int u = wunits[k];
-        for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t) {
-          for (long long q = C.ptr[ord[t]]; q < C.ptr[ord[t] + 1]; ++q) {
-            WChunk ch = C.flat[q];
-            ch.job = jpos[t];
-            chunks[nch++] = ch;
+        for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t) cnt += C.ptr[ord[t] + 1] - C.ptr[ord[t]];
+      }
+      wstart[w + 1] = wstart[w] + cnt;
+      woff.push_back((int)wstart[w]);
+    }
+    {
+      const int nthr = std::max(1, std::min<int>((int)std::max(1u, std::thread::hardware_concurrency()),
+                                                 std::min(16, NWARPS)));
+      auto fill = [&](int w0, int w1) {
+        for (int w = w0; w < w1; ++w) {
+          long long o = (long long)nch + wstart[w];
+          for (int k = wptr[w]; k < wptr[w + 1]; ++k) {
+            const int u = wunits[k];
+            for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t) {
+              for (long long q = C.ptr[ord[t]]; q < C.ptr[ord[t] + 1]; ++q) {
+                WChunk ch = C.flat[q];
+                ch.job = jpos[t];
+                chunks[o++] = ch;
+              }
+            }
           }
         }
-      }
+      };
+      std::vector<std::thread> th;
+      for (int t = 0; t + 1 < nthr; ++t)
+        th.emplace_back(fill, NWARPS * t / nthr, NWARPS * (t + 1) / nthr);
+      fill(NWARPS * (nthr - 1) / nthr, NWARPS);
+      for (auto& x : th) x.join();
     }
-    woff.push_back((int)(nch - c->p_chunk_base[pass]));
+    nch += (size_t)wstart[NWARPS];
+    woff.push_back((int)wstart[NWARPS]);
     c->p_nwarps_pass[pass] = NWARPS;
   }
   c->p_nwarps = c->p_nwarps_pass[0];
@@ -1719,7 +1878,7 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
   c->spare_arena.ensure((size_t)alen + 2, c->device);
   if (!packs.empty()) {
     DBuf<PackDesc> d_packs;
-    d_packs.upload(packs, c->stream);
+    d_packs.upload(packs.data(), packs.size(), c->stream);
     c->timed("pack", [&] {
       pack_kernel<<<grid_for(c, ((long long)packs.size() + 7) / 8, 16), 256, 0, c->stream>>>(
           d_packs.p, (int)packs.size(), c->d_arena.p, c->spare_arena.p);
