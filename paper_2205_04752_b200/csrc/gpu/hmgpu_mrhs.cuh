@@ -5,23 +5,27 @@
 // multiply-adds, so the sweep needs the fp64 tensor pipe as much as HBM:
 // these are the "batched fp64 factor products" of the north star.
 //
-// Two persistent, TMA-fed passes; a CTA of 4 warps runs a ring of NS stages
-// in shared memory, every stage brought in by cp.async.bulk (one mbarrier
-// transaction per stage: descriptor + data), the warps compute DMMA from the
-// stage while the next one is in flight:
+// Two persistent, TMA-fed passes.  A CTA = 8 consumer warps + 1 producer
+// warp around a ring of NS stages in shared memory (3 CTAs per SM by
+// default): the producer issues each stage's bulk copies (cp.async.bulk, one
+// mbarrier transaction per stage, L2 evict-first for streamed data and
+// evict-last for re-read x rows / Z) as soon as every consumer released the
+// slot; the consumers compute DMMA on fragments read from the stage:
 //
-//   phase 1 (hmv16_z_kernel)  one task per (admissible block, group of
-//            component l-ranges, <= 64 l in all): Z_c = V_c^T X_C and
-//            W_c = V_c^T X_R accumulated in registers over the block's
-//            column chunks (all the group's components share the staged X
-//            rows: x is read once per block and chunk, not once per
-//            component), written once ([l][ZP] rows, no partial sums)
-//   phase 2 (hmv16_y_kernel)  one task per leaf of the row tree: for the
-//            blocks covering the leaf in a fixed order, Y_R += U_c Z_c,
-//            Y_C += U_c W_c (the block's Z staged once per leaf and shared
-//            by the 4 warps) and, for near-field blocks, Y_R += D_c X_C,
-//            Y_C += D_c X_R; y written once per row (deterministic, no
-//            atomics, no partial rows).
+//   phase 1 (hmv16_z_kernel)  one task per (admissible block, <= 64 l of its
+//            components): the task's rows of V^T are tiled in 8-row m-tiles
+//            per x-operand group (x_0: Z_00 W_01 W_02, x_1: Z_01 Z_11 W_12,
+//            x_2: Z_02 Z_12 Z_22), so the padding is per group, not per
+//            component; Z_c = V_c^T X_C and W_c = V_c^T X_R accumulate in
+//            registers over the block's column chunks (every chunk stages
+//            its x rows once for all components) and are written once
+//   phase 2 (hmv16_y_kernel)  one task per leaf of the row tree (leaves
+//            dealt to the CTAs cyclically): stages of up to 14 items -- a
+//            low-rank block piece with the block's Z (staged once per leaf,
+//            shared by the 8 warps: Y_R += U_c Z_c, Y_C += U_c W_c) or a
+//            near-field column group with its x rows (Y_R += D_c X_C,
+//            Y_C += D_c X_R) -- in the leaf's fixed block order; y written
+//            once per row (deterministic, no atomics, no partial rows).
 //
 // Data (all chosen so that the DMMA fragment loads from shared memory are
 // free of bank conflicts: a half-warp (g, t) in [0,4)^2 reads element
