@@ -289,6 +289,11 @@ struct VArena {
       reclaim_idle_memory();
       rc = api.create(&hnd, delta, &pr, 0);
     }
+    const size_t need = (want - mapped + gran - 1) / gran * gran;
+    if (rc == CUDA_ERROR_OUT_OF_MEMORY && need < delta) {  // the 1/8 headroom does not fit
+      delta = need;
+      rc = api.create(&hnd, delta, &pr, 0);
+    }
     CU(rc);
     CUresult r = api.map(base + mapped, delta, 0, hnd, 0);
     if (r != CUDA_SUCCESS) {
@@ -878,7 +883,19 @@ void arena_reserve(hmgpu_ctx* c, long long extra_doubles, long long extra_piv) {
   const long long need = c->arena_used + extra_doubles;
   if (need > (long long)c->d_arena.n) {
     c->sync();  // mapping is synchronous with the host
-    c->d_arena.ensure((size_t)need, c->device);
+    try {
+      c->d_arena.ensure((size_t)need, c->device);
+    } catch (const Fail& f) {
+      // out of memory with the idle compaction arena still mapped (it only
+      // hosts the stream / 16-RHS plans, rebuilt on the next matvec): give
+      // it back and retry
+      if (f.code != HMGPU_ERR_OOM || c->spare_arena.mapped == 0) throw;
+      c->spare_arena.free();
+      c->plan_valid = false;
+      c->p16_valid = false;
+      if (verbose()) std::fprintf(stderr, "[hmgpu] arena: idle spare arena released\n");
+      c->d_arena.ensure((size_t)need, c->device);
+    }
   }
   const long long needp = c->piv_used + extra_piv;
   if (needp > (long long)c->d_piv.n) {
