@@ -342,6 +342,10 @@ int hmgpu_fp64_peak(int device, double* tflops);
 /* measured fp64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s:
    the peak the multi-RHS sweep is reported against */
 int hmgpu_dmma_peak(int device, double* tflops);
+/* the same chains launched back to back for `seconds` (0.2 .. 10): the mean
+   rate over the second half of the run, i.e. at the clocks the power limit
+   settles on under a long fp64 tensor load (burst: hmgpu_dmma_peak) */
+int hmgpu_dmma_peak_sustained(int device, double seconds, double* tflops);
 
 /* CUDA-event timing of every kernel launch (off by default).  names are
  * "gather", "nearfield", "aca", "hmv_blocks", "hmv_reduce", "tail", ...

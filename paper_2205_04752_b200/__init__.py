@@ -3,7 +3,7 @@
 blocks, near-field fill and the H-matvec on sm_100a, behind the C ABI of
 include/hmgpu.h, with a host layer mirroring the reference's operator API.
 """
-from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflops, dmma_peak_tflops, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
+from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflops, dmma_peak_tflops, dmma_peak_sustained_tflops, AmvmConfig, AmvmIteration, AmvmReport, AssemblyConfig,
                   AssemblyStats, BlockTerm, ClusterTree, ConfigError, DeviceError,
                   DimensionError, Error, GammaContributions, HMatrix, LameSingleLayer, Mesh,
                   OperatorSet, lame_constants, InteriorEvaluator, pair_rule, sparse_op, BacaConfig, BacaReport, VddPreconditioner,
@@ -15,7 +15,7 @@ from .api import (AcaStop, admissible, gauss_rule, random_vector, fp64_peak_tflo
                   assemble_rhs)
 
 __all__ = [
-    "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
+    "AcaStop", "admissible", "gauss_rule", "random_vector", "fp64_peak_tflops", "dmma_peak_tflops", "dmma_peak_sustained_tflops", "AmvmConfig", "AmvmIteration", "AmvmReport", "AssemblyConfig",
     "AssemblyStats", "BlockTerm", "ClusterTree", "ConfigError", "DeviceError",
     "DimensionError", "Error", "GammaContributions", "HMatrix", "LameSingleLayer", "Mesh",
     "OperatorSet", "lame_constants", "InteriorEvaluator", "pair_rule", "sparse_op", "BacaConfig", "BacaReport", "VddPreconditioner",

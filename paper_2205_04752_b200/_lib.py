@@ -99,6 +99,7 @@ _sig(gpu, "hmgpu_kernel_times", I, P, C.c_char_p, DP, LLP, I)
 _sig(gpu, "hmgpu_storage", I, P, P)
 _sig(gpu, "hmgpu_fp64_peak", I, I, DP)
 _sig(gpu, "hmgpu_dmma_peak", I, I, DP)
+_sig(gpu, "hmgpu_dmma_peak_sustained", I, I, D, DP)
 _sig(gpu, "hmgpu_set_matvec_policy", I, P, I)
 _sig(gpu, "hmgpu_get_matvec_policy", I, P, IP)
 # multi-GPU block-row shards

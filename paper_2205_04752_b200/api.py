@@ -1993,6 +1993,16 @@ def dmma_peak_tflops(device: int = 0) -> float:
     return v.value
 
 
+def dmma_peak_sustained_tflops(device: int = 0, seconds: float = 1.0) -> float:
+    """DMMA throughput over the second half of `seconds` of back-to-back
+    launches: the rate at the clocks the power limit settles on."""
+    v = C.c_double()
+    st = _lib.gpu.hmgpu_dmma_peak_sustained(device, float(seconds), C.byref(v))
+    if st:
+        raise DeviceError("hmgpu_dmma_peak_sustained failed", st)
+    return v.value
+
+
 def fp64_peak_tflops(device: int = 0) -> float:
     """Measured DFMA throughput of the device (fp64 roofline denominator)."""
     v = C.c_double()

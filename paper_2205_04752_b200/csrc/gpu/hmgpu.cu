@@ -515,6 +515,8 @@ struct hmgpu_ctx {
   int p16_mode = -1;
   int p16_ns = 2, p16_stage = 0, p16_ncta = 0;
   int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8, p16_ynw = 8;
+  // per-CTA cost terms of the plan (bytes, DMMA steps per warp, items, stages)
+  std::vector<std::array<long long, 4>> p16_ycost, p16_zcost;
   long long p16_zsize = 0, p16_alen = 0;
   int n_zch16 = 0, n_yst16 = 0;
   DBuf<ZChunk16> d_zch16;
@@ -1933,11 +1935,13 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
 // ---- multi-RHS plan (hmgpu_mrhs.cuh) ----------------------------------------
 // HMGPU_M16_CFG="ns,stage": ring depth (3, 4, 6 or 9) and doubles per stage
 struct M16Cfg {  // measured on config 3: 3 x 3072 (3 CTAs / SM) best
-  int ns = 3, stage = 3072;
+  int ns = 3, stage = 0;  // stage 0: 3072 doubles at 3 CTAs per SM, 2304 at 4
   // phase 1 (HMGPU_M16_ZCFG="ns,stage,warps"): its own ring and consumer
-  // warps (8 or 12)
-  int zns = 3, zstage = 3072, znw = 8;
-  int ynw = 8;  // phase-2 consumer warps (HMGPU_M16_YNW: 8 or 16, 16 = one CTA per SM)
+  // warps (6, 8 or 12; 6 runs 4 CTAs per SM)
+  int zns = 3, zstage = 0, znw = 6;
+  // phase-2 consumer warps (HMGPU_M16_YNW: 5, 6, 8 or 16; 0 = from the
+  // leaves' row tiles, so that no warp idles through a leaf)
+  int ynw = 0;
 };
 M16Cfg m16_cfg() {
   static const M16Cfg cfg = [] {
@@ -1951,7 +1955,10 @@ M16Cfg m16_cfg() {
       r.zstage = b;
     }
     const char* yw = std::getenv("HMGPU_M16_YNW");
-    if (yw) r.ynw = std::atoi(yw) == 16 ? 16 : 8;
+    if (yw) {
+      const int v = std::atoi(yw);
+      r.ynw = (v == 5 || v == 6 || v == 16) ? v : 8;
+    }
     const char* z = std::getenv("HMGPU_M16_ZCFG");
     if (z && std::sscanf(z, "%d,%d,%d", &a, &b, &w) == 3) {
       r.zns = a;
@@ -1982,15 +1989,37 @@ std::vector<int> split_runs(const std::vector<long long>& bytes, int ncta) {
   return first;
 }
 
+// DMMA instructions one consumer warp issues for a phase-2 piece (both RHS
+// halves): the plan's cost term of a leaf
+long long y16_steps(const YStage16& d) {
+  if (d.kind == Y16_DENSE) return (long long)((d.jd + 3) / 4) * 18;
+  static const int w[6] = {2, 4, 4, 2, 4, 2};  // diagonal components: Z only
+  long long n = 0;
+  for (int q = 0; q < 6; ++q) n += (long long)((d.hi[q] - d.lo[q] + 3) / 4) * w[q];
+  return n;
+}
+
 // Multi-RHS plan: phase-1 tasks (block, <= 64 l of its components) with
 // their column chunks, phase-2 stages per leaf, the p16 arena (current-rank
 // factors re-packed in stage order, zero padded to the conflict-free
 // pitches), the Z layout and the per-CTA runs of both passes.
 void build_plan16(hmgpu_ctx* c, int mode) {
-  const M16Cfg cfg = m16_cfg();
+  M16Cfg cfg = m16_cfg();
+  if (cfg.ynw == 0) {  // consumer warps = row tiles of the tallest leaf
+    int rmax = 1;
+    for (size_t L = 0; L < c->leaf_begin.size(); ++L)
+      rmax = std::max(rmax, c->leaf_end[L] - c->leaf_begin[L]);
+    const int rt = (rmax + 7) / 8;
+    cfg.ynw = (rt == 6 || rt == 3) ? 6 : (rt == 5 ? 5 : 8);
+  }
+  const bool y4 = cfg.ynw == 5 || cfg.ynw == 6;  // 4 CTAs per SM
+  if (cfg.stage == 0) {
+    cfg.stage = y4 ? 2304 : 3072;
+    if (cfg.zstage == 0) cfg.zstage = 2304;  // 6 consumer warps, 4 CTAs per SM
+  }
   if ((cfg.ns != 3 && cfg.ns != 4 && cfg.ns != 6 && cfg.ns != 9) || cfg.stage < 2048 || (cfg.stage & 3))
     fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_CFG");
-  if ((cfg.zns != 3 && cfg.zns != 4) || (cfg.znw != 8 && cfg.znw != 12) || cfg.zstage < 2048 ||
+  if ((cfg.zns != 3 && cfg.zns != 4) || (cfg.znw != 6 && cfg.znw != 8 && cfg.znw != 12) || cfg.zstage < 2048 ||
       (cfg.zstage & 3))
     fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_ZCFG");
   const int SD = cfg.zstage - M16_HDR;  // phase-1 data doubles per stage
@@ -2071,6 +2100,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         tk.gtile[r + 1] = (unsigned char)(tk.gtile[r] + (grows[r] + 7) / 8);
       }
       tk.ntiles = tk.gtile[3];
+      if (tk.ntiles > 3 * cfg.znw) fail(HMGPU_ERR_INVALID, "multi-RHS task above 3 m-tiles per warp");
       // widest chunk whose V^T and X rows fit one stage
       int jc = std::min(n, 252);
       while (jc > 4 && (long long)(L + XP) * cf_pitch(jc) > SD) jc -= 4;
@@ -2135,6 +2165,13 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         int jd = SDY / (PD + XP) + 1;
         while (jd > 0 && (long long)jd * PD + (long long)((jd + 3) & ~3) * XP > SDY) --jd;
         if (jd < 1) fail(HMGPU_ERR_INVALID, "near-field block too tall for the multi-RHS stage");
+        // whole k-steps of 4 columns (the last one of a block is predicated);
+        // HMGPU_M16_JD4=0: as many columns as fit (A/B)
+        static const bool jd4 = [] {
+          const char* e = std::getenv("HMGPU_M16_JD4");
+          return !(e && std::atoi(e) == 0);
+        }();
+        if (jd4 && jd > 4) jd &= ~3;
         for (int j0 = 0; j0 < mb.n; j0 += jd) {
           const int jj = std::min(jd, mb.n - j0);
           YStage16 d{};
@@ -2222,14 +2259,14 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   // phase 1 by tasks, phase 2 by leaves (a leaf's accumulators live in one
   // CTA); within a CTA's leaves, consecutive pieces are packed into stages
   // of up to Y16_MAXIT items, their records and bulk copies
-  const size_t ring_bytes = (size_t)cfg.ns * cfg.stage * sizeof(double);
+  const size_t ring_bytes = ((size_t)cfg.ns * cfg.stage + M16_SLACK) * sizeof(double);
   const int per_sm = cfg.ynw == 16 ? 1
-                     : std::max(1, std::min(3, (int)((227 * 1024) / (ring_bytes + 1024))));
+                     : std::max(1, std::min(y4 ? 4 : 3, (int)((227 * 1024) / (ring_bytes + 1024))));
   if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
   const int ncta = c->sm_count * per_sm;
   const size_t zring_bytes = (size_t)cfg.zns * cfg.zstage * sizeof(double);
   if (zring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_ZCFG ring too large");
-  const int zcta_sm = std::max(1, std::min(cfg.znw == 8 ? 3 : 2,
+  const int zcta_sm = std::max(1, std::min(cfg.znw == 8 ? 3 : (cfg.znw == 6 ? 4 : 2),
                                            (int)((227 * 1024) / (zring_bytes + 1024))));
   const int nctaz = c->sm_count * zcta_sm;
   std::vector<int> zcoff(nctaz + 1), ycoff(ncta + 1);
@@ -2266,11 +2303,29 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     if (!yruns)
       for (int L = 0; L < nl; ++L) cleaves[L % ncta].push_back(L);
     std::vector<int> cpieces;
+    c->p16_ycost.assign(ncta, {0, 0, 0, 0});
+    c->p16_zcost.assign(nctaz, {0, 0, 0, 0});
+    for (int k = 0; k < nctaz; ++k)
+      for (int ti = ft[k]; ti < ft[k + 1]; ++ti) {
+        const int tw = (tasks[ti].ntiles + cfg.znw - 1) / cfg.znw;  // m-tiles of the busiest warp
+        for (int q = tptr[ti]; q < tptr[ti + 1]; ++q) {
+          c->p16_zcost[k][0] += 8LL * (zch[q].vlen + (long long)zch[q].P * XP);
+          c->p16_zcost[k][1] += (long long)(zch[q].P / 4) * 2 * tw;
+          c->p16_zcost[k][3] += 1;
+        }
+        c->p16_zcost[k][2] += 1;
+      }
     for (int k = 0; k < ncta; ++k) {
       ycoff[k] = (int)ystages.size();
       cpieces.clear();
       for (int L : cleaves[k])
         for (int q = lptr[L]; q < lptr[L + 1]; ++q) cpieces.push_back(q);
+      for (int q : cpieces) {
+        const YStage16& d = yst[q];
+        c->p16_ycost[k][0] += 8 * plen(d);
+        c->p16_ycost[k][1] += y16_steps(d);
+        c->p16_ycost[k][2] += 1;
+      }
       const int p1 = (int)cpieces.size();
       for (int pi = 0; pi < p1;) {
         int pe = pi;
@@ -2321,6 +2376,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         st.ncopies = (int)ycopies.size() - st.cbeg;
         st.bytes = (int)bytes;
         ystages.push_back(st);
+        c->p16_ycost[k][3] += 1;
         pi = pe;
       }
     }
@@ -2386,7 +2442,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
 
 template <int NS, int NW = 8>
 void launch_m16(hmgpu_ctx* c, M16Params P) {  // phase 2
-  const size_t smem = (size_t)NS * c->p16_stage * sizeof(double);
+  const size_t smem = ((size_t)NS * c->p16_stage + M16_SLACK) * sizeof(double);
   CK(cudaFuncSetAttribute(hmv16_y_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   hmv16_y_kernel<NS, NW><<<c->p16_ncta, 32 * (NW + 1), smem, c->stream>>>(P);
@@ -2422,8 +2478,8 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
   P.dbg = dbg;
   static DBuf<unsigned long long> prof;
   if (dbg == 3) {
-    prof.ensure(8);
-    CK(cudaMemsetAsync(prof.p, 0, 64, c->stream));
+    prof.ensure(16 + 2 * M16_PROF_CTAS);
+    CK(cudaMemsetAsync(prof.p, 0, (16 + 2 * M16_PROF_CTAS) * 8, c->stream));
     P.prof = prof.p;
   }
   for (int s0 = 0; s0 < nrhs; s0 += MR) {
@@ -2440,7 +2496,9 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
         P.desc = c->d_zch16.p;
         P.coff = c->d_zcoff16.p;
         const int key = c->p16_zns * 100 + c->p16_znw;
-        if (key == 412) launch_m16z<4, 12>(c, P);
+        if (key == 306) launch_m16z<3, 6>(c, P);
+        else if (key == 406) launch_m16z<4, 6>(c, P);
+        else if (key == 412) launch_m16z<4, 12>(c, P);
         else if (key == 408) launch_m16z<4, 8>(c, P);
         else if (key == 312) launch_m16z<3, 12>(c, P);
         else launch_m16z<3, 8>(c, P);
@@ -2454,6 +2512,12 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
         if (c->p16_ns == 6) launch_m16<6, 16>(c, P);
         else if (c->p16_ns == 9) launch_m16<9, 16>(c, P);
         else launch_m16<4, 16>(c, P);
+      } else if (c->p16_ynw == 6) {
+        if (c->p16_ns == 4) launch_m16<4, 6>(c, P);
+        else launch_m16<3, 6>(c, P);
+      } else if (c->p16_ynw == 5) {
+        if (c->p16_ns == 4) launch_m16<4, 5>(c, P);
+        else launch_m16<3, 5>(c, P);
       } else {
         switch (c->p16_ns) {
           case 4: launch_m16<4>(c, P); break;
@@ -2465,9 +2529,27 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
     });
   }
   if (dbg == 3) {
-    unsigned long long h[8];
-    CK(cudaMemcpyAsync(h, prof.p, 64, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<unsigned long long> hv(16 + 2 * M16_PROF_CTAS);
+    CK(cudaMemcpyAsync(hv.data(), prof.p, hv.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+    const unsigned long long* h = hv.data();
+    if (h[9])
+      std::fprintf(stderr, "[hmgpu] m16 phase 2, CTA 0: %.4g cycles in %.4g ms -> SM clock %.0f MHz\n",
+                   (double)h[8], h[9] * 1e-6, (double)h[8] / (double)h[9] * 1e3);
+    // per-CTA loop cycles next to the plan's per-CTA cost terms
+    // (HMGPU_M16_PROF_FILE): pass, CTA, cycles, bytes, DMMA steps, items, stages
+    if (const char* pf = std::getenv("HMGPU_M16_PROF_FILE")) {
+      if (FILE* f = std::fopen(pf, "w")) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const std::vector<std::array<long long, 4>>& cost = pass ? c->p16_zcost : c->p16_ycost;
+          for (size_t b = 0; b < cost.size() && b < (size_t)M16_PROF_CTAS; ++b)
+            std::fprintf(f, "%d %zu %llu %lld %lld %lld %lld\n", pass, b,
+                         h[16 + pass * M16_PROF_CTAS + b], cost[b][0], cost[b][1], cost[b][2],
+                         cost[b][3]);
+        }
+        std::fclose(f);
+      }
+    }
     std::fprintf(stderr, "[hmgpu] m16 cycles (sum over warps): z consumer wait %.3g work %.3g, "
                  "producer wait %.3g issue %.3g; y consumer wait %.3g work %.3g, producer "
                  "wait %.3g issue %.3g\n", (double)h[0], (double)h[1], (double)h[2], (double)h[3],
@@ -4514,6 +4596,45 @@ int hmgpu_dmma_peak(int device, double* tflops) {
   if (e != cudaSuccess) return HMGPU_ERR_CUDA;
   const double flops = 512.0 * 8.0 * iters * (double)grid * 8.0;  // 8 warps per CTA
   *tflops = flops / (best * 1e-3) / 1e12;
+  return HMGPU_OK;
+}
+
+int hmgpu_dmma_peak_sustained(int device, double seconds, double* tflops) {
+  if (!tflops || !(seconds >= 0.2 && seconds <= 10.0)) return HMGPU_ERR_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return HMGPU_ERR_NODEVICE;
+  if (device < 0 || device >= count) return HMGPU_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return HMGPU_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return HMGPU_ERR_OOM;
+  const int grid = sms * 8, iters = 1 << 12, batch = 8;
+  const double flops = 512.0 * 8.0 * iters * (double)grid * 8.0;  // per launch
+  cudaEvent_t ev[3];
+  for (auto& e : ev) cudaEventCreate(&e);
+  dmma_peak_kernel<<<grid, 256>>>(out, 64);  // warm-up
+  // batches of launches until `seconds` have passed; the rate of the second half
+  std::vector<float> ms;
+  double total = 0.0;
+  while (total < seconds * 1e3 && ms.size() < 100000) {
+    cudaEventRecord(ev[0]);
+    for (int r = 0; r < batch; ++r) dmma_peak_kernel<<<grid, 256>>>(out, iters);
+    cudaEventRecord(ev[1]);
+    if (cudaEventSynchronize(ev[1]) != cudaSuccess) break;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[0], ev[1]);
+    ms.push_back(t);
+    total += t;
+  }
+  const cudaError_t e = cudaGetLastError();
+  for (auto& v : ev) cudaEventDestroy(v);
+  cudaFree(out);
+  if (e != cudaSuccess || ms.empty()) return HMGPU_ERR_CUDA;
+  double t2 = 0.0;
+  const size_t h = ms.size() / 2;
+  for (size_t q = h; q < ms.size(); ++q) t2 += ms[q];
+  *tflops = flops * batch * (double)(ms.size() - h) / (t2 * 1e-3) / 1e12;
   return HMGPU_OK;
 }
 

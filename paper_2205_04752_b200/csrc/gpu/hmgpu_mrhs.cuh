@@ -55,6 +55,8 @@ constexpr int M16_NW = 8;       // consumer warps per CTA
 constexpr int M16_NT = 32 * (M16_NW + 1);  // + one producer warp
 constexpr int M16_HDR = 16;     // doubles of stage header (descriptors)
 constexpr int M16_XPAD = 256;   // zero columns after the last gathered column
+constexpr int M16_PROF_CTAS = 1024;  // per-CTA cycle slots of the dbg-3 profile (per pass)
+constexpr int M16_SLACK = 128;  // doubles of shared memory after the ring (tail over-reads)
 
 // smallest pitch >= n, multiple of 4, = 4 or 12 mod 16 (conflict-free DMMA
 // fragment loads, 16-byte aligned rows)
@@ -161,6 +163,14 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
+// L2 prefetch of a streamed range (A/B: HMGPU_M16_PF = stages ahead of the ring)
+#ifndef HMGPU_M16_PF
+#define HMGPU_M16_PF 0
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // D = A B + D, A 8x4 (row), B 4x8 (col), fp64; lane (g = lane/4, t = lane%4)
 // holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1]
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -200,6 +210,10 @@ __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* 
   // stage's data sees finite values (previous stages or zero), so fragment
   // loads past a segment's end may run unpredicated when A is zero
   for (int e = threadIdx.x; e < NS * stage; e += blockDim.x) sm[e] = 0.0;
+  // the zero fill (generic proxy) is ordered before the first bulk copies
+  // (async proxy) into the ring; later refills of a slot follow the
+  // consumers' reads through the empty mbarrier and need no proxy fence
+  fence_proxy_async();
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -264,23 +278,22 @@ __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t*
 // ---------------------------------------------------------------------------
 // phase 1
 __device__ __forceinline__ void z16_issue(const M16Params& P, double* st, uint64_t* bar,
-                                          const ZChunk16& ch, const ZChunk16* gch, int lane) {
+                                          const ZChunk16& ch, const ZChunk16* gch, int lane,
+                                          uint64_t pol_stream, uint64_t pol_keep) {
   if (lane != 0) return;
   const bool hdr = P.dbg == 2;  // A/B: descriptors only (compute on stale data)
   const uint32_t vb = hdr ? 0u : (uint32_t)ch.vlen * 8u, xb = hdr ? 0u : (uint32_t)ch.P * XP * 8u;
-  fence_proxy_async();
   mbar_expect_tx(bar, 32u + 80u + vb + xb);
   bulk_g2s(st, gch, 32u, bar);
   bulk_g2s(st + 4, P.tasks + ch.task, 80u, bar);
-  if (vb) bulk_g2s_hint(st + M16_HDR, P.arena + ch.vsrc, vb, bar, l2_policy(false));
+  if (vb) bulk_g2s_hint(st + M16_HDR, P.arena + ch.vsrc, vb, bar, pol_stream);
   if (xb)
-    bulk_g2s_hint(st + M16_HDR + ch.vlen, P.xp + (long long)ch.xcol * XP, xb, bar,
-                  l2_policy(true));
+    bulk_g2s_hint(st + M16_HDR + ch.vlen, P.xp + (long long)ch.xcol * XP, xb, bar, pol_keep);
 }
 
 // NW consumer warps (+ one producer warp)
 template <int NS, int NW>
-__global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 2) hmv16_z_kernel(M16Params P) {
+__global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)) hmv16_z_kernel(M16Params P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -297,10 +310,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 2) hmv16_z_kernel
   int zdst[3] = {-1, -1, -1};  // its Z row * ZP + part * 16 (-1: padding row)
   ZChunk16 nxt{};
   if (warp == NW && n > 0) nxt = chunks[c0];
+  const uint64_t pol_stream = l2_policy(false), pol_keep = l2_policy(true);
   auto issue = [&](double* st, uint64_t* bar, int j) {
     const ZChunk16 cur = nxt;
     if (j + 1 < n) nxt = chunks[c0 + j + 1];
-    z16_issue(P, st, bar, cur, chunks + c0 + j, lane);
+    z16_issue(P, st, bar, cur, chunks + c0 + j, lane, pol_stream, pol_keep);
+    if (HMGPU_M16_PF > 0 && lane == 0 && j + HMGPU_M16_PF < n) {
+      const ZChunk16 pf = chunks[c0 + j + HMGPU_M16_PF];
+      if (pf.vlen > 0) bulk_prefetch_l2(P.arena + pf.vsrc, (uint32_t)pf.vlen * 8u);
+    }
   };
   auto compute = [&](double* st) {
     const ZChunk16& ch = *reinterpret_cast<const ZChunk16*>(st);
@@ -361,7 +379,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 2) hmv16_z_kernel
       }
     }
   };
+  const bool tm = P.dbg == 3 && P.prof && threadIdx.x == 0;
+  const long long ck0 = tm ? clock64() : 0;
   stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof);
+  if (tm && blockIdx.x < M16_PROF_CTAS)
+    P.prof[16 + M16_PROF_CTAS + blockIdx.x] = (unsigned long long)(clock64() - ck0);
 }
 
 // ---------------------------------------------------------------------------
@@ -369,24 +391,20 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 2) hmv16_z_kernel
 // issue one phase-2 stage whose records the producer warp holds: the stage
 // (every lane) and its first 32 copies (lane q: copy q)
 __device__ __forceinline__ void y16_issue(const M16Params& P, double* st, uint64_t* bar,
-                                          const M16Stage& d, const M16Copy& mine, int lane) {
+                                          const M16Stage& d, const M16Copy& mine, int lane,
+                                          uint64_t pol_stream, uint64_t pol_keep) {
   const bool hdr = P.dbg == 2;  // A/B: the item records only (compute on stale data)
-  if (lane == 0) {
-    fence_proxy_async();
+  if (lane == 0)
     mbar_expect_tx(bar, hdr ? (uint32_t)(64 * (1 + d.nitems)) : (uint32_t)d.bytes);
-  }
   __syncwarp();
   const int nc = hdr ? 1 : d.ncopies;  // copy 0 is the item records
-  if (lane < nc) {
-    fence_proxy_async();
+  if (lane < nc)
     bulk_g2s_hint(st + (mine.dst & M16_DST_MASK), reinterpret_cast<const void*>(mine.src),
-                  (uint32_t)mine.bytes, bar, l2_policy(mine.dst & M16_KEEP));
-  }
+                  (uint32_t)mine.bytes, bar, (mine.dst & M16_KEEP) ? pol_keep : pol_stream);
   for (int q = lane + 32; q < nc; q += 32) {
     const M16Copy cp = P.copies[d.cbeg + q];
-    fence_proxy_async();
     bulk_g2s_hint(st + (cp.dst & M16_DST_MASK), reinterpret_cast<const void*>(cp.src),
-                  (uint32_t)cp.bytes, bar, l2_policy(cp.dst & M16_KEEP));
+                  (uint32_t)cp.bytes, bar, (cp.dst & M16_KEEP) ? pol_keep : pol_stream);
   }
 }
 
@@ -401,6 +419,9 @@ __device__ __forceinline__ void y16_adm(const double* sU, int PR, const double* 
   const double* zr = sZ + t * ZP + g;
 #pragma unroll 2
   for (int l0 = lo; l0 < hi; l0 += 4) {
+    // rows past hi are loaded and dropped (cheaper than a predicated load):
+    // they lie at most 3 PR + 64 doubles past the piece, inside the item's Z
+    // rows plus the M16_SLACK doubles the launch allocates after the ring
     const double u = ur[0];
     const double a = l0 + t < hi ? u : 0.0;
 #pragma unroll
@@ -451,7 +472,9 @@ __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int
     const int j = j0 + t;
     const bool ok = j < d.jd;
     const double* xr = sX + j * XP;
-    const double* dr = sD + j * PD;
+    // columns past the group read column 0 (their A is zeroed): a group
+    // at the end of the last slot must not read past the ring
+    const double* dr = sD + (ok ? j : 0) * PD;
     double a[6];
 #pragma unroll
     for (int cc = 0; cc < 6; ++cc) {
@@ -470,12 +493,18 @@ __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int
   }
 }
 
-// Leaves of at most 64 rows (8 row tiles).  NW = 8 consumer warps: warp w
-// takes row tile w with both RHS halves, or, for leaves of at most 32 rows,
-// row tile w % 4 with RHS half w / 4.  NW = 16: row tile w % 8, RHS half
-// w / 8 (or, for leaves of at most 32 rows, the 8 spare warps idle).
+// Leaves of at most 64 rows (8 row tiles of 8 rows).  The plan picks the
+// number of consumer warps NW from the leaves' row tiles RT so that no warp
+// idles through a leaf (a 48-row leaf keeps 6 of 8 warps busy: a quarter of
+// the consumer issue slots was spent waiting): NW = RT with both RHS halves
+// per warp, or, for leaves of at most NW / 2 row tiles, row tile w % (NW / 2)
+// with RHS half w / (NW / 2).  NW <= 6 runs 4 CTAs per SM (smaller stages),
+// NW = 8 three.  NW = 16: row tile w % 8, RHS half w / 8 (one CTA per SM,
+// measured slower).
+template <int NW>
+constexpr int y16_ctas_per_sm() { return NW == 16 ? 1 : (NW == 8 ? 3 : 4); }
 template <int NS, int NW>
-__global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 1) hmv16_y_kernel(M16Params P) {
+__global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_kernel(M16Params P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -495,13 +524,23 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 1) hmv16_y_kernel
     if (n > 1) rec1 = stages[c0 + 1];
     if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
   }
+  const uint64_t pol_stream = l2_policy(false), pol_keep = l2_policy(true);
   auto issue = [&](double* st, uint64_t* bar, int j) {
     const M16Stage cur = rec0;
     const M16Copy mine = cp0;
     rec0 = rec1;
     if (j + 1 < n && lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
     if (j + 2 < n) rec1 = stages[c0 + j + 2];
-    y16_issue(P, st, bar, cur, mine, lane);
+    y16_issue(P, st, bar, cur, mine, lane, pol_stream, pol_keep);
+    if (HMGPU_M16_PF > 0 && j + HMGPU_M16_PF < n) {
+      const M16Stage pf = stages[c0 + j + HMGPU_M16_PF];
+      for (int q = lane; q < pf.ncopies; q += 32) {
+        const M16Copy cp = P.copies[pf.cbeg + q];
+        // streamed data only: the kept x rows / Z are L2 residents already
+        if (!(cp.dst & M16_KEEP) && q > 0)
+          bulk_prefetch_l2(reinterpret_cast<const void*>(cp.src), (uint32_t)cp.bytes);
+      }
+    }
   };
   auto compute = [&](double* st) {
     const int nit = *reinterpret_cast<const int*>(st);
@@ -509,16 +548,17 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 1) hmv16_y_kernel
     for (int it = 0; it < nit; ++it) {
     const YItem16& d = items[it];
     const int RT = (d.R + 7) >> 3;
-    const bool split = NW == 16 || RT <= 4;
-    const int rt = NW == 16 ? (warp & 7) : (split ? (warp & 3) : warp);
-    const int h0 = NW == 16 ? (warp >> 3) : (split ? (warp >> 2) : 0);
+    constexpr int HS = NW == 16 ? 8 : NW / 2;  // row tiles in split mode
+    const bool split = NW == 16 || RT <= HS;
+    const int rt = split ? warp % HS : warp;
+    const int h0 = split ? warp / HS : 0;
     if (d.flags & 1) {
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int h = 0; h < 2; ++h) acc[r][h][0] = acc[r][h][1] = 0.0;
     }
-    if (rt < RT) {  // warp-uniform
+    if (rt < RT && h0 < 2) {  // warp-uniform
       if (split) y16_item<1>(d, st, rt, 8 * h0, g, t, acc);
       else y16_item<2>(d, st, rt, 0, g, t, acc);
       if (d.flags & 2) {  // the leaf is complete: y rows, external order
@@ -544,8 +584,27 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : 1) hmv16_y_kernel
     }
     }
   };
+  // A/B (dbg 3): SM cycles of every CTA's stage loop (balance of the plan)
+  // and nanoseconds of CTA 0's -> the SM clock the sweep runs at
+  const bool tm = P.dbg == 3 && P.prof && threadIdx.x == 0;
+  long long ck0 = 0;
+  unsigned long long ns0 = 0;
+  if (tm) {
+    ck0 = clock64();
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ns0));
+  }
   stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg,
                      P.prof ? P.prof + 4 : nullptr);
+  if (tm) {
+    unsigned long long ns1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ns1));
+    const unsigned long long cyc = (unsigned long long)(clock64() - ck0);
+    if (blockIdx.x < M16_PROF_CTAS) P.prof[16 + blockIdx.x] = cyc;
+    if (blockIdx.x == 0) {
+      P.prof[8] = cyc;
+      P.prof[9] = ns1 - ns0;
+    }
+  }
 }
 
 // fp64 tensor-core peak probe: eight independent DMMA chains per warp

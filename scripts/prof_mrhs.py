@@ -19,4 +19,8 @@ names = ["gather", "hmv16_z", "hmv16_leaf", "pack16"]
 for k in names:
     ms, n = h.kernel_times(k, reset=True)
     print(f"{k:12s} {ms / max(n, 1) * 1:.3f} ms/launch  ({n} launches)")
+y0 = h.matvec(np.ascontiguousarray(X[:, 0]))
+err = np.linalg.norm(Y[:, 0] - y0) / np.linalg.norm(y0)
+print(f"col 0 vs 1-RHS sweep: rel {err:.2e}")
+assert err < 1e-12
 print("ok")
