@@ -515,8 +515,8 @@ struct hmgpu_ctx {
   int p16_mode = -1;
   int p16_ns = 2, p16_stage = 0, p16_ncta = 0;
   int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8, p16_ynw = 8;
-  // per-CTA cost terms of the plan (bytes, DMMA steps per warp, items, stages)
-  std::vector<std::array<long long, 4>> p16_ycost, p16_zcost;
+  int p16_zunits = 0, p16_yunits = 0;  // dynamically scheduled work units per pass
+  DBuf<int> d_m16ctr;                  // their hand-out counters (phase 1, phase 2)
   long long p16_zsize = 0, p16_alen = 0;
   int n_zch16 = 0, n_yst16 = 0;
   DBuf<ZChunk16> d_zch16;
@@ -572,7 +572,7 @@ struct hmgpu_ctx {
     d_xi.free(); d_ypart.free();
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
-    d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free();
+    d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free(); d_m16ctr.free();
     d_yitem16.free(); d_ycopy16.free();
     d_z16buf.free(); d_xp16.free(); d_ablocks.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
@@ -1970,35 +1970,6 @@ M16Cfg m16_cfg() {
   return cfg;
 }
 
-// contiguous runs of work units over ncta CTAs with about equal bytes:
-// first[k] = first unit of CTA k, first[ncta] = number of units
-std::vector<int> split_runs(const std::vector<long long>& bytes, int ncta) {
-  long long total = 0;
-  for (long long b : bytes) total += b;
-  const double share = std::max(1.0, (double)total / ncta);
-  std::vector<int> first(ncta + 1, 0);
-  long long cum = 0;
-  int k = 0;
-  for (size_t u = 0; u < bytes.size(); ++u) {
-    const int owner =
-        (int)std::min<double>(ncta - 1, std::floor((cum + 0.5 * bytes[u]) / share));
-    while (k < owner) first[++k] = (int)u;
-    cum += bytes[u];
-  }
-  while (k < ncta) first[++k] = (int)bytes.size();
-  return first;
-}
-
-// DMMA instructions one consumer warp issues for a phase-2 piece (both RHS
-// halves): the plan's cost term of a leaf
-long long y16_steps(const YStage16& d) {
-  if (d.kind == Y16_DENSE) return (long long)((d.jd + 3) / 4) * 18;
-  static const int w[6] = {2, 4, 4, 2, 4, 2};  // diagonal components: Z only
-  long long n = 0;
-  for (int q = 0; q < 6; ++q) n += (long long)((d.hi[q] - d.lo[q] + 3) / 4) * w[q];
-  return n;
-}
-
 // Multi-RHS plan: phase-1 tasks (block, <= 64 l of its components) with
 // their column chunks, phase-2 stages per leaf, the p16 arena (current-rank
 // factors re-packed in stage order, zero padded to the conflict-free
@@ -2269,15 +2240,34 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   const int zcta_sm = std::max(1, std::min(cfg.znw == 8 ? 3 : (cfg.znw == 6 ? 4 : 2),
                                            (int)((227 * 1024) / (zring_bytes + 1024))));
   const int nctaz = c->sm_count * zcta_sm;
-  std::vector<int> zcoff(nctaz + 1), ycoff(ncta + 1);
+  // work units handed out dynamically (hmgpu_mrhs.cuh UnitCursor): phase 1 a
+  // run of consecutive tasks of >= M16_UNIT_BYTES, phase 2 a run of
+  // consecutive leaves of >= M16_UNIT_BYTES (a leaf's accumulators live in
+  // one CTA); the units go out in order, so the CTAs work on a window of
+  // neighbouring leaves at any time and the Z of the blocks above them is
+  // read from L2 by all of them.  zcoff / ycoff: first stage of each unit;
+  // the entry after the last unit is the END stage both passes append.
+  constexpr long long M16_UNIT_BYTES = 96 * 1024 / 8;  // doubles
+  std::vector<int> zcoff, ycoff;
   std::vector<M16Stage> ystages;
   std::vector<YItem16> yitems;
   std::vector<M16Copy> ycopies;
   std::vector<unsigned char> ckind;  // copy source: 0 items, 1 p16 arena, 2 Z, 3 dense, 4 x
   {
-    const std::vector<int> ft = split_runs(tbytes, nctaz);
-    for (int k = 0; k <= nctaz; ++k) zcoff[k] = tptr[ft[k]];
-    const std::vector<int> fl = split_runs(lbytes, ncta);
+    {
+      long long acc = 0;
+      for (size_t ti = 0; ti < tbytes.size(); ++ti) {
+        if (ti == 0 || acc >= M16_UNIT_BYTES) {
+          zcoff.push_back(tptr[ti]);
+          acc = 0;
+        }
+        acc += tbytes[ti];
+      }
+      zcoff.push_back((int)zch.size());  // = END chunk
+      ZChunk16 end{};
+      end.flags = 4;
+      zch.push_back(end);
+    }
     const int SD2 = cfg.stage - Y16_HDR;
     auto plen = [](const YStage16& d) -> long long {
       return d.kind == Y16_ADM ? (long long)d.len + d.len2 : (long long)d.jd * d.PR + d.len2;
@@ -2288,44 +2278,25 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       ycopies.push_back(M16Copy{(unsigned long long)src_bytes, (int)dst | keep, (int)bytes});
       ckind.push_back((unsigned char)kind);
     };
-    // leaves per CTA: contiguous runs of about equal bytes, or (default)
-    // cyclic -- leaf i on CTA i mod ncta, so the CTAs work on a window of
-    // neighbouring leaves at any time and the Z of the blocks above them is
-    // read from L2 by all of them (HMGPU_M16_YORDER=runs for the runs)
-    static const bool yruns = [] {
-      const char* e = std::getenv("HMGPU_M16_YORDER");
-      return e && std::string(e) == "runs";
-    }();
-    std::vector<std::vector<int>> cleaves(ncta);
-    for (int k = 0; k < ncta; ++k)
-      if (yruns)
-        for (int L = fl[k]; L < fl[k + 1]; ++L) cleaves[k].push_back(L);
-    if (!yruns)
-      for (int L = 0; L < nl; ++L) cleaves[L % ncta].push_back(L);
-    std::vector<int> cpieces;
-    c->p16_ycost.assign(ncta, {0, 0, 0, 0});
-    c->p16_zcost.assign(nctaz, {0, 0, 0, 0});
-    for (int k = 0; k < nctaz; ++k)
-      for (int ti = ft[k]; ti < ft[k + 1]; ++ti) {
-        const int tw = (tasks[ti].ntiles + cfg.znw - 1) / cfg.znw;  // m-tiles of the busiest warp
-        for (int q = tptr[ti]; q < tptr[ti + 1]; ++q) {
-          c->p16_zcost[k][0] += 8LL * (zch[q].vlen + (long long)zch[q].P * XP);
-          c->p16_zcost[k][1] += (long long)(zch[q].P / 4) * 2 * tw;
-          c->p16_zcost[k][3] += 1;
+    std::vector<std::vector<int>> cleaves;  // leaves of each unit
+    {
+      long long acc = 0;
+      for (int L = 0; L < nl; ++L) {
+        if (L == 0 || acc >= M16_UNIT_BYTES) {
+          cleaves.emplace_back();
+          acc = 0;
         }
-        c->p16_zcost[k][2] += 1;
+        cleaves.back().push_back(L);
+        acc += lbytes[L];
       }
-    for (int k = 0; k < ncta; ++k) {
-      ycoff[k] = (int)ystages.size();
+    }
+    const int nunits = (int)cleaves.size();
+    std::vector<int> cpieces;
+    for (int k = 0; k < nunits; ++k) {
+      ycoff.push_back((int)ystages.size());
       cpieces.clear();
       for (int L : cleaves[k])
         for (int q = lptr[L]; q < lptr[L + 1]; ++q) cpieces.push_back(q);
-      for (int q : cpieces) {
-        const YStage16& d = yst[q];
-        c->p16_ycost[k][0] += 8 * plen(d);
-        c->p16_ycost[k][1] += y16_steps(d);
-        c->p16_ycost[k][2] += 1;
-      }
       const int p1 = (int)cpieces.size();
       for (int pi = 0; pi < p1;) {
         int pe = pi;
@@ -2376,11 +2347,22 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         st.ncopies = (int)ycopies.size() - st.cbeg;
         st.bytes = (int)bytes;
         ystages.push_back(st);
-        c->p16_ycost[k][3] += 1;
         pi = pe;
       }
     }
-    ycoff[ncta] = (int)ystages.size();
+    ycoff.push_back((int)ystages.size());  // = END stage: a count record of -1
+    {
+      M16Stage st{};
+      st.cbeg = (int)ycopies.size();
+      st.ncopies = 1;
+      st.bytes = (int)sizeof(YItem16);
+      YItem16 cnt{};
+      cnt.kind = -1;
+      copy(0, (long long)yitems.size() * (long long)sizeof(YItem16), 0,
+           (long long)sizeof(YItem16));
+      yitems.push_back(cnt);
+      ystages.push_back(st);
+    }
   }
   c->d_zch16.upload(zch, c->stream);
   c->d_ztask16.upload(tasks, c->stream);
@@ -2418,8 +2400,11 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     c->sync();
     d_packs.free();
   }
-  c->n_zch16 = (int)zch.size();
-  c->n_yst16 = (int)ystages.size();
+  c->n_zch16 = (int)zch.size() - 1;  // without the END records
+  c->n_yst16 = (int)ystages.size() - 1;
+  c->p16_zunits = (int)zcoff.size() - 1;
+  c->p16_yunits = (int)ycoff.size() - 1;
+  c->d_m16ctr.ensure(2);
   c->p16_ns = cfg.ns;
   c->p16_stage = cfg.stage;
   c->p16_ncta = ncta;
@@ -2434,10 +2419,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_valid = true;
   c->sync();
   if (verbose())
-    std::fprintf(stderr, "[hmgpu] plan16: tasks=%zu chunks=%zu stages=%zu arena=%.3f GB "
-                         "Z=%.3f GB ctas=%d ring=%zu B\n",
-                 tasks.size(), zch.size(), ystages.size(), 8.0 * alen / 1e9, 8.0 * zsize / 1e9,
-                 ncta, ring_bytes);
+    std::fprintf(stderr, "[hmgpu] plan16: tasks=%zu chunks=%zu (units %d) stages=%zu (units %d) "
+                         "arena=%.3f GB Z=%.3f GB ctas=%d/%d warps=%d/%d ring=%zu B\n",
+                 tasks.size(), zch.size(), c->p16_zunits, ystages.size(), c->p16_yunits,
+                 8.0 * alen / 1e9, 8.0 * zsize / 1e9, nctaz, ncta, cfg.znw, cfg.ynw, ring_bytes);
 }
 
 template <int NS, int NW = 8>
@@ -2445,7 +2430,11 @@ void launch_m16(hmgpu_ctx* c, M16Params P) {  // phase 2
   const size_t smem = ((size_t)NS * c->p16_stage + M16_SLACK) * sizeof(double);
   CK(cudaFuncSetAttribute(hmv16_y_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
-  hmv16_y_kernel<NS, NW><<<c->p16_ncta, 32 * (NW + 1), smem, c->stream>>>(P);
+  P.coff = c->d_ycoff16.p;
+  P.nunits = c->p16_yunits;
+  P.ctr = c->d_m16ctr.p + 1;
+  hmv16_y_kernel<NS, NW><<<std::max(1, std::min(c->p16_ncta, c->p16_yunits)), 32 * (NW + 1), smem,
+                           c->stream>>>(P);
   CK(cudaGetLastError());
 }
 template <int NS, int NW>
@@ -2454,7 +2443,11 @@ void launch_m16z(hmgpu_ctx* c, M16Params P) {  // phase 1
   CK(cudaFuncSetAttribute(hmv16_z_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   P.stage = c->p16_zstage;
-  hmv16_z_kernel<NS, NW><<<c->p16_nctaz, 32 * (NW + 1), smem, c->stream>>>(P);
+  P.coff = c->d_zcoff16.p;
+  P.nunits = c->p16_zunits;
+  P.ctr = c->d_m16ctr.p;
+  hmv16_z_kernel<NS, NW><<<std::max(1, std::min(c->p16_nctaz, c->p16_zunits)), 32 * (NW + 1), smem,
+                           c->stream>>>(P);
   CK(cudaGetLastError());
 }
 
@@ -2486,6 +2479,7 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
     const int nr = std::min(MR, nrhs - s0);
     P.s0 = s0;
     P.nr = nr;
+    CK(cudaMemsetAsync(c->d_m16ctr.p, 0, 2 * sizeof(int), c->stream));
     c->timed("gather", [&] {
       const long long total = 48LL * c->n_cols;
       gather16_kernel<<<grid_for(c, (total + 255) / 256, 16), 256, 0, c->stream>>>(
@@ -2536,16 +2530,13 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
     if (h[9])
       std::fprintf(stderr, "[hmgpu] m16 phase 2, CTA 0: %.4g cycles in %.4g ms -> SM clock %.0f MHz\n",
                    (double)h[8], h[9] * 1e-6, (double)h[8] / (double)h[9] * 1e3);
-    // per-CTA loop cycles next to the plan's per-CTA cost terms
-    // (HMGPU_M16_PROF_FILE): pass, CTA, cycles, bytes, DMMA steps, items, stages
+    // per-CTA loop cycles (HMGPU_M16_PROF_FILE): pass (0 phase 2, 1 phase 1), CTA, cycles
     if (const char* pf = std::getenv("HMGPU_M16_PROF_FILE")) {
       if (FILE* f = std::fopen(pf, "w")) {
         for (int pass = 0; pass < 2; ++pass) {
-          const std::vector<std::array<long long, 4>>& cost = pass ? c->p16_zcost : c->p16_ycost;
-          for (size_t b = 0; b < cost.size() && b < (size_t)M16_PROF_CTAS; ++b)
-            std::fprintf(f, "%d %zu %llu %lld %lld %lld %lld\n", pass, b,
-                         h[16 + pass * M16_PROF_CTAS + b], cost[b][0], cost[b][1], cost[b][2],
-                         cost[b][3]);
+          const int n = std::min(M16_PROF_CTAS, pass ? c->p16_nctaz : c->p16_ncta);
+          for (int b = 0; b < n; ++b)
+            std::fprintf(f, "%d %d %llu\n", pass, b, h[16 + pass * M16_PROF_CTAS + b]);
         }
         std::fclose(f);
       }

@@ -70,7 +70,7 @@ struct __align__(16) ZChunk16 {  // phase-1 stage (32 B)
   int xcol;        // first gathered column of the chunk
   int P;           // pitch = staged X rows
   int task;
-  int flags;       // 1 first chunk of the task, 2 last
+  int flags;       // 1 first chunk of the task, 2 last, 4 END stage (no data)
   int pad;
 };
 static_assert(sizeof(ZChunk16) == 32, "ZChunk16 layout");
@@ -129,7 +129,9 @@ struct M16Params {
   const void* desc;          // ZChunk16[] (phase 1) or M16Stage[] (phase 2)
   const M16Copy* copies;     // phase 2
   const ZTask16* tasks;
-  const int* coff;           // stages of CTA b: [coff[b], coff[b + 1])
+  const int* coff;           // stages of work unit u: [coff[u], coff[u + 1])
+  int nunits;                // work units; stage coff[nunits] is the END stage
+  int* ctr;                  // next unit to hand out (zeroed before the launch)
   const double* arena;       // p16 arena
   const double* dense;
   const double* xp;
@@ -161,14 +163,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
-}
-
-// L2 prefetch of a streamed range (A/B: HMGPU_M16_PF = stages ahead of the ring)
-#ifndef HMGPU_M16_PF
-#define HMGPU_M16_PF 0
-#endif
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // D = A B + D, A 8x4 (row), B 4x8 (col), fp64; lane (g = lane/4, t = lane%4)
@@ -225,30 +219,34 @@ __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* 
 }
 
 // Stage loop shared by both passes: a producer warp (the CTA's last) issues
-// stage j into slot j % NS as soon as every consumer warp released the
-// slot's previous stage, running up to NS stages ahead; the consumer warps
-// wait for each stage's bytes, compute, and release the slot.  issue(slot,
-// bar, j) loads the records of stage j + 1 after issuing stage j, so their
-// latency overlaps the wait for the next free slot.
+// stage after stage into the ring as soon as every consumer warp released
+// the slot's previous stage; the consumer warps wait for each stage's bytes,
+// compute, and release the slot.  Work is handed out dynamically: the
+// producer pulls work units (runs of stages: a leaf's stages in phase 2, a
+// few tasks' chunks in phase 1) from a global counter, so a CTA that shares
+// its SM with slower neighbours simply takes fewer units (static shares left
+// the CTAs between 74 % and 84 % busy on average); the consumers learn the
+// end from an END stage the producer issues last.  issue(slot, bar) returns
+// false after it issued the END stage, compute(slot) returns false on it.
 template <int NS, int NW = M16_NW, class ISSUE, class COMPUTE>
 __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t* empty,
-                                           int stage, int n, ISSUE issue,
-                                           COMPUTE compute, int dbg = 0,
-                                           unsigned long long* prof = nullptr) {
+                                           int stage, ISSUE issue, COMPUTE compute,
+                                           int dbg = 0, unsigned long long* prof = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tm = dbg == 3 && prof != nullptr;
   long long t_wait = 0, t_work = 0;
   if (warp == NW) {
-    for (int j = 0; j < n; ++j) {
+    for (int j = 0;; ++j) {
       const int s = j % NS;
       const long long t0 = tm ? clock64() : 0;
       if (j >= NS) mbar_wait(&empty[s], (uint32_t)(((j / NS) - 1) & 1));
       const long long t1 = tm ? clock64() : 0;
-      issue(sm + (long long)s * stage, &full[s], j);  // prefetches stage j + 1's records
+      const bool more = issue(sm + (long long)s * stage, &full[s]);
       if (tm) {
         t_wait += t1 - t0;
         t_work += clock64() - t1;
       }
+      if (!more) break;
     }
     if (tm && lane == 0) {
       atomicAdd(prof + 2, (unsigned long long)t_wait);
@@ -256,24 +254,69 @@ __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t*
     }
     return;
   }
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0;; ++i) {
     const int s = i % NS;
     const long long t0 = tm ? clock64() : 0;
     mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
     const long long t1 = tm ? clock64() : 0;
-    if (dbg != 1) compute(sm + (long long)s * stage);
+    const bool more = compute(sm + (long long)s * stage);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tm) {
       t_wait += t1 - t0;
       t_work += clock64() - t1;
     }
+    if (!more) break;
   }
   if (tm && lane == 0) {
     atomicAdd(prof + 0, (unsigned long long)t_wait);
     atomicAdd(prof + 1, (unsigned long long)t_work);
   }
 }
+
+// The producer's cursor over the stage sequence of the units it pulls: the
+// current unit's remaining stages [q, qend) and the next unit's range,
+// fetched one unit ahead so that neither the atomic nor the loads of the
+// unit's bounds sit on the issue path.  next() returns the following stage
+// index, or the END stage index once the units are exhausted (and keeps
+// returning it).
+struct UnitCursor {
+  const int* ub;
+  int* ctr;
+  int nunits, end;
+  int q, qend, nq, nqend;
+  __device__ __forceinline__ void fetch() {  // next unit -> (nq, nqend), all lanes alike
+    int u = 0;
+    if ((threadIdx.x & 31) == 0) u = atomicAdd(ctr, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < nunits) {
+      nq = ub[u];
+      nqend = ub[u + 1];
+    } else {
+      nq = nqend = end;
+    }
+  }
+  __device__ __forceinline__ void init(const int* ub_, int* ctr_, int nunits_) {
+    ub = ub_;
+    ctr = ctr_;
+    nunits = nunits_;
+    end = ub_[nunits_];
+    fetch();
+    q = nq;
+    qend = nqend;
+    fetch();
+  }
+  __device__ __forceinline__ int next() {
+    while (q >= qend) {  // unit done (or empty): on to the prefetched one
+      if (q >= end) return end;
+      q = nq;
+      qend = nqend;
+      if (q >= end) return end;
+      fetch();
+    }
+    return q++;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // phase 1
@@ -300,28 +343,36 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
   const int g = lane >> 2, t = lane & 3;
   ring_init<NS, NW>(sm, full, empty, P.stage);
   const ZChunk16* chunks = static_cast<const ZChunk16*>(P.desc);
-  const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
-  // m-tiles warp, warp + 8, warp + 16 of the task; their rows are resolved
+  // m-tiles warp, warp + NW, warp + 2 NW of the task; their rows are resolved
   // once per task (the task's first chunk) and kept in registers
   double acc[3][2][2];
   int ntl = 0;                 // this warp's m-tiles in the task
   int arow[3] = {0, 0, 0};     // this lane's row in the staged V^T (its tile's)
   int xcol[3] = {0, 0, 0};     // its operand group r: x columns 16 r ..
   int zdst[3] = {-1, -1, -1};  // its Z row * ZP + part * 16 (-1: padding row)
+  // producer: the chunk to issue (index i0, record nxt) and the one after
+  UnitCursor cur{};
   ZChunk16 nxt{};
-  if (warp == NW && n > 0) nxt = chunks[c0];
+  int i0 = 0;
+  if (warp == NW) {
+    cur.init(P.coff, P.ctr, P.nunits);
+    i0 = cur.next();
+    nxt = chunks[i0];
+  }
   const uint64_t pol_stream = l2_policy(false), pol_keep = l2_policy(true);
-  auto issue = [&](double* st, uint64_t* bar, int j) {
-    const ZChunk16 cur = nxt;
-    if (j + 1 < n) nxt = chunks[c0 + j + 1];
-    z16_issue(P, st, bar, cur, chunks + c0 + j, lane, pol_stream, pol_keep);
-    if (HMGPU_M16_PF > 0 && lane == 0 && j + HMGPU_M16_PF < n) {
-      const ZChunk16 pf = chunks[c0 + j + HMGPU_M16_PF];
-      if (pf.vlen > 0) bulk_prefetch_l2(P.arena + pf.vsrc, (uint32_t)pf.vlen * 8u);
+  auto issue = [&](double* st, uint64_t* bar) -> bool {
+    const ZChunk16 ch = nxt;
+    const int i = i0;
+    if (i != cur.end) {
+      i0 = cur.next();
+      nxt = chunks[i0];
     }
+    z16_issue(P, st, bar, ch, chunks + i, lane, pol_stream, pol_keep);
+    return i != cur.end;
   };
-  auto compute = [&](double* st) {
+  auto compute = [&](double* st) -> bool {
     const ZChunk16& ch = *reinterpret_cast<const ZChunk16*>(st);
+    if (ch.flags & 4) return false;  // END stage
     const ZTask16& tk = *reinterpret_cast<const ZTask16*>(st + 4);
     const double* sV = st + M16_HDR;
     const double* sX = sV + ch.vlen;
@@ -378,10 +429,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
         *reinterpret_cast<double2*>(zr + 8) = make_double2(acc[q][1][0], acc[q][1][1]);
       }
     }
+    return true;
   };
   const bool tm = P.dbg == 3 && P.prof && threadIdx.x == 0;
   const long long ck0 = tm ? clock64() : 0;
-  stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg, P.prof);
+  stage_loop<NS, NW>(sm, full, empty, P.stage, issue, compute, P.dbg, P.prof);
   if (tm && blockIdx.x < M16_PROF_CTAS)
     P.prof[16 + M16_PROF_CTAS + blockIdx.x] = (unsigned long long)(clock64() - ck0);
 }
@@ -511,39 +563,41 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
   const int g = lane >> 2, t = lane & 3;
   ring_init<NS, NW>(sm, full, empty, P.stage);
   const M16Stage* stages = static_cast<const M16Stage*>(P.desc);
-  const int c0 = P.coff[blockIdx.x], n = P.coff[blockIdx.x + 1] - c0;
   double acc[3][2][2];  // [output component][RHS half][pair]
   const long long ndof = 3LL * P.nrows;
-  // producer state: the records of stage j (rec0, its copies cp0) and j + 1
-  // (rec1); issuing stage j loads stage j + 1's copies and stage j + 2's
-  // record, so no load sits on the issue path
+  // producer state: the stage to issue (index i0, record rec0, its copies
+  // cp0) and the one after it (i1, rec1); issuing a stage loads the next
+  // one's copies and the record after that, so no load sits on the issue path
+  UnitCursor cur{};
   M16Stage rec0{}, rec1{};
   M16Copy cp0{};
+  int i0 = 0, i1 = 0;
   if (warp == NW) {
-    if (n > 0) rec0 = stages[c0];
-    if (n > 1) rec1 = stages[c0 + 1];
+    cur.init(P.coff, P.ctr, P.nunits);
+    i0 = cur.next();
+    i1 = cur.next();
+    rec0 = stages[i0];
+    rec1 = stages[i1];
     if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
   }
   const uint64_t pol_stream = l2_policy(false), pol_keep = l2_policy(true);
-  auto issue = [&](double* st, uint64_t* bar, int j) {
-    const M16Stage cur = rec0;
+  auto issue = [&](double* st, uint64_t* bar) -> bool {
+    const M16Stage d = rec0;
     const M16Copy mine = cp0;
+    const bool more = i0 != cur.end;
+    i0 = i1;
     rec0 = rec1;
-    if (j + 1 < n && lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
-    if (j + 2 < n) rec1 = stages[c0 + j + 2];
-    y16_issue(P, st, bar, cur, mine, lane, pol_stream, pol_keep);
-    if (HMGPU_M16_PF > 0 && j + HMGPU_M16_PF < n) {
-      const M16Stage pf = stages[c0 + j + HMGPU_M16_PF];
-      for (int q = lane; q < pf.ncopies; q += 32) {
-        const M16Copy cp = P.copies[pf.cbeg + q];
-        // streamed data only: the kept x rows / Z are L2 residents already
-        if (!(cp.dst & M16_KEEP) && q > 0)
-          bulk_prefetch_l2(reinterpret_cast<const void*>(cp.src), (uint32_t)cp.bytes);
-      }
+    if (more) {
+      if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
+      i1 = cur.next();
+      rec1 = stages[i1];
     }
+    y16_issue(P, st, bar, d, mine, lane, pol_stream, pol_keep);
+    return more;
   };
-  auto compute = [&](double* st) {
+  auto compute = [&](double* st) -> bool {
     const int nit = *reinterpret_cast<const int*>(st);
+    if (nit < 0) return false;  // END stage
     const YItem16* items = reinterpret_cast<const YItem16*>(st) + 1;
     for (int it = 0; it < nit; ++it) {
     const YItem16& d = items[it];
@@ -583,6 +637,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
       }
     }
     }
+    return true;
   };
   // A/B (dbg 3): SM cycles of every CTA's stage loop (balance of the plan)
   // and nanoseconds of CTA 0's -> the SM clock the sweep runs at
@@ -593,7 +648,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
     ck0 = clock64();
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ns0));
   }
-  stage_loop<NS, NW>(sm, full, empty, P.stage, n, issue, compute, P.dbg,
+  stage_loop<NS, NW>(sm, full, empty, P.stage, issue, compute, P.dbg,
                      P.prof ? P.prof + 4 : nullptr);
   if (tm) {
     unsigned long long ns1;
