@@ -517,6 +517,9 @@ struct hmgpu_ctx {
   int p16_zns = 3, p16_zstage = 0, p16_nctaz = 0, p16_znw = 8, p16_ynw = 8;
   int p16_zunits = 0, p16_yunits = 0;  // dynamically scheduled work units per pass
   DBuf<int> d_m16ctr;                  // their hand-out counters (phase 1, phase 2)
+  int p16_nparts = 1;                  // parts per leaf in phase 2 (> 1: partial slices + reduce)
+  int p16_row0 = 0, p16_row1 = 0;      // internal row positions covered by the leaves
+  DBuf<double> d_y16part;              // [part][16 RHS][3][rows] partial slices
   long long p16_zsize = 0, p16_alen = 0;
   int n_zch16 = 0, n_yst16 = 0;
   DBuf<ZChunk16> d_zch16;
@@ -572,7 +575,7 @@ struct hmgpu_ctx {
     d_xi.free(); d_ypart.free();
     d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free();
     d_pentries.free(); d_pleaf_ptr.free();
-    d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free(); d_m16ctr.free();
+    d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free(); d_m16ctr.free(); d_y16part.free();
     d_yitem16.free(); d_ycopy16.free();
     d_z16buf.free(); d_xp16.free(); d_ablocks.free();
     d_row_leaf.free(); d_sortp.free(); d_tix.free(); d_term_bi.free(); d_cnt.free();
@@ -2220,21 +2223,83 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       d.PR = PR;
       yst.push_back(d);
     }
-    yst[first].flags |= 1;
-    yst.back().flags |= 2;
     lbytes.push_back(std::max<long long>(by, 1));
     lptr.push_back((int)yst.size());
   }
+  // A leaf is the unit of the dynamic hand-out, and a pass over few leaves
+  // per CTA ends with CTAs idling for up to a leaf's time (config 3: 6.9
+  // leaves per CTA, the CTAs 93 % busy; config 2: 1.7 and 73 %).  Below 16
+  // units per CTA every leaf's piece list is therefore cut into P parts of
+  // about equal bytes; part p accumulates its own rows into slice p of a
+  // partial buffer and y16_reduce_kernel adds the slices in part order
+  // (deterministic).  P = 1: the leaves write y directly.
+  const size_t ring_bytes = ((size_t)cfg.ns * cfg.stage + M16_SLACK) * sizeof(double);
+  if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
+  const int per_sm = cfg.ynw == 16 ? 1
+                     : std::max(1, std::min(y4 ? 4 : 3, (int)((227 * 1024) / (ring_bytes + 1024))));
+  const int ncta = c->sm_count * per_sm;
+  int nparts = 1;
+  {
+    static const int forced = [] {
+      const char* e = std::getenv("HMGPU_M16_PARTS");
+      return e ? std::atoi(e) : 0;
+    }();
+    long long total = 0;
+    for (long long b : lbytes) total += b;
+    nparts = (int)std::min<long long>(8, (16LL * ncta + nl - 1) / std::max(nl, 1));
+    // parts of at least 128 KB on average
+    nparts = (int)std::min<long long>(nparts, total / std::max(nl, 1) / (128 * 1024 / 8));
+    nparts = std::max(nparts, 1);
+    if (forced >= 1 && forced <= 8) nparts = forced;
+  }
+  {
+    std::vector<YStage16> parts;
+    std::vector<long long> sbytes;
+    std::vector<int> sptr{0};
+    parts.reserve(yst.size() + (size_t)nl * nparts);
+    auto plen0 = [](const YStage16& d) -> long long {
+      return d.kind == Y16_ADM ? (long long)d.len + d.len2 : (long long)d.jd * d.PR + d.len2;
+    };
+    for (int L = 0; L < nl; ++L) {
+      long long total = 0;
+      for (int q = lptr[L]; q < lptr[L + 1]; ++q) total += plen0(yst[q]);
+      long long cum = 0;
+      int q = lptr[L];
+      for (int pt = 0; pt < nparts; ++pt) {
+        const size_t first = parts.size();
+        long long by = 0;
+        // pieces up to the part's share of the bytes (the last part takes the rest)
+        const long long upto = pt == nparts - 1 ? total + 1 : (total * (pt + 1)) / nparts;
+        while (q < lptr[L + 1] && (pt == nparts - 1 || cum + plen0(yst[q]) / 2 < upto)) {
+          cum += plen0(yst[q]);
+          by += plen0(yst[q]);
+          parts.push_back(yst[q++]);
+        }
+        if (parts.size() == first) {  // nothing for this part: its rows are written as 0
+          YStage16 d{};
+          d.kind = Y16_ADM;
+          d.leaf = L;
+          d.R = c->leaf_end[L] - c->leaf_begin[L];
+          d.PR = cf_pitch(d.R);
+          parts.push_back(d);
+        }
+        for (size_t e = first; e < parts.size(); ++e) parts[e].part = pt;
+        parts[first].flags |= 1;
+        parts.back().flags |= 2;
+        sbytes.push_back(std::max<long long>(by, 1));
+        sptr.push_back((int)parts.size());
+      }
+    }
+    yst.swap(parts);
+    lbytes.swap(sbytes);  // from here on per (leaf, part) segment
+    lptr.swap(sptr);
+  }
+  const int nseg = (int)lbytes.size();
 
   // ---- per-CTA runs (up to 3 CTAs per SM, as many as their rings fit):
   // phase 1 by tasks, phase 2 by leaves (a leaf's accumulators live in one
   // CTA); within a CTA's leaves, consecutive pieces are packed into stages
   // of up to Y16_MAXIT items, their records and bulk copies
-  const size_t ring_bytes = ((size_t)cfg.ns * cfg.stage + M16_SLACK) * sizeof(double);
-  const int per_sm = cfg.ynw == 16 ? 1
-                     : std::max(1, std::min(y4 ? 4 : 3, (int)((227 * 1024) / (ring_bytes + 1024))));
-  if (ring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_CFG ring too large");
-  const int ncta = c->sm_count * per_sm;
   const size_t zring_bytes = (size_t)cfg.zns * cfg.zstage * sizeof(double);
   if (zring_bytes + 1024 > 227 * 1024) fail(HMGPU_ERR_INVALID, "HMGPU_M16_ZCFG ring too large");
   const int zcta_sm = std::max(1, std::min(cfg.znw == 8 ? 3 : (cfg.znw == 6 ? 4 : 2),
@@ -2278,10 +2343,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       ycopies.push_back(M16Copy{(unsigned long long)src_bytes, (int)dst | keep, (int)bytes});
       ckind.push_back((unsigned char)kind);
     };
-    std::vector<std::vector<int>> cleaves;  // leaves of each unit
+    std::vector<std::vector<int>> cleaves;  // (leaf, part) segments of each unit
     {
       long long acc = 0;
-      for (int L = 0; L < nl; ++L) {
+      for (int L = 0; L < nseg; ++L) {
         if (L == 0 || acc >= M16_UNIT_BYTES) {
           cleaves.emplace_back();
           acc = 0;
@@ -2325,6 +2390,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           it.jd = d.jd;
           it.m = d.m;
           it.roff = d.roff;
+          it.part = d.part;
           std::copy(d.lo, d.lo + 6, it.lo);
           std::copy(d.hi, d.hi + 6, it.hi);
           it.off1 = (int)off;
@@ -2405,6 +2471,17 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_zunits = (int)zcoff.size() - 1;
   c->p16_yunits = (int)ycoff.size() - 1;
   c->d_m16ctr.ensure(2);
+  c->p16_nparts = nparts;
+  c->p16_row0 = c->p16_row1 = 0;  // internal row positions the leaves cover
+  if (nl > 0) {
+    c->p16_row0 = c->leaf_begin[0];
+    c->p16_row1 = c->leaf_end[0];
+    for (int L = 1; L < nl; ++L) {
+      c->p16_row0 = std::min(c->p16_row0, c->leaf_begin[L]);
+      c->p16_row1 = std::max(c->p16_row1, c->leaf_end[L]);
+    }
+  }
+
   c->p16_ns = cfg.ns;
   c->p16_stage = cfg.stage;
   c->p16_ncta = ncta;
@@ -2462,6 +2539,10 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
   P.leaf_begin = c->d_leaf_begin.p;
   P.rperm = c->yperm();
   P.y = dy;
+  // slices sized for the rows of this product (a shard's segment or all rows)
+  if (c->p16_nparts > 1) c->d_y16part.ensure((size_t)c->p16_nparts * MR * 3 * (size_t)c->ynrows());
+  P.ypart = c->d_y16part.p;
+  P.nparts = c->p16_nparts;
   P.nrows = c->ynrows();
   P.stage = c->p16_stage;
   static const int dbg = [] {
@@ -2519,6 +2600,15 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
           case 9: launch_m16<9>(c, P); break;
           default: launch_m16<3>(c, P);
         }
+      }
+      if (c->p16_nparts > 1) {  // the leaf parts' slices -> y, in part order
+        const int nint = c->p16_row1 - c->p16_row0;
+        const long long total = (long long)nint * 3 * nr;
+        if (total > 0)
+          y16_reduce_kernel<<<grid_for(c, (total + 255) / 256, 16), 256, 0, c->stream>>>(
+              c->d_y16part.p, dy, c->yperm() + c->p16_row0, nint, c->ynrows(), c->p16_nparts, s0,
+              nr);
+        CK(cudaGetLastError());
       }
     });
   }

@@ -99,7 +99,8 @@ struct __align__(16) YItem16 {  // 64 B
   int PR;                    // ADM: U pitch; DENSE: column pitch in shared memory
   int off1, off2;            // stage offsets (doubles): ADM U, Z; DENSE D, X
   int jd;                    // DENSE: columns
-  int m, roff, pad0, pad1;   // DENSE: block rows (component stride), first row of the leaf
+  int m, roff, part, pad1;   // DENSE: block rows (component stride), first row of the leaf;
+                             // part: the leaf part the item belongs to (slice of ypart)
   unsigned char lo[6], hi[6];  // ADM: l range of each component
   int pad2;
 };
@@ -121,7 +122,7 @@ constexpr int M16_DST_MASK = M16_KEEP - 1;
 // host-side piece of the phase-2 plan (one block piece / column group)
 struct YStage16 {
   long long src, src2;
-  int len, len2, kind, leaf, flags, R, PR, jd, spitch, m, roff;
+  int len, len2, kind, leaf, flags, R, PR, jd, spitch, m, roff, part;
   unsigned char lo[6], hi[6];
 };
 
@@ -139,6 +140,8 @@ struct M16Params {
   const int* leaf_begin;
   const int* rperm;
   double* y;
+  double* ypart;             // nparts > 1: [part][16][3][nrows] partial slices
+  int nparts;
   int nrows, s0, nr, stage;  // stage: doubles per stage (header included)
   int dbg;                   // A/B: 1 = stream only (no compute), 2 = compute only
   unsigned long long* prof;  // A/B (dbg 3): cycle counters of the stage loop
@@ -628,9 +631,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int sx = (split ? 8 * h0 : 8 * h) + 2 * t + e;
-                if (sx < P.nr)
-                  P.y[(long long)(P.s0 + sx) * ndof + r * (long long)P.nrows + row] =
-                      acc[r][h][e];
+                if (sx < P.nr) {
+                  if (P.nparts > 1)
+                    P.ypart[((long long)d.part * MR + sx) * ndof + r * (long long)P.nrows + row] =
+                        acc[r][h][e];
+                  else
+                    P.y[(long long)(P.s0 + sx) * ndof + r * (long long)P.nrows + row] =
+                        acc[r][h][e];
+                }
               }
             }
         }
@@ -659,6 +667,25 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
       P.prof[8] = cyc;
       P.prof[9] = ns1 - ns0;
     }
+  }
+}
+
+// y = sum over the leaf parts' slices, in part order (nparts > 1); every
+// internal row b of the operator (rperm[b] = its output row) and RHS
+__global__ void y16_reduce_kernel(const double* __restrict__ ypart, double* __restrict__ y,
+                                  const int* __restrict__ rperm, int nint, int nrows, int nparts,
+                                  int s0, int nr) {
+  const long long ndof = 3LL * nrows;
+  const long long total = (long long)nint * 3 * nr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e % nint);
+    const long long q = e / nint;
+    const int r = (int)(q % 3), sx = (int)(q / 3);
+    const long long o = r * (long long)nrows + rperm[b];
+    double v = ypart[(long long)sx * ndof + o];
+    for (int p = 1; p < nparts; ++p) v += ypart[((long long)p * MR + sx) * ndof + o];
+    y[(long long)(s0 + sx) * ndof + o] = v;
   }
 }
 
