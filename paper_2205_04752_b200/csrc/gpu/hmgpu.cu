@@ -2074,11 +2074,13 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         tk.gtile[r + 1] = (unsigned char)(tk.gtile[r] + (grows[r] + 7) / 8);
       }
       tk.ntiles = tk.gtile[3];
+      tk.pad0 = L;  // the zero row of the staged V^T
       if (tk.ntiles > 3 * cfg.znw) fail(HMGPU_ERR_INVALID, "multi-RHS task above 3 m-tiles per warp");
       // widest chunk whose V^T and X rows fit one stage
       int jc = std::min(n, 252);
-      while (jc > 4 && (long long)(L + XP) * cf_pitch(jc) > SD) jc -= 4;
-      if ((long long)(L + XP) * cf_pitch(jc) > SD)
+      // (+ 1: a zero row after the V^T rows, read by the padding rows of the m-tiles)
+      while (jc > 4 && (long long)(L + 1 + XP) * cf_pitch(jc) > SD) jc -= 4;
+      if ((long long)(L + 1 + XP) * cf_pitch(jc) > SD)
         fail(HMGPU_ERR_INVALID, "multi-RHS stage too small");
       const int ti = (int)tasks.size();
       tasks.push_back(tk);
@@ -2088,7 +2090,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         const int j0 = q * jc, jj = std::min(jc, n - j0), Pp = cf_pitch(jj);
         ZChunk16 ch{};
         ch.vsrc = alen;
-        ch.vlen = L * Pp;
+        ch.vlen = (L + 1) * Pp;
         ch.xcol = mb.col0 + j0;
         ch.P = Pp;
         ch.task = ti;
@@ -2099,8 +2101,8 @@ void build_plan16(hmgpu_ctx* c, int mode) {
                                    alen + (long long)tk.vrow[e] * Pp, n, Pp, jj,
                                    sg.hi - sg.lo, 0, 0});
         }
-        alen += (long long)L * Pp;
-        by += (long long)L * Pp + (long long)Pp * XP;
+        alen += (long long)(L + 1) * Pp;
+        by += (long long)(L + 1) * Pp + (long long)Pp * XP;
         zch.push_back(ch);
       }
       tbytes.push_back(by);

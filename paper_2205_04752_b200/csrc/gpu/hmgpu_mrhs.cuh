@@ -46,8 +46,17 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace hmgpu {
 
+#ifndef M16_UNROLL_Z  // inner-loop unrolling (A/B builds: 1 beats 2 by 4 %, 3 and 4 lose 3-10 %)
+#define M16_UNROLL_Z 1
+#endif
+#ifndef M16_UNROLL_Y
+#define M16_UNROLL_Y 1
+#endif
+constexpr int kUnrollZ = M16_UNROLL_Z, kUnrollY = M16_UNROLL_Y;
 constexpr int MR = 16;          // right-hand sides per pass
 constexpr int XP = 52;          // doubles per gathered column
 constexpr int ZP = 36;          // doubles per Z row
@@ -77,7 +86,8 @@ static_assert(sizeof(ZChunk16) == 32, "ZChunk16 layout");
 
 struct __align__(16) ZTask16 {  // phase-1 task (80 B)
   long long zdst;            // doubles: the block's Z region
-  int ntiles, pad0;          // 8-row m-tiles over the three operand groups
+  int ntiles, pad0;          // 8-row m-tiles over the three operand groups; pad0 = the zero
+                             // row that follows the task's rows in every staged V^T
   short zrow[6];             // Z row (of the block) of each segment's first l
   unsigned char len[6];      // l count of the segment (<= 64)
   unsigned char vrow[6];     // first row of the segment in the staged V^T
@@ -231,25 +241,44 @@ __device__ __forceinline__ void ring_init(double* sm, uint64_t* full, uint64_t* 
 // the CTAs between 74 % and 84 % busy on average); the consumers learn the
 // end from an END stage the producer issues last.  issue(slot, bar) returns
 // false after it issued the END stage, compute(slot) returns false on it.
+// Cycle counters of the stage loop (HMGPU_M16_DBG=3) are compiled in only
+// with -DHMGPU_M16_PROF: even predicated off they cost ten issue slots per
+// stage, and a stage holds only 15-35 DMMA per warp.
+#ifdef HMGPU_M16_PROF
+constexpr bool kM16Prof = true;
+#else
+constexpr bool kM16Prof = false;
+#endif
 template <int NS, int NW = M16_NW, class ISSUE, class COMPUTE>
 __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t* empty,
                                            int stage, ISSUE issue, COMPUTE compute,
                                            int dbg = 0, unsigned long long* prof = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool tm = dbg == 3 && prof != nullptr;
+  const bool tm = kM16Prof && dbg == 3 && prof != nullptr;
   long long t_wait = 0, t_work = 0;
+  // slot s and the parity of its current use, stepped instead of i % NS, i / NS
+  int s = 0;
+  uint32_t par = 0;
+  double* slot = sm;
   if (warp == NW) {
-    for (int j = 0;; ++j) {
-      const int s = j % NS;
+    bool wrapped = false;
+    for (;;) {
       const long long t0 = tm ? clock64() : 0;
-      if (j >= NS) mbar_wait(&empty[s], (uint32_t)(((j / NS) - 1) & 1));
+      if (wrapped) mbar_wait(&empty[s], par ^ 1u);
       const long long t1 = tm ? clock64() : 0;
-      const bool more = issue(sm + (long long)s * stage, &full[s]);
+      const bool more = issue(slot, &full[s]);
       if (tm) {
         t_wait += t1 - t0;
         t_work += clock64() - t1;
       }
       if (!more) break;
+      slot += stage;
+      if (++s == NS) {
+        s = 0;
+        slot = sm;
+        par ^= 1u;
+        wrapped = true;
+      }
     }
     if (tm && lane == 0) {
       atomicAdd(prof + 2, (unsigned long long)t_wait);
@@ -257,12 +286,11 @@ __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t*
     }
     return;
   }
-  for (int i = 0;; ++i) {
-    const int s = i % NS;
+  for (;;) {
     const long long t0 = tm ? clock64() : 0;
-    mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+    mbar_wait(&full[s], par);
     const long long t1 = tm ? clock64() : 0;
-    const bool more = compute(sm + (long long)s * stage);
+    const bool more = compute(slot);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tm) {
@@ -270,6 +298,12 @@ __device__ __forceinline__ void stage_loop(double* sm, uint64_t* full, uint64_t*
       t_work += clock64() - t1;
     }
     if (!more) break;
+    slot += stage;
+    if (++s == NS) {
+      s = 0;
+      slot = sm;
+      par ^= 1u;
+    }
   }
   if (tm && lane == 0) {
     atomicAdd(prof + 0, (unsigned long long)t_wait);
@@ -403,26 +437,39 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
           const int l = rho - cum;
           arow[q] = tk.vrow[seg] + l;
           zdst[q] = (tk.zrow[seg] + l) * ZP + (tk.gent[r][e] & 1) * 16;
-        } else {
-          arow[q] = -1;
+        } else {  // padding row of the tile: the zero row, nothing stored
+          arow[q] = tk.pad0;
           zdst[q] = -1;
         }
       }
     }
     const double* X0 = sX + t * XP + g;
-    // k-steps outer, the warp's tiles inner: 2 ntl independent DMMA chains
-#pragma unroll 2
-    for (int kk = 0; kk < Pp; kk += 4) {
-      const double* xk = X0 + kk * XP;
+    // k-steps outer, the warp's tiles inner: 2 ntl independent DMMA chains;
+    // one loop instance per tile count, so nothing branches inside
+    auto sweep = [&](auto ntl_c) {
+      constexpr int NT = decltype(ntl_c)::value;
+      const double* vr[NT];
+      const double* xr[NT];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (q >= ntl) break;  // warp-uniform
-        const double u = sV[(arow[q] < 0 ? 0 : arow[q]) * Pp + kk + t];
-        const double a = arow[q] < 0 ? 0.0 : u;
-        dmma(acc[q][0][0], acc[q][0][1], a, xk[xcol[q]]);
-        dmma(acc[q][1][0], acc[q][1][1], a, xk[xcol[q] + 8]);
+      for (int q = 0; q < NT; ++q) {
+        vr[q] = sV + arow[q] * Pp + t;
+        xr[q] = X0 + xcol[q];
       }
-    }
+#pragma unroll kUnrollZ
+      for (int kk = 0; kk < Pp; kk += 4) {
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          const double a = vr[q][0];
+          dmma(acc[q][0][0], acc[q][0][1], a, xr[q][0]);
+          dmma(acc[q][1][0], acc[q][1][1], a, xr[q][8]);
+          vr[q] += 4;
+          xr[q] += 4 * XP;
+        }
+      }
+    };
+    if (ntl == 3) sweep(std::integral_constant<int, 3>{});
+    else if (ntl == 2) sweep(std::integral_constant<int, 2>{});
+    else if (ntl == 1) sweep(std::integral_constant<int, 1>{});
     if (ch.flags & 2) {  // last chunk: this lane's Z rows
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -434,7 +481,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
     }
     return true;
   };
-  const bool tm = P.dbg == 3 && P.prof && threadIdx.x == 0;
+  const bool tm = kM16Prof && P.dbg == 3 && P.prof && threadIdx.x == 0;
   const long long ck0 = tm ? clock64() : 0;
   stage_loop<NS, NW>(sm, full, empty, P.stage, issue, compute, P.dbg, P.prof);
   if (tm && blockIdx.x < M16_PROF_CTAS)
@@ -472,7 +519,30 @@ __device__ __forceinline__ void y16_adm(const double* sU, int PR, const double* 
                                         double (&acc)[3][2][2]) {
   const double* ur = sU + t * PR + rt * 8 + g;
   const double* zr = sZ + t * ZP + g;
-#pragma unroll 2
+#ifdef M16_Y_PEEL  // A/B: whole l-steps unpredicated, the ragged last one apart
+  int l0 = lo;
+#pragma unroll kUnrollY
+  for (; l0 + 4 <= hi; l0 += 4) {
+    const double a = ur[0];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
+      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
+    }
+    ur += 4 * PR;
+    zr += 4 * ZP;
+  }
+  if (l0 < hi) {
+    const double u = ur[0];
+    const double a = l0 + t < hi ? u : 0.0;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
+      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
+    }
+  }
+#else
+#pragma unroll kUnrollY
   for (int l0 = lo; l0 < hi; l0 += 4) {
     // rows past hi are loaded and dropped (cheaper than a predicated load):
     // they lie at most 3 PR + 64 doubles past the piece, inside the item's Z
@@ -487,6 +557,7 @@ __device__ __forceinline__ void y16_adm(const double* sU, int PR, const double* 
     ur += 4 * PR;
     zr += 4 * ZP;
   }
+#endif
 }
 
 // one phase-2 item for the warp's row tile rt; hoff = first RHS of the half
@@ -598,6 +669,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
     y16_issue(P, st, bar, d, mine, lane, pol_stream, pol_keep);
     return more;
   };
+  constexpr int HS = NW == 16 ? 8 : NW / 2;  // row tiles in split mode
+  const int wmod = warp % HS, wdiv = warp / HS;
   auto compute = [&](double* st) -> bool {
     const int nit = *reinterpret_cast<const int*>(st);
     if (nit < 0) return false;  // END stage
@@ -605,10 +678,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
     for (int it = 0; it < nit; ++it) {
     const YItem16& d = items[it];
     const int RT = (d.R + 7) >> 3;
-    constexpr int HS = NW == 16 ? 8 : NW / 2;  // row tiles in split mode
     const bool split = NW == 16 || RT <= HS;
-    const int rt = split ? warp % HS : warp;
-    const int h0 = split ? warp / HS : 0;
+    const int rt = split ? wmod : warp;
+    const int h0 = split ? wdiv : 0;
     if (d.flags & 1) {
 #pragma unroll
       for (int r = 0; r < 3; ++r)
@@ -649,7 +721,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
   };
   // A/B (dbg 3): SM cycles of every CTA's stage loop (balance of the plan)
   // and nanoseconds of CTA 0's -> the SM clock the sweep runs at
-  const bool tm = P.dbg == 3 && P.prof && threadIdx.x == 0;
+  const bool tm = kM16Prof && P.dbg == 3 && P.prof && threadIdx.x == 0;
   long long ck0 = 0;
   unsigned long long ns0 = 0;
   if (tm) {
