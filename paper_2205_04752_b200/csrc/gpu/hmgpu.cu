@@ -2098,10 +2098,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         for (size_t e = 0; e < grp.size(); ++e) {
           const Seg& sg = grp[e];
           packs.push_back(PackDesc{c->items[mb.item0 + sg.c].v_off + (long long)sg.lo * n + j0,
-                                   alen + (long long)tk.vrow[e] * Pp, n, Pp, jj,
+                                   alen + M16_HDR + (long long)tk.vrow[e] * Pp, n, Pp, jj,
                                    sg.hi - sg.lo, 0, 0});
         }
-        alen += (long long)(L + 1) * Pp;
+        alen += M16_HDR + (long long)(L + 1) * Pp;  // records, V^T rows, the zero row
         by += (long long)(L + 1) * Pp + (long long)Pp * XP;
         zch.push_back(ch);
       }
@@ -2333,6 +2333,8 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       zcoff.push_back((int)zch.size());  // = END chunk
       ZChunk16 end{};
       end.flags = 4;
+      end.vsrc = alen;  // records only
+      alen += M16_HDR;
       zch.push_back(end);
     }
     const int SD2 = cfg.stage - Y16_HDR;
@@ -2433,6 +2435,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     }
   }
   c->d_zch16.upload(zch, c->stream);
+  if (tasks.empty()) tasks.push_back(ZTask16{});  // the END chunk's header names task 0
   c->d_ztask16.upload(tasks, c->stream);
   c->d_zcoff16.upload(zcoff, c->stream);
   c->d_ycoff16.upload(ycoff, c->stream);
@@ -2468,6 +2471,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     c->sync();
     d_packs.free();
   }
+  // phase-1 stage headers into the arena, in front of each chunk's V^T
+  z16_hdr_kernel<<<grid_for(c, ((long long)zch.size() + 255) / 256, 16), 256, 0, c->stream>>>(
+      c->d_zch16.p, c->d_ztask16.p, (int)zch.size(), c->spare_arena.p);
+  CK(cudaGetLastError());
   c->n_zch16 = (int)zch.size() - 1;  // without the END records
   c->n_yst16 = (int)ystages.size() - 1;
   c->p16_zunits = (int)zcoff.size() - 1;
