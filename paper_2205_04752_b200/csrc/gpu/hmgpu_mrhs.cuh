@@ -529,54 +529,33 @@ __device__ __forceinline__ void y16_issue(const M16Params& P, double* st, uint64
   }
 }
 
-// Y rows of the warp's row tile += U_c [Z_c | W_c] over the item's l range
-// of component c = (RR, CC), for NH RHS halves (NH = 1: the half at the
-// caller's offset into Z, accumulated in acc[..][0])
+// Y rows of the warp's row tile += U_c [Z_c | W_c] over n rows (l) of
+// component c = (RR, CC), for NH RHS halves (NH = 1: the half at the caller's
+// offset into Z, accumulated in acc[..][0]).  ur / zr: this lane's element of
+// the component's first U row / Z row; both run on over the components of
+// the item (their U pieces and Z rows follow each other in the stage).
 template <int RR, int CC, int NH>
-__device__ __forceinline__ void y16_adm(const double* sU, int PR, const double* sZ, int lo,
-                                        int hi, int rt, int g, int t,
-                                        double (&acc)[3][2][2]) {
-  const double* ur = sU + t * PR + rt * 8 + g;
-  const double* zr = sZ + t * ZP + g;
-#ifdef M16_Y_PEEL  // A/B: whole l-steps unpredicated, the ragged last one apart
-  int l0 = lo;
+__device__ __forceinline__ void y16_adm(const double*& ur, const double*& zr, int PR4, int n,
+                                        int t, double (&acc)[3][2][2]) {
+  const double* u_ = ur;
+  const double* z_ = zr;
 #pragma unroll kUnrollY
-  for (; l0 + 4 <= hi; l0 += 4) {
-    const double a = ur[0];
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
-      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
-    }
-    ur += 4 * PR;
-    zr += 4 * ZP;
-  }
-  if (l0 < hi) {
-    const double u = ur[0];
-    const double a = l0 + t < hi ? u : 0.0;
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
-      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
-    }
-  }
-#else
-#pragma unroll kUnrollY
-  for (int l0 = lo; l0 < hi; l0 += 4) {
-    // rows past hi are loaded and dropped (cheaper than a predicated load):
+  for (int l0 = 0; l0 < n; l0 += 4) {
+    // rows past n are loaded and dropped (cheaper than a predicated load):
     // they lie at most 3 PR + 64 doubles past the piece, inside the item's Z
     // rows plus the M16_SLACK doubles the launch allocates after the ring
-    const double u = ur[0];
-    const double a = l0 + t < hi ? u : 0.0;
+    const double u = u_[0];
+    const double a = l0 + t < n ? u : 0.0;
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-      dmma(acc[RR][h][0], acc[RR][h][1], a, zr[8 * h]);
-      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, zr[16 + 8 * h]);
+      dmma(acc[RR][h][0], acc[RR][h][1], a, z_[8 * h]);
+      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, z_[16 + 8 * h]);
     }
-    ur += 4 * PR;
-    zr += 4 * ZP;
+    u_ += PR4;
+    z_ += 4 * ZP;
   }
-#endif
+  ur += (PR4 >> 2) * n;
+  zr = z_;  // (ceil4(n) rows: the component's Z rows are padded to l-steps)
 }
 
 // one phase-2 item for the warp's row tile rt; hoff = first RHS of the half
@@ -585,17 +564,17 @@ template <int NH>
 __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int rt, int hoff,
                                          int g, int t, double (&acc)[3][2][2]) {
   if (d.kind == Y16_ADM) {
-    const double* sU = st + d.off1;
-    const double* sZ = st + d.off2 + hoff;
-    int uo = 0, zo = 0;
+    // the l ranges of the six components in one 16-byte load
+    const uint4 lh = *reinterpret_cast<const uint4*>(d.lo);
+    const int PR4 = 4 * d.PR;
+    const double* ur = st + d.off1 + t * d.PR + rt * 8 + g;
+    const double* zr = st + d.off2 + hoff + t * ZP + g;
+#define Y16_LO(CI) ((CI) < 4 ? (lh.x >> (8 * (CI))) & 255u : (lh.y >> (8 * ((CI) - 4))) & 255u)
+#define Y16_HI(CI) ((CI) < 2 ? (lh.y >> (8 * ((CI) + 2))) & 255u : (lh.z >> (8 * ((CI) - 2))) & 255u)
 #define Y16_COMP(CI, RR, CC)                                                              \
   {                                                                                       \
-    const int lo = d.lo[CI], hi = d.hi[CI];                                               \
-    if (lo < hi) {                                                                        \
-      y16_adm<RR, CC, NH>(sU + uo, d.PR, sZ + zo, lo, hi, rt, g, t, acc);                \
-      uo += (hi - lo) * d.PR;                                                             \
-      zo += (((hi + 3) & ~3) - lo) * ZP;                                                  \
-    }                                                                                     \
+    const int n = (int)Y16_HI(CI) - (int)Y16_LO(CI);                                      \
+    if (n > 0) y16_adm<RR, CC, NH>(ur, zr, PR4, n, t, acc);                               \
   }
     Y16_COMP(0, 0, 0)
     Y16_COMP(1, 0, 1)
@@ -603,6 +582,8 @@ __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int
     Y16_COMP(3, 1, 1)
     Y16_COMP(4, 1, 2)
     Y16_COMP(5, 2, 2)
+#undef Y16_LO
+#undef Y16_HI
 #undef Y16_COMP
     return;
   }
