@@ -518,6 +518,7 @@ def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
                     "algorithmic_flops_per_step": flops,
                     "algorithmic_bytes_per_step": alg_bytes,
                     "hbm_frac": alg_bytes / (ms_dom * 1e-3) / 1e9 / peak,
+                    "hbm_traffic_frac": (traffic / (ms_dom * 1e-3) / 1e9 / peak) if traffic else None,
                     "ms_kernel": ms_dom, "ms_matvec_device": ms_step}
     else:
         ms_stream = (kt["hmv_stream"][0] + kt["hmv_ypart"][0]) / nprof
@@ -716,6 +717,9 @@ def mrhs_leg(hm, torch, h, steps, warmup, device, name):
                          "algorithmic_flops_per_step": flops,
                          "algorithmic_bytes_per_step": alg_bytes,
                          "hbm_frac": alg_bytes / (ms_dom * 1e-3) / 1e9 / peak,
+                         "hbm_traffic_frac": (traffic / (ms_dom * 1e-3) / 1e9 / peak) if traffic
+                         else None,
+                    "hbm_traffic_frac": (traffic / (ms_dom * 1e-3) / 1e9 / peak) if traffic else None,
                          "hbm_peak_source": peak_src, "ms_kernel": ms_dom}}
 
 
