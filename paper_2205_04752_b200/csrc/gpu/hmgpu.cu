@@ -2242,10 +2242,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   const int ncta = c->sm_count * per_sm;
   int nparts = 1;
   {
-    static const int forced = [] {
-      const char* e = std::getenv("HMGPU_M16_PARTS");
-      return e ? std::atoi(e) : 0;
-    }();
+    // HMGPU_M16_PARTS=1..8 forces the count (read per plan: tests and A/B runs)
+    const char* fe = std::getenv("HMGPU_M16_PARTS");
+    const int forced = fe ? std::atoi(fe) : 0;
     long long total = 0;
     for (long long b : lbytes) total += b;
     nparts = (int)std::min<long long>(8, (16LL * ncta + nl - 1) / std::max(nl, 1));

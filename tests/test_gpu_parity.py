@@ -436,6 +436,36 @@ def test_multi_rhs_plans_share_the_spare_arena_and_follow_rank_changes():
     assert rel(Y3, C3) < 1e-13 and rel(Y3, Y1) > 1e-12  # the new ranks are used
 
 
+@pytest.mark.parametrize("mesh_name,rows,parts", [
+    ("ico3", 40, 0),     # 40-row leaves: 5 consumer warps, a row tile each
+    ("cube16", 48, 0),   # 48-row leaves: 6 consumer warps (config 3's shape)
+    ("cube12", 54, 0),   # 54-row leaves: 8 consumer warps, 7 row tiles
+    ("cube16", 48, 3),   # every leaf cut into 3 parts: partial slices + ordered reduce
+    ("ico3", 40, 8),
+])
+def test_multi_rhs_consumer_warp_configurations(mesh_name, rows, parts, monkeypatch):
+    """The 16-RHS sweep picks its consumer warps from the leaves' row tiles and
+    may cut leaves into parts; every configuration gives the 1-RHS product."""
+    mesh = {"ico3": lambda: hm.Mesh.icosphere(3), "cube16": lambda: hm.Mesh.voxel_cube(16, 0.0, 1.0),
+            "cube12": lambda: hm.Mesh.voxel_cube(12, 0.0, 1.0)}[mesh_name]()
+    if parts:
+        monkeypatch.setenv("HMGPU_M16_PARTS", str(parts))
+    g = hm.HMatrix.kelvin(mesh, b_min=64, eta=1.0, device=0)
+    g.assemble(eps=1e-4, beta=0.8, lookahead=2)
+    t = g.tree()
+    leaves = t.nodes[t.nodes[:, 2] < 0]
+    sizes = leaves[:, 1] - leaves[:, 0]
+    assert sizes.max() == rows and sizes.max() <= 64
+    for nrhs in (16, 19):
+        X = np.asfortranarray(np.stack([RV(g.cols, 400 + s) for s in range(nrhs)], axis=1))
+        for mode in (hm.Mode.Current, hm.Mode.Lookahead):
+            Y = g.matvec(X, mode)
+            assert (Y == g.matvec(X, mode)).all()  # deterministic (dynamic hand-out included)
+            for q in (0, 9, nrhs - 1):
+                y = g.matvec(np.ascontiguousarray(X[:, q]), mode)
+                assert rel(Y[:, q], y) < 1e-13
+
+
 def test_multi_rhs_large_leaves_fall_back_to_the_block_sweep():
     """Leaves above 64 rows are outside the TMA-fed sweep's tiling: the
     product runs on the block-sweep kernel and stays the same product."""
