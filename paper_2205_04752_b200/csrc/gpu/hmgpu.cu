@@ -2503,6 +2503,13 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_mode = mode;
   c->p16_valid = true;
   c->sync();
+  if (verbose()) {
+    long long kb[5] = {0, 0, 0, 0, 0};  // staged bytes of phase 2 by source
+    for (size_t q = 0; q < ycopies.size(); ++q) kb[ckind[q]] += ycopies[q].bytes;
+    std::fprintf(stderr, "[hmgpu] plan16 phase-2 bytes per product: records %.3f GB, U %.3f GB, "
+                         "Z %.3f GB, near field %.3f GB, x rows %.3f GB (parts %d)\n",
+                 kb[0] / 1e9, kb[1] / 1e9, kb[2] / 1e9, kb[3] / 1e9, kb[4] / 1e9, nparts);
+  }
   if (verbose())
     std::fprintf(stderr, "[hmgpu] plan16: tasks=%zu chunks=%zu (units %d) stages=%zu (units %d) "
                          "arena=%.3f GB Z=%.3f GB ctas=%d/%d warps=%d/%d ring=%zu B\n",
