@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <array>
+#include <unordered_map>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -518,6 +519,7 @@ struct hmgpu_ctx {
   int p16_zunits = 0, p16_yunits = 0;  // dynamically scheduled work units per pass
   DBuf<int> d_m16ctr;                  // their hand-out counters (phase 1, phase 2)
   int p16_nparts = 1;                  // parts per leaf in phase 2 (> 1: partial slices + reduce)
+  bool p16_ypair = false;              // phase 2 over pairs of leaves (hmv16_y2_kernel)
   int p16_row0 = 0, p16_row1 = 0;      // internal row positions covered by the leaves
   DBuf<double> d_y16part;              // [part][16 RHS][3][rows] partial slices
   long long p16_zsize = 0, p16_alen = 0;
@@ -1986,7 +1988,21 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     const int rt = (rmax + 7) / 8;
     cfg.ynw = (rt == 6 || rt == 3) ? 6 : (rt == 5 ? 5 : 8);
   }
-  const bool y4 = cfg.ynw == 5 || cfg.ynw == 6;  // 4 CTAs per SM
+  // phase 2 over pairs of neighbouring leaves (hmv16_y2_kernel): when the
+  // leaves fill their row tiles (rows = 8 warps, so the second leaf's tiles
+  // start at a tile boundary) and the warps are not split over RHS halves;
+  // HMGPU_M16_PAIR=0 keeps one leaf per unit
+  bool ypair = false;
+  {
+    const char* e = std::getenv("HMGPU_M16_PAIR");
+    int rmax = 1;
+    for (size_t L = 0; L < c->leaf_begin.size(); ++L)
+      rmax = std::max(rmax, c->leaf_end[L] - c->leaf_begin[L]);
+    ypair = !(e && std::atoi(e) == 0) && cfg.ynw != 16 && (cfg.ns == 3 || cfg.ns == 4) &&
+            rmax == 8 * cfg.ynw &&
+            c->leaf_begin.size() >= 2;
+  }
+  const bool y4 = !ypair && (cfg.ynw == 5 || cfg.ynw == 6);  // 4 CTAs per SM
   if (cfg.stage == 0) {
     cfg.stage = y4 ? 2304 : 3072;
     if (cfg.zstage == 0) cfg.zstage = 2304;  // 6 consumer warps, 4 CTAs per SM
@@ -2123,17 +2139,38 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   std::vector<long long> lbytes;
   std::vector<int> lptr{0};
   const int nl = (int)c->leaf_begin.size();
-  for (int L = 0; L < nl; ++L) {
+  // groups: one leaf, or (ypair) two neighbouring leaves whose first fills its tiles
+  std::vector<int2> groups;  // (first leaf, second leaf or -1)
+  for (int L = 0; L < nl;) {
     const int R = c->leaf_end[L] - c->leaf_begin[L];
     if (R > 64) fail(HMGPU_ERR_INVALID, "leaf above 64 rows for the multi-RHS sweep");
-    const int PR = cf_pitch(R);
+    if (ypair && L + 1 < nl && R == 8 * cfg.ynw && c->leaf_end[L] == c->leaf_begin[L + 1] &&
+        c->leaf_end[L + 1] - c->leaf_begin[L + 1] <= 8 * cfg.ynw) {
+      groups.push_back(make_int2(L, L + 1));
+      L += 2;
+    } else {
+      groups.push_back(make_int2(L, -1));
+      L += 1;
+    }
+  }
+  const int ng = (int)groups.size();
+  std::vector<int> grows(ng), gb0(ng);
+  for (int G = 0; G < ng; ++G) {
+    const int LA = groups[G].x, LB = groups[G].y;
+    const int RA = c->leaf_end[LA] - c->leaf_begin[LA];
+    const int RB = LB >= 0 ? c->leaf_end[LB] - c->leaf_begin[LB] : 0;
+    const int rg = RA + RB;
+    grows[G] = rg;
+    gb0[G] = c->leaf_begin[LA];
     const size_t first = yst.size();
     long long by = 0;
-    for (int e = c->leaf_ptr[L]; e < c->leaf_ptr[L + 1]; ++e) {
-      const int bi = c->leaf_blk[e].x, roff = c->leaf_blk[e].y;
+    // the pieces of one block for R rows from row roff of the block: tile
+    // slot tsel (0 first leaf, 1 second, 2 both: R = both leaves' rows)
+    auto add_block = [&](int bi, int roff, int R, int tsel) {
+      const int PR = cf_pitch(R);
       const MvBlock& mb = c->mvb[bi];
       if (mb.dense) {
-        if (skip == 1) continue;
+        if (skip == 1) return;
         const long long cp = align2(6LL * mb.m);
         const int PD = cf_pitch(6 * mb.m);
         // as many columns as fit with their x rows (ceil4 of them); any
@@ -2152,7 +2189,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           const int jj = std::min(jd, mb.n - j0);
           YStage16 d{};
           d.kind = Y16_DENSE;
-          d.leaf = L;
+          d.leaf = G;
+          d.tsel = tsel;
+          d.rg = rg;
           d.R = R;
           d.src = mb.dense_off + (long long)j0 * cp;
           d.len = 6 * mb.m;
@@ -2166,9 +2205,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           yst.push_back(d);
           by += (long long)jj * 6 * mb.m + d.len2;
         }
-        continue;
+        return;
       }
-      if (zb[bi] < 0 || skip == 2) continue;
+      if (zb[bi] < 0 || skip == 2) return;
       YStage16 d{};
       bool open = false;
       int used = 0;
@@ -2184,9 +2223,12 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           if (!open) {
             d = YStage16{};
             d.kind = Y16_ADM;
-            d.leaf = L;
+            d.leaf = G;
+          d.tsel = tsel;
+          d.rg = rg;
             d.R = R;
             d.PR = PR;
+            d.m = RA;  // rows of the first leaf (tsel 2: offset of the second's)
             d.src = alen;
             d.src2 = zb[bi] + (long long)(zo[bi][q] + lo) * ZP;
             used = 0;
@@ -2216,13 +2258,36 @@ void build_plan16(hmgpu_ctx* c, int mode) {
         }
       }
       if (open) flush();
+        };
+    if (LB < 0) {
+      for (int e = c->leaf_ptr[LA]; e < c->leaf_ptr[LA + 1]; ++e)
+        add_block(c->leaf_blk[e].x, c->leaf_blk[e].y, RA, 0);
+    } else {
+      // blocks covering both leaves (the second's rows follow the first's in
+      // the block) take both tile slots; the rest one
+      std::unordered_map<int, int> inb;  // block -> row offset of the second leaf
+      for (int e = c->leaf_ptr[LB]; e < c->leaf_ptr[LB + 1]; ++e)
+        inb[c->leaf_blk[e].x] = c->leaf_blk[e].y;
+      for (int e = c->leaf_ptr[LA]; e < c->leaf_ptr[LA + 1]; ++e) {
+        const int bi = c->leaf_blk[e].x, roff = c->leaf_blk[e].y;
+        auto it = inb.find(bi);
+        if (it != inb.end() && it->second == roff + RA && !c->mvb[bi].dense) {
+          add_block(bi, roff, RA + RB, 2);
+          inb.erase(it);
+        } else {
+          add_block(bi, roff, RA, 0);
+        }
+      }
+      for (int e = c->leaf_ptr[LB]; e < c->leaf_ptr[LB + 1]; ++e)
+        if (inb.count(c->leaf_blk[e].x)) add_block(c->leaf_blk[e].x, c->leaf_blk[e].y, RB, 1);
     }
     if (yst.size() == first) {  // no contribution: the leaf's rows are written as 0
       YStage16 d{};
       d.kind = Y16_ADM;
-      d.leaf = L;
-      d.R = R;
-      d.PR = PR;
+      d.leaf = G;
+      d.R = RA;
+      d.PR = cf_pitch(RA);
+      d.rg = rg;
       yst.push_back(d);
     }
     lbytes.push_back(std::max<long long>(by, 1));
@@ -2247,9 +2312,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     const int forced = fe ? std::atoi(fe) : 0;
     long long total = 0;
     for (long long b : lbytes) total += b;
-    nparts = (int)std::min<long long>(8, (16LL * ncta + nl - 1) / std::max(nl, 1));
+    nparts = (int)std::min<long long>(8, (16LL * ncta + ng - 1) / std::max(ng, 1));
     // parts of at least 128 KB on average
-    nparts = (int)std::min<long long>(nparts, total / std::max(nl, 1) / (128 * 1024 / 8));
+    nparts = (int)std::min<long long>(nparts, total / std::max(ng, 1) / (128 * 1024 / 8));
     nparts = std::max(nparts, 1);
     if (forced >= 1 && forced <= 8) nparts = forced;
   }
@@ -2257,11 +2322,11 @@ void build_plan16(hmgpu_ctx* c, int mode) {
     std::vector<YStage16> parts;
     std::vector<long long> sbytes;
     std::vector<int> sptr{0};
-    parts.reserve(yst.size() + (size_t)nl * nparts);
+    parts.reserve(yst.size() + (size_t)ng * nparts);
     auto plen0 = [](const YStage16& d) -> long long {
       return d.kind == Y16_ADM ? (long long)d.len + d.len2 : (long long)d.jd * d.PR + d.len2;
     };
-    for (int L = 0; L < nl; ++L) {
+    for (int L = 0; L < ng; ++L) {
       long long total = 0;
       for (int q = lptr[L]; q < lptr[L + 1]; ++q) total += plen0(yst[q]);
       long long cum = 0;
@@ -2280,8 +2345,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           YStage16 d{};
           d.kind = Y16_ADM;
           d.leaf = L;
-          d.R = c->leaf_end[L] - c->leaf_begin[L];
+          d.R = std::min(grows[L], 8 * cfg.ynw);
           d.PR = cf_pitch(d.R);
+          d.rg = grows[L];
           parts.push_back(d);
         }
         for (size_t e = first; e < parts.size(); ++e) parts[e].part = pt;
@@ -2386,7 +2452,9 @@ void build_plan16(hmgpu_ctx* c, int mode) {
           const YStage16& d = yst[cpieces[q]];
           YItem16 it{};
           it.kind = d.kind;
-          it.leaf = d.leaf;
+          it.leaf = gb0[d.leaf];  // first internal row position of the leaf (pair)
+          it.tsel = d.tsel;
+          it.rg = d.rg;
           it.flags = d.flags;
           it.R = d.R;
           it.PR = d.PR;
@@ -2480,6 +2548,7 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->p16_yunits = (int)ycoff.size() - 1;
   c->d_m16ctr.ensure(2);
   c->p16_nparts = nparts;
+  c->p16_ypair = ypair;
   c->p16_row0 = c->p16_row1 = 0;  // internal row positions the leaves cover
   if (nl > 0) {
     c->p16_row0 = c->leaf_begin[0];
@@ -2512,9 +2581,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   }
   if (verbose())
     std::fprintf(stderr, "[hmgpu] plan16: tasks=%zu chunks=%zu (units %d) stages=%zu (units %d) "
-                         "arena=%.3f GB Z=%.3f GB ctas=%d/%d warps=%d/%d ring=%zu B\n",
+                         "arena=%.3f GB Z=%.3f GB ctas=%d/%d warps=%d/%d%s ring=%zu B\n",
                  tasks.size(), zch.size(), c->p16_zunits, ystages.size(), c->p16_yunits,
-                 8.0 * alen / 1e9, 8.0 * zsize / 1e9, nctaz, ncta, cfg.znw, cfg.ynw, ring_bytes);
+                 8.0 * alen / 1e9, 8.0 * zsize / 1e9, nctaz, ncta, cfg.znw, cfg.ynw,
+                 ypair ? " (leaf pairs)" : "", ring_bytes);
 }
 
 template <int NS, int NW = 8>
@@ -2527,6 +2597,18 @@ void launch_m16(hmgpu_ctx* c, M16Params P) {  // phase 2
   P.ctr = c->d_m16ctr.p + 1;
   hmv16_y_kernel<NS, NW><<<std::max(1, std::min(c->p16_ncta, c->p16_yunits)), 32 * (NW + 1), smem,
                            c->stream>>>(P);
+  CK(cudaGetLastError());
+}
+template <int NS, int NW>
+void launch_m16y2(hmgpu_ctx* c, M16Params P) {  // phase 2 over pairs of leaves
+  const size_t smem = ((size_t)NS * c->p16_stage + M16_SLACK) * sizeof(double);
+  CK(cudaFuncSetAttribute(hmv16_y2_kernel<NS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  P.coff = c->d_ycoff16.p;
+  P.nunits = c->p16_yunits;
+  P.ctr = c->d_m16ctr.p + 1;
+  hmv16_y2_kernel<NS, NW><<<std::max(1, std::min(c->p16_ncta, c->p16_yunits)), 32 * (NW + 1), smem,
+                            c->stream>>>(P);
   CK(cudaGetLastError());
 }
 template <int NS, int NW>
@@ -2598,7 +2680,15 @@ void launch_mrhs(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode)
       P.copies = c->d_ycopy16.p;
       P.coff = c->d_ycoff16.p;
       P.stage = c->p16_stage;
-      if (c->p16_ynw == 16) {
+      if (c->p16_ypair) {
+        if (c->p16_ns == 4) {
+          if (c->p16_ynw == 5) launch_m16y2<4, 5>(c, P);
+          else if (c->p16_ynw == 6) launch_m16y2<4, 6>(c, P);
+          else launch_m16y2<4, 8>(c, P);
+        } else if (c->p16_ynw == 5) launch_m16y2<3, 5>(c, P);
+        else if (c->p16_ynw == 6) launch_m16y2<3, 6>(c, P);
+        else launch_m16y2<3, 8>(c, P);
+      } else if (c->p16_ynw == 16) {
         if (c->p16_ns == 6) launch_m16<6, 16>(c, P);
         else if (c->p16_ns == 9) launch_m16<9, 16>(c, P);
         else launch_m16<4, 16>(c, P);

@@ -105,14 +105,17 @@ enum { Y16_ADM = 0, Y16_DENSE = 1 };
 // one near-field column group, for one leaf; a stage carries up to
 // Y16_MAXIT of them (consecutive in leaf order, possibly across leaves)
 struct __align__(16) YItem16 {  // 64 B
-  int kind, leaf, flags, R;  // flags: 1 first item of the leaf, 2 last
+  int kind, leaf, flags, R;  // leaf: first internal row position of the leaf (pair);
+                             // flags: 1 first item of the leaf part, 2 last; R: rows of the piece
   int PR;                    // ADM: U pitch; DENSE: column pitch in shared memory
   int off1, off2;            // stage offsets (doubles): ADM U, Z; DENSE D, X
   int jd;                    // DENSE: columns
-  int m, roff, part, pad1;   // DENSE: block rows (component stride), first row of the leaf;
-                             // part: the leaf part the item belongs to (slice of ypart)
+  int m, roff, part, tsel;   // DENSE: block rows (component stride), first row of the leaf;
+                             // part: the leaf part the item belongs to (slice of ypart);
+                             // paired leaves: tsel 0 = first leaf's rows (tile slot 0), 1 =
+                             // second leaf's (slot 1), 2 = both (ADM, m = rows of the first)
   unsigned char lo[6], hi[6];  // ADM: l range of each component
-  int pad2;
+  int rg;                      // rows of the leaf (pair): the rows written at flags & 2
 };
 static_assert(sizeof(YItem16) == 64, "YItem16 layout");
 constexpr int Y16_MAXIT = 14;
@@ -132,7 +135,7 @@ constexpr int M16_DST_MASK = M16_KEEP - 1;
 // host-side piece of the phase-2 plan (one block piece / column group)
 struct YStage16 {
   long long src, src2;
-  int len, len2, kind, leaf, flags, R, PR, jd, spitch, m, roff, part;
+  int len, len2, kind, leaf, flags, R, PR, jd, spitch, m, roff, part, tsel, rg;
   unsigned char lo[6], hi[6];
 };
 
@@ -691,9 +694,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
       if (split) y16_item<1>(d, st, rt, 8 * h0, g, t, acc);
       else y16_item<2>(d, st, rt, 0, g, t, acc);
       if (d.flags & 2) {  // the leaf is complete: y rows, external order
-        const int b0 = P.leaf_begin[d.leaf];
+        const int b0 = d.leaf;
         const int i = rt * 8 + g;
-        if (i < d.R) {
+        if (i < d.rg) {
           const long long row = P.rperm[b0 + i];
 #pragma unroll
           for (int r = 0; r < 3; ++r)
@@ -740,6 +743,203 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
       P.prof[9] = ns1 - ns0;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// phase 2 over PAIRS of neighbouring leaves.  Phase 2 is bound by HBM on what
+// it stages, and per l of a block it stages the leaf's U rows (pitch 52 at
+// 48 rows) plus the block's Z row (36): the Z of a block is re-read by every
+// leaf the block covers and almost never found in L2.  Two neighbouring
+// leaves share every block above the leaf level, so a CTA that takes both
+// stages the Z once: 100 + 36 instead of 2 (52 + 36) doubles per l.  Warp w
+// owns row tile w of the first leaf (tile slot 0) and of the second (slot
+// 1); a shared block's piece feeds both slots from one B fragment (fewer
+// fragment loads per DMMA too), pieces of leaf-level blocks and the near
+// field feed one.  Needs the first leaf to fill its NW tiles (rows = 8 NW).
+template <int RR, int CC, int TS>
+__device__ __forceinline__ void y2_adm(const double*& ur, const double*& zr, int PR4, int n, int t,
+                                       int offB, double (&acc)[2][3][2][2]) {
+  const double* u_ = ur;
+  const double* z_ = zr;
+#pragma unroll kUnrollY
+  for (int l0 = 0; l0 < n; l0 += 4) {
+    const bool in = l0 + t < n;
+    const double u0 = u_[0];
+    const double a = in ? u0 : 0.0;  // slot 0 (TS 0, 2) or slot 1 (TS 1)
+    double b = 0.0;
+    if (TS == 2) {
+      const double u1 = u_[offB];
+      b = in ? u1 : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double z = z_[8 * h];
+      if (TS != 1) dmma(acc[0][RR][h][0], acc[0][RR][h][1], a, z);
+      if (TS == 1) dmma(acc[1][RR][h][0], acc[1][RR][h][1], a, z);
+      if (TS == 2) dmma(acc[1][RR][h][0], acc[1][RR][h][1], b, z);
+      if (RR != CC) {
+        const double w = z_[16 + 8 * h];
+        if (TS != 1) dmma(acc[0][CC][h][0], acc[0][CC][h][1], a, w);
+        if (TS == 1) dmma(acc[1][CC][h][0], acc[1][CC][h][1], a, w);
+        if (TS == 2) dmma(acc[1][CC][h][0], acc[1][CC][h][1], b, w);
+      }
+    }
+    u_ += PR4;
+    z_ += 4 * ZP;
+  }
+  ur += (PR4 >> 2) * n;
+  zr = z_;
+}
+
+template <int TS>
+__device__ __forceinline__ void y2_adm_item(const YItem16& d, const double* st, int w, int g,
+                                            int t, double (&acc)[2][3][2][2]) {
+  const uint4 lh = *reinterpret_cast<const uint4*>(d.lo);
+  const int PR4 = 4 * d.PR, offB = d.m;
+  const double* ur = st + d.off1 + t * d.PR + w * 8 + g;
+  const double* zr = st + d.off2 + t * ZP + g;
+#define Y16_LO(CI) ((CI) < 4 ? (lh.x >> (8 * (CI))) & 255u : (lh.y >> (8 * ((CI) - 4))) & 255u)
+#define Y16_HI(CI) ((CI) < 2 ? (lh.y >> (8 * ((CI) + 2))) & 255u : (lh.z >> (8 * ((CI) - 2))) & 255u)
+#define Y16_COMP(CI, RR, CC)                                                              \
+  {                                                                                       \
+    const int n = (int)Y16_HI(CI) - (int)Y16_LO(CI);                                      \
+    if (n > 0) y2_adm<RR, CC, TS>(ur, zr, PR4, n, t, offB, acc);                          \
+  }
+  Y16_COMP(0, 0, 0)
+  Y16_COMP(1, 0, 1)
+  Y16_COMP(2, 0, 2)
+  Y16_COMP(3, 1, 1)
+  Y16_COMP(4, 1, 2)
+  Y16_COMP(5, 2, 2)
+#undef Y16_LO
+#undef Y16_HI
+#undef Y16_COMP
+}
+
+// near field of one leaf of the pair into tile slot SLOT
+template <int SLOT>
+__device__ __forceinline__ void y2_dense_item(const YItem16& d, const double* st, int w, int g,
+                                              int t, double (&acc)[2][3][2][2]) {
+  const double* sD = st + d.off1 + d.roff + w * 8 + g;
+  const double* sX = st + d.off2 + g;
+  const int m = d.m, PD = d.PR;
+  constexpr int Rs[6] = {0, 0, 0, 1, 1, 2}, Cs[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll 1
+  for (int j0 = 0; j0 < d.jd; j0 += 4) {
+    const int j = j0 + t;
+    const bool ok = j < d.jd;
+    const double* xr = sX + j * XP;
+    const double* dr = sD + (ok ? j : 0) * PD;
+    double a[6];
+#pragma unroll
+    for (int cc = 0; cc < 6; ++cc) {
+      const double v = dr[cc * m];
+      a[cc] = ok ? v : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double bx[3] = {xr[8 * h], xr[16 + 8 * h], xr[32 + 8 * h]};
+#pragma unroll
+      for (int cc = 0; cc < 6; ++cc) {
+        dmma(acc[SLOT][Rs[cc]][h][0], acc[SLOT][Rs[cc]][h][1], a[cc], bx[Cs[cc]]);
+        if (Rs[cc] != Cs[cc])
+          dmma(acc[SLOT][Cs[cc]][h][0], acc[SLOT][Cs[cc]][h][1], a[cc], bx[Rs[cc]]);
+      }
+    }
+  }
+}
+
+template <int NS, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 3) hmv16_y2_kernel(M16Params P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  ring_init<NS, NW>(sm, full, empty, P.stage);
+  const M16Stage* stages = static_cast<const M16Stage*>(P.desc);
+  double acc[2][3][2][2];  // [tile slot][output component][RHS half][pair]
+  const long long ndof = 3LL * P.nrows;
+  UnitCursor cur{};
+  M16Stage rec0{}, rec1{};
+  M16Copy cp0{};
+  int i0 = 0, i1 = 0;
+  if (warp == NW) {
+    cur.init(P.coff, P.ctr, P.nunits);
+    i0 = cur.next();
+    i1 = cur.next();
+    rec0 = stages[i0];
+    rec1 = stages[i1];
+    if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
+  }
+  const uint64_t pol_stream = l2_policy(false), pol_keep = l2_policy(true);
+  auto issue = [&](double* st, uint64_t* bar) -> bool {
+    const M16Stage d = rec0;
+    const M16Copy mine = cp0;
+    const bool more = i0 != cur.end;
+    i0 = i1;
+    rec0 = rec1;
+    if (more) {
+      if (lane < rec0.ncopies) cp0 = P.copies[rec0.cbeg + lane];
+      i1 = cur.next();
+      rec1 = stages[i1];
+    }
+    y16_issue(P, st, bar, d, mine, lane, pol_stream, pol_keep);
+    return more;
+  };
+  auto compute = [&](double* st) -> bool {
+    const int nit = *reinterpret_cast<const int*>(st);
+    if (nit < 0) return false;  // END stage
+    const YItem16* items = reinterpret_cast<const YItem16*>(st) + 1;
+    for (int it = 0; it < nit; ++it) {
+      const YItem16& d = items[it];
+      if (d.flags & 1) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[s][r][h][0] = acc[s][r][h][1] = 0.0;
+      }
+      // a tile past the piece's rows has nothing to add (its rows are not written)
+      if (d.tsel == 2 || warp * 8 < d.R) {  // warp-uniform
+        if (d.kind == Y16_ADM) {
+          if (d.tsel == 2) y2_adm_item<2>(d, st, warp, g, t, acc);
+          else if (d.tsel == 1) y2_adm_item<1>(d, st, warp, g, t, acc);
+          else y2_adm_item<0>(d, st, warp, g, t, acc);
+        } else {
+          if (d.tsel == 1) y2_dense_item<1>(d, st, warp, g, t, acc);
+          else y2_dense_item<0>(d, st, warp, g, t, acc);
+        }
+      }
+      if (d.flags & 2) {  // the leaves are complete: y rows, external order
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int i = (s * NW + warp) * 8 + g;
+          if (i >= d.rg) continue;
+          const long long row = P.rperm[d.leaf + i];
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int sx = 8 * h + 2 * t + e;
+                if (sx < P.nr) {
+                  if (P.nparts > 1)
+                    P.ypart[((long long)d.part * MR + sx) * ndof + r * (long long)P.nrows + row] =
+                        acc[s][r][h][e];
+                  else
+                    P.y[(long long)(P.s0 + sx) * ndof + r * (long long)P.nrows + row] =
+                        acc[s][r][h][e];
+                }
+              }
+        }
+      }
+    }
+    return true;
+  };
+  stage_loop<NS, NW>(sm, full, empty, P.stage, issue, compute, P.dbg,
+                     P.prof ? P.prof + 4 : nullptr);
 }
 
 // y = sum over the leaf parts' slices, in part order (nparts > 1); every

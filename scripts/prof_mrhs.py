@@ -13,8 +13,18 @@ h = hm.HMatrix.kelvin(mesh, b_min=bmin, eta=1.0, device=0)
 h.assemble(eps=eps, beta=0.8)
 X = np.asfortranarray(hm.random_vector(h.cols * nrhs, 2, "normal").reshape(nrhs, -1).T)
 h.set_profiling(True)
-for it in range(3):
-    Y = h.matvec(X)
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3  # many: the power-limited steady state
+import torch
+Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda")  # column-major (dofs x nrhs)
+Yd = torch.empty_like(Xd)
+for it in range(iters):
+    if iters > 3:
+        h.matvec_ptr(Xd.data_ptr(), Yd.data_ptr(), nrhs)
+    else:
+        Y = h.matvec(X)
+torch.cuda.synchronize()
+if iters > 3:
+    Y = Yd.cpu().numpy().T
 names = ["gather", "hmv16_z", "hmv16_leaf", "pack16"]
 for k in names:
     ms, n = h.kernel_times(k, reset=True)
