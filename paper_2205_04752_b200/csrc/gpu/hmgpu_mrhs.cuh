@@ -5,27 +5,39 @@
 // multiply-adds, so the sweep needs the fp64 tensor pipe as much as HBM:
 // these are the "batched fp64 factor products" of the north star.
 //
-// Two persistent, TMA-fed passes.  A CTA = 8 consumer warps + 1 producer
-// warp around a ring of NS stages in shared memory (3 CTAs per SM by
-// default): the producer issues each stage's bulk copies (cp.async.bulk, one
-// mbarrier transaction per stage, L2 evict-first for streamed data and
-// evict-last for re-read x rows / Z) as soon as every consumer released the
-// slot; the consumers compute DMMA on fragments read from the stage:
+// Two persistent, TMA-fed passes.  A CTA = NW consumer warps + 1 producer
+// warp around a ring of NS stages in shared memory: the producer issues each
+// stage's bulk copies (cp.async.bulk, one mbarrier transaction per stage, L2
+// evict-first for streamed data and evict-last for re-read x rows / Z) as
+// soon as every consumer released the slot; the consumers compute DMMA on
+// fragments read from the stage.  Work is handed out dynamically: the
+// producer pulls work units (runs of stages) from a global counter and ends
+// the consumers with an END stage, so the CTAs stay busy whatever their SM
+// neighbours do.
 //
-//   phase 1 (hmv16_z_kernel)  one task per (admissible block, <= 64 l of its
-//            components): the task's rows of V^T are tiled in 8-row m-tiles
-//            per x-operand group (x_0: Z_00 W_01 W_02, x_1: Z_01 Z_11 W_12,
-//            x_2: Z_02 Z_12 Z_22), so the padding is per group, not per
-//            component; Z_c = V_c^T X_C and W_c = V_c^T X_R accumulate in
-//            registers over the block's column chunks (every chunk stages
-//            its x rows once for all components) and are written once
-//   phase 2 (hmv16_y_kernel)  one task per leaf of the row tree (leaves
-//            dealt to the CTAs cyclically): stages of up to 14 items -- a
+//   phase 1 (hmv16_z_kernel)  6 consumer warps, 4 CTAs per SM.  One task per
+//            (admissible block, <= 64 l of its components): the task's rows
+//            of V^T are tiled in 8-row m-tiles per x-operand group (x_0: Z_00
+//            W_01 W_02, x_1: Z_01 Z_11 W_12, x_2: Z_02 Z_12 Z_22), so the
+//            padding is per group, not per component; Z_c = V_c^T X_C and
+//            W_c = V_c^T X_R accumulate in registers over the block's column
+//            chunks (every chunk stages its x rows once for all components;
+//            its records travel in front of its V^T in one bulk copy) and
+//            are written once.  One loop instance per tile count of the warp
+//            and a zero row for the padding rows: nothing branches inside.
+//   phase 2 (hmv16_y_kernel / hmv16_y2_kernel)  consumer warps = row tiles
+//            of the leaves (5, 6 or 8), so no warp idles through a leaf.  One
+//            unit per leaf part (a leaf's piece list is cut into parts when
+//            there are few leaves per CTA; the parts' rows are summed in part
+//            order by y16_reduce_kernel): stages of up to 14 items -- a
 //            low-rank block piece with the block's Z (staged once per leaf,
-//            shared by the 8 warps: Y_R += U_c Z_c, Y_C += U_c W_c) or a
+//            shared by the warps: Y_R += U_c Z_c, Y_C += U_c W_c) or a
 //            near-field column group with its x rows (Y_R += D_c X_C,
 //            Y_C += D_c X_R) -- in the leaf's fixed block order; y written
-//            once per row (deterministic, no atomics, no partial rows).
+//            once per row (deterministic, no atomics).  hmv16_y2_kernel takes
+//            PAIRS of neighbouring leaves, two row tiles per warp: the Z of
+//            every block above the leaf level is staged once for both leaves
+//            (the pass is bound by HBM on what it stages).
 //
 // Data (all chosen so that the DMMA fragment loads from shared memory are
 // free of bank conflicts: a half-warp (g, t) in [0,4)^2 reads element
