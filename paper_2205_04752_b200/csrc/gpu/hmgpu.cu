@@ -2776,9 +2776,26 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     P.woff = c->d_pwoff.p + c->p_woff_base[pass];
     const int g = P.nwarps / cfg.warps;  // the layout's grid: one CTA per SM
     const size_t smem = c->p_smem_pass[pass];
+#ifdef HMGPU_MV_PROF  // per-warp loop cycles -> HMGPU_MV_PROF_FILE.<pass> (balance of the plan)
+    static DBuf<unsigned long long> mvprof;
+    mvprof.ensure((size_t)P.nwarps);
+    CK(cudaMemsetAsync(mvprof.p, 0, (size_t)P.nwarps * 8, c->stream));
+    P.prof = mvprof.p;
+#endif
     auto go = [&](auto kernel) {
       CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kernel<<<g, cfg.warps * 32, smem, c->stream>>>(P);
+#ifdef HMGPU_MV_PROF
+      if (const char* pf = std::getenv("HMGPU_MV_PROF_FILE")) {
+        std::vector<unsigned long long> h((size_t)P.nwarps);
+        CK(cudaMemcpyAsync(h.data(), mvprof.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (FILE* f = std::fopen((std::string(pf) + "." + std::to_string(pass)).c_str(), "w")) {
+          for (size_t q = 0; q < h.size(); ++q) std::fprintf(f, "%zu %llu\n", q, h[q]);
+          std::fclose(f);
+        }
+      }
+#endif
     };
 #define HMV_CASE(W, S)                                        \
   if (cfg.warps == W && cfg.ns == S) {                        \

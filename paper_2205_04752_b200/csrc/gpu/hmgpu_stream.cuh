@@ -128,6 +128,7 @@ struct WarpStreamParams {
   double* ypart;         // partial rows, 3 doubles each (1 for scalar kernels)
   int stage;             // doubles per stage (data + aux)
   int scratch;           // doubles of per-warp job scratch
+  unsigned long long* prof;  // -DHMGPU_MV_PROF: cycles of every warp's chunk loop (balance)
 };
 
 template <int NC>
@@ -458,6 +459,9 @@ hmv_warp_kernel(WarpStreamParams P) {
         bulk_g2s(st + kHdr + len, (aux_kind == WA_X ? P.xi : P.win) + aux * 4, abytes, &bar[s]);
     }
   };
+#ifdef HMGPU_MV_PROF
+  const long long ck0 = clock64();
+#endif
   for (int s = 0; s < NS; ++s) issue(s, s);
 
   // rows lane, lane+32 x 3 outputs; VSPLIT: f_s of columns lane, lane+32
@@ -600,6 +604,9 @@ hmv_warp_kernel(WarpStreamParams P) {
     __syncwarp();  // all lanes done with stage s
     issue(consumed + NS, s);
   }
+#ifdef HMGPU_MV_PROF
+  if (P.prof && lane == 0 && gw < P.nwarps) P.prof[gw] = (unsigned long long)(clock64() - ck0);
+#endif
 }
 
 // per leaf: y(p) = sum over covering job rows (fixed order).  The leaf's
