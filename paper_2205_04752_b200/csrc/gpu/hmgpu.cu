@@ -478,6 +478,8 @@ struct hmgpu_ctx {
   int p_woff_base[2] = {0, 0}, p_chunk_base[2] = {0, 0};
   int p_nwarps = 0, p_njb = 0;
   int p_nwarps_pass[2] = {0, 0};
+  int p_ngroups_pass[2] = {0, 0};  // pooled groups of small chain units per pass (dynamic tail)
+  DBuf<int> d_mvctr;               // their counters (zeroed by the gather kernel)
   size_t p_smem_pass[2] = {0, 0};
   DBuf<double> d_zpart;
   DBuf<LeafEntry> d_pentries;
@@ -575,7 +577,7 @@ struct hmgpu_ctx {
     d_mvorder.free(); d_leaf_begin.free(); d_leaf_end.free();
     d_leaf_ptr.free(); d_leaf_prow.free(); d_leaf_blk.free(); d_x.free(); d_y.free();
     d_xi.free(); d_ypart.free();
-    d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free();
+    d_pjobs.free(); d_pchunks.free(); d_pwoff.free(); d_zpart.free(); d_mvctr.free();
     d_pentries.free(); d_pleaf_ptr.free();
     d_zch16.free(); d_ztask16.free(); d_yst16.free(); d_zcoff16.free(); d_ycoff16.free(); d_m16ctr.free(); d_y16part.free();
     d_yitem16.free(); d_ycopy16.free();
@@ -1372,6 +1374,16 @@ int mv_layout(int pass) {
   }();
   return pass == 0 ? a : b;
 }
+// share of a pass's bytes (its smallest chain units) handed out dynamically
+// after the static shares (HMGPU_MV_POOL, per cent; 0 = all static)
+double mv_pool_frac() {
+  static const double v = [] {
+    const char* e = std::getenv("HMGPU_MV_POOL");
+    const double pc = e ? std::atof(e) : 12.5;
+    return pc < 0.0 || pc > 90.0 ? 0.125 : pc / 100.0;
+  }();
+  return v;
+}
 long long mv_unit_cap() {
   static const long long v = [] {
     const char* e = std::getenv("HMGPU_MV_UNIT");
@@ -1819,6 +1831,20 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
                        [&](int x, int y) { return usize[x] > usize[y]; });
       for (size_t i = 0; i < nu; ++i) uwarp[uord[i]] = (int)(i % NWARPS);
     }
+    // Static shares leave the warps 86-90 % busy at config 2 (a warp's pace
+    // depends on its SM neighbours, not only on its bytes), and handing
+    // everything out dynamically loses the locality of a warp's run.  So the
+    // round-robin layout keeps the SMALLEST units -- the last ~1/8 of the
+    // bytes in the size-sorted order -- out of the static deal: they form a
+    // pool of groups the warps pull from a global counter once their own
+    // share is done.  ipool = first pooled position of uord.
+    size_t ipool = nu;
+    if (!contiguous && mv_pool_frac() > 0.0) {
+      long long tail = 0;
+      while (ipool > 0 && (double)(tail + usize[uord[ipool - 1]]) <= mv_pool_frac() * (double)total)
+        tail += usize[uord[--ipool]];
+      ipool -= ipool % (size_t)NWARPS;  // whole rounds of the static deal
+    }
     std::vector<int> jpos(nj);  // ord position -> job table index
     for (size_t i = 0; i < nu; ++i) {
       const int u = uord[i];
@@ -1838,11 +1864,11 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
     }
     // per warp, its units in emission order (CSR over warps)
     std::vector<int> wptr(NWARPS + 1, 0), wunits(nu);
-    for (size_t u = 0; u < nu; ++u) ++wptr[uwarp[u] + 1];
+    for (size_t i = 0; i < ipool; ++i) ++wptr[uwarp[uord[i]] + 1];
     for (int w = 0; w < NWARPS; ++w) wptr[w + 1] += wptr[w];
     {
       std::vector<int> fill(wptr.begin(), wptr.end() - 1);
-      for (size_t i = 0; i < nu; ++i) wunits[fill[uwarp[uord[i]]]++] = uord[i];
+      for (size_t i = 0; i < ipool; ++i) wunits[fill[uwarp[uord[i]]]++] = uord[i];
     }
     pphase(pass == 0 ? "layout A/u" : "layout B/u");
     c->p_woff_base[pass] = (int)woff.size();
@@ -1883,8 +1909,33 @@ void build_plan(hmgpu_ctx* c, int mode, int nrhs) {
       fill(NWARPS * (nthr - 1) / nthr, NWARPS);
       for (auto& x : th) x.join();
     }
-    nch += (size_t)wstart[NWARPS];
     woff.push_back((int)wstart[NWARPS]);
+    // the pool: its units in size order after the static part, in groups of
+    // >= 1/64 of a share (offsets relative to the pass's chunks)
+    {
+      long long o = wstart[NWARPS];
+      const long long gsize = std::max<long long>(2048, total / NWARPS / 64);
+      long long acc = 0;
+      int ngroups = 0;
+      for (size_t i = ipool; i < nu; ++i) {
+        if (i == ipool || acc >= gsize) {
+          woff.push_back((int)o);
+          ++ngroups;
+          acc = 0;
+        }
+        const int u = uord[i];
+        acc += usize[u];
+        for (size_t t = ubeg[u]; t < ubeg[u + 1]; ++t)
+          for (long long q = C.ptr[ord[t]]; q < C.ptr[ord[t] + 1]; ++q) {
+            WChunk ch = C.flat[q];
+            ch.job = jpos[t];
+            chunks[nch + o++] = ch;
+          }
+      }
+      woff.push_back((int)o);
+      c->p_ngroups_pass[pass] = ngroups;
+      nch += (size_t)o;
+    }
     c->p_nwarps_pass[pass] = NWARPS;
   }
   c->p_nwarps = c->p_nwarps_pass[0];
@@ -2747,13 +2798,16 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
   (void)nrhs;
   const int NOUT = c->NC == 6 ? 3 : 1;
   c->d_xi.ensure((size_t)c->n_cols * 4 + 2);
+  c->d_mvctr.ensure(2);
   c->timed("gather", [&] {
     const long long total = 4LL * c->n_cols;
     const int grid = grid_for(c, (total + 255) / 256, 16);
     if (NOUT == 3)
-      gather4_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols);
+      gather4_kernel<3><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols,
+                                                     c->d_mvctr.p);
     else
-      gather4_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols);
+      gather4_kernel<1><<<grid, 256, 0, c->stream>>>(dx, c->d_xi.p, c->d_cperm.p, c->n_cols,
+                                                     c->d_mvctr.p);
   });
   c->d_ypart.ensure((size_t)std::max<long long>(1, c->p_slots * NOUT));
   c->d_zpart.ensure((size_t)std::max<long long>(1, c->p_zslots * 4));
@@ -2774,6 +2828,9 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     P.nwarps = c->p_nwarps_pass[pass];
     P.chunks = c->d_pchunks.p + c->p_chunk_base[pass];
     P.woff = c->d_pwoff.p + c->p_woff_base[pass];
+    P.goff = P.woff + P.nwarps + 1;  // the pool's group bounds follow the warps' offsets
+    P.ngroups = c->p_ngroups_pass[pass];
+    P.ctr = c->d_mvctr.p + pass;
     const int g = P.nwarps / cfg.warps;  // the layout's grid: one CTA per SM
     const size_t smem = c->p_smem_pass[pass];
 #ifdef HMGPU_MV_PROF  // per-warp loop cycles -> HMGPU_MV_PROF_FILE.<pass> (balance of the plan)
@@ -2799,8 +2856,13 @@ void launch_stream(hmgpu_ctx* c, const double* dx, double* dy, int nrhs) {
     };
 #define HMV_CASE(W, S)                                        \
   if (cfg.warps == W && cfg.ns == S) {                        \
-    if (c->NC == 6) go(hmv_warp_kernel<6, S, W>);             \
-    else go(hmv_warp_kernel<1, S, W>);                        \
+    if (P.ngroups > 0) {                                      \
+      if (c->NC == 6) go(hmv_warp_kernel<6, S, W, true>);     \
+      else go(hmv_warp_kernel<1, S, W, true>);                \
+    } else {                                                  \
+      if (c->NC == 6) go(hmv_warp_kernel<6, S, W, false>);    \
+      else go(hmv_warp_kernel<1, S, W, false>);               \
+    }                                                         \
     return;                                                   \
   }
     c->timed(name, [&] {

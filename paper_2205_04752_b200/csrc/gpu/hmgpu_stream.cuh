@@ -117,8 +117,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // ---------------------------------------------------------------------------
 struct WarpStreamParams {
   const WJob* jobs;
-  const WChunk* chunks;   // warp-major: warp w's chunks at [woff[w], woff[w+1])
-  const int* woff;
+  const WChunk* chunks;   // warp-major: warp w's static share at [woff[w], woff[w+1]),
+  const int* woff;        // then the pool: group g at [goff[g], goff[g+1])
+  const int* goff;
+  int ngroups;            // pooled groups (the pass's smallest chain units), pulled from
+  int* ctr;               // *ctr by warps that finished their share (zeroed by the gather)
   int nwarps;             // warps the chunk table was laid out for
   const double* arena;   // packed factors
   const double* dense;   // near-field blocks, [j][c][i] per block
@@ -406,7 +409,9 @@ __device__ __forceinline__ void drows(const double* D, int m, int cp, int ncol,
 // arrive in the same mbarrier transaction as the data.
 constexpr int kHdr = 16;  // doubles of stage header
 
-template <int NC, int NS, int WARPS>
+// POOL: the warp goes on with groups from the pass's pool after its static
+// share (layouts with a pool only: the cursor costs ~2 % where there is none)
+template <int NC, int NS, int WARPS, bool POOL>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 hmv_warp_kernel(WarpStreamParams P) {
   constexpr int NOUT = NC == 6 ? 3 : 1;
@@ -424,20 +429,49 @@ hmv_warp_kernel(WarpStreamParams P) {
   }
   __syncwarp();
 
-  // this warp's chunk sequence; descriptors are fetched 32 at a time (one
-  // coalesced load, lane l holds chunk base + l) and handed to lane 0 by
-  // shuffles when it issues, so no global latency sits on the issue path
-  const int c0 = gw < P.nwarps ? P.woff[gw] : 0;
-  const int nch = gw < P.nwarps ? P.woff[gw + 1] - c0 : 0;
+  // This warp's chunk sequence: its static share, then groups pulled from
+  // the pool's counter, one after the other without draining the ring (the
+  // next group is fetched while the current range streams).  Descriptors are
+  // fetched 32 at a time (one coalesced load, lane l holds chunk win_base +
+  // l) and handed to lane 0 by shuffles when it issues, so no global latency
+  // sits on the issue path.
+  int gq = gw < P.nwarps ? P.woff[gw] : 0;        // current range: next chunk, end
+  int gend = gw < P.nwarps ? P.woff[gw + 1] : 0;
+  int nq = -1, nend = -1;                          // prefetched pool group (-1: pool empty)
+  int issued = POOL ? 0 : gend - gq;
+  auto fetch_group = [&]() {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(P.ctr, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g < P.ngroups) {
+      nq = P.goff[g];
+      nend = P.goff[g + 1];
+    } else {
+      nq = nend = -1;
+    }
+  };
+  if (POOL) fetch_group();
+  const int ntotal = POOL ? P.goff[P.ngroups] : gend;
   WChunk win{};
   int win_base = -64;
   auto load_window = [&](int base) {
     win_base = base;
-    if (base + lane < nch) win = P.chunks[c0 + base + lane];
+    if (base + lane < ntotal) win = P.chunks[base + lane];
   };
-  auto issue = [&](int idx, int s) {  // all lanes call (shuffles), lane 0 issues
-    if (idx >= nch) return;
-    if (idx >= win_base + 32) load_window(idx & ~31);
+  auto issue = [&](int s) {  // all lanes call (shuffles), lane 0 issues the next chunk
+    if (POOL) {
+      while (gq >= 0 && gq >= gend) {  // range used up: on to the prefetched pool group
+        gq = nq;
+        gend = nend;
+        if (gq >= 0) fetch_group();
+      }
+      if (gq < 0) return;
+      ++issued;
+    } else if (gq >= gend) {
+      return;
+    }
+    const int idx = gq++;
+    if (idx < win_base || idx >= win_base + 32) load_window(idx);
     const int src_l = idx - win_base;
     const long long src = __shfl_sync(0xffffffffu, win.src, src_l);
     const long long aux = __shfl_sync(0xffffffffu, win.aux, src_l);
@@ -452,7 +486,7 @@ hmv_warp_kernel(WarpStreamParams P) {
       const uint32_t abytes = aux_kind == WA_NONE ? 0u : (uint32_t)aux_len * 32u;
       fence_proxy_async();
       mbar_expect_tx(&bar[s], 128u + bytes + abytes);
-      bulk_g2s(st, &P.chunks[c0 + idx], 48u, &bar[s]);
+      bulk_g2s(st, &P.chunks[idx], 48u, &bar[s]);
       bulk_g2s(st + 6, &P.jobs[job], 80u, &bar[s]);
       if (bytes) bulk_g2s(st + kHdr, (src_kind == 0 ? P.arena : P.dense) + src, bytes, &bar[s]);
       if (abytes)
@@ -462,11 +496,11 @@ hmv_warp_kernel(WarpStreamParams P) {
 #ifdef HMGPU_MV_PROF
   const long long ck0 = clock64();
 #endif
-  for (int s = 0; s < NS; ++s) issue(s, s);
+  for (int s = 0; s < NS; ++s) issue(s);
 
   // rows lane, lane+32 x 3 outputs; VSPLIT: f_s of columns lane, lane+32
   double y[6] = {0, 0, 0, 0, 0, 0};
-  for (int consumed = 0; consumed < nch; ++consumed) {
+  for (int consumed = 0; consumed < issued; ++consumed) {
     const int s = consumed % NS;
     mbar_wait(&bar[s], (uint32_t)((consumed / NS) & 1));
     const double* st = ring + s * P.stage;
@@ -602,7 +636,7 @@ hmv_warp_kernel(WarpStreamParams P) {
       }
     }
     __syncwarp();  // all lanes done with stage s
-    issue(consumed + NS, s);
+    issue(s);
   }
 #ifdef HMGPU_MV_PROF
   if (P.prof && lane == 0 && gw < P.nwarps) P.prof[gw] = (unsigned long long)(clock64() - ck0);
@@ -694,7 +728,9 @@ hmv_leaf_reduce_kernel(const int* __restrict__ leaf_begin, const int* __restrict
 // gather x into the stream layout: 4 doubles per internal column
 template <int NOUT>
 __global__ void gather4_kernel(const double* __restrict__ x, double* __restrict__ xi,
-                               const int* __restrict__ cperm, int ncols) {
+                               const int* __restrict__ cperm, int ncols, int* ctr) {
+  // the pool counters of the two stream passes that follow
+  if (blockIdx.x == 0 && threadIdx.x < 2) ctr[threadIdx.x] = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 4LL * ncols;
        t += (long long)gridDim.x * blockDim.x) {
     const int p = (int)(t >> 2), r = (int)(t & 3);
