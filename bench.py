@@ -508,7 +508,7 @@ def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
         dmma_sus = hm.dmma_peak_sustained_tflops(device, 1.0)
         dmma_peak = hm.dmma_peak_tflops(device)
         achieved = flops / (ms_dom * 1e-3) / 1e12
-        roofline = {"bound": "tensor", "kernel": "hmv16_z_kernel + hmv16_y_kernel (DMMA, TMA-fed)",
+        roofline = {"bound": "tensor", "kernel": "hmv16_z_kernel + hmv16_y(2)_kernel (DMMA, TMA-fed)",
                     "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
                     "frac": achieved / dmma_peak, "traffic": traffic,
                     "peak_source": "measured (hmgpu_dmma_peak, fp64 m8n8k4 chains, burst)",
@@ -705,7 +705,7 @@ def mrhs_leg(hm, torch, h, steps, warmup, device, name):
             "ms_per_step": ms_step,
             "kernel_ms": {k: kt[k][0] / nprof for k in ("gather", "hmv16_z", "hmv16_leaf")},
             "roofline": {"bound": "tensor",
-                         "kernel": "hmv16_z_kernel + hmv16_y_kernel (DMMA, TMA-fed)",
+                         "kernel": "hmv16_z_kernel + hmv16_y(2)_kernel (DMMA, TMA-fed)",
                          "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
                          "frac": achieved / dmma_peak, "traffic": traffic,
                          "traffic_source": traffic_src,

@@ -59,14 +59,14 @@ def full(rep, out_json):
                        "passes (hmv_warp_kernel A + B) per matvec, ncu --set full "
                        "(cold-cache replay)")
     z = [e for e in launches if "hmv16_z_kernel" in e["kernel"]]
-    y = [e for e in launches if "hmv16_y_kernel" in e["kernel"]]
+    y = [e for e in launches if "hmv16_y_kernel" in e["kernel"] or "hmv16_y2_kernel" in e["kernel"]]
     if z and y:
         # phase 1 + phase 2 of one 16-RHS pass
         per = (sum(e["dram_read"] + e["dram_write"] for e in z) / len(z) +
                sum(e["dram_read"] + e["dram_write"] for e in y) / len(y))
         res["dram_bytes_per_matvec"] = per
         res["note"] = ("dram__bytes_read.sum + dram__bytes_write.sum of hmv16_z_kernel + "
-                       "hmv16_y_kernel per 16-RHS pass, ncu --set full (cold-cache replay)")
+                       "hmv16_y(2)_kernel per 16-RHS pass, ncu --set full (cold-cache replay)")
     with open(out_json, "w") as fh:
         json.dump(res, fh, indent=1)
     for e in launches:
