@@ -2263,6 +2263,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
       bool open = false;
       int used = 0;
       auto flush = [&]() {
+        // leaf pairs: a tile's last l-step may load U rows up to 3 PR + 127
+        // doubles past the piece (dropped: their A is zero); at least 16 Z rows
+        // after the U rows keep those loads inside the item, whatever follows it
+        if (ypair && d.len2 < 16 * ZP) d.len2 = 16 * ZP;
         yst.push_back(d);
         by += d.len + d.len2;
         open = false;
@@ -2559,9 +2563,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   c->d_ycoff16.upload(ycoff, c->stream);
   c->d_yst16.upload(ystages, c->stream);
   c->d_yitem16.upload(yitems, c->stream);
-  c->d_z16buf.ensure((size_t)zsize + 2);
+  // (+ 16 rows: a small piece of a leaf pair stages that many, see flush())
+  c->d_z16buf.ensure((size_t)zsize + 16 * ZP);
   // rows past k_c of a component's last l-step stay zero (A is zero there)
-  CK(cudaMemsetAsync(c->d_z16buf.p, 0, ((size_t)zsize + 2) * sizeof(double), c->stream));
+  CK(cudaMemsetAsync(c->d_z16buf.p, 0, ((size_t)zsize + 16 * ZP) * sizeof(double), c->stream));
   c->d_xp16.ensure(((size_t)c->n_cols + M16_XPAD) * XP);
   CK(cudaMemsetAsync(c->d_xp16.p, 0, c->d_xp16.n * sizeof(double), c->stream));
   // the packed factors live in the idle compaction arena, like the 1-RHS

@@ -775,6 +775,8 @@ __device__ __forceinline__ void y2_adm(const double*& ur, const double*& zr, int
   const double* z_ = zr;
 #pragma unroll kUnrollY
   for (int l0 = 0; l0 < n; l0 += 4) {
+    // rows past n are loaded and dropped: at most 3 PR + 127 doubles past the
+    // piece, inside the item's Z rows (the plan stages at least 16 of them)
     const bool in = l0 + t < n;
     const double u0 = u_[0];
     const double a = in ? u0 : 0.0;  // slot 0 (TS 0, 2) or slot 1 (TS 1)
