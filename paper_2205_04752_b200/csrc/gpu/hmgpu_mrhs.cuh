@@ -193,6 +193,27 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
+// -DHMGPU_M16_BOUNDS (test builds): every fragment load of the consumers is
+// checked against the CTA's shared-memory window (ring + slack) and traps
+// outside it -- compute-sanitizer's job, done by hand
+#ifdef HMGPU_M16_BOUNDS
+__device__ __forceinline__ double m16_ld(const double* p) {
+  extern __shared__ __align__(128) double m16_sm_base[];
+  unsigned dyn;
+  asm("mov.u32 %0, %dynamic_smem_size;" : "=r"(dyn));
+  const long long off = p - m16_sm_base;
+  if (off < 0 || off >= (long long)(dyn / 8)) {
+    printf("hmgpu m16: fragment load %lld doubles into a window of %u (block %d thread %d)\n",
+           off, dyn / 8, (int)blockIdx.x, (int)threadIdx.x);
+    __trap();
+  }
+  return *p;
+}
+#define M16_LD(p) m16_ld(p)
+#else
+#define M16_LD(p) (*(p))
+#endif
+
 // D = A B + D, A 8x4 (row), B 4x8 (col), fp64; lane (g = lane/4, t = lane%4)
 // holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1]
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -493,9 +514,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
       for (int kk = 0; kk < Pp; kk += 4) {
 #pragma unroll
         for (int q = 0; q < NT; ++q) {
-          const double a = vr[q][0];
-          dmma(acc[q][0][0], acc[q][0][1], a, xr[q][0]);
-          dmma(acc[q][1][0], acc[q][1][1], a, xr[q][8]);
+          const double a = M16_LD(vr[q]);
+          dmma(acc[q][0][0], acc[q][0][1], a, M16_LD(xr[q]));
+          dmma(acc[q][1][0], acc[q][1][1], a, M16_LD(xr[q] + 8));
           vr[q] += 4;
           xr[q] += 4 * XP;
         }
@@ -559,12 +580,12 @@ __device__ __forceinline__ void y16_adm(const double*& ur, const double*& zr, in
     // rows past n are loaded and dropped (cheaper than a predicated load):
     // they lie at most 3 PR + 64 doubles past the piece, inside the item's Z
     // rows plus the M16_SLACK doubles the launch allocates after the ring
-    const double u = u_[0];
+    const double u = M16_LD(u_);
     const double a = l0 + t < n ? u : 0.0;
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-      dmma(acc[RR][h][0], acc[RR][h][1], a, z_[8 * h]);
-      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, z_[16 + 8 * h]);
+      dmma(acc[RR][h][0], acc[RR][h][1], a, M16_LD(z_ + 8 * h));
+      if (RR != CC) dmma(acc[CC][h][0], acc[CC][h][1], a, M16_LD(z_ + 16 + 8 * h));
     }
     u_ += PR4;
     z_ += 4 * ZP;
@@ -619,12 +640,12 @@ __device__ __forceinline__ void y16_item(const YItem16& d, const double* st, int
     double a[6];
 #pragma unroll
     for (int cc = 0; cc < 6; ++cc) {
-      const double v = dr[cc * m];
+      const double v = M16_LD(dr + cc * m);
       a[cc] = ok ? v : 0.0;
     }
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-      const double bx[3] = {xr[8 * h], xr[16 + 8 * h], xr[32 + 8 * h]};
+      const double bx[3] = {M16_LD(xr + 8 * h), M16_LD(xr + 16 + 8 * h), M16_LD(xr + 32 + 8 * h)};
 #pragma unroll
       for (int cc = 0; cc < 6; ++cc) {
         dmma(acc[Rs[cc]][h][0], acc[Rs[cc]][h][1], a[cc], bx[Cs[cc]]);
@@ -778,21 +799,21 @@ __device__ __forceinline__ void y2_adm(const double*& ur, const double*& zr, int
     // rows past n are loaded and dropped: at most 3 PR + 127 doubles past the
     // piece, inside the item's Z rows (the plan stages at least 16 of them)
     const bool in = l0 + t < n;
-    const double u0 = u_[0];
+    const double u0 = M16_LD(u_);
     const double a = in ? u0 : 0.0;  // slot 0 (TS 0, 2) or slot 1 (TS 1)
     double b = 0.0;
     if (TS == 2) {
-      const double u1 = u_[offB];
+      const double u1 = M16_LD(u_ + offB);
       b = in ? u1 : 0.0;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const double z = z_[8 * h];
+      const double z = M16_LD(z_ + 8 * h);
       if (TS != 1) dmma(acc[0][RR][h][0], acc[0][RR][h][1], a, z);
       if (TS == 1) dmma(acc[1][RR][h][0], acc[1][RR][h][1], a, z);
       if (TS == 2) dmma(acc[1][RR][h][0], acc[1][RR][h][1], b, z);
       if (RR != CC) {
-        const double w = z_[16 + 8 * h];
+        const double w = M16_LD(z_ + 16 + 8 * h);
         if (TS != 1) dmma(acc[0][CC][h][0], acc[0][CC][h][1], a, w);
         if (TS == 1) dmma(acc[1][CC][h][0], acc[1][CC][h][1], a, w);
         if (TS == 2) dmma(acc[1][CC][h][0], acc[1][CC][h][1], b, w);
@@ -847,12 +868,12 @@ __device__ __forceinline__ void y2_dense_item(const YItem16& d, const double* st
     double a[6];
 #pragma unroll
     for (int cc = 0; cc < 6; ++cc) {
-      const double v = dr[cc * m];
+      const double v = M16_LD(dr + cc * m);
       a[cc] = ok ? v : 0.0;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const double bx[3] = {xr[8 * h], xr[16 + 8 * h], xr[32 + 8 * h]};
+      const double bx[3] = {M16_LD(xr + 8 * h), M16_LD(xr + 16 + 8 * h), M16_LD(xr + 32 + 8 * h)};
 #pragma unroll
       for (int cc = 0; cc < 6; ++cc) {
         dmma(acc[SLOT][Rs[cc]][h][0], acc[SLOT][Rs[cc]][h][1], a[cc], bx[Cs[cc]]);
