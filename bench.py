@@ -424,6 +424,19 @@ def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
         else:
             h.matvec_ptr(xt.data_ptr(), yt.data_ptr(), nrhs)
 
+    # a single product right after the assembly can skip the plan: the direct
+    # policy (hmgpu_set_matvec_policy) sweeps the blocks in place
+    direct_ms = None
+    if world == 1 and nrhs == 1:
+        h.set_matvec_policy(True)
+        try:
+            torch.cuda.synchronize()
+            t_d = time.perf_counter()
+            step()
+            torch.cuda.synchronize()
+            direct_ms = 1e3 * (time.perf_counter() - t_d)
+        finally:
+            h.set_matvec_policy(False)
     # the first product after the assembly builds the streamed plan (host
     # job tables, packing of the current-rank factors): config 2's
     # "assembly plus one matvec" includes it
@@ -564,7 +577,11 @@ def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
                      # host's item setup and matvec tables
                      "ms_wall": asm_wall,
                      "first_matvec_ms_wall": first_ms,
-                     "assembly_plus_one_matvec_ms_wall": asm_wall + first_ms},
+                     "assembly_plus_one_matvec_ms_wall": asm_wall + first_ms,
+                     # one-shot use: the plan-free direct sweep (matvec policy)
+                     "direct_matvec_ms_wall": direct_ms,
+                     "assembly_plus_one_direct_matvec_ms_wall":
+                     (asm_wall + direct_ms) if direct_ms is not None else None},
         "kernel_ms": {k: (v[0] / nprof) for k, v in kt.items() if v[1]},
         "host_setup_s": host_setup_s,
     }
