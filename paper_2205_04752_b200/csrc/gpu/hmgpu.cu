@@ -1165,11 +1165,14 @@ void compact(hmgpu_ctx* c, int slack) {
 }
 
 // block-row matvec work lists and the leaf reduction CSR
-void build_matvec(hmgpu_ctx* c) {
+// Host tables of the matvec that depend on the partition only (owned blocks,
+// partial-row offsets, leaves of the row tree and their covering blocks): no
+// CUDA call and no rank in here, so hmgpu_assemble runs it on a host thread
+// while the ACA kernel works (it was 12 of the assembly call's 45 ms of wall
+// time at config 2).
+void build_matvec_tables(hmgpu_ctx* c) {
   c->mvb.clear();
-  c->kmax = 1;
   long long prow = 0;
-  std::vector<long long> bytes;
   for (int b = 0; b < c->n_blocks; ++b) {
     const int* B = &c->blocks[4 * b];
     const int* rn = &c->rnodes[4 * B[0]];
@@ -1185,27 +1188,10 @@ void build_matvec(hmgpu_ctx* c) {
     mb.dense_off = mb.dense ? c->dblocks[c->dense_of_block[b]].off : 0;
     mb.prow = prow;
     prow += mb.m;
-    long long by = 0;
-    if (mb.dense) {
-      by = (long long)c->NC * mb.m * mb.n;
-    } else {
-      for (int q = 0; q < c->NC; ++q) {
-        const Item& it = c->items[mb.item0 + q];
-        by += (long long)it.k * (mb.m + mb.n);
-        c->kmax = std::max(c->kmax, it.k);
-      }
-    }
-    bytes.push_back(by);
     c->mvb.push_back(mb);
   }
   c->part_rows = prow;
   c->n_mv = (int)c->mvb.size();
-  std::vector<int> order(c->n_mv);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return bytes[a] > bytes[b]; });
-  c->d_mvb.upload(c->mvb, c->stream);
-  c->d_mvorder.upload(order, c->stream);
 
   // leaves of the row tree inside the shard, in index order
   c->leaf_begin.clear();
@@ -1230,27 +1216,56 @@ void build_matvec(hmgpu_ctx* c) {
   c->leaf_begin = lb;
   c->leaf_end = le;
   const int nl = (int)lb.size();
-  std::vector<std::vector<long long>> lists(nl);
-  std::vector<std::vector<int2>> blks(nl);
-  for (int bi = 0; bi < (int)c->mvb.size(); ++bi) {
-    const MvBlock& mb = c->mvb[bi];
-    // leaves covered by rows [row0, row0+m)
+  // two passes over the blocks (count, fill) instead of a vector per leaf
+  std::vector<int> cnt(nl + 1, 0);
+  auto leaves_of = [&](const MvBlock& mb, auto&& f) {
     int l0 = (int)(std::lower_bound(lb.begin(), lb.end(), mb.row0) - lb.begin());
     for (int l = l0; l < nl && lb[l] < mb.row0 + mb.m; ++l) {
       if (le[l] > mb.row0 + mb.m)
         fail(HMGPU_ERR_INVALID, "block rows do not align with row-tree leaves");
-      lists[l].push_back(mb.prow + (lb[l] - mb.row0));
-      blks[l].push_back(make_int2(bi, lb[l] - mb.row0));
+      f(l);
     }
-  }
+  };
+  for (const MvBlock& mb : c->mvb) leaves_of(mb, [&](int l) { ++cnt[l + 1]; });
   c->leaf_ptr.assign(nl + 1, 0);
-  c->leaf_prow.clear();
-  c->leaf_blk.clear();
-  for (int l = 0; l < nl; ++l) {
-    c->leaf_ptr[l + 1] = c->leaf_ptr[l] + (int)lists[l].size();
-    c->leaf_prow.insert(c->leaf_prow.end(), lists[l].begin(), lists[l].end());
-    c->leaf_blk.insert(c->leaf_blk.end(), blks[l].begin(), blks[l].end());
+  for (int l = 0; l < nl; ++l) c->leaf_ptr[l + 1] = c->leaf_ptr[l] + cnt[l + 1];
+  c->leaf_prow.assign((size_t)c->leaf_ptr[nl], 0);
+  c->leaf_blk.assign((size_t)c->leaf_ptr[nl], make_int2(0, 0));
+  std::vector<int> fill(c->leaf_ptr.begin(), c->leaf_ptr.end() - 1);
+  for (int bi = 0; bi < (int)c->mvb.size(); ++bi) {
+    const MvBlock& mb = c->mvb[bi];
+    leaves_of(mb, [&](int l) {
+      const int o = fill[l]++;
+      c->leaf_prow[o] = mb.prow + (lb[l] - mb.row0);
+      c->leaf_blk[o] = make_int2(bi, lb[l] - mb.row0);
+    });
   }
+}
+
+// The rank-dependent part (block order by bytes, kmax) and the uploads.
+void build_matvec_finish(hmgpu_ctx* c) {
+  c->kmax = 1;
+  std::vector<long long> bytes(c->mvb.size());
+  for (size_t b = 0; b < c->mvb.size(); ++b) {
+    const MvBlock& mb = c->mvb[b];
+    long long by = 0;
+    if (mb.dense) {
+      by = (long long)c->NC * mb.m * mb.n;
+    } else {
+      for (int q = 0; q < c->NC; ++q) {
+        const Item& it = c->items[mb.item0 + q];
+        by += (long long)it.k * (mb.m + mb.n);
+        c->kmax = std::max(c->kmax, it.k);
+      }
+    }
+    bytes[b] = by;
+  }
+  std::vector<int> order(c->n_mv);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return bytes[a] > bytes[b]; });
+  c->d_mvb.upload(c->mvb, c->stream);
+  c->d_mvorder.upload(order, c->stream);
   c->d_leaf_begin.upload(c->leaf_begin, c->stream);
   c->d_leaf_end.upload(c->leaf_end, c->stream);
   c->d_leaf_ptr.upload(c->leaf_ptr, c->stream);
@@ -1260,6 +1275,11 @@ void build_matvec(hmgpu_ctx* c) {
   c->t_valid = false;
   c->d_leaf_prow.upload(c->leaf_prow, c->stream);
   c->sync();
+}
+
+void build_matvec(hmgpu_ctx* c) {
+  build_matvec_tables(c);
+  build_matvec_finish(c);
 }
 
 // tables of the transposed matvec: a partial-row range per owned block over
@@ -3427,6 +3447,22 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     c->d_dblocks.upload(c->dblocks, c->stream);
 
     phase("alloc+upload");
+    // the partition-only tables of the matvec on a host thread, beside the
+    // near-field and ACA kernels (joined before build_matvec_finish)
+    std::exception_ptr tables_err;
+    std::thread tables([&] {
+      try {
+        build_matvec_tables(c);
+      } catch (...) {
+        tables_err = std::current_exception();
+      }
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } tables_join{tables};
     // near-field fill
     CK(cudaMemsetAsync(c->d_nq.p, 0, sizeof(unsigned long long), c->stream));
     CK(cudaEventRecord(tn0, c->stream));
@@ -3520,7 +3556,9 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     cudaEventDestroy(t1);
     cudaEventDestroy(tn0);
     cudaEventDestroy(tn1);
-    build_matvec(c);
+    tables.join();
+    if (tables_err) std::rethrow_exception(tables_err);
+    build_matvec_finish(c);
     c->plan_valid = false;
     c->p16_valid = false;
     phase("build_matvec");
