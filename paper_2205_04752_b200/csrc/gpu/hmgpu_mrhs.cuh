@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), NW == 8 ? 3 : (NW == 6 ? 4 : 2)
   auto compute = [&](double* st) -> bool {
     const ZChunk16& ch = *reinterpret_cast<const ZChunk16*>(st);
     if (ch.flags & 4) return false;  // END stage
+    if (P.dbg == 1) return true;     // A/B: stream only
     const ZTask16& tk = *reinterpret_cast<const ZTask16*>(st + 4);
     const double* sV = st + M16_HDR;
     const double* sX = sV + ch.vlen;
@@ -710,6 +711,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), y16_ctas_per_sm<NW>()) hmv16_y_
   auto compute = [&](double* st) -> bool {
     const int nit = *reinterpret_cast<const int*>(st);
     if (nit < 0) return false;  // END stage
+    if (P.dbg == 1) return true;  // A/B: stream only
     const YItem16* items = reinterpret_cast<const YItem16*>(st) + 1;
     for (int it = 0; it < nit; ++it) {
     const YItem16& d = items[it];
@@ -924,6 +926,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 3) hmv16_y2_kernel(M16Params P)
   auto compute = [&](double* st) -> bool {
     const int nit = *reinterpret_cast<const int*>(st);
     if (nit < 0) return false;  // END stage
+    if (P.dbg == 1) return true;  // A/B: stream only
     const YItem16* items = reinterpret_cast<const YItem16*>(st) + 1;
     for (int it = 0; it < nit; ++it) {
       const YItem16& d = items[it];
