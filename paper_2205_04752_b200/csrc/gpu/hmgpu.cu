@@ -1277,11 +1277,6 @@ void build_matvec_finish(hmgpu_ctx* c) {
   c->sync();
 }
 
-void build_matvec(hmgpu_ctx* c) {
-  build_matvec_tables(c);
-  build_matvec_finish(c);
-}
-
 // tables of the transposed matvec: a partial-row range per owned block over
 // its column cluster, and per column-tree leaf the covering blocks in block
 // order (deterministic reduction)
