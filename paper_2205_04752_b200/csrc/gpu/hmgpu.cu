@@ -2009,7 +2009,7 @@ struct M16Cfg {  // measured on config 3: 3 x 3072 (3 CTAs / SM) b
   int ns = 3, stage = 0;  // stage 0: 3072 doubles at 3 CTAs per SM, 2304 at 4
   // phase 1 (HMGPU_M16_ZCFG="ns,stage,warps"): its own ring and consumer
   // warps (6, 8 or 12; 6 runs 4 CTAs per SM)
-  int zns = 3, zstage = 0, znw = 6;
+  int zns = 3, zstage = 0, znw = 8;
   // phase-2 consumer warps (HMGPU_M16_YNW: 5, 6, 8 or 16; 0 = from the
   // leaves' row tiles, so that no warp idles through a leaf)
   int ynw = 0;
@@ -2071,7 +2071,10 @@ void build_plan16(hmgpu_ctx* c, int mode) {
   const bool y4 = !ypair && (cfg.ynw == 5 || cfg.ynw == 6);  // 4 CTAs per SM
   if (cfg.stage == 0) {
     cfg.stage = y4 ? 2304 : 3072;
-    if (cfg.zstage == 0) cfg.zstage = 2304;  // 6 consumer warps, 4 CTAs per SM
+    // phase 1: 8 consumer warps and 3 CTAs per SM (6 warps x 4 CTAs with
+    // 2304-double stages was ahead until the loops lost their branches; now
+    // 2 % behind, profiles/ab_r02_mrhs_session4.txt)
+    if (cfg.zstage == 0) cfg.zstage = cfg.znw == 6 ? 2304 : 3072;
   }
   if ((cfg.ns != 3 && cfg.ns != 4 && cfg.ns != 6 && cfg.ns != 9) || cfg.stage < 2048 || (cfg.stage & 3))
     fail(HMGPU_ERR_INVALID, "bad HMGPU_M16_CFG");

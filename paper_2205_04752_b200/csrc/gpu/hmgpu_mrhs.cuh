@@ -15,7 +15,7 @@
 // the consumers with an END stage, so the CTAs stay busy whatever their SM
 // neighbours do.
 //
-//   phase 1 (hmv16_z_kernel)  6 consumer warps, 4 CTAs per SM.  One task per
+//   phase 1 (hmv16_z_kernel)  8 consumer warps, 3 CTAs per SM.  One task per
 //            (admissible block, <= 64 l of its components): the task's rows
 //            of V^T are tiled in 8-row m-tiles per x-operand group (x_0: Z_00
 //            W_01 W_02, x_1: Z_01 Z_11 W_12, x_2: Z_02 Z_12 Z_22), so the
