@@ -428,6 +428,7 @@ def measure(hm, torch, name, cfg, steps, warmup, world, rank, device, dist):
     # policy (hmgpu_set_matvec_policy) sweeps the blocks in place
     direct_ms = direct_rep_ms = None
     if world == 1 and nrhs == 1:
+        # (policy "auto" does this by itself for the first product after a rank change)
         h.set_matvec_policy(True)
         try:
             for rep in range(2):  # the first call also allocates its partial-row buffer

@@ -255,9 +255,12 @@ int hmgpu_extend(hmgpu_ctx* ctx, int n, const int* comp_block, int steps);
    runs the adaptive loop through the term-level API (hmb_amvm, operator.cpp
    amvm_multiply_sharded). */
 int hmgpu_amvm_estimate(hmgpu_ctx* ctx, const double* x, double* gamma, double* difference);
-/* direct != 0: 1-RHS matvecs sweep the blocks in place instead of building the
+/* direct = 1: 1-RHS matvecs sweep the blocks in place instead of building the
    packed stream plan (for one matvec per rank change, as in the adaptive loop;
-   the plan pays off from the second matvec on the same ranks) */
+   the plan pays off from the second matvec on the same ranks); 2: automatic --
+   the first 1-RHS product after a rank change (assembly, promote, extend) runs
+   in place and the plan is built when a second one follows (the two differ
+   in the order of their sums, ~1e-16 relative); 0 (default): always the plan */
 int hmgpu_set_matvec_policy(hmgpu_ctx* ctx, int direct);
 int hmgpu_get_matvec_policy(hmgpu_ctx* ctx, int* direct);
 int hmgpu_amvm_mark(hmgpu_ctx* ctx, double theta, int c_sp, long long m_rows,

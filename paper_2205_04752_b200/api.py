@@ -352,10 +352,13 @@ class HMatrix:
     def gpu_ctx(self):
         return _h.hmb_op_gpu(self._h)
 
-    def set_matvec_policy(self, direct: bool) -> None:
-        """direct=True: 1-RHS matvecs sweep the blocks in place (no stream
-        plan; for one matvec per rank change), False: the packed stream plan."""
-        st = _lib.gpu.hmgpu_set_matvec_policy(self.gpu_ctx, 1 if direct else 0)
+    def set_matvec_policy(self, direct) -> None:
+        """direct=True (1): 1-RHS matvecs sweep the blocks in place (no stream
+        plan; for one matvec per rank change), False (0): the packed stream
+        plan, "auto" (2): the first product after a rank change in place, the
+        plan from the second on."""
+        pol = 2 if direct == "auto" or direct == 2 else (1 if direct else 0)
+        st = _lib.gpu.hmgpu_set_matvec_policy(self.gpu_ctx, pol)
         if st:
             raise DeviceError("hmgpu_set_matvec_policy failed", st)
 

@@ -499,7 +499,11 @@ struct hmgpu_ctx {
   DBuf<int> d_tleaf_begin, d_tleaf_end, d_tleaf_ptr;
   DBuf<double> d_tpart, d_xr;
   bool am_have_mark = false;  // hmgpu_amvm_mark ran since the last refine
-  bool mv_direct = false;  // hmgpu_set_matvec_policy: 1-RHS matvecs without a stream plan
+  // hmgpu_set_matvec_policy: 0 the packed stream plan, 1 1-RHS matvecs sweep the
+  // blocks in place, 2 automatic: the first 1-RHS product after a rank change
+  // (assembly, promote, extend) runs in place, the plan is built for the second
+  int mv_policy = 0;
+  bool mv_auto_used = false;  // policy 2: the in-place product of these ranks is spent
   DBuf<int> d_row_leaf, d_sortp, d_tix, d_term_bi, d_cnt, d_ptr, d_lists, d_order, d_idx,
       d_marked, d_nm, d_mids;
   DBuf<long long> d_spoff, d_eptr, d_eidx, d_ecnt;
@@ -3559,6 +3563,7 @@ int hmgpu_assemble(hmgpu_ctx* c, double eps, double beta_stop, int initial_rank,
     build_matvec_finish(c);
     c->plan_valid = false;
     c->p16_valid = false;
+    c->mv_auto_used = false;
     phase("build_matvec");
     c->assembled = true;
     if (stats) {
@@ -3699,7 +3704,13 @@ void matvec_local(hmgpu_ctx* c, const double* dx, double* dy, int nrhs, int mode
       return;
     }
   }
-  bool streamed = !force_v1 && !(c->mv_direct && nrhs == 1);
+  bool direct_now = c->mv_policy == 1;
+  if (c->mv_policy == 2 && nrhs == 1 && !c->mv_auto_used &&
+      !(c->plan_valid && c->plan_mode == mode && c->plan_nrhs == nrhs)) {
+    direct_now = true;
+    c->mv_auto_used = true;
+  }
+  bool streamed = !force_v1 && !(direct_now && nrhs == 1);
   if (streamed && (!c->plan_valid || c->plan_mode != mode || c->plan_nrhs != nrhs)) {
     try {
       const auto tp = std::chrono::steady_clock::now();
@@ -4069,6 +4080,7 @@ void promote_ids(hmgpu_ctx* c, const std::vector<int>& ids) {
   for (int i : ids) c->items[i].kcur = c->items[i].k;
   c->plan_valid = false;
   c->p16_valid = false;
+  c->mv_auto_used = false;
   c->sync();
 }
 
@@ -4131,6 +4143,7 @@ void extend_ids(hmgpu_ctx* c, std::vector<int> ids, int steps) {
   phase("ranks");
   c->plan_valid = false;
   c->p16_valid = false;
+  c->mv_auto_used = false;
 }
 
 // per-partition tables of the estimator: leaf of every internal row, and per
@@ -4208,13 +4221,16 @@ int hmgpu_extend(hmgpu_ctx* c, int n, const int* comp_block, int steps) {
 }
 
 int hmgpu_set_matvec_policy(hmgpu_ctx* c, int direct) {
-  return guard(c, [&] { c->mv_direct = direct != 0; });
+  return guard(c, [&] {
+    if (direct < 0 || direct > 2) fail(HMGPU_ERR_INVALID, "matvec policy must be 0, 1 or 2");
+    c->mv_policy = direct;
+  });
 }
 
 int hmgpu_get_matvec_policy(hmgpu_ctx* c, int* direct) {
   return guard(c, [&] {
     if (!direct) fail(HMGPU_ERR_INVALID, "null direct");
-    *direct = c->mv_direct ? 1 : 0;
+    *direct = c->mv_policy;
   });
 }
 

@@ -436,6 +436,44 @@ def test_multi_rhs_plans_share_the_spare_arena_and_follow_rank_changes():
     assert rel(Y3, C3) < 1e-13 and rel(Y3, Y1) > 1e-12  # the new ranks are used
 
 
+def test_auto_matvec_policy_runs_the_first_product_in_place(c1):
+    """Policy "auto": the first 1-RHS product after a rank change sweeps the
+    blocks in place (no plan), the second builds the plan; a rank change
+    re-arms it.  Both agree with the planned product to rounding."""
+    mesh = hm.Mesh.icosphere(3)
+    g = hm.HMatrix.kelvin(mesh, b_min=32, eta=1.0, device=0)
+    g.assemble(eps=1e-4, beta=0.8, lookahead=2)
+    x = RV(g.cols, 21)
+    g.set_profiling(True)
+
+    def launches():
+        return {k: g.kernel_times(k, reset=True)[1] for k in ("hmv_blocks", "hmv_stream")}
+
+    launches()
+    g.set_matvec_policy("auto")
+    try:
+        y1 = g.matvec(x)
+        n1 = launches()
+        y2 = g.matvec(x)
+        n2 = launches()
+        y3 = g.matvec(x)
+        assert n1["hmv_blocks"] == 1 and n1["hmv_stream"] == 0  # in place
+        assert n2["hmv_blocks"] == 0 and n2["hmv_stream"] == 1  # the plan
+        assert (y2 == y3).all() and rel(y1, y2) < 1e-13
+        launches()
+        kc, kl, _, _ = g.ranks()
+        pairs = [(q, b) for q in range(6) for b in range(kc.shape[1])
+                 if kc[q, b] >= 0 and kl[q, b] > kc[q, b]][:5]
+        g.promote(pairs)
+        g.matvec(x)
+        n4 = launches()
+        assert n4["hmv_blocks"] == 1 and n4["hmv_stream"] == 0  # re-armed by the rank change
+    finally:
+        g.set_matvec_policy(False)
+        g.set_profiling(False)
+    assert hm.api._lib.gpu.hmgpu_set_matvec_policy(g.gpu_ctx, 3) != 0  # 0, 1, 2 only
+
+
 @pytest.mark.parametrize("mesh_name,rows,parts", [
     ("ico3", 40, 0),     # 40-row leaves: 5 consumer warps, a row tile each
     ("cube16", 48, 0),   # 48-row leaves: 6 consumer warps (config 3's shape)
